@@ -1,0 +1,251 @@
+/*
+ * hygro_b200.h — C ABI of the B200-native Dufort–Frankel (DF) wall solver.
+ *
+ * This is the drop-in boundary for the reference's DF hot path
+ * (reference: /root/reference/proj, "hygrosim").  The reference exposes the
+ * path as per-wall, per-step C++ calls; on a GPU one launch per wall-step is
+ * meaningless, so the boundary moves one level up to a batched, multi-step
+ * context that owns the device-resident state of many walls (and zones):
+ *
+ *   reference call (file:line)                         replaced by
+ *   -------------------------------------------------  -------------------------
+ *   df_step_coupled(f,grid,p,L,R,dt)  wall.hpp:81-82   hyg_advance  (constant walls)
+ *   df_step_nonlinear(...)            wall.hpp:88-90   hyg_advance  (HYG_COEFF_ANALYTIC_D)
+ *   euler_explicit_step(...)          wall.hpp:95-97   hyg_bootstrap(HYG_BOOT_EXPLICIT)
+ *   bootstrap_first_layer(...)        wall.hpp:119-122 hyg_bootstrap(HYG_BOOT_IMPLICIT)
+ *   step_implicit (DF bootstrap)      building.hpp:75  hyg_bootstrap(HYG_BOOT_IMPLICIT)
+ *   step_explicit(model,state)        building.hpp:69  hyg_advance  (zones present)
+ *   run(model,cadence,partial)        building.hpp:101 hyg_run
+ *   check_bounded / max_abs_field     building.cpp:282-300, wall.cpp:579-587
+ *                                                      fused guard -> HYG_EDIVERGED
+ *   BuildingModel / BuildingWall      building.hpp:24-53  hyg_model_desc
+ *   WallField (u/v prev/curr, t_star) wall.hpp:23-29   hyg_set_state / hyg_get_state
+ *   Signal::operator()(t)             signal.hpp:39-50 hyg_signal (host-evaluated
+ *                                                      per time layer, uploaded as tables)
+ *
+ * Errors: every call returns an int code.  The codes map one-to-one onto the
+ * reference's exception taxonomy (errors.hpp:8-45); include/hygro_b200.hpp
+ * rethrows them as the matching C++ exception types.
+ *
+ * Layout of host state arrays: wall-major, [n_walls][n_nodes] doubles.
+ * Plain pointers and sizes only; no CUDA or torch types cross this boundary.
+ */
+#ifndef HYGRO_B200_H
+#define HYGRO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HYG_ABI_VERSION 1
+
+/* ---- return codes (errors.hpp:8-45) ------------------------------------ */
+enum {
+    HYG_OK = 0,
+    HYG_EINVAL = 1,     /* std::invalid_argument   wall.cpp:14,19,519; building.cpp:295 */
+    HYG_ESCHEMA = 2,    /* hygro::schema_error     building.cpp:12-52 (validate)        */
+    HYG_EDIVERGED = 3,  /* hygro::numerical_error  building.cpp:282-300 (check_bounded) */
+    HYG_EDOMAIN = 4,    /* hygro::domain_error     wall.cpp:105-126 (strict StarTables) */
+    HYG_ECONVERGE = 5,  /* hygro::convergence_error wall.cpp:538-543, building.cpp:249  */
+    HYG_ESCALING = 6,   /* hygro::scaling_error    scaling.cpp:9-16                     */
+    HYG_ECUDA = 7,      /* device / driver failure (no reference equivalent)            */
+    HYG_ENOTSUP = 8     /* configuration outside what this build implements             */
+};
+
+/* ---- dimensionless parameter blocks (scaling.hpp, wall.hpp) ------------ */
+typedef struct { double Fo_M, Fo_TT, Fo_TM, gamma; } hyg_wall_groups; /* WallGroups scaling.hpp:20-25 */
+typedef struct { double Bi_M, Bi_TT, Bi_TM; } hyg_face_biot;          /* FaceBiot   scaling.hpp:28-32 */
+typedef struct { double u_inf, v_inf, g_inf, q_inf; } hyg_ambient;    /* ambient part of FaceValues wall.hpp:32-36 */
+
+/* ---- forcing signals (signal.hpp:13-86) -------------------------------- */
+enum { HYG_SIG_CONSTANT = 0, HYG_SIG_SIN = 1, HYG_SIG_SIN2 = 2 };
+typedef struct { double from, to, value; } hyg_window; /* Signal::Window signal.hpp:19-21 */
+typedef struct {
+    int32_t form;            /* HYG_SIG_*                                  */
+    int32_t n_windows;       /* additive piecewise-constant schedule       */
+    double base, amplitude, period, phase;
+    const hyg_window* windows;
+} hyg_signal;
+
+/* An exterior forcing channel: the four ambient signals of a face
+ * (FaceAttachment::u_inf/v_inf/g_inf/q_inf, building.hpp:17-20). */
+typedef struct { hyg_signal u_inf, v_inf, g_inf, q_inf; } hyg_channel;
+
+/* Zone source schedules (ZoneDimensionless::g_o/q_o/q_h, scaling.hpp:63). */
+typedef struct { hyg_signal g_o, q_o, q_h; } hyg_zone_sources;
+
+/* ---- topology ----------------------------------------------------------- */
+enum { HYG_FACE_EXTERIOR = 0, HYG_FACE_ZONE = 1 };
+typedef struct {
+    int32_t kind;   /* HYG_FACE_EXTERIOR: index = forcing channel; HYG_FACE_ZONE: index = zone */
+    int32_t index;
+} hyg_face_attach;   /* FaceAttachment building.hpp:13-21 */
+
+typedef struct {
+    int32_t wall, face;                     /* ZoneWallLink zone.hpp:24-29 */
+    double Bi_M, Bi_TT, Bi_TM, theta_T, theta_M;
+} hyg_zone_wall_link;
+
+typedef struct {
+    int32_t peer;                           /* ZoneInterzoneLink zone.hpp:32-35 */
+    double g_inz, q_inz1, q_inz2;
+} hyg_interzone_link;
+
+enum { HYG_MOISTURE_AS_PRINTED = 0, HYG_MOISTURE_FLUX_CONSISTENT = 1 }; /* zone.hpp:21 */
+
+typedef struct {
+    double kappa_a_tt1, g_v, q_v1, q_v2;    /* ZoneDimensionless scaling.hpp:61-67 */
+    int32_t sources;                        /* index into hyg_model_desc::zone_sources */
+    int32_t moisture_sign;                  /* HYG_MOISTURE_*                          */
+    int32_t n_walls;
+    const hyg_zone_wall_link* walls;
+    int32_t n_interzone;
+    const hyg_interzone_link* interzone;
+} hyg_zone_desc;                            /* ZoneConfig zone.hpp:47-54 (no radiation) */
+
+/* ---- coefficient models (CoefficientModel wall.hpp:41-60) -------------- */
+enum {
+    HYG_COEFF_CONSTANT = 0,   /* CoefficientModel::constant(): all six starred coefficients 1 */
+    /* Device functor (API extension; the reference can only express it through
+     * the test oracle's StarFn callback, tests/support/df_oracle.hpp:19):
+     *   k_M*(u,v) = 1 + p0*v + p1*exp(-p2*(v - p3)^2), other five starred coefficients 1 */
+    HYG_COEFF_ANALYTIC_D = 1
+};
+
+enum { HYG_F64 = 0, HYG_F32 = 1 };
+enum { HYG_BOOT_IMPLICIT = 0, HYG_BOOT_EXPLICIT = 1 };
+
+typedef struct {
+    int32_t n_walls;
+    int32_t n_nodes;          /* Grid1D::n, shared by every wall of a model (wall.hpp:12-19) */
+    double dx;                /* Grid1D::dx                                              */
+    int32_t precision;        /* HYG_F64, or HYG_F32 (fp32 state + fp64 boundary fluxes)  */
+    int32_t coeff_kind;       /* HYG_COEFF_*                                             */
+    double coeff_params[4];
+    const hyg_wall_groups* groups;    /* [n_walls]                                       */
+    const hyg_face_biot* biot;        /* [n_walls][2]; [0] is x*=0, [1] is x*=1          */
+    const hyg_face_attach* attach;    /* [n_walls][2]                                    */
+    int32_t n_channels;
+    const hyg_channel* channels;      /* [n_channels]                                    */
+    int32_t n_zones;
+    const hyg_zone_desc* zones;       /* [n_zones]                                       */
+    int32_t n_zone_sources;
+    const hyg_zone_sources* zone_sources;
+    hyg_signal outdoor_u, outdoor_v;  /* BuildingModel::outdoor_u/v building.hpp:41-42  */
+    double dt;                        /* BuildingModel::dt                               */
+    double divergence_norm;           /* BuildingModel::divergence_norm (default 1e3)    */
+    double eta_factor;                /* BuildingModel::eta_factor (implicit bootstrap)  */
+    int32_t max_subiters;             /* BuildingModel::max_subiters                     */
+    int32_t device;                   /* CUDA ordinal                                    */
+} hyg_model_desc;
+
+typedef struct {
+    int32_t code;            /* HYG_*                                          */
+    int32_t wall;            /* first failing wall (lowest index), -1 if none  */
+    int32_t zone;            /* failing zone, -1 if none                       */
+    int32_t subiterations;   /* implicit bootstrap passes (StepReport)         */
+    int64_t layer;           /* time-layer index after the failing step        */
+    double t_star;           /* numerical_error::t_star                         */
+    double residual;         /* convergence_error::residual                    */
+    char message[256];
+} hyg_status;
+
+typedef struct hyg_ctx hyg_ctx;
+
+int hyg_abi_version(void);
+const char* hyg_strerror(int code);
+
+/* Validates (BuildingModel::validate building.cpp:12-52), uploads parameters,
+ * allocates device state.  State starts uniform at 1 (WallField::uniform). */
+int hyg_create(const hyg_model_desc* desc, hyg_ctx** out, hyg_status* status);
+void hyg_destroy(hyg_ctx* ctx);
+
+/* Host <-> device state.  Arrays are [n_walls*n_nodes] wall-major; zone
+ * arrays are [n_zones] (may be NULL when n_zones == 0).  t_star is the
+ * time of layer "curr" (BuildingState::t).  `layer` is the integer index of
+ * layer curr (0 after initialisation). */
+int hyg_set_state(hyg_ctx* ctx, const double* u_prev, const double* u_curr,
+                  const double* v_prev, const double* v_curr,
+                  const double* zone_u, const double* zone_v, double t_star, int64_t layer);
+int hyg_get_state(hyg_ctx* ctx, double* u_prev, double* u_curr, double* v_prev,
+                  double* v_curr, double* zone_u, double* zone_v, double* t_star,
+                  int64_t* layer);
+
+/* Device-resident checkpoint of the complete resumable state (both time
+ * layers of every wall, zone states, t_star, layer index — the state a DF
+ * march needs, wall.hpp:23-29 + building.hpp:55-59).  hyg_snapshot copies
+ * the current state into the context's snapshot buffer; hyg_restore copies
+ * it back.  Device-to-device only. */
+int hyg_snapshot(hyg_ctx* ctx);
+int hyg_restore(hyg_ctx* ctx);
+
+/* Overrides channel `channel` with explicit ambient values for time layers
+ * [first_layer, first_layer + n_layers): the value used by the step that
+ * starts at layer n (forcing at layer-n time, building.cpp:153,168-169) and by
+ * the implicit bootstrap into layer n (t^{n+1} forcing, building.cpp:196). */
+int hyg_set_channel_table(hyg_ctx* ctx, int32_t channel, int64_t first_layer,
+                          int64_t n_layers, const hyg_ambient* values);
+
+/* One starting step producing layer 1 from layer 0 (run() counts it as step 1,
+ * building.cpp:317-323).  Guarded like every step. */
+int hyg_bootstrap(hyg_ctx* ctx, int32_t kind, hyg_status* status);
+
+/* nsteps DF steps with time step dt (dt <= 0: the model dt), each followed by
+ * the divergence guard.  On HYG_EDIVERGED the state is left at the last
+ * layer that passed the guard for every wall and status names the first
+ * failing layer and the lowest failing wall index. */
+int hyg_advance(hyg_ctx* ctx, int64_t nsteps, double dt, hyg_status* status);
+
+/* run() building.cpp:303-356: nsteps = lround(horizon/dt); DF bootstrap
+ * (`boot_kind`) counted as step 1; frames every lround(cadence/dt) steps and
+ * at the end through `frame` (may be NULL), which may call hyg_get_state. */
+typedef void (*hyg_frame_fn)(void* user, int64_t layer, double t_star, hyg_ctx* ctx);
+int hyg_run(hyg_ctx* ctx, double horizon, double cadence, int32_t boot_kind,
+            hyg_frame_fn frame, void* user, hyg_status* status);
+
+
+/* ---- host-side setup: dimensionless groups (scaling.cpp, materials.cpp) -
+ * Coefficient sets are {c_M, k_M, c_TT, k_TT, c_TM, k_TM} (CoefficientSet,
+ * materials.hpp:21-28).  Scaling context from (T_i [K], phi_i, t_0 [s]),
+ * ScalingContext::from_state scaling.cpp:20-28. */
+int hyg_saturation_pressure(double T, double* out);                         /* materials.cpp:33-40 */
+int hyg_scale_wall(const double reference[6], double L, double h_T0, double h_M0, double h_T1,
+                   double h_M1, double T_i, double phi_i, double t_0, hyg_wall_groups* groups,
+                   hyg_face_biot face[2]);                                   /* scaling.cpp:30-58 */
+/* out = {kappa_a_tt1, g_v, q_v1, q_v2, g_o per kg/s, q_o per kg/s, q_h per W} */
+int hyg_scale_zone(double volume, double rho_a, double c_pa, double c_pv, double ventilation_ach,
+                   double T_i, double phi_i, double t_0, double out[7]);     /* scaling.cpp:60-83 */
+/* out = {theta_T, theta_M} */
+int hyg_attach_wall_to_zone(const double reference[6], double area, double L, double volume,
+                            double rho_a, double c_pa, double T_i, double phi_i, double t_0,
+                            double out[2]);                                  /* scaling.cpp:85-90 */
+/* out = {g_inz, q_inz1, q_inz2} */
+int hyg_scale_interzone(double ach, double volume, double rho_a, double c_pa, double c_pv,
+                        double T_i, double phi_i, double t_0, double out[3]); /* scaling.cpp:92-101 */
+
+/* ---- measurement hooks (bench.py) --------------------------------------- */
+int hyg_synchronize(hyg_ctx* ctx);
+int hyg_host_register(void* ptr, size_t bytes);   /* cudaHostRegister (pinned H2D/D2H) */
+int hyg_host_unregister(void* ptr);
+/* CUDA events on the context's stream; slot in [0, 16). */
+int hyg_event_record(hyg_ctx* ctx, int32_t slot);
+int hyg_event_elapsed_ms(hyg_ctx* ctx, int32_t slot_a, int32_t slot_b, double* ms);
+/* Per-kernel launch accounting (CUDA events around every launch while on). */
+int hyg_set_profiling(hyg_ctx* ctx, int32_t on);
+int hyg_kernel_stats_count(hyg_ctx* ctx);
+int hyg_kernel_stats(hyg_ctx* ctx, int32_t i, const char** name, int64_t* launches,
+                     double* total_ms, double* node_updates);
+int hyg_reset_kernel_stats(hyg_ctx* ctx);
+/* Number of kernels this context has launched since creation. */
+int64_t hyg_launch_count(hyg_ctx* ctx);
+
+/* Device FP64 FMA throughput probe (DFMA loop), TFLOP/s counting FMA = 2. */
+int hyg_probe_fp64_peak(int32_t device, double* tflops, double* sm_clock_mhz);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HYGRO_B200_H */

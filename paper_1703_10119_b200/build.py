@@ -1,0 +1,64 @@
+"""Build the in-tree CUDA library (sm_100a) and the oracle/test libraries.
+
+Product:  paper_1703_10119_b200/libhygro_b200.so  (nvcc, -gencode sm_100a, static cudart)
+Checker:  oracle/liboracle.so, oracle/_ref/libhygro_ref.so (oracle/Makefile; the
+          latter only where /root/reference exists — the GPU box uses the prebuilt file)
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "libhygro_b200.so"
+SOURCES = [CSRC / "hyg_api.cu", CSRC / "hyg_scaling.cpp"]
+DEPS = SOURCES + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "hygro_b200.h"]
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+    "-cudart", "static", "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills",
+]
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and Path(cand).exists():
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _stale(target: Path, deps) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(Path(d).stat().st_mtime > t for d in deps)
+
+
+def build_library(force: bool = False, verbose: bool = False) -> Path:
+    if force or _stale(LIB, DEPS):
+        cmd = [_nvcc(), *NVCC_FLAGS, "-o", str(LIB), *map(str, SOURCES)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True, cwd=ROOT)
+    return LIB
+
+
+def build_oracle(verbose: bool = False) -> None:
+    """Checker libraries (test infrastructure, never linked by the product)."""
+    subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "all"], check=True)
+    if Path("/root/reference/proj/src/wall.cpp").exists():
+        subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "ref"], check=True)
+
+
+def build_all(force: bool = False, verbose: bool = False) -> None:
+    build_library(force=force, verbose=verbose)
+    build_oracle(verbose=verbose)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv, verbose=True)

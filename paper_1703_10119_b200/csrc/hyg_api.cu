@@ -1,0 +1,1156 @@
+// hyg_api.cu — host runtime behind include/hygro_b200.h.
+//
+// A context owns the device-resident state of one model (a batch of walls on
+// one grid, optionally coupled to zones) and plays the role of the
+// reference's BuildingModel + BuildingState + run() (building.hpp:38-102):
+//   * independent exterior walls with constant coefficients on a grid that
+//     tiles onto lanes  -> K1 (k_coupled.cuh), many steps fused per launch;
+//   * everything else (zones, analytic coefficients, any N) -> the one-step
+//     kernels of k_step.cuh, one launch per step (+ one zone launch).
+// Forcing signals are evaluated on the host per time layer exactly as
+// Signal::operator() (signal.hpp:39-50) at the accumulated time t
+// (BuildingState::t, building.cpp:185), and uploaded as per-layer tables.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hygro_b200.h"
+#include "k_coupled.cuh"
+#include "k_step.cuh"
+
+using namespace hyg;
+
+namespace {
+
+constexpr int kChunk = 128;     // forcing rows staged per shared-memory chunk
+constexpr int kWarps = 4;       // warps per CTA of K1
+
+struct SigHost {
+    hyg_signal s{};
+    std::vector<hyg_window> win;
+    void set(const hyg_signal& x) {
+        s = x;
+        win.assign(x.windows, x.windows + (x.windows ? x.n_windows : 0));
+        s.n_windows = static_cast<int32_t>(win.size());
+        s.windows = nullptr;
+    }
+    double operator()(double t) const {   // signal.hpp:39-50
+        double v = s.base;
+        if (s.form == HYG_SIG_SIN) {
+            v += s.amplitude * std::sin(2.0 * M_PI * (t - s.phase) / s.period);
+        } else if (s.form == HYG_SIG_SIN2) {
+            const double x = std::sin(2.0 * M_PI * (t - s.phase) / s.period);
+            v += s.amplitude * x * x;
+        }
+        for (const auto& w : win)
+            if (t >= w.from && t < w.to) v += w.value;
+        return v;
+    }
+};
+
+struct ChannelHost {
+    SigHost u, v, g, q;
+    int64_t tab_first = 0;
+    std::vector<hyg_ambient> tab;   // explicit per-layer override
+    bool flux_free() const {        // g and q identically zero: K1 without flux terms
+        auto zero = [](const SigHost& s) {
+            if (s.s.form != HYG_SIG_CONSTANT || s.s.base != 0.0) return false;
+            for (const auto& w : s.win)
+                if (w.value != 0.0) return false;
+            return true;
+        };
+        if (!zero(g) || !zero(q)) return false;
+        for (const auto& a : tab)
+            if (a.g_inf != 0.0 || a.q_inf != 0.0) return false;
+        return true;
+    }
+    Ambient at(int64_t layer, double t) const {
+        if (!tab.empty() && layer >= tab_first && layer < tab_first + static_cast<int64_t>(tab.size())) {
+            const hyg_ambient& a = tab[layer - tab_first];
+            return Ambient{a.u_inf, a.v_inf, a.g_inf, a.q_inf};
+        }
+        return Ambient{u(t), v(t), g(t), q(t)};
+    }
+};
+
+struct Pending { int stat; cudaEvent_t e0, e1; double updates; };
+struct Stat { std::string name; int64_t launches = 0; double ms = 0, updates = 0; };
+
+void set_status(hyg_status* st, int code, const char* msg) {
+    if (!st) return;
+    st->code = code;
+    std::snprintf(st->message, sizeof st->message, "%s", msg);
+}
+
+void clear_status(hyg_status* st) {
+    if (!st) return;
+    std::memset(st, 0, sizeof *st);
+    st->wall = -1;
+    st->zone = -1;
+    st->layer = -1;
+}
+
+}  // namespace
+
+struct hyg_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    // model
+    int n_walls = 0, n = 0;
+    double dx = 0;
+    int precision = HYG_F64, coeff_kind = HYG_COEFF_CONSTANT;
+    double p[4] = {0, 0, 0, 0};
+    std::vector<Groups> groups;
+    std::vector<Biot> biot;
+    std::vector<Attach> attach;
+    std::vector<ChannelHost> channels;
+    std::vector<ZoneDev> zones;
+    std::vector<ZoneLinkDev> zlinks;
+    std::vector<InzLinkDev> inz;
+    std::vector<SigHost> zsrc;    // [n_sources*3]: g_o, q_o, q_h
+    SigHost out_u, out_v;
+    double dt = 1e-3, norm = 1e3, eta_factor = 1e-2;
+    int max_subiters = 100;
+    // device state (ping-pong)
+    double* s64[2][4] = {};
+    float* s32[2][4] = {};
+    int cur = 0;
+    double* zu[2] = {};
+    double* zv[2] = {};
+    int zcur = 0;
+    void* snap[4] = {};          // hyg_snapshot buffers (allocated on first use)
+    double* snap_z[2] = {};
+    double snap_t = 0.0;
+    int64_t snap_layer = -1;
+    Groups* d_groups = nullptr;
+    Biot* d_biot = nullptr;
+    Attach* d_attach = nullptr;
+    int* d_chan = nullptr;
+    WallCoef* d_coef = nullptr;
+    double coef_dt = -1.0;
+    ZoneDev* d_zones = nullptr;
+    ZoneLinkDev* d_zlinks = nullptr;
+    InzLinkDev* d_inz = nullptr;
+    Ambient* d_table = nullptr;
+    size_t table_cap = 0;
+    std::vector<Ambient> h_table;
+    Ambient* d_boot = nullptr;     // ambient row of the starting step
+    std::vector<Ambient> h_boot;
+    bool tab_valid = false;        // cache key of the table on the device
+    int64_t tab_layer0 = 0;
+    size_t tab_rows = 0;
+    uint64_t tab_gen = 0, gen = 0; // gen bumps on hyg_set_channel_table
+    double tab_t0 = 0, tab_t1 = 0;
+    double* d_src = nullptr;
+    size_t src_cap = 0;
+    std::vector<double> h_src;
+    int* d_flag = nullptr;
+    unsigned long long* d_key = nullptr;
+    // time
+    double t = 0.0;
+    int64_t layer = 0;
+    // dispatch
+    bool fused = false;
+    bool flux = true;
+    int seg_len = 4096;
+    // measurement
+    cudaEvent_t ev[16] = {};
+    bool profiling = false;
+    std::vector<Pending> pending;
+    std::vector<Stat> stats;
+    int64_t launches = 0;
+
+    int64_t cells() const { return static_cast<int64_t>(n_walls) * n; }
+};
+
+#define HYG_CUDA(call)                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess) {                                                        \
+            char m_[200];                                                               \
+            std::snprintf(m_, sizeof m_, "CUDA error %s at %s:%d", cudaGetErrorString(e_), \
+                          __FILE__, __LINE__);                                          \
+            set_status(status, HYG_ECUDA, m_);                                          \
+            return HYG_ECUDA;                                                           \
+        }                                                                               \
+    } while (0)
+
+namespace {
+
+int stat_index(hyg_ctx* c, const char* name) {
+    for (size_t i = 0; i < c->stats.size(); ++i)
+        if (c->stats[i].name == name) return static_cast<int>(i);
+    c->stats.push_back(Stat{name});
+    return static_cast<int>(c->stats.size() - 1);
+}
+
+// bracket one launch with events when profiling is on
+struct LaunchScope {
+    hyg_ctx* c;
+    Pending p{};
+    bool on;
+    LaunchScope(hyg_ctx* ctx, const char* name, double updates) : c(ctx), on(ctx->profiling) {
+        ++c->launches;
+        if (!on) return;
+        p.stat = stat_index(c, name);
+        p.updates = updates;
+        cudaEventCreate(&p.e0);
+        cudaEventCreate(&p.e1);
+        cudaEventRecord(p.e0, c->stream);
+    }
+    ~LaunchScope() {
+        if (!on) return;
+        cudaEventRecord(p.e1, c->stream);
+        c->pending.push_back(p);
+    }
+};
+
+void drain_pending(hyg_ctx* c) {
+    for (auto& p : c->pending) {
+        float ms = 0.f;
+        cudaEventSynchronize(p.e1);
+        cudaEventElapsedTime(&ms, p.e0, p.e1);
+        Stat& s = c->stats[p.stat];
+        s.launches += 1;
+        s.ms += ms;
+        s.updates += p.updates;
+        cudaEventDestroy(p.e0);
+        cudaEventDestroy(p.e1);
+    }
+    c->pending.clear();
+}
+
+// ---- K1 dispatch -------------------------------------------------------------
+template <typename Real>
+using SegFn = void (*)(const CoupledSegArgs<Real>&, int grid, int smem, cudaStream_t);
+
+template <typename Real, int LPW, int NPT, bool FLUX, bool EXACT>
+void launch_seg(const CoupledSegArgs<Real>& a, int grid, int smem, cudaStream_t s) {
+    auto k = k_df_coupled<Real, LPW, NPT, kWarps, kChunk, FLUX, EXACT>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        attr = true;
+    }
+    k<<<grid, kWarps * 32, smem, s>>>(a);
+}
+
+template <typename Real, int LPW, int NPT>
+SegFn<Real> pick4(bool flux, bool exact) {
+    if (flux) return exact ? launch_seg<Real, LPW, NPT, true, true> : launch_seg<Real, LPW, NPT, true, false>;
+    return exact ? launch_seg<Real, LPW, NPT, false, true> : launch_seg<Real, LPW, NPT, false, false>;
+}
+
+// supported fused grids: N = LPW * NPT
+template <typename Real>
+SegFn<Real> pick_seg(int n, bool flux, bool exact, int* lpw) {
+    switch (n) {
+        case 64: *lpw = 16; return pick4<Real, 16, 4>(flux, exact);
+        case 128: *lpw = 16; return pick4<Real, 16, 8>(flux, exact);
+        case 256: *lpw = 16; return pick4<Real, 16, 16>(flux, exact);
+        case 512: *lpw = 32; return pick4<Real, 32, 16>(flux, exact);
+        default: return nullptr;
+    }
+}
+
+bool fused_grid(int n) { return n == 64 || n == 128 || n == 256 || n == 512; }
+
+// ---- forcing tables ---------------------------------------------------------------
+// rows for layers [layer0, layer0 + rows), row k evaluated at time times[k]
+int upload_table(hyg_ctx* c, int64_t layer0, const std::vector<double>& times, hyg_status* status) {
+    const size_t rows = times.size();
+    const int nch = std::max<int>(1, static_cast<int>(c->channels.size()));
+    // the device copy is reused when the same layers at the same times were
+    // uploaded last (repeated runs from a snapshot)
+    if (c->tab_valid && c->tab_layer0 == layer0 && c->tab_rows == rows && c->tab_gen == c->gen &&
+        c->tab_t0 == times.front() && c->tab_t1 == times.back())
+        return HYG_OK;
+    c->tab_valid = true;
+    c->tab_layer0 = layer0;
+    c->tab_rows = rows;
+    c->tab_gen = c->gen;
+    c->tab_t0 = times.front();
+    c->tab_t1 = times.back();
+    c->h_table.resize(rows * nch);
+    for (size_t k = 0; k < rows; ++k)
+        for (int ch = 0; ch < static_cast<int>(c->channels.size()); ++ch)
+            c->h_table[k * nch + ch] = c->channels[ch].at(layer0 + static_cast<int64_t>(k), times[k]);
+    if (c->channels.empty())
+        for (size_t k = 0; k < rows; ++k) c->h_table[k] = Ambient{1, 1, 0, 0};
+    const size_t bytes = rows * nch * sizeof(Ambient);
+    if (bytes > c->table_cap) {
+        if (c->d_table) cudaFree(c->d_table);
+        HYG_CUDA(cudaMalloc(&c->d_table, bytes));
+        c->table_cap = bytes;
+    }
+    HYG_CUDA(cudaMemcpyAsync(c->d_table, c->h_table.data(), bytes, cudaMemcpyHostToDevice, c->stream));
+    // the host vector must outlive the async copy
+    HYG_CUDA(cudaStreamSynchronize(c->stream));
+    return HYG_OK;
+}
+
+// zone sources + outdoor per step: [rows][n_src*3 + 2]
+int upload_src(hyg_ctx* c, const std::vector<double>& times, hyg_status* status) {
+    const int nsrc = static_cast<int>(c->zsrc.size() / 3);
+    const int w = nsrc * 3 + 2;
+    c->h_src.resize(times.size() * w);
+    for (size_t k = 0; k < times.size(); ++k) {
+        double* r = &c->h_src[k * w];
+        for (int i = 0; i < nsrc * 3; ++i) r[i] = c->zsrc[i](times[k]);
+        r[nsrc * 3 + 0] = c->out_u(times[k]);
+        r[nsrc * 3 + 1] = c->out_v(times[k]);
+    }
+    const size_t bytes = c->h_src.size() * sizeof(double);
+    if (bytes > c->src_cap) {
+        if (c->d_src) cudaFree(c->d_src);
+        HYG_CUDA(cudaMalloc(&c->d_src, bytes));
+        c->src_cap = bytes;
+    }
+    HYG_CUDA(cudaMemcpyAsync(c->d_src, c->h_src.data(), bytes, cudaMemcpyHostToDevice, c->stream));
+    HYG_CUDA(cudaStreamSynchronize(c->stream));
+    return HYG_OK;
+}
+
+StepArgs step_args(hyg_ctx* c, int from, double dt) {
+    StepArgs a{};
+    a.n_walls = c->n_walls;
+    a.n = c->n;
+    a.dx = c->dx;
+    a.dt = dt;
+    a.groups = c->d_groups;
+    a.biot = c->d_biot;
+    a.attach = c->d_attach;
+    a.n_channels = std::max<int>(1, static_cast<int>(c->channels.size()));
+    a.zu = c->zu[c->zcur];
+    a.zv = c->zv[c->zcur];
+    a.coeff_kind = c->coeff_kind == HYG_COEFF_ANALYTIC_D ? kCoeffAnalyticD : kCoeffConstant;
+    for (int i = 0; i < 4; ++i) a.p[i] = c->p[i];
+    for (int i = 0; i < 4; ++i) {
+        a.in[i] = c->s64[from][i];
+        a.out[i] = c->s64[1 - from][i];
+    }
+    a.layer = c->layer;
+    a.norm = c->norm;
+    a.fail_key = c->d_key;
+    return a;
+}
+
+int read_key(hyg_ctx* c, unsigned long long* key, hyg_status* status) {
+    HYG_CUDA(cudaMemcpyAsync(key, c->d_key, sizeof *key, cudaMemcpyDeviceToHost, c->stream));
+    HYG_CUDA(cudaStreamSynchronize(c->stream));
+    return HYG_OK;
+}
+
+int diverged(hyg_ctx* c, unsigned long long key, hyg_status* st) {
+    const int64_t lay = static_cast<int64_t>(key >> 32);
+    const unsigned w = static_cast<unsigned>(key & 0xffffffffu);
+    if (st) {
+        st->code = HYG_EDIVERGED;
+        st->layer = lay;
+        st->wall = w == 0xffffffffu ? -1 : static_cast<int>(w);
+        st->t_star = c->t;
+        if (w == 0xffffffffu) {
+            std::snprintf(st->message, sizeof st->message, "zone state diverged at t* = %.17g", c->t);
+        } else {
+            std::snprintf(st->message, sizeof st->message,
+                          "field norm exceeded %.17g in wall %u at t* = %.17g (layer %lld)", c->norm, w,
+                          c->t, static_cast<long long>(lay));
+        }
+    }
+    return HYG_EDIVERGED;
+}
+
+// ---- the per-step path ---------------------------------------------------------
+int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
+    if (c->precision != HYG_F64) {
+        set_status(status, HYG_ENOTSUP, "fp32 state needs a fused grid (N in {64,128,256,512})");
+        return HYG_ENOTSUP;
+    }
+    const int64_t block = 65536;     // forcing rows per upload
+    HYG_CUDA(cudaMemsetAsync(c->d_key, 0xff, sizeof(unsigned long long), c->stream));
+    for (int64_t done = 0; done < nsteps;) {
+        const int64_t rows = std::min(block, nsteps - done);
+        std::vector<double> times(rows);
+        double t = c->t;
+        for (int64_t k = 0; k < rows; ++k) {
+            times[k] = t;
+            t += dt;
+        }
+        int rc = upload_table(c, c->layer, times, status);
+        if (rc) return rc;
+        if (!c->zones.empty()) {
+            rc = upload_src(c, times, status);
+            if (rc) return rc;
+        }
+        const int nch = std::max<int>(1, static_cast<int>(c->channels.size()));
+        const int threads = 256;
+        const int grid = static_cast<int>((c->cells() + threads - 1) / threads);
+        const int nsrc = static_cast<int>(c->zsrc.size() / 3);
+        for (int64_t k = 0; k < rows; ++k) {
+            StepArgs a = step_args(c, c->cur, dt);
+            a.amb = c->d_table + k * nch;
+            a.layer = c->layer + k;
+            {
+                LaunchScope ls(c, "df_step_general", static_cast<double>(c->cells()));
+                k_df_step_general<<<grid, threads, 0, c->stream>>>(a);
+            }
+            if (!c->zones.empty()) {
+                ZoneArgs z{};
+                z.n_zones = static_cast<int>(c->zones.size());
+                z.n = c->n;
+                z.dt = dt;
+                z.zones = c->d_zones;
+                z.links = c->d_zlinks;
+                z.inz = c->d_inz;
+                z.src = c->d_src + k * (nsrc * 3 + 2);
+                z.n_sources = nsrc;
+                z.uc = c->s64[c->cur][1];    // layer n samples (before the wall step)
+                z.vc = c->s64[c->cur][3];
+                z.zu_in = c->zu[c->zcur];
+                z.zv_in = c->zv[c->zcur];
+                z.zu_out = c->zu[1 - c->zcur];
+                z.zv_out = c->zv[1 - c->zcur];
+                z.layer = c->layer + k;
+                z.norm = c->norm;
+                z.fail_key = c->d_key;
+                LaunchScope ls(c, "zone_step", 0.0);
+                k_zone_step<<<(z.n_zones + 127) / 128, 128, 0, c->stream>>>(z);
+                c->zcur ^= 1;
+            }
+            c->cur ^= 1;
+        }
+        HYG_CUDA(cudaGetLastError());
+        unsigned long long key;
+        rc = read_key(c, &key, status);
+        if (rc) return rc;
+        if (key != ~0ull) {
+            // kernels after the failing step returned early: undo their buffer flips
+            const int64_t fail_layer = static_cast<int64_t>(key >> 32);
+            const int64_t ran = fail_layer - c->layer;     // steps whose outputs exist
+            if ((rows - ran) % 2) c->cur ^= 1;
+            if (!c->zones.empty() && (rows - ran) % 2) c->zcur ^= 1;
+            c->t = times[ran - 1] + dt;
+            c->layer = fail_layer;
+            return diverged(c, key, status);
+        }
+        c->t = t;
+        c->layer += rows;
+        done += rows;
+    }
+    return HYG_OK;
+}
+
+// ---- the fused path (K1) -----------------------------------------------------------
+template <typename Real>
+int advance_fused_t(hyg_ctx* c, Real* (&buf)[2][4], int64_t nsteps, double dt, hyg_status* status) {
+    if (c->coef_dt != dt) {
+        LaunchScope ls(c, "coupled_coef", 0.0);
+        k_coupled_coef<<<(c->n_walls + 127) / 128, 128, 0, c->stream>>>(c->n_walls, c->dx, dt, c->d_groups,
+                                                                         c->d_biot, c->d_coef);
+        c->coef_dt = dt;
+    }
+    int lpw = 16;
+    SegFn<Real> fast = pick_seg<Real>(c->n, c->flux, false, &lpw);
+    SegFn<Real> exact = pick_seg<Real>(c->n, c->flux, true, &lpw);
+    const int walls_per_cta = kWarps * 32 / lpw;
+    const int grid = (c->n_walls + walls_per_cta - 1) / walls_per_cta;
+    const int nch = std::max<int>(1, static_cast<int>(c->channels.size()));
+    const int smem = kChunk * nch * static_cast<int>(sizeof(Ambient));
+    if (smem > 64 * 1024) {
+        set_status(status, HYG_ENOTSUP, "too many forcing channels for the fused kernel");
+        return HYG_ENOTSUP;
+    }
+    const int64_t block = 1 << 18;    // layers per table upload
+    for (int64_t done = 0; done < nsteps;) {
+        const int64_t rows = std::min(block, nsteps - done);
+        std::vector<double> times(rows);
+        double t = c->t;
+        for (int64_t k = 0; k < rows; ++k) {
+            times[k] = t;
+            t += dt;
+        }
+        int rc = upload_table(c, c->layer, times, status);
+        if (rc) return rc;
+        HYG_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+        HYG_CUDA(cudaMemsetAsync(c->d_key, 0xff, sizeof(unsigned long long), c->stream));
+        CoupledSegArgs<Real> a{};
+        a.n_walls = c->n_walls;
+        a.n_channels = nch;
+        a.divergence_norm = c->norm;
+        a.coef = c->d_coef;
+        a.chan = c->d_chan;
+        a.stop = c->d_flag;
+        a.suspect = c->d_flag;
+        a.fail_key = c->d_key;
+        const int cur0 = c->cur;
+        int nseg = 0;
+        for (int64_t s0 = 0; s0 < rows; s0 += c->seg_len, ++nseg) {
+            const int len = static_cast<int>(std::min<int64_t>(c->seg_len, rows - s0));
+            a.nsteps = len;
+            a.layer0 = c->layer + s0;
+            a.table = c->d_table + s0 * nch;
+            a.seg_index = nseg;
+            const int from = (cur0 + nseg) & 1;
+            for (int i = 0; i < 4; ++i) {
+                a.in[i] = buf[from][i];
+                a.out[i] = buf[1 - from][i];
+            }
+            LaunchScope ls(c, sizeof(Real) == 8 ? "df_coupled_fused_f64" : "df_coupled_fused_f32",
+                           static_cast<double>(c->cells()) * len);
+            fast(a, grid, smem, c->stream);
+        }
+        HYG_CUDA(cudaGetLastError());
+        int flag = 0;
+        HYG_CUDA(cudaMemcpyAsync(&flag, c->d_flag, sizeof flag, cudaMemcpyDeviceToHost, c->stream));
+        HYG_CUDA(cudaStreamSynchronize(c->stream));
+        if (flag == 0) {
+            c->cur = (cur0 + nseg) & 1;
+            c->t = t;
+            c->layer += rows;
+            done += rows;
+            continue;
+        }
+        // The fast guard fired: flag = index + 1 of the first flagged segment K.
+        // Later segments returned without writing, so buf[(cur0 + K) & 1] still
+        // holds K's input.  Replay K.. with the exact per-step guard of
+        // check_bounded (building.cpp:282-300); stop at the first failure.
+        const int K = flag - 1;
+        auto time_of = [&](int64_t L) {   // time of absolute layer L inside this block
+            const int64_t i = L - c->layer;
+            return i < rows ? times[i] : t;
+        };
+        for (int k = K; k < nseg; ++k) {
+            const int from = (cur0 + k) & 1;
+            const int64_t s0 = static_cast<int64_t>(k) * c->seg_len;
+            const int len = static_cast<int>(std::min<int64_t>(c->seg_len, rows - s0));
+            a.nsteps = len;
+            a.layer0 = c->layer + s0;
+            a.seg_index = k;
+            a.table = c->d_table + s0 * nch;
+            for (int i = 0; i < 4; ++i) {
+                a.in[i] = buf[from][i];
+                a.out[i] = buf[1 - from][i];
+            }
+            HYG_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+            {
+                LaunchScope ls(c, sizeof(Real) == 8 ? "df_coupled_exact_f64" : "df_coupled_exact_f32",
+                               static_cast<double>(c->cells()) * len);
+                exact(a, grid, smem, c->stream);
+            }
+            HYG_CUDA(cudaGetLastError());
+            unsigned long long key;
+            rc = read_key(c, &key, status);
+            if (rc) return rc;
+            if (key != ~0ull) {
+                // walls that failed stopped at their failing layer (curr = the
+                // failing layer), the others at the segment end; the state is a
+                // diagnostic snapshot, `layer` names the first failing layer
+                c->cur = 1 - from;
+                const int64_t L = static_cast<int64_t>(key >> 32);
+                c->t = time_of(L);
+                c->layer = L;
+                return diverged(c, key, status);
+            }
+        }
+        // |x| >= 2 somewhere but within the norm: the exact replay produced the
+        // same state the fast pass would have
+        c->cur = (cur0 + nseg) & 1;
+        c->t = t;
+        c->layer += rows;
+        done += rows;
+    }
+    return HYG_OK;
+}
+
+int advance_fused(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
+    if (c->precision == HYG_F32) return advance_fused_t<float>(c, c->s32, nsteps, dt, status);
+    return advance_fused_t<double>(c, c->s64, nsteps, dt, status);
+}
+
+int to_f32(hyg_ctx* c, hyg_status* status) {
+    if (c->precision != HYG_F32) return HYG_OK;
+    const int threads = 256;
+    const int grid = static_cast<int>((c->cells() + threads - 1) / threads);
+    for (int i = 0; i < 4; ++i) {
+        LaunchScope ls(c, "to_dev32", 0.0);
+        k_to_dev32<<<grid, threads, 0, c->stream>>>(c->cells(), c->s64[c->cur][i], c->s32[c->cur][i]);
+    }
+    HYG_CUDA(cudaGetLastError());
+    return HYG_OK;
+}
+
+int from_f32(hyg_ctx* c, hyg_status* status) {
+    if (c->precision != HYG_F32) return HYG_OK;
+    const int threads = 256;
+    const int grid = static_cast<int>((c->cells() + threads - 1) / threads);
+    for (int i = 0; i < 4; ++i) {
+        LaunchScope ls(c, "from_dev32", 0.0);
+        k_from_dev32<<<grid, threads, 0, c->stream>>>(c->cells(), c->s32[c->cur][i], c->s64[c->cur][i]);
+    }
+    HYG_CUDA(cudaGetLastError());
+    return HYG_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+int hyg_abi_version(void) { return HYG_ABI_VERSION; }
+
+const char* hyg_strerror(int code) {
+    switch (code) {
+        case HYG_OK: return "ok";
+        case HYG_EINVAL: return "invalid argument";
+        case HYG_ESCHEMA: return "schema error";
+        case HYG_EDIVERGED: return "numerical error (divergence)";
+        case HYG_EDOMAIN: return "domain error";
+        case HYG_ECONVERGE: return "convergence error";
+        case HYG_ESCALING: return "scaling error";
+        case HYG_ECUDA: return "CUDA error";
+        case HYG_ENOTSUP: return "not supported";
+        default: return "unknown";
+    }
+}
+
+int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
+    clear_status(status);
+    if (!d || !out) {
+        set_status(status, HYG_EINVAL, "null argument");
+        return HYG_EINVAL;
+    }
+    *out = nullptr;
+    if (d->n_walls < 1 || d->n_nodes < 3 || !(d->dx > 0.0) || !d->groups || !d->biot || !d->attach) {
+        set_status(status, HYG_EINVAL, "need n_walls >= 1, n_nodes >= 3 (Grid1D wall.cpp:14), dx > 0");
+        return HYG_EINVAL;
+    }
+    if (!(d->dt > 0.0)) {   // BuildingModel::validate building.cpp:14
+        set_status(status, HYG_ESCHEMA, "dt must be positive");
+        return HYG_ESCHEMA;
+    }
+    if (d->coeff_kind != HYG_COEFF_CONSTANT && d->coeff_kind != HYG_COEFF_ANALYTIC_D) {
+        set_status(status, HYG_ENOTSUP, "coefficient model not implemented on the device");
+        return HYG_ENOTSUP;
+    }
+    // validate (building.cpp:12-52): face and link references must resolve
+    for (int w = 0; w < d->n_walls; ++w) {
+        for (int k = 0; k < 2; ++k) {
+            const hyg_face_attach& a = d->attach[2 * w + k];
+            const int lim = a.kind == HYG_FACE_ZONE ? d->n_zones : d->n_channels;
+            if (a.index < 0 || a.index >= lim || (a.kind != HYG_FACE_ZONE && a.kind != HYG_FACE_EXTERIOR)) {
+                char m[160];
+                std::snprintf(m, sizeof m, "wall %d face %d references %s %d which does not exist", w, k,
+                              a.kind == HYG_FACE_ZONE ? "zone" : "channel", a.index);
+                set_status(status, HYG_ESCHEMA, m);
+                return HYG_ESCHEMA;
+            }
+        }
+    }
+    for (int z = 0; z < d->n_zones; ++z) {
+        const hyg_zone_desc& zd = d->zones[z];
+        for (int i = 0; i < zd.n_walls; ++i)
+            if (zd.walls[i].wall < 0 || zd.walls[i].wall >= d->n_walls) {
+                set_status(status, HYG_ESCHEMA, "zone links a wall which does not exist");
+                return HYG_ESCHEMA;
+            }
+        for (int i = 0; i < zd.n_interzone; ++i)
+            if (zd.interzone[i].peer < 0 || zd.interzone[i].peer >= d->n_zones) {
+                set_status(status, HYG_ESCHEMA, "zone links a peer zone which does not exist");
+                return HYG_ESCHEMA;
+            }
+        if (zd.sources < 0 || zd.sources >= d->n_zone_sources) {
+            set_status(status, HYG_ESCHEMA, "zone references missing source schedules");
+            return HYG_ESCHEMA;
+        }
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+        set_status(status, HYG_ECUDA, "no CUDA device (this library has no CPU fallback)");
+        return HYG_ECUDA;
+    }
+    hyg_ctx* c = new hyg_ctx();
+    c->device = d->device;
+    if (cudaSetDevice(c->device) != cudaSuccess) {
+        delete c;
+        set_status(status, HYG_ECUDA, "cudaSetDevice failed");
+        return HYG_ECUDA;
+    }
+    c->n_walls = d->n_walls;
+    c->n = d->n_nodes;
+    c->dx = d->dx;
+    c->precision = d->precision;
+    c->coeff_kind = d->coeff_kind;
+    for (int i = 0; i < 4; ++i) c->p[i] = d->coeff_params[i];
+    c->dt = d->dt;
+    c->norm = d->divergence_norm > 0 ? d->divergence_norm : 1e3;
+    c->eta_factor = d->eta_factor > 0 ? d->eta_factor : 1e-2;
+    c->max_subiters = d->max_subiters > 0 ? d->max_subiters : 100;
+    c->groups.resize(c->n_walls);
+    c->biot.resize(2 * c->n_walls);
+    c->attach.resize(2 * c->n_walls);
+    std::vector<int> chan(2 * c->n_walls, 0);
+    bool all_exterior = true;
+    for (int w = 0; w < c->n_walls; ++w) {
+        const hyg_wall_groups& g = d->groups[w];
+        c->groups[w] = Groups{g.Fo_M, g.Fo_TT, g.Fo_TM, g.gamma};
+        for (int k = 0; k < 2; ++k) {
+            const hyg_face_biot& b = d->biot[2 * w + k];
+            c->biot[2 * w + k] = Biot{b.Bi_M, b.Bi_TT, b.Bi_TM};
+            const hyg_face_attach& a = d->attach[2 * w + k];
+            c->attach[2 * w + k] = Attach{a.kind, a.index};
+            if (a.kind == HYG_FACE_EXTERIOR) chan[2 * w + k] = a.index;
+            else all_exterior = false;
+        }
+    }
+    c->channels.resize(d->n_channels);
+    for (int i = 0; i < d->n_channels; ++i) {
+        c->channels[i].u.set(d->channels[i].u_inf);
+        c->channels[i].v.set(d->channels[i].v_inf);
+        c->channels[i].g.set(d->channels[i].g_inf);
+        c->channels[i].q.set(d->channels[i].q_inf);
+    }
+    for (int z = 0; z < d->n_zones; ++z) {
+        const hyg_zone_desc& zd = d->zones[z];
+        ZoneDev zz{};
+        zz.kappa_a_tt1 = zd.kappa_a_tt1;
+        zz.g_v = zd.g_v;
+        zz.q_v1 = zd.q_v1;
+        zz.q_v2 = zd.q_v2;
+        zz.sign = zd.moisture_sign == HYG_MOISTURE_AS_PRINTED ? 1.0 : -1.0;
+        zz.sources = zd.sources;
+        zz.wall_begin = static_cast<int>(c->zlinks.size());
+        for (int i = 0; i < zd.n_walls; ++i) {
+            const hyg_zone_wall_link& l = zd.walls[i];
+            c->zlinks.push_back(ZoneLinkDev{l.wall, l.face, l.Bi_M, l.Bi_TT, l.Bi_TM, l.theta_T, l.theta_M});
+        }
+        zz.wall_end = static_cast<int>(c->zlinks.size());
+        zz.inz_begin = static_cast<int>(c->inz.size());
+        for (int i = 0; i < zd.n_interzone; ++i) {
+            const hyg_interzone_link& l = zd.interzone[i];
+            c->inz.push_back(InzLinkDev{l.peer, l.g_inz, l.q_inz1, l.q_inz2});
+        }
+        zz.inz_end = static_cast<int>(c->inz.size());
+        c->zones.push_back(zz);
+    }
+    c->zsrc.resize(3 * d->n_zone_sources);
+    for (int i = 0; i < d->n_zone_sources; ++i) {
+        c->zsrc[3 * i + 0].set(d->zone_sources[i].g_o);
+        c->zsrc[3 * i + 1].set(d->zone_sources[i].q_o);
+        c->zsrc[3 * i + 2].set(d->zone_sources[i].q_h);
+    }
+    c->out_u.set(d->outdoor_u);
+    c->out_v.set(d->outdoor_v);
+    c->fused = all_exterior && d->n_zones == 0 && d->coeff_kind == HYG_COEFF_CONSTANT && fused_grid(c->n);
+    if (c->precision == HYG_F32 && !c->fused) {
+        delete c;
+        set_status(status, HYG_ENOTSUP, "fp32 state is implemented for exterior constant walls on fused grids only");
+        return HYG_ENOTSUP;
+    }
+    if (c->precision == HYG_F32 && !(c->norm >= 3.0)) {
+        delete c;
+        set_status(status, HYG_ENOTSUP, "fp32 state needs divergence_norm >= 3");
+        return HYG_ENOTSUP;
+    }
+    c->flux = false;
+    for (const auto& ch : c->channels)
+        if (!ch.flux_free()) c->flux = true;
+
+    auto fail = [&](const char* m) {
+        set_status(status, HYG_ECUDA, m);
+        hyg_destroy(c);
+        return HYG_ECUDA;
+    };
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
+    const size_t cells = static_cast<size_t>(c->cells());
+    for (int b = 0; b < 2; ++b)
+        for (int i = 0; i < 4; ++i) {
+            if (cudaMalloc(&c->s64[b][i], cells * sizeof(double)) != cudaSuccess) return fail("state alloc");
+            if (c->precision == HYG_F32 && cudaMalloc(&c->s32[b][i], cells * sizeof(float)) != cudaSuccess)
+                return fail("state alloc");
+        }
+    if (cudaMalloc(&c->d_groups, sizeof(Groups) * c->n_walls) != cudaSuccess ||
+        cudaMalloc(&c->d_biot, sizeof(Biot) * 2 * c->n_walls) != cudaSuccess ||
+        cudaMalloc(&c->d_attach, sizeof(Attach) * 2 * c->n_walls) != cudaSuccess ||
+        cudaMalloc(&c->d_chan, sizeof(int) * 2 * c->n_walls) != cudaSuccess ||
+        cudaMalloc(&c->d_coef, sizeof(WallCoef) * c->n_walls) != cudaSuccess ||
+        cudaMalloc(&c->d_flag, sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&c->d_key, sizeof(unsigned long long)) != cudaSuccess)
+        return fail("parameter alloc");
+    cudaMemcpy(c->d_groups, c->groups.data(), sizeof(Groups) * c->n_walls, cudaMemcpyHostToDevice);
+    cudaMemcpy(c->d_biot, c->biot.data(), sizeof(Biot) * 2 * c->n_walls, cudaMemcpyHostToDevice);
+    cudaMemcpy(c->d_attach, c->attach.data(), sizeof(Attach) * 2 * c->n_walls, cudaMemcpyHostToDevice);
+    cudaMemcpy(c->d_chan, chan.data(), sizeof(int) * 2 * c->n_walls, cudaMemcpyHostToDevice);
+    const int nz = std::max<int>(1, static_cast<int>(c->zones.size()));
+    for (int b = 0; b < 2; ++b)
+        if (cudaMalloc(&c->zu[b], sizeof(double) * nz) != cudaSuccess ||
+            cudaMalloc(&c->zv[b], sizeof(double) * nz) != cudaSuccess)
+            return fail("zone alloc");
+    if (!c->zones.empty()) {
+        if (cudaMalloc(&c->d_zones, sizeof(ZoneDev) * c->zones.size()) != cudaSuccess ||
+            cudaMalloc(&c->d_zlinks, sizeof(ZoneLinkDev) * std::max<size_t>(1, c->zlinks.size())) != cudaSuccess ||
+            cudaMalloc(&c->d_inz, sizeof(InzLinkDev) * std::max<size_t>(1, c->inz.size())) != cudaSuccess)
+            return fail("zone alloc");
+        cudaMemcpy(c->d_zones, c->zones.data(), sizeof(ZoneDev) * c->zones.size(), cudaMemcpyHostToDevice);
+        if (!c->zlinks.empty())
+            cudaMemcpy(c->d_zlinks, c->zlinks.data(), sizeof(ZoneLinkDev) * c->zlinks.size(), cudaMemcpyHostToDevice);
+        if (!c->inz.empty())
+            cudaMemcpy(c->d_inz, c->inz.data(), sizeof(InzLinkDev) * c->inz.size(), cudaMemcpyHostToDevice);
+    }
+    // WallField::uniform (wall.cpp:24-31) and ZoneState{} (zone.hpp:11-14): all 1
+    {
+        std::vector<double> ones(std::max<size_t>(cells, static_cast<size_t>(nz)), 1.0);
+        for (int i = 0; i < 4; ++i)
+            cudaMemcpy(c->s64[0][i], ones.data(), cells * sizeof(double), cudaMemcpyHostToDevice);
+        cudaMemcpy(c->zu[0], ones.data(), sizeof(double) * nz, cudaMemcpyHostToDevice);
+        cudaMemcpy(c->zv[0], ones.data(), sizeof(double) * nz, cudaMemcpyHostToDevice);
+    }
+    for (auto& e : c->ev) cudaEventCreate(&e);
+    if (cudaDeviceSynchronize() != cudaSuccess) return fail("init");
+    hyg_status tmp;
+    if (to_f32(c, &tmp) != HYG_OK) return fail("init f32");
+    *out = c;
+    return HYG_OK;
+}
+
+void hyg_destroy(hyg_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    drain_pending(c);
+    for (int b = 0; b < 2; ++b) {
+        for (int i = 0; i < 4; ++i) {
+            cudaFree(c->s64[b][i]);
+            cudaFree(c->s32[b][i]);
+        }
+        cudaFree(c->zu[b]);
+        cudaFree(c->zv[b]);
+    }
+    for (int i = 0; i < 4; ++i) cudaFree(c->snap[i]);
+    cudaFree(c->snap_z[0]);
+    cudaFree(c->snap_z[1]);
+    cudaFree(c->d_groups);
+    cudaFree(c->d_biot);
+    cudaFree(c->d_attach);
+    cudaFree(c->d_chan);
+    cudaFree(c->d_coef);
+    cudaFree(c->d_zones);
+    cudaFree(c->d_zlinks);
+    cudaFree(c->d_inz);
+    cudaFree(c->d_table);
+    cudaFree(c->d_boot);
+    cudaFree(c->d_src);
+    cudaFree(c->d_flag);
+    cudaFree(c->d_key);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+int hyg_set_state(hyg_ctx* c, const double* up, const double* uc, const double* vp, const double* vc,
+                  const double* zu, const double* zv, double t_star, int64_t layer) {
+    hyg_status* status = nullptr;
+    if (!c) return HYG_EINVAL;
+    cudaSetDevice(c->device);
+    const size_t bytes = static_cast<size_t>(c->cells()) * sizeof(double);
+    const double* src[4] = {up, uc, vp, vc};
+    for (int i = 0; i < 4; ++i)
+        if (src[i]) HYG_CUDA(cudaMemcpyAsync(c->s64[c->cur][i], src[i], bytes, cudaMemcpyHostToDevice, c->stream));
+    if (!c->zones.empty()) {
+        const size_t zb = c->zones.size() * sizeof(double);
+        if (zu) HYG_CUDA(cudaMemcpyAsync(c->zu[c->zcur], zu, zb, cudaMemcpyHostToDevice, c->stream));
+        if (zv) HYG_CUDA(cudaMemcpyAsync(c->zv[c->zcur], zv, zb, cudaMemcpyHostToDevice, c->stream));
+    }
+    c->t = t_star;
+    c->layer = layer;
+    hyg_status tmp;
+    int rc = to_f32(c, &tmp);
+    if (rc) return rc;
+    HYG_CUDA(cudaStreamSynchronize(c->stream));
+    return HYG_OK;
+}
+
+int hyg_get_state(hyg_ctx* c, double* up, double* uc, double* vp, double* vc, double* zu, double* zv,
+                  double* t_star, int64_t* layer) {
+    hyg_status* status = nullptr;
+    if (!c) return HYG_EINVAL;
+    cudaSetDevice(c->device);
+    hyg_status tmp;
+    int rc = from_f32(c, &tmp);
+    if (rc) return rc;
+    const size_t bytes = static_cast<size_t>(c->cells()) * sizeof(double);
+    double* dst[4] = {up, uc, vp, vc};
+    for (int i = 0; i < 4; ++i)
+        if (dst[i]) HYG_CUDA(cudaMemcpyAsync(dst[i], c->s64[c->cur][i], bytes, cudaMemcpyDeviceToHost, c->stream));
+    if (!c->zones.empty()) {
+        const size_t zb = c->zones.size() * sizeof(double);
+        if (zu) HYG_CUDA(cudaMemcpyAsync(zu, c->zu[c->zcur], zb, cudaMemcpyDeviceToHost, c->stream));
+        if (zv) HYG_CUDA(cudaMemcpyAsync(zv, c->zv[c->zcur], zb, cudaMemcpyDeviceToHost, c->stream));
+    }
+    HYG_CUDA(cudaStreamSynchronize(c->stream));
+    if (t_star) *t_star = c->t;
+    if (layer) *layer = c->layer;
+    return HYG_OK;
+}
+
+int hyg_snapshot(hyg_ctx* c) {
+    hyg_status* status = nullptr;
+    if (!c) return HYG_EINVAL;
+    cudaSetDevice(c->device);
+    const size_t es = c->precision == HYG_F32 ? sizeof(float) : sizeof(double);
+    const size_t bytes = static_cast<size_t>(c->cells()) * es;
+    const size_t nz = std::max<size_t>(1, c->zones.size());
+    for (int i = 0; i < 4; ++i) {
+        if (!c->snap[i]) HYG_CUDA(cudaMalloc(&c->snap[i], bytes));
+        const void* src = c->precision == HYG_F32 ? static_cast<const void*>(c->s32[c->cur][i])
+                                                  : static_cast<const void*>(c->s64[c->cur][i]);
+        HYG_CUDA(cudaMemcpyAsync(c->snap[i], src, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    for (int i = 0; i < 2; ++i) {
+        if (!c->snap_z[i]) HYG_CUDA(cudaMalloc(&c->snap_z[i], nz * sizeof(double)));
+        HYG_CUDA(cudaMemcpyAsync(c->snap_z[i], i ? c->zv[c->zcur] : c->zu[c->zcur], nz * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, c->stream));
+    }
+    c->snap_t = c->t;
+    c->snap_layer = c->layer;
+    return HYG_OK;
+}
+
+int hyg_restore(hyg_ctx* c) {
+    hyg_status* status = nullptr;
+    if (!c || c->snap_layer < 0) return HYG_EINVAL;
+    cudaSetDevice(c->device);
+    const size_t es = c->precision == HYG_F32 ? sizeof(float) : sizeof(double);
+    const size_t bytes = static_cast<size_t>(c->cells()) * es;
+    const size_t nz = std::max<size_t>(1, c->zones.size());
+    for (int i = 0; i < 4; ++i) {
+        void* dst = c->precision == HYG_F32 ? static_cast<void*>(c->s32[c->cur][i])
+                                            : static_cast<void*>(c->s64[c->cur][i]);
+        HYG_CUDA(cudaMemcpyAsync(dst, c->snap[i], bytes, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    for (int i = 0; i < 2; ++i)
+        HYG_CUDA(cudaMemcpyAsync(i ? c->zv[c->zcur] : c->zu[c->zcur], c->snap_z[i], nz * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, c->stream));
+    c->t = c->snap_t;
+    c->layer = c->snap_layer;
+    return HYG_OK;
+}
+
+int hyg_set_channel_table(hyg_ctx* c, int32_t channel, int64_t first_layer, int64_t n_layers,
+                          const hyg_ambient* values) {
+    if (!c || channel < 0 || channel >= static_cast<int>(c->channels.size()) || n_layers < 0 ||
+        (n_layers > 0 && !values))
+        return HYG_EINVAL;
+    ChannelHost& ch = c->channels[channel];
+    ch.tab_first = first_layer;
+    ch.tab.assign(values, values + n_layers);
+    ++c->gen;
+    c->flux = false;
+    for (const auto& x : c->channels)
+        if (!x.flux_free()) c->flux = true;
+    return HYG_OK;
+}
+
+int hyg_bootstrap(hyg_ctx* c, int32_t kind, hyg_status* status) {
+    clear_status(status);
+    if (!c) return HYG_EINVAL;
+    cudaSetDevice(c->device);
+    if (kind != HYG_BOOT_IMPLICIT && kind != HYG_BOOT_EXPLICIT) {
+        set_status(status, HYG_EINVAL, "unknown bootstrap kind");
+        return HYG_EINVAL;
+    }
+    if (kind == HYG_BOOT_IMPLICIT && (c->coeff_kind != HYG_COEFF_CONSTANT || !c->zones.empty())) {
+        set_status(status, HYG_ENOTSUP,
+                   "implicit starting step on the device: constant-coefficient walls without zones only");
+        return HYG_ENOTSUP;
+    }
+    int rc = from_f32(c, status);
+    if (rc) return rc;
+    // forcing: explicit step at layer-n time, implicit step at t^{n+1} (building.cpp:196)
+    const double t_force = kind == HYG_BOOT_EXPLICIT ? c->t : c->t + c->dt;
+    {   // one ambient row, kept apart from the cached per-layer table
+        const int64_t lay = c->layer + (kind == HYG_BOOT_EXPLICIT ? 0 : 1);
+        const int nch = std::max<int>(1, static_cast<int>(c->channels.size()));
+        c->h_boot.assign(nch, Ambient{1, 1, 0, 0});
+        for (int ch = 0; ch < static_cast<int>(c->channels.size()); ++ch)
+            c->h_boot[ch] = c->channels[ch].at(lay, t_force);
+        if (!c->d_boot) HYG_CUDA(cudaMalloc(&c->d_boot, sizeof(Ambient) * nch));
+        HYG_CUDA(cudaMemcpyAsync(c->d_boot, c->h_boot.data(), sizeof(Ambient) * nch, cudaMemcpyHostToDevice,
+                                 c->stream));
+    }
+    HYG_CUDA(cudaMemsetAsync(c->d_key, 0xff, sizeof(unsigned long long), c->stream));
+    StepArgs a = step_args(c, c->cur, c->dt);
+    a.amb = c->d_boot;
+    if (kind == HYG_BOOT_EXPLICIT) {
+        LaunchScope ls(c, "explicit_boot", static_cast<double>(c->cells()));
+        k_explicit_boot<<<static_cast<int>((c->cells() + 255) / 256), 256, 0, c->stream>>>(a);
+    } else {
+        double* scr = nullptr;
+        HYG_CUDA(cudaMallocAsync(&scr, sizeof(double) * 3 * static_cast<size_t>(c->cells()), c->stream));
+        {
+            LaunchScope ls(c, "implicit_unit_boot", static_cast<double>(c->cells()));
+            k_implicit_unit_boot<<<(c->n_walls + 127) / 128, 128, 0, c->stream>>>(a, scr);
+        }
+        HYG_CUDA(cudaFreeAsync(scr, c->stream));
+    }
+    HYG_CUDA(cudaGetLastError());
+    c->cur ^= 1;
+    if (!c->zones.empty()) {
+        // zone states carry over unchanged for the explicit start (zones are
+        // advanced by the building steps only)
+    }
+    unsigned long long key;
+    rc = read_key(c, &key, status);
+    if (rc) return rc;
+    c->t = c->t + c->dt;
+    c->layer += 1;
+    if (status) status->subiterations = kind == HYG_BOOT_IMPLICIT ? 2 : 0;
+    rc = to_f32(c, status);
+    if (rc) return rc;
+    if (key != ~0ull) return diverged(c, key, status);
+    return HYG_OK;
+}
+
+int hyg_advance(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
+    clear_status(status);
+    if (!c || nsteps < 0) return HYG_EINVAL;
+    if (nsteps == 0) return HYG_OK;
+    cudaSetDevice(c->device);
+    if (!(dt > 0.0)) dt = c->dt;
+    int rc = c->fused ? advance_fused(c, nsteps, dt, status) : advance_general(c, nsteps, dt, status);
+    if (status && rc == HYG_OK) status->code = HYG_OK;
+    return rc;
+}
+
+int hyg_run(hyg_ctx* c, double horizon, double cadence, int32_t boot_kind, hyg_frame_fn frame,
+            void* user, hyg_status* status) {
+    clear_status(status);
+    if (!c) return HYG_EINVAL;
+    if (!(horizon >= 0.0)) {   // validate building.cpp:13
+        set_status(status, HYG_ESCHEMA, "horizon must be non-negative");
+        return HYG_ESCHEMA;
+    }
+    const int64_t nsteps = std::llround(horizon / c->dt);
+    const int64_t stride = std::max<int64_t>(1, std::llround(cadence / c->dt));
+    if (frame) frame(user, c->layer, c->t, c);
+    int64_t done = 0;
+    if (nsteps > 0) {
+        const int rc = hyg_bootstrap(c, boot_kind, status);
+        if (rc) return rc;
+        ++done;
+        if (frame && (done % stride == 0 || done == nsteps)) frame(user, c->layer, c->t, c);
+    }
+    while (done < nsteps) {
+        const int64_t chunk = std::min(stride - done % stride, nsteps - done);
+        const int rc = hyg_advance(c, chunk, c->dt, status);
+        if (rc) return rc;
+        done += chunk;
+        if (frame && (done % stride == 0 || done == nsteps)) frame(user, c->layer, c->t, c);
+    }
+    return HYG_OK;
+}
+
+int hyg_synchronize(hyg_ctx* c) {
+    if (!c) return HYG_EINVAL;
+    cudaSetDevice(c->device);
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) return HYG_ECUDA;
+    drain_pending(c);
+    return HYG_OK;
+}
+
+int hyg_host_register(void* ptr, size_t bytes) {
+    return cudaHostRegister(ptr, bytes, cudaHostRegisterDefault) == cudaSuccess ? HYG_OK : HYG_ECUDA;
+}
+int hyg_host_unregister(void* ptr) { return cudaHostUnregister(ptr) == cudaSuccess ? HYG_OK : HYG_ECUDA; }
+
+int hyg_event_record(hyg_ctx* c, int32_t slot) {
+    if (!c || slot < 0 || slot >= 16) return HYG_EINVAL;
+    return cudaEventRecord(c->ev[slot], c->stream) == cudaSuccess ? HYG_OK : HYG_ECUDA;
+}
+
+int hyg_event_elapsed_ms(hyg_ctx* c, int32_t a, int32_t b, double* ms) {
+    if (!c || a < 0 || a >= 16 || b < 0 || b >= 16 || !ms) return HYG_EINVAL;
+    if (cudaEventSynchronize(c->ev[b]) != cudaSuccess) return HYG_ECUDA;
+    float f = 0.f;
+    if (cudaEventElapsedTime(&f, c->ev[a], c->ev[b]) != cudaSuccess) return HYG_ECUDA;
+    *ms = f;
+    return HYG_OK;
+}
+
+int hyg_set_profiling(hyg_ctx* c, int32_t on) {
+    if (!c) return HYG_EINVAL;
+    c->profiling = on != 0;
+    return HYG_OK;
+}
+int hyg_kernel_stats_count(hyg_ctx* c) {
+    if (!c) return 0;
+    hyg_synchronize(c);
+    return static_cast<int>(c->stats.size());
+}
+int hyg_kernel_stats(hyg_ctx* c, int32_t i, const char** name, int64_t* launches, double* ms,
+                     double* updates) {
+    if (!c || i < 0 || i >= static_cast<int>(c->stats.size())) return HYG_EINVAL;
+    const Stat& s = c->stats[i];
+    if (name) *name = s.name.c_str();
+    if (launches) *launches = s.launches;
+    if (ms) *ms = s.ms;
+    if (updates) *updates = s.updates;
+    return HYG_OK;
+}
+int hyg_reset_kernel_stats(hyg_ctx* c) {
+    if (!c) return HYG_EINVAL;
+    hyg_synchronize(c);
+    c->stats.clear();
+    return HYG_OK;
+}
+int64_t hyg_launch_count(hyg_ctx* c) { return c ? c->launches : 0; }
+
+}  // extern "C"
+
+// ---- FP64 pipe probe (roofline denominator; MEASURED_PEAKS.json has no FP64) ----
+namespace {
+__global__ void k_dfma_probe(double* out, int iters) {
+    double a0 = threadIdx.x * 1e-9, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+           a6 = a0 + 6, a7 = a0 + 7;
+    const double b = 0.999999, c = 1e-7;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+            a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+        }
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+}
+}  // namespace
+
+extern "C" int hyg_probe_fp64_peak(int32_t device, double* tflops, double* sm_clock_mhz) {
+    hyg_status* status = nullptr;
+    HYG_CUDA(cudaSetDevice(device));
+    int sms = 0, clk = 0;
+    HYG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, device);
+    const int blocks = sms * 8, threads = 256, iters = 20000;
+    double* o = nullptr;
+    HYG_CUDA(cudaMalloc(&o, sizeof(double) * blocks * threads));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_dfma_probe<<<blocks, threads>>>(o, 200);   // warm-up
+    cudaEventRecord(e0);
+    k_dfma_probe<<<blocks, threads>>>(o, iters);
+    cudaEventRecord(e1);
+    HYG_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(o);
+    const double flops = 2.0 * 64.0 * iters * static_cast<double>(blocks) * threads;
+    if (tflops) *tflops = flops / (ms * 1e-3) / 1e12;
+    if (sm_clock_mhz) *sm_clock_mhz = clk / 1000.0;
+    return HYG_OK;
+}

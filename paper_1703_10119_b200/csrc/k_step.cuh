@@ -1,0 +1,383 @@
+// k_step.cuh — one-step kernels: the general DF step (any grid size, zone
+// faces, analytic coefficient functor), the explicit and implicit starting
+// steps, the zone air balance and small utility kernels.
+//
+// These are the paths the fused K1 kernel does not cover: walls whose faces
+// read zone states every step (step_explicit, building.cpp:152-187), grids
+// that do not tile onto lanes, state-dependent coefficients.  One thread per
+// (wall, node); layers stream through HBM/L2, so these kernels are
+// memory-bound (48 B/node-update for the four read + two written layers).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "hyg_coef.cuh"
+#include "k_coupled.cuh"
+
+namespace hyg {
+
+enum : int { kCoeffConstant = 0, kCoeffAnalyticD = 1 };
+
+struct Attach { int kind, index; };   // 0 exterior(channel), 1 zone
+
+struct StepArgs {
+    int n_walls, n;
+    double dx, dt;
+    const Groups* groups;
+    const Biot* biot;           // [2*w+k]
+    const Attach* attach;       // [2*w+k]
+    int n_channels;
+    const Ambient* amb;         // ambient row of this step [n_channels]
+    const double* zu;           // zone states of layer n (nullable)
+    const double* zv;
+    int coeff_kind;
+    double p[4];
+    const double* in[4];        // up, uc, vp, vc
+    double* out[4];             // new prev (= old curr), new curr
+    int64_t layer;              // index of layer n
+    double norm;
+    unsigned long long* fail_key;
+};
+
+// d(v) functor of HYG_COEFF_ANALYTIC_D: k_M* = 1 + p0 v + p1 exp(-p2 (v - p3)^2)
+__device__ __forceinline__ double analytic_kM(const double* p, double v) {
+    const double d = v - p[3];
+    return 1.0 + p[0] * v + p[1] * exp(-p[2] * d * d);
+}
+
+struct FaceVals { double Bi_M, Bi_TT, Bi_TM, u_inf, v_inf, g_inf, q_inf; };
+
+__device__ __forceinline__ FaceVals resolve(const StepArgs& a, int w, int k) {
+    // resolve_face (building.cpp:107-126), no radiation
+    const Biot b = a.biot[2 * w + k];
+    const Attach at = a.attach[2 * w + k];
+    FaceVals f{b.Bi_M, b.Bi_TT, b.Bi_TM, 1.0, 1.0, 0.0, 0.0};
+    if (at.kind == 0) {
+        const Ambient am = a.amb[at.index];
+        f.u_inf = am.u;
+        f.v_inf = am.v;
+        f.g_inf = am.g;
+        f.q_inf = am.q + 0.0;
+    } else {
+        f.u_inf = a.zu[at.index];
+        f.v_inf = a.zv[at.index];
+    }
+    return f;
+}
+
+// df_step_coupled (wall.cpp:144-194), one node per thread, literal form.
+__device__ __forceinline__ void coupled_node(const StepArgs& a, int w, int j, double& un,
+                                             double& vn) {
+    const int n = a.n;
+    const double dx = a.dx, dt = a.dt;
+    const Groups p = a.groups[w];
+    const size_t o = static_cast<size_t>(w) * n;
+    const double *up = a.in[0] + o, *uc = a.in[1] + o, *vp = a.in[2] + o, *vc = a.in[3] + o;
+    const double lam = 2.0 * p.Fo_M * dt / (dx * dx);
+    const double mu = 2.0 * p.Fo_TT * dt / (dx * dx);
+    const double beta = 2.0 * p.Fo_TM * p.gamma * dt / (dx * dx);
+    const double ratio = p.Fo_TT != 0.0 ? p.Fo_TM * p.gamma / p.Fo_TT : 0.0;
+    if (j > 0 && j < n - 1) {
+        vn = ((1.0 - lam) * vp[j] + lam * (vc[j + 1] + vc[j - 1])) / (1.0 + lam);
+        un = ((1.0 - mu) * up[j] + mu * (uc[j + 1] + uc[j - 1]) + (p.gamma - beta) * vp[j] +
+              beta * (vc[j + 1] + vc[j - 1]) - (p.gamma + beta) * vn) /
+             (1.0 + mu);
+        return;
+    }
+    const int k = j == 0 ? 0 : 1;
+    const int jn = j == 0 ? 1 : n - 2;
+    const FaceVals b = resolve(a, w, k);
+    const double cpl = lam * dx * b.Bi_M;
+    vn = ((1.0 - lam - cpl) * vp[j] + 2.0 * lam * vc[jn] + 2.0 * lam * dx * (b.Bi_M * b.v_inf + b.g_inf)) /
+         (1.0 + lam + cpl);
+    const double vbar = 0.5 * (vn + vp[j]);
+    const double vg = vc[jn] - 2.0 * dx * (b.Bi_M * (vbar - b.v_inf) - b.g_inf);
+    const double cplu = mu * dx * b.Bi_TT;
+    un = ((1.0 - mu - cplu) * up[j] + 2.0 * mu * uc[jn] + mu * ratio * (vc[jn] - vg) +
+          2.0 * mu * dx * (b.Bi_TT * b.u_inf - b.Bi_TM * (vbar - b.v_inf) + b.q_inf) +
+          (p.gamma - beta) * vp[j] + beta * (vc[jn] + vg) - (p.gamma + beta) * vn) /
+         (1.0 + mu + cplu);
+}
+
+// df_step_nonlinear (wall.cpp:196-264) for the analytic functor (k_M* = d(v),
+// the other five starred coefficients 1), one node per thread.  StarTables
+// (wall.cpp:89-138): node values at j, half-node values at the midpoint
+// state average.
+__device__ __forceinline__ void analytic_node(const StepArgs& a, int w, int j, double& un,
+                                              double& vn) {
+    const int n = a.n;
+    const double dx = a.dx, dt = a.dt;
+    const Groups p = a.groups[w];
+    const size_t o = static_cast<size_t>(w) * n;
+    const double *up = a.in[0] + o, *uc = a.in[1] + o, *vp = a.in[2] + o, *vc = a.in[3] + o;
+    const double ad = p.Fo_M * dt / (dx * dx);
+    const double b_ = p.Fo_TT * dt / (dx * dx);
+    const double g_ = p.Fo_TM * p.gamma * dt / (dx * dx);
+    const double ratio = p.Fo_TT != 0.0 ? p.Fo_TM * p.gamma / p.Fo_TT : 0.0;
+    const double cm = 1.0, ctt = 1.0, ctm = 1.0;
+    if (j > 0 && j < n - 1) {
+        const double kp = analytic_kM(a.p, 0.5 * (vc[j] + vc[j + 1]));
+        const double km = analytic_kM(a.p, 0.5 * (vc[j - 1] + vc[j]));
+        vn = ((cm - ad * (kp + km)) * vp[j] + 2.0 * ad * (kp * vc[j + 1] + km * vc[j - 1])) /
+             (cm + ad * (kp + km));
+        const double ktp = 1.0, ktm = 1.0, kmp = 1.0, kmm = 1.0;
+        un = ((ctt - b_ * (ktp + ktm)) * up[j] - p.gamma * ctm * (vn - vp[j]) +
+              2.0 * b_ * (ktp * uc[j + 1] + ktm * uc[j - 1]) +
+              2.0 * g_ * (kmp * vc[j + 1] + kmm * vc[j - 1]) - g_ * (kmp + kmm) * (vn + vp[j])) /
+             (ctt + b_ * (ktp + ktm));
+        return;
+    }
+    const int k = j == 0 ? 0 : 1;
+    const int jn = j == 0 ? 1 : n - 2;
+    const FaceVals b = resolve(a, w, k);
+    const double km_b = analytic_kM(a.p, vc[j]);                       // ghost side: node value
+    const double kp_b = analytic_kM(a.p, j == 0 ? 0.5 * (vc[0] + vc[1]) : 0.5 * (vc[n - 2] + vc[n - 1]));
+    const double cpl = 2.0 * ad * dx * b.Bi_M;
+    vn = ((cm - ad * (kp_b + km_b) - cpl) * vp[j] + 2.0 * ad * (kp_b + km_b) * vc[jn] +
+          4.0 * ad * dx * (b.Bi_M * b.v_inf + b.g_inf)) /
+         (cm + ad * (kp_b + km_b) + cpl);
+    const double kt_b = 1.0, kTM_b = 1.0, ktp_b = 1.0, kmp_b = 1.0;
+    const double vbar = 0.5 * (vn + vp[j]);
+    const double vg = vc[jn] - (2.0 * dx / km_b) * (b.Bi_M * (vbar - b.v_inf) - b.g_inf);
+    const double cplu = 2.0 * b_ * dx * b.Bi_TT;
+    un = ((ctt - b_ * (ktp_b + kt_b) - cplu) * up[j] - p.gamma * ctm * (vn - vp[j]) +
+          2.0 * b_ * (ktp_b + kt_b) * uc[jn] + 2.0 * b_ * ratio * kTM_b * (vc[jn] - vg) -
+          4.0 * b_ * dx * (b.Bi_TM * (vbar - b.v_inf) - b.q_inf) + 2.0 * cplu * b.u_inf +
+          2.0 * g_ * (kmp_b * vc[jn] + kTM_b * vg) - g_ * (kmp_b + kTM_b) * (vn + vp[j])) /
+         (ctt + b_ * (ktp_b + kt_b) + cplu);
+}
+
+// One DF step of every wall; guard per node (exact check_bounded semantics).
+__global__ void k_df_step_general(const StepArgs a) {
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t total = static_cast<int64_t>(a.n_walls) * a.n;
+    if (tid >= total) return;
+    if (*a.fail_key != ~0ull) return;    // an earlier step failed: freeze
+    const int w = static_cast<int>(tid / a.n), j = static_cast<int>(tid % a.n);
+    double un, vn;
+    if (a.coeff_kind == kCoeffConstant) coupled_node(a, w, j, un, vn);
+    else analytic_node(a, w, j, un, vn);
+    a.out[0][tid] = a.in[1][tid];
+    a.out[2][tid] = a.in[3][tid];
+    a.out[1][tid] = un;
+    a.out[3][tid] = vn;
+    if (!(fabs(un) <= a.norm) || !(fabs(vn) <= a.norm)) {
+        const unsigned long long key =
+            (static_cast<unsigned long long>(a.layer + 1) << 32) | static_cast<unsigned>(w);
+        atomicMin(a.fail_key, key);
+    }
+}
+
+// ---- zones -----------------------------------------------------------------
+struct ZoneDev {
+    double kappa_a_tt1, g_v, q_v1, q_v2, sign;
+    int sources;
+    int wall_begin, wall_end;     // range in the link arrays
+    int inz_begin, inz_end;
+};
+struct ZoneLinkDev { int wall, face; double Bi_M, Bi_TT, Bi_TM, theta_T, theta_M; };
+struct InzLinkDev { int peer; double g_inz, q_inz1, q_inz2; };
+
+struct ZoneArgs {
+    int n_zones, n;
+    double dt;
+    const ZoneDev* zones;
+    const ZoneLinkDev* links;
+    const InzLinkDev* inz;
+    const double* src;       // this step: [n_sources][3] (g_o, q_o, q_h) then outdoor u, v
+    int n_sources;
+    const double* uc;        // wall layer n (surface samples)
+    const double* vc;
+    const double* zu_in;
+    const double* zv_in;
+    double* zu_out;
+    double* zv_out;
+    int64_t layer;
+    double norm;
+    unsigned long long* fail_key;
+};
+
+// zone_step_explicit (zone.cpp:69-74) of zone_rhs (zone.cpp:26-53) with the
+// layer-n samples gathered as in building.cpp:128-140,162-164.
+__global__ void k_zone_step(const ZoneArgs a) {
+    const int z = blockIdx.x * blockDim.x + threadIdx.x;
+    if (z >= a.n_zones) return;
+    if (*a.fail_key != ~0ull) return;
+    const ZoneDev d = a.zones[z];
+    const double u_a = a.zu_in[z], v_a = a.zv_in[z];
+    const double* s = a.src + 3 * d.sources;
+    const double u_inf = a.src[3 * a.n_sources + 0], v_inf = a.src[3 * a.n_sources + 1];
+    double du = s[1] + s[2] + d.q_v1 * (u_inf * v_inf - u_a * v_a) + d.q_v2 * (u_inf - u_a);
+    double dv = s[0] + d.g_v * (v_inf - v_a);
+    for (int i = d.inz_begin; i < d.inz_end; ++i) {
+        const InzLinkDev l = a.inz[i];
+        const double pu = a.zu_in[l.peer], pv = a.zv_in[l.peer];
+        du += l.q_inz1 * (pu * pv - u_a * v_a) + l.q_inz2 * (pu - u_a);
+        dv += l.g_inz * (pv - v_a);
+    }
+    for (int i = d.wall_begin; i < d.wall_end; ++i) {
+        const ZoneLinkDev l = a.links[i];
+        const size_t idx = static_cast<size_t>(l.wall) * a.n + (l.face == 0 ? 0 : a.n - 1);
+        const double us = a.uc[idx], vs = a.vc[idx];
+        du += l.Bi_TT * l.theta_T * (us - u_a) + l.Bi_TM * l.theta_T * (vs - v_a);
+        dv += d.sign * l.Bi_M * l.theta_M * (v_a - vs);
+    }
+    const double nu = u_a + a.dt * (du / (1.0 + d.kappa_a_tt1));
+    const double nv = v_a + a.dt * dv;
+    a.zu_out[z] = nu;
+    a.zv_out[z] = nv;
+    if (!isfinite(nu) || !isfinite(nv) || fabs(nu) > a.norm || fabs(nv) > a.norm) {
+        // zone failures rank after every wall of the same layer (building.cpp:288-299)
+        const unsigned long long key = (static_cast<unsigned long long>(a.layer + 1) << 32) | 0xffffffffu;
+        atomicMin(a.fail_key, key);
+    }
+}
+
+// ---- starting steps --------------------------------------------------------
+// euler_explicit_step (wall.cpp:266-317), one node per thread; coefficient
+// evaluations are clamped (strict=false) — the analytic functor has no box.
+__global__ void k_explicit_boot(const StepArgs a) {
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t total = static_cast<int64_t>(a.n_walls) * a.n;
+    if (tid >= total) return;
+    const int n = a.n;
+    const int w = static_cast<int>(tid / n), j = static_cast<int>(tid % n);
+    const Groups p = a.groups[w];
+    const double dx = a.dx, dt = a.dt;
+    const size_t o = static_cast<size_t>(w) * n;
+    const double *uc = a.in[1] + o, *vc = a.in[3] + o;
+    const bool an = a.coeff_kind == kCoeffAnalyticD;
+    auto kM_node = [&](int i) { return an ? analytic_kM(a.p, vc[i]) : 1.0; };
+    auto kM_half = [&](int i) { return an ? analytic_kM(a.p, 0.5 * (vc[i] + vc[i + 1])) : 1.0; };
+    // ghost values from layer-n boundary states (wall.cpp:276-288)
+    auto ghosts = [&](int k, double& vg, double& ug) {
+        const int jb = k == 0 ? 0 : n - 1, jn = k == 0 ? 1 : n - 2;
+        const FaceVals b = resolve(a, w, k);
+        const double nkM = kM_node(jb), nkTM = 1.0, nkTT = 1.0;
+        vg = vc[jn] - (2.0 * dx / nkM) * (b.Bi_M * (vc[jb] - b.v_inf) - b.g_inf);
+        ug = uc[jn] + (p.Fo_TM * p.gamma * nkTM) / (p.Fo_TT * nkTT) * (vc[jn] - vg) -
+             (2.0 * dx / nkTT) * (b.Bi_TT * (uc[jb] - b.u_inf) + b.Bi_TM * (vc[jb] - b.v_inf) - b.q_inf);
+    };
+    double vL, vR, uL, uR;
+    if (j == 0) ghosts(0, vL, uL); else { vL = vc[j - 1]; uL = uc[j - 1]; }
+    if (j == n - 1) ghosts(1, vR, uR); else { vR = vc[j + 1]; uR = uc[j + 1]; }
+    const double rdt = dt / (dx * dx);
+    const double km = j == 0 ? kM_node(0) : kM_half(j - 1);
+    const double kp = j == n - 1 ? kM_node(n - 1) : kM_half(j);
+    const double ktm = 1.0, ktp = 1.0, kmm = 1.0, kmp = 1.0, cM = 1.0, cTM = 1.0, cTT = 1.0;
+    const double div_v = kp * (vR - vc[j]) - km * (vc[j] - vL);
+    const double vn = vc[j] + rdt * p.Fo_M * div_v / cM;
+    const double div_u = ktp * (uR - uc[j]) - ktm * (uc[j] - uL);
+    const double div_vm = kmp * (vR - vc[j]) - kmm * (vc[j] - vL);
+    const double un = uc[j] + (rdt * (p.Fo_TT * div_u + p.Fo_TM * p.gamma * div_vm) -
+                               p.gamma * cTM * (vn - vc[j])) / cTT;
+    a.out[0][tid] = uc[j];
+    a.out[2][tid] = vc[j];
+    a.out[1][tid] = un;
+    a.out[3][tid] = vn;
+    if (!(fabs(un) <= a.norm) || !(fabs(vn) <= a.norm)) {
+        const unsigned long long key =
+            (static_cast<unsigned long long>(a.layer + 1) << 32) | static_cast<unsigned>(w);
+        atomicMin(a.fail_key, key);
+    }
+}
+
+// implicit_wall_pass_unit (wall.cpp:398-429) with the factorisation of
+// cached_factors (wall.cpp:360-395) and FactoredTridiag (wall.cpp:322-346).
+// One thread per wall; scratch is node-major [n][n_walls] (coalesced).
+// Used for the constant-coefficient starting step (bootstrap_first_layer,
+// and step_implicit without zones, which converges after the second pass
+// with an identical iterate).  Writes layer 1 into out[1]/out[3] and copies
+// layer 0 into out[0]/out[2].
+__global__ void k_implicit_unit_boot(const StepArgs a, double* scr) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= a.n_walls) return;
+    const int n = a.n, B = a.n_walls;
+    const double dx = a.dx, dt = a.dt;
+    const Groups p = a.groups[w];
+    const size_t o = static_cast<size_t>(w) * n;
+    const double *uc = a.in[1] + o, *vc = a.in[3] + o;
+    double* M = scr;                         // m[i]
+    double* INV = scr + static_cast<size_t>(n) * B;
+    double* X = scr + 2 * static_cast<size_t>(n) * B;   // solution vector
+    auto at = [&](double* base, int i) -> double& { return base[static_cast<size_t>(i) * B + w]; };
+    const FaceVals L = resolve(a, w, 0), R = resolve(a, w, 1);
+    const double r = p.Fo_M * dt / (dx * dx);
+    const double rb = p.Fo_TT * dt / (dx * dx);
+    const double rg = p.Fo_TM * p.gamma * dt / (dx * dx);
+    // tridiagonal coefficient of row i for the unit matrices (wall.cpp:369-393)
+    auto lo_ = [&](int i, double rr) { return i == 0 ? 0.0 : (i == n - 1 ? -2.0 * rr : -rr); };
+    auto up_ = [&](int i, double rr) { return i == 0 ? -2.0 * rr : (i == n - 1 ? 0.0 : -rr); };
+    auto di_ = [&](int i, double rr, double b0, double b1) {
+        return i == 0 ? 1.0 + 2.0 * rr + 2.0 * rr * dx * b0
+                      : (i == n - 1 ? 1.0 + 2.0 * rr + 2.0 * rr * dx * b1 : 1.0 + 2.0 * rr);
+    };
+    auto factor = [&](double rr, double b0, double b1) {
+        double dp = di_(0, rr, b0, b1);
+        at(M, 0) = 0.0;
+        at(INV, 0) = 1.0 / dp;
+        for (int i = 1; i < n; ++i) {
+            const double m = lo_(i, rr) * at(INV, i - 1);
+            at(M, i) = m;
+            dp = di_(i, rr, b0, b1) - m * up_(i - 1, rr);
+            at(INV, i) = 1.0 / dp;
+        }
+    };
+    auto solve = [&](double rr) {
+        for (int i = 1; i < n; ++i) at(X, i) -= at(M, i) * at(X, i - 1);
+        at(X, n - 1) *= at(INV, n - 1);
+        for (int i = n - 1; i-- > 0;) at(X, i) = (at(X, i) - up_(i, rr) * at(X, i + 1)) * at(INV, i);
+    };
+    // moisture
+    factor(r, L.Bi_M, R.Bi_M);
+    for (int i = 0; i < n; ++i) at(X, i) = vc[i];
+    at(X, 0) += 2.0 * r * dx * (L.Bi_M * L.v_inf + L.g_inf);
+    at(X, n - 1) += 2.0 * r * dx * (R.Bi_M * R.v_inf + R.g_inf);
+    solve(r);
+    double* vout = a.out[3] + o;
+    for (int i = 0; i < n; ++i) vout[i] = at(X, i);
+    const double* vN = vout;
+    // energy right-hand side with the new moisture layer
+    for (int j = 1; j + 1 < n; ++j)
+        at(X, j) = uc[j] - p.gamma * (vN[j] - vc[j]) + rg * (vN[j + 1] - 2.0 * vN[j] + vN[j - 1]);
+    at(X, 0) = uc[0] - p.gamma * (vN[0] - vc[0]) + 2.0 * rg * (vN[1] - vN[0]) +
+               2.0 * rb * dx * (L.Bi_TT * L.u_inf - L.Bi_TM * (vN[0] - L.v_inf) + L.q_inf);
+    at(X, n - 1) = uc[n - 1] - p.gamma * (vN[n - 1] - vc[n - 1]) + 2.0 * rg * (vN[n - 2] - vN[n - 1]) +
+                   2.0 * rb * dx * (R.Bi_TT * R.u_inf - R.Bi_TM * (vN[n - 1] - R.v_inf) + R.q_inf);
+    factor(rb, L.Bi_TT, R.Bi_TT);
+    solve(rb);
+    double* uout = a.out[1] + o;
+    double mx = 0.0;
+    bool finite = true;
+    for (int i = 0; i < n; ++i) {
+        uout[i] = at(X, i);
+        a.out[0][o + i] = uc[i];
+        a.out[2][o + i] = vc[i];
+        mx = fmax(mx, fmax(fabs(uout[i]), fabs(vout[i])));
+        finite = finite && isfinite(uout[i]) && isfinite(vout[i]);
+    }
+    if (!(mx <= a.norm) || !finite) {
+        const unsigned long long key =
+            (static_cast<unsigned long long>(a.layer + 1) << 32) | static_cast<unsigned>(w);
+        atomicMin(a.fail_key, key);
+    }
+}
+
+// ---- utilities ---------------------------------------------------------------
+__global__ void k_coupled_coef(int n_walls, double dx, double dt, const Groups* g, const Biot* b,
+                               WallCoef* c) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w < n_walls) coupled_coef(g[w], dx, dt, b[2 * w], b[2 * w + 1], c[w]);
+}
+
+// fp64 state <-> fp32 deviations from the uniform state 1
+__global__ void k_to_dev32(int64_t count, const double* in, float* out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < count) out[i] = static_cast<float>(in[i] - 1.0);
+}
+__global__ void k_from_dev32(int64_t count, const float* in, double* out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < count) out[i] = 1.0 + static_cast<double>(in[i]);
+}
+
+}  // namespace hyg
