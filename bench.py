@@ -84,7 +84,10 @@ class Clocks:
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) == 7:
-                self.rows.append(parts)
+                self.rows.append((time.time(), parts))
+
+    def mark(self, which: str):
+        setattr(self, which, time.time())
 
     def stop(self) -> dict:
         if self.proc is None:
@@ -95,7 +98,8 @@ class Clocks:
         except subprocess.TimeoutExpired:
             self.proc.kill()
         self.t.join(timeout=2)
-        rows = [r for r in self.rows if r[0].replace(".", "").isdigit()]
+        t0, t1 = getattr(self, "t_start", 0.0), getattr(self, "t_end", 1e30)
+        rows = [r for (ts, r) in self.rows if t0 <= ts <= t1 and r[0].replace(".", "").isdigit()]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         sm = [float(r[0]) for r in rows]
@@ -206,11 +210,14 @@ def main():
         ctx.bootstrap(w.boot)
         ctx.advance(nsteps - 1)
 
+    # the sampler starts before the warm-up: nvidia-smi start-up stalls the
+    # device briefly and must not fall inside the timed region
+    clocks = Clocks(local)
+    clocks.start()
     for _ in range(args.warmup):
         one_run()
     ctx.synchronize()
-    clocks = Clocks(local)
-    clocks.start()
+    clocks.mark("t_start")
     launches0 = ctx.launches
     barrier()
     torch.cuda.synchronize()
@@ -222,6 +229,7 @@ def main():
     barrier()
     torch.cuda.synchronize()
     ms = ctx.elapsed_ms(0, 1)
+    clocks.mark("t_end")
     clk = clocks.stop()
     launches = ctx.launches - launches0
     ms_max = max_over_ranks(ms)
@@ -245,7 +253,8 @@ def main():
     if not args.no_e2e:
         host = {k: np.ascontiguousarray(v) for k, v in w.init.items()}
         out = {k: np.empty_like(host[k]) for k in ("u_prev", "u_curr", "v_prev", "v_curr")}
-        for a in list(host.values()) + list(out.values()):
+        pinned = list(host.values()) + list(out.values())
+        for a in pinned:
             api.load_library().hyg_host_register(a.ctypes.data, a.nbytes)
         e2e_steps = max(1, min(args.steps, 3))
         barrier()
@@ -258,7 +267,7 @@ def main():
             ctx.get_state(out)
         ctx.record(3)
         ms_e2e = max_over_ranks(ctx.elapsed_ms(2, 3))
-        for a in list(host.values()) + list(out.values()):
+        for a in pinned:
             api.load_library().hyg_host_unregister(a.ctypes.data)
         b = 4 * w.cells * 8
         e2e = {"value": float(w.cells) * nsteps * e2e_steps * world / (ms_e2e * 1e-3), "unit": UNIT,

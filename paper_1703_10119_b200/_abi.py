@@ -135,4 +135,4 @@ def header_symbols(path) -> list[str]:
     """Function names declared in include/hygro_b200.h."""
     import re
     text = open(path).read()
-    return sorted(set(re.findall(r"\b(hyg_[a-z0-9_]+)\s*\(", text)) - {"hyg_frame_fn"})
+    return sorted(set(re.findall(r"\b(hyg_[a-z0-9_]+)\s*\(", text)) - {"hyg_frame_fn", "hyg_signal"})

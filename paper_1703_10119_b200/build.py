@@ -41,7 +41,8 @@ def _stale(target: Path, deps) -> bool:
 
 def build_library(force: bool = False, verbose: bool = False) -> Path:
     if force or _stale(LIB, DEPS):
-        cmd = [_nvcc(), *NVCC_FLAGS, "-o", str(LIB), *map(str, SOURCES)]
+        ccbin = ["-ccbin", "/usr/bin/g++"] if Path("/usr/bin/g++").exists() else []
+        cmd = [_nvcc(), *ccbin, *NVCC_FLAGS, "-o", str(LIB), *map(str, SOURCES)]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True, cwd=ROOT)

@@ -486,8 +486,12 @@ int advance_fused_t(hyg_ctx* c, Real* (&buf)[2][4], int64_t nsteps, double dt, h
         a.suspect = c->d_flag;
         a.fail_key = c->d_key;
         const int cur0 = c->cur;
+        // the bit-30 test proves |x| <= norm only for norm >= 2 (fp32 deviations: 3);
+        // below that every segment runs the exact guard
+        const bool fast_ok = c->norm >= (sizeof(Real) == 4 ? 3.0 : 2.0);
         int nseg = 0;
         for (int64_t s0 = 0; s0 < rows; s0 += c->seg_len, ++nseg) {
+            if (!fast_ok) continue;
             const int len = static_cast<int>(std::min<int64_t>(c->seg_len, rows - s0));
             a.nsteps = len;
             a.layer0 = c->layer + s0;
@@ -506,6 +510,7 @@ int advance_fused_t(hyg_ctx* c, Real* (&buf)[2][4], int64_t nsteps, double dt, h
         int flag = 0;
         HYG_CUDA(cudaMemcpyAsync(&flag, c->d_flag, sizeof flag, cudaMemcpyDeviceToHost, c->stream));
         HYG_CUDA(cudaStreamSynchronize(c->stream));
+        if (!fast_ok) flag = 1;           // exact guard from the first segment
         if (flag == 0) {
             c->cur = (cur0 + nseg) & 1;
             c->t = t;
@@ -962,9 +967,9 @@ int hyg_bootstrap(hyg_ctx* c, int32_t kind, hyg_status* status) {
         set_status(status, HYG_EINVAL, "unknown bootstrap kind");
         return HYG_EINVAL;
     }
-    if (kind == HYG_BOOT_IMPLICIT && (c->coeff_kind != HYG_COEFF_CONSTANT || !c->zones.empty())) {
+    if (kind == HYG_BOOT_IMPLICIT && c->coeff_kind != HYG_COEFF_CONSTANT) {
         set_status(status, HYG_ENOTSUP,
-                   "implicit starting step on the device: constant-coefficient walls without zones only");
+                   "implicit starting step on the device: constant-coefficient walls only");
         return HYG_ENOTSUP;
     }
     int rc = from_f32(c, status);
@@ -981,33 +986,150 @@ int hyg_bootstrap(hyg_ctx* c, int32_t kind, hyg_status* status) {
         HYG_CUDA(cudaMemcpyAsync(c->d_boot, c->h_boot.data(), sizeof(Ambient) * nch, cudaMemcpyHostToDevice,
                                  c->stream));
     }
+    const int nsrc = static_cast<int>(c->zsrc.size() / 3);
+    if (!c->zones.empty()) {
+        std::vector<double> tf{t_force};
+        rc = upload_src(c, tf, status);
+        if (rc) return rc;
+    }
     HYG_CUDA(cudaMemsetAsync(c->d_key, 0xff, sizeof(unsigned long long), c->stream));
     StepArgs a = step_args(c, c->cur, c->dt);
     a.amb = c->d_boot;
+    int passes = 0;
     if (kind == HYG_BOOT_EXPLICIT) {
-        LaunchScope ls(c, "explicit_boot", static_cast<double>(c->cells()));
-        k_explicit_boot<<<static_cast<int>((c->cells() + 255) / 256), 256, 0, c->stream>>>(a);
-    } else {
-        double* scr = nullptr;
-        HYG_CUDA(cudaMallocAsync(&scr, sizeof(double) * 3 * static_cast<size_t>(c->cells()), c->stream));
+        // euler_explicit_step per wall (wall.cpp:266-317); with zones this is the
+        // reference's EulerExplicit building step (building.cpp:174-183)
         {
-            LaunchScope ls(c, "implicit_unit_boot", static_cast<double>(c->cells()));
-            k_implicit_unit_boot<<<(c->n_walls + 127) / 128, 128, 0, c->stream>>>(a, scr);
+            LaunchScope ls(c, "explicit_boot", static_cast<double>(c->cells()));
+            k_explicit_boot<<<static_cast<int>((c->cells() + 255) / 256), 256, 0, c->stream>>>(a);
+        }
+        if (!c->zones.empty()) {
+            ZoneArgs z{};
+            z.n_zones = static_cast<int>(c->zones.size());
+            z.n = c->n;
+            z.dt = c->dt;
+            z.zones = c->d_zones;
+            z.links = c->d_zlinks;
+            z.inz = c->d_inz;
+            z.src = c->d_src;
+            z.n_sources = nsrc;
+            z.uc = c->s64[c->cur][1];
+            z.vc = c->s64[c->cur][3];
+            z.zu_in = c->zu[c->zcur];
+            z.zv_in = c->zv[c->zcur];
+            z.zu_out = c->zu[1 - c->zcur];
+            z.zv_out = c->zv[1 - c->zcur];
+            z.layer = c->layer;
+            z.norm = c->norm;
+            z.fail_key = c->d_key;
+            LaunchScope ls(c, "zone_step", 0.0);
+            k_zone_step<<<(z.n_zones + 127) / 128, 128, 0, c->stream>>>(z);
+            c->zcur ^= 1;
+        }
+    } else {
+        // step_implicit (building.cpp:189-268): walls and zones iterated jointly
+        // until the max-norm change of every wall node and zone scalar < eta
+        const double eta = c->eta_factor * c->dt;
+        const size_t cells = static_cast<size_t>(c->cells());
+        const int nz = std::max<int>(1, static_cast<int>(c->zones.size()));
+        double* scr = nullptr;
+        double* zit = nullptr;         // zone iterates: [4][nz] = (u,v) x (snapshot, new)
+        unsigned long long* d_diff = nullptr;
+        HYG_CUDA(cudaMallocAsync(&scr, sizeof(double) * 4 * cells, c->stream));
+        HYG_CUDA(cudaMallocAsync(&zit, sizeof(double) * 4 * nz, c->stream));
+        HYG_CUDA(cudaMallocAsync(&d_diff, sizeof(unsigned long long), c->stream));
+        // iterates start from layer n (building.cpp:200-206)
+        HYG_CUDA(cudaMemcpyAsync(a.out[1], a.in[1], cells * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+        HYG_CUDA(cudaMemcpyAsync(a.out[3], a.in[3], cells * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+        HYG_CUDA(cudaMemcpyAsync(zit, c->zu[c->zcur], nz * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+        HYG_CUDA(cudaMemcpyAsync(zit + nz, c->zv[c->zcur], nz * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+        int snap = 0;                  // zit[snap*2*nz ...] is the snapshot
+        double diff = 0.0;
+        int rcl = HYG_OK;
+        for (;;) {
+            ++passes;
+            HYG_CUDA(cudaMemsetAsync(d_diff, 0, sizeof(unsigned long long), c->stream));
+            HYG_CUDA(cudaMemsetAsync(c->d_key, 0xff, sizeof(unsigned long long), c->stream));
+            double* zs_u = zit + snap * 2 * nz;
+            double* zs_v = zs_u + nz;
+            double* zn_u = zit + (1 - snap) * 2 * nz;
+            double* zn_v = zn_u + nz;
+            a.zu = zs_u;
+            a.zv = zs_v;
+            {
+                LaunchScope ls(c, "implicit_unit_pass", static_cast<double>(c->cells()));
+                k_implicit_unit_pass<<<(c->n_walls + 127) / 128, 128, 0, c->stream>>>(a, scr, d_diff);
+            }
+            if (!c->zones.empty()) {
+                ZoneImplicitArgs z{};
+                z.n_zones = static_cast<int>(c->zones.size());
+                z.n = c->n;
+                z.dt = c->dt;
+                z.zones = c->d_zones;
+                z.links = c->d_zlinks;
+                z.inz = c->d_inz;
+                z.src = c->d_src;
+                z.n_sources = nsrc;
+                z.wu = a.out[1];
+                z.wv = a.out[3];
+                z.zu_n = c->zu[c->zcur];
+                z.zv_n = c->zv[c->zcur];
+                z.zu_s = zs_u;
+                z.zv_s = zs_v;
+                z.zu_out = zn_u;
+                z.zv_out = zn_v;
+                z.layer = c->layer;
+                z.norm = c->norm;
+                z.diff = d_diff;
+                z.fail_key = c->d_key;
+                LaunchScope ls(c, "zone_implicit", 0.0);
+                k_zone_implicit<<<(z.n_zones + 127) / 128, 128, 0, c->stream>>>(z);
+                snap ^= 1;
+            }
+            HYG_CUDA(cudaGetLastError());
+            unsigned long long bits = 0;
+            HYG_CUDA(cudaMemcpyAsync(&bits, d_diff, sizeof bits, cudaMemcpyDeviceToHost, c->stream));
+            HYG_CUDA(cudaStreamSynchronize(c->stream));
+            std::memcpy(&diff, &bits, sizeof diff);
+            if (diff < eta) break;
+            if (passes >= c->max_subiters) {
+                rcl = HYG_ECONVERGE;
+                break;
+            }
+        }
+        if (rcl == HYG_OK && !c->zones.empty()) {
+            // zone states := the converged iterate (last written = current snapshot)
+            HYG_CUDA(cudaMemcpyAsync(c->zu[1 - c->zcur], zit + snap * 2 * nz, nz * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, c->stream));
+            HYG_CUDA(cudaMemcpyAsync(c->zv[1 - c->zcur], zit + snap * 2 * nz + nz, nz * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, c->stream));
+            c->zcur ^= 1;
         }
         HYG_CUDA(cudaFreeAsync(scr, c->stream));
+        HYG_CUDA(cudaFreeAsync(zit, c->stream));
+        HYG_CUDA(cudaFreeAsync(d_diff, c->stream));
+        if (rcl != HYG_OK) {
+            HYG_CUDA(cudaStreamSynchronize(c->stream));
+            if (status) {
+                status->code = HYG_ECONVERGE;
+                status->residual = diff;
+                status->subiterations = passes;
+                std::snprintf(status->message, sizeof status->message,
+                              "building fixed point did not converge in %d sub-iterations at t* = %.17g "
+                              "(residual %.17g)", c->max_subiters, c->t + c->dt, diff);
+            }
+            to_f32(c, nullptr);
+            return HYG_ECONVERGE;
+        }
     }
     HYG_CUDA(cudaGetLastError());
     c->cur ^= 1;
-    if (!c->zones.empty()) {
-        // zone states carry over unchanged for the explicit start (zones are
-        // advanced by the building steps only)
-    }
     unsigned long long key;
     rc = read_key(c, &key, status);
     if (rc) return rc;
     c->t = c->t + c->dt;
     c->layer += 1;
-    if (status) status->subiterations = kind == HYG_BOOT_IMPLICIT ? 2 : 0;
+    if (status) status->subiterations = passes;
     rc = to_f32(c, status);
     if (rc) return rc;
     if (key != ~0ull) return diverged(c, key, status);

@@ -283,13 +283,20 @@ __global__ void k_explicit_boot(const StepArgs a) {
 }
 
 // implicit_wall_pass_unit (wall.cpp:398-429) with the factorisation of
-// cached_factors (wall.cpp:360-395) and FactoredTridiag (wall.cpp:322-346).
-// One thread per wall; scratch is node-major [n][n_walls] (coalesced).
-// Used for the constant-coefficient starting step (bootstrap_first_layer,
-// and step_implicit without zones, which converges after the second pass
-// with an identical iterate).  Writes layer 1 into out[1]/out[3] and copies
-// layer 0 into out[0]/out[2].
-__global__ void k_implicit_unit_boot(const StepArgs a, double* scr) {
+// cached_factors (wall.cpp:360-395) and FactoredTridiag (wall.cpp:322-346):
+// one pass of the whole-building fixed point step_implicit
+// (building.cpp:189-268) for constant-coefficient walls.  Faces read the zone
+// iterate snapshot (a.zu/a.zv) and forcing at t^{n+1}.  One thread per wall;
+// scratch is node-major [n][n_walls] (coalesced).  out[1]/out[3] hold the
+// wall iterate (initialised to layer n by the host before pass 1); the pass
+// overwrites it and accumulates max |new - old| into *diff (non-negative
+// doubles order like their bit patterns).  out[0]/out[2] receive layer n.
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long* p, double x) {
+    if (!(x >= 0.0)) x = __longlong_as_double(0x7ff0000000000000ll);   // NaN -> +inf
+    atomicMax(p, static_cast<unsigned long long>(__double_as_longlong(x)));
+}
+
+__global__ void k_implicit_unit_pass(const StepArgs a, double* scr, unsigned long long* diff) {
     const int w = blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= a.n_walls) return;
     const int n = a.n, B = a.n_walls;
@@ -297,15 +304,15 @@ __global__ void k_implicit_unit_boot(const StepArgs a, double* scr) {
     const Groups p = a.groups[w];
     const size_t o = static_cast<size_t>(w) * n;
     const double *uc = a.in[1] + o, *vc = a.in[3] + o;
-    double* M = scr;                         // m[i]
+    double* M = scr;
     double* INV = scr + static_cast<size_t>(n) * B;
-    double* X = scr + 2 * static_cast<size_t>(n) * B;   // solution vector
+    double* XV = scr + 2 * static_cast<size_t>(n) * B;
+    double* XU = scr + 3 * static_cast<size_t>(n) * B;
     auto at = [&](double* base, int i) -> double& { return base[static_cast<size_t>(i) * B + w]; };
     const FaceVals L = resolve(a, w, 0), R = resolve(a, w, 1);
     const double r = p.Fo_M * dt / (dx * dx);
     const double rb = p.Fo_TT * dt / (dx * dx);
     const double rg = p.Fo_TM * p.gamma * dt / (dx * dx);
-    // tridiagonal coefficient of row i for the unit matrices (wall.cpp:369-393)
     auto lo_ = [&](int i, double rr) { return i == 0 ? 0.0 : (i == n - 1 ? -2.0 * rr : -rr); };
     auto up_ = [&](int i, double rr) { return i == 0 ? -2.0 * rr : (i == n - 1 ? 0.0 : -rr); };
     auto di_ = [&](int i, double rr, double b0, double b1) {
@@ -323,42 +330,119 @@ __global__ void k_implicit_unit_boot(const StepArgs a, double* scr) {
             at(INV, i) = 1.0 / dp;
         }
     };
-    auto solve = [&](double rr) {
+    auto solve = [&](double* X, double rr) {
         for (int i = 1; i < n; ++i) at(X, i) -= at(M, i) * at(X, i - 1);
         at(X, n - 1) *= at(INV, n - 1);
         for (int i = n - 1; i-- > 0;) at(X, i) = (at(X, i) - up_(i, rr) * at(X, i + 1)) * at(INV, i);
     };
-    // moisture
+    // moisture (wall.cpp:409-413)
     factor(r, L.Bi_M, R.Bi_M);
-    for (int i = 0; i < n; ++i) at(X, i) = vc[i];
-    at(X, 0) += 2.0 * r * dx * (L.Bi_M * L.v_inf + L.g_inf);
-    at(X, n - 1) += 2.0 * r * dx * (R.Bi_M * R.v_inf + R.g_inf);
-    solve(r);
-    double* vout = a.out[3] + o;
-    for (int i = 0; i < n; ++i) vout[i] = at(X, i);
-    const double* vN = vout;
-    // energy right-hand side with the new moisture layer
+    for (int i = 0; i < n; ++i) at(XV, i) = vc[i];
+    at(XV, 0) += 2.0 * r * dx * (L.Bi_M * L.v_inf + L.g_inf);
+    at(XV, n - 1) += 2.0 * r * dx * (R.Bi_M * R.v_inf + R.g_inf);
+    solve(XV, r);
+    // energy right-hand side with the new moisture layer (wall.cpp:415-427)
     for (int j = 1; j + 1 < n; ++j)
-        at(X, j) = uc[j] - p.gamma * (vN[j] - vc[j]) + rg * (vN[j + 1] - 2.0 * vN[j] + vN[j - 1]);
-    at(X, 0) = uc[0] - p.gamma * (vN[0] - vc[0]) + 2.0 * rg * (vN[1] - vN[0]) +
-               2.0 * rb * dx * (L.Bi_TT * L.u_inf - L.Bi_TM * (vN[0] - L.v_inf) + L.q_inf);
-    at(X, n - 1) = uc[n - 1] - p.gamma * (vN[n - 1] - vc[n - 1]) + 2.0 * rg * (vN[n - 2] - vN[n - 1]) +
-                   2.0 * rb * dx * (R.Bi_TT * R.u_inf - R.Bi_TM * (vN[n - 1] - R.v_inf) + R.q_inf);
+        at(XU, j) = uc[j] - p.gamma * (at(XV, j) - vc[j]) +
+                    rg * (at(XV, j + 1) - 2.0 * at(XV, j) + at(XV, j - 1));
+    at(XU, 0) = uc[0] - p.gamma * (at(XV, 0) - vc[0]) + 2.0 * rg * (at(XV, 1) - at(XV, 0)) +
+                2.0 * rb * dx * (L.Bi_TT * L.u_inf - L.Bi_TM * (at(XV, 0) - L.v_inf) + L.q_inf);
+    at(XU, n - 1) = uc[n - 1] - p.gamma * (at(XV, n - 1) - vc[n - 1]) +
+                    2.0 * rg * (at(XV, n - 2) - at(XV, n - 1)) +
+                    2.0 * rb * dx * (R.Bi_TT * R.u_inf - R.Bi_TM * (at(XV, n - 1) - R.v_inf) + R.q_inf);
     factor(rb, L.Bi_TT, R.Bi_TT);
-    solve(rb);
+    solve(XU, rb);
     double* uout = a.out[1] + o;
-    double mx = 0.0;
+    double* vout = a.out[3] + o;
+    double d = 0.0, mx = 0.0;
     bool finite = true;
     for (int i = 0; i < n; ++i) {
-        uout[i] = at(X, i);
+        const double nu = at(XU, i), nv = at(XV, i);
+        d = fmax(d, fabs(nu - uout[i]));     // building.cpp:231-234
+        d = fmax(d, fabs(nv - vout[i]));
+        uout[i] = nu;
+        vout[i] = nv;
         a.out[0][o + i] = uc[i];
         a.out[2][o + i] = vc[i];
-        mx = fmax(mx, fmax(fabs(uout[i]), fabs(vout[i])));
-        finite = finite && isfinite(uout[i]) && isfinite(vout[i]);
+        mx = fmax(mx, fmax(fabs(nu), fabs(nv)));
+        finite = finite && isfinite(nu) && isfinite(nv);
     }
+    atomic_max_nonneg(diff, finite ? d : NAN);
     if (!(mx <= a.norm) || !finite) {
         const unsigned long long key =
             (static_cast<unsigned long long>(a.layer + 1) << 32) | static_cast<unsigned>(w);
+        atomicMin(a.fail_key, key);
+    }
+}
+
+// zone_step_implicit (zone.cpp:76-115) inside the building fixed point:
+// samples from the current wall iterate, peers from the zone snapshot.
+struct ZoneImplicitArgs {
+    int n_zones, n;
+    double dt;
+    const ZoneDev* zones;
+    const ZoneLinkDev* links;
+    const InzLinkDev* inz;
+    const double* src;          // row at t^{n+1}: [n_sources][3] then outdoor u, v
+    int n_sources;
+    const double* wu;           // wall iterate [n_walls][n]
+    const double* wv;
+    const double* zu_n;         // zone state at layer n
+    const double* zv_n;
+    const double* zu_s;         // zone iterate snapshot (peers)
+    const double* zv_s;
+    double* zu_out;
+    double* zv_out;
+    int64_t layer;
+    double norm;
+    unsigned long long* diff;
+    unsigned long long* fail_key;
+};
+
+__global__ void k_zone_implicit(const ZoneImplicitArgs a) {
+    const int z = blockIdx.x * blockDim.x + threadIdx.x;
+    if (z >= a.n_zones) return;
+    const ZoneDev d = a.zones[z];
+    const double* s = a.src + 3 * d.sources;
+    const double u_inf = a.src[3 * a.n_sources + 0], v_inf = a.src[3 * a.n_sources + 1];
+    double sum_gz = 0.0, sum_gz_v = 0.0;
+    for (int i = d.inz_begin; i < d.inz_end; ++i) {
+        sum_gz += a.inz[i].g_inz;
+        sum_gz_v += a.inz[i].g_inz * a.zv_s[a.inz[i].peer];
+    }
+    double S_M = 0.0, W_M = 0.0;
+    for (int i = d.wall_begin; i < d.wall_end; ++i) {
+        const ZoneLinkDev l = a.links[i];
+        const size_t idx = static_cast<size_t>(l.wall) * a.n + (l.face == 0 ? 0 : a.n - 1);
+        S_M += l.Bi_M * l.theta_M;
+        W_M += l.Bi_M * l.theta_M * a.wv[idx];
+    }
+    const double dt = a.dt;
+    const double v_den = 1.0 + dt * (d.g_v + sum_gz - d.sign * S_M);
+    const double v_num = a.zv_n[z] + dt * (s[0] + d.g_v * v_inf + sum_gz_v - d.sign * W_M);
+    const double v1 = v_num / v_den;
+    double u_coef = (1.0 + d.kappa_a_tt1) + dt * (d.q_v1 * v1 + d.q_v2);
+    double u_rhs = (1.0 + d.kappa_a_tt1) * a.zu_n[z] +
+                   dt * (s[1] + s[2] + d.q_v1 * u_inf * v_inf + d.q_v2 * u_inf);
+    for (int i = d.inz_begin; i < d.inz_end; ++i) {
+        const InzLinkDev l = a.inz[i];
+        const double pu = a.zu_s[l.peer], pv = a.zv_s[l.peer];
+        u_coef += dt * (l.q_inz1 * v1 + l.q_inz2);
+        u_rhs += dt * (l.q_inz1 * pu * pv + l.q_inz2 * pu);
+    }
+    for (int i = d.wall_begin; i < d.wall_end; ++i) {
+        const ZoneLinkDev l = a.links[i];
+        const size_t idx = static_cast<size_t>(l.wall) * a.n + (l.face == 0 ? 0 : a.n - 1);
+        u_coef += dt * l.Bi_TT * l.theta_T;
+        u_rhs += dt * (l.Bi_TT * l.theta_T * a.wu[idx] + l.Bi_TM * l.theta_T * (a.wv[idx] - v1));
+    }
+    const double u1 = u_rhs / u_coef;
+    const double dd = fmax(fabs(u1 - a.zu_s[z]), fabs(v1 - a.zv_s[z]));   // building.cpp:240-243
+    atomic_max_nonneg(a.diff, dd);
+    a.zu_out[z] = u1;
+    a.zv_out[z] = v1;
+    if (!isfinite(u1) || !isfinite(v1) || fabs(u1) > a.norm || fabs(v1) > a.norm) {
+        const unsigned long long key = (static_cast<unsigned long long>(a.layer + 1) << 32) | 0xffffffffu;
         atomicMin(a.fail_key, key);
     }
 }

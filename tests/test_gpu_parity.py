@@ -1,0 +1,212 @@
+"""CUDA path (through the C ABI) vs the C oracle, at the BASELINE configs.
+
+Tolerances (north_star): relative L-inf <= 1e-10 in fp64 after the full run,
+<= 1e-4 for the fp32 variant.  Relative L-inf = max|gpu - ref| / max|ref| over
+both time layers of both fields.  Full-size configs are
+checked on seeded strided subsets at the full horizon plus all walls on a
+short horizon (SURVEY.md §8d parity procedure).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1703_10119_b200 import Context, NumericalError, workloads
+from paper_1703_10119_b200.api import ChannelSpec, Model, Signal
+
+from .helpers import FIELDS, gpu_run, oracle_run, random_walls, rel_linf
+
+pytestmark = pytest.mark.gpu
+
+TOL64, TOL32 = 1e-10, 1e-4
+
+
+def _subset(w, idx):
+    """Workload restricted to walls idx (same parameters, same initial rows)."""
+    m = w.model
+    n = m.n_nodes
+    sub = Model(n, m.dx, m.groups[idx], m.biot[idx], m.attach[idx], channels=m.channels, dt=m.dt,
+                precision=m.precision, divergence_norm=m.divergence_norm)
+    rows = (np.asarray(idx)[:, None] * n + np.arange(n)[None, :]).reshape(-1)
+    init = {k: v[rows] for k, v in w.init.items() if k in FIELDS}
+    return sub, init, rows
+
+
+def _extreme_walls(m, k=256):
+    """Strided subset plus the walls at the extremes of lambda, mu, Bi."""
+    W = m.n_walls
+    idx = set(range(0, W, max(1, W // (k - 24))))
+    for col in (m.groups[:, 0], m.groups[:, 1], m.groups[:, 2] * m.groups[:, 3], m.biot[:, 0, 0],
+                m.biot[:, 1, 0], m.biot[:, 0, 1], m.biot[:, 0, 2]):
+        order = np.argsort(col)
+        idx.update(order[:2].tolist() + order[-2:].tolist())
+    return np.array(sorted(idx))
+
+
+@pytest.fixture(scope="module")
+def cfg1():
+    return workloads.batched_walls()     # 65,536 walls x 256, 1e5 steps
+
+
+def test_cfg1_full_horizon_subset(cfg1):
+    """All 65,536 walls on the GPU for the full 1e5 steps (implicit start);
+    the oracle runs a strided + extreme-parameter subset of them."""
+    w = cfg1
+    got = gpu_run(w.model, w.init, w.nsteps, w.boot, w.tables)
+    assert got["launches"] > 0 and got["layer"] == w.nsteps
+    assert abs(got["t"] - workloads.accumulate_times(np.full(w.nsteps, w.model.dt))[-1]) == 0.0
+    idx = _extreme_walls(w.model)
+    sub, init, rows = _subset(w, idx)
+    ref = oracle_run("oracle", sub, init, w.nsteps, w.boot, w.tables)
+    err = rel_linf({k: got[k][rows] for k in FIELDS}, ref)
+    assert err <= TOL64, err
+
+
+def test_cfg1_all_walls_short_horizon(cfg1):
+    w = cfg1
+    n = 300
+    got = gpu_run(w.model, w.init, n, w.boot, w.tables)
+    ref = oracle_run("oracle", w.model, w.init, n, w.boot, w.tables)
+    err = rel_linf(got, ref)
+    assert err <= TOL64, err
+
+
+def test_cfg2_fp32_variable_dt():
+    """fp32 state (deviations from 1, fp64 boundary flux terms) with dt doubling
+    every 1e4 steps up to 16 dt0, against the fp64 oracle on the same schedule."""
+    w = workloads.batched_walls(n_walls=4096, precision="f32", variable_dt=True)
+    got = gpu_run(w.model, w.init, w.nsteps, w.boot, w.tables, dt_schedule=w.dt_schedule)
+    idx = _extreme_walls(w.model, 128)
+    sub, init, rows = _subset(w, idx)
+    sub.precision = "f64"
+    ref = oracle_run("oracle", sub, init, w.nsteps, w.boot, w.tables, dt_schedule=w.dt_schedule)
+    err = rel_linf({k: got[k][rows] for k in FIELDS}, ref)
+    assert err <= TOL32, err
+    assert abs(got["t"] - 1110.0) < 1e-9
+
+
+def test_cfg0_single_wall_full_run():
+    """configs[0]: N=101, d(v), 1 explicit start + 99,999 DF steps."""
+    w = workloads.single_wall_d()
+    got = gpu_run(w.model, w.init, w.nsteps, w.boot)
+    ref = oracle_run("oracle", w.model, w.init, w.nsteps, w.boot)
+    err = rel_linf(got, ref)
+    assert err <= TOL64, err
+    assert float(np.max(np.abs(got["u_curr"] - 1.0))) < 1e-12     # gamma = 0: u stays 1
+    assert 0.4 < float(got["v_curr"].min()) and float(got["v_curr"].max()) < 1.9
+
+
+def test_cfg4_long_domain_reduced():
+    """configs[4] at N=2^16 for 2000 steps (full size: tests/test_gpu_long.py)."""
+    w = workloads.long_domain(n_nodes=1 << 16, nsteps=2000)
+    got = gpu_run(w.model, w.init, w.nsteps, w.boot)
+    ref = oracle_run("oracle", w.model, w.init, w.nsteps, w.boot, nthreads=1)
+    err = rel_linf(got, ref)
+    assert err <= TOL64, err
+
+
+@pytest.mark.parametrize("n_zones,wpz,n,steps", [(1, 4, 101, 3000), (16, 6, 128, 2000)])
+def test_cfg3_building_ring(n_zones, wpz, n, steps):
+    """Zones: implicit building start (joint wall/zone fixed point) then
+    step_explicit with zone faces and the inter-zone ring."""
+    w = workloads.zone_ring(n_zones=n_zones, walls_per_zone=wpz, n_nodes=n, nsteps=steps)
+    with Context(w.model) as ctx:
+        ctx.set_state(**w.init)
+        st = ctx.bootstrap("implicit")
+        ctx.advance(steps - 1)
+        got = ctx.get_state()
+    b = O.Building(w.model, w.init)
+    rc, _, passes = b.run("oracle", steps)
+    assert rc == 0 and st.subiterations == passes
+    ref = dict(b.state)
+    err = rel_linf(got, ref)
+    zerr = max(float(np.max(np.abs(got["zone_u"] - b.zu))), float(np.max(np.abs(got["zone_v"] - b.zv))))
+    assert err <= TOL64 and zerr <= TOL64, (err, zerr)
+
+
+@pytest.mark.parametrize("n_nodes", [64, 128, 256, 512, 37])
+def test_fused_and_general_grids_with_flux(n_nodes):
+    """Every fused grid (and a non-fused one through the general kernel), with
+    imposed face fluxes g_inf/q_inf and several channels."""
+    model, init = random_walls(300, n_nodes, seed=n_nodes, flux=True, channels=3)
+    for boot in ("implicit", "explicit"):
+        got = gpu_run(model, init, 1500, boot)
+        ref = oracle_run("oracle", model, init, 1500, boot)
+        assert rel_linf(got, ref) <= TOL64, (boot, rel_linf(got, ref))
+
+
+def test_guard_first_failing_layer_and_wall():
+    """check_bounded semantics (building.cpp:282-300): divergence_norm below the
+    ambient excursion -> same first failing layer and lowest wall as the oracle."""
+    model, init = random_walls(64, 256, seed=2)
+    model.divergence_norm = 1.012
+    times = workloads.accumulate_times(np.full(3000, model.dt))
+    tab = O.forcing_table(model, times, 0)
+    wb = O.WallBatch(model, init, tab)
+    O.bootstrap("oracle", wb, "implicit", model.dt)
+    wb.set_layer0(1, tab[1:])
+    rc, fl, fw = O.march("oracle", wb, 2999, model.dt, O.threads())
+    assert rc == 3 and fl > 1
+    with Context(model) as ctx:
+        ctx.set_state(**init)
+        ctx.bootstrap("implicit")
+        with pytest.raises(NumericalError) as e:
+            ctx.advance(2999)
+    assert (e.value.layer, e.value.wall) == (fl, fw)
+    assert e.value.t_star == pytest.approx(times[fl], abs=0)
+
+
+def test_guard_nan_and_fast_guard_false_positive():
+    model, init = random_walls(40, 128, seed=9)
+    bad = {k: v.copy() for k, v in init.items()}
+    bad["v_curr"][17 * 128 + 40] = math.nan          # wall 17
+    with Context(model) as ctx:
+        ctx.set_state(**bad)
+        with pytest.raises(NumericalError) as e:
+            ctx.bootstrap("implicit")
+        assert (e.value.layer, e.value.wall) == (1, 17)
+    # |v| >= 2 somewhere but bounded: the fast guard fires, the exact replay
+    # finds no failure, and the result is unchanged
+    big = {k: v.copy() for k, v in init.items()}
+    for k in FIELDS:
+        big[k][5 * 128: 6 * 128] += 2.5
+    got = gpu_run(model, big, 2000, "implicit")
+    ref = oracle_run("oracle", model, big, 2000, "implicit")
+    assert rel_linf(got, ref) <= TOL64
+
+
+def test_run_frames_snapshot_and_state_roundtrip():
+    """hyg_run (run(), building.cpp:303-356): frames at cadence incl. the
+    initial and final states; snapshot/restore; exact state round trip."""
+    model, init = random_walls(48, 128, seed=4)
+    frames = []
+    with Context(model) as ctx:
+        ctx.set_state(**init)
+        back = ctx.get_state()
+        for k in FIELDS:
+            assert np.array_equal(back[k], init[k])
+        ctx.snapshot()
+
+        def frame(layer, t, c):
+            frames.append((layer, t, c.get_state()["v_curr"].copy()))
+        ctx.run(horizon=1.0, cadence=0.25, boot="implicit", frame=frame)
+        final = ctx.get_state()
+        ctx.restore()
+        again = ctx.get_state()
+        for k in FIELDS:
+            assert np.array_equal(again[k], init[k])
+    assert [f[0] for f in frames] == [0, 250, 500, 750, 1000]
+    ref = oracle_run("oracle", model, init, 1000, "implicit")
+    assert rel_linf(final, ref) <= TOL64
+    mid = oracle_run("oracle", model, init, 500, "implicit")
+    assert float(np.max(np.abs(frames[2][2] - mid["v_curr"]))) <= TOL64
+
+
+def test_advance_with_per_call_dt_fp64():
+    """dt is a per-call argument (wall.hpp:81-82): fp64 walls on cfg2's schedule."""
+    model, init = random_walls(128, 256, seed=6)
+    sched = [(500, 1e-3), (500, 2e-3), (500, 4e-3)]
+    got = gpu_run(model, init, 1500, "implicit", dt_schedule=sched)
+    ref = oracle_run("oracle", model, init, 1500, "implicit", dt_schedule=sched)
+    assert rel_linf(got, ref) <= TOL64
