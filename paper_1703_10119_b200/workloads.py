@@ -133,8 +133,12 @@ def long_domain(n_nodes=1 << 26, nsteps=10_000, dt=1e-3, seed=4, modes=16) -> Wo
 
     Initial u, v = 1 + sum_k a_k sin(2 pi m_k x / X + phi_k), X = (N-1) dx,
     a_k ~ U[-0.3/16, 0.3/16], m_k ~ U{1..2^16}, phi_k ~ U[0, 2 pi); both layers equal.
-    Groups of test_wall.cpp:144-148 (Fo_M=0.1 as cfg0); Bi_M 2/1 with cfg0's v_inf;
-    Bi_TT/Bi_TM 1.7/0.678 (x*=0), 2.72/0.101 (x*=1); explicit start.
+    North-wall groups of test_wall.cpp:144-148; Bi_M 2/1 with cfg0's v_inf;
+    Bi_TT/Bi_TM 1.7/0.678 (x*=0), 2.72/0.101 (x*=1).  The DF march starts
+    directly from the two equal initial layers (as test_wall.cpp:251-272 does):
+    an Euler-explicit start at Fo_M dt/dx^2 d(v) ~ 50 kicks the face nodes
+    into an odd-even mode that the frozen-coefficient DF then amplifies past
+    divergence_norm within ~80 steps ("cfg4 start").
     """
     rng = np.random.default_rng(seed)
     dx = 1e-2
@@ -142,21 +146,22 @@ def long_domain(n_nodes=1 << 26, nsteps=10_000, dt=1e-3, seed=4, modes=16) -> Wo
     x = np.arange(n_nodes) * dx
     def field_():
         a = rng.uniform(-0.3 / modes, 0.3 / modes, modes)
-        m = rng.integers(1, 1 << 16, modes, endpoint=True)
+        # shortest wavelength >= 1024 nodes at every N (2^16 modes at N = 2^26)
+        m = rng.integers(1, max(1, (n_nodes - 1) // 1024), modes, endpoint=True)
         ph = rng.uniform(0.0, 2.0 * math.pi, modes)
         f = np.ones(n_nodes)
         for k in range(modes):
             f += a[k] * np.sin(2.0 * math.pi * m[k] * x / X + ph[k])
         return f
     u0, v0 = field_(), field_()
-    groups = np.array([[0.1, 0.137, 3.76, 7.87e-3]])
+    groups = np.array([[0.116, 0.137, 3.76, 7.87e-3]])
     biot = np.array([[[2.0, 1.7, 0.678], [1.0, 2.72, 0.101]]])
     attach = np.array([[[0, 0], [0, 1]]], dtype=np.int32)
     ch = [ChannelSpec(v_inf=Signal.sinusoid(1.0, 0.8, 24.0)), ChannelSpec()]
     model = Model(n_nodes, dx, groups, biot, attach, channels=ch, dt=dt, coeff_kind="analytic_d",
                   coeff_params=D_PARAMS)
     init = dict(u_prev=u0.copy(), u_curr=u0, v_prev=v0.copy(), v_curr=v0)
-    return Workload("cfg4_long_domain", model, init, nsteps, "explicit", notes=f"N={n_nodes}, seed {seed}")
+    return Workload("cfg4_long_domain", model, init, nsteps, "none", notes=f"N={n_nodes}, seed {seed}")
 
 
 # frozen coefficient sets of one_zone_linear.json:5-7 / test_building.cpp:13-15

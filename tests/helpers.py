@@ -55,10 +55,12 @@ def oracle_run(impl, model, init, nsteps, boot, tables=None, dt=None, nthreads=N
     times = workloads.accumulate_times(dts)
     tab = O.forcing_table(model, times, 0, tables or {})
     wb = O.WallBatch(model, init, tab)
-    rc = O.bootstrap(impl, wb, boot, dts[0], eta=model.eta_factor * dts[0], max_subiters=model.max_subiters,
-                     nthreads=nthreads)
-    assert rc == 0, rc
-    L = 1
+    L = 0
+    if boot != "none":       # "none": DF straight from the two given layers
+        rc = O.bootstrap(impl, wb, boot, dts[0], eta=model.eta_factor * dts[0], max_subiters=model.max_subiters,
+                         nthreads=nthreads)
+        assert rc == 0, rc
+        L = 1
     # constant-dt runs of the schedule
     while L < nsteps:
         d = dts[L]
@@ -91,6 +93,8 @@ def gpu_run(model, init, nsteps, boot, tables=None, dt_schedule=None):
                 if n > 0:
                     ctx.advance(n, d)
                 left -= n
+        elif boot == "none":
+            ctx.advance(nsteps)
         else:
             ctx.bootstrap(boot)
             ctx.advance(nsteps - 1)

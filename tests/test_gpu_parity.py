@@ -98,12 +98,33 @@ def test_cfg0_single_wall_full_run():
 
 
 def test_cfg4_long_domain_reduced():
-    """configs[4] at N=2^16 for 2000 steps (full size: tests/test_gpu_long.py)."""
+    """configs[4] at N=2^16 for 2000 steps (the full N=2^26 is checked on a
+    short horizon in test_cfg4_full_size_short_horizon)."""
     w = workloads.long_domain(n_nodes=1 << 16, nsteps=2000)
     got = gpu_run(w.model, w.init, w.nsteps, w.boot)
     ref = oracle_run("oracle", w.model, w.init, w.nsteps, w.boot, nthreads=1)
     err = rel_linf(got, ref)
     assert err <= TOL64, err
+
+
+def test_cfg4_full_size_short_horizon():
+    """configs[4] at the full N = 2^26.  After k DF steps node j depends only on
+    nodes j-k..j+k (three-level stencil), so windows of 2^14 nodes at both
+    faces and in the middle, padded by k+2 nodes of real initial data, are
+    checked exactly by the oracle treating the far pad end as a face."""
+    N, k, W = 1 << 26, 100, 1 << 14
+    w = workloads.long_domain(n_nodes=N, nsteps=k)
+    got = gpu_run(w.model, w.init, k, w.boot)
+    pad = k + 2
+    m = w.model
+    for lo, hi, keep in ((0, W + pad, slice(0, W)), (N - W - pad, N, slice(pad, W + pad)),
+                         (N // 2 - pad, N // 2 + W + pad, slice(pad, pad + W))):
+        sub = Model(hi - lo, m.dx, m.groups, m.biot, m.attach, channels=m.channels, dt=m.dt,
+                    coeff_kind=m.coeff_kind, coeff_params=m.coeff_params)
+        init = {f: w.init[f][lo:hi] for f in FIELDS}
+        ref = oracle_run("oracle", sub, init, k, w.boot, nthreads=1)
+        err = rel_linf({f: got[f][lo:hi][keep] for f in FIELDS}, {f: ref[f][keep] for f in FIELDS})
+        assert err <= TOL64, (lo, err)
 
 
 @pytest.mark.parametrize("n_zones,wpz,n,steps", [(1, 4, 101, 3000), (16, 6, 128, 2000)])
