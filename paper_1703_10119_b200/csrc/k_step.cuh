@@ -291,8 +291,10 @@ __global__ void k_explicit_boot(const StepArgs a) {
 // wall iterate (initialised to layer n by the host before pass 1); the pass
 // overwrites it and accumulates max |new - old| into *diff (non-negative
 // doubles order like their bit patterns).  out[0]/out[2] receive layer n.
+// The reference folds residuals with std::max(diff, |x|) (building.cpp:232-243),
+// which drops NaN; fmax does the same and NaN never reaches the atomic.
 __device__ __forceinline__ void atomic_max_nonneg(unsigned long long* p, double x) {
-    if (!(x >= 0.0)) x = __longlong_as_double(0x7ff0000000000000ll);   // NaN -> +inf
+    if (!(x >= 0.0)) return;
     atomicMax(p, static_cast<unsigned long long>(__double_as_longlong(x)));
 }
 
@@ -367,7 +369,7 @@ __global__ void k_implicit_unit_pass(const StepArgs a, double* scr, unsigned lon
         mx = fmax(mx, fmax(fabs(nu), fabs(nv)));
         finite = finite && isfinite(nu) && isfinite(nv);
     }
-    atomic_max_nonneg(diff, finite ? d : NAN);
+    atomic_max_nonneg(diff, d);
     if (!(mx <= a.norm) || !finite) {
         const unsigned long long key =
             (static_cast<unsigned long long>(a.layer + 1) << 32) | static_cast<unsigned>(w);
