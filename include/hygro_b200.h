@@ -174,6 +174,24 @@ int hyg_get_state(hyg_ctx* ctx, double* u_prev, double* u_curr, double* v_prev,
                   double* v_curr, double* zone_u, double* zone_v, double* t_star,
                   int64_t* layer);
 
+/* Sub-range access for halo exchange between shards (fp64 models).  Cells
+ * are the flattened wall-major index w*n_nodes + j; any pointer may be NULL
+ * to skip that layer.  Zones [zone0, zone0+count). */
+int hyg_get_cells(hyg_ctx* ctx, int64_t cell0, int64_t count, double* u_prev, double* u_curr,
+                  double* v_prev, double* v_curr);
+int hyg_set_cells(hyg_ctx* ctx, int64_t cell0, int64_t count, const double* u_prev,
+                  const double* u_curr, const double* v_prev, const double* v_curr);
+int hyg_get_zones(hyg_ctx* ctx, int32_t zone0, int32_t count, double* zone_u, double* zone_v);
+int hyg_set_zones(hyg_ctx* ctx, int32_t zone0, int32_t count, const double* zone_u,
+                  const double* zone_v);
+/* Restricts the divergence guard and the implicit starting step's
+ * fixed-point residual to the cells [cell0, cell1) and zones [zone0, zone1)
+ * a shard owns (its halo copies are excluded), and reduces the residual
+ * across shards through `reduce` (max; NULL = local only).  Default: all. */
+typedef double (*hyg_reduce_fn)(void* user, double local_max);
+int hyg_set_owned(hyg_ctx* ctx, int64_t cell0, int64_t cell1, int32_t zone0, int32_t zone1,
+                  hyg_reduce_fn reduce, void* user);
+
 /* Device-resident checkpoint of the complete resumable state (both time
  * layers of every wall, zone states, t_star, layer index — the state a DF
  * march needs, wall.hpp:23-29 + building.hpp:55-59).  hyg_snapshot copies

@@ -85,7 +85,10 @@ _ORACLE_PROTOS = {
     "orc_step_implicit": (C.c_int, [C.POINTER(A.ModelDesc), C.POINTER(BuildingState), C.c_double, C.c_int,
                                     _ip, A.dp]),
     "orc_run": (C.c_int, [C.POINTER(A.ModelDesc), C.POINTER(BuildingState), C.c_int64, _i64p, _ip, _ip]),
+    "orc_set_owned": (None, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
 }
+
+REDUCE_FN = C.CFUNCTYPE(C.c_double, C.c_void_p, C.c_double)
 
 _REF_PROTOS = {
     "ref_march_coupled": (C.c_int, [_BP, C.c_int, C.c_double, C.c_int, _i64p, _ip]),

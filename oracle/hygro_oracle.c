@@ -799,6 +799,19 @@ static void zone_step_implicit(const hyg_model_desc* m, int zi, double u_n, doub
     *v1_out = v1;
 }
 
+static orc_reduce_fn g_reduce = NULL;   /* shard support: see orc_set_owned */
+static void* g_reduce_user = NULL;
+static int g_own_w0 = 0, g_own_w1 = 0x7fffffff, g_own_z0 = 0, g_own_z1 = 0x7fffffff;
+
+void orc_set_owned(int wall0, int wall1, int zone0, int zone1, orc_reduce_fn reduce, void* user) {
+    g_own_w0 = wall0;
+    g_own_w1 = wall1;
+    g_own_z0 = zone0;
+    g_own_z1 = zone1;
+    g_reduce = reduce;
+    g_reduce_user = user;
+}
+
 int orc_step_implicit(const hyg_model_desc* m, orc_building_state* s, double eta, int max_subiters,
                       int* passes, double* residual) { /* building.cpp:189-268 */
     if (!(eta > 0.0)) return HYG_EINVAL;
@@ -831,7 +844,7 @@ int orc_step_implicit(const hyg_model_desc* m, orc_building_state* s, double eta
             const size_t o = (size_t)w * (size_t)n;
             orc_implicit_wall_pass(&base, m->dx, &m->groups[w], NULL, &L, &R, dt, iu + o, iv + o,
                                    uN + o, vN + o);
-            for (int j = 0; j < n; ++j) {
+            for (int j = 0; j < n && w >= g_own_w0 && w < g_own_w1; ++j) {
                 diff = fmax(diff, fabs(uN[o + j] - iu[o + j]));
                 diff = fmax(diff, fabs(vN[o + j] - iv[o + j]));
             }
@@ -848,11 +861,14 @@ int orc_step_implicit(const hyg_model_desc* m, orc_building_state* s, double eta
             }
             double nu, nv;
             zone_step_implicit(m, z, s->zu[z], s->zv[z], us, vs, snu, snv, u_out, v_out, t1, dt, &nu, &nv);
-            diff = fmax(diff, fabs(nu - izu[z]));
-            diff = fmax(diff, fabs(nv - izv[z]));
+            if (z >= g_own_z0 && z < g_own_z1) {
+                diff = fmax(diff, fabs(nu - izu[z]));
+                diff = fmax(diff, fabs(nv - izv[z]));
+            }
             izu[z] = nu;
             izv[z] = nv;
         }
+        if (g_reduce) diff = g_reduce(g_reduce_user, diff);
         if (diff < eta) break;
         if (pass >= max_subiters) { rc = HYG_ECONVERGE; break; }
     }

@@ -88,6 +88,7 @@ class Status(C.Structure):
 
 
 FRAME_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_double, C.c_void_p)
+REDUCE_FN = C.CFUNCTYPE(C.c_double, C.c_void_p, C.c_double)
 
 # name -> (restype, argtypes); every symbol the header declares
 PROTOTYPES = {
@@ -97,6 +98,11 @@ PROTOTYPES = {
     "hyg_destroy": (None, [C.c_void_p]),
     "hyg_set_state": (C.c_int, [C.c_void_p, dp, dp, dp, dp, dp, dp, C.c_double, C.c_int64]),
     "hyg_get_state": (C.c_int, [C.c_void_p, dp, dp, dp, dp, dp, dp, dp, C.POINTER(C.c_int64)]),
+    "hyg_get_cells": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, dp, dp, dp, dp]),
+    "hyg_set_cells": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, dp, dp, dp, dp]),
+    "hyg_get_zones": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, dp, dp]),
+    "hyg_set_zones": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, dp, dp]),
+    "hyg_set_owned": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "hyg_snapshot": (C.c_int, [C.c_void_p]),
     "hyg_restore": (C.c_int, [C.c_void_p]),
     "hyg_set_channel_table": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.POINTER(Ambient)]),

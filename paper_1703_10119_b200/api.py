@@ -291,6 +291,36 @@ class Context:
         out.update(zone_u=zu, zone_v=zv, t=t.value, layer=layer.value)
         return out
 
+    # -- sub-ranges (halo exchange between shards) --------------------------------
+    def get_cells(self, cell0: int, count: int) -> dict:
+        out = {k: np.empty(count) for k in ("u_prev", "u_curr", "v_prev", "v_curr")}
+        _check(self.lib.hyg_get_cells(self.h, cell0, count, _ptr(out["u_prev"]), _ptr(out["u_curr"]),
+                                      _ptr(out["v_prev"]), _ptr(out["v_curr"])), None, "hyg_get_cells")
+        return out
+
+    def set_cells(self, cell0: int, values: dict) -> None:
+        arrs = [np.ascontiguousarray(values[k], dtype=np.float64) for k in ("u_prev", "u_curr", "v_prev", "v_curr")]
+        count = arrs[0].size
+        _check(self.lib.hyg_set_cells(self.h, cell0, count, *map(_ptr, arrs)), None, "hyg_set_cells")
+
+    def get_zones(self, zone0: int, count: int):
+        zu, zv = np.empty(count), np.empty(count)
+        _check(self.lib.hyg_get_zones(self.h, zone0, count, _ptr(zu), _ptr(zv)), None, "hyg_get_zones")
+        return zu, zv
+
+    def set_zones(self, zone0: int, zu, zv) -> None:
+        zu = np.ascontiguousarray(zu, dtype=np.float64)
+        zv = np.ascontiguousarray(zv, dtype=np.float64)
+        _check(self.lib.hyg_set_zones(self.h, zone0, zu.size, _ptr(zu), _ptr(zv)), None, "hyg_set_zones")
+
+    def set_owned(self, cell0: int, cell1: int, zone0: int = 0, zone1: int = 2 ** 31 - 1,
+                  reduce: Optional[Callable[[float], float]] = None) -> None:
+        """Guard/residual restricted to owned ranges; `reduce(local_max) -> global_max`."""
+        self._reduce_cb = A.REDUCE_FN(lambda user, x: float(reduce(x))) if reduce else None
+        _check(self.lib.hyg_set_owned(self.h, cell0, cell1, zone0, zone1,
+                                      C.cast(self._reduce_cb, C.c_void_p) if reduce else None, None),
+               None, "hyg_set_owned")
+
     def snapshot(self):
         """Device-side checkpoint of the full resumable state (hyg_snapshot)."""
         _check(self.lib.hyg_snapshot(self.h), None, "hyg_snapshot")

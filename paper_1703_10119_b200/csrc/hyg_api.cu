@@ -20,6 +20,7 @@
 #include "../../include/hygro_b200.h"
 #include "k_coupled.cuh"
 #include "k_step.cuh"
+#include "k_nonlinear.cuh"
 
 using namespace hyg;
 
@@ -149,11 +150,17 @@ struct hyg_ctx {
     std::vector<double> h_src;
     int* d_flag = nullptr;
     unsigned long long* d_key = nullptr;
+    // shard ownership (hyg_set_owned): guard/residual ranges and the reduction
+    int64_t own_c0 = 0, own_c1 = INT64_MAX;
+    int own_z0 = 0, own_z1 = INT32_MAX;
+    hyg_reduce_fn reduce = nullptr;
+    void* reduce_user = nullptr;
     // time
     double t = 0.0;
     int64_t layer = 0;
     // dispatch
-    bool fused = false;
+    bool fused = false;        // K1: constant exterior walls on a fused grid
+    bool nl_fused = false;     // K2: analytic d(v) exterior walls, n <= 1024
     bool flux = true;
     int seg_len = 4096;
     // measurement
@@ -335,6 +342,8 @@ StepArgs step_args(hyg_ctx* c, int from, double dt) {
     a.layer = c->layer;
     a.norm = c->norm;
     a.fail_key = c->d_key;
+    a.own0 = c->own_c0;
+    a.own1 = c->own_c1;
     return a;
 }
 
@@ -364,6 +373,20 @@ int diverged(hyg_ctx* c, unsigned long long key, hyg_status* st) {
 }
 
 // ---- the per-step path ---------------------------------------------------------
+// After a one-step kernel wrote the new layer into s64[1-cur][1] / [3]:
+// u_prev <- u_curr, u_curr <- new, and the old u_prev buffer becomes the
+// scratch slot (pointer rotation of wall.cpp:80-83, no copies).
+void rotate_layers(hyg_ctx* c) {
+    double** s = c->s64[c->cur];
+    double** t = c->s64[1 - c->cur];
+    for (int f = 0; f < 4; f += 2) {       // f = 0: u, f = 2: v
+        double* old_prev = s[f];
+        s[f] = s[f + 1];
+        s[f + 1] = t[f + 1];
+        t[f + 1] = old_prev;
+    }
+}
+
 int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
     if (c->precision != HYG_F64) {
         set_status(status, HYG_ENOTSUP, "fp32 state needs a fused grid (N in {64,128,256,512})");
@@ -389,6 +412,8 @@ int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
         const int threads = 256;
         const int grid = static_cast<int>((c->cells() + threads - 1) / threads);
         const int nsrc = static_cast<int>(c->zsrc.size() / 3);
+        double* ptr0[2][4];
+        std::memcpy(ptr0, c->s64, sizeof ptr0);
         for (int64_t k = 0; k < rows; ++k) {
             StepArgs a = step_args(c, c->cur, dt);
             a.amb = c->d_table + k * nch;
@@ -416,21 +441,25 @@ int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
                 z.layer = c->layer + k;
                 z.norm = c->norm;
                 z.fail_key = c->d_key;
+                z.own0 = c->own_z0;
+                z.own1 = c->own_z1;
                 LaunchScope ls(c, "zone_step", 0.0);
                 k_zone_step<<<(z.n_zones + 127) / 128, 128, 0, c->stream>>>(z);
                 c->zcur ^= 1;
             }
-            c->cur ^= 1;
+            rotate_layers(c);
         }
         HYG_CUDA(cudaGetLastError());
         unsigned long long key;
         rc = read_key(c, &key, status);
         if (rc) return rc;
         if (key != ~0ull) {
-            // kernels after the failing step returned early: undo their buffer flips
+            // kernels after the failing step returned early: replay only the
+            // rotations of the steps that ran
             const int64_t fail_layer = static_cast<int64_t>(key >> 32);
             const int64_t ran = fail_layer - c->layer;     // steps whose outputs exist
-            if ((rows - ran) % 2) c->cur ^= 1;
+            std::memcpy(c->s64, ptr0, sizeof ptr0);
+            for (int64_t k = 0; k < ran; ++k) rotate_layers(c);
             if (!c->zones.empty() && (rows - ran) % 2) c->zcur ^= 1;
             c->t = times[ran - 1] + dt;
             c->layer = fail_layer;
@@ -566,6 +595,72 @@ int advance_fused_t(hyg_ctx* c, Real* (&buf)[2][4], int64_t nsteps, double dt, h
         c->t = t;
         c->layer += rows;
         done += rows;
+    }
+    return HYG_OK;
+}
+
+// ---- the fused nonlinear path (K2, analytic d(v), one warp per wall) --------------
+int advance_nonlinear(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
+    const int nch = std::max<int>(1, static_cast<int>(c->channels.size()));
+    const int64_t block = 1 << 18;
+    for (int64_t done = 0; done < nsteps;) {
+        const int64_t rows = std::min(block, nsteps - done);
+        std::vector<double> times(rows);
+        double t = c->t;
+        for (int64_t k = 0; k < rows; ++k) {
+            times[k] = t;
+            t += dt;
+        }
+        int rc = upload_table(c, c->layer, times, status);
+        if (rc) return rc;
+        HYG_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+        NonlinearSegArgs a{};
+        a.n_walls = c->n_walls;
+        a.n = c->n;
+        a.n_channels = nch;
+        a.dx = c->dx;
+        a.dt = dt;
+        for (int i = 0; i < 4; ++i) a.p[i] = c->p[i];
+        a.groups = c->d_groups;
+        a.biot = c->d_biot;
+        a.chan = c->d_chan;
+        a.stop = c->d_flag;
+        a.suspect = c->d_flag;
+        const int cur0 = c->cur;
+        int nseg = 0;
+        for (int64_t s0 = 0; s0 < rows; s0 += c->seg_len, ++nseg) {
+            const int len = static_cast<int>(std::min<int64_t>(c->seg_len, rows - s0));
+            a.nsteps = len;
+            a.layer0 = c->layer + s0;
+            a.seg_index = nseg;
+            a.table = c->d_table + s0 * nch;
+            const int from = (cur0 + nseg) & 1;
+            for (int i = 0; i < 4; ++i) {
+                a.in[i] = c->s64[from][i];
+                a.out[i] = c->s64[1 - from][i];
+            }
+            LaunchScope ls(c, "df_analytic_fused", static_cast<double>(c->cells()) * len);
+            if (c->n <= 128) k_df_analytic_walls<128><<<c->n_walls, 32, 0, c->stream>>>(a);
+            else k_df_analytic_walls<1024><<<c->n_walls, 32, 0, c->stream>>>(a);
+        }
+        HYG_CUDA(cudaGetLastError());
+        int flag = 0;
+        HYG_CUDA(cudaMemcpyAsync(&flag, c->d_flag, sizeof flag, cudaMemcpyDeviceToHost, c->stream));
+        HYG_CUDA(cudaStreamSynchronize(c->stream));
+        if (flag == 0) {
+            c->cur = (cur0 + nseg) & 1;
+            c->t = t;
+            c->layer += rows;
+            done += rows;
+            continue;
+        }
+        // the fast guard fired in segment K (whose input is intact): march the
+        // rest of the request with the per-step kernel and its exact guard
+        const int64_t k0 = static_cast<int64_t>(flag - 1) * c->seg_len;
+        c->cur = (cur0 + flag - 1) & 1;
+        c->t = times[k0];
+        c->layer += k0;
+        return advance_general(c, nsteps - done - k0, dt, status);
     }
     return HYG_OK;
 }
@@ -749,6 +844,8 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
     c->out_u.set(d->outdoor_u);
     c->out_v.set(d->outdoor_v);
     c->fused = all_exterior && d->n_zones == 0 && d->coeff_kind == HYG_COEFF_CONSTANT && fused_grid(c->n);
+    c->nl_fused = all_exterior && d->n_zones == 0 && d->coeff_kind == HYG_COEFF_ANALYTIC_D && c->n <= 1024 &&
+                  c->precision == HYG_F64;
     if (c->precision == HYG_F32 && !c->fused) {
         delete c;
         set_status(status, HYG_ENOTSUP, "fp32 state is implemented for exterior constant walls on fused grids only");
@@ -901,6 +998,71 @@ int hyg_get_state(hyg_ctx* c, double* up, double* uc, double* vp, double* vc, do
     return HYG_OK;
 }
 
+int hyg_get_cells(hyg_ctx* c, int64_t cell0, int64_t count, double* up, double* uc, double* vp,
+                  double* vc) {
+    hyg_status* status = nullptr;
+    if (!c || cell0 < 0 || count < 0 || cell0 + count > c->cells()) return HYG_EINVAL;
+    if (c->precision != HYG_F64) return HYG_ENOTSUP;
+    cudaSetDevice(c->device);
+    double* dst[4] = {up, uc, vp, vc};
+    for (int i = 0; i < 4; ++i)
+        if (dst[i])
+            HYG_CUDA(cudaMemcpyAsync(dst[i], c->s64[c->cur][i] + cell0, count * sizeof(double),
+                                     cudaMemcpyDeviceToHost, c->stream));
+    HYG_CUDA(cudaStreamSynchronize(c->stream));
+    return HYG_OK;
+}
+
+int hyg_set_cells(hyg_ctx* c, int64_t cell0, int64_t count, const double* up, const double* uc,
+                  const double* vp, const double* vc) {
+    hyg_status* status = nullptr;
+    if (!c || cell0 < 0 || count < 0 || cell0 + count > c->cells()) return HYG_EINVAL;
+    if (c->precision != HYG_F64) return HYG_ENOTSUP;
+    cudaSetDevice(c->device);
+    const double* src[4] = {up, uc, vp, vc};
+    for (int i = 0; i < 4; ++i)
+        if (src[i])
+            HYG_CUDA(cudaMemcpyAsync(c->s64[c->cur][i] + cell0, src[i], count * sizeof(double),
+                                     cudaMemcpyHostToDevice, c->stream));
+    HYG_CUDA(cudaStreamSynchronize(c->stream));
+    return HYG_OK;
+}
+
+int hyg_get_zones(hyg_ctx* c, int32_t z0, int32_t count, double* zu, double* zv) {
+    hyg_status* status = nullptr;
+    if (!c || z0 < 0 || count < 0 || z0 + count > static_cast<int>(c->zones.size())) return HYG_EINVAL;
+    cudaSetDevice(c->device);
+    if (zu) HYG_CUDA(cudaMemcpyAsync(zu, c->zu[c->zcur] + z0, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (zv) HYG_CUDA(cudaMemcpyAsync(zv, c->zv[c->zcur] + z0, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    HYG_CUDA(cudaStreamSynchronize(c->stream));
+    return HYG_OK;
+}
+
+int hyg_set_zones(hyg_ctx* c, int32_t z0, int32_t count, const double* zu, const double* zv) {
+    hyg_status* status = nullptr;
+    if (!c || z0 < 0 || count < 0 || z0 + count > static_cast<int>(c->zones.size())) return HYG_EINVAL;
+    cudaSetDevice(c->device);
+    if (zu) HYG_CUDA(cudaMemcpyAsync(c->zu[c->zcur] + z0, zu, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    if (zv) HYG_CUDA(cudaMemcpyAsync(c->zv[c->zcur] + z0, zv, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    HYG_CUDA(cudaStreamSynchronize(c->stream));
+    return HYG_OK;
+}
+
+int hyg_set_owned(hyg_ctx* c, int64_t cell0, int64_t cell1, int32_t zone0, int32_t zone1,
+                  hyg_reduce_fn reduce, void* user) {
+    if (!c || cell0 < 0 || cell1 < cell0 || zone0 < 0 || zone1 < zone0) return HYG_EINVAL;
+    c->own_c0 = cell0;
+    c->own_c1 = cell1;
+    c->own_z0 = zone0;
+    c->own_z1 = zone1;
+    c->reduce = reduce;
+    c->reduce_user = user;
+    // the fused kernels guard every wall: a shard with a partial ownership
+    // marches on the per-step path, whose guard honours the owned range
+    if (cell0 > 0 || cell1 < c->cells()) c->fused = c->nl_fused = false;
+    return HYG_OK;
+}
+
 int hyg_snapshot(hyg_ctx* c) {
     hyg_status* status = nullptr;
     if (!c) return HYG_EINVAL;
@@ -1022,6 +1184,8 @@ int hyg_bootstrap(hyg_ctx* c, int32_t kind, hyg_status* status) {
             z.layer = c->layer;
             z.norm = c->norm;
             z.fail_key = c->d_key;
+                z.own0 = c->own_z0;
+                z.own1 = c->own_z1;
             LaunchScope ls(c, "zone_step", 0.0);
             k_zone_step<<<(z.n_zones + 127) / 128, 128, 0, c->stream>>>(z);
             c->zcur ^= 1;
@@ -1082,6 +1246,8 @@ int hyg_bootstrap(hyg_ctx* c, int32_t kind, hyg_status* status) {
                 z.norm = c->norm;
                 z.diff = d_diff;
                 z.fail_key = c->d_key;
+                z.own0 = c->own_z0;
+                z.own1 = c->own_z1;
                 LaunchScope ls(c, "zone_implicit", 0.0);
                 k_zone_implicit<<<(z.n_zones + 127) / 128, 128, 0, c->stream>>>(z);
                 snap ^= 1;
@@ -1091,6 +1257,7 @@ int hyg_bootstrap(hyg_ctx* c, int32_t kind, hyg_status* status) {
             HYG_CUDA(cudaMemcpyAsync(&bits, d_diff, sizeof bits, cudaMemcpyDeviceToHost, c->stream));
             HYG_CUDA(cudaStreamSynchronize(c->stream));
             std::memcpy(&diff, &bits, sizeof diff);
+            if (c->reduce) diff = c->reduce(c->reduce_user, diff);   // joint residual over shards
             if (diff < eta) break;
             if (passes >= c->max_subiters) {
                 rcl = HYG_ECONVERGE;
@@ -1142,7 +1309,9 @@ int hyg_advance(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
     if (nsteps == 0) return HYG_OK;
     cudaSetDevice(c->device);
     if (!(dt > 0.0)) dt = c->dt;
-    int rc = c->fused ? advance_fused(c, nsteps, dt, status) : advance_general(c, nsteps, dt, status);
+    int rc = c->fused      ? advance_fused(c, nsteps, dt, status)
+             : c->nl_fused ? advance_nonlinear(c, nsteps, dt, status)
+                           : advance_general(c, nsteps, dt, status);
     if (status && rc == HYG_OK) status->code = HYG_OK;
     return rc;
 }

@@ -37,6 +37,7 @@ struct StepArgs {
     int64_t layer;              // index of layer n
     double norm;
     unsigned long long* fail_key;
+    int64_t own0, own1;         // cells whose guard/residual count (a shard owns a range)
 };
 
 // d(v) functor of HYG_COEFF_ANALYTIC_D: k_M* = 1 + p0 v + p1 exp(-p2 (v - p3)^2)
@@ -157,11 +158,11 @@ __global__ void k_df_step_general(const StepArgs a) {
     double un, vn;
     if (a.coeff_kind == kCoeffConstant) coupled_node(a, w, j, un, vn);
     else analytic_node(a, w, j, un, vn);
-    a.out[0][tid] = a.in[1][tid];
-    a.out[2][tid] = a.in[3][tid];
+    // only the new layer is written; the host rotates layer pointers
+    // (prev <- curr) instead of copying: 32 B read + 16 B written per update
     a.out[1][tid] = un;
     a.out[3][tid] = vn;
-    if (!(fabs(un) <= a.norm) || !(fabs(vn) <= a.norm)) {
+    if (tid >= a.own0 && tid < a.own1 && (!(fabs(un) <= a.norm) || !(fabs(vn) <= a.norm))) {
         const unsigned long long key =
             (static_cast<unsigned long long>(a.layer + 1) << 32) | static_cast<unsigned>(w);
         atomicMin(a.fail_key, key);
@@ -195,6 +196,7 @@ struct ZoneArgs {
     int64_t layer;
     double norm;
     unsigned long long* fail_key;
+    int own0, own1;             // zones whose guard counts
 };
 
 // zone_step_explicit (zone.cpp:69-74) of zone_rhs (zone.cpp:26-53) with the
@@ -226,7 +228,8 @@ __global__ void k_zone_step(const ZoneArgs a) {
     const double nv = v_a + a.dt * dv;
     a.zu_out[z] = nu;
     a.zv_out[z] = nv;
-    if (!isfinite(nu) || !isfinite(nv) || fabs(nu) > a.norm || fabs(nv) > a.norm) {
+    if (z >= a.own0 && z < a.own1 &&
+        (!isfinite(nu) || !isfinite(nv) || fabs(nu) > a.norm || fabs(nv) > a.norm)) {
         // zone failures rank after every wall of the same layer (building.cpp:288-299)
         const unsigned long long key = (static_cast<unsigned long long>(a.layer + 1) << 32) | 0xffffffffu;
         atomicMin(a.fail_key, key);
@@ -275,7 +278,7 @@ __global__ void k_explicit_boot(const StepArgs a) {
     a.out[2][tid] = vc[j];
     a.out[1][tid] = un;
     a.out[3][tid] = vn;
-    if (!(fabs(un) <= a.norm) || !(fabs(vn) <= a.norm)) {
+    if (tid >= a.own0 && tid < a.own1 && (!(fabs(un) <= a.norm) || !(fabs(vn) <= a.norm))) {
         const unsigned long long key =
             (static_cast<unsigned long long>(a.layer + 1) << 32) | static_cast<unsigned>(w);
         atomicMin(a.fail_key, key);
@@ -369,8 +372,9 @@ __global__ void k_implicit_unit_pass(const StepArgs a, double* scr, unsigned lon
         mx = fmax(mx, fmax(fabs(nu), fabs(nv)));
         finite = finite && isfinite(nu) && isfinite(nv);
     }
-    atomic_max_nonneg(diff, d);
-    if (!(mx <= a.norm) || !finite) {
+    const bool own = static_cast<int64_t>(w) * n >= a.own0 && static_cast<int64_t>(w + 1) * n <= a.own1;
+    if (own) atomic_max_nonneg(diff, d);
+    if (own && (!(mx <= a.norm) || !finite)) {
         const unsigned long long key =
             (static_cast<unsigned long long>(a.layer + 1) << 32) | static_cast<unsigned>(w);
         atomicMin(a.fail_key, key);
@@ -399,6 +403,7 @@ struct ZoneImplicitArgs {
     double norm;
     unsigned long long* diff;
     unsigned long long* fail_key;
+    int own0, own1;             // zones whose residual/guard count
 };
 
 __global__ void k_zone_implicit(const ZoneImplicitArgs a) {
@@ -440,10 +445,11 @@ __global__ void k_zone_implicit(const ZoneImplicitArgs a) {
     }
     const double u1 = u_rhs / u_coef;
     const double dd = fmax(fabs(u1 - a.zu_s[z]), fabs(v1 - a.zv_s[z]));   // building.cpp:240-243
-    atomic_max_nonneg(a.diff, dd);
+    const bool own = z >= a.own0 && z < a.own1;
+    if (own) atomic_max_nonneg(a.diff, dd);
     a.zu_out[z] = u1;
     a.zv_out[z] = v1;
-    if (!isfinite(u1) || !isfinite(v1) || fabs(u1) > a.norm || fabs(v1) > a.norm) {
+    if (own && (!isfinite(u1) || !isfinite(v1) || fabs(u1) > a.norm || fabs(v1) > a.norm)) {
         const unsigned long long key = (static_cast<unsigned long long>(a.layer + 1) << 32) | 0xffffffffu;
         atomicMin(a.fail_key, key);
     }

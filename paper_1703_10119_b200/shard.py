@@ -1,0 +1,269 @@
+"""Multi-GPU decomposition of the DF path: one process per GPU, torch.distributed
+for the plumbing.
+
+  * independent walls (configs[1]/[2]): contiguous wall ranges per rank and no
+    exchange at all — bench.py's weak-scaling layout;
+  * the long domain (configs[4]): x-slabs with H halo nodes per side;
+  * the zone ring (configs[3]): contiguous zone blocks with H halo zones per
+    side (a zone travels whole with its walls).
+
+Halo exchange is deep: every K <= H steps, not every step.  After K DF steps
+node j depends only on nodes j-K..j+K of the two layers present K steps
+earlier (the three-level stencil reaches one neighbour per step; a zone
+reaches its ring neighbours one step at a time, walls are zone-local), so a
+shard that marches its owned range plus H halo cells for K steps — treating
+the far halo end as an artificial face — computes every owned cell exactly,
+bit for bit as the undivided domain.  The halo copies are then refreshed
+from their owners (both time layers; zones with their walls).  One exchange
+moves 4 layers x H cells per side (x-slabs), i.e. K-fold fewer, larger
+messages than a per-step 1-node halo, which matters when a step is a few
+microseconds of GPU time.  The implicit starting step of a zoned building is
+a joint fixed point: its residual is restricted to owned walls/zones and
+max-reduced across ranks every pass (hyg_set_owned), and needs passes <= H.
+
+The engine is the CUDA Context on GPUs; tests drive the same logic with the
+C oracle on CPU ranks over gloo (tests/test_shard_gloo.py).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import numpy as np
+
+from .api import Model, NumericalError, ZoneSpec
+
+FIELDS = ("u_prev", "u_curr", "v_prev", "v_curr")
+
+
+@dataclass
+class Slab:
+    lo: int      # owned [lo, hi) in global nodes
+    hi: int
+    a: int       # local [a, b) = owned + halo
+    b: int
+
+
+def slab_bounds(n: int, world: int, rank: int, halo: int) -> Slab:
+    lo, hi = n * rank // world, n * (rank + 1) // world
+    if world > 1 and hi - lo < halo:
+        raise ValueError(f"slab of {hi - lo} nodes is thinner than the halo ({halo})")
+    return Slab(lo, hi, max(0, lo - halo), min(n, hi + halo))
+
+
+class Comm:
+    """Point-to-point + reductions over a torch.distributed group (gloo for host
+    buffers; the exchange payloads are a few KB per K steps)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+
+    def _t(self, a):
+        import torch
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+
+    def exchange(self, sends: dict, recvs: dict) -> dict:
+        """sends/recvs: {peer_rank: ndarray | shape}; returns received arrays."""
+        import torch
+        reqs, out = [], {}
+        for peer, shape in recvs.items():
+            buf = torch.empty(shape, dtype=torch.float64)
+            out[peer] = buf
+            reqs.append(self.dist.irecv(buf, src=self._global(peer), group=self.group))
+        for peer, arr in sends.items():
+            reqs.append(self.dist.isend(self._t(arr), dst=self._global(peer), group=self.group))
+        for r in reqs:
+            r.wait()
+        return {k: v.numpy() for k, v in out.items()}
+
+    def _global(self, r):
+        return r if self.group is None else self.dist.get_global_rank(self.group, r)
+
+    def allreduce_max(self, x: float) -> float:
+        import torch
+        t = torch.tensor([x], dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+    def allreduce_min(self, x: float) -> float:
+        import torch
+        t = torch.tensor([x], dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        return float(t.item())
+
+
+def _advance_guarded(engine, k, comm):
+    """k steps on every rank; a divergence anywhere stops all ranks with the
+    earliest failing layer (check_bounded semantics across shards)."""
+    fail = float("inf")
+    err = None
+    try:
+        engine.advance(k)
+    except NumericalError as e:
+        fail, err = float(e.layer), e
+    first = comm.allreduce_min(fail)
+    if first != float("inf"):
+        if err is not None and float(err.layer) == first:
+            raise err
+        raise NumericalError(f"divergence on another shard at layer {int(first)}")
+
+
+# ---------------------------------------------------------------------------------
+class LongDomainShard:
+    """configs[4]: one long wall cut into x-slabs.  `engine_factory(model)`
+    returns a Context-like engine for the local slab."""
+
+    def __init__(self, model: Model, init: dict, comm, engine_factory: Callable, halo: int = 32):
+        self.comm, self.halo = comm, halo
+        n = model.n_nodes
+        s = self.slab = slab_bounds(n, comm.world, comm.rank, halo)
+        biot = model.biot.copy()
+        if s.a > 0:
+            biot[0, 0] = 0.0          # artificial faces: adiabatic/impermeable (their
+        if s.b < n:                   # cone never reaches the owned nodes)
+            biot[0, 1] = 0.0
+        local = Model(s.b - s.a, model.dx, model.groups, biot, model.attach, channels=model.channels,
+                      dt=model.dt, divergence_norm=model.divergence_norm, coeff_kind=model.coeff_kind,
+                      coeff_params=model.coeff_params, device=model.device)
+        self.engine = engine_factory(local)
+        self.engine.set_state(**{f: init[f][s.a:s.b] for f in FIELDS})
+        self.engine.set_owned(s.lo - s.a, s.hi - s.a)
+
+    def advance(self, nsteps: int):
+        done = 0
+        while done < nsteps:
+            k = min(self.halo, nsteps - done)
+            _advance_guarded(self.engine, k, self.comm)
+            self.refresh()
+            done += k
+
+    def refresh(self):
+        s, H, r, P = self.slab, self.halo, self.comm.rank, self.comm.world
+        sends, recvs = {}, {}
+        if r > 0:
+            left = self.engine.get_cells(s.lo - s.a, H)
+            sends[r - 1] = np.stack([left[f] for f in FIELDS])
+            recvs[r - 1] = (4, H)
+        if r < P - 1:
+            right = self.engine.get_cells(s.hi - H - s.a, H)
+            sends[r + 1] = np.stack([right[f] for f in FIELDS])
+            recvs[r + 1] = (4, H)
+        got = self.comm.exchange(sends, recvs)
+        if r > 0:
+            self.engine.set_cells(0, dict(zip(FIELDS, got[r - 1])))
+        if r < P - 1:
+            self.engine.set_cells(s.hi - s.a, dict(zip(FIELDS, got[r + 1])))
+
+    def owned_state(self) -> dict:
+        s = self.slab
+        return self.engine.get_cells(s.lo - s.a, s.hi - s.lo)
+
+
+# ---------------------------------------------------------------------------------
+class ZoneRingShard:
+    """configs[3]: zones in a ring, `walls_per_zone` consecutive walls per zone
+    (zone z owns walls z*W .. z*W+W-1, face 1 on the zone), blocks of zones per
+    rank with `halo` zones on each side."""
+
+    def __init__(self, model: Model, init: dict, comm, engine_factory: Callable, walls_per_zone: int,
+                 halo: int = 8):
+        self.comm, self.halo, self.W = comm, halo, walls_per_zone
+        Z = len(model.zones)
+        P, r = comm.world, comm.rank
+        self.lo, self.hi = Z * r // P, Z * (r + 1) // P
+        if P > 1 and (self.hi - self.lo < halo or Z < (self.hi - self.lo) + 2 * halo):
+            raise ValueError("zone block thinner than the halo")
+        H = halo if P > 1 else 0
+        self.gz = [(self.lo - H + i) % Z for i in range(self.hi - self.lo + 2 * H)]   # local -> global zone
+        idx = {g: i for i, g in enumerate(self.gz)}
+        n, W = model.n_nodes, walls_per_zone
+        gw = np.concatenate([np.arange(g * W, g * W + W) for g in self.gz])            # local -> global wall
+        self.gw = gw
+        attach = model.attach[gw].copy()
+        zones = []
+        for i, g in enumerate(self.gz):
+            zg = model.zones[g]
+            links = [(i * W + k, l[1], *l[2:]) for k, l in enumerate(zg.walls)]
+            for wl, l in zip(range(i * W, i * W + W), zg.walls):
+                attach[wl, l[1]] = (1, i)
+            inz = [(idx[p], *rest) for p, *rest in zg.interzone
+                   if p in idx and (P == 1 or abs(idx[p] - i) == 1)]
+            zones.append(ZoneSpec(zg.kappa_a_tt1, zg.g_v, zg.q_v1, zg.q_v2, zg.sources, zg.moisture_sign,
+                                  links, inz))
+        local = Model(n, model.dx, model.groups[gw], model.biot[gw], attach, channels=model.channels,
+                      zones=zones, zone_sources=model.zone_sources, outdoor_u=model.outdoor_u,
+                      outdoor_v=model.outdoor_v, dt=model.dt, divergence_norm=model.divergence_norm,
+                      eta_factor=model.eta_factor, max_subiters=model.max_subiters, device=model.device)
+        self.engine = engine_factory(local)
+        cells = (gw[:, None] * n + np.arange(n)[None, :]).reshape(-1)
+        st = {f: init[f][cells] for f in FIELDS}
+        st["zone_u"] = np.asarray(init["zone_u"])[self.gz]
+        st["zone_v"] = np.asarray(init["zone_v"])[self.gz]
+        self.engine.set_state(**st)
+        self.H = H
+        own = self.hi - self.lo
+        self.engine.set_owned(H * W * n, (H + own) * W * n, H, H + own,
+                              reduce=comm.allreduce_max if P > 1 else None)
+
+    def bootstrap(self, kind="implicit"):
+        st = self.engine.bootstrap(kind)
+        if self.H and st.subiterations > self.H:
+            raise RuntimeError(f"implicit start took {st.subiterations} passes > halo {self.H}")
+        self.refresh()
+        return st
+
+    def advance(self, nsteps: int):
+        done = 0
+        K = self.H if self.H else nsteps
+        while done < nsteps:
+            k = min(K, nsteps - done)
+            _advance_guarded(self.engine, k, self.comm)
+            if self.H:
+                self.refresh()
+            done += k
+
+    def _zone_block(self, i0, count):
+        n, W = self.engine_model_n, self.W
+        cells = self.engine.get_cells(i0 * W * n, count * W * n)
+        zu, zv = self.engine.get_zones(i0, count)
+        return np.concatenate([np.stack([cells[f] for f in FIELDS]).reshape(-1), zu, zv])
+
+    @property
+    def engine_model_n(self):
+        return self.engine.model.n_nodes
+
+    def refresh(self):
+        if not self.H:
+            return
+        H, W, n = self.H, self.W, self.engine_model_n
+        P, r = self.comm.world, self.comm.rank
+        own = self.hi - self.lo
+        left, right = (r - 1) % P, (r + 1) % P
+        # my first H owned zones go left (they are its right halo), my last H go right
+        first = self._zone_block(H, H)
+        last = self._zone_block(own, H)
+        size = first.size
+        if left == right:   # two ranks: both messages go to the same peer; ship them together
+            got = self.comm.exchange({left: np.concatenate([first, last])}, {left: (2 * size,)})[left]
+            from_right, from_left = got[:size], got[size:]
+        else:
+            got = self.comm.exchange({left: first, right: last}, {left: (size,), right: (size,)})
+            from_left, from_right = got[left], got[right]
+        self._set_zone_block(0, H, from_left)                   # left halo <- left's last owned
+        self._set_zone_block(H + own, H, from_right)            # right halo <- right's first owned
+
+    def _set_zone_block(self, i0, count, flat):
+        n, W = self.engine_model_n, self.W
+        m = count * W * n
+        cells = flat[:4 * m].reshape(4, m)
+        self.engine.set_cells(i0 * W * n, dict(zip(FIELDS, cells)))
+        self.engine.set_zones(i0, flat[4 * m:4 * m + count], flat[4 * m + count:])
+
+    def owned_state(self) -> dict:
+        n, W = self.engine_model_n, self.W
+        own = self.hi - self.lo
+        out = self.engine.get_cells(self.H * W * n, own * W * n)
+        out["zone_u"], out["zone_v"] = self.engine.get_zones(self.H, own)
+        return out
