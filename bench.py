@@ -1,25 +1,29 @@
 #!/usr/bin/env python3
 """Benchmark of the DF hot path (BASELINE.json metric) — one JSON line on rank 0.
 
-Workload (configs[1], the config the metric is quoted on): 65,536 independent
-coupled walls x 256 nodes, fp64, 1e5 steps per run (one implicit starting
-step + 99,999 Dufort–Frankel steps, the run() convention building.cpp:311-323).
-A bench "step" is one such full run from the initial state.  Weak scaling:
-every rank marches its own 65,536 walls (seeded per rank), no data-path
+Default workload = configs[1], the config the metric is quoted on: 65,536
+independent coupled walls x 256 nodes, fp64, 1e5 steps per run (one implicit
+starting step + 99,999 Dufort-Frankel steps, the run() convention
+building.cpp:311-323).  A bench "step" is one such full run from the
+initial state (restored from a device snapshot: inputs resident in HBM).
+Weak scaling: every rank marches its own 65,536 walls, no data-path
 collective; `value` = all ranks' node-updates / max-over-ranks device time.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                  [--run-steps S] [--walls B]
+                  [--config cfg0|cfg1|cfg2|cfg3|cfg4] [--run-steps S]
 
+--config selects the other BASELINE configs (supplementary lines): cfg0 the
+single nonlinear wall (replicas at N>1), cfg2 fp32 + variable dt (weak),
+cfg3 the zone ring and cfg4 the long domain (strong scaling through
+shard.py's deep-halo decomposition at N>1).
 --impl reference times the reference's own CPU implementation of the path
 (oracle/_ref: the unmodified reference library compiled from its sources, or
-the C restatement when that is absent) on the host cores with all threads.
+the C restatement where that is absent) on the host cores.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -35,8 +39,21 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "DF node-updates/sec (fp64) and % of min(HBM,FP64) roofline, 1/2/4/8 B200"
 UNIT = "node-updates/s"
-FLOP_PER_UPDATE = 14      # SURVEY.md §8d convention for cfg1 (add/mul 1, FMA 2)
-BYTES_PER_UPDATE_HBM = 0  # whole profile register-resident inside a launch
+
+# per config: algorithmic flop and HBM bytes per node-update,
+# the bound, the dominant kernel and how the work divides over ranks
+CONFIGS = {
+    "cfg0": dict(flop=21, bytes=0, bound="fp64 (one SM: latency-bound single wall)",
+                 kernel="df_analytic_fused", scaling="replicas", dtype="f64", run_steps=100_000),
+    "cfg1": dict(flop=14, bytes=0, bound="fp64", kernel="df_coupled_fused_f64", scaling="weak", dtype="f64",
+                 run_steps=100_000),
+    "cfg2": dict(flop=14, bytes=0, bound="fp32", kernel="df_coupled_fused_f32", scaling="weak", dtype="f32",
+                 run_steps=100_000),
+    "cfg3": dict(flop=14.1, bytes=48, bound="hbm", kernel="df_step_general", scaling="strong", dtype="f64",
+                 run_steps=80_000),
+    "cfg4": dict(flop=33, bytes=48, bound="hbm", kernel="df_step_general", scaling="strong", dtype="f64",
+                 run_steps=10_000),
+}
 
 
 def parse():
@@ -45,23 +62,30 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--run-steps", type=int, default=100_000, help="time steps per run (incl. the start)")
+    p.add_argument("--config", default="cfg1", choices=sorted(CONFIGS))
+    p.add_argument("--run-steps", type=int, default=0, help="time steps per run incl. the start (0: config default)")
     p.add_argument("--walls", type=int, default=65536)
     p.add_argument("--nodes", type=int, default=256)
+    p.add_argument("--zones", type=int, default=8192)
+    p.add_argument("--long-nodes", type=int, default=1 << 26)
+    p.add_argument("--halo", type=int, default=0, help="shard halo depth (0: config default)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    return p.parse_args()
+    a = p.parse_args()
+    if not a.run_steps:
+        a.run_steps = CONFIGS[a.config]["run_steps"]
+    return a
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line).
+    Started before the warm-up (its start-up must not fall inside the timed
+    region); samples are filtered to the region's wall-clock window."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -105,41 +129,104 @@ class Clocks:
         sm = [float(r[0]) for r in rows]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower().startswith("active")})
+        pw = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
-                "samples": len(rows), "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())}
+                "samples": len(rows), "power_w_max": max(pw) if pw else None}
 
 
-def make_workload(args, rank):
+def make_workload(args, rank, world):
     from paper_1703_10119_b200 import workloads
-    return workloads.batched_walls(n_walls=args.walls, n_nodes=args.nodes, nsteps=args.run_steps, seed=1 + rank)
+    c = args.config
+    if c == "cfg1":
+        return workloads.batched_walls(n_walls=args.walls, n_nodes=args.nodes, nsteps=args.run_steps, seed=1 + rank)
+    if c == "cfg2":
+        return workloads.batched_walls(n_walls=args.walls, n_nodes=args.nodes, nsteps=args.run_steps, seed=1 + rank,
+                                       precision="f32", variable_dt=True)
+    if c == "cfg0":
+        return workloads.single_wall_d(nsteps=args.run_steps)
+    if c == "cfg3":
+        return workloads.zone_ring(n_zones=args.zones, nsteps=args.run_steps)
+    return workloads.long_domain(n_nodes=args.long_nodes, nsteps=args.run_steps)
 
 
-def workload_config(args, world):
-    return {"workload": f"cfg1_batched_fp64: {args.walls} walls x {args.nodes} nodes per GPU, "
-                        f"{args.run_steps} steps per run (1 implicit start + {args.run_steps - 1} DF), dt*=1e-3",
-            "walls_per_gpu": args.walls, "nodes": args.nodes, "steps_per_run": args.run_steps,
-            "state_bytes_per_gpu": args.walls * args.nodes * 32,
-            "l2": "inputs larger than L2 (state 537 MB per GPU at the default size)",
-            "parallelism": f"walls sharded per rank (weak), {world} rank(s), no collective on the data path"}
+def workload_config(args, w, world):
+    c = CONFIGS[args.config]
+    d = {"workload": f"{w.name}: {w.notes}, {args.run_steps} steps per run "
+                     f"(start: {w.boot}{'' if w.boot == 'none' else ', counted as step 1'})",
+         "config_index": int(args.config[-1]), "nodes": w.model.n_nodes, "walls": w.model.n_walls,
+         "zones": len(w.model.zones), "steps_per_run": args.run_steps, "dt": w.model.dt,
+         "state_bytes": w.cells * 32,
+         "l2": ("inputs larger than L2" if w.cells * 32 > 126e6 else
+                "working set L2/on-chip resident (single wall); no L2 flush between runs"),
+         "parallelism": {"weak": f"walls sharded per rank (weak), {world} rank(s), no collective on the data path",
+                         "replicas": f"{world} independent replica(s)",
+                         "strong": f"{'deep-halo shards (shard.py)' if world > 1 else 'one GPU'}, {world} rank(s)"}
+         [c["scaling"]]}
+    if w.dt_schedule:
+        d["dt_schedule"] = w.dt_schedule
+    return d
+
+
+def run_steps_of(w):
+    """[(nsteps, dt)] for advance() after the start step."""
+    if w.dt_schedule:
+        out, first = [], True
+        for n, d in w.dt_schedule:
+            out.append((n - 1 if first and w.boot != "none" else n, d))
+            first = False
+        return out
+    return [(w.nsteps - (0 if w.boot == "none" else 1), w.model.dt)]
 
 
 # ---------------------------------------------------------------------------------
-def cpu_reference_rate(w, nsteps, threads, implicit=False):
-    """Time the reference CPU DF path (or its Euler-implicit path) on w for nsteps."""
+def cpu_reference_rate(args, w, threads):
+    """Time the reference CPU path on a bounded sample of w; returns (rate, sample, kind, implicit)."""
     import oracle as O
     from paper_1703_10119_b200 import workloads
-    impl = "ref" if O.ref_lib() is not None else "oracle"
+    ref = O.ref_lib() is not None
+    impl, kind = ("ref", "reference") if ref else ("oracle", "port")
     dt = w.model.dt
-    times = workloads.accumulate_times(np.full(nsteps + 1, dt))
-    tab = O.forcing_table(w.model, times, 0, w.tables)
-    wb = O.WallBatch(w.model, w.init, tab)
-    t0 = time.perf_counter()
-    if implicit:
-        O.march_implicit(impl, wb, nsteps, dt, nthreads=threads)
+    c = args.config
+    if c in ("cfg3",):
+        nsteps = 40
+        b = O.Building(w.model, w.init)
+        t0 = time.perf_counter()
+        b.run(impl, nsteps, with_bootstrap=False)
+        sec = time.perf_counter() - t0
+        return (w.cells * nsteps / sec, f"all {len(w.model.zones)} zones x {nsteps} step_explicit steps "
+                f"(single thread: one building, building.cpp:152-187), {sec:.1f} s", kind, None)
+    if c == "cfg4":
+        n = min(w.model.n_nodes, 1 << 22)
+        from paper_1703_10119_b200.api import Model
+        m = w.model
+        sub = Model(n, m.dx, m.groups, m.biot, m.attach, channels=m.channels, dt=dt, coeff_kind=m.coeff_kind,
+                    coeff_params=m.coeff_params)
+        init = {k: w.init[k][:n] for k in ("u_prev", "u_curr", "v_prev", "v_curr")}
+        nsteps = 10
+    elif c == "cfg0":
+        sub, init, nsteps = w.model, w.init, 20_000
     else:
-        O.march(impl, wb, nsteps, dt, threads)
+        sub, init = w.model, w.init
+        nsteps = max(1, int(4e8 // w.cells))
+    times = workloads.accumulate_times(np.full(nsteps + 1, dt))
+    tab = O.forcing_table(sub, times, 0, w.tables)
+    wb = O.WallBatch(sub, init, tab)
+    t0 = time.perf_counter()
+    rc = O.march(impl, wb, nsteps, dt, threads)
     sec = time.perf_counter() - t0
-    return w.cells * nsteps / sec, sec, ("reference" if impl == "ref" else "port")
+    cells = sub.n_walls * sub.n_nodes
+    what = {"cfg0": "the reference's d(v) transcription oracle (df_oracle.hpp)" if ref else "oracle restatement",
+            "cfg4": "the reference's d(v) transcription oracle on the first 2^22 nodes" if ref else "oracle",
+            }.get(c, "df_step_coupled (wall.cpp:144-194), threads split walls")
+    imp = None
+    if c in ("cfg1", "cfg2"):
+        wi = O.WallBatch(sub, init, tab)
+        ns = max(1, nsteps // 4)
+        t1 = time.perf_counter()
+        O.march_implicit(impl, wi, ns, dt, nthreads=threads)
+        imp = (cells * ns / (time.perf_counter() - t1), f"all walls x {ns} Euler-implicit steps")
+    return cells * nsteps / sec, f"{sub.n_walls} wall(s) x {sub.n_nodes} nodes x {nsteps} steps, {what}, " \
+                                  f"{sec:.1f} s", kind, imp
 
 
 def run_reference(args):
@@ -147,42 +234,82 @@ def run_reference(args):
     if rank != 0:
         return 0
     threads = len(os.sched_getaffinity(0))
-    w = make_workload(args, 0)
-    # bounded sample per step: all walls, a few steps (each step a few seconds of CPU work)
-    sample_steps = max(1, int(4e8 // w.cells))
-    for _ in range(args.warmup):
-        cpu_reference_rate(w, max(1, sample_steps // 4), threads)
+    w = make_workload(args, 0, 1)
     rates, secs = [], []
-    kind = "port"
-    for _ in range(args.steps):
-        r, s, kind = cpu_reference_rate(w, sample_steps, threads)
-        rates.append(r)
-        secs.append(s)
+    kind, sample = "port", ""
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        r, sample, kind, _ = cpu_reference_rate(args, w, threads)
+        if i >= args.warmup:
+            rates.append(r)
+            secs.append(time.perf_counter() - t0)
     value = statistics.median(rates)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(secs), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
-            "config": workload_config(args, 1), "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                             "sample": f"all {w.model.n_walls} walls x {sample_steps} DF steps per bench step "
-                                       f"(df_step_coupled, wall.cpp:144-194, threads split walls)"},
+            "scaling": CONFIGS[args.config]["scaling"], "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded)", "config": workload_config(args, w, 1), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ---------------------------------------------------------------------------------
+class Runner:
+    """One rank's engine for the selected config: a Context, or a shard of one."""
+
+    def __init__(self, args, w, rank, world, local, gloo):
+        from paper_1703_10119_b200 import Context, shard
+        self.w, self.args = w, args
+        cfg = CONFIGS[args.config]
+        w.model.device = local
+        self.shard = None
+        if cfg["scaling"] == "strong" and world > 1:
+            comm = shard.Comm(gloo)
+            if args.config == "cfg4":
+                self.shard = shard.LongDomainShard(w.model, w.init, comm, Context, halo=args.halo or 64)
+            else:
+                self.shard = shard.ZoneRingShard(w.model, w.init, comm, Context, walls_per_zone=6,
+                                                 halo=args.halo or 8)
+            self.ctx = self.shard.engine
+            self.updates = w.cells / world
+        else:
+            self.ctx = Context(w.model)
+            for ch, (first, tab) in w.tables.items():
+                self.ctx.set_channel_table(ch, first, tab)
+            self.ctx.set_state(**w.init)
+            self.updates = w.cells
+        self.ctx.snapshot()
+
+    def run(self):
+        self.ctx.restore()
+        w = self.w
+        if self.shard is not None:
+            if w.boot != "none":
+                self.shard.bootstrap(w.boot)
+            for n, d in run_steps_of(w):
+                self.shard.advance(n)
+            return
+        if w.boot != "none":
+            self.ctx.bootstrap(w.boot)
+        for n, d in run_steps_of(w):
+            self.ctx.advance(n, d)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
     rank, world, local = dist_env()
+    cfg = CONFIGS[args.config]
     import torch
     import torch.distributed as dist
+    gloo = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        gloo = dist.new_group(backend="gloo")
     torch.cuda.set_device(local)
-    from paper_1703_10119_b200 import Context, api
+    from paper_1703_10119_b200 import api
 
     def barrier():
         if world > 1:
@@ -195,27 +322,16 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    w = make_workload(args, rank)
-    w.model.device = local
-    fp64_peak = api.probe_fp64_peak(local)
-    ctx = Context(w.model)
-    for ch, (first, tab) in w.tables.items():
-        ctx.set_channel_table(ch, first, tab)
-    ctx.set_state(**w.init)
-    ctx.snapshot()                      # inputs resident in HBM; each run restores them
-    nsteps = w.nsteps
+    w = make_workload(args, rank if cfg["scaling"] != "strong" else 0, world)
+    peak64 = api.probe_fp64_peak(local)
+    peak32 = api.probe_fp32_peak(local) if cfg["bound"] == "fp32" else None
+    R = Runner(args, w, rank, world, local, gloo)
+    ctx = R.ctx
 
-    def one_run():
-        ctx.restore()
-        ctx.bootstrap(w.boot)
-        ctx.advance(nsteps - 1)
-
-    # the sampler starts before the warm-up: nvidia-smi start-up stalls the
-    # device briefly and must not fall inside the timed region
     clocks = Clocks(local)
     clocks.start()
     for _ in range(args.warmup):
-        one_run()
+        R.run()
     ctx.synchronize()
     clocks.mark("t_start")
     launches0 = ctx.launches
@@ -223,7 +339,7 @@ def main():
     torch.cuda.synchronize()
     ctx.record(0)
     for _ in range(args.steps):
-        one_run()
+        R.run()
     ctx.record(1)
     ctx.synchronize()
     barrier()
@@ -233,60 +349,75 @@ def main():
     clk = clocks.stop()
     launches = ctx.launches - launches0
     ms_max = max_over_ranks(ms)
-    updates = float(w.cells) * nsteps * args.steps * world
-    value = updates / (ms_max * 1e-3)
+    total_updates = float(w.cells if cfg["scaling"] == "strong" else w.cells * world) * w.nsteps * args.steps
+    value = total_updates / (ms_max * 1e-3)
 
-    # dominant kernel: per-launch CUDA events on the launching stream (one extra run)
+    # dominant kernel: CUDA events around every launch on the launching stream (one extra run)
     ctx.reset_kernel_stats()
     ctx.profiling(True)
-    one_run()
+    R.run()
     ctx.synchronize()
     ctx.profiling(False)
     stats = ctx.kernel_stats()
     top = max(stats, key=lambda s: s["ms"])
-    kernel_rate = top["node_updates"] / (top["ms"] * 1e-3)
-    achieved_tf = kernel_rate * FLOP_PER_UPDATE / 1e12
+    kernel_rate = top["node_updates"] / (top["ms"] * 1e-3) if top["node_updates"] else 0.0
     share = top["ms"] / sum(s["ms"] for s in stats)
+    if cfg["bound"] == "hbm":
+        achieved = kernel_rate * cfg["bytes"] / 1e9
+        peak, unit, peak_src = 6458.4, "GB/s", "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
+        try:
+            peak = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+        except Exception:
+            peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+    elif cfg["bound"] == "fp32":
+        achieved, peak, unit = kernel_rate * cfg["flop"] / 1e12, peak32, "TFLOP/s"
+        peak_src = "FFMA probe measured in this run"
+    else:
+        achieved, peak, unit = kernel_rate * cfg["flop"] / 1e12, peak64, "TFLOP/s"
+        peak_src = ("DFMA probe measured in this run (MEASURED_PEAKS.json has no FP64 figure); "
+                    "nominal 148 SM x 64 x 2 x 1.965 GHz = 37.2")
+        if args.config == "cfg0":
+            peak = peak64 / 148.0
+            peak_src = "one SM's share of the DFMA probe (a single wall is one dependency chain per step)"
 
-    # e2e through the public API with host buffers (pinned), H2D + D2H inside
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and R.shard is None:
         host = {k: np.ascontiguousarray(v) for k, v in w.init.items()}
         out = {k: np.empty_like(host[k]) for k in ("u_prev", "u_curr", "v_prev", "v_curr")}
         pinned = list(host.values()) + list(out.values())
+        lib = api.load_library()
         for a in pinned:
-            api.load_library().hyg_host_register(a.ctypes.data, a.nbytes)
+            lib.hyg_host_register(a.ctypes.data, a.nbytes)
         e2e_steps = max(1, min(args.steps, 3))
         barrier()
         ctx.synchronize()
         ctx.record(2)
         for _ in range(e2e_steps):
             ctx.set_state(**host)
-            ctx.bootstrap(w.boot)
-            ctx.advance(nsteps - 1)
+            if w.boot != "none":
+                ctx.bootstrap(w.boot)
+            for n, d in run_steps_of(w):
+                ctx.advance(n, d)
             ctx.get_state(out)
         ctx.record(3)
         ms_e2e = max_over_ranks(ctx.elapsed_ms(2, 3))
         for a in pinned:
-            api.load_library().hyg_host_unregister(a.ctypes.data)
-        b = 4 * w.cells * 8
-        e2e = {"value": float(w.cells) * nsteps * e2e_steps * world / (ms_e2e * 1e-3), "unit": UNIT,
+            lib.hyg_host_unregister(a.ctypes.data)
+        b = 4 * w.cells * 8 + 2 * len(w.model.zones) * 8 * ("zone_u" in host)
+        e2e = {"value": float(w.cells) * w.nsteps * e2e_steps * world / (ms_e2e * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": b, "d2h_bytes_per_step": b,
                "path": "Context.set_state -> bootstrap -> advance -> get_state (hyg_* C ABI), pinned host buffers"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = len(os.sched_getaffinity(0))
-        sample = max(1, int(4e8 // w.cells))
-        r, sec, kind = cpu_reference_rate(w, sample, threads)
-        ri, seci, _ = cpu_reference_rate(w, max(1, sample // 4), threads, implicit=True)
-        cpu = {"value": r, "unit": UNIT, "cores": threads, "kind": kind,
-               "sample": f"all {w.model.n_walls} walls x {sample} DF steps ({sec:.1f} s)",
-               "implicit_value": ri,
-               "implicit_sample": f"all walls x {max(1, sample // 4)} Euler-implicit steps ({seci:.1f} s)"}
+        r, sample, kind, imp = cpu_reference_rate(args, w, threads)
+        cpu = {"value": r, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample}
+        if imp:
+            cpu["implicit_value"], cpu["implicit_sample"] = imp
 
     traffic = None
-    tf = ROOT / "profiles" / "k1_traffic.json"
+    tf = ROOT / "profiles" / f"{top['name']}_traffic.json"
     if tf.exists():
         try:
             traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
@@ -296,18 +427,17 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
-                "config": workload_config(args, world),
-                "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": fp64_peak, "unit": "TFLOP/s",
-                             "frac": achieved_tf / fp64_peak, "traffic": traffic,
+                "scaling": "strong" if cfg["scaling"] == "strong" else "weak", "vs_baseline": None,
+                "dtype": cfg["dtype"], "data": "synthetic (seeded)", "config": workload_config(args, w, world),
+                "roofline": {"bound": cfg["bound"], "achieved": achieved, "peak": peak, "unit": unit,
+                             "frac": achieved / peak if peak else None, "traffic": traffic,
                              "kernel": top["name"], "kernel_share_of_step": share,
-                             "flop_per_update": FLOP_PER_UPDATE,
-                             "peak_source": "DFMA probe measured in this run (MEASURED_PEAKS.json has no FP64 figure); "
-                                            "nominal 148 SM x 64 x 2 x 1.965 GHz = 37.2",
-                             "kernel_node_updates_per_s": kernel_rate},
+                             "flop_per_update": cfg["flop"], "bytes_per_update": cfg["bytes"],
+                             "peak_source": peak_src, "kernel_node_updates_per_s": kernel_rate},
                 "clocks": clk, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
-    ctx.close()
+    if R.shard is None:
+        ctx.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -207,6 +207,15 @@ int hyg_restore(hyg_ctx* ctx);
 int hyg_set_channel_table(hyg_ctx* ctx, int32_t channel, int64_t first_layer,
                           int64_t n_layers, const hyg_ambient* values);
 
+/* Per-layer overrides of the zone source schedules (source `source`:
+ * values [n_layers][3] = g_o, q_o, q_h) and of the outdoor signals
+ * (values [n_layers][2] = u, v), same layer convention as channel tables.
+ * With these, a caller holding opaque Signal objects (signal.hpp exposes only
+ * operator()(t)) evaluates them itself at the layer times. */
+int hyg_set_source_table(hyg_ctx* ctx, int32_t source, int64_t first_layer, int64_t n_layers,
+                         const double* values);
+int hyg_set_outdoor_table(hyg_ctx* ctx, int64_t first_layer, int64_t n_layers, const double* values);
+
 /* One starting step producing layer 1 from layer 0 (run() counts it as step 1,
  * building.cpp:317-323).  Guarded like every step. */
 int hyg_bootstrap(hyg_ctx* ctx, int32_t kind, hyg_status* status);
@@ -262,6 +271,8 @@ int64_t hyg_launch_count(hyg_ctx* ctx);
 
 /* Device FP64 FMA throughput probe (DFMA loop), TFLOP/s counting FMA = 2. */
 int hyg_probe_fp64_peak(int32_t device, double* tflops, double* sm_clock_mhz);
+/* Device FP32 FMA throughput probe (FFMA loop), TFLOP/s counting FMA = 2. */
+int hyg_probe_fp32_peak(int32_t device, double* tflops);
 
 #ifdef __cplusplus
 }

@@ -106,6 +106,8 @@ PROTOTYPES = {
     "hyg_snapshot": (C.c_int, [C.c_void_p]),
     "hyg_restore": (C.c_int, [C.c_void_p]),
     "hyg_set_channel_table": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.POINTER(Ambient)]),
+    "hyg_set_source_table": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, dp]),
+    "hyg_set_outdoor_table": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, dp]),
     "hyg_bootstrap": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Status)]),
     "hyg_advance": (C.c_int, [C.c_void_p, C.c_int64, C.c_double, C.POINTER(Status)]),
     "hyg_run": (C.c_int, [C.c_void_p, C.c_double, C.c_double, C.c_int32, FRAME_FN, C.c_void_p, C.POINTER(Status)]),
@@ -120,6 +122,7 @@ PROTOTYPES = {
     "hyg_reset_kernel_stats": (C.c_int, [C.c_void_p]),
     "hyg_launch_count": (C.c_int64, [C.c_void_p]),
     "hyg_probe_fp64_peak": (C.c_int, [C.c_int32, dp, dp]),
+    "hyg_probe_fp32_peak": (C.c_int, [C.c_int32, dp]),
     "hyg_saturation_pressure": (C.c_int, [C.c_double, dp]),
     "hyg_scale_wall": (C.c_int, [dp, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                  C.c_double, C.c_double, C.c_double, C.POINTER(WallGroups), C.POINTER(FaceBiot)]),

@@ -440,6 +440,12 @@ def scale_interzone(ach, volume, rho_a=1.0, c_pa=1005.0, c_pv=1960.0, T_i=293.15
     return tuple(out)
 
 
+def probe_fp32_peak(device: int = 0) -> float:
+    tf = C.c_double()
+    _check(load_library().hyg_probe_fp32_peak(device, C.byref(tf)), None, "probe_fp32_peak")
+    return tf.value
+
+
 def probe_fp64_peak(device: int = 0) -> float:
     tf, mhz = C.c_double(), C.c_double()
     _check(load_library().hyg_probe_fp64_peak(device, C.byref(tf), C.byref(mhz)), None, "probe_fp64_peak")

@@ -77,6 +77,16 @@ struct ChannelHost {
     }
 };
 
+// explicit per-layer values (zone sources: 3 per layer, outdoor: 2 per layer)
+struct TableHost {
+    int64_t first = 0;
+    int width = 1;
+    std::vector<double> v;
+    bool covers(int64_t L) const {
+        return !v.empty() && L >= first && L < first + static_cast<int64_t>(v.size() / width);
+    }
+};
+
 struct Pending { int stat; cudaEvent_t e0, e1; double updates; };
 struct Stat { std::string name; int64_t launches = 0; double ms = 0, updates = 0; };
 
@@ -113,6 +123,8 @@ struct hyg_ctx {
     std::vector<InzLinkDev> inz;
     std::vector<SigHost> zsrc;    // [n_sources*3]: g_o, q_o, q_h
     SigHost out_u, out_v;
+    std::vector<TableHost> src_tab;   // [n_sources] overrides (hyg_set_source_table)
+    TableHost out_tab;                // outdoor override (hyg_set_outdoor_table)
     double dt = 1e-3, norm = 1e3, eta_factor = 1e-2;
     int max_subiters = 100;
     // device state (ping-pong)
@@ -300,15 +312,29 @@ int upload_table(hyg_ctx* c, int64_t layer0, const std::vector<double>& times, h
 }
 
 // zone sources + outdoor per step: [rows][n_src*3 + 2]
-int upload_src(hyg_ctx* c, const std::vector<double>& times, hyg_status* status) {
+// zone sources + outdoor, rows for layers [layer0, layer0 + times.size())
+int upload_src(hyg_ctx* c, int64_t layer0, const std::vector<double>& times, hyg_status* status) {
     const int nsrc = static_cast<int>(c->zsrc.size() / 3);
     const int w = nsrc * 3 + 2;
     c->h_src.resize(times.size() * w);
     for (size_t k = 0; k < times.size(); ++k) {
+        const int64_t L = layer0 + static_cast<int64_t>(k);
         double* r = &c->h_src[k * w];
-        for (int i = 0; i < nsrc * 3; ++i) r[i] = c->zsrc[i](times[k]);
-        r[nsrc * 3 + 0] = c->out_u(times[k]);
-        r[nsrc * 3 + 1] = c->out_v(times[k]);
+        for (int s = 0; s < nsrc; ++s) {
+            const TableHost& tb = c->src_tab[s];
+            if (tb.covers(L)) {
+                for (int i = 0; i < 3; ++i) r[3 * s + i] = tb.v[(L - tb.first) * 3 + i];
+            } else {
+                for (int i = 0; i < 3; ++i) r[3 * s + i] = c->zsrc[3 * s + i](times[k]);
+            }
+        }
+        if (c->out_tab.covers(L)) {
+            r[nsrc * 3 + 0] = c->out_tab.v[(L - c->out_tab.first) * 2 + 0];
+            r[nsrc * 3 + 1] = c->out_tab.v[(L - c->out_tab.first) * 2 + 1];
+        } else {
+            r[nsrc * 3 + 0] = c->out_u(times[k]);
+            r[nsrc * 3 + 1] = c->out_v(times[k]);
+        }
     }
     const size_t bytes = c->h_src.size() * sizeof(double);
     if (bytes > c->src_cap) {
@@ -405,7 +431,7 @@ int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
         int rc = upload_table(c, c->layer, times, status);
         if (rc) return rc;
         if (!c->zones.empty()) {
-            rc = upload_src(c, times, status);
+            rc = upload_src(c, c->layer, times, status);
             if (rc) return rc;
         }
         const int nch = std::max<int>(1, static_cast<int>(c->channels.size()));
@@ -843,6 +869,8 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
     }
     c->out_u.set(d->outdoor_u);
     c->out_v.set(d->outdoor_v);
+    c->src_tab.assign(d->n_zone_sources, TableHost{0, 3, {}});
+    c->out_tab.width = 2;
     c->fused = all_exterior && d->n_zones == 0 && d->coeff_kind == HYG_COEFF_CONSTANT && fused_grid(c->n);
     c->nl_fused = all_exterior && d->n_zones == 0 && d->coeff_kind == HYG_COEFF_ANALYTIC_D && c->n <= 1024 &&
                   c->precision == HYG_F64;
@@ -1121,6 +1149,21 @@ int hyg_set_channel_table(hyg_ctx* c, int32_t channel, int64_t first_layer, int6
     return HYG_OK;
 }
 
+int hyg_set_source_table(hyg_ctx* c, int32_t source, int64_t first_layer, int64_t n_layers,
+                         const double* values) {
+    if (!c || source < 0 || source >= static_cast<int>(c->src_tab.size()) || n_layers < 0 ||
+        (n_layers > 0 && !values))
+        return HYG_EINVAL;
+    c->src_tab[source] = TableHost{first_layer, 3, std::vector<double>(values, values + 3 * n_layers)};
+    return HYG_OK;
+}
+
+int hyg_set_outdoor_table(hyg_ctx* c, int64_t first_layer, int64_t n_layers, const double* values) {
+    if (!c || n_layers < 0 || (n_layers > 0 && !values)) return HYG_EINVAL;
+    c->out_tab = TableHost{first_layer, 2, std::vector<double>(values, values + 2 * n_layers)};
+    return HYG_OK;
+}
+
 int hyg_bootstrap(hyg_ctx* c, int32_t kind, hyg_status* status) {
     clear_status(status);
     if (!c) return HYG_EINVAL;
@@ -1151,7 +1194,7 @@ int hyg_bootstrap(hyg_ctx* c, int32_t kind, hyg_status* status) {
     const int nsrc = static_cast<int>(c->zsrc.size() / 3);
     if (!c->zones.empty()) {
         std::vector<double> tf{t_force};
-        rc = upload_src(c, tf, status);
+        rc = upload_src(c, c->layer + (kind == HYG_BOOT_EXPLICIT ? 0 : 1), tf, status);
         if (rc) return rc;
     }
     HYG_CUDA(cudaMemsetAsync(c->d_key, 0xff, sizeof(unsigned long long), c->stream));
@@ -1325,12 +1368,17 @@ int hyg_run(hyg_ctx* c, double horizon, double cadence, int32_t boot_kind, hyg_f
         return HYG_ESCHEMA;
     }
     const int64_t nsteps = std::llround(horizon / c->dt);
-    const int64_t stride = std::max<int64_t>(1, std::llround(cadence / c->dt));
+    // lround of a huge cadence overflows in the reference (UB); here a cadence
+    // beyond the horizon means initial and final frames only
+    const double strides = cadence / c->dt;
+    const int64_t stride = !(strides < 4.0e18) ? nsteps + 1 : std::max<int64_t>(1, std::llround(strides));
     if (frame) frame(user, c->layer, c->t, c);
     int64_t done = 0;
+    int boot_passes = 0;
     if (nsteps > 0) {
         const int rc = hyg_bootstrap(c, boot_kind, status);
         if (rc) return rc;
+        boot_passes = status ? status->subiterations : 0;
         ++done;
         if (frame && (done % stride == 0 || done == nsteps)) frame(user, c->layer, c->t, c);
     }
@@ -1341,6 +1389,7 @@ int hyg_run(hyg_ctx* c, double horizon, double cadence, int32_t boot_kind, hyg_f
         done += chunk;
         if (frame && (done % stride == 0 || done == nsteps)) frame(user, c->layer, c->t, c);
     }
+    if (status) status->subiterations = boot_passes;   // SimulationResult::bootstrap_subiters
     return HYG_OK;
 }
 
@@ -1417,6 +1466,50 @@ __global__ void k_dfma_probe(double* out, int iters) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
 }
 }  // namespace
+
+namespace {
+__global__ void k_ffma_probe(float* out, int iters) {
+    float a[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) a[k] = threadIdx.x * 1e-6f + k;
+    const float b = 0.9999f, c = 1e-4f;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int k = 0; k < 16; ++k) a[k] = fmaf(a[k], b, c);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s += a[k];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+}  // namespace
+
+extern "C" int hyg_probe_fp32_peak(int32_t device, double* tflops) {
+    hyg_status* status = nullptr;
+    HYG_CUDA(cudaSetDevice(device));
+    int sms = 0;
+    HYG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const int blocks = sms * 8, threads = 256, iters = 40000;
+    float* o = nullptr;
+    HYG_CUDA(cudaMalloc(&o, sizeof(float) * blocks * threads));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_ffma_probe<<<blocks, threads>>>(o, 200);
+    cudaEventRecord(e0);
+    k_ffma_probe<<<blocks, threads>>>(o, iters);
+    cudaEventRecord(e1);
+    HYG_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(o);
+    if (tflops) *tflops = 2.0 * 64.0 * iters * static_cast<double>(blocks) * threads / (ms * 1e-3) / 1e12;
+    return HYG_OK;
+}
 
 extern "C" int hyg_probe_fp64_peak(int32_t device, double* tflops, double* sm_clock_mhz) {
     hyg_status* status = nullptr;
