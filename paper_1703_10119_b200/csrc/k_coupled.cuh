@@ -121,8 +121,9 @@ __device__ __forceinline__ void coupled_step(Real (&vP)[NPT], Real (&vC)[NPT], R
     }
 }
 
-template <typename Real, int LPW, int NPT, int WARPS, int CHUNK, bool FLUX, bool EXACT>
-__global__ void __launch_bounds__(WARPS * 32)
+// MINB > 0 caps registers (launch_bounds min blocks per SM) for occupancy experiments.
+template <typename Real, int LPW, int NPT, int WARPS, int CHUNK, bool FLUX, bool EXACT, int MINB = 0>
+__global__ void __launch_bounds__(WARPS * 32, MINB)
 k_df_coupled(const CoupledSegArgs<Real> a) {
     constexpr bool DEV = sizeof(Real) == 4;   // fp32 state = deviations from 1
     constexpr int WALLS_PER_CTA = WARPS * 32 / LPW;

@@ -1,0 +1,134 @@
+// k1_variants.cu — layout/occupancy probe for K1 (not product code): times
+// k_df_coupled variants on cfg1-like random walls (65,536 x 256, 4096 steps)
+// and checks they agree with the production variant bit for bit.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <vector>
+
+#include "../paper_1703_10119_b200/csrc/k_coupled.cuh"
+
+using namespace hyg;
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
+    std::printf("CUDA %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); std::exit(1);} } while (0)
+
+__global__ void k_coef(int B, double dx, double dt, const Groups* g, const Biot* b, WallCoef* c) {
+    int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w < B) coupled_coef(g[w], dx, dt, b[2 * w], b[2 * w + 1], c[w]);
+}
+
+struct Bufs { double* in[4]; double* out[4]; };
+
+template <int LPW, int NPT, int WARPS, int MINB>
+float run(const char* name, CoupledSegArgs<double> a, Bufs& b, int B, int steps, std::vector<double>* result) {
+    constexpr int CHUNK = 128;
+    auto kern = k_df_coupled<double, LPW, NPT, WARPS, CHUNK, false, false, MINB>;
+    const int smem = CHUNK * a.n_channels * sizeof(Ambient);
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaFuncAttributes attr;
+    cudaFuncGetAttributes(&attr, kern);
+    const int wpc = WARPS * 32 / LPW;
+    const int grid = (B + wpc - 1) / wpc;
+    for (int k = 0; k < 4; ++k) { a.in[k] = b.in[k]; a.out[k] = b.out[k]; }
+    a.nsteps = steps;
+    kern<<<grid, WARPS * 32, smem>>>(a);   // warm-up
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    const int reps = 3;
+    for (int r = 0; r < reps; ++r) kern<<<grid, WARPS * 32, smem>>>(a);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    CK(cudaGetLastError());
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= reps;
+    const double rate = (double)B * 256 * steps / (ms * 1e-3);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, smem);
+    std::printf("%-22s regs %3d  warps/SM %2d  %.3f ms  %.3e upd/s  %.1f TF(14 flop)\n", name, attr.numRegs,
+                occ * WARPS, ms, rate, rate * 14 / 1e12);
+    if (result) {
+        result->resize((size_t)B * 256 * 4);
+        for (int k = 0; k < 4; ++k)
+            CK(cudaMemcpy(result->data() + (size_t)k * B * 256, b.out[k], (size_t)B * 256 * 8, cudaMemcpyDeviceToHost));
+    }
+    return ms;
+}
+
+int main(int argc, char** argv) {
+    const int B = 65536, n = 256, steps = argc > 1 ? atoi(argv[1]) : 4096;
+    const double dx = 1.0 / (n - 1), dt = 1e-3;
+    std::mt19937_64 rng(1);
+    auto lu = [&](double lo, double hi) {
+        std::uniform_real_distribution<double> d(std::log(lo), std::log(hi));
+        return std::exp(d(rng));
+    };
+    std::vector<Groups> g(B);
+    std::vector<Biot> bi(2 * B);
+    for (int w = 0; w < B; ++w) {
+        g[w] = Groups{lu(3.7e-5, 0.35), lu(0.018, 1.4), lu(1.1e-3, 10.4), lu(1.7e-5, 6.6e-3)};
+        bi[2 * w] = Biot{lu(200, 2e4), lu(1.25, 25), lu(0.1, 2.0)};
+        bi[2 * w + 1] = Biot{lu(30, 3e3), lu(0.4, 8), lu(0.01, 0.3)};
+    }
+    const int nch = 2;
+    std::vector<Ambient> tab((size_t)steps * nch);
+    double t = 0;
+    for (int s = 0; s < steps; ++s) {
+        tab[s * nch] = Ambient{1.0 + 0.02 * std::sin(2 * M_PI * t / 24), 1.0 + 0.2 * std::sin(2 * M_PI * t / 24), 0, 0};
+        tab[s * nch + 1] = Ambient{1.0, 1.0, 0, 0};
+        t += dt;
+    }
+    std::normal_distribution<double> nd(0.0, 0.01);
+    std::vector<double> init((size_t)B * n);
+    for (auto& x : init) x = 1.0 + nd(rng);
+    Groups* dg; Biot* db; WallCoef* dc; Ambient* dtab; int *dchan, *dflag; unsigned long long* dkey;
+    CK(cudaMalloc(&dg, B * sizeof(Groups)));
+    CK(cudaMalloc(&db, 2 * B * sizeof(Biot)));
+    CK(cudaMalloc(&dc, B * sizeof(WallCoef)));
+    CK(cudaMalloc(&dtab, tab.size() * sizeof(Ambient)));
+    CK(cudaMalloc(&dchan, 2 * B * sizeof(int)));
+    CK(cudaMalloc(&dflag, 4));
+    CK(cudaMalloc(&dkey, 8));
+    std::vector<int> chan(2 * B);
+    for (int w = 0; w < B; ++w) { chan[2 * w] = 0; chan[2 * w + 1] = 1; }
+    CK(cudaMemcpy(dg, g.data(), B * sizeof(Groups), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(db, bi.data(), 2 * B * sizeof(Biot), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dtab, tab.data(), tab.size() * sizeof(Ambient), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dchan, chan.data(), 2 * B * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemset(dflag, 0, 4));
+    k_coef<<<(B + 127) / 128, 128>>>(B, dx, dt, dg, db, dc);
+    Bufs b;
+    for (int k = 0; k < 4; ++k) {
+        CK(cudaMalloc(&b.in[k], (size_t)B * n * 8));
+        CK(cudaMalloc(&b.out[k], (size_t)B * n * 8));
+        CK(cudaMemcpy(b.in[k], init.data(), (size_t)B * n * 8, cudaMemcpyHostToDevice));
+    }
+    CoupledSegArgs<double> a{};
+    a.n_walls = B;
+    a.n_channels = nch;
+    a.divergence_norm = 1e3;
+    a.coef = dc;
+    a.chan = dchan;
+    a.table = dtab;
+    a.stop = dflag;
+    a.suspect = dflag;
+    a.fail_key = dkey;
+    std::vector<double> ref, got;
+    run<16, 16, 4, 0>("16x16 w4 (prod)", a, b, B, steps, &ref);
+    auto check = [&](const char* nm) {
+        double m = 0;
+        for (size_t i = 0; i < ref.size(); ++i) m = std::max(m, std::fabs(ref[i] - got[i]));
+        std::printf("    %s max |diff| vs prod %.3e\n", nm, m);
+    };
+    run<16, 16, 2, 0>("16x16 w2", a, b, B, steps, nullptr);
+    run<16, 16, 8, 0>("16x16 w8", a, b, B, steps, nullptr);
+    run<16, 16, 4, 3>("16x16 w4 minb3", a, b, B, steps, &got); check("minb3");
+    run<32, 8, 4, 0>("32x8 w4", a, b, B, steps, &got); check("32x8");
+    run<32, 8, 4, 4>("32x8 w4 minb4", a, b, B, steps, nullptr);
+    run<32, 8, 2, 8>("32x8 w2 minb8", a, b, B, steps, nullptr);
+    run<8, 32, 4, 1>("8x32 w4", a, b, B, steps, nullptr);
+    return 0;
+}
