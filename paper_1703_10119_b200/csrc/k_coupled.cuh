@@ -191,35 +191,51 @@ k_df_coupled(const CoupledSegArgs<Real> a) {
         }
     };
     int failed_at = -1;      // exact mode: steps completed when the guard failed
+    // Exact mode: a wall group that fails stores the failing layer pair at once
+    // and is then frozen, but keeps stepping in lockstep — the other wall group
+    // of the warp still needs its lanes in every full-mask shuffle and ballot.
+    auto store = [&](const Real (&u0)[NPT], const Real (&u1)[NPT], const Real (&v0)[NPT],
+                     const Real (&v1)[NPT]) {
+        if (!active) return;
+#pragma unroll
+        for (int j = 0; j < NPT; ++j) {
+            const size_t i = base + (rev ? NPT - 1 - j : j);
+            a.out[0][i] = u0[j];
+            a.out[1][i] = u1[j];
+            a.out[2][i] = v0[j];
+            a.out[3][i] = v1[j];
+        }
+    };
 
     for (int c0s = 0; c0s < a.nsteps; c0s += CHUNK) {
         const int clen = min(CHUNK, a.nsteps - c0s);
         __syncthreads();
         for (int i = tid; i < clen * nch; i += WARPS * 32) s_tab[i] = a.table[(size_t)c0s * nch + i];
         __syncthreads();
-        if (failed_at >= 0) continue;   // keep the barrier count, no work
         int s = 0;
         // two steps per iteration: the layer rotation is a register renaming
         for (; s + 1 < clen; s += 2) {
             coupled_step<Real, LPW, NPT, FLUX, EXACT>(vp, vc, up, uc, ci, c0, amb(s), mirror0, rev, acc,
                                                       bad, norm);
-            if (EXACT && group_bad(bad)) {
-                swap_layers();           // curr := the failing layer
+            if (EXACT && failed_at < 0 && group_bad(bad)) {
                 failed_at = c0s + s + 1;
-                break;
+                store(uc, up, vc, vp);   // after this step curr lives in the P registers
             }
             coupled_step<Real, LPW, NPT, FLUX, EXACT>(vc, vp, uc, up, ci, c0, amb(s + 1), mirror0, rev,
                                                       acc, bad, norm);
-            if (EXACT && group_bad(bad)) {
+            if (EXACT && failed_at < 0 && group_bad(bad)) {
                 failed_at = c0s + s + 2;
-                break;
+                store(up, uc, vp, vc);
             }
         }
-        if (failed_at < 0 && s < clen) {   // odd tail (last chunk only)
+        if (s < clen) {   // odd tail (last chunk only)
             coupled_step<Real, LPW, NPT, FLUX, EXACT>(vp, vc, up, uc, ci, c0, amb(s), mirror0, rev, acc,
                                                       bad, norm);
             swap_layers();
-            if (EXACT && group_bad(bad)) failed_at = c0s + s + 1;
+            if (EXACT && failed_at < 0 && group_bad(bad)) {
+                failed_at = c0s + s + 1;
+                store(up, uc, vp, vc);
+            }
         }
     }
     if (EXACT && failed_at >= 0 && active && first) {
@@ -233,16 +249,7 @@ k_df_coupled(const CoupledSegArgs<Real> a) {
         const unsigned any = __reduce_or_sync(0xffffffffu, active ? acc : 0u);
         if ((any & 0x40000000u) && (tid % 32) == 0) atomicCAS(a.suspect, 0, a.seg_index + 1);
     }
-    if (active) {
-#pragma unroll
-        for (int j = 0; j < NPT; ++j) {
-            const size_t i = base + (rev ? NPT - 1 - j : j);
-            a.out[0][i] = up[j];
-            a.out[1][i] = uc[j];
-            a.out[2][i] = vp[j];
-            a.out[3][i] = vc[j];
-        }
-    }
+    if (failed_at < 0) store(up, uc, vp, vc);
 }
 
 }  // namespace hyg
