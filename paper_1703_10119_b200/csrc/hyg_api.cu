@@ -21,6 +21,7 @@
 #include "k_coupled.cuh"
 #include "k_step.cuh"
 #include "k_nonlinear.cuh"
+#include "k_tiled.cuh"
 
 using namespace hyg;
 
@@ -173,6 +174,7 @@ struct hyg_ctx {
     // dispatch
     bool fused = false;        // K1: constant exterior walls on a fused grid
     bool nl_fused = false;     // K2: analytic d(v) exterior walls, n <= 1024
+    bool tiled = false;        // K3: one long analytic d(v) exterior wall, n > 1024
     bool flux = true;
     int seg_len = 4096;
     // measurement
@@ -370,6 +372,7 @@ StepArgs step_args(hyg_ctx* c, int from, double dt) {
     a.fail_key = c->d_key;
     a.own0 = c->own_c0;
     a.own1 = c->own_c1;
+    a.coef = c->d_coef;
     return a;
 }
 
@@ -419,6 +422,12 @@ int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
         return HYG_ENOTSUP;
     }
     const int64_t block = 65536;     // forcing rows per upload
+    if (c->coeff_kind == HYG_COEFF_CONSTANT && c->coef_dt != dt) {
+        LaunchScope ls(c, "coupled_coef", 0.0);
+        k_coupled_coef<<<(c->n_walls + 127) / 128, 128, 0, c->stream>>>(c->n_walls, c->dx, dt, c->d_groups,
+                                                                         c->d_biot, c->d_coef);
+        c->coef_dt = dt;
+    }
     HYG_CUDA(cudaMemsetAsync(c->d_key, 0xff, sizeof(unsigned long long), c->stream));
     for (int64_t done = 0; done < nsteps;) {
         const int64_t rows = std::min(block, nsteps - done);
@@ -691,6 +700,73 @@ int advance_nonlinear(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status)
     return HYG_OK;
 }
 
+// ---- the temporally blocked long-wall path (K3, analytic d(v), one wall) ----------
+constexpr int kTileT = 1024, kTileS = 16, kTileThreads = 256;
+
+int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
+    const int nch = std::max<int>(1, static_cast<int>(c->channels.size()));
+    const int64_t block = 1 << 18;
+    for (int64_t done = 0; done < nsteps;) {
+        const int64_t rows = std::min(block, nsteps - done);
+        std::vector<double> times(rows);
+        double t = c->t;
+        for (int64_t k = 0; k < rows; ++k) {
+            times[k] = t;
+            t += dt;
+        }
+        int rc = upload_table(c, c->layer, times, status);
+        if (rc) return rc;
+        HYG_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+        TiledArgs a{};
+        a.n = c->n;
+        a.n_channels = nch;
+        a.chl = c->attach[0].index;
+        a.chr = c->attach[1].index;
+        a.dx = c->dx;
+        a.dt = dt;
+        for (int i = 0; i < 4; ++i) a.p[i] = c->p[i];
+        a.groups = c->groups[0];
+        a.bl = c->biot[0];
+        a.br = c->biot[1];
+        a.stop = c->d_flag;
+        a.suspect = c->d_flag;
+        const int grid = static_cast<int>((c->n + kTileT - 1) / kTileT);
+        const int smem = 5 * (kTileT + 2 * kTileS) * static_cast<int>(sizeof(double));
+        const int cur0 = c->cur;
+        int nseg = 0;
+        for (int64_t s0 = 0; s0 < rows; s0 += kTileS, ++nseg) {
+            a.steps = static_cast<int>(std::min<int64_t>(kTileS, rows - s0));
+            a.seg_index = nseg;
+            a.table = c->d_table + s0 * nch;
+            const int from = (cur0 + nseg) & 1;
+            for (int i = 0; i < 4; ++i) {
+                a.in[i] = c->s64[from][i];
+                a.out[i] = c->s64[1 - from][i];
+            }
+            LaunchScope ls(c, "df_analytic_tiled", static_cast<double>(c->cells()) * a.steps);
+            k_df_analytic_tiled<kTileT, kTileS, kTileThreads><<<grid, kTileThreads, smem, c->stream>>>(a);
+        }
+        HYG_CUDA(cudaGetLastError());
+        int flag = 0;
+        HYG_CUDA(cudaMemcpyAsync(&flag, c->d_flag, sizeof flag, cudaMemcpyDeviceToHost, c->stream));
+        HYG_CUDA(cudaStreamSynchronize(c->stream));
+        if (flag == 0) {
+            c->cur = (cur0 + nseg) & 1;
+            c->t = t;
+            c->layer += rows;
+            done += rows;
+            continue;
+        }
+        // fast guard fired in launch K (input intact): exact per-step path from there
+        const int64_t k0 = static_cast<int64_t>(flag - 1) * kTileS;
+        c->cur = (cur0 + flag - 1) & 1;
+        c->t = times[k0];
+        c->layer += k0;
+        return advance_general(c, nsteps - done - k0, dt, status);
+    }
+    return HYG_OK;
+}
+
 int advance_fused(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
     if (c->precision == HYG_F32) return advance_fused_t<float>(c, c->s32, nsteps, dt, status);
     return advance_fused_t<double>(c, c->s64, nsteps, dt, status);
@@ -874,6 +950,8 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
     c->fused = all_exterior && d->n_zones == 0 && d->coeff_kind == HYG_COEFF_CONSTANT && fused_grid(c->n);
     c->nl_fused = all_exterior && d->n_zones == 0 && d->coeff_kind == HYG_COEFF_ANALYTIC_D && c->n <= 1024 &&
                   c->precision == HYG_F64;
+    c->tiled = all_exterior && d->n_zones == 0 && d->coeff_kind == HYG_COEFF_ANALYTIC_D && c->n > 1024 &&
+               c->n_walls == 1 && c->precision == HYG_F64;
     if (c->precision == HYG_F32 && !c->fused) {
         delete c;
         set_status(status, HYG_ENOTSUP, "fp32 state is implemented for exterior constant walls on fused grids only");
@@ -1087,7 +1165,7 @@ int hyg_set_owned(hyg_ctx* c, int64_t cell0, int64_t cell1, int32_t zone0, int32
     c->reduce_user = user;
     // the fused kernels guard every wall: a shard with a partial ownership
     // marches on the per-step path, whose guard honours the owned range
-    if (cell0 > 0 || cell1 < c->cells()) c->fused = c->nl_fused = false;
+    if (cell0 > 0 || cell1 < c->cells()) c->fused = c->nl_fused = c->tiled = false;
     return HYG_OK;
 }
 
@@ -1354,6 +1432,7 @@ int hyg_advance(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
     if (!(dt > 0.0)) dt = c->dt;
     int rc = c->fused      ? advance_fused(c, nsteps, dt, status)
              : c->nl_fused ? advance_nonlinear(c, nsteps, dt, status)
+             : c->tiled    ? advance_tiled(c, nsteps, dt, status)
                            : advance_general(c, nsteps, dt, status);
     if (status && rc == HYG_OK) status->code = HYG_OK;
     return rc;

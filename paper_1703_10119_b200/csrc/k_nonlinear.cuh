@@ -52,6 +52,48 @@ __device__ __forceinline__ double d_of(const double* p, double v) {
 
 constexpr int kNlChunk = 64;   // forcing rows staged per chunk
 
+// Per-wall scalars of the d(v) rows (wall.cpp:199-204).
+struct AnalyticRow { double a, b, g, gamma, ratio, dx, inv_u; };
+
+__device__ __forceinline__ AnalyticRow analytic_row(const Groups& g, double dx, double dt) {
+    AnalyticRow r;
+    r.a = g.Fo_M * dt / (dx * dx);
+    r.b = g.Fo_TT * dt / (dx * dx);
+    r.g = g.Fo_TM * g.gamma * dt / (dx * dx);
+    r.gamma = g.gamma;
+    r.ratio = g.Fo_TT != 0.0 ? g.Fo_TM * g.gamma / g.Fo_TT : 0.0;
+    r.dx = dx;
+    r.inv_u = 1.0 / (1.0 + 2.0 * r.b);
+    return r;
+}
+
+// Interior node (wall.cpp:213-217, 231-240) with half-node coefficients km, kp.
+__device__ __forceinline__ void analytic_interior(const AnalyticRow& r, double vp, double up, double vL,
+                                                  double vR, double uL, double uR, double km, double kp,
+                                                  double& vn, double& un) {
+    vn = vp + 2.0 * r.a * (kp * (vR - vp) + km * (vL - vp)) / (1.0 + r.a * (kp + km));
+    un = up + (2.0 * r.b * (uR + uL - 2.0 * up) + 2.0 * r.g * (vR + vL - vn - vp) - r.gamma * (vn - vp)) *
+                  r.inv_u;
+}
+
+// Face node (wall.cpp:218-229, 241-259): jn = interior neighbour, km_b = node
+// value d(v_face) (ghost side), kp_b = half-node value next to the face.
+__device__ __forceinline__ void analytic_face(const AnalyticRow& r, const Biot& fb, const Ambient& am,
+                                              double vp, double up, double vcn, double ucn, double km_b,
+                                              double kp_b, double& vn, double& un) {
+    const double S = kp_b + km_b;
+    const double cpl = 2.0 * r.a * r.dx * fb.Bi_M;
+    vn = vp + (2.0 * r.a * S * (vcn - vp) + 2.0 * cpl * (am.v - vp) + 4.0 * r.a * r.dx * am.g) /
+                  (1.0 + r.a * S + cpl);
+    const double vbar = 0.5 * (vn + vp);
+    const double vg = vcn - (2.0 * r.dx / km_b) * (fb.Bi_M * (vbar - am.v) - am.g);
+    const double cplu = 2.0 * r.b * r.dx * fb.Bi_TT;
+    un = up + (4.0 * r.b * (ucn - up) + 2.0 * cplu * (am.u - up) - r.gamma * (vn - vp) +
+               2.0 * r.b * r.ratio * (vcn - vg) - 4.0 * r.b * r.dx * (fb.Bi_TM * (vbar - am.v) - am.q) +
+               2.0 * r.g * (vcn + vg) - 2.0 * r.g * (vn + vp)) /
+                  (1.0 + 2.0 * r.b + cplu);
+}
+
 template <int MAXN>
 __global__ void __launch_bounds__(32) k_df_analytic_walls(const NonlinearSegArgs A) {
     __shared__ double s_lay[4][MAXN];            // up, uc, vp, vc (roles rotate)
@@ -67,11 +109,7 @@ __global__ void __launch_bounds__(32) k_df_analytic_walls(const NonlinearSegArgs
     }
     const Groups g = A.groups[w];
     const double dx = A.dx, dt = A.dt;
-    const double a = g.Fo_M * dt / (dx * dx);                  // wall.cpp:201-204
-    const double b = g.Fo_TT * dt / (dx * dx);
-    const double gg = g.Fo_TM * g.gamma * dt / (dx * dx);
-    const double ratio = g.Fo_TT != 0.0 ? g.Fo_TM * g.gamma / g.Fo_TT : 0.0;
-    const double inv_u = 1.0 / (1.0 + 2.0 * b);
+    const AnalyticRow rc = analytic_row(g, dx, dt);
     const Biot bl = A.biot[2 * w], br = A.biot[2 * w + 1];
     const int chl = A.chan[2 * w], chr = A.chan[2 * w + 1];
     double p[4] = {A.p[0], A.p[1], A.p[2], A.p[3]};
@@ -95,31 +133,15 @@ __global__ void __launch_bounds__(32) k_df_analytic_walls(const NonlinearSegArgs
                 const double vpj = vp[j], upj = up[j], vcj = vc[j];
                 double vn, un;
                 if (j > 0 && j < n - 1) {
-                    const double vL = vc[j - 1], vR = vc[j + 1], uL = uc[j - 1], uR = uc[j + 1];
-                    const double kp = d_of(p, 0.5 * (vcj + vR));
-                    const double km = d_of(p, 0.5 * (vL + vcj));
-                    vn = vpj + 2.0 * a * (kp * (vR - vpj) + km * (vL - vpj)) / (1.0 + a * (kp + km));
-                    un = upj + (2.0 * b * (uR + uL - 2.0 * upj) + 2.0 * gg * (vR + vL - vn - vpj) -
-                                g.gamma * (vn - vpj)) * inv_u;
+                    const double vL = vc[j - 1], vR = vc[j + 1];
+                    analytic_interior(rc, vpj, upj, vL, vR, uc[j - 1], uc[j + 1],
+                                      d_of(p, 0.5 * (vL + vcj)), d_of(p, 0.5 * (vcj + vR)), vn, un);
                 } else {
                     const bool left = j == 0;
                     const int jn = left ? 1 : n - 2;
-                    const Biot fb = left ? bl : br;
-                    const Ambient am = s_amb[s][left ? 0 : 1];
-                    const double vcn = vc[jn], ucn = uc[jn];
-                    const double km_b = d_of(p, vcj);                  // ghost side: node value
-                    const double kp_b = d_of(p, 0.5 * (vcj + vcn));    // half_front / half_back
-                    const double S = kp_b + km_b;
-                    const double cpl = 2.0 * a * dx * fb.Bi_M;
-                    vn = vpj + (2.0 * a * S * (vcn - vpj) + 2.0 * cpl * (am.v - vpj) + 4.0 * a * dx * am.g) /
-                                   (1.0 + a * S + cpl);
-                    const double vbar = 0.5 * (vn + vpj);
-                    const double vg = vcn - (2.0 * dx / km_b) * (fb.Bi_M * (vbar - am.v) - am.g);
-                    const double cplu = 2.0 * b * dx * fb.Bi_TT;
-                    un = upj + (4.0 * b * (ucn - upj) + 2.0 * cplu * (am.u - upj) - g.gamma * (vn - vpj) +
-                                2.0 * b * ratio * (vcn - vg) - 4.0 * b * dx * (fb.Bi_TM * (vbar - am.v) - am.q) +
-                                2.0 * gg * (vcn + vg) - 2.0 * gg * (vn + vpj)) /
-                               (1.0 + 2.0 * b + cplu);
+                    const double vcn = vc[jn];
+                    analytic_face(rc, left ? bl : br, s_amb[s][left ? 0 : 1], vpj, upj, vcn, uc[jn],
+                                  d_of(p, vcj), d_of(p, 0.5 * (vcj + vcn)), vn, un);
                 }
                 acc |= static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn));
                 vp[j] = vn;     // layer n-1 slot becomes layer n+1

@@ -38,6 +38,7 @@ struct StepArgs {
     double norm;
     unsigned long long* fail_key;
     int64_t own0, own1;         // cells whose guard/residual count (a shard owns a range)
+    const WallCoef* coef;       // constant walls: per-wall rows for this dt (k_coupled_coef)
 };
 
 // d(v) functor of HYG_COEFF_ANALYTIC_D: k_M* = 1 + p0 v + p1 exp(-p2 (v - p3)^2)
@@ -66,38 +67,31 @@ __device__ __forceinline__ FaceVals resolve(const StepArgs& a, int w, int k) {
     return f;
 }
 
-// df_step_coupled (wall.cpp:144-194), one node per thread, literal form.
+// df_step_coupled (wall.cpp:144-194), one node per thread, in the increment
+// form of hyg_coef.cuh with the per-wall coefficients of this dt (a.coef):
+// the same arithmetic as K1, so fused and per-step marches agree, and no
+// divisions per node (the per-step path stays HBM-bound, 48 B/update).
 __device__ __forceinline__ void coupled_node(const StepArgs& a, int w, int j, double& un,
                                              double& vn) {
     const int n = a.n;
-    const double dx = a.dx, dt = a.dt;
-    const Groups p = a.groups[w];
     const size_t o = static_cast<size_t>(w) * n;
     const double *up = a.in[0] + o, *uc = a.in[1] + o, *vp = a.in[2] + o, *vc = a.in[3] + o;
-    const double lam = 2.0 * p.Fo_M * dt / (dx * dx);
-    const double mu = 2.0 * p.Fo_TT * dt / (dx * dx);
-    const double beta = 2.0 * p.Fo_TM * p.gamma * dt / (dx * dx);
-    const double ratio = p.Fo_TT != 0.0 ? p.Fo_TM * p.gamma / p.Fo_TT : 0.0;
-    if (j > 0 && j < n - 1) {
-        vn = ((1.0 - lam) * vp[j] + lam * (vc[j + 1] + vc[j - 1])) / (1.0 + lam);
-        un = ((1.0 - mu) * up[j] + mu * (uc[j + 1] + uc[j - 1]) + (p.gamma - beta) * vp[j] +
-              beta * (vc[j + 1] + vc[j - 1]) - (p.gamma + beta) * vn) /
-             (1.0 + mu);
+    const bool face = j == 0 || j == n - 1;
+    const int jl = j == 0 ? 1 : j - 1, jr = j == n - 1 ? n - 2 : j + 1;   // mirrored at faces
+    const double vpj = vp[j], upj = up[j];
+    const double d = fma(-2.0, vpj, vc[jl] + vc[jr]);
+    const double du = fma(-2.0, upj, uc[jl] + uc[jr]);
+    if (!face) {
+        const RowCoef& c = a.coef[w].in;
+        vn = fma(c.b, d, vpj);
+        un = fma(c.c_sv, d, fma(c.c_su, du, upj));
         return;
     }
-    const int k = j == 0 ? 0 : 1;
-    const int jn = j == 0 ? 1 : n - 2;
-    const FaceVals b = resolve(a, w, k);
-    const double cpl = lam * dx * b.Bi_M;
-    vn = ((1.0 - lam - cpl) * vp[j] + 2.0 * lam * vc[jn] + 2.0 * lam * dx * (b.Bi_M * b.v_inf + b.g_inf)) /
-         (1.0 + lam + cpl);
-    const double vbar = 0.5 * (vn + vp[j]);
-    const double vg = vc[jn] - 2.0 * dx * (b.Bi_M * (vbar - b.v_inf) - b.g_inf);
-    const double cplu = mu * dx * b.Bi_TT;
-    un = ((1.0 - mu - cplu) * up[j] + 2.0 * mu * uc[jn] + mu * ratio * (vc[jn] - vg) +
-          2.0 * mu * dx * (b.Bi_TT * b.u_inf - b.Bi_TM * (vbar - b.v_inf) + b.q_inf) +
-          (p.gamma - beta) * vp[j] + beta * (vc[jn] + vg) - (p.gamma + beta) * vn) /
-         (1.0 + mu + cplu);
+    const RowCoef& c = a.coef[w].face[j == 0 ? 0 : 1];
+    const FaceVals b = resolve(a, w, j == 0 ? 0 : 1);
+    const double t = b.v_inf - vpj, tu = b.u_inf - upj;
+    vn = fma(c.e, t, fma(c.b, d, fma(c.e_g, b.g_inf, vpj)));
+    un = fma(c.c_tv, t, fma(c.c_sv, d, fma(c.c_tu, tu, fma(c.c_su, du, fma(c.c_q, b.q_inf, fma(c.c_g, b.g_inf, upj))))));
 }
 
 // df_step_nonlinear (wall.cpp:196-264) for the analytic functor (k_M* = d(v),

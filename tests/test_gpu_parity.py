@@ -107,6 +107,29 @@ def test_cfg4_long_domain_reduced():
     assert err <= TOL64, err
 
 
+@pytest.mark.parametrize("n_nodes,steps", [(1025, 37), (3000, 50), ((1 << 16) + 7, 33)])
+def test_tiled_long_wall_edges(n_nodes, steps):
+    """K3 (temporal blocking): tiles not dividing N, steps not dividing S,
+    a face inside the first and the last tile."""
+    w = workloads.long_domain(n_nodes=n_nodes, nsteps=steps)
+    got = gpu_run(w.model, w.init, steps, w.boot)
+    ref = oracle_run("oracle", w.model, w.init, steps, w.boot, nthreads=1)
+    assert rel_linf(got, ref) <= TOL64
+
+
+def test_nonlinear_fast_guard_fallback():
+    """|v| >= 2 in a nonlinear wall: K2/K3's fast guard fires, the march
+    continues on the per-step kernel with the exact guard, same result."""
+    for n in (101, 4000):
+        w = workloads.long_domain(n_nodes=n, nsteps=300)
+        for k in FIELDS:
+            w.init[k] = w.init[k].copy()
+            w.init[k][n // 2: n // 2 + 5] += 1.2
+        got = gpu_run(w.model, w.init, 300, "none")
+        ref = oracle_run("oracle", w.model, w.init, 300, "none", nthreads=1)
+        assert rel_linf(got, ref) <= TOL64, n
+
+
 def test_cfg4_full_size_short_horizon():
     """configs[4] at the full N = 2^26.  After k DF steps node j depends only on
     nodes j-k..j+k (three-level stencil), so windows of 2^14 nodes at both
