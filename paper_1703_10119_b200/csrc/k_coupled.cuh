@@ -74,7 +74,7 @@ template <typename Real> struct StepAmb { Real u_inf, v_inf, ev, eu; };
 
 // One fused DF step for this lane's NPT nodes.  P holds layer n-1 on entry
 // and layer n+1 on exit; C holds layer n.
-template <typename Real, int LPW, int NPT, bool FLUX, bool EXACT>
+template <typename Real, int LPW, int NPT, bool FLUX, bool EXACT, bool EDGE_FIRST = false>
 __device__ __forceinline__ void coupled_step(Real (&vP)[NPT], Real (&vC)[NPT], Real (&uP)[NPT],
                                              Real (&uC)[NPT], const InRow<Real>& ci,
                                              const FaceRow<Real>& c0, const StepAmb<Real>& am,
@@ -94,7 +94,9 @@ __device__ __forceinline__ void coupled_step(Real (&vP)[NPT], Real (&vC)[NPT], R
     const Real vx1 = rev ? vup : vdn;
     const Real ux1 = rev ? uup : udn;
 #pragma unroll
-    for (int j = 0; j < NPT; ++j) {
+    for (int jj = 0; jj < NPT; ++jj) {
+        // EDGE_FIRST: registers 0 and NPT-1 (the ones the next step shuffles) first
+        const int j = !EDGE_FIRST ? jj : (jj == 0 ? 0 : (jj == 1 ? NPT - 1 : jj - 1));
         const Real sv = (j == 0 ? vx0 : vC[j - 1]) + (j == NPT - 1 ? vx1 : vC[j + 1]);
         const Real su = (j == 0 ? ux0 : uC[j - 1]) + (j == NPT - 1 ? ux1 : uC[j + 1]);
         const Real d = fma(Real(-2), vP[j], sv);
@@ -122,7 +124,8 @@ __device__ __forceinline__ void coupled_step(Real (&vP)[NPT], Real (&vC)[NPT], R
 }
 
 // MINB > 0 caps registers (launch_bounds min blocks per SM) for occupancy experiments.
-template <typename Real, int LPW, int NPT, int WARPS, int CHUNK, bool FLUX, bool EXACT, int MINB = 0>
+template <typename Real, int LPW, int NPT, int WARPS, int CHUNK, bool FLUX, bool EXACT, int MINB = 0,
+          int UNROLL = 2, bool EDGE_FIRST = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
 k_df_coupled(const CoupledSegArgs<Real> a) {
     constexpr bool DEV = sizeof(Real) == 4;   // fp32 state = deviations from 1
@@ -213,26 +216,32 @@ k_df_coupled(const CoupledSegArgs<Real> a) {
         for (int i = tid; i < clen * nch; i += WARPS * 32) s_tab[i] = a.table[(size_t)c0s * nch + i];
         __syncthreads();
         int s = 0;
-        // two steps per iteration: the layer rotation is a register renaming
-        for (; s + 1 < clen; s += 2) {
-            coupled_step<Real, LPW, NPT, FLUX, EXACT>(vp, vc, up, uc, ci, c0, amb(s), mirror0, rev, acc,
-                                                      bad, norm);
-            if (EXACT && failed_at < 0 && group_bad(bad)) {
-                failed_at = c0s + s + 1;
+        // an even number of steps per iteration: the layer rotation is a
+        // register renaming (UNROLL > 2 shortens the per-iteration drain)
+        auto pair = [&](int s2) {
+            coupled_step<Real, LPW, NPT, FLUX, EXACT, EDGE_FIRST>(vp, vc, up, uc, ci, c0, amb(s2), mirror0, rev,
+                                                                  acc, bad, norm);
+            if (EXACT && group_bad(bad) && failed_at < 0) {   // ballot first: every lane votes
+                failed_at = c0s + s2 + 1;
                 store(uc, up, vc, vp);   // after this step curr lives in the P registers
             }
-            coupled_step<Real, LPW, NPT, FLUX, EXACT>(vc, vp, uc, up, ci, c0, amb(s + 1), mirror0, rev,
-                                                      acc, bad, norm);
-            if (EXACT && failed_at < 0 && group_bad(bad)) {
-                failed_at = c0s + s + 2;
+            coupled_step<Real, LPW, NPT, FLUX, EXACT, EDGE_FIRST>(vc, vp, uc, up, ci, c0, amb(s2 + 1), mirror0,
+                                                                  rev, acc, bad, norm);
+            if (EXACT && group_bad(bad) && failed_at < 0) {
+                failed_at = c0s + s2 + 2;
                 store(up, uc, vp, vc);
             }
+        };
+        for (; s + UNROLL - 1 < clen; s += UNROLL) {
+#pragma unroll
+            for (int q = 0; q < UNROLL; q += 2) pair(s + q);
         }
+        for (; s + 1 < clen; s += 2) pair(s);
         if (s < clen) {   // odd tail (last chunk only)
             coupled_step<Real, LPW, NPT, FLUX, EXACT>(vp, vc, up, uc, ci, c0, amb(s), mirror0, rev, acc,
                                                       bad, norm);
             swap_layers();
-            if (EXACT && failed_at < 0 && group_bad(bad)) {
+            if (EXACT && group_bad(bad) && failed_at < 0) {   // ballot first: every lane votes
                 failed_at = c0s + s + 1;
                 store(up, uc, vp, vc);
             }
