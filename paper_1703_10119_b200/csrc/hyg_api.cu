@@ -675,8 +675,9 @@ int advance_nonlinear(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status)
                 a.out[i] = c->s64[1 - from][i];
             }
             LaunchScope ls(c, "df_analytic_fused", static_cast<double>(c->cells()) * len);
-            if (c->n <= 128) k_df_analytic_walls<128><<<c->n_walls, 32, 0, c->stream>>>(a);
-            else k_df_analytic_walls<1024><<<c->n_walls, 32, 0, c->stream>>>(a);
+            if (c->n <= 128) k_df_analytic_walls<128, 128><<<c->n_walls, 128, 0, c->stream>>>(a);
+            else if (c->n <= 256) k_df_analytic_walls<256, 256><<<c->n_walls, 256, 0, c->stream>>>(a);
+            else k_df_analytic_walls<1024, 256><<<c->n_walls, 256, 0, c->stream>>>(a);
         }
         HYG_CUDA(cudaGetLastError());
         int flag = 0;

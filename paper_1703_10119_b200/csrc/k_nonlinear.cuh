@@ -8,9 +8,9 @@
 //
 // configs[0] is one wall of 101 nodes marched 1e5 steps: the work per step is
 // ~100 node-updates, so the step is latency-bound (one dependency chain:
-// neighbours -> half-node d(v) (exp) -> reciprocal -> v -> u).  One warp per
-// wall keeps the chain inside a warp (shared memory + __syncwarp, no block
-// barrier); batches of such walls run one warp each.
+// neighbours -> half-node d(v) (exp) -> reciprocal -> v -> u).  One CTA per
+// wall with a thread per node keeps one node's chain + one barrier per step;
+// batches of such walls run one CTA each.
 //
 // Rows are the reference's, rewritten in increment form around the layer
 // n-1 value (exact in real arithmetic; a uniform state at ambient values is
@@ -94,14 +94,17 @@ __device__ __forceinline__ void analytic_face(const AnalyticRow& r, const Biot& 
                   (1.0 + 2.0 * r.b + cplu);
 }
 
-template <int MAXN>
-__global__ void __launch_bounds__(32) k_df_analytic_walls(const NonlinearSegArgs A) {
+// One CTA of THREADS threads per wall; node j is handled by thread j % THREADS.
+// For configs[0] (n = 101) THREADS = 128: one node per thread, so the step's
+// latency is one node's chain plus a block barrier.
+template <int MAXN, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_df_analytic_walls(const NonlinearSegArgs A) {
     __shared__ double s_lay[4][MAXN];            // up, uc, vp, vc (roles rotate)
     __shared__ Ambient s_amb[kNlChunk][2];       // [step][face]
     if (*A.stop) return;
-    const int w = blockIdx.x, lane = threadIdx.x, n = A.n;
+    const int w = blockIdx.x, tid = threadIdx.x, n = A.n;
     const size_t o = static_cast<size_t>(w) * n;
-    for (int j = lane; j < n; j += 32) {
+    for (int j = tid; j < n; j += THREADS) {
         s_lay[0][j] = A.in[0][o + j];
         s_lay[1][j] = A.in[1][o + j];
         s_lay[2][j] = A.in[2][o + j];
@@ -114,22 +117,22 @@ __global__ void __launch_bounds__(32) k_df_analytic_walls(const NonlinearSegArgs
     const int chl = A.chan[2 * w], chr = A.chan[2 * w + 1];
     double p[4] = {A.p[0], A.p[1], A.p[2], A.p[3]};
     unsigned acc = 0;
-    int P = 0;    // s_lay[2*... ] roles: u_prev = s_lay[P], u_curr = s_lay[1-P], same for v (+2)
-    __syncwarp();
+    int P = 0;    // roles: u_prev = s_lay[P], u_curr = s_lay[1-P], v_prev = s_lay[2+P], v_curr = s_lay[3-P]
 
     for (int c0 = 0; c0 < A.nsteps; c0 += kNlChunk) {
         const int clen = min(kNlChunk, A.nsteps - c0);
-        for (int i = lane; i < 2 * clen; i += 32) {
+        __syncthreads();
+        for (int i = tid; i < 2 * clen; i += THREADS) {
             const int s = i >> 1, f = i & 1;
             s_amb[s][f] = A.table[static_cast<size_t>(c0 + s) * A.n_channels + (f ? chr : chl)];
         }
-        __syncwarp();
+        __syncthreads();
         for (int s = 0; s < clen; ++s) {
             double* up = s_lay[P];
             const double* uc = s_lay[1 - P];
             double* vp = s_lay[2 + P];
             const double* vc = s_lay[3 - P];
-            for (int j = lane; j < n; j += 32) {
+            for (int j = tid; j < n; j += THREADS) {
                 const double vpj = vp[j], upj = up[j], vcj = vc[j];
                 double vn, un;
                 if (j > 0 && j < n - 1) {
@@ -147,18 +150,18 @@ __global__ void __launch_bounds__(32) k_df_analytic_walls(const NonlinearSegArgs
                 vp[j] = vn;     // layer n-1 slot becomes layer n+1
                 up[j] = un;
             }
-            __syncwarp();
+            __syncthreads();
             P ^= 1;
         }
     }
     // fast guard verdict (bit 30 of the high word: |x| >= 2 or not finite)
     const unsigned any = __reduce_or_sync(0xffffffffu, acc);
-    if ((any & 0x40000000u) && lane == 0) atomicCAS(A.suspect, 0, A.seg_index + 1);
+    if ((any & 0x40000000u) && (tid % 32) == 0) atomicCAS(A.suspect, 0, A.seg_index + 1);
     const double* up = s_lay[P];
     const double* uc = s_lay[1 - P];
     const double* vp = s_lay[2 + P];
     const double* vc = s_lay[3 - P];
-    for (int j = lane; j < n; j += 32) {
+    for (int j = tid; j < n; j += THREADS) {
         A.out[0][o + j] = up[j];
         A.out[1][o + j] = uc[j];
         A.out[2][o + j] = vp[j];

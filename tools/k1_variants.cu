@@ -20,10 +20,10 @@ __global__ void k_coef(int B, double dx, double dt, const Groups* g, const Biot*
 
 struct Bufs { double* in[4]; double* out[4]; };
 
-template <int LPW, int NPT, int WARPS, int MINB>
+template <int LPW, int NPT, int WARPS, int MINB, int UNROLL = 2, bool EDGE = false>
 float run(const char* name, CoupledSegArgs<double> a, Bufs& b, int B, int steps, std::vector<double>* result) {
     constexpr int CHUNK = 128;
-    auto kern = k_df_coupled<double, LPW, NPT, WARPS, CHUNK, false, false, MINB>;
+    auto kern = k_df_coupled<double, LPW, NPT, WARPS, CHUNK, false, false, MINB, UNROLL, EDGE>;
     const int smem = CHUNK * a.n_channels * sizeof(Ambient);
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cudaFuncAttributes attr;
@@ -123,12 +123,11 @@ int main(int argc, char** argv) {
         for (size_t i = 0; i < ref.size(); ++i) m = std::max(m, std::fabs(ref[i] - got[i]));
         std::printf("    %s max |diff| vs prod %.3e\n", nm, m);
     };
-    run<16, 16, 2, 0>("16x16 w2", a, b, B, steps, nullptr);
-    run<16, 16, 8, 0>("16x16 w8", a, b, B, steps, nullptr);
-    run<16, 16, 4, 3>("16x16 w4 minb3", a, b, B, steps, &got); check("minb3");
-    run<32, 8, 4, 0>("32x8 w4", a, b, B, steps, &got); check("32x8");
-    run<32, 8, 4, 4>("32x8 w4 minb4", a, b, B, steps, nullptr);
-    run<32, 8, 2, 8>("32x8 w2 minb8", a, b, B, steps, nullptr);
-    run<8, 32, 4, 1>("8x32 w4", a, b, B, steps, nullptr);
+    run<16, 16, 4, 0, 4, false>("16x16 unroll4", a, b, B, steps, &got); check("unroll4");
+    run<16, 16, 4, 0, 2, true>("16x16 edge-first", a, b, B, steps, &got); check("edge-first");
+    run<16, 16, 4, 0, 4, true>("16x16 unroll4 edge", a, b, B, steps, &got); check("unroll4+edge");
+    run<16, 16, 4, 0, 8, false>("16x16 unroll8", a, b, B, steps, &got); check("unroll8");
+    run<32, 8, 4, 0, 4, true>("32x8 unroll4 edge", a, b, B, steps, &got); check("32x8 u4e");
+    run<32, 8, 4, 4, 4, true>("32x8 u4 edge minb4", a, b, B, steps, nullptr);
     return 0;
 }
