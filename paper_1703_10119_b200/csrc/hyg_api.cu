@@ -453,11 +453,10 @@ int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
             StepArgs a = step_args(c, c->cur, dt);
             a.amb = c->d_table + k * nch;
             a.layer = c->layer + k;
-            {
+            if (c->zones.empty()) {
                 LaunchScope ls(c, "df_step_general", static_cast<double>(c->cells()));
                 k_df_step_general<<<grid, threads, 0, c->stream>>>(a);
-            }
-            if (!c->zones.empty()) {
+            } else {
                 ZoneArgs z{};
                 z.n_zones = static_cast<int>(c->zones.size());
                 z.n = c->n;
@@ -467,7 +466,7 @@ int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
                 z.inz = c->d_inz;
                 z.src = c->d_src + k * (nsrc * 3 + 2);
                 z.n_sources = nsrc;
-                z.uc = c->s64[c->cur][1];    // layer n samples (before the wall step)
+                z.uc = c->s64[c->cur][1];    // layer n samples (building.cpp:162-164)
                 z.vc = c->s64[c->cur][3];
                 z.zu_in = c->zu[c->zcur];
                 z.zv_in = c->zv[c->zcur];
@@ -478,8 +477,9 @@ int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
                 z.fail_key = c->d_key;
                 z.own0 = c->own_z0;
                 z.own1 = c->own_z1;
-                LaunchScope ls(c, "zone_step", 0.0);
-                k_zone_step<<<(z.n_zones + 127) / 128, 128, 0, c->stream>>>(z);
+                const int zblocks = (z.n_zones + threads - 1) / threads;
+                LaunchScope ls(c, "building_step", static_cast<double>(c->cells()));
+                k_building_step<<<grid + zblocks, threads, 0, c->stream>>>(a, z, grid);
                 c->zcur ^= 1;
             }
             rotate_layers(c);
@@ -702,7 +702,7 @@ int advance_nonlinear(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status)
 }
 
 // ---- the temporally blocked long-wall path (K3, analytic d(v), one wall) ----------
-constexpr int kTileT = 1024, kTileS = 16, kTileThreads = 256;
+constexpr int kTileT = 992, kTileS = 16, kTileThreads = 256;   // W = T + 2S = 4 x 256
 
 int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
     const int nch = std::max<int>(1, static_cast<int>(c->channels.size()));

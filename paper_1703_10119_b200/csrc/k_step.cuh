@@ -143,11 +143,7 @@ __device__ __forceinline__ void analytic_node(const StepArgs& a, int w, int j, d
 }
 
 // One DF step of every wall; guard per node (exact check_bounded semantics).
-__global__ void k_df_step_general(const StepArgs a) {
-    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t total = static_cast<int64_t>(a.n_walls) * a.n;
-    if (tid >= total) return;
-    if (*a.fail_key != ~0ull) return;    // an earlier step failed: freeze
+__device__ __forceinline__ void wall_node_step(const StepArgs& a, int64_t tid) {
     const int w = static_cast<int>(tid / a.n), j = static_cast<int>(tid % a.n);
     double un, vn;
     if (a.coeff_kind == kCoeffConstant) coupled_node(a, w, j, un, vn);
@@ -161,6 +157,13 @@ __global__ void k_df_step_general(const StepArgs a) {
             (static_cast<unsigned long long>(a.layer + 1) << 32) | static_cast<unsigned>(w);
         atomicMin(a.fail_key, key);
     }
+}
+
+__global__ void k_df_step_general(const StepArgs a) {
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (tid >= static_cast<int64_t>(a.n_walls) * a.n) return;
+    if (*a.fail_key != ~0ull) return;    // an earlier step failed: freeze
+    wall_node_step(a, tid);
 }
 
 // ---- zones -----------------------------------------------------------------
@@ -195,10 +198,7 @@ struct ZoneArgs {
 
 // zone_step_explicit (zone.cpp:69-74) of zone_rhs (zone.cpp:26-53) with the
 // layer-n samples gathered as in building.cpp:128-140,162-164.
-__global__ void k_zone_step(const ZoneArgs a) {
-    const int z = blockIdx.x * blockDim.x + threadIdx.x;
-    if (z >= a.n_zones) return;
-    if (*a.fail_key != ~0ull) return;
+__device__ __forceinline__ void zone_update(const ZoneArgs& a, int z) {
     const ZoneDev d = a.zones[z];
     const double u_a = a.zu_in[z], v_a = a.zv_in[z];
     const double* s = a.src + 3 * d.sources;
@@ -227,6 +227,28 @@ __global__ void k_zone_step(const ZoneArgs a) {
         // zone failures rank after every wall of the same layer (building.cpp:288-299)
         const unsigned long long key = (static_cast<unsigned long long>(a.layer + 1) << 32) | 0xffffffffu;
         atomicMin(a.fail_key, key);
+    }
+}
+
+__global__ void k_zone_step(const ZoneArgs a) {
+    const int z = blockIdx.x * blockDim.x + threadIdx.x;
+    if (z >= a.n_zones) return;
+    if (*a.fail_key != ~0ull) return;
+    zone_update(a, z);
+}
+
+// One building step (step_explicit, building.cpp:152-187) in one launch: the
+// first wall_blocks blocks advance the wall nodes with layer-n zone values,
+// the remaining blocks advance the zones with layer-n surface samples.  Both
+// halves read layer n only and write disjoint buffers.
+__global__ void k_building_step(const StepArgs a, const ZoneArgs z, int wall_blocks) {
+    if (*a.fail_key != ~0ull) return;
+    if (static_cast<int>(blockIdx.x) < wall_blocks) {
+        const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        if (tid < static_cast<int64_t>(a.n_walls) * a.n) wall_node_step(a, tid);
+    } else {
+        const int zi = (static_cast<int>(blockIdx.x) - wall_blocks) * blockDim.x + threadIdx.x;
+        if (zi < z.n_zones) zone_update(z, zi);
     }
 }
 

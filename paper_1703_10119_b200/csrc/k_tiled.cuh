@@ -7,7 +7,7 @@
 // HBM.  Here a CTA loads a tile of T nodes plus S halo nodes on each side
 // (both layers of both fields) into shared memory, advances S steps there and
 // writes the T owned nodes back: 64 B per node per S steps plus the halo, i.e.
-// (32 (T + 2S) + 32 T) / (T S) ~ 4 B per update at T = 1024, S = 16.
+// (32 (T + 2S) + 32 T) / (T S) ~ 4 B per update at T = 992, S = 16.
 //
 // Exactness: at step k only nodes whose three-level stencil is still valid
 // are computed — the window shrinks by one node per side and step
@@ -16,6 +16,12 @@
 // the value the untiled march produces; the shrunk-away halo is discarded.
 // Half-node coefficients d(v) are computed once per half node and step into
 // shared memory (the per-step kernel evaluates each twice).
+//
+// Shape: W = T + 2S = 1024 = 4 x 256 threads, each thread owning 4 window
+// slots (unrolled: independent chains interleave, no imbalance at the
+// barriers); the layer roles rotate by unrolling two steps so every shared
+// access has a compile-time base (a runtime-indexed pointer table would turn
+// them into generic loads).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -40,70 +46,104 @@ struct TiledArgs {
     int* suspect;
 };
 
+template <int W, int THREADS>
+struct TileCtx {
+    double (*lay)[W];          // [4][W] in shared memory
+    double* kp;                // [W]
+    int lmin, lmax, lf, rf;    // real-node range, face slots (-1 if absent)
+    int tid;
+};
+
+// One step with compile-time roles: layer n-1 in (UP, VP) becomes layer n+1.
+template <int W, int THREADS, int UP, int UC, int VP, int VC>
+__device__ __forceinline__ void tiled_step(const TileCtx<W, THREADS>& c, const TiledArgs& A,
+                                           const AnalyticRow& rc, const double (&p)[4], int k,
+                                           unsigned& acc) {
+    constexpr int NQ = W / THREADS;
+    double* up = c.lay[UP];
+    double* vp = c.lay[VP];
+    const double* uc = c.lay[UC];
+    const double* vc = c.lay[VC];
+    const int lo = c.lf >= 0 ? c.lf : k;
+    const int hi = c.rf >= 0 ? c.rf + 1 : W - k;
+    const int h0 = max(lo - 1, c.lmin), h1 = min(hi, c.lmax - 1);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int i = c.tid + q * THREADS;
+        if (i >= h0 && i < h1) c.kp[i] = d_of(p, 0.5 * (vc[i] + vc[i + 1]));
+    }
+    __syncthreads();
+    const Ambient* row = A.table + static_cast<size_t>(k - 1) * A.n_channels;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int j = c.tid + q * THREADS;
+        if (j < lo || j >= hi) continue;
+        double vn, un;
+        if (j == c.lf) {
+            analytic_face(rc, A.bl, row[A.chl], vp[j], up[j], vc[j + 1], uc[j + 1], d_of(p, vc[j]), c.kp[j],
+                          vn, un);
+        } else if (j == c.rf) {
+            analytic_face(rc, A.br, row[A.chr], vp[j], up[j], vc[j - 1], uc[j - 1], d_of(p, vc[j]),
+                          c.kp[j - 1], vn, un);
+        } else {
+            analytic_interior(rc, vp[j], up[j], vc[j - 1], vc[j + 1], uc[j - 1], uc[j + 1], c.kp[j - 1],
+                              c.kp[j], vn, un);
+        }
+        acc |= static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn));
+        vp[j] = vn;
+        up[j] = un;
+    }
+    __syncthreads();
+}
+
 template <int T, int S, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_df_analytic_tiled(const TiledArgs A) {
     constexpr int W = T + 2 * S;
+    static_assert(W % THREADS == 0, "window must split evenly over the threads");
     extern __shared__ double sm[];           // lay[4][W], kp[W]
-    double* lay[4] = {sm, sm + W, sm + 2 * W, sm + 3 * W};
-    double* kp = sm + 4 * W;                 // kp[i]: half node between local i and i+1
     if (*A.stop) return;
-    const int tid = threadIdx.x;
+    TileCtx<W, THREADS> c;
+    c.lay = reinterpret_cast<double(*)[W]>(sm);
+    c.kp = sm + 4 * W;
+    c.tid = threadIdx.x;
     const int64_t n = A.n;
     const int64_t g0 = static_cast<int64_t>(blockIdx.x) * T - S;   // global index of local 0
-    for (int i = tid; i < W; i += THREADS) {
+#pragma unroll
+    for (int q = 0; q < W / THREADS; ++q) {
+        const int i = c.tid + q * THREADS;
         const int64_t gi = g0 + i;
         const bool real = gi >= 0 && gi < n;
 #pragma unroll
-        for (int f = 0; f < 4; ++f) lay[f][i] = real ? A.in[f][gi] : 1.0;
+        for (int f = 0; f < 4; ++f) c.lay[f][i] = real ? A.in[f][gi] : 1.0;
     }
-    const int lmin = static_cast<int>(g0 < 0 ? -g0 : 0);            // first real local node
-    const int lmax = static_cast<int>(n - g0 < W ? n - g0 : W);      // one past the last
-    const bool left_face = g0 <= 0;                                 // global node 0 is local -g0
-    const bool right_face = n - 1 - g0 < W;                         // global n-1 is local n-1-g0
+    c.lmin = static_cast<int>(g0 < 0 ? -g0 : 0);               // first real local node
+    c.lmax = static_cast<int>(n - g0 < W ? n - g0 : W);         // one past the last
+    c.lf = g0 <= 0 ? c.lmin : -1;                               // global node 0
+    c.rf = n - 1 - g0 < W ? static_cast<int>(n - 1 - g0) : -1;  // global node n-1
     const double p[4] = {A.p[0], A.p[1], A.p[2], A.p[3]};
     const AnalyticRow rc = analytic_row(A.groups, A.dx, A.dt);
     unsigned acc = 0;
-    int P = 0;     // up = lay[P], uc = lay[1-P], vp = lay[2+P], vc = lay[3-P]
     __syncthreads();
-    for (int k = 1; k <= A.steps; ++k) {
-        double* up = lay[P];
-        const double* uc = lay[1 - P];
-        double* vp = lay[2 + P];
-        const double* vc = lay[3 - P];
-        const int lo = left_face ? lmin : k;
-        const int hi = right_face ? lmax : W - k;
-        const int h0 = max(lo - 1, lmin), h1 = min(hi, lmax - 1);
-        for (int i = h0 + tid; i < h1; i += THREADS) kp[i] = d_of(p, 0.5 * (vc[i] + vc[i + 1]));
-        __syncthreads();
-        const Ambient* row = A.table + static_cast<size_t>(k - 1) * A.n_channels;
-        for (int j = lo + tid; j < hi; j += THREADS) {
-            const int64_t gj = g0 + j;
-            double vn, un;
-            if (gj == 0) {
-                analytic_face(rc, A.bl, row[A.chl], vp[j], up[j], vc[j + 1], uc[j + 1], d_of(p, vc[j]), kp[j],
-                              vn, un);
-            } else if (gj == n - 1) {
-                analytic_face(rc, A.br, row[A.chr], vp[j], up[j], vc[j - 1], uc[j - 1], d_of(p, vc[j]),
-                              kp[j - 1], vn, un);
-            } else {
-                analytic_interior(rc, vp[j], up[j], vc[j - 1], vc[j + 1], uc[j - 1], uc[j + 1], kp[j - 1], kp[j],
-                                  vn, un);
-            }
-            acc |= static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn));
-            vp[j] = vn;
-            up[j] = un;
-        }
-        __syncthreads();
-        P ^= 1;
+    int k = 1;
+    for (; k + 1 <= A.steps; k += 2) {
+        tiled_step<W, THREADS, 0, 1, 2, 3>(c, A, rc, p, k, acc);       // prev slots 0/2 -> n+1
+        tiled_step<W, THREADS, 1, 0, 3, 2>(c, A, rc, p, k + 1, acc);
     }
+    const bool odd = k <= A.steps;
+    if (odd) tiled_step<W, THREADS, 0, 1, 2, 3>(c, A, rc, p, k, acc);
     const unsigned any = __reduce_or_sync(0xffffffffu, acc);
-    if ((any & 0x40000000u) && (tid % 32) == 0) atomicCAS(A.suspect, 0, A.seg_index + 1);
-    const double* fin[4] = {lay[P], lay[1 - P], lay[2 + P], lay[3 - P]};
-    for (int i = S + tid; i < S + T; i += THREADS) {
-        const int64_t gi = g0 + i;
-        if (gi >= n) break;
+    if ((any & 0x40000000u) && (c.tid % 32) == 0) atomicCAS(A.suspect, 0, A.seg_index + 1);
+    // roles after an even number of steps: up = 0, uc = 1, vp = 2, vc = 3; odd: swapped
+    const int ru_p = odd ? 1 : 0, rv_p = odd ? 3 : 2;
 #pragma unroll
-        for (int f = 0; f < 4; ++f) A.out[f][gi] = fin[f][i];
+    for (int q = 0; q < W / THREADS; ++q) {
+        const int i = c.tid + q * THREADS;
+        const int64_t gi = g0 + i;
+        if (i < S || i >= S + T || gi >= n) continue;
+        A.out[0][gi] = c.lay[ru_p][i];
+        A.out[1][gi] = c.lay[1 - ru_p][i];
+        A.out[2][gi] = c.lay[rv_p][i];
+        A.out[3][gi] = c.lay[5 - rv_p][i];
     }
 }
 
