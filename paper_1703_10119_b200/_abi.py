@@ -123,6 +123,7 @@ PROTOTYPES = {
     "hyg_launch_count": (C.c_int64, [C.c_void_p]),
     "hyg_probe_fp64_peak": (C.c_int, [C.c_int32, dp, dp]),
     "hyg_probe_fp32_peak": (C.c_int, [C.c_int32, dp]),
+    "hyg_selftest_fastmath": (C.c_int, [C.c_int32, C.c_int32, dp, dp, dp]),
     "hyg_saturation_pressure": (C.c_int, [C.c_double, dp]),
     "hyg_scale_wall": (C.c_int, [dp, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                  C.c_double, C.c_double, C.c_double, C.POINTER(WallGroups), C.POINTER(FaceBiot)]),

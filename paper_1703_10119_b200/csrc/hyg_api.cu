@@ -675,9 +675,9 @@ int advance_nonlinear(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status)
                 a.out[i] = c->s64[1 - from][i];
             }
             LaunchScope ls(c, "df_analytic_fused", static_cast<double>(c->cells()) * len);
-            if (c->n <= 128) k_df_analytic_walls<128, 128><<<c->n_walls, 128, 0, c->stream>>>(a);
-            else if (c->n <= 256) k_df_analytic_walls<256, 256><<<c->n_walls, 256, 0, c->stream>>>(a);
-            else k_df_analytic_walls<1024, 256><<<c->n_walls, 256, 0, c->stream>>>(a);
+            if (c->n <= 130) k_df_analytic_walls<130, 128><<<c->n_walls, 160, 0, c->stream>>>(a);
+            else if (c->n <= 258) k_df_analytic_walls<258, 256><<<c->n_walls, 288, 0, c->stream>>>(a);
+            else k_df_analytic_walls<1024, 256><<<c->n_walls, 288, 0, c->stream>>>(a);
         }
         HYG_CUDA(cudaGetLastError());
         int flag = 0;
@@ -1565,6 +1565,32 @@ __global__ void k_ffma_probe(float* out, int iters) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 }  // namespace
+
+namespace {
+__global__ void k_fastmath(int n, const double* x, double* e, double* r) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        e[i] = fexp(x[i]);
+        r[i] = frcp(x[i]);
+    }
+}
+}  // namespace
+
+extern "C" int hyg_selftest_fastmath(int32_t device, int32_t n, const double* x, double* exp_out,
+                                     double* rcp_out) {
+    hyg_status* status = nullptr;
+    if (n <= 0 || !x || !exp_out || !rcp_out) return HYG_EINVAL;
+    HYG_CUDA(cudaSetDevice(device));
+    double* d = nullptr;
+    HYG_CUDA(cudaMalloc(&d, sizeof(double) * 3 * n));
+    HYG_CUDA(cudaMemcpy(d, x, sizeof(double) * n, cudaMemcpyHostToDevice));
+    k_fastmath<<<(n + 255) / 256, 256>>>(n, d, d + n, d + 2 * n);
+    HYG_CUDA(cudaGetLastError());
+    HYG_CUDA(cudaMemcpy(exp_out, d + n, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    HYG_CUDA(cudaMemcpy(rcp_out, d + 2 * n, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    return HYG_OK;
+}
 
 extern "C" int hyg_probe_fp32_peak(int32_t device, double* tflops) {
     hyg_status* status = nullptr;

@@ -1,5 +1,5 @@
 // k_nonlinear.cuh — K2: nonlinear DF march for walls with the analytic
-// coefficient functor k_M* = d(v) (HYG_COEFF_ANALYTIC_D), one warp per wall,
+// coefficient functor k_M* = d(v) (HYG_COEFF_ANALYTIC_D), one CTA per wall,
 // the four layers in shared memory, all steps of a segment in one launch.
 //
 // Replaces: df_step_nonlinear (/root/reference/proj/src/wall.cpp:196-264) with
@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include "hyg_coef.cuh"
+#include "hyg_fastmath.cuh"
 #include "k_coupled.cuh"
 
 namespace hyg {
@@ -47,7 +48,7 @@ struct NonlinearSegArgs {
 
 __device__ __forceinline__ double d_of(const double* p, double v) {
     const double e = v - p[3];
-    return 1.0 + p[0] * v + p[1] * exp(-p[2] * e * e);
+    return 1.0 + p[0] * v + p[1] * fexp(-p[2] * e * e);
 }
 
 constexpr int kNlChunk = 64;   // forcing rows staged per chunk
@@ -71,7 +72,7 @@ __device__ __forceinline__ AnalyticRow analytic_row(const Groups& g, double dx, 
 __device__ __forceinline__ void analytic_interior(const AnalyticRow& r, double vp, double up, double vL,
                                                   double vR, double uL, double uR, double km, double kp,
                                                   double& vn, double& un) {
-    vn = vp + 2.0 * r.a * (kp * (vR - vp) + km * (vL - vp)) / (1.0 + r.a * (kp + km));
+    vn = vp + 2.0 * r.a * (kp * (vR - vp) + km * (vL - vp)) * frcp(1.0 + r.a * (kp + km));
     un = up + (2.0 * r.b * (uR + uL - 2.0 * up) + 2.0 * r.g * (vR + vL - vn - vp) - r.gamma * (vn - vp)) *
                   r.inv_u;
 }
@@ -83,22 +84,24 @@ __device__ __forceinline__ void analytic_face(const AnalyticRow& r, const Biot& 
                                               double kp_b, double& vn, double& un) {
     const double S = kp_b + km_b;
     const double cpl = 2.0 * r.a * r.dx * fb.Bi_M;
-    vn = vp + (2.0 * r.a * S * (vcn - vp) + 2.0 * cpl * (am.v - vp) + 4.0 * r.a * r.dx * am.g) /
-                  (1.0 + r.a * S + cpl);
+    vn = vp + (2.0 * r.a * S * (vcn - vp) + 2.0 * cpl * (am.v - vp) + 4.0 * r.a * r.dx * am.g) *
+                  frcp(1.0 + r.a * S + cpl);
     const double vbar = 0.5 * (vn + vp);
-    const double vg = vcn - (2.0 * r.dx / km_b) * (fb.Bi_M * (vbar - am.v) - am.g);
+    const double vg = vcn - (2.0 * r.dx * frcp(km_b)) * (fb.Bi_M * (vbar - am.v) - am.g);
     const double cplu = 2.0 * r.b * r.dx * fb.Bi_TT;
     un = up + (4.0 * r.b * (ucn - up) + 2.0 * cplu * (am.u - up) - r.gamma * (vn - vp) +
                2.0 * r.b * r.ratio * (vcn - vg) - 4.0 * r.b * r.dx * (fb.Bi_TM * (vbar - am.v) - am.q) +
-               2.0 * r.g * (vcn + vg) - 2.0 * r.g * (vn + vp)) /
-                  (1.0 + 2.0 * r.b + cplu);
+               2.0 * r.g * (vcn + vg) - 2.0 * r.g * (vn + vp)) *
+                  frcp(1.0 + 2.0 * r.b + cplu);
 }
 
-// One CTA of THREADS threads per wall; node j is handled by thread j % THREADS.
-// For configs[0] (n = 101) THREADS = 128: one node per thread, so the step's
-// latency is one node's chain plus a block barrier.
-template <int MAXN, int THREADS>
-__global__ void __launch_bounds__(THREADS) k_df_analytic_walls(const NonlinearSegArgs A) {
+// One CTA per wall: IT threads stride over the interior nodes 1..n-2 and one
+// extra warp takes the two face nodes (lanes 0 and 1), so no warp mixes the
+// interior and face rows.  For configs[0] (n = 101) IT = 128: one interior
+// node per thread; a step costs one node's chain plus a block barrier.
+template <int MAXN, int IT>
+__global__ void __launch_bounds__(IT + 32) k_df_analytic_walls(const NonlinearSegArgs A) {
+    constexpr int THREADS = IT + 32;
     __shared__ double s_lay[4][MAXN];            // up, uc, vp, vc (roles rotate)
     __shared__ Ambient s_amb[kNlChunk][2];       // [step][face]
     if (*A.stop) return;
@@ -113,7 +116,9 @@ __global__ void __launch_bounds__(THREADS) k_df_analytic_walls(const NonlinearSe
     const Groups g = A.groups[w];
     const double dx = A.dx, dt = A.dt;
     const AnalyticRow rc = analytic_row(g, dx, dt);
-    const Biot bl = A.biot[2 * w], br = A.biot[2 * w + 1];
+    const bool face_warp = tid >= IT;
+    const int flane = tid - IT;                  // 0: x*=0 face, 1: x*=1 face
+    const Biot fb = A.biot[2 * w + (flane == 1 ? 1 : 0)];
     const int chl = A.chan[2 * w], chr = A.chan[2 * w + 1];
     double p[4] = {A.p[0], A.p[1], A.p[2], A.p[3]};
     unsigned acc = 0;
@@ -132,22 +137,27 @@ __global__ void __launch_bounds__(THREADS) k_df_analytic_walls(const NonlinearSe
             const double* uc = s_lay[1 - P];
             double* vp = s_lay[2 + P];
             const double* vc = s_lay[3 - P];
-            for (int j = tid; j < n; j += THREADS) {
-                const double vpj = vp[j], upj = up[j], vcj = vc[j];
-                double vn, un;
-                if (j > 0 && j < n - 1) {
+            if (!face_warp) {
+                for (int j = 1 + tid; j < n - 1; j += IT) {
+                    const double vpj = vp[j], upj = up[j], vcj = vc[j];
                     const double vL = vc[j - 1], vR = vc[j + 1];
+                    double vn, un;
                     analytic_interior(rc, vpj, upj, vL, vR, uc[j - 1], uc[j + 1],
                                       d_of(p, 0.5 * (vL + vcj)), d_of(p, 0.5 * (vcj + vR)), vn, un);
-                } else {
-                    const bool left = j == 0;
-                    const int jn = left ? 1 : n - 2;
-                    const double vcn = vc[jn];
-                    analytic_face(rc, left ? bl : br, s_amb[s][left ? 0 : 1], vpj, upj, vcn, uc[jn],
-                                  d_of(p, vcj), d_of(p, 0.5 * (vcj + vcn)), vn, un);
+                    acc |= static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn));
+                    vp[j] = vn;     // layer n-1 slot becomes layer n+1
+                    up[j] = un;
                 }
+            } else if (flane < 2) {
+                const bool left = flane == 0;
+                const int j = left ? 0 : n - 1;
+                const int jn = left ? 1 : n - 2;
+                const double vcj = vc[j], vcn = vc[jn];
+                double vn, un;
+                analytic_face(rc, fb, s_amb[s][flane], vp[j], up[j], vcn, uc[jn], d_of(p, vcj),
+                              d_of(p, 0.5 * (vcj + vcn)), vn, un);
                 acc |= static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn));
-                vp[j] = vn;     // layer n-1 slot becomes layer n+1
+                vp[j] = vn;
                 up[j] = un;
             }
             __syncthreads();

@@ -67,87 +67,103 @@ __device__ __forceinline__ FaceVals resolve(const StepArgs& a, int w, int k) {
     return f;
 }
 
+// The node's inputs, loaded before anything else so a warp's loads are all in
+// flight together (the per-step path is memory-latency-bound).  At a face
+// the missing neighbour is the mirrored interior one.
+struct NodeIn { double vp, up, vc, uc, vl, vr, ul, ur; };
+
+__device__ __forceinline__ NodeIn load_node(const StepArgs& a, int w, int j) {
+    const int n = a.n;
+    const size_t o = static_cast<size_t>(w) * n;
+    const int jl = j == 0 ? 1 : j - 1, jr = j == n - 1 ? n - 2 : j + 1;
+    NodeIn x;
+    x.vp = a.in[2][o + j];
+    x.up = a.in[0][o + j];
+    x.vc = a.in[3][o + j];
+    x.uc = a.in[1][o + j];
+    x.vl = a.in[3][o + jl];
+    x.vr = a.in[3][o + jr];
+    x.ul = a.in[1][o + jl];
+    x.ur = a.in[1][o + jr];
+    return x;
+}
+
 // df_step_coupled (wall.cpp:144-194), one node per thread, in the increment
 // form of hyg_coef.cuh with the per-wall coefficients of this dt (a.coef):
 // the same arithmetic as K1, so fused and per-step marches agree, and no
 // divisions per node (the per-step path stays HBM-bound, 48 B/update).
-__device__ __forceinline__ void coupled_node(const StepArgs& a, int w, int j, double& un,
+__device__ __forceinline__ void coupled_node(const StepArgs& a, int w, int j, const NodeIn& x, double& un,
                                              double& vn) {
     const int n = a.n;
-    const size_t o = static_cast<size_t>(w) * n;
-    const double *up = a.in[0] + o, *uc = a.in[1] + o, *vp = a.in[2] + o, *vc = a.in[3] + o;
-    const bool face = j == 0 || j == n - 1;
-    const int jl = j == 0 ? 1 : j - 1, jr = j == n - 1 ? n - 2 : j + 1;   // mirrored at faces
-    const double vpj = vp[j], upj = up[j];
-    const double d = fma(-2.0, vpj, vc[jl] + vc[jr]);
-    const double du = fma(-2.0, upj, uc[jl] + uc[jr]);
-    if (!face) {
+    const double d = fma(-2.0, x.vp, x.vl + x.vr);
+    const double du = fma(-2.0, x.up, x.ul + x.ur);
+    if (j > 0 && j < n - 1) {
         const RowCoef& c = a.coef[w].in;
-        vn = fma(c.b, d, vpj);
-        un = fma(c.c_sv, d, fma(c.c_su, du, upj));
+        vn = fma(c.b, d, x.vp);
+        un = fma(c.c_sv, d, fma(c.c_su, du, x.up));
         return;
     }
     const RowCoef& c = a.coef[w].face[j == 0 ? 0 : 1];
     const FaceVals b = resolve(a, w, j == 0 ? 0 : 1);
-    const double t = b.v_inf - vpj, tu = b.u_inf - upj;
-    vn = fma(c.e, t, fma(c.b, d, fma(c.e_g, b.g_inf, vpj)));
-    un = fma(c.c_tv, t, fma(c.c_sv, d, fma(c.c_tu, tu, fma(c.c_su, du, fma(c.c_q, b.q_inf, fma(c.c_g, b.g_inf, upj))))));
+    const double t = b.v_inf - x.vp, tu = b.u_inf - x.up;
+    vn = fma(c.e, t, fma(c.b, d, fma(c.e_g, b.g_inf, x.vp)));
+    un = fma(c.c_tv, t, fma(c.c_sv, d, fma(c.c_tu, tu, fma(c.c_su, du, fma(c.c_q, b.q_inf, fma(c.c_g, b.g_inf, x.up))))));
 }
 
 // df_step_nonlinear (wall.cpp:196-264) for the analytic functor (k_M* = d(v),
-// the other five starred coefficients 1), one node per thread.  StarTables
-// (wall.cpp:89-138): node values at j, half-node values at the midpoint
-// state average.
-__device__ __forceinline__ void analytic_node(const StepArgs& a, int w, int j, double& un,
+// the other five starred coefficients 1), one node per thread, literal form.
+// StarTables (wall.cpp:89-138): node values at j, half-node values at the
+// midpoint state average.
+__device__ __forceinline__ void analytic_node(const StepArgs& a, int w, int j, const NodeIn& x, double& un,
                                               double& vn) {
     const int n = a.n;
     const double dx = a.dx, dt = a.dt;
     const Groups p = a.groups[w];
-    const size_t o = static_cast<size_t>(w) * n;
-    const double *up = a.in[0] + o, *uc = a.in[1] + o, *vp = a.in[2] + o, *vc = a.in[3] + o;
     const double ad = p.Fo_M * dt / (dx * dx);
     const double b_ = p.Fo_TT * dt / (dx * dx);
     const double g_ = p.Fo_TM * p.gamma * dt / (dx * dx);
     const double ratio = p.Fo_TT != 0.0 ? p.Fo_TM * p.gamma / p.Fo_TT : 0.0;
     const double cm = 1.0, ctt = 1.0, ctm = 1.0;
     if (j > 0 && j < n - 1) {
-        const double kp = analytic_kM(a.p, 0.5 * (vc[j] + vc[j + 1]));
-        const double km = analytic_kM(a.p, 0.5 * (vc[j - 1] + vc[j]));
-        vn = ((cm - ad * (kp + km)) * vp[j] + 2.0 * ad * (kp * vc[j + 1] + km * vc[j - 1])) /
-             (cm + ad * (kp + km));
+        const double kp = analytic_kM(a.p, 0.5 * (x.vc + x.vr));
+        const double km = analytic_kM(a.p, 0.5 * (x.vl + x.vc));
+        vn = ((cm - ad * (kp + km)) * x.vp + 2.0 * ad * (kp * x.vr + km * x.vl)) / (cm + ad * (kp + km));
         const double ktp = 1.0, ktm = 1.0, kmp = 1.0, kmm = 1.0;
-        un = ((ctt - b_ * (ktp + ktm)) * up[j] - p.gamma * ctm * (vn - vp[j]) +
-              2.0 * b_ * (ktp * uc[j + 1] + ktm * uc[j - 1]) +
-              2.0 * g_ * (kmp * vc[j + 1] + kmm * vc[j - 1]) - g_ * (kmp + kmm) * (vn + vp[j])) /
+        un = ((ctt - b_ * (ktp + ktm)) * x.up - p.gamma * ctm * (vn - x.vp) +
+              2.0 * b_ * (ktp * x.ur + ktm * x.ul) + 2.0 * g_ * (kmp * x.vr + kmm * x.vl) -
+              g_ * (kmp + kmm) * (vn + x.vp)) /
              (ctt + b_ * (ktp + ktm));
         return;
     }
     const int k = j == 0 ? 0 : 1;
-    const int jn = j == 0 ? 1 : n - 2;
+    const double vcn = j == 0 ? x.vr : x.vl, ucn = j == 0 ? x.ur : x.ul;   // vc[jn], uc[jn]
     const FaceVals b = resolve(a, w, k);
-    const double km_b = analytic_kM(a.p, vc[j]);                       // ghost side: node value
-    const double kp_b = analytic_kM(a.p, j == 0 ? 0.5 * (vc[0] + vc[1]) : 0.5 * (vc[n - 2] + vc[n - 1]));
+    const double km_b = analytic_kM(a.p, x.vc);                        // ghost side: node value
+    const double kp_b = analytic_kM(a.p, j == 0 ? 0.5 * (x.vc + vcn) : 0.5 * (vcn + x.vc));
     const double cpl = 2.0 * ad * dx * b.Bi_M;
-    vn = ((cm - ad * (kp_b + km_b) - cpl) * vp[j] + 2.0 * ad * (kp_b + km_b) * vc[jn] +
+    vn = ((cm - ad * (kp_b + km_b) - cpl) * x.vp + 2.0 * ad * (kp_b + km_b) * vcn +
           4.0 * ad * dx * (b.Bi_M * b.v_inf + b.g_inf)) /
          (cm + ad * (kp_b + km_b) + cpl);
     const double kt_b = 1.0, kTM_b = 1.0, ktp_b = 1.0, kmp_b = 1.0;
-    const double vbar = 0.5 * (vn + vp[j]);
-    const double vg = vc[jn] - (2.0 * dx / km_b) * (b.Bi_M * (vbar - b.v_inf) - b.g_inf);
+    const double vbar = 0.5 * (vn + x.vp);
+    const double vg = vcn - (2.0 * dx / km_b) * (b.Bi_M * (vbar - b.v_inf) - b.g_inf);
     const double cplu = 2.0 * b_ * dx * b.Bi_TT;
-    un = ((ctt - b_ * (ktp_b + kt_b) - cplu) * up[j] - p.gamma * ctm * (vn - vp[j]) +
-          2.0 * b_ * (ktp_b + kt_b) * uc[jn] + 2.0 * b_ * ratio * kTM_b * (vc[jn] - vg) -
+    un = ((ctt - b_ * (ktp_b + kt_b) - cplu) * x.up - p.gamma * ctm * (vn - x.vp) +
+          2.0 * b_ * (ktp_b + kt_b) * ucn + 2.0 * b_ * ratio * kTM_b * (vcn - vg) -
           4.0 * b_ * dx * (b.Bi_TM * (vbar - b.v_inf) - b.q_inf) + 2.0 * cplu * b.u_inf +
-          2.0 * g_ * (kmp_b * vc[jn] + kTM_b * vg) - g_ * (kmp_b + kTM_b) * (vn + vp[j])) /
+          2.0 * g_ * (kmp_b * vcn + kTM_b * vg) - g_ * (kmp_b + kTM_b) * (vn + x.vp)) /
          (ctt + b_ * (ktp_b + kt_b) + cplu);
 }
 
-// One DF step of every wall; guard per node (exact check_bounded semantics).
+// One DF step of one node; guard per node (exact check_bounded semantics).
+// The state loads are issued before the stop flag is read, so they overlap.
 __device__ __forceinline__ void wall_node_step(const StepArgs& a, int64_t tid) {
     const int w = static_cast<int>(tid / a.n), j = static_cast<int>(tid % a.n);
+    const NodeIn x = load_node(a, w, j);
+    if (*a.fail_key != ~0ull) return;    // an earlier step failed: freeze
     double un, vn;
-    if (a.coeff_kind == kCoeffConstant) coupled_node(a, w, j, un, vn);
-    else analytic_node(a, w, j, un, vn);
+    if (a.coeff_kind == kCoeffConstant) coupled_node(a, w, j, x, un, vn);
+    else analytic_node(a, w, j, x, un, vn);
     // only the new layer is written; the host rotates layer pointers
     // (prev <- curr) instead of copying: 32 B read + 16 B written per update
     a.out[1][tid] = un;
@@ -159,10 +175,11 @@ __device__ __forceinline__ void wall_node_step(const StepArgs& a, int64_t tid) {
     }
 }
 
-__global__ void k_df_step_general(const StepArgs a) {
+constexpr int kStepThreads = 256;
+
+__global__ void __launch_bounds__(kStepThreads, 4) k_df_step_general(const StepArgs a) {
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (tid >= static_cast<int64_t>(a.n_walls) * a.n) return;
-    if (*a.fail_key != ~0ull) return;    // an earlier step failed: freeze
     wall_node_step(a, tid);
 }
 
@@ -241,14 +258,14 @@ __global__ void k_zone_step(const ZoneArgs a) {
 // first wall_blocks blocks advance the wall nodes with layer-n zone values,
 // the remaining blocks advance the zones with layer-n surface samples.  Both
 // halves read layer n only and write disjoint buffers.
-__global__ void k_building_step(const StepArgs a, const ZoneArgs z, int wall_blocks) {
-    if (*a.fail_key != ~0ull) return;
+__global__ void __launch_bounds__(kStepThreads, 4) k_building_step(const StepArgs a, const ZoneArgs z,
+                                                                  int wall_blocks) {
     if (static_cast<int>(blockIdx.x) < wall_blocks) {
         const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
         if (tid < static_cast<int64_t>(a.n_walls) * a.n) wall_node_step(a, tid);
     } else {
         const int zi = (static_cast<int>(blockIdx.x) - wall_blocks) * blockDim.x + threadIdx.x;
-        if (zi < z.n_zones) zone_update(z, zi);
+        if (zi < z.n_zones && *z.fail_key == ~0ull) zone_update(z, zi);
     }
 }
 

@@ -70,28 +70,41 @@ __device__ __forceinline__ void tiled_step(const TileCtx<W, THREADS>& c, const T
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
         const int i = c.tid + q * THREADS;
-        if (i >= h0 && i < h1) c.kp[i] = d_of(p, 0.5 * (vc[i] + vc[i + 1]));
+        const double kv = d_of(p, 0.5 * (vc[i] + vc[min(i + 1, W - 1)]));
+        if (i >= h0 && i < h1) c.kp[i] = kv;
     }
     __syncthreads();
-    const Ambient* row = A.table + static_cast<size_t>(k - 1) * A.n_channels;
+    // interior rows, branch-free over the thread's slots (out-of-window slots
+    // compute on clamped neighbours and are not stored): the slots' chains
+    // interleave
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
         const int j = c.tid + q * THREADS;
-        if (j < lo || j >= hi) continue;
+        const bool valid = j >= lo && j < hi && j != c.lf && j != c.rf;
+        const int jl = max(j - 1, 0), jr = min(j + 1, W - 1);
         double vn, un;
-        if (j == c.lf) {
-            analytic_face(rc, A.bl, row[A.chl], vp[j], up[j], vc[j + 1], uc[j + 1], d_of(p, vc[j]), c.kp[j],
-                          vn, un);
-        } else if (j == c.rf) {
-            analytic_face(rc, A.br, row[A.chr], vp[j], up[j], vc[j - 1], uc[j - 1], d_of(p, vc[j]),
-                          c.kp[j - 1], vn, un);
-        } else {
-            analytic_interior(rc, vp[j], up[j], vc[j - 1], vc[j + 1], uc[j - 1], uc[j + 1], c.kp[j - 1],
-                              c.kp[j], vn, un);
+        analytic_interior(rc, vp[j], up[j], vc[jl], vc[jr], uc[jl], uc[jr], c.kp[jl], c.kp[j], vn, un);
+        if (valid) {
+            acc |= static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn));
+            vp[j] = vn;
+            up[j] = un;
         }
-        acc |= static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn));
-        vp[j] = vn;
-        up[j] = un;
+    }
+    if (c.lf >= 0 || c.rf >= 0) {   // the first and the last tile hold the faces
+        const Ambient* row = A.table + static_cast<size_t>(k - 1) * A.n_channels;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int j = c.tid + q * THREADS;
+            if (j != c.lf && j != c.rf) continue;
+            const bool left = j == c.lf;
+            const int jn = left ? j + 1 : j - 1;
+            double vn, un;
+            analytic_face(rc, left ? A.bl : A.br, row[left ? A.chl : A.chr], vp[j], up[j], vc[jn], uc[jn],
+                          d_of(p, vc[j]), c.kp[left ? j : j - 1], vn, un);
+            acc |= static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn));
+            vp[j] = vn;
+            up[j] = un;
+        }
     }
     __syncthreads();
 }

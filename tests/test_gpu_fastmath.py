@@ -1,0 +1,37 @@
+"""The device exp / reciprocal of the d(v) rows (hyg_fastmath.cuh) against
+numpy (correctly rounded to ~0.5 ulp): within 2 ulp on the d(v) argument
+range and beyond, flush-to-zero below -708, NaN propagation."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_1703_10119_b200 import api
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(x):
+    lib = api.load_library()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    e, r = np.empty_like(x), np.empty_like(x)
+    p = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+    assert lib.hyg_selftest_fastmath(0, x.size, p(x), p(e), p(r)) == 0
+    return e, r
+
+
+def _ulps(a, b):
+    return np.abs(a - b) / np.spacing(np.abs(b))
+
+
+def test_fexp_frcp_accuracy():
+    rng = np.random.default_rng(0)
+    x = np.concatenate([rng.uniform(-10.0, 0.0, 200_000),       # d(v): -p2 (v - p3)^2
+                        rng.uniform(-700.0, 700.0, 100_000), np.linspace(-1.0, 1.0, 10_001)])
+    e, r = _run(x)
+    assert _ulps(e, np.exp(x)).max() <= 2.0
+    nz = x[np.abs(x) > 1e-300]
+    _, rr = _run(nz)
+    assert _ulps(rr, 1.0 / nz).max() <= 2.0
+    e2, _ = _run(np.array([-800.0, -708.5, np.nan, 710.0, 0.0]))
+    assert e2[0] == 0.0 and e2[1] == 0.0 and np.isnan(e2[2]) and np.isinf(e2[3]) and e2[4] == 1.0
