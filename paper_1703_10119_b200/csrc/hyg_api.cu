@@ -1164,9 +1164,11 @@ int hyg_set_owned(hyg_ctx* c, int64_t cell0, int64_t cell1, int32_t zone0, int32
     c->own_z1 = zone1;
     c->reduce = reduce;
     c->reduce_user = user;
-    // the fused kernels guard every wall: a shard with a partial ownership
-    // marches on the per-step path, whose guard honours the owned range
-    if (cell0 > 0 || cell1 < c->cells()) c->fused = c->nl_fused = c->tiled = false;
+    // K1/K2 guard every wall: a wall-batch shard with partial ownership marches
+    // on the per-step path, whose guard honours the owned range.  K3 (one long
+    // wall) stays: its fast guard only decides whether to replay on the
+    // per-step path, which then applies the owned range exactly.
+    if (cell0 > 0 || cell1 < c->cells()) c->fused = c->nl_fused = false;
     return HYG_OK;
 }
 
