@@ -445,7 +445,8 @@ int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
         }
         const int nch = std::max<int>(1, static_cast<int>(c->channels.size()));
         const int threads = 256;
-        const int grid = static_cast<int>((c->cells() + threads - 1) / threads);
+        const int cells_per_block = step_cells(c->coeff_kind == HYG_COEFF_CONSTANT ? kCoeffConstant : kCoeffAnalyticD);
+        const int grid = static_cast<int>((c->cells() + cells_per_block - 1) / cells_per_block);
         const int nsrc = static_cast<int>(c->zsrc.size() / 3);
         double* ptr0[2][4];
         std::memcpy(ptr0, c->s64, sizeof ptr0);
@@ -455,7 +456,10 @@ int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
             a.layer = c->layer + k;
             if (c->zones.empty()) {
                 LaunchScope ls(c, "df_step_general", static_cast<double>(c->cells()));
-                k_df_step_general<<<grid, threads, 0, c->stream>>>(a);
+                if (c->coeff_kind == HYG_COEFF_CONSTANT)
+                    k_df_step_general<kCoeffConstant><<<grid, threads, 0, c->stream>>>(a);
+                else
+                    k_df_step_general<kCoeffAnalyticD><<<grid, threads, 0, c->stream>>>(a);
             } else {
                 ZoneArgs z{};
                 z.n_zones = static_cast<int>(c->zones.size());
@@ -479,7 +483,10 @@ int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
                 z.own1 = c->own_z1;
                 const int zblocks = (z.n_zones + threads - 1) / threads;
                 LaunchScope ls(c, "building_step", static_cast<double>(c->cells()));
-                k_building_step<<<grid + zblocks, threads, 0, c->stream>>>(a, z, grid);
+                if (c->coeff_kind == HYG_COEFF_CONSTANT)
+                    k_building_step<kCoeffConstant><<<grid + zblocks, threads, 0, c->stream>>>(a, z, grid);
+                else
+                    k_building_step<kCoeffAnalyticD><<<grid + zblocks, threads, 0, c->stream>>>(a, z, grid);
                 c->zcur ^= 1;
             }
             rotate_layers(c);

@@ -155,32 +155,63 @@ __device__ __forceinline__ void analytic_node(const StepArgs& a, int w, int j, c
          (ctt + b_ * (ktp_b + kt_b) + cplu);
 }
 
-// One DF step of one node; guard per node (exact check_bounded semantics).
-// The state loads are issued before the stop flag is read, so they overlap.
-__device__ __forceinline__ void wall_node_step(const StepArgs& a, int64_t tid) {
-    const int w = static_cast<int>(tid / a.n), j = static_cast<int>(tid % a.n);
-    const NodeIn x = load_node(a, w, j);
+// One DF step of NPT nodes per thread (cells base + k * stride); guard per
+// node (exact check_bounded semantics).  Every state load of all NPT nodes is
+// issued before the stop flag is read and before any arithmetic, so a thread
+// keeps 4·NPT DRAM loads in flight (the per-step path is bound by bytes in
+// flight, profiles/r01_cfg3_cfg0_cfg4_ncu_summary.md).
+template <int NPT, int KIND>
+__device__ __forceinline__ void wall_nodes_step(const StepArgs& a, int64_t base, int stride) {
+    const int64_t total = static_cast<int64_t>(a.n_walls) * a.n;
+    const bool narrow = total <= 0xffffffffll;       // 32-bit cell -> (wall, node)
+    NodeIn x[NPT];
+    int w[NPT], j[NPT];
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+        const int64_t cell = base + static_cast<int64_t>(k) * stride;
+        w[k] = -1;
+        if (cell < total) {
+            if (narrow) {
+                const unsigned c32 = static_cast<unsigned>(cell), n32 = static_cast<unsigned>(a.n);
+                w[k] = static_cast<int>(c32 / n32);
+                j[k] = static_cast<int>(c32 - static_cast<unsigned>(w[k]) * n32);
+            } else {
+                w[k] = static_cast<int>(cell / a.n);
+                j[k] = static_cast<int>(cell - static_cast<int64_t>(w[k]) * a.n);
+            }
+            x[k] = load_node(a, w[k], j[k]);
+        }
+    }
     if (*a.fail_key != ~0ull) return;    // an earlier step failed: freeze
-    double un, vn;
-    if (a.coeff_kind == kCoeffConstant) coupled_node(a, w, j, x, un, vn);
-    else analytic_node(a, w, j, x, un, vn);
-    // only the new layer is written; the host rotates layer pointers
-    // (prev <- curr) instead of copying: 32 B read + 16 B written per update
-    a.out[1][tid] = un;
-    a.out[3][tid] = vn;
-    if (tid >= a.own0 && tid < a.own1 && (!(fabs(un) <= a.norm) || !(fabs(vn) <= a.norm))) {
-        const unsigned long long key =
-            (static_cast<unsigned long long>(a.layer + 1) << 32) | static_cast<unsigned>(w);
-        atomicMin(a.fail_key, key);
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+        if (w[k] < 0) continue;
+        const int64_t cell = base + static_cast<int64_t>(k) * stride;
+        double un, vn;
+        if (KIND == kCoeffConstant) coupled_node(a, w[k], j[k], x[k], un, vn);
+        else analytic_node(a, w[k], j[k], x[k], un, vn);
+        // only the new layer is written; the host rotates layer pointers
+        // (prev <- curr) instead of copying: 32 B read + 16 B written per update
+        a.out[1][cell] = un;
+        a.out[3][cell] = vn;
+        if (cell >= a.own0 && cell < a.own1 && (!(fabs(un) <= a.norm) || !(fabs(vn) <= a.norm))) {
+            const unsigned long long key =
+                (static_cast<unsigned long long>(a.layer + 1) << 32) | static_cast<unsigned>(w[k]);
+            atomicMin(a.fail_key, key);
+        }
     }
 }
 
 constexpr int kStepThreads = 256;
+// nodes per thread of the per-step kernels: two for the lean constant rows,
+// one for the d(v) rows (two would spill at the 64-register budget)
+__host__ __device__ constexpr int step_npt(int kind) { return kind == kCoeffConstant ? 2 : 1; }
+__host__ __device__ constexpr int step_cells(int kind) { return kStepThreads * step_npt(kind); }
 
-__global__ void __launch_bounds__(kStepThreads, 4) k_df_step_general(const StepArgs a) {
-    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (tid >= static_cast<int64_t>(a.n_walls) * a.n) return;
-    wall_node_step(a, tid);
+template <int KIND>
+__global__ void __launch_bounds__(kStepThreads, KIND == kCoeffConstant ? 4 : 3) k_df_step_general(const StepArgs a) {
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * step_cells(KIND) + threadIdx.x;
+    wall_nodes_step<step_npt(KIND), KIND>(a, base, kStepThreads);
 }
 
 // ---- zones -----------------------------------------------------------------
@@ -258,11 +289,12 @@ __global__ void k_zone_step(const ZoneArgs a) {
 // first wall_blocks blocks advance the wall nodes with layer-n zone values,
 // the remaining blocks advance the zones with layer-n surface samples.  Both
 // halves read layer n only and write disjoint buffers.
-__global__ void __launch_bounds__(kStepThreads, 4) k_building_step(const StepArgs a, const ZoneArgs z,
+template <int KIND>
+__global__ void __launch_bounds__(kStepThreads, KIND == kCoeffConstant ? 4 : 3) k_building_step(const StepArgs a, const ZoneArgs z,
                                                                   int wall_blocks) {
     if (static_cast<int>(blockIdx.x) < wall_blocks) {
-        const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-        if (tid < static_cast<int64_t>(a.n_walls) * a.n) wall_node_step(a, tid);
+        const int64_t base = static_cast<int64_t>(blockIdx.x) * step_cells(KIND) + threadIdx.x;
+        wall_nodes_step<step_npt(KIND), KIND>(a, base, kStepThreads);
     } else {
         const int zi = (static_cast<int>(blockIdx.x) - wall_blocks) * blockDim.x + threadIdx.x;
         if (zi < z.n_zones && *z.fail_key == ~0ull) zone_update(z, zi);
