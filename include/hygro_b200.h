@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define HYG_ABI_VERSION 1
+#define HYG_ABI_VERSION 2
 
 /* ---- return codes (errors.hpp:8-45) ------------------------------------ */
 enum {
@@ -96,6 +96,16 @@ typedef struct {
 
 enum { HYG_MOISTURE_AS_PRINTED = 0, HYG_MOISTURE_FLUX_CONSISTENT = 1 }; /* zone.hpp:21 */
 
+/* Long-wave exchange between two wall surfaces bounding a zone: the flux
+ * s*eps*sigma*(T_e^4 - T_r^4) [W/m2] is added to the receiver face's imposed
+ * heat flux, scaled by L/(T_i k_TT0) of the receiving wall (RadiationLink
+ * zone.hpp:39-45, radiative_flux zone.cpp:55-67, radiation_fluxes
+ * building.cpp:88-105). */
+typedef struct {
+    int32_t emitter_wall, receiver_wall;
+    double view_factor, emissivity;
+} hyg_radiation_link;
+
 typedef struct {
     double kappa_a_tt1, g_v, q_v1, q_v2;    /* ZoneDimensionless scaling.hpp:61-67 */
     int32_t sources;                        /* index into hyg_model_desc::zone_sources */
@@ -104,7 +114,9 @@ typedef struct {
     const hyg_zone_wall_link* walls;
     int32_t n_interzone;
     const hyg_interzone_link* interzone;
-} hyg_zone_desc;                            /* ZoneConfig zone.hpp:47-54 (no radiation) */
+    int32_t n_radiation;                    /* ABI 2: ZoneConfig::radiation            */
+    const hyg_radiation_link* radiation;
+} hyg_zone_desc;                            /* ZoneConfig zone.hpp:47-54 */
 
 /* ---- coefficient models (CoefficientModel wall.hpp:41-60) -------------- */
 enum {
@@ -112,8 +124,20 @@ enum {
     /* Device functor (API extension; the reference can only express it through
      * the test oracle's StarFn callback, tests/support/df_oracle.hpp:19):
      *   k_M*(u,v) = 1 + p0*v + p1*exp(-p2*(v - p3)^2), other five starred coefficients 1 */
-    HYG_COEFF_ANALYTIC_D = 1
+    HYG_COEFF_ANALYTIC_D = 1,
+    /* CoefficientModel::material (wall.cpp:33-58): the load-bearing material
+     * correlations (MaterialModel::evaluate materials.cpp:91-114, default
+     * PhysicalConstants materials.hpp:7-15) at (u*T_i, v*P_vi), divided by the
+     * wall's reference set.  Strict in DF steps (box violation -> HYG_EDOMAIN
+     * naming wall and node / half node, wall.cpp:99-126), clamped in the
+     * starting steps (evaluate_clamped materials.cpp:116-121).  Per wall through
+     * hyg_model_desc::wall_coeff (constant walls keep df_step_coupled,
+     * building.cpp:172-176). */
+    HYG_COEFF_MATERIAL = 2
 };
+
+/* CoefficientSet materials.hpp:21-28 */
+typedef struct { double c_M, k_M, c_TT, k_TT, c_TM, k_TM; } hyg_coeff_set;
 
 enum { HYG_F64 = 0, HYG_F32 = 1 };
 enum { HYG_BOOT_IMPLICIT = 0, HYG_BOOT_EXPLICIT = 1 };
@@ -140,6 +164,14 @@ typedef struct {
     double eta_factor;                /* BuildingModel::eta_factor (implicit bootstrap)  */
     int32_t max_subiters;             /* BuildingModel::max_subiters                     */
     int32_t device;                   /* CUDA ordinal                                    */
+    /* ---- ABI 2: material walls and radiation -------------------------------- */
+    double T_i, P_vi;                 /* ScalingContext (scaling.hpp:11-16)              */
+    const int32_t* wall_coeff;        /* [n_walls] HYG_COEFF_CONSTANT / _MATERIAL when
+                                         coeff_kind == HYG_COEFF_MATERIAL; NULL: all material */
+    const hyg_coeff_set* wall_reference; /* [n_walls] CoefficientModel::reference_ of
+                                         material walls (NULL only without material walls) */
+    const double* wall_thickness;     /* [n_walls] BuildingWall::thickness (radiation)   */
+    const double* wall_k_TT0;         /* [n_walls] BuildingWall::k_TT0     (radiation)   */
 } hyg_model_desc;
 
 typedef struct {
@@ -150,6 +182,8 @@ typedef struct {
     int64_t layer;           /* time-layer index after the failing step        */
     double t_star;           /* numerical_error::t_star                         */
     double residual;         /* convergence_error::residual                    */
+    int32_t node;            /* ABI 2, HYG_EDOMAIN: node j, or half node j+1/2  */
+    int32_t half;            /*   when half == 1 (StarTables wall.cpp:105-126)  */
     char message[256];
 } hyg_status;
 
@@ -239,6 +273,10 @@ int hyg_run(hyg_ctx* ctx, double horizon, double cadence, int32_t boot_kind,
  * materials.hpp:21-28).  Scaling context from (T_i [K], phi_i, t_0 [s]),
  * ScalingContext::from_state scaling.cpp:20-28. */
 int hyg_saturation_pressure(double T, double* out);                         /* materials.cpp:33-40 */
+/* MaterialModel::evaluate / evaluate_clamped (materials.cpp:91-121) on the
+ * host: e.g. the reference set of a material wall, evaluate(T_i, P_vi)
+ * (scenario.cpp:178).  HYG_EDOMAIN outside the admissible box. */
+int hyg_material_evaluate(double T, double P_v, int32_t clamped, hyg_coeff_set* out);
 int hyg_scale_wall(const double reference[6], double L, double h_T0, double h_M0, double h_T1,
                    double h_M1, double T_i, double phi_i, double t_0, hyg_wall_groups* groups,
                    hyg_face_biot face[2]);                                   /* scaling.cpp:30-58 */

@@ -86,6 +86,8 @@ _ORACLE_PROTOS = {
                                     _ip, A.dp]),
     "orc_run": (C.c_int, [C.POINTER(A.ModelDesc), C.POINTER(BuildingState), C.c_int64, _i64p, _ip, _ip]),
     "orc_set_owned": (None, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "orc_last_domain": (None, [_ip, _ip]),
+    "orc_last_domain_wall": (C.c_int, []),
 }
 
 REDUCE_FN = C.CFUNCTYPE(C.c_double, C.c_void_p, C.c_double)
@@ -108,6 +110,7 @@ _REF_PROTOS = {
                                      _i64p, _ip]),
     "ref_run": (C.c_int, [C.POINTER(A.ModelDesc), C.c_double, A.dp, A.dp, A.dp, A.dp, C.POINTER(C.c_long), A.dp]),
     "ref_hardware_threads": (C.c_int, []),
+    "ref_last_domain": (None, [_ip, _ip, _ip]),
 }
 
 _cache: dict = {}
@@ -195,10 +198,15 @@ class WallBatch:
 
 
 def coeff_model(model) -> CoeffModel:
+    """One coefficient model for a whole batch (material: wall 0's reference set)."""
     m = CoeffModel()
     if model.coeff_kind == "analytic_d":
         m.kind = ORC_COEFF_ANALYTIC_D
         m.p = (C.c_double * 4)(*model.coeff_params)
+    elif model.coeff_kind == "material":
+        m.kind = ORC_COEFF_MATERIAL
+        m.T_i, m.P_vi = model.T_i, model.P_vi
+        m.reference = Coeffs(*map(float, model.wall_reference[0]))
     else:
         m.kind = ORC_COEFF_CONSTANT
     return m
@@ -218,6 +226,9 @@ def march(impl: str, wb: WallBatch, nsteps: int, dt: float, nthreads: int = 1):
         lib = ref_lib()
         if m.kind == ORC_COEFF_CONSTANT:
             rc = lib.ref_march_coupled(C.byref(wb.b), nsteps, dt, nthreads, C.byref(fl), C.byref(fw))
+        elif m.kind == ORC_COEFF_MATERIAL:
+            rc = lib.ref_march_nonlinear_material(C.byref(wb.b), C.byref(m), nsteps, dt, nthreads, C.byref(fl),
+                                                  C.byref(fw))
         else:   # d(v) is expressible only through the reference's test oracle (df_oracle.hpp)
             rc = lib.ref_oracle_march_analytic(C.byref(wb.b), C.byref(m), nsteps, dt, nthreads, C.byref(fl), C.byref(fw))
     return rc, fl.value, fw.value
@@ -268,8 +279,23 @@ class Building:
             else:
                 rc = 0
                 for _ in range(nsteps):
-                    lib.orc_step_explicit(C.byref(self.desc), C.byref(self.s))
+                    rc = lib.orc_step_explicit(C.byref(self.desc), C.byref(self.s))
+                    if rc:
+                        fl.value = self.s.layer + 1
+                        break
         else:
             rc = ref_lib().ref_building_march(C.byref(self.desc), C.byref(self.s), nsteps, int(with_bootstrap),
                                               C.byref(fl), C.byref(bp))
         return rc, fl.value, bp.value
+
+    @staticmethod
+    def domain(impl: str):
+        """(wall, node, half) of the last HYG_EDOMAIN of a building march."""
+        w, j, h = C.c_int(-1), C.c_int(-1), C.c_int(0)
+        if impl == "oracle":
+            lib = oracle_lib()
+            lib.orc_last_domain(C.byref(j), C.byref(h))
+            w.value = lib.orc_last_domain_wall()
+        else:
+            ref_lib().ref_last_domain(C.byref(w), C.byref(j), C.byref(h))
+        return w.value, j.value, bool(h.value)

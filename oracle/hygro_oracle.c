@@ -176,6 +176,14 @@ void orc_df_step_coupled(orc_field* f, double dx, const hyg_wall_groups* p, cons
 /* StarTables (wall.cpp:89-138): node[n], half[n-1]; NULL tables = unit */
 typedef struct { orc_coeffs* node; orc_coeffs* half; int unit; } star_tables;
 
+/* where the last strict evaluation left the box: node j or half node j+1/2
+ * (the "[node j]" / "[half node j+1/2]" annotation of wall.cpp:105-126) */
+static int g_dom_node = -1, g_dom_half = 0;
+void orc_last_domain(int* node, int* half) {
+    *node = g_dom_node;
+    *half = g_dom_half;
+}
+
 static int build_tables(star_tables* s, const orc_model* m, int n, const double* u,
                         const double* v, int strict) {
     s->node = s->half = NULL;
@@ -185,13 +193,21 @@ static int build_tables(star_tables* s, const orc_model* m, int n, const double*
     s->half = s->node + n;
     for (int j = 0; j < n; ++j) {
         const int rc = orc_star(m, u[j], v[j], strict, &s->node[j]);
-        if (rc) return rc;
+        if (rc) {
+            g_dom_node = j;
+            g_dom_half = 0;
+            return rc;
+        }
     }
     for (int j = 0; j + 1 < n; ++j) {
         const double um = 0.5 * (u[j] + u[j + 1]);
         const double vm = 0.5 * (v[j] + v[j + 1]);
         const int rc = orc_star(m, um, vm, strict, &s->half[j]);
-        if (rc) return rc;
+        if (rc) {
+            g_dom_node = j;
+            g_dom_half = 1;
+            return rc;
+        }
     }
     return 0;
 }
@@ -687,8 +703,9 @@ void orc_zone_rhs(const hyg_model_desc* m, int zi, double u_a, double v_a, const
 }
 
 /* resolve_face (building.cpp:107-126) without radiation */
+/* resolve_face (building.cpp:107-126); q_rad = radiation flux of this face */
 static void resolve_face(const hyg_model_desc* m, int w, int k, const double* zu, const double* zv,
-                         double t, orc_face* f) {
+                         double t, double q_rad, orc_face* f) {
     const hyg_face_biot* bi = &m->biot[2 * w + k];
     const hyg_face_attach* a = &m->attach[2 * w + k];
     f->Bi_M = bi->Bi_M;
@@ -699,13 +716,69 @@ static void resolve_face(const hyg_model_desc* m, int w, int k, const double* zu
         f->u_inf = orc_signal(&c->u_inf, t);
         f->v_inf = orc_signal(&c->v_inf, t);
         f->g_inf = orc_signal(&c->g_inf, t);
-        f->q_inf = orc_signal(&c->q_inf, t) + 0.0;
+        f->q_inf = orc_signal(&c->q_inf, t) + q_rad;
     } else {
         f->u_inf = zu[a->index];
         f->v_inf = zv[a->index];
         f->g_inf = 0.0;
-        f->q_inf = 0.0;
+        f->q_inf = q_rad;
     }
+}
+
+/* Per-wall coefficient model of a building (BuildingWall::coeffs): constant,
+ * the analytic functor, or CoefficientModel::material (wall.cpp:33-41). */
+static void wall_model(const hyg_model_desc* m, int w, orc_model* out) {
+    memset(out, 0, sizeof *out);
+    out->kind = ORC_COEFF_CONSTANT;
+    if (m->coeff_kind == HYG_COEFF_ANALYTIC_D) {
+        out->kind = ORC_COEFF_ANALYTIC_D;
+        memcpy(out->p, m->coeff_params, sizeof out->p);
+    } else if (m->coeff_kind == HYG_COEFF_MATERIAL &&
+               (m->wall_coeff == NULL || m->wall_coeff[w] == HYG_COEFF_MATERIAL)) {
+        const hyg_coeff_set* r = &m->wall_reference[w];
+        out->kind = ORC_COEFF_MATERIAL;
+        out->T_i = m->T_i;
+        out->P_vi = m->P_vi;
+        out->reference.c_M = r->c_M;
+        out->reference.k_M = r->k_M;
+        out->reference.c_TT = r->c_TT;
+        out->reference.k_TT = r->k_TT;
+        out->reference.c_TM = r->c_TM;
+        out->reference.k_TM = r->k_TM;
+    }
+}
+
+/* radiation_fluxes (building.cpp:88-105) with zone_surface_u (:77-86) and
+ * radiative_flux (zone.cpp:55-67) from the wall temperature layer u
+ * ([n_walls][n]); q[2*w+face] (zeroed here). */
+static void radiation_fluxes(const hyg_model_desc* m, const double* u, double* q) {
+    const int n = m->n_nodes, nw = m->n_walls;
+    const double sigma = 5.67e-8;                 /* PhysicalConstants materials.hpp:14 */
+    for (int i = 0; i < 2 * nw; ++i) q[i] = 0.0;
+    double* surf = (double*)malloc(sizeof(double) * (size_t)(nw + 1));
+    for (int z = 0; z < m->n_zones; ++z) {
+        const hyg_zone_desc* zd = &m->zones[z];
+        if (zd->n_radiation == 0) continue;
+        for (int i = 0; i < nw; ++i) surf[i] = 0.0;
+        for (int i = 0; i < zd->n_walls; ++i) {
+            const hyg_zone_wall_link* l = &zd->walls[i];
+            surf[l->wall] = u[(size_t)l->wall * (size_t)n + (l->face == 0 ? 0 : (size_t)(n - 1))];
+        }
+        for (int i = 0; i < zd->n_walls; ++i) {
+            const hyg_zone_wall_link* l = &zd->walls[i];
+            double q_rw = 0.0;
+            for (int r = 0; r < zd->n_radiation; ++r) {
+                const hyg_radiation_link* rl = &zd->radiation[r];
+                if (rl->receiver_wall != l->wall) continue;
+                const double Te = surf[rl->emitter_wall] * m->T_i;
+                const double Tr = surf[rl->receiver_wall] * m->T_i;
+                q_rw += rl->view_factor * rl->emissivity * sigma * (Te * Te * Te * Te - Tr * Tr * Tr * Tr);
+            }
+            if (q_rw != 0.0)
+                q[2 * l->wall + l->face] += m->wall_thickness[l->wall] * q_rw / (m->T_i * m->wall_k_TT0[l->wall]);
+        }
+    }
+    free(surf);
 }
 
 static orc_field bfield(const hyg_model_desc* m, orc_building_state* s, int w) {
@@ -715,6 +788,9 @@ static orc_field bfield(const hyg_model_desc* m, orc_building_state* s, int w) {
 }
 
 static int face_node(const hyg_model_desc* m, int face) { return face == 0 ? 0 : m->n_nodes - 1; }
+
+static int g_dom_wall = -1;
+int orc_last_domain_wall(void) { return g_dom_wall; }
 
 int orc_step_explicit(const hyg_model_desc* m, orc_building_state* s) { /* building.cpp:152-187 */
     const double t = s->t;
@@ -737,13 +813,27 @@ int orc_step_explicit(const hyg_model_desc* m, orc_building_state* s) { /* build
             vs[o] = s->vc[idx];
         }
     }
+    double* qr = (double*)malloc(sizeof(double) * (size_t)(2 * m->n_walls + 1));
+    radiation_fluxes(m, s->uc, qr);                 /* from layer n (building.cpp:158) */
     for (int w = 0; w < m->n_walls; ++w) {
         orc_face L, R;
-        resolve_face(m, w, 0, zu0, zv0, t, &L);
-        resolve_face(m, w, 1, zu0, zv0, t, &R);
+        resolve_face(m, w, 0, zu0, zv0, t, qr[2 * w], &L);
+        resolve_face(m, w, 1, zu0, zv0, t, qr[2 * w + 1], &R);
         orc_field f = bfield(m, s, w);
-        orc_df_step_coupled(&f, m->dx, &m->groups[w], &L, &R, dt);
+        orc_model wm;
+        wall_model(m, w, &wm);
+        if (wm.kind == ORC_COEFF_CONSTANT) {
+            orc_df_step_coupled(&f, m->dx, &m->groups[w], &L, &R, dt);
+        } else if (orc_df_step_nonlinear(&f, m->dx, &m->groups[w], &wm, &L, &R, dt)) {
+            /* domain_error propagates out of step_explicit (building.cpp:175) */
+            g_dom_wall = w;
+            free(qr);
+            free(us);
+            free(zu0);
+            return HYG_EDOMAIN;
+        }
     }
+    free(qr);
     const double u_out = orc_signal(&m->outdoor_u, t), v_out = orc_signal(&m->outdoor_v, t);
     for (int z = 0, o = 0; z < nz; ++z) {
         double du, dv;
@@ -828,6 +918,7 @@ int orc_step_implicit(const hyg_model_desc* m, orc_building_state* s, double eta
     memcpy(izu, s->zu, sizeof(double) * (size_t)nz);
     memcpy(izv, s->zv, sizeof(double) * (size_t)nz);
     const double u_out = orc_signal(&m->outdoor_u, t1), v_out = orc_signal(&m->outdoor_v, t1);
+    double* qr = (double*)malloc(sizeof(double) * (size_t)(2 * nw + 1));
     int pass = 0;
     double diff = 0.0;
     int rc = 0;
@@ -836,13 +927,16 @@ int orc_step_implicit(const hyg_model_desc* m, orc_building_state* s, double eta
         diff = 0.0;
         memcpy(snu, izu, sizeof(double) * (size_t)nz);
         memcpy(snv, izv, sizeof(double) * (size_t)nz);
+        radiation_fluxes(m, iu, qr);          /* refreshed from the iterate (building.cpp:212) */
         for (int w = 0; w < nw; ++w) {
             orc_face L, R;
-            resolve_face(m, w, 0, snu, snv, t1, &L);
-            resolve_face(m, w, 1, snu, snv, t1, &R);
+            resolve_face(m, w, 0, snu, snv, t1, qr[2 * w], &L);
+            resolve_face(m, w, 1, snu, snv, t1, qr[2 * w + 1], &R);
             orc_field base = bfield(m, s, w);
             const size_t o = (size_t)w * (size_t)n;
-            orc_implicit_wall_pass(&base, m->dx, &m->groups[w], NULL, &L, &R, dt, iu + o, iv + o,
+            orc_model wm;
+            wall_model(m, w, &wm);
+            orc_implicit_wall_pass(&base, m->dx, &m->groups[w], &wm, &L, &R, dt, iu + o, iv + o,
                                    uN + o, vN + o);
             for (int j = 0; j < n && w >= g_own_w0 && w < g_own_w1; ++j) {
                 diff = fmax(diff, fabs(uN[o + j] - iu[o + j]));
@@ -884,6 +978,7 @@ int orc_step_implicit(const hyg_model_desc* m, orc_building_state* s, double eta
     }
     if (passes) *passes = pass;
     if (residual) *residual = diff;
+    free(qr);
     free(iu);
     free(izu);
     return rc;
@@ -928,7 +1023,11 @@ int orc_run(const hyg_model_desc* m, orc_building_state* s, int64_t nsteps, int6
         ++done;
     }
     while (done < nsteps) {
-        orc_step_explicit(m, s);
+        if (orc_step_explicit(m, s) == HYG_EDOMAIN) {
+            if (fail_layer) *fail_layer = s->layer + 1;
+            if (fail_wall) *fail_wall = g_dom_wall;
+            return HYG_EDOMAIN;
+        }
         int w;
         if (orc_check_bounded(m, s, &w)) {
             if (fail_layer) *fail_layer = s->layer;

@@ -229,12 +229,21 @@ BuildingModel building_of(const hyg_model_desc* d) {
     m.max_subiters = d->max_subiters;
     m.outdoor_u = to_signal(d->outdoor_u);
     m.outdoor_v = to_signal(d->outdoor_v);
+    m.ctx.T_i = d->T_i;
+    m.ctx.P_vi = d->P_vi;
     for (int w = 0; w < d->n_walls; ++w) {
         BuildingWall bw;
         bw.name = "w" + std::to_string(w);
         bw.grid = Grid1D{d->n_nodes, d->dx};
         bw.groups = groups_of(d->groups[w]);
         bw.coeffs = CoefficientModel::constant();
+        if (d->coeff_kind == HYG_COEFF_MATERIAL && (!d->wall_coeff || d->wall_coeff[w] == HYG_COEFF_MATERIAL)) {
+            const hyg_coeff_set& r = d->wall_reference[w];
+            bw.coeffs = CoefficientModel::material(MaterialModel{}, m.ctx,
+                                                   CoefficientSet{r.c_M, r.k_M, r.c_TT, r.k_TT, r.c_TM, r.k_TM});
+        }
+        if (d->wall_thickness) bw.thickness = d->wall_thickness[w];
+        if (d->wall_k_TT0) bw.k_TT0 = d->wall_k_TT0[w];
         for (int k = 0; k < 2; ++k) {
             bw.biot[k].Bi_M = d->biot[2 * w + k].Bi_M;
             bw.biot[k].Bi_TT = d->biot[2 * w + k].Bi_TT;
@@ -286,6 +295,14 @@ BuildingModel building_of(const hyg_model_desc* d) {
             l.q_inz1 = zd.interzone[i].q_inz1;
             l.q_inz2 = zd.interzone[i].q_inz2;
             zc.interzone.push_back(l);
+        }
+        for (int i = 0; i < zd.n_radiation; ++i) {
+            RadiationLink r;
+            r.emitter_wall = zd.radiation[i].emitter_wall;
+            r.receiver_wall = zd.radiation[i].receiver_wall;
+            r.view_factor = zd.radiation[i].view_factor;
+            r.emissivity = zd.radiation[i].emissivity;
+            zc.radiation.push_back(r);
         }
         m.zones.push_back(zc);
     }
@@ -413,6 +430,17 @@ int ref_attach_wall(const orc_coeffs* ref, double area, double L, double volume,
 
 // Building: step_implicit bootstrap + step_explicit loop with check_bounded, i.e.
 // run() (building.cpp:303-356) but returning both time layers.  State arrays in/out.
+// Location of the last domain_error of ref_building_march: the failing wall is
+// the first wall whose t_star did not advance (step_explicit steps walls in
+// order, building.cpp:166-177); node / half node parsed from the annotation
+// df_step_nonlinear adds (wall.cpp:105-126).
+static int g_ref_dom_wall = -1, g_ref_dom_node = -1, g_ref_dom_half = 0;
+void ref_last_domain(int* wall, int* node, int* half) {
+    *wall = g_ref_dom_wall;
+    *node = g_ref_dom_node;
+    *half = g_ref_dom_half;
+}
+
 int ref_building_march(const hyg_model_desc* d, orc_building_state* s, int64_t nsteps,
                        int with_bootstrap, int64_t* fail_layer, int* boot_passes) {
     const BuildingModel m = building_of(d);
@@ -455,6 +483,18 @@ int ref_building_march(const hyg_model_desc* d, orc_building_state* s, int64_t n
         }
     } catch (const convergence_error&) {
         rc = HYG_ECONVERGE;
+    } catch (const domain_error& e) {
+        rc = HYG_EDOMAIN;
+        if (fail_layer) *fail_layer = s->layer + 1;
+        g_ref_dom_wall = -1;
+        for (std::size_t i = 0; i < st.walls.size(); ++i)
+            if (st.walls[i].t_star == st.t) { g_ref_dom_wall = static_cast<int>(i); break; }
+        const std::string msg = e.what();
+        const auto hp = msg.rfind("[half node ");
+        const auto np = msg.rfind("[node ");
+        g_ref_dom_half = hp != std::string::npos;
+        g_ref_dom_node = g_ref_dom_half ? std::atoi(msg.c_str() + hp + 11)
+                                        : (np != std::string::npos ? std::atoi(msg.c_str() + np + 6) : -1);
     }
     for (int w = 0; w < d->n_walls; ++w) {
         const size_t o = static_cast<size_t>(w) * n;
@@ -498,6 +538,8 @@ int ref_run(const hyg_model_desc* d, double horizon, double* uc, double* vc, dou
         return HYG_ECONVERGE;
     } catch (const schema_error&) {
         return HYG_ESCHEMA;
+    } catch (const domain_error&) {
+        return HYG_EDOMAIN;
     }
 }
 

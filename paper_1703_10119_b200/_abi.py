@@ -12,7 +12,7 @@ HYG_OK, HYG_EINVAL, HYG_ESCHEMA, HYG_EDIVERGED, HYG_EDOMAIN, HYG_ECONVERGE, HYG_
 HYG_SIG_CONSTANT, HYG_SIG_SIN, HYG_SIG_SIN2 = 0, 1, 2
 HYG_FACE_EXTERIOR, HYG_FACE_ZONE = 0, 1
 HYG_MOISTURE_AS_PRINTED, HYG_MOISTURE_FLUX_CONSISTENT = 0, 1
-HYG_COEFF_CONSTANT, HYG_COEFF_ANALYTIC_D = 0, 1
+HYG_COEFF_CONSTANT, HYG_COEFF_ANALYTIC_D, HYG_COEFF_MATERIAL = 0, 1, 2
 HYG_F64, HYG_F32 = 0, 1
 HYG_BOOT_IMPLICIT, HYG_BOOT_EXPLICIT = 0, 1
 
@@ -62,11 +62,22 @@ class InterzoneLink(C.Structure):
     _fields_ = [("peer", C.c_int32), ("g_inz", C.c_double), ("q_inz1", C.c_double), ("q_inz2", C.c_double)]
 
 
+class RadiationLink(C.Structure):
+    _fields_ = [("emitter_wall", C.c_int32), ("receiver_wall", C.c_int32), ("view_factor", C.c_double),
+                ("emissivity", C.c_double)]
+
+
+class CoeffSet(C.Structure):
+    _fields_ = [("c_M", C.c_double), ("k_M", C.c_double), ("c_TT", C.c_double), ("k_TT", C.c_double),
+                ("c_TM", C.c_double), ("k_TM", C.c_double)]
+
+
 class ZoneDesc(C.Structure):
     _fields_ = [("kappa_a_tt1", C.c_double), ("g_v", C.c_double), ("q_v1", C.c_double), ("q_v2", C.c_double),
                 ("sources", C.c_int32), ("moisture_sign", C.c_int32), ("n_walls", C.c_int32),
                 ("walls", C.POINTER(ZoneWallLink)), ("n_interzone", C.c_int32),
-                ("interzone", C.POINTER(InterzoneLink))]
+                ("interzone", C.POINTER(InterzoneLink)), ("n_radiation", C.c_int32),
+                ("radiation", C.POINTER(RadiationLink))]
 
 
 class ModelDesc(C.Structure):
@@ -78,13 +89,15 @@ class ModelDesc(C.Structure):
                 ("n_zone_sources", C.c_int32), ("zone_sources", C.POINTER(ZoneSources)),
                 ("outdoor_u", Signal), ("outdoor_v", Signal), ("dt", C.c_double),
                 ("divergence_norm", C.c_double), ("eta_factor", C.c_double), ("max_subiters", C.c_int32),
-                ("device", C.c_int32)]
+                ("device", C.c_int32), ("T_i", C.c_double), ("P_vi", C.c_double),
+                ("wall_coeff", C.POINTER(C.c_int32)), ("wall_reference", C.POINTER(CoeffSet)),
+                ("wall_thickness", dp), ("wall_k_TT0", dp)]
 
 
 class Status(C.Structure):
     _fields_ = [("code", C.c_int32), ("wall", C.c_int32), ("zone", C.c_int32), ("subiterations", C.c_int32),
                 ("layer", C.c_int64), ("t_star", C.c_double), ("residual", C.c_double),
-                ("message", C.c_char * 256)]
+                ("node", C.c_int32), ("half", C.c_int32), ("message", C.c_char * 256)]
 
 
 FRAME_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_double, C.c_void_p)
@@ -125,6 +138,7 @@ PROTOTYPES = {
     "hyg_probe_fp32_peak": (C.c_int, [C.c_int32, dp]),
     "hyg_selftest_fastmath": (C.c_int, [C.c_int32, C.c_int32, dp, dp, dp]),
     "hyg_saturation_pressure": (C.c_int, [C.c_double, dp]),
+    "hyg_material_evaluate": (C.c_int, [C.c_double, C.c_double, C.c_int32, C.POINTER(CoeffSet)]),
     "hyg_scale_wall": (C.c_int, [dp, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                  C.c_double, C.c_double, C.c_double, C.POINTER(WallGroups), C.POINTER(FaceBiot)]),
     "hyg_scale_zone": (C.c_int, [C.c_double] * 8 + [dp]),

@@ -65,7 +65,17 @@ class NumericalError(HygroError):
 
 
 class DomainError(HygroError):
+    """hygro::domain_error of a strict coefficient evaluation (wall.cpp:99-126):
+    the wall, the node j (half=False) or half node j+1/2 (half=True), and the
+    time layer whose step failed (the state stays at the layer before it)."""
     code = A.HYG_EDOMAIN
+
+    def __init__(self, message, status=None):
+        super().__init__(message, status)
+        self.wall = status.wall if status is not None else -1
+        self.node = status.node if status is not None else -1
+        self.half = bool(status.half) if status is not None else False
+        self.layer = status.layer if status is not None else -1
 
 
 class ConvergenceError(HygroError):
@@ -172,6 +182,7 @@ class ZoneSpec:
     moisture_sign: int = A.HYG_MOISTURE_FLUX_CONSISTENT
     walls: Sequence[tuple] = ()      # (wall, face, Bi_M, Bi_TT, Bi_TM, theta_T, theta_M)
     interzone: Sequence[tuple] = ()  # (peer, g_inz, q_inz1, q_inz2)
+    radiation: Sequence[tuple] = ()  # (emitter_wall, receiver_wall, view_factor, emissivity)
 
 
 @dataclass
@@ -186,12 +197,16 @@ class Model:
 
     groups: (W,4) [Fo_M, Fo_TT, Fo_TM, gamma]; biot: (W,2,3) [Bi_M, Bi_TT, Bi_TM] per face;
     attach: (W,2,2) [kind, index] per face (kind 0 = exterior channel, 1 = zone).
+    coeff_kind "material": CoefficientModel::material with ScalingContext (T_i, P_vi),
+    wall_reference (W,6) [c_M, k_M, c_TT, k_TT, c_TM, k_TM] and wall_material (W,) bool
+    (None = every wall); wall_thickness / wall_k_TT0 (W,) scale zone radiation fluxes.
     """
 
     def __init__(self, n_nodes: int, dx: float, groups, biot, attach=None, channels=(ChannelSpec(),),
                  zones=(), zone_sources=(), outdoor_u=None, outdoor_v=None, dt=1e-3,
                  divergence_norm=1e3, eta_factor=1e-2, max_subiters=100, precision="f64",
-                 coeff_kind="constant", coeff_params=(0.0, 0.0, 0.0, 0.0), device=0):
+                 coeff_kind="constant", coeff_params=(0.0, 0.0, 0.0, 0.0), device=0, T_i=293.15,
+                 P_vi=None, wall_reference=None, wall_material=None, wall_thickness=None, wall_k_TT0=None):
         self.groups = np.ascontiguousarray(groups, dtype=np.float64).reshape(-1, 4)
         self.n_walls = self.groups.shape[0]
         self.biot = np.ascontiguousarray(biot, dtype=np.float64).reshape(self.n_walls, 2, 3)
@@ -210,12 +225,25 @@ class Model:
         self.coeff_kind = coeff_kind
         self.coeff_params = tuple(float(x) for x in coeff_params)
         self.device = int(device)
+        self.T_i = float(T_i)
+        self.P_vi = float(P_vi) if P_vi is not None else 0.0
+        W = self.n_walls
+        self.wall_reference = (None if wall_reference is None else
+                               np.ascontiguousarray(wall_reference, dtype=np.float64).reshape(W, 6))
+        self.wall_material = (None if wall_material is None else
+                              np.ascontiguousarray(np.asarray(wall_material, dtype=bool).astype(np.int32)
+                                                   * A.HYG_COEFF_MATERIAL).reshape(W))
+        self.wall_thickness = (None if wall_thickness is None else
+                               np.ascontiguousarray(wall_thickness, dtype=np.float64).reshape(W))
+        self.wall_k_TT0 = (None if wall_k_TT0 is None else
+                           np.ascontiguousarray(wall_k_TT0, dtype=np.float64).reshape(W))
 
     def desc(self, keep: list) -> A.ModelDesc:
         d = A.ModelDesc()
         d.n_walls, d.n_nodes, d.dx = self.n_walls, self.n_nodes, self.dx
         d.precision = A.HYG_F32 if self.precision == "f32" else A.HYG_F64
-        d.coeff_kind = A.HYG_COEFF_ANALYTIC_D if self.coeff_kind == "analytic_d" else A.HYG_COEFF_CONSTANT
+        d.coeff_kind = {"analytic_d": A.HYG_COEFF_ANALYTIC_D, "material": A.HYG_COEFF_MATERIAL}.get(
+            self.coeff_kind, A.HYG_COEFF_CONSTANT)
         d.coeff_params = (C.c_double * 4)(*self.coeff_params)
         keep += [self.groups, self.biot, self.attach]
         d.groups = self.groups.ctypes.data_as(C.POINTER(A.WallGroups))
@@ -230,9 +258,10 @@ class Model:
         for i, z in enumerate(self.zones):
             wl = (A.ZoneWallLink * max(1, len(z.walls)))(*[A.ZoneWallLink(*w) for w in z.walls])
             il = (A.InterzoneLink * max(1, len(z.interzone)))(*[A.InterzoneLink(*x) for x in z.interzone])
-            keep += [wl, il]
+            rl = (A.RadiationLink * max(1, len(z.radiation)))(*[A.RadiationLink(*x) for x in z.radiation])
+            keep += [wl, il, rl]
             zs[i] = A.ZoneDesc(z.kappa_a_tt1, z.g_v, z.q_v1, z.q_v2, z.sources, z.moisture_sign,
-                               len(z.walls), wl, len(z.interzone), il)
+                               len(z.walls), wl, len(z.interzone), il, len(z.radiation), rl)
         keep.append(zs)
         d.n_zones, d.zones = len(self.zones), zs
         src = (A.ZoneSources * max(1, len(self.zone_sources)))()
@@ -243,6 +272,18 @@ class Model:
         d.outdoor_u, d.outdoor_v = self.outdoor_u.to_c(keep), self.outdoor_v.to_c(keep)
         d.dt, d.divergence_norm = self.dt, self.divergence_norm
         d.eta_factor, d.max_subiters, d.device = self.eta_factor, self.max_subiters, self.device
+        d.T_i, d.P_vi = self.T_i, self.P_vi
+        if self.wall_material is not None:
+            keep.append(self.wall_material)
+            d.wall_coeff = self.wall_material.ctypes.data_as(C.POINTER(C.c_int32))
+        if self.wall_reference is not None:
+            keep.append(self.wall_reference)
+            d.wall_reference = self.wall_reference.ctypes.data_as(C.POINTER(A.CoeffSet))
+        for name in ("wall_thickness", "wall_k_TT0"):
+            a = getattr(self, name)
+            if a is not None:
+                keep.append(a)
+                setattr(d, name, a.ctypes.data_as(A.dp))
         return d
 
 
@@ -408,6 +449,14 @@ def saturation_pressure(T: float) -> float:
     out = C.c_double()
     _check(load_library().hyg_saturation_pressure(T, C.byref(out)), None, "saturation_pressure")
     return out.value
+
+
+def material_evaluate(T: float, P_v: float, clamped: bool = False) -> tuple:
+    """MaterialModel::evaluate(_clamped) (materials.cpp:91-121) on the host:
+    (c_M, k_M, c_TT, k_TT, c_TM, k_TM)."""
+    out = A.CoeffSet()
+    _check(load_library().hyg_material_evaluate(T, P_v, int(clamped), C.byref(out)), None, "material_evaluate")
+    return (out.c_M, out.k_M, out.c_TT, out.k_TT, out.c_TM, out.k_TM)
 
 
 def scale_wall(reference, L, h_T0, h_M0, h_T1, h_M1, T_i=293.15, phi_i=0.5, t_0=3600.0):

@@ -1,0 +1,107 @@
+// hyg_material.cuh — the load-bearing material correlations
+// (MaterialModel, materials.cpp:11-121) as one host/device functor.
+//
+// Every expression keeps the reference's operand order, so the host build
+// (glibc exp/log/pow, used for setup: the reference set of a material wall,
+// hyg_material_evaluate) is bit-identical to the reference, and the device
+// build differs only by the CUDA math library's rounding (exp/log ≤1 ulp,
+// pow ≤2 ulp) and FMA contraction.  Default PhysicalConstants
+// (materials.hpp:7-15) — the scenario loader always uses them
+// (scenario.cpp:161).
+#pragma once
+#include <math.h>
+
+#if defined(__CUDACC__)
+#define HYG_HD __host__ __device__ __forceinline__
+#else
+#define HYG_HD inline
+#endif
+
+namespace hyg {
+namespace mat {
+
+constexpr double kRho0 = 790.0, kC0 = 870.0, kCw = 4180.0, kRhoL = 1000.0, kRv = 461.5, kLv = 2.5e6;
+constexpr double kC1 = 1.25e-5, kC2 = 1.8e-5, kSat = 157.0;         // materials.cpp:12-14
+constexpr double kBoxTMin = 274.15, kBoxTMax = 313.15;              // materials.hpp:50-53
+constexpr double kBoxPhiMin = 0.01, kBoxPhiMax = 0.99;
+
+struct Set { double c_M, k_M, c_TT, k_TT, c_TM, k_TM; };             // CoefficientSet
+
+HYG_HD double saturation_pressure(double T) {                      // materials.cpp:33-40 (range by caller)
+    return exp(23.5771 - 4042.9 / (T - 37.58));
+}
+
+HYG_HD double plateau(double s) {                                  // materials.cpp:17-20
+    return 47.1 * pow(1.0 + pow(kC1 * s, 1.65), -0.39) + 109.9 * pow(1.0 + pow(kC2 * s, 6.0), -0.83);
+}
+
+HYG_HD double moisture_content(double T, double phi) {             // materials.cpp:61-63
+    return plateau(kRv * T * (-log(phi)));
+}
+
+HYG_HD double vapour_permeability(double T, double f) {            // materials.cpp:65-68
+    const double z = 1.0 - f / kSat;
+    return 1.88e-6 / T * z / (0.503 * z * z + 0.497);
+}
+
+HYG_HD double thermal_conductivity(double f) { return 0.2 + 0.0045 * f; }   // materials.cpp:70-72
+
+HYG_HD double moisture_transport(double P_v, double P_s) {         // materials.cpp:74-78
+    const double r = 2.0 * P_v / P_s;
+    return 1.97e-10 * pow(10.0, 1.44 - 0.07 * log10(r)) + 1.77e-7 * exp(-8.0 * (r - 2.0) * (r - 2.0));
+}
+
+HYG_HD double moisture_storage(double T, double P_v, double P_s) { // materials.cpp:80-89
+    const double x = -log(P_v / P_s);
+    const double rt = kRv * T;
+    const double x1 = kC1 * rt * x, x2 = kC2 * rt * x;
+    const double t1 = 30.62 * (kC1 * rt / P_v) * pow(x1, 0.65) * pow(1.0 + pow(x1, 1.65), -1.39);
+    const double t2 = 549.5 * (kC2 * rt / P_v) * pow(x2, 5.0) * pow(1.0 + pow(x2, 6.0), -1.83);
+    return t1 + t2;
+}
+
+// MaterialModel::evaluate (materials.cpp:91-114); false where the reference
+// throws domain_error (state outside the admissible box).
+HYG_HD bool evaluate(double T, double P_v, Set& out) {
+    const double tol = 1e-9;
+    const double P_s = (T >= kBoxTMin - tol && T <= kBoxTMax + tol) ? saturation_pressure(T) : 0.0;
+    const double phi = P_s > 0.0 ? P_v / P_s : -1.0;
+    if (!(P_s > 0.0) || !(phi >= kBoxPhiMin * (1.0 - tol) && phi <= kBoxPhiMax * (1.0 + tol))) return false;
+    const double f = moisture_content(T, phi);
+    const double c_M = moisture_storage(T, P_v, P_s);
+    out.c_M = c_M;
+    out.k_M = moisture_transport(P_v, P_s);
+    out.c_TT = kRho0 * kC0 + kCw * f;
+    out.k_TT = thermal_conductivity(f);
+    out.c_TM = kCw * (T - 273.15) * c_M;
+    out.k_TM = kLv * vapour_permeability(T, f);
+    return true;
+}
+
+HYG_HD double clampd(double x, double lo, double hi) { return x < lo ? lo : (hi < x ? hi : x); }  // std::clamp
+
+// MaterialModel::evaluate_clamped (materials.cpp:116-121)
+HYG_HD bool evaluate_clamped(double T, double P_v, Set& out) {
+    const double Tc = clampd(T, kBoxTMin, kBoxTMax);
+    const double P_s = saturation_pressure(Tc);
+    const double phi = clampd(P_v / P_s, kBoxPhiMin, kBoxPhiMax);
+    return evaluate(Tc, phi * P_s, out);
+}
+
+// CoefficientModel::star / star_clamped (wall.cpp:50-58): the set at
+// (u T_i, v P_vi) divided by the wall's reference set.
+HYG_HD bool star(double u, double v, double T_i, double P_vi, const Set& ref, bool strict, Set& out) {
+    Set a;
+    const bool ok = strict ? evaluate(u * T_i, v * P_vi, a) : evaluate_clamped(u * T_i, v * P_vi, a);
+    if (!ok) return false;
+    out.c_M = a.c_M / ref.c_M;
+    out.k_M = a.k_M / ref.k_M;
+    out.c_TT = a.c_TT / ref.c_TT;
+    out.k_TT = a.k_TT / ref.k_TT;
+    out.c_TM = a.c_TM / ref.c_TM;
+    out.k_TM = a.k_TM / ref.k_TM;
+    return true;
+}
+
+}  // namespace mat
+}  // namespace hyg

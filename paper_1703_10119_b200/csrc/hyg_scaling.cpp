@@ -5,6 +5,7 @@
 #include <cmath>
 
 #include "../../include/hygro_b200.h"
+#include "hyg_material.cuh"
 
 namespace {
 // PhysicalConstants (materials.hpp:7-15) and kPv0 (scaling.hpp:74)
@@ -49,6 +50,16 @@ extern "C" {
 int hyg_saturation_pressure(double T, double* out) {
     if (!(T >= 273.15 && T <= 373.15)) return HYG_EDOMAIN;
     *out = psat(T);
+    return HYG_OK;
+}
+
+int hyg_material_evaluate(double T, double P_v, int32_t clamped, hyg_coeff_set* out) {
+    if (!out) return HYG_EINVAL;
+    hyg::mat::Set s;
+    if (clamped && !(T == T)) return HYG_EDOMAIN;     // saturation_pressure(NaN) throws
+    const bool ok = clamped ? hyg::mat::evaluate_clamped(T, P_v, s) : hyg::mat::evaluate(T, P_v, s);
+    if (!ok) return HYG_EDOMAIN;
+    *out = hyg_coeff_set{s.c_M, s.k_M, s.c_TT, s.k_TT, s.c_TM, s.k_TM};
     return HYG_OK;
 }
 

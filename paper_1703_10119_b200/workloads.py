@@ -238,3 +238,108 @@ BUILDERS = {
     "cfg3": zone_ring,
     "cfg4": long_domain,
 }
+
+
+# ---- load-bearing material walls -----------------------
+def material_reference(T_i=T_I, phi_i=PHI_I):
+    """Reference set of the built-in material: evaluate(T_i, P_vi) (scenario.cpp:178)."""
+    P_vi = phi_i * api.saturation_pressure(T_i)
+    return P_vi, np.array(api.material_evaluate(T_i, P_vi))
+
+
+def material_walls(n_walls=4096, n_nodes=101, nsteps=2000, dt=1e-3, seed=5) -> Workload:
+    """Independent load-bearing material walls (CoefficientModel::material), both
+    faces exterior: a humid side v = 1 + 0.4 sin(2 pi t/6) and an outdoor side
+    v = 1 + 0.24 sin(2 pi (t-6)/24), u = 1 (shapes of a single-slab scenario);
+    per-wall film coefficients log-uniform h_T in [5, 25], h_M in [3e-8, 8e-7];
+    L = 0.1 m, dx = 1/(n-1).  Strict evaluation in every DF step; implicit start."""
+    rng = np.random.default_rng(seed)
+    P_vi, ref = material_reference()
+    groups = np.empty((n_walls, 4))
+    biot = np.empty((n_walls, 2, 3))
+    hT = _log_uniform(rng, 5.0, 25.0, (n_walls, 2))
+    hM = _log_uniform(rng, 3e-8, 8e-7, (n_walls, 2))
+    for w in range(n_walls):
+        g, b = api.scale_wall(ref, 0.1, hT[w, 0], hM[w, 0], hT[w, 1], hM[w, 1], T_I, PHI_I, T0)
+        groups[w], biot[w] = g, b
+    attach = np.zeros((n_walls, 2, 2), dtype=np.int32)
+    attach[:, 1, 1] = 1
+    ch = [ChannelSpec(v_inf=Signal.sinusoid(1.0, 0.40, 6.0)),
+          ChannelSpec(v_inf=Signal.sinusoid(1.0, 0.24, 24.0, 6.0))]
+    model = Model(n_nodes, 1.0 / (n_nodes - 1), groups, biot, attach, channels=ch, dt=dt, eta_factor=1e-2,
+                  coeff_kind="material", T_i=T_I, P_vi=P_vi, wall_reference=np.tile(ref, (n_walls, 1)))
+    one = np.ones(n_walls * n_nodes)
+    init = dict(u_prev=one.copy(), u_curr=one.copy(), v_prev=one.copy(), v_curr=one.copy())
+    return Workload("material_walls", model, init, nsteps, "implicit",
+                    notes=f"{n_walls} material walls x {n_nodes}")
+
+
+def material_building(n_zones=2, n_nodes=101, nsteps=2000, dt=1e-3, mixed=False, radiation=True,
+                      ach=0.5, inz_ach=0.3) -> Workload:
+    """Zones in a ring, each bounded by three exterior load-bearing walls
+    (areas 18/18/9 m2, h_T 5/25/12, h_M 2e-7/8e-7/4e-7 outside, 8/3e-8 inside)
+    and one partition shared with the next zone (face 0 -> zone z, face 1 ->
+    zone z+1; exterior when n_zones == 1).  Long-wave radiation between every
+    ordered pair of a zone's walls (view factor 0.2, emissivity 0.5, 0.9 for
+    the partition), exterior u = 1 - 0.02 sin^2(2 pi t/24), v = 1 + 0.06
+    sin(2 pi t/24), q = 0.02 sin^2(2 pi t/24).  `mixed`: every exterior wall
+    of odd zones keeps constant (linearised) coefficients, so both step kinds
+    meet in one building (building.cpp:172-176)."""
+    V = 54.0
+    P_vi, ref = material_reference()
+    zd = api.scale_zone(V, 1.0, 1005.0, 1960.0, ach, T_I, PHI_I, T0)
+    g_inz, q_inz1, q_inz2 = api.scale_interzone(inz_ach, V, 1.0, 1005.0, 1960.0, T_I, PHI_I, T0)
+    moist = Signal.schedule(6.9e-6, [(6.0, 9.0, 1.1e-4), (30.0, 33.0, 1.1e-4)])
+    src = SourceSpec(g_o=Signal("constant", moist.base * zd["g_o_per"], 0.0, 1.0, 0.0,
+                                tuple((a, b, x * zd["g_o_per"]) for a, b, x in moist.windows)),
+                     q_o=Signal("constant", moist.base * zd["q_o_per"], 0.0, 1.0, 0.0,
+                                tuple((a, b, x * zd["q_o_per"]) for a, b, x in moist.windows)))
+    out_u, out_v = Signal.sin_squared(1.0, -0.02, 24.0), Signal.sinusoid(1.0, 0.06, 24.0)
+    ext = [(18.0, 5.0, 2e-7), (18.0, 25.0, 8e-7), (9.0, 12.0, 4e-7)]
+    wpz = len(ext) + 1
+    nw = n_zones * wpz
+    groups, biot = np.empty((nw, 4)), np.empty((nw, 2, 3))
+    attach = np.zeros((nw, 2, 2), dtype=np.int32)
+    material = np.ones(nw, dtype=bool)
+    links = [[] for _ in range(n_zones)]
+    for z in range(n_zones):
+        for i, (area, hT, hM) in enumerate(ext):
+            w = z * wpz + i
+            groups[w], biot[w] = api.scale_wall(ref, 0.1, hT, hM, 8.0, 3e-8, T_I, PHI_I, T0)
+            attach[w, 0], attach[w, 1] = (0, 0), (1, z)
+            th = api.attach_wall_to_zone(ref, area, 0.1, V, 1.0, 1005.0, T_I, PHI_I, T0)
+            links[z].append((w, 1, *biot[w, 1], *th))
+            material[w] = not (mixed and z % 2 == 1)
+        p = z * wpz + len(ext)                        # partition
+        groups[p], biot[p] = api.scale_wall(ref, 0.1, 8.0, 3e-8, 8.0, 3e-8, T_I, PHI_I, T0)
+        th = api.attach_wall_to_zone(ref, 9.0, 0.1, V, 1.0, 1005.0, T_I, PHI_I, T0)
+        attach[p, 0] = (1, z)
+        links[z].append((p, 0, *biot[p, 0], *th))
+        if n_zones > 1:
+            zn = (z + 1) % n_zones
+            attach[p, 1] = (1, zn)
+            links[zn].append((p, 1, *biot[p, 1], *th))
+        else:
+            attach[p, 1] = (0, 0)
+    zones = []
+    for z in range(n_zones):
+        inz = ([((z - 1) % n_zones, g_inz, q_inz1, q_inz2), ((z + 1) % n_zones, g_inz, q_inz1, q_inz2)]
+               if n_zones > 2 else ([((z + 1) % 2, g_inz, q_inz1, q_inz2)] if n_zones == 2 else []))
+        rad = []
+        if radiation:
+            ws = [l[0] for l in links[z]]
+            for r in ws:
+                for e in ws:
+                    if e != r:
+                        rad.append((e, r, 0.2, 0.9 if e % wpz == len(ext) else 0.5))
+        zones.append(ZoneSpec(zd["kappa_a_tt1"], zd["g_v"], zd["q_v1"], zd["q_v2"], 0, 1, links[z], inz, rad))
+    ch = [ChannelSpec(u_inf=out_u, v_inf=out_v, q_inf=Signal.sin_squared(0.0, 0.02, 24.0))]
+    model = Model(n_nodes, 1.0 / (n_nodes - 1), groups, biot, attach, channels=ch, zones=zones,
+                  zone_sources=[src], outdoor_u=out_u, outdoor_v=out_v, dt=dt, eta_factor=1e-2,
+                  coeff_kind="material", T_i=T_I, P_vi=P_vi, wall_reference=np.tile(ref, (nw, 1)),
+                  wall_material=material, wall_thickness=np.full(nw, 0.1), wall_k_TT0=np.full(nw, ref[3]))
+    one = np.ones(nw * n_nodes)
+    init = dict(u_prev=one.copy(), u_curr=one.copy(), v_prev=one.copy(), v_curr=one.copy(),
+                zone_u=np.ones(n_zones), zone_v=np.ones(n_zones))
+    return Workload("material_building", model, init, nsteps, "implicit",
+                    notes=f"{n_zones} zones x {wpz} material walls x {n_nodes}, radiation={radiation}")
