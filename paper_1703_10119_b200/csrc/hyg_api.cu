@@ -22,6 +22,7 @@
 #include "k_step.cuh"
 #include "k_nonlinear.cuh"
 #include "k_tiled.cuh"
+#include "k_material.cuh"
 
 using namespace hyg;
 
@@ -183,6 +184,20 @@ struct hyg_ctx {
     std::vector<Pending> pending;
     std::vector<Stat> stats;
     int64_t launches = 0;
+
+    // state-dependent coefficients (per-wall CoefficientModel) and radiation
+    std::vector<int> wall_kind;      // kCoeff* per wall
+    bool any_nonlinear = false, any_material = false;
+    double T_i = 293.15, P_vi = 0.0;
+    int* d_wall_kind = nullptr;
+    mat::Set* d_ref = nullptr;       // reference sets of material walls
+    double* d_star = nullptr;        // StarTables scratch [9][cells] (allocated on first use)
+    unsigned long long* d_dom = nullptr;
+    bool has_rad = false;
+    int rad_groups = 0, rad_terms = 0;
+    int *d_rad_tgt = nullptr, *d_rad_grp = nullptr;
+    double *d_rad_num = nullptr, *d_rad_den = nullptr, *d_rad_coef = nullptr, *d_qrad = nullptr;
+    int64_t *d_rad_e = nullptr, *d_rad_r = nullptr;
 
     int64_t cells() const { return static_cast<int64_t>(n_walls) * n; }
 };
@@ -373,7 +388,85 @@ StepArgs step_args(hyg_ctx* c, int from, double dt) {
     a.own0 = c->own_c0;
     a.own1 = c->own_c1;
     a.coef = c->d_coef;
+    a.wall_kind = c->d_wall_kind;
+    a.star = StarTab{c->d_star, c->d_star ? c->d_star + 6 * c->cells() : nullptr, c->cells()};
+    a.q_rad = c->has_rad ? c->d_qrad : nullptr;
+    a.dom_key = c->d_dom;
+    if (c->coeff_kind == HYG_COEFF_MATERIAL) a.coeff_kind = kCoeffMaterial;
     return a;
+}
+
+// StarTables of layer (u, v) for every nonlinear wall into c->d_star.
+int launch_star_tables(hyg_ctx* c, const double* u, const double* v, bool strict, int64_t layer,
+                       hyg_status* status) {
+    if (!c->d_star) HYG_CUDA(cudaMalloc(&c->d_star, sizeof(double) * 9 * static_cast<size_t>(c->cells())));
+    StarArgs s{};
+    s.n_walls = c->n_walls;
+    s.n = c->n;
+    s.u = u;
+    s.v = v;
+    s.wall_kind = c->d_wall_kind;
+    for (int i = 0; i < 4; ++i) s.p[i] = c->p[i];
+    s.T_i = c->T_i;
+    s.P_vi = c->P_vi;
+    s.ref = c->d_ref;
+    s.strict = strict ? 1 : 0;
+    s.node = c->d_star;
+    s.half = c->d_star + 6 * c->cells();
+    s.cells = c->cells();
+    s.layer = layer;
+    s.fail_key = c->d_key;
+    s.dom_key = c->d_dom;
+    s.own0 = c->own_c0;
+    s.own1 = c->own_c1;
+    LaunchScope ls(c, strict ? "star_tables" : "star_tables_clamped", static_cast<double>(c->cells()));
+    k_star_tables<<<static_cast<int>((c->cells() + 127) / 128), 128, 0, c->stream>>>(s);
+    return HYG_OK;
+}
+
+// radiation_fluxes (building.cpp:88-105) from the wall temperature layer u into c->d_qrad
+void launch_radiation(hyg_ctx* c, const double* u) {
+    RadArgs r{};
+    r.n_targets = 2 * c->n_walls;
+    r.tgt_off = c->d_rad_tgt;
+    r.grp_off = c->d_rad_grp;
+    r.grp_num = c->d_rad_num;
+    r.grp_den = c->d_rad_den;
+    r.t_e = c->d_rad_e;
+    r.t_r = c->d_rad_r;
+    r.t_coef = c->d_rad_coef;
+    r.T_i = c->T_i;
+    r.u = u;
+    r.q = c->d_qrad;
+    LaunchScope ls(c, "radiation", 0.0);
+    k_radiation<<<(r.n_targets + 127) / 128, 128, 0, c->stream>>>(r);
+}
+
+// a strict evaluation left the material box in the step into layer `lay`
+int domain_failure(hyg_ctx* c, int64_t lay, hyg_status* st) {
+    unsigned long long dom = ~0ull;
+    cudaMemcpy(&dom, c->d_dom, sizeof dom, cudaMemcpyDeviceToHost);
+    const int w = static_cast<int>(dom >> 32);
+    const unsigned order = static_cast<unsigned>(dom & 0xffffffffu);
+    const bool half = order >= static_cast<unsigned>(c->n);
+    const int j = static_cast<int>(half ? order - c->n : order);
+    if (st) {
+        st->code = HYG_EDOMAIN;
+        st->layer = lay;
+        st->wall = w;
+        st->node = j;
+        st->half = half ? 1 : 0;
+        st->t_star = c->t;
+        if (half)
+            std::snprintf(st->message, sizeof st->message,
+                          "material state outside admissible box in wall %d [half node %d+1/2] (step into layer %lld)",
+                          w, j, static_cast<long long>(lay));
+        else
+            std::snprintf(st->message, sizeof st->message,
+                          "material state outside admissible box in wall %d [node %d] (step into layer %lld)", w, j,
+                          static_cast<long long>(lay));
+    }
+    return HYG_EDOMAIN;
 }
 
 int read_key(hyg_ctx* c, unsigned long long* key, hyg_status* status) {
@@ -422,13 +515,17 @@ int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
         return HYG_ENOTSUP;
     }
     const int64_t block = 65536;     // forcing rows per upload
-    if (c->coeff_kind == HYG_COEFF_CONSTANT && c->coef_dt != dt) {
+    if (c->coeff_kind != HYG_COEFF_ANALYTIC_D && c->coef_dt != dt) {
         LaunchScope ls(c, "coupled_coef", 0.0);
         k_coupled_coef<<<(c->n_walls + 127) / 128, 128, 0, c->stream>>>(c->n_walls, c->dx, dt, c->d_groups,
                                                                          c->d_biot, c->d_coef);
         c->coef_dt = dt;
     }
+    const int kind = c->coeff_kind == HYG_COEFF_MATERIAL ? kCoeffMaterial
+                     : c->coeff_kind == HYG_COEFF_ANALYTIC_D ? kCoeffAnalyticD
+                                                             : kCoeffConstant;
     HYG_CUDA(cudaMemsetAsync(c->d_key, 0xff, sizeof(unsigned long long), c->stream));
+    HYG_CUDA(cudaMemsetAsync(c->d_dom, 0xff, sizeof(unsigned long long), c->stream));
     for (int64_t done = 0; done < nsteps;) {
         const int64_t rows = std::min(block, nsteps - done);
         std::vector<double> times(rows);
@@ -445,21 +542,29 @@ int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
         }
         const int nch = std::max<int>(1, static_cast<int>(c->channels.size()));
         const int threads = 256;
-        const int cells_per_block = step_cells(c->coeff_kind == HYG_COEFF_CONSTANT ? kCoeffConstant : kCoeffAnalyticD);
+        const int cells_per_block = step_cells(kind);
         const int grid = static_cast<int>((c->cells() + cells_per_block - 1) / cells_per_block);
         const int nsrc = static_cast<int>(c->zsrc.size() / 3);
         double* ptr0[2][4];
         std::memcpy(ptr0, c->s64, sizeof ptr0);
         for (int64_t k = 0; k < rows; ++k) {
+            // layer-n radiation fluxes and frozen coefficients (building.cpp:158; wall.cpp:206)
+            if (c->has_rad) launch_radiation(c, c->s64[c->cur][1]);
+            if (c->any_material) {
+                rc = launch_star_tables(c, c->s64[c->cur][1], c->s64[c->cur][3], true, c->layer + k, status);
+                if (rc) return rc;
+            }
             StepArgs a = step_args(c, c->cur, dt);
             a.amb = c->d_table + k * nch;
             a.layer = c->layer + k;
             if (c->zones.empty()) {
                 LaunchScope ls(c, "df_step_general", static_cast<double>(c->cells()));
-                if (c->coeff_kind == HYG_COEFF_CONSTANT)
+                if (kind == kCoeffConstant)
                     k_df_step_general<kCoeffConstant><<<grid, threads, 0, c->stream>>>(a);
-                else
+                else if (kind == kCoeffAnalyticD)
                     k_df_step_general<kCoeffAnalyticD><<<grid, threads, 0, c->stream>>>(a);
+                else
+                    k_df_step_general<kCoeffMaterial><<<grid, threads, 0, c->stream>>>(a);
             } else {
                 ZoneArgs z{};
                 z.n_zones = static_cast<int>(c->zones.size());
@@ -483,10 +588,12 @@ int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
                 z.own1 = c->own_z1;
                 const int zblocks = (z.n_zones + threads - 1) / threads;
                 LaunchScope ls(c, "building_step", static_cast<double>(c->cells()));
-                if (c->coeff_kind == HYG_COEFF_CONSTANT)
+                if (kind == kCoeffConstant)
                     k_building_step<kCoeffConstant><<<grid + zblocks, threads, 0, c->stream>>>(a, z, grid);
-                else
+                else if (kind == kCoeffAnalyticD)
                     k_building_step<kCoeffAnalyticD><<<grid + zblocks, threads, 0, c->stream>>>(a, z, grid);
+                else
+                    k_building_step<kCoeffMaterial><<<grid + zblocks, threads, 0, c->stream>>>(a, z, grid);
                 c->zcur ^= 1;
             }
             rotate_layers(c);
@@ -499,12 +606,17 @@ int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
             // kernels after the failing step returned early: replay only the
             // rotations of the steps that ran
             const int64_t fail_layer = static_cast<int64_t>(key >> 32);
-            const int64_t ran = fail_layer - c->layer;     // steps whose outputs exist
+            unsigned long long dom = ~0ull;
+            if (c->any_material)
+                HYG_CUDA(cudaMemcpy(&dom, c->d_dom, sizeof dom, cudaMemcpyDeviceToHost));
+            // divergence: the failing layer exists; domain error: its step never ran
+            const int64_t ran = fail_layer - c->layer - (dom != ~0ull ? 1 : 0);
             std::memcpy(c->s64, ptr0, sizeof ptr0);
             for (int64_t k = 0; k < ran; ++k) rotate_layers(c);
             if (!c->zones.empty() && (rows - ran) % 2) c->zcur ^= 1;
-            c->t = times[ran - 1] + dt;
-            c->layer = fail_layer;
+            c->t = ran < rows ? times[ran] : t;
+            c->layer += ran;
+            if (dom != ~0ull) return domain_failure(c, fail_layer, status);
             return diverged(c, key, status);
         }
         c->t = t;
@@ -841,9 +953,25 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
         set_status(status, HYG_ESCHEMA, "dt must be positive");
         return HYG_ESCHEMA;
     }
-    if (d->coeff_kind != HYG_COEFF_CONSTANT && d->coeff_kind != HYG_COEFF_ANALYTIC_D) {
+    if (d->coeff_kind != HYG_COEFF_CONSTANT && d->coeff_kind != HYG_COEFF_ANALYTIC_D &&
+        d->coeff_kind != HYG_COEFF_MATERIAL) {
         set_status(status, HYG_ENOTSUP, "coefficient model not implemented on the device");
         return HYG_ENOTSUP;
+    }
+    if (d->coeff_kind == HYG_COEFF_MATERIAL) {
+        bool need_ref = false;
+        for (int w = 0; w < d->n_walls; ++w) {
+            const int k = d->wall_coeff ? d->wall_coeff[w] : HYG_COEFF_MATERIAL;
+            if (k != HYG_COEFF_CONSTANT && k != HYG_COEFF_MATERIAL) {
+                set_status(status, HYG_EINVAL, "wall_coeff entries must be HYG_COEFF_CONSTANT or HYG_COEFF_MATERIAL");
+                return HYG_EINVAL;
+            }
+            need_ref = need_ref || k == HYG_COEFF_MATERIAL;
+        }
+        if (need_ref && (!d->wall_reference || !(d->T_i > 0.0) || !(d->P_vi > 0.0))) {
+            set_status(status, HYG_EINVAL, "material walls need wall_reference and a scaling context (T_i, P_vi > 0)");
+            return HYG_EINVAL;
+        }
     }
     // validate (building.cpp:12-52): face and link references must resolve
     for (int w = 0; w < d->n_walls; ++w) {
@@ -874,6 +1002,18 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
         if (zd.sources < 0 || zd.sources >= d->n_zone_sources) {
             set_status(status, HYG_ESCHEMA, "zone references missing source schedules");
             return HYG_ESCHEMA;
+        }
+        for (int i = 0; i < zd.n_radiation; ++i) {
+            const hyg_radiation_link& r = zd.radiation[i];
+            if (r.emitter_wall < 0 || r.emitter_wall >= d->n_walls || r.receiver_wall < 0 ||
+                r.receiver_wall >= d->n_walls) {
+                set_status(status, HYG_ESCHEMA, "radiation link references a wall which does not exist");
+                return HYG_ESCHEMA;
+            }
+        }
+        if (zd.n_radiation > 0 && (!d->wall_thickness || !d->wall_k_TT0 || !(d->T_i > 0.0))) {
+            set_status(status, HYG_EINVAL, "radiation needs wall_thickness, wall_k_TT0 and T_i");
+            return HYG_EINVAL;
         }
     }
     int ndev = 0;
@@ -955,6 +1095,62 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
     c->out_v.set(d->outdoor_v);
     c->src_tab.assign(d->n_zone_sources, TableHost{0, 3, {}});
     c->out_tab.width = 2;
+    // per-wall coefficient models (BuildingWall::coeffs building.hpp:28)
+    c->T_i = d->T_i;
+    c->P_vi = d->P_vi;
+    c->wall_kind.assign(c->n_walls, kCoeffConstant);
+    std::vector<mat::Set> refs(c->n_walls, mat::Set{1, 1, 1, 1, 1, 1});
+    for (int w = 0; w < c->n_walls; ++w) {
+        if (d->coeff_kind == HYG_COEFF_ANALYTIC_D) c->wall_kind[w] = kCoeffAnalyticD;
+        if (d->coeff_kind == HYG_COEFF_MATERIAL &&
+            (!d->wall_coeff || d->wall_coeff[w] == HYG_COEFF_MATERIAL)) {
+            c->wall_kind[w] = kCoeffMaterial;
+            const hyg_coeff_set& r = d->wall_reference[w];
+            refs[w] = mat::Set{r.c_M, r.k_M, r.c_TT, r.k_TT, r.c_TM, r.k_TM};
+            c->any_material = true;
+        }
+        c->any_nonlinear = c->any_nonlinear || c->wall_kind[w] != kCoeffConstant;
+    }
+    // radiation CSR (radiation_fluxes building.cpp:88-105, zone_surface_u :77-86):
+    // groups in zone / link order, bucketed by target face in that order
+    struct RadGroup { int target; double num, den; std::vector<int64_t> e, r; std::vector<double> coef; };
+    std::vector<RadGroup> rg;
+    for (int z = 0; z < d->n_zones; ++z) {
+        const hyg_zone_desc& zd = d->zones[z];
+        if (zd.n_radiation == 0) continue;
+        std::vector<int64_t> surf(c->n_walls, -1);      // last link of each wall in this zone wins
+        for (int i = 0; i < zd.n_walls; ++i)
+            surf[zd.walls[i].wall] = static_cast<int64_t>(zd.walls[i].wall) * c->n + (zd.walls[i].face == 0 ? 0 : c->n - 1);
+        for (int i = 0; i < zd.n_walls; ++i) {
+            const hyg_zone_wall_link& l = zd.walls[i];
+            RadGroup g{2 * l.wall + (l.face == 0 ? 0 : 1), d->wall_thickness[l.wall], d->T_i * d->wall_k_TT0[l.wall], {}, {}, {}};
+            for (int k = 0; k < zd.n_radiation; ++k) {
+                const hyg_radiation_link& r = zd.radiation[k];
+                if (r.receiver_wall != l.wall) continue;
+                g.e.push_back(surf[r.emitter_wall]);
+                g.r.push_back(surf[r.receiver_wall]);
+                g.coef.push_back(r.view_factor * r.emissivity * 5.67e-8);   // PhysicalConstants::sigma
+            }
+            rg.push_back(std::move(g));
+        }
+    }
+    std::stable_sort(rg.begin(), rg.end(), [](const RadGroup& x, const RadGroup& y) { return x.target < y.target; });
+    std::vector<int> rad_tgt(2 * c->n_walls + 1, 0), rad_grp(1, 0);
+    std::vector<double> rad_num, rad_den, rad_coef;
+    std::vector<int64_t> rad_e, rad_r;
+    for (const auto& g : rg) {
+        rad_tgt[g.target + 1] += 1;
+        rad_num.push_back(g.num);
+        rad_den.push_back(g.den);
+        for (size_t i = 0; i < g.e.size(); ++i) {
+            rad_e.push_back(g.e[i]);
+            rad_r.push_back(g.r[i]);
+            rad_coef.push_back(g.coef[i]);
+        }
+        rad_grp.push_back(static_cast<int>(rad_e.size()));
+    }
+    for (int i = 0; i < 2 * c->n_walls; ++i) rad_tgt[i + 1] += rad_tgt[i];
+    c->has_rad = !rg.empty();
     c->fused = all_exterior && d->n_zones == 0 && d->coeff_kind == HYG_COEFF_CONSTANT && fused_grid(c->n);
     c->nl_fused = all_exterior && d->n_zones == 0 && d->coeff_kind == HYG_COEFF_ANALYTIC_D && c->n <= 1024 &&
                   c->precision == HYG_F64;
@@ -993,8 +1189,26 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
         cudaMalloc(&c->d_chan, sizeof(int) * 2 * c->n_walls) != cudaSuccess ||
         cudaMalloc(&c->d_coef, sizeof(WallCoef) * c->n_walls) != cudaSuccess ||
         cudaMalloc(&c->d_flag, sizeof(int)) != cudaSuccess ||
-        cudaMalloc(&c->d_key, sizeof(unsigned long long)) != cudaSuccess)
+        cudaMalloc(&c->d_key, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&c->d_dom, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&c->d_wall_kind, sizeof(int) * c->n_walls) != cudaSuccess ||
+        cudaMalloc(&c->d_ref, sizeof(mat::Set) * c->n_walls) != cudaSuccess)
         return fail("parameter alloc");
+    cudaMemcpy(c->d_wall_kind, c->wall_kind.data(), sizeof(int) * c->n_walls, cudaMemcpyHostToDevice);
+    cudaMemcpy(c->d_ref, refs.data(), sizeof(mat::Set) * c->n_walls, cudaMemcpyHostToDevice);
+    cudaMemset(c->d_dom, 0xff, sizeof(unsigned long long));
+    if (c->has_rad) {
+        auto up = [&](auto*& dst, const auto& v) {
+            using T = typename std::decay_t<decltype(v)>::value_type;
+            if (cudaMalloc(&dst, sizeof(T) * std::max<size_t>(1, v.size())) != cudaSuccess) return false;
+            if (!v.empty()) cudaMemcpy(dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice);
+            return true;
+        };
+        if (!up(c->d_rad_tgt, rad_tgt) || !up(c->d_rad_grp, rad_grp) || !up(c->d_rad_num, rad_num) ||
+            !up(c->d_rad_den, rad_den) || !up(c->d_rad_coef, rad_coef) || !up(c->d_rad_e, rad_e) ||
+            !up(c->d_rad_r, rad_r) || cudaMalloc(&c->d_qrad, sizeof(double) * 2 * c->n_walls) != cudaSuccess)
+            return fail("radiation alloc");
+    }
     cudaMemcpy(c->d_groups, c->groups.data(), sizeof(Groups) * c->n_walls, cudaMemcpyHostToDevice);
     cudaMemcpy(c->d_biot, c->biot.data(), sizeof(Biot) * 2 * c->n_walls, cudaMemcpyHostToDevice);
     cudaMemcpy(c->d_attach, c->attach.data(), sizeof(Attach) * 2 * c->n_walls, cudaMemcpyHostToDevice);
@@ -1060,6 +1274,15 @@ void hyg_destroy(hyg_ctx* c) {
     cudaFree(c->d_src);
     cudaFree(c->d_flag);
     cudaFree(c->d_key);
+    cudaFree(c->d_dom);
+    cudaFree(c->d_wall_kind);
+    cudaFree(c->d_ref);
+    cudaFree(c->d_star);
+    for (void* q : {static_cast<void*>(c->d_rad_tgt), static_cast<void*>(c->d_rad_grp),
+                    static_cast<void*>(c->d_rad_num), static_cast<void*>(c->d_rad_den),
+                    static_cast<void*>(c->d_rad_coef), static_cast<void*>(c->d_qrad),
+                    static_cast<void*>(c->d_rad_e), static_cast<void*>(c->d_rad_r)})
+        cudaFree(q);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -1260,11 +1483,6 @@ int hyg_bootstrap(hyg_ctx* c, int32_t kind, hyg_status* status) {
         set_status(status, HYG_EINVAL, "unknown bootstrap kind");
         return HYG_EINVAL;
     }
-    if (kind == HYG_BOOT_IMPLICIT && c->coeff_kind != HYG_COEFF_CONSTANT) {
-        set_status(status, HYG_ENOTSUP,
-                   "implicit starting step on the device: constant-coefficient walls only");
-        return HYG_ENOTSUP;
-    }
     int rc = from_f32(c, status);
     if (rc) return rc;
     // forcing: explicit step at layer-n time, implicit step at t^{n+1} (building.cpp:196)
@@ -1289,9 +1507,16 @@ int hyg_bootstrap(hyg_ctx* c, int32_t kind, hyg_status* status) {
     StepArgs a = step_args(c, c->cur, c->dt);
     a.amb = c->d_boot;
     int passes = 0;
+    a.star.node = a.star.half = nullptr;     // no tables unless built below
     if (kind == HYG_BOOT_EXPLICIT) {
         // euler_explicit_step per wall (wall.cpp:266-317); with zones this is the
         // reference's EulerExplicit building step (building.cpp:174-183)
+        if (c->has_rad) launch_radiation(c, a.in[1]);
+        if (c->any_material) {      // clamped tables of layer n (wall.cpp:271)
+            rc = launch_star_tables(c, a.in[1], a.in[3], false, c->layer, status);
+            if (rc) return rc;
+            a.star = StarTab{c->d_star, c->d_star + 6 * c->cells(), c->cells()};
+        }
         {
             LaunchScope ls(c, "explicit_boot", static_cast<double>(c->cells()));
             k_explicit_boot<<<static_cast<int>((c->cells() + 255) / 256), 256, 0, c->stream>>>(a);
@@ -1330,7 +1555,7 @@ int hyg_bootstrap(hyg_ctx* c, int32_t kind, hyg_status* status) {
         double* scr = nullptr;
         double* zit = nullptr;         // zone iterates: [4][nz] = (u,v) x (snapshot, new)
         unsigned long long* d_diff = nullptr;
-        HYG_CUDA(cudaMallocAsync(&scr, sizeof(double) * 4 * cells, c->stream));
+        HYG_CUDA(cudaMallocAsync(&scr, sizeof(double) * 5 * cells, c->stream));
         HYG_CUDA(cudaMallocAsync(&zit, sizeof(double) * 4 * nz, c->stream));
         HYG_CUDA(cudaMallocAsync(&d_diff, sizeof(unsigned long long), c->stream));
         // iterates start from layer n (building.cpp:200-206)
@@ -1351,6 +1576,16 @@ int hyg_bootstrap(hyg_ctx* c, int32_t kind, hyg_status* status) {
             double* zn_v = zn_u + nz;
             a.zu = zs_u;
             a.zv = zs_v;
+            // radiation refreshed from the iterate surfaces (building.cpp:212), clamped
+            // tables of the iterate for the nonlinear walls (wall.cpp:450)
+            if (c->has_rad) launch_radiation(c, a.out[1]);
+            if (c->any_nonlinear) {
+                rc = launch_star_tables(c, a.out[1], a.out[3], false, c->layer, status);
+                if (rc) return rc;
+                a.star = StarTab{c->d_star, c->d_star + 6 * c->cells(), c->cells()};
+                LaunchScope ls(c, "implicit_table_pass", static_cast<double>(c->cells()));
+                k_implicit_table_pass<<<(c->n_walls + 127) / 128, 128, 0, c->stream>>>(a, scr, d_diff);
+            }
             {
                 LaunchScope ls(c, "implicit_unit_pass", static_cast<double>(c->cells()));
                 k_implicit_unit_pass<<<(c->n_walls + 127) / 128, 128, 0, c->stream>>>(a, scr, d_diff);

@@ -16,7 +16,20 @@
 
 namespace hyg {
 
-enum : int { kCoeffConstant = 0, kCoeffAnalyticD = 1 };
+enum : int { kCoeffConstant = 0, kCoeffAnalyticD = 1, kCoeffMaterial = 2 };
+
+// Frozen starred coefficients of one layer (StarTables wall.cpp:89-138), SoA
+// over cells: node sets at node j, half sets at the midpoint j+1/2 (stored at
+// the cell of node j).  Built by k_star_tables (k_material.cuh).
+enum : int { kSc_M = 0, kSk_M = 1, kSc_TT = 2, kSk_TT = 3, kSc_TM = 4, kSk_TM = 5 };   // node[6]
+enum : int { kHk_M = 0, kHk_TT = 1, kHk_TM = 2 };                                    // half[3]
+struct StarTab {
+    const double* node;     // [6][cells]
+    const double* half;     // [3][cells]
+    int64_t cells;
+    __device__ __forceinline__ double nd(int f, int64_t c) const { return node[f * cells + c]; }
+    __device__ __forceinline__ double hf(int f, int64_t c) const { return half[f * cells + c]; }
+};
 
 struct Attach { int kind, index; };   // 0 exterior(channel), 1 zone
 
@@ -39,7 +52,20 @@ struct StepArgs {
     unsigned long long* fail_key;
     int64_t own0, own1;         // cells whose guard/residual count (a shard owns a range)
     const WallCoef* coef;       // constant walls: per-wall rows for this dt (k_coupled_coef)
+    const int* wall_kind;       // [n_walls] kCoeff* of each wall (per-wall CoefficientModel)
+    StarTab star;               // nonlinear walls: tables of this layer (node == nullptr: none)
+    const double* q_rad;        // [2*n_walls] zone radiation flux per face (nullable)
+    const unsigned long long* dom_key;   // set by this step's k_star_tables on a domain error
 };
+
+// A failure raised by an EARLIER step (key layer <= this step's input layer)
+// freezes the march; failures raised within the step itself do not, so every
+// failing wall of the step reports and atomicMin keeps the lowest index
+// (check_bounded walks walls in order, building.cpp:282-300).
+__device__ __forceinline__ bool frozen_before(const unsigned long long* key, int64_t layer) {
+    const unsigned long long k = *key;
+    return k != ~0ull && static_cast<int64_t>(k >> 32) <= layer;
+}
 
 // d(v) functor of HYG_COEFF_ANALYTIC_D: k_M* = 1 + p0 v + p1 exp(-p2 (v - p3)^2)
 __device__ __forceinline__ double analytic_kM(const double* p, double v) {
@@ -53,16 +79,18 @@ __device__ __forceinline__ FaceVals resolve(const StepArgs& a, int w, int k) {
     // resolve_face (building.cpp:107-126), no radiation
     const Biot b = a.biot[2 * w + k];
     const Attach at = a.attach[2 * w + k];
+    const double q_rad = a.q_rad ? a.q_rad[2 * w + k] : 0.0;   // radiation_fluxes building.cpp:88-105
     FaceVals f{b.Bi_M, b.Bi_TT, b.Bi_TM, 1.0, 1.0, 0.0, 0.0};
     if (at.kind == 0) {
         const Ambient am = a.amb[at.index];
         f.u_inf = am.u;
         f.v_inf = am.v;
         f.g_inf = am.g;
-        f.q_inf = am.q + 0.0;
+        f.q_inf = am.q + q_rad;
     } else {
         f.u_inf = a.zu[at.index];
         f.v_inf = a.zv[at.index];
+        f.q_inf = q_rad;
     }
     return f;
 }
@@ -155,6 +183,53 @@ __device__ __forceinline__ void analytic_node(const StepArgs& a, int w, int j, c
          (ctt + b_ * (ktp_b + kt_b) + cplu);
 }
 
+// df_step_nonlinear (wall.cpp:196-264) with all six starred coefficients
+// read from the layer's tables (material walls), literal form.
+__device__ __forceinline__ void table_node(const StepArgs& a, int w, int j, const NodeIn& x, double& un,
+                                           double& vn) {
+    const int n = a.n;
+    const double dx = a.dx, dt = a.dt;
+    const Groups p = a.groups[w];
+    const double ad = p.Fo_M * dt / (dx * dx);
+    const double b_ = p.Fo_TT * dt / (dx * dx);
+    const double g_ = p.Fo_TM * p.gamma * dt / (dx * dx);
+    const double ratio = p.Fo_TT != 0.0 ? p.Fo_TM * p.gamma / p.Fo_TT : 0.0;
+    const StarTab& s = a.star;
+    const int64_t c = static_cast<int64_t>(w) * n + j;
+    if (j > 0 && j < n - 1) {
+        const double kp = s.hf(kHk_M, c), km = s.hf(kHk_M, c - 1), cm = s.nd(kSc_M, c);
+        vn = ((cm - ad * (kp + km)) * x.vp + 2.0 * ad * (kp * x.vr + km * x.vl)) / (cm + ad * (kp + km));
+        const double ktp = s.hf(kHk_TT, c), ktm = s.hf(kHk_TT, c - 1);
+        const double kmp = s.hf(kHk_TM, c), kmm = s.hf(kHk_TM, c - 1);
+        const double ctt = s.nd(kSc_TT, c), ctm = s.nd(kSc_TM, c);
+        un = ((ctt - b_ * (ktp + ktm)) * x.up - p.gamma * ctm * (vn - x.vp) +
+              2.0 * b_ * (ktp * x.ur + ktm * x.ul) + 2.0 * g_ * (kmp * x.vr + kmm * x.vl) -
+              g_ * (kmp + kmm) * (vn + x.vp)) /
+             (ctt + b_ * (ktp + ktm));
+        return;
+    }
+    const int k = j == 0 ? 0 : 1;
+    const double vcn = j == 0 ? x.vr : x.vl, ucn = j == 0 ? x.ur : x.ul;   // vc[jn], uc[jn]
+    const int64_t ch = j == 0 ? c : c - 1;                                  // half_front / half_back
+    const FaceVals b = resolve(a, w, k);
+    const double km_b = s.nd(kSk_M, c), kp_b = s.hf(kHk_M, ch), cm = s.nd(kSc_M, c);
+    const double cpl = 2.0 * ad * dx * b.Bi_M;
+    vn = ((cm - ad * (kp_b + km_b) - cpl) * x.vp + 2.0 * ad * (kp_b + km_b) * vcn +
+          4.0 * ad * dx * (b.Bi_M * b.v_inf + b.g_inf)) /
+         (cm + ad * (kp_b + km_b) + cpl);
+    const double kt_b = s.nd(kSk_TT, c), kTM_b = s.nd(kSk_TM, c);
+    const double ktp_b = s.hf(kHk_TT, ch), kmp_b = s.hf(kHk_TM, ch);
+    const double ctt = s.nd(kSc_TT, c), ctm = s.nd(kSc_TM, c);
+    const double vbar = 0.5 * (vn + x.vp);
+    const double vg = vcn - (2.0 * dx / km_b) * (b.Bi_M * (vbar - b.v_inf) - b.g_inf);
+    const double cplu = 2.0 * b_ * dx * b.Bi_TT;
+    un = ((ctt - b_ * (ktp_b + kt_b) - cplu) * x.up - p.gamma * ctm * (vn - x.vp) +
+          2.0 * b_ * (ktp_b + kt_b) * ucn + 2.0 * b_ * ratio * kTM_b * (vcn - vg) -
+          4.0 * b_ * dx * (b.Bi_TM * (vbar - b.v_inf) - b.q_inf) + 2.0 * cplu * b.u_inf +
+          2.0 * g_ * (kmp_b * vcn + kTM_b * vg) - g_ * (kmp_b + kTM_b) * (vn + x.vp)) /
+         (ctt + b_ * (ktp_b + kt_b) + cplu);
+}
+
 // One DF step of NPT nodes per thread (cells base + k * stride); guard per
 // node (exact check_bounded semantics).  Every state load of all NPT nodes is
 // issued before the stop flag is read and before any arithmetic, so a thread
@@ -182,14 +257,18 @@ __device__ __forceinline__ void wall_nodes_step(const StepArgs& a, int64_t base,
             x[k] = load_node(a, w[k], j[k]);
         }
     }
-    if (*a.fail_key != ~0ull) return;    // an earlier step failed: freeze
+    // an earlier step failed, or this step's coefficient tables left the box
+    // (domain_error preempts the step, wall.cpp:206): freeze
+    if (frozen_before(a.fail_key, a.layer) || (KIND == kCoeffMaterial && *a.dom_key != ~0ull)) return;
 #pragma unroll
     for (int k = 0; k < NPT; ++k) {
         if (w[k] < 0) continue;
         const int64_t cell = base + static_cast<int64_t>(k) * stride;
         double un, vn;
         if (KIND == kCoeffConstant) coupled_node(a, w[k], j[k], x[k], un, vn);
-        else analytic_node(a, w[k], j[k], x[k], un, vn);
+        else if (KIND == kCoeffAnalyticD) analytic_node(a, w[k], j[k], x[k], un, vn);
+        else if (a.wall_kind[w[k]] == kCoeffConstant) coupled_node(a, w[k], j[k], x[k], un, vn);
+        else table_node(a, w[k], j[k], x[k], un, vn);   // df_step_nonlinear of a material wall
         // only the new layer is written; the host rotates layer pointers
         // (prev <- curr) instead of copying: 32 B read + 16 B written per update
         a.out[1][cell] = un;
@@ -281,7 +360,7 @@ __device__ __forceinline__ void zone_update(const ZoneArgs& a, int z) {
 __global__ void k_zone_step(const ZoneArgs a) {
     const int z = blockIdx.x * blockDim.x + threadIdx.x;
     if (z >= a.n_zones) return;
-    if (*a.fail_key != ~0ull) return;
+    if (frozen_before(a.fail_key, a.layer)) return;
     zone_update(a, z);
 }
 
@@ -297,13 +376,17 @@ __global__ void __launch_bounds__(kStepThreads, KIND == kCoeffConstant ? 4 : 3) 
         wall_nodes_step<step_npt(KIND), KIND>(a, base, kStepThreads);
     } else {
         const int zi = (static_cast<int>(blockIdx.x) - wall_blocks) * blockDim.x + threadIdx.x;
-        if (zi < z.n_zones && *z.fail_key == ~0ull) zone_update(z, zi);
+        if (zi < z.n_zones && !frozen_before(z.fail_key, z.layer) &&
+            !(KIND == kCoeffMaterial && *a.dom_key != ~0ull))
+            zone_update(z, zi);
     }
 }
 
 // ---- starting steps --------------------------------------------------------
-// euler_explicit_step (wall.cpp:266-317), one node per thread; coefficient
-// evaluations are clamped (strict=false) — the analytic functor has no box.
+// euler_explicit_step (wall.cpp:266-317), one node per thread.  Coefficients
+// are clamped (strict=false): material walls read the layer's tables (built
+// clamped by k_star_tables), the analytic functor (no box) is evaluated
+// inline, constant walls use the unit set.
 __global__ void k_explicit_boot(const StepArgs a) {
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t total = static_cast<int64_t>(a.n_walls) * a.n;
@@ -314,14 +397,22 @@ __global__ void k_explicit_boot(const StepArgs a) {
     const double dx = a.dx, dt = a.dt;
     const size_t o = static_cast<size_t>(w) * n;
     const double *uc = a.in[1] + o, *vc = a.in[3] + o;
-    const bool an = a.coeff_kind == kCoeffAnalyticD;
-    auto kM_node = [&](int i) { return an ? analytic_kM(a.p, vc[i]) : 1.0; };
-    auto kM_half = [&](int i) { return an ? analytic_kM(a.p, 0.5 * (vc[i] + vc[i + 1])) : 1.0; };
+    const int wk = a.wall_kind ? a.wall_kind[w] : a.coeff_kind;
+    const bool tab = a.star.node != nullptr && wk != kCoeffConstant;
+    const bool an = !tab && wk == kCoeffAnalyticD;
+    auto NS = [&](int f, int i) -> double {            // StarTables::at_node(i)
+        if (tab) return a.star.nd(f, static_cast<int64_t>(o) + i);
+        return (an && f == kSk_M) ? analytic_kM(a.p, vc[i]) : 1.0;
+    };
+    auto HS = [&](int f, int i) -> double {            // StarTables::at_half(i), i+1/2
+        if (tab) return a.star.hf(f, static_cast<int64_t>(o) + i);
+        return (an && f == kHk_M) ? analytic_kM(a.p, 0.5 * (vc[i] + vc[i + 1])) : 1.0;
+    };
     // ghost values from layer-n boundary states (wall.cpp:276-288)
     auto ghosts = [&](int k, double& vg, double& ug) {
         const int jb = k == 0 ? 0 : n - 1, jn = k == 0 ? 1 : n - 2;
         const FaceVals b = resolve(a, w, k);
-        const double nkM = kM_node(jb), nkTM = 1.0, nkTT = 1.0;
+        const double nkM = NS(kSk_M, jb), nkTM = NS(kSk_TM, jb), nkTT = NS(kSk_TT, jb);
         vg = vc[jn] - (2.0 * dx / nkM) * (b.Bi_M * (vc[jb] - b.v_inf) - b.g_inf);
         ug = uc[jn] + (p.Fo_TM * p.gamma * nkTM) / (p.Fo_TT * nkTT) * (vc[jn] - vg) -
              (2.0 * dx / nkTT) * (b.Bi_TT * (uc[jb] - b.u_inf) + b.Bi_TM * (vc[jb] - b.v_inf) - b.q_inf);
@@ -330,9 +421,14 @@ __global__ void k_explicit_boot(const StepArgs a) {
     if (j == 0) ghosts(0, vL, uL); else { vL = vc[j - 1]; uL = uc[j - 1]; }
     if (j == n - 1) ghosts(1, vR, uR); else { vR = vc[j + 1]; uR = uc[j + 1]; }
     const double rdt = dt / (dx * dx);
-    const double km = j == 0 ? kM_node(0) : kM_half(j - 1);
-    const double kp = j == n - 1 ? kM_node(n - 1) : kM_half(j);
-    const double ktm = 1.0, ktp = 1.0, kmm = 1.0, kmp = 1.0, cM = 1.0, cTM = 1.0, cTT = 1.0;
+    // ghost-side half-node coefficients collapse onto the boundary node (wall.cpp:297-303)
+    const double km = j == 0 ? NS(kSk_M, 0) : HS(kHk_M, j - 1);
+    const double kp = j == n - 1 ? NS(kSk_M, n - 1) : HS(kHk_M, j);
+    const double ktm = j == 0 ? NS(kSk_TT, 0) : HS(kHk_TT, j - 1);
+    const double ktp = j == n - 1 ? NS(kSk_TT, n - 1) : HS(kHk_TT, j);
+    const double kmm = j == 0 ? NS(kSk_TM, 0) : HS(kHk_TM, j - 1);
+    const double kmp = j == n - 1 ? NS(kSk_TM, n - 1) : HS(kHk_TM, j);
+    const double cM = NS(kSc_M, j), cTM = NS(kSc_TM, j), cTT = NS(kSc_TT, j);
     const double div_v = kp * (vR - vc[j]) - km * (vc[j] - vL);
     const double vn = vc[j] + rdt * p.Fo_M * div_v / cM;
     const double div_u = ktp * (uR - uc[j]) - ktm * (uc[j] - uL);
@@ -369,6 +465,7 @@ __device__ __forceinline__ void atomic_max_nonneg(unsigned long long* p, double 
 __global__ void k_implicit_unit_pass(const StepArgs a, double* scr, unsigned long long* diff) {
     const int w = blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= a.n_walls) return;
+    if (a.wall_kind && a.wall_kind[w] != kCoeffConstant) return;   // k_implicit_table_pass
     const int n = a.n, B = a.n_walls;
     const double dx = a.dx, dt = a.dt;
     const Groups p = a.groups[w];

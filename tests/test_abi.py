@@ -30,7 +30,7 @@ def test_library_exports_every_header_symbol():
     assert missing == []
     # and the binding's prototype table covers the header exactly
     assert sorted(A.PROTOTYPES) == declared
-    assert lib.hyg_abi_version() == 1
+    assert lib.hyg_abi_version() == 2
     assert lib.hyg_strerror(A.HYG_EDIVERGED).decode().startswith("numerical error")
 
 
@@ -110,3 +110,33 @@ def test_signals_match_reference_formula():
         cs = sig.to_c(keep)
         for t in np.linspace(0, 80, 37):
             assert lib.orc_signal(C.byref(cs), float(t)) == sig(float(t))
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """The ctypes mirror (_abi.py) has the same sizes and field offsets as the
+    C structs of include/hygro_b200.h (compiled here with gcc)."""
+    import subprocess
+    import ctypes as C
+    from paper_1703_10119_b200 import _abi as A
+    structs = {"hyg_model_desc": A.ModelDesc, "hyg_zone_desc": A.ZoneDesc, "hyg_status": A.Status,
+               "hyg_signal": A.Signal, "hyg_channel": A.Channel, "hyg_zone_wall_link": A.ZoneWallLink,
+               "hyg_interzone_link": A.InterzoneLink, "hyg_radiation_link": A.RadiationLink,
+               "hyg_coeff_set": A.CoeffSet, "hyg_zone_sources": A.ZoneSources}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "hygro_b200.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            cf = "from" if fname == "from_" else fname
+            lines.append(f'printf("{cname}.{fname} %zu\\n", offsetof({cname}, {cf}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)],
+                   check=True)
+    got = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True, check=True)
+               .stdout.splitlines())
+    for cname, py in structs.items():
+        assert int(got[cname]) == C.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert int(got[f"{cname}.{fname}"]) == getattr(py, fname).offset, (cname, fname)

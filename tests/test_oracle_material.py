@@ -90,3 +90,17 @@ def test_material_domain_error_location(ref, wall, node, field, value):
     assert O.Building.domain("oracle") == O.Building.domain("ref")
     dw, dn, half = O.Building.domain("ref")
     assert dw == wall and dn == node and not half
+
+
+def test_material_domain_error_half_node(ref):
+    """Both nodes at phi = 0.9895 at different temperatures: P_s is convex, so
+    the midpoint state leaves the box and the half node j+1/2 fails."""
+    w = workloads.material_building(n_zones=1, n_nodes=41)
+    init = {k: np.array(v, dtype=np.float64, copy=True) for k, v in w.init.items()}
+    c = 3 * 41 + 20
+    for cell, u in ((c, 1.0), (c + 1, 0.9665)):
+        init["u_curr"][cell] = u
+        init["v_curr"][cell] = 0.9895 * api.saturation_pressure(u * 293.15) / w.model.P_vi
+    _, _, ra, rb = _run_pair(w, 2, with_bootstrap=False, init=init)
+    assert ra[:2] == rb[:2] == (api.A.HYG_EDOMAIN, 1)
+    assert O.Building.domain("oracle") == O.Building.domain("ref") == (3, 20, True)
