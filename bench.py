@@ -10,7 +10,7 @@ Weak scaling: every rank marches its own 65,536 walls, no data-path
 collective; `value` = all ranks' node-updates / max-over-ranks device time.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                  [--config cfg0|cfg1|cfg2|cfg3|cfg4] [--run-steps S]
+                  [--config cfg0|cfg1|cfg2|cfg3|cfg4|cfg5] [--run-steps S]
 
 --config selects the other BASELINE configs (supplementary lines): cfg0 the
 single nonlinear wall (replicas at N>1), cfg2 fp32 + variable dt (weak),
@@ -55,6 +55,11 @@ CONFIGS = {
     # so min(HBM, FP64) is the FP64 side; sharded (N>1) it streams 48 B/update
     "cfg4": dict(flop=33, bytes=4.06, bound="fp64", kernel="df_analytic_tiled", scaling="strong", dtype="f64",
                  run_steps=10_000),
+    # beyond BASELINE's five: load-bearing material walls.
+    # flop = the strict StarTables kernel's 2 evaluations x 82 flop (exp/log/pow/
+    # div = 1, §8(d) convention); the DF rows add ~41 flop and 48 B per update
+    "cfg5": dict(flop=164, bytes=0, bound="fp64", kernel="star_tables", scaling="weak", dtype="f64",
+                 run_steps=1_000),
 }
 
 
@@ -70,6 +75,7 @@ def parse():
     p.add_argument("--nodes", type=int, default=256)
     p.add_argument("--zones", type=int, default=8192)
     p.add_argument("--long-nodes", type=int, default=1 << 26)
+    p.add_argument("--material-walls", type=int, default=16384)
     p.add_argument("--halo", type=int, default=0, help="shard halo depth (0: config default)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -148,6 +154,9 @@ def make_workload(args, rank, world):
         return workloads.single_wall_d(nsteps=args.run_steps)
     if c == "cfg3":
         return workloads.zone_ring(n_zones=args.zones, nsteps=args.run_steps)
+    if c == "cfg5":
+        return workloads.material_walls(n_walls=args.material_walls, n_nodes=101, nsteps=args.run_steps,
+                                        seed=5 + rank)
     return workloads.long_domain(n_nodes=args.long_nodes, nsteps=args.run_steps)
 
 
@@ -207,6 +216,16 @@ def cpu_reference_rate(args, w, threads):
         nsteps = 10
     elif c == "cfg0":
         sub, init, nsteps = w.model, w.init, 20_000
+    elif c == "cfg5":
+        # the reference's df_step_nonlinear with CoefficientModel::material
+        nw = min(w.model.n_walls, 16 * threads)
+        from paper_1703_10119_b200.api import Model
+        m = w.model
+        n = m.n_nodes
+        sub = Model(n, m.dx, m.groups[:nw], m.biot[:nw], m.attach[:nw], channels=m.channels, dt=dt,
+                    coeff_kind="material", T_i=m.T_i, P_vi=m.P_vi, wall_reference=m.wall_reference[:nw])
+        init = {k: w.init[k][:nw * n] for k in ("u_prev", "u_curr", "v_prev", "v_curr")}
+        nsteps = 100
     else:
         sub, init = w.model, w.init
         nsteps = max(1, int(4e8 // w.cells))
@@ -219,6 +238,8 @@ def cpu_reference_rate(args, w, threads):
     cells = sub.n_walls * sub.n_nodes
     what = {"cfg0": "the reference's d(v) transcription oracle (df_oracle.hpp)" if ref else "oracle restatement",
             "cfg4": "the reference's d(v) transcription oracle on the first 2^22 nodes" if ref else "oracle",
+            "cfg5": "the reference's df_step_nonlinear with the load-bearing material (wall.cpp:196-264), "
+                    "threads split walls" if ref else "oracle restatement",
             }.get(c, "df_step_coupled (wall.cpp:144-194), threads split walls")
     imp = None
     if c in ("cfg1", "cfg2"):

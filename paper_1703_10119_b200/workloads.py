@@ -249,22 +249,25 @@ def material_reference(T_i=T_I, phi_i=PHI_I):
 
 def material_walls(n_walls=4096, n_nodes=101, nsteps=2000, dt=1e-3, seed=5) -> Workload:
     """Independent load-bearing material walls (CoefficientModel::material), both
-    faces exterior: a humid side v = 1 + 0.4 sin(2 pi t/6) and an outdoor side
+    faces exterior: a humid side v = 1 + 0.3 sin(2 pi t/6) and an outdoor side
     v = 1 + 0.24 sin(2 pi (t-6)/24), u = 1 (shapes of a single-slab scenario);
-    per-wall film coefficients log-uniform h_T in [5, 25], h_M in [3e-8, 8e-7];
+    per-wall film coefficients log-uniform around a slab's values, humid side
+    h_T in [15, 35], h_M in [8e-8, 2e-7], outdoor side h_T in [5, 12], h_M in
+    [2e-8, 5e-8] (larger moisture films cool the outdoor face by evaporation
+    until phi leaves the material box — a domain error in the reference too);
     L = 0.1 m, dx = 1/(n-1).  Strict evaluation in every DF step; implicit start."""
     rng = np.random.default_rng(seed)
     P_vi, ref = material_reference()
     groups = np.empty((n_walls, 4))
     biot = np.empty((n_walls, 2, 3))
-    hT = _log_uniform(rng, 5.0, 25.0, (n_walls, 2))
-    hM = _log_uniform(rng, 3e-8, 8e-7, (n_walls, 2))
+    hT = np.stack([_log_uniform(rng, 15.0, 35.0, n_walls), _log_uniform(rng, 5.0, 12.0, n_walls)], axis=1)
+    hM = np.stack([_log_uniform(rng, 8e-8, 2e-7, n_walls), _log_uniform(rng, 2e-8, 5e-8, n_walls)], axis=1)
     for w in range(n_walls):
         g, b = api.scale_wall(ref, 0.1, hT[w, 0], hM[w, 0], hT[w, 1], hM[w, 1], T_I, PHI_I, T0)
         groups[w], biot[w] = g, b
     attach = np.zeros((n_walls, 2, 2), dtype=np.int32)
     attach[:, 1, 1] = 1
-    ch = [ChannelSpec(v_inf=Signal.sinusoid(1.0, 0.40, 6.0)),
+    ch = [ChannelSpec(v_inf=Signal.sinusoid(1.0, 0.30, 6.0)),
           ChannelSpec(v_inf=Signal.sinusoid(1.0, 0.24, 24.0, 6.0))]
     model = Model(n_nodes, 1.0 / (n_nodes - 1), groups, biot, attach, channels=ch, dt=dt, eta_factor=1e-2,
                   coeff_kind="material", T_i=T_I, P_vi=P_vi, wall_reference=np.tile(ref, (n_walls, 1)))

@@ -1,0 +1,5 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-.}"
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_material.py -q -p no:cacheprovider -s > gpurun_out/pytest_gpu_mat1.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_mat1.log
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu_9.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_9.log
