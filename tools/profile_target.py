@@ -24,6 +24,8 @@ def main():
         w = workloads.single_wall_d(nsteps=steps)
     elif cfg == "cfg3":
         w = workloads.zone_ring(nsteps=steps)
+    elif cfg == "cfg5":
+        w = workloads.material_walls(n_walls=16384, n_nodes=101, nsteps=steps)
     else:
         w = workloads.long_domain(nsteps=steps)
     with Context(w.model) as ctx:
