@@ -10,8 +10,11 @@
 //    (signal.hpp exposes only operator()(t)), so the adapter evaluates every
 //    face, zone-source and outdoor Signal at the run's layer times (the
 //    reference's accumulated t) and uploads them as per-layer tables.
-//    Device coverage: constant-coefficient walls on one grid, zones,
-//    interzone links; no radiation.  Anything else throws
+//    Device coverage: walls on one grid with constant coefficients or the
+//    load-bearing material (CoefficientModel::material with the model's
+//    ScalingContext), zones, interzone links and radiation links.  Anything
+//    else (another scheme, mixed grids, a material model whose starred sets
+//    the device cannot reproduce bit for bit on the host) throws
 //    std::invalid_argument before touching the device.
 #pragma once
 
@@ -58,6 +61,7 @@ private:
 #ifdef HYGRO_B200_WITH_REFERENCE
 #include "hygro/building.hpp"
 #include "hygro/errors.hpp"
+#include "hygro/materials.hpp"
 
 namespace hygro::gpu {
 
@@ -82,6 +86,52 @@ inline hyg_signal constant(double v) {
         case HYG_EINVAL: throw std::invalid_argument(msg);
         default: throw std::runtime_error(msg);
     }
+}
+
+// The reference set of a material wall.  CoefficientModel keeps it private;
+// star(u, v) = evaluate(u T_i, v P_vi) / reference (wall.cpp:50-53), so at
+// (1, 1) reference = evaluate(T_i, P_vi) / star(1, 1), then checked (and
+// nudged by an ulp where the division rounded) against star() at sample
+// states, so the device divides by exactly the reference's numbers.
+inline hyg_coeff_set material_reference(const CoefficientModel& cm, const ScalingContext& ctx) {
+    const MaterialModel mm;
+    const CoefficientSet e = mm.evaluate(ctx.T_i, ctx.P_vi), s = cm.star(1.0, 1.0);
+    double r[6] = {e.c_M / s.c_M, e.k_M / s.k_M, e.c_TT / s.c_TT, e.k_TT / s.k_TT, e.c_TM / s.c_TM, e.k_TM / s.k_TM};
+    const double probes[4][2] = {{1.0, 1.0}, {1.01, 0.9}, {0.98, 1.2}, {1.03, 0.7}};
+    for (int f = 0; f < 6; ++f) {
+        auto field = [f](const CoefficientSet& c) {
+            const double v[6] = {c.c_M, c.k_M, c.c_TT, c.k_TT, c.c_TM, c.k_TM};
+            return v[f];
+        };
+        auto matches = [&](double ref) {
+            for (const auto& p : probes) {
+                CoefficientSet a, b;
+                try {                     // probes outside the material box are skipped
+                    a = mm.evaluate(p[0] * ctx.T_i, p[1] * ctx.P_vi);
+                    b = cm.star(p[0], p[1]);
+                } catch (const domain_error&) {
+                    continue;
+                }
+                if (field(a) / ref != field(b)) return false;
+            }
+            return true;
+        };
+        const double lo1 = std::nextafter(r[f], 0.0), hi1 = std::nextafter(r[f], 1e300);
+        const double cands[5] = {r[f], lo1, hi1, std::nextafter(lo1, 0.0), std::nextafter(hi1, 1e300)};
+        bool ok = false;
+        for (double cand : cands) {
+            if (matches(cand)) {
+                r[f] = cand;
+                ok = true;
+                break;
+            }
+        }
+        if (!ok)
+            throw std::invalid_argument(
+                "hygro::gpu::run: material wall whose starred sets the device cannot reproduce "
+                "(a scaling context or physical constants other than the model's)");
+    }
+    return hyg_coeff_set{r[0], r[1], r[2], r[3], r[4], r[5]};
 }
 
 struct Frames {
@@ -121,14 +171,22 @@ inline SimulationResult run(const BuildingModel& m, double cadence, SimulationRe
     const int nw = static_cast<int>(m.walls.size());
     const int nz = static_cast<int>(m.zones.size());
     const int n = m.walls[0].grid.n;
-    for (const auto& w : m.walls) {
-        if (w.grid.n != n || w.grid.dx != m.walls[0].grid.dx)
+    std::vector<int32_t> wall_coeff(nw, HYG_COEFF_CONSTANT);
+    std::vector<hyg_coeff_set> wall_ref(nw, hyg_coeff_set{1, 1, 1, 1, 1, 1});
+    std::vector<double> thickness(nw), k_TT0(nw);
+    bool any_material = false;
+    for (int w = 0; w < nw; ++w) {
+        const BuildingWall& bw = m.walls[w];
+        if (bw.grid.n != n || bw.grid.dx != m.walls[0].grid.dx)
             throw std::invalid_argument("hygro::gpu::run: walls must share one grid");
-        if (!w.coeffs.is_constant())
-            throw std::invalid_argument("hygro::gpu::run: material walls are not on the device yet");
+        if (!bw.coeffs.is_constant()) {
+            wall_coeff[w] = HYG_COEFF_MATERIAL;
+            wall_ref[w] = detail::material_reference(bw.coeffs, m.ctx);
+            any_material = true;
+        }
+        thickness[w] = bw.thickness;
+        k_TT0[w] = bw.k_TT0;
     }
-    for (const auto& z : m.zones)
-        if (!z.radiation.empty()) throw std::invalid_argument("hygro::gpu::run: radiation not supported");
 
     const long nsteps = std::lround(m.horizon / m.dt);
     std::vector<double> times(static_cast<size_t>(nsteps) + 1);
@@ -160,6 +218,7 @@ inline SimulationResult run(const BuildingModel& m, double cadence, SimulationRe
     std::vector<hyg_channel> channels(std::max<size_t>(1, ext.size()), hyg_channel{c1, c1, c0, c0});
     std::vector<std::vector<hyg_zone_wall_link>> zl(nz);
     std::vector<std::vector<hyg_interzone_link>> il(nz);
+    std::vector<std::vector<hyg_radiation_link>> rl(nz);
     std::vector<hyg_zone_desc> zones(nz);
     std::vector<hyg_zone_sources> sources(std::max(1, nz), hyg_zone_sources{c0, c0, c0});
     for (int z = 0; z < nz; ++z) {
@@ -167,18 +226,27 @@ inline SimulationResult run(const BuildingModel& m, double cadence, SimulationRe
         for (const auto& l : zc.walls)
             zl[z].push_back(hyg_zone_wall_link{l.wall, l.face, l.Bi_M, l.Bi_TT, l.Bi_TM, l.theta_T, l.theta_M});
         for (const auto& l : zc.interzone) il[z].push_back(hyg_interzone_link{l.peer, l.g_inz, l.q_inz1, l.q_inz2});
+        for (const auto& r : zc.radiation)
+            rl[z].push_back(hyg_radiation_link{r.emitter_wall, r.receiver_wall, r.view_factor, r.emissivity});
         zones[z] = hyg_zone_desc{zc.params.kappa_a_tt1, zc.params.g_v, zc.params.q_v1, zc.params.q_v2, z,
                                  zc.moisture_sign == MoistureWallSign::AsPrinted ? HYG_MOISTURE_AS_PRINTED
                                                                                   : HYG_MOISTURE_FLUX_CONSISTENT,
                                  static_cast<int32_t>(zl[z].size()), zl[z].data(),
-                                 static_cast<int32_t>(il[z].size()), il[z].data()};
+                                 static_cast<int32_t>(il[z].size()), il[z].data(),
+                                 static_cast<int32_t>(rl[z].size()), rl[z].data()};
     }
     hyg_model_desc d{};
     d.n_walls = nw;
     d.n_nodes = n;
     d.dx = m.walls[0].grid.dx;
     d.precision = HYG_F64;
-    d.coeff_kind = HYG_COEFF_CONSTANT;
+    d.coeff_kind = any_material ? HYG_COEFF_MATERIAL : HYG_COEFF_CONSTANT;
+    d.T_i = m.ctx.T_i;
+    d.P_vi = m.ctx.P_vi;
+    d.wall_coeff = wall_coeff.data();
+    d.wall_reference = wall_ref.data();
+    d.wall_thickness = thickness.data();
+    d.wall_k_TT0 = k_TT0.data();
     d.groups = groups.data();
     d.biot = biot.data();
     d.attach = attach.data();

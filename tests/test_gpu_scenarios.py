@@ -1,0 +1,30 @@
+"""`hygrosim run` end to end: scenario JSON -> the
+reference's loader -> run() on the CPU and the drop-in hygro::gpu::run on the
+device -> the reference's own time-series CSV writer for both, compared row
+by row (oracle/scenario_check.cpp).  Scenarios (tests/golden/scenarios/,
+written for these tests in the reference's schema): a load-bearing slab, a
+two-zone building with material and frozen walls, a shared partition,
+radiation links, solar flux and schedules, and a three-zone frozen ring."""
+import subprocess
+
+import pytest
+
+from .conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+EXE = ROOT / "oracle" / "_ref" / "scenario_check"
+SCEN = sorted((ROOT / "tests" / "golden" / "scenarios").glob("*.json"))
+
+
+@pytest.mark.skipif(not EXE.exists(), reason="scenario_check not built (needs /root/reference at build time)")
+@pytest.mark.parametrize("path", SCEN, ids=[p.stem for p in SCEN])
+def test_scenario_csv_matches_reference(path, tmp_path):
+    r = subprocess.run([str(EXE), str(path), str(tmp_path)], capture_output=True, text=True, timeout=900)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stdout + r.stderr
+    cpu = (tmp_path / "cpu.csv").read_text().splitlines()
+    gpu = (tmp_path / "gpu.csv").read_text().splitlines()
+    assert len(cpu) == len(gpu) > 1
+    same = sum(a == b for a, b in zip(cpu, gpu))
+    assert same / len(cpu) > 0.95        # %.12g hides the ~1e-14 differences in nearly every row
