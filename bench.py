@@ -91,22 +91,54 @@ def dist_env():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line).
-    Started before the warm-up (its start-up must not fall inside the timed
-    region); samples are filtered to the region's wall-clock window."""
+    """SM clock / throttle-reason sampling during the timed region (the
+    B200_PROFILING.md clocks line).  In-process NVML queries every 200 ms
+    (cheap ioctls; a polling nvidia-smi child takes driver locks that stall
+    launch-heavy paths), nvidia-smi -lms as the fallback.  Started before the
+    warm-up; samples are filtered to the region's wall-clock window."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.proc, self.nvml = index, [], None, None
+        self.stop_flag = threading.Event()
+        self.source = "none"
 
     def start(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            bits = [N.nvmlClocksThrottleReasonHwSlowdown, N.nvmlClocksThrottleReasonHwThermalSlowdown,
+                    N.nvmlClocksThrottleReasonSwThermalSlowdown, N.nvmlClocksThrottleReasonSwPowerCap]
+            smax = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+
+            def poll():
+                while not self.stop_flag.is_set():
+                    try:
+                        sm = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                        pw = N.nvmlDeviceGetPowerUsage(h) / 1000.0
+                        r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                        self.rows.append((time.time(), [sm, smax, pw] + [bool(r & b) for b in bits]))
+                    except Exception:
+                        pass
+                    self.stop_flag.wait(0.2)
+
+            self.nvml = N
+            self.source = "nvml"
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.source = "nvidia-smi"
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except OSError:
@@ -115,31 +147,36 @@ class Clocks:
     def _read(self):
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 7:
-                self.rows.append((time.time(), parts))
+            if len(parts) == 7 and parts[0].replace(".", "").isdigit():
+                try:
+                    self.rows.append((time.time(), [float(parts[0]), float(parts[1]),
+                                                    float(parts[2]) if parts[2].replace(".", "").isdigit() else 0.0]
+                                      + [p.lower().startswith("active") for p in parts[3:]]))
+                except ValueError:
+                    pass
 
     def mark(self, which: str):
         setattr(self, which, time.time())
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
+        self.stop_flag.set()
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.source == "none":
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock source"]}
         self.t.join(timeout=2)
         t0, t1 = getattr(self, "t_start", 0.0), getattr(self, "t_end", 1e30)
-        rows = [r for (ts, r) in self.rows if t0 <= ts <= t1 and r[0].replace(".", "").isdigit()]
+        rows = [r for (ts, r) in self.rows if t0 <= ts <= t1]
         if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = [float(r[0]) for r in rows]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower().startswith("active")})
-        pw = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
-                "samples": len(rows), "power_w_max": max(pw) if pw else None}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "source": self.source}
+        sm = [r[0] for r in rows]
+        reasons = sorted({self.NAMES[i] for r in rows for i in range(4) if r[3 + i]})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": rows[0][1], "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(r[2] for r in rows), "source": self.source}
 
 
 def make_workload(args, rank, world):
