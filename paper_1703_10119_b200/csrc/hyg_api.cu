@@ -396,10 +396,7 @@ StepArgs step_args(hyg_ctx* c, int from, double dt) {
     return a;
 }
 
-// StarTables of layer (u, v) for every nonlinear wall into c->d_star.
-int launch_star_tables(hyg_ctx* c, const double* u, const double* v, bool strict, int64_t layer,
-                       hyg_status* status) {
-    if (!c->d_star) HYG_CUDA(cudaMalloc(&c->d_star, sizeof(double) * 9 * static_cast<size_t>(c->cells())));
+StarArgs star_args(hyg_ctx* c, const double* u, const double* v, bool strict, int64_t layer) {
     StarArgs s{};
     s.n_walls = c->n_walls;
     s.n = c->n;
@@ -419,6 +416,14 @@ int launch_star_tables(hyg_ctx* c, const double* u, const double* v, bool strict
     s.dom_key = c->d_dom;
     s.own0 = c->own_c0;
     s.own1 = c->own_c1;
+    return s;
+}
+
+// StarTables of layer (u, v) for every nonlinear wall into c->d_star.
+int launch_star_tables(hyg_ctx* c, const double* u, const double* v, bool strict, int64_t layer,
+                       hyg_status* status) {
+    if (!c->d_star) HYG_CUDA(cudaMalloc(&c->d_star, sizeof(double) * 9 * static_cast<size_t>(c->cells())));
+    StarArgs s = star_args(c, u, v, strict, layer);
     LaunchScope ls(c, strict ? "star_tables" : "star_tables_clamped", static_cast<double>(c->cells()));
     k_star_tables<<<static_cast<int>((c->cells() + 127) / 128), 128, 0, c->stream>>>(s);
     return HYG_OK;
@@ -550,21 +555,45 @@ int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
         for (int64_t k = 0; k < rows; ++k) {
             // layer-n radiation fluxes and frozen coefficients (building.cpp:158; wall.cpp:206)
             if (c->has_rad) launch_radiation(c, c->s64[c->cur][1]);
-            if (c->any_material) {
-                rc = launch_star_tables(c, c->s64[c->cur][1], c->s64[c->cur][3], true, c->layer + k, status);
-                if (rc) return rc;
-            }
             StepArgs a = step_args(c, c->cur, dt);
             a.amb = c->d_table + k * nch;
             a.layer = c->layer + k;
-            if (c->zones.empty()) {
+            if (kind == kCoeffMaterial) {
+                // StarTables + rows + zones in one launch (k_material_step)
+                const StarArgs sa = star_args(c, a.in[1], a.in[3], true, c->layer + k);
+                ZoneArgs z{};
+                if (!c->zones.empty()) {
+                    z.n_zones = static_cast<int>(c->zones.size());
+                    z.n = c->n;
+                    z.dt = dt;
+                    z.zones = c->d_zones;
+                    z.links = c->d_zlinks;
+                    z.inz = c->d_inz;
+                    z.src = c->d_src + k * (nsrc * 3 + 2);
+                    z.n_sources = nsrc;
+                    z.uc = c->s64[c->cur][1];
+                    z.vc = c->s64[c->cur][3];
+                    z.zu_in = c->zu[c->zcur];
+                    z.zv_in = c->zv[c->zcur];
+                    z.zu_out = c->zu[1 - c->zcur];
+                    z.zv_out = c->zv[1 - c->zcur];
+                    z.layer = c->layer + k;
+                    z.norm = c->norm;
+                    z.fail_key = c->d_key;
+                    z.own0 = c->own_z0;
+                    z.own1 = c->own_z1;
+                }
+                const int mgrid = static_cast<int>((c->cells() + kMatCells - 1) / kMatCells);
+                const int zblocks = (z.n_zones + kMatThreads - 1) / kMatThreads;
+                LaunchScope ls(c, "material_step", static_cast<double>(c->cells()));
+                k_material_step<<<mgrid + zblocks, kMatThreads, 0, c->stream>>>(a, sa, z, mgrid);
+                if (!c->zones.empty()) c->zcur ^= 1;
+            } else if (c->zones.empty()) {
                 LaunchScope ls(c, "df_step_general", static_cast<double>(c->cells()));
                 if (kind == kCoeffConstant)
                     k_df_step_general<kCoeffConstant><<<grid, threads, 0, c->stream>>>(a);
-                else if (kind == kCoeffAnalyticD)
-                    k_df_step_general<kCoeffAnalyticD><<<grid, threads, 0, c->stream>>>(a);
                 else
-                    k_df_step_general<kCoeffMaterial><<<grid, threads, 0, c->stream>>>(a);
+                    k_df_step_general<kCoeffAnalyticD><<<grid, threads, 0, c->stream>>>(a);
             } else {
                 ZoneArgs z{};
                 z.n_zones = static_cast<int>(c->zones.size());
@@ -590,10 +619,8 @@ int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
                 LaunchScope ls(c, "building_step", static_cast<double>(c->cells()));
                 if (kind == kCoeffConstant)
                     k_building_step<kCoeffConstant><<<grid + zblocks, threads, 0, c->stream>>>(a, z, grid);
-                else if (kind == kCoeffAnalyticD)
-                    k_building_step<kCoeffAnalyticD><<<grid + zblocks, threads, 0, c->stream>>>(a, z, grid);
                 else
-                    k_building_step<kCoeffMaterial><<<grid + zblocks, threads, 0, c->stream>>>(a, z, grid);
+                    k_building_step<kCoeffAnalyticD><<<grid + zblocks, threads, 0, c->stream>>>(a, z, grid);
                 c->zcur ^= 1;
             }
             rotate_layers(c);

@@ -219,3 +219,132 @@ __global__ void k_radiation(const RadArgs a) {
 }
 
 }  // namespace hyg
+
+namespace hyg {
+
+// ---- fused material step --------------------------------------------------------
+// One DF step of a building whose walls are (partly) material walls, StarTables
+// and rows in one launch: a 256-thread CTA owns 255 consecutive cells; thread t
+// evaluates the node set of cell base+t (t < 255) and the half set between
+// cells base+t-1 and base+t (the 256 half nodes its 255 cells need), both into
+// shared memory — two evaluations per lane as in the reference, balanced
+// across warps — then runs the literal rows of df_step_nonlinear (material
+// walls) or the increment rows (constant walls) for its cell.  A strict
+// evaluation outside the box raises the domain key; the step's outputs go to
+// the scratch layer and the host discards them (the failing step never ran).
+// Blocks >= wall_blocks advance the zones (k_building_step).
+constexpr int kMatThreads = 256, kMatCells = 255;
+
+// df_step_nonlinear rows (wall.cpp:213-259) from the CTA's shared tables:
+// node f at nS[f*256 + t], half (j-1)+1/2 at hS[f*256 + t], j+1/2 at hS[f*256 + t+1]
+__device__ __forceinline__ void material_cell(const StepArgs& a, const NodeIn& x, int w, int j, const double* nS,
+                                              const double* hS, int t, double& un, double& vn) {
+    const int n = a.n;
+    const double dx = a.dx, dt = a.dt;
+    const Groups p = a.groups[w];
+    const double ad = p.Fo_M * dt / (dx * dx);
+    const double b_ = p.Fo_TT * dt / (dx * dx);
+    const double g_ = p.Fo_TM * p.gamma * dt / (dx * dx);
+    const double ratio = p.Fo_TT != 0.0 ? p.Fo_TM * p.gamma / p.Fo_TT : 0.0;
+    auto nd = [&](int f) { return nS[f * kMatThreads + t]; };
+    auto hl = [&](int f) { return hS[f * kMatThreads + t]; };       // (j-1)+1/2
+    auto hr = [&](int f) { return hS[f * kMatThreads + t + 1]; };   // j+1/2
+    if (j > 0 && j < n - 1) {
+        const double kp = hr(kHk_M), km = hl(kHk_M), cm = nd(kSc_M);
+        vn = ((cm - ad * (kp + km)) * x.vp + 2.0 * ad * (kp * x.vr + km * x.vl)) / (cm + ad * (kp + km));
+        const double ktp = hr(kHk_TT), ktm = hl(kHk_TT), kmp = hr(kHk_TM), kmm = hl(kHk_TM);
+        const double ctt = nd(kSc_TT), ctm = nd(kSc_TM);
+        un = ((ctt - b_ * (ktp + ktm)) * x.up - p.gamma * ctm * (vn - x.vp) +
+              2.0 * b_ * (ktp * x.ur + ktm * x.ul) + 2.0 * g_ * (kmp * x.vr + kmm * x.vl) -
+              g_ * (kmp + kmm) * (vn + x.vp)) /
+             (ctt + b_ * (ktp + ktm));
+        return;
+    }
+    const int k = j == 0 ? 0 : 1;
+    const double vcn = j == 0 ? x.vr : x.vl, ucn = j == 0 ? x.ur : x.ul;
+    const FaceVals b = resolve(a, w, k);
+    auto hb = [&](int f) { return j == 0 ? hr(f) : hl(f); };         // half_front / half_back
+    const double km_b = nd(kSk_M), kp_b = hb(kHk_M), cm = nd(kSc_M);
+    const double cpl = 2.0 * ad * dx * b.Bi_M;
+    vn = ((cm - ad * (kp_b + km_b) - cpl) * x.vp + 2.0 * ad * (kp_b + km_b) * vcn +
+          4.0 * ad * dx * (b.Bi_M * b.v_inf + b.g_inf)) /
+         (cm + ad * (kp_b + km_b) + cpl);
+    const double kt_b = nd(kSk_TT), kTM_b = nd(kSk_TM);
+    const double ktp_b = hb(kHk_TT), kmp_b = hb(kHk_TM);
+    const double ctt = nd(kSc_TT), ctm = nd(kSc_TM);
+    const double vbar = 0.5 * (vn + x.vp);
+    const double vg = vcn - (2.0 * dx / km_b) * (b.Bi_M * (vbar - b.v_inf) - b.g_inf);
+    const double cplu = 2.0 * b_ * dx * b.Bi_TT;
+    un = ((ctt - b_ * (ktp_b + kt_b) - cplu) * x.up - p.gamma * ctm * (vn - x.vp) +
+          2.0 * b_ * (ktp_b + kt_b) * ucn + 2.0 * b_ * ratio * kTM_b * (vcn - vg) -
+          4.0 * b_ * dx * (b.Bi_TM * (vbar - b.v_inf) - b.q_inf) + 2.0 * cplu * b.u_inf +
+          2.0 * g_ * (kmp_b * vcn + kTM_b * vg) - g_ * (kmp_b + kTM_b) * (vn + x.vp)) /
+         (ctt + b_ * (ktp_b + kt_b) + cplu);
+}
+
+__global__ void __launch_bounds__(kMatThreads) k_material_step(const StepArgs a, const StarArgs s,
+                                                              const ZoneArgs z, int wall_blocks) {
+    if (static_cast<int>(blockIdx.x) >= wall_blocks) {              // zones (step_explicit :179-183)
+        const int zi = (static_cast<int>(blockIdx.x) - wall_blocks) * blockDim.x + threadIdx.x;
+        if (zi < z.n_zones && !frozen_before(z.fail_key, z.layer)) zone_update(z, zi);
+        return;
+    }
+    __shared__ double nS[6 * kMatThreads];
+    __shared__ double hS[3 * kMatThreads];
+    const int t = threadIdx.x;
+    const int64_t total = static_cast<int64_t>(a.n_walls) * a.n;
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * kMatCells + t;
+    const bool out_cell = t < kMatCells && c < total;
+    // loads first (they overlap the evaluations)
+    int w = 0, j = 0;
+    NodeIn x{};
+    if (c < total) {
+        w = static_cast<int>(c / a.n);
+        j = static_cast<int>(c - static_cast<int64_t>(w) * a.n);
+    }
+    if (out_cell) x = load_node(a, w, j);
+    const bool frozen = frozen_before(a.fail_key, a.layer);
+    const int wk = c < total ? a.wall_kind[w] : kCoeffConstant;
+    const bool own = c >= a.own0 && c < a.own1;
+    const double nan = __longlong_as_double(0x7ff8000000000000ll);
+    if (!frozen && wk != kCoeffConstant) {
+        mat::Set m;
+        if (out_cell) {                                              // node j
+            if (!star_at(s, wk, w, x.uc, x.vc, m)) {
+                if (own) star_fail(s, w, static_cast<unsigned>(j));
+                m = mat::Set{nan, nan, nan, nan, nan, nan};
+            }
+            nS[kSc_M * kMatThreads + t] = m.c_M;
+            nS[kSk_M * kMatThreads + t] = m.k_M;
+            nS[kSc_TT * kMatThreads + t] = m.c_TT;
+            nS[kSk_TT * kMatThreads + t] = m.k_TT;
+            nS[kSc_TM * kMatThreads + t] = m.c_TM;
+            nS[kSk_TM * kMatThreads + t] = m.k_TM;
+        }
+        if (j > 0) {                                                 // half (j-1)+1/2
+            const double ul = a.in[1][c - 1], vl = a.in[3][c - 1];
+            const double uh = out_cell ? x.uc : a.in[1][c], vh = out_cell ? x.vc : a.in[3][c];
+            if (!star_at(s, wk, w, 0.5 * (ul + uh), 0.5 * (vl + vh), m)) {
+                if (own) star_fail(s, w, static_cast<unsigned>(a.n + j - 1));
+                m.k_M = m.k_TT = m.k_TM = nan;
+            }
+            hS[kHk_M * kMatThreads + t] = m.k_M;
+            hS[kHk_TT * kMatThreads + t] = m.k_TT;
+            hS[kHk_TM * kMatThreads + t] = m.k_TM;
+        }
+    }
+    __syncthreads();
+    if (!out_cell || frozen) return;
+    double un, vn;
+    if (wk == kCoeffConstant) coupled_node(a, w, j, x, un, vn);
+    else material_cell(a, x, w, j, nS, hS, t, un, vn);
+    a.out[1][c] = un;
+    a.out[3][c] = vn;
+    if (own && (!(fabs(un) <= a.norm) || !(fabs(vn) <= a.norm))) {
+        const unsigned long long key =
+            (static_cast<unsigned long long>(a.layer + 1) << 32) | static_cast<unsigned>(w);
+        atomicMin(a.fail_key, key);
+    }
+}
+
+}  // namespace hyg
