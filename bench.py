@@ -55,10 +55,10 @@ CONFIGS = {
     # so min(HBM, FP64) is the FP64 side; sharded (N>1) it streams 48 B/update
     "cfg4": dict(flop=33, bytes=4.06, bound="fp64", kernel="df_analytic_tiled", scaling="strong", dtype="f64",
                  run_steps=10_000),
-    # beyond BASELINE's five: load-bearing material walls.
-    # flop = the strict StarTables kernel's 2 evaluations x 82 flop (exp/log/pow/
-    # div = 1, §8(d) convention); the DF rows add ~41 flop and 48 B per update
-    "cfg5": dict(flop=164, bytes=0, bound="fp64", kernel="star_tables", scaling="weak", dtype="f64",
+    # beyond BASELINE's five: load-bearing material walls,
+    # k_material_step: 2 strict evaluations x 82 flop (exp/log/pow/div = 1, the
+    # §8(d) convention) + ~41 flop of df_step_nonlinear rows per update, 48 B
+    "cfg5": dict(flop=205, bytes=48, bound="fp64", kernel="material_step", scaling="weak", dtype="f64",
                  run_steps=1_000),
 }
 

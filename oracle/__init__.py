@@ -286,6 +286,7 @@ class Building:
         else:
             rc = ref_lib().ref_building_march(C.byref(self.desc), C.byref(self.s), nsteps, int(with_bootstrap),
                                               C.byref(fl), C.byref(bp))
+        self.fail_wall = fw.value
         return rc, fl.value, bp.value
 
     @staticmethod

@@ -23,12 +23,14 @@
 #include "k_nonlinear.cuh"
 #include "k_tiled.cuh"
 #include "k_material.cuh"
+#include "k_ring.cuh"
 
 using namespace hyg;
 
 namespace {
 
 constexpr int kChunk = 128;     // forcing rows staged per shared-memory chunk
+constexpr int kRingS = 8;       // K4: steps per launch (halo depth S-1 zones)
 constexpr int kWarps = 4;       // warps per CTA of K1
 
 struct SigHost {
@@ -194,6 +196,8 @@ struct hyg_ctx {
     double* d_star = nullptr;        // StarTables scratch [9][cells] (allocated on first use)
     unsigned long long* d_dom = nullptr;
     bool has_rad = false;
+    bool ring = false;               // K4: zone-ring temporal blocking applies
+    int ring_W = 0, ring_B = 0;
     int rad_groups = 0, rad_terms = 0;
     int *d_rad_tgt = nullptr, *d_rad_grp = nullptr;
     double *d_rad_num = nullptr, *d_rad_den = nullptr, *d_rad_coef = nullptr, *d_qrad = nullptr;
@@ -914,6 +918,107 @@ int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
     return HYG_OK;
 }
 
+// ---- the zone-ring temporally blocked path (K4) ---------------------------------
+template <int NPT>
+void launch_ring(const RingArgs& a, int grid, int threads, size_t smem, cudaStream_t s) {
+    auto k = k_ring_tiled<NPT, kRingS>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
+    }
+    k<<<grid, threads, smem, s>>>(a);
+}
+
+int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
+    if (c->coef_dt != dt) {
+        LaunchScope ls(c, "coupled_coef", 0.0);
+        k_coupled_coef<<<(c->n_walls + 127) / 128, 128, 0, c->stream>>>(c->n_walls, c->dx, dt, c->d_groups,
+                                                                         c->d_biot, c->d_coef);
+        c->coef_dt = dt;
+    }
+    const int nch = std::max<int>(1, static_cast<int>(c->channels.size()));
+    const int nsrc = static_cast<int>(c->zsrc.size() / 3);
+    const int Z = static_cast<int>(c->zones.size()), W = c->ring_W, B = c->ring_B, npt = c->n / 16;
+    const int grid = (Z + B - 1) / B;
+    const int threads = RingShape<8, kRingS>::threads(B, W);
+    const size_t smem = npt == 4 ? RingShape<4, kRingS>::smem_bytes(B, W)
+                        : npt == 8 ? RingShape<8, kRingS>::smem_bytes(B, W)
+                                   : RingShape<16, kRingS>::smem_bytes(B, W);
+    const int64_t block = 65536 / kRingS * kRingS;
+    for (int64_t done = 0; done < nsteps;) {
+        const int64_t rows = std::min(block, nsteps - done);
+        std::vector<double> times(rows);
+        double t = c->t;
+        for (int64_t k = 0; k < rows; ++k) {
+            times[k] = t;
+            t += dt;
+        }
+        int rc = upload_table(c, c->layer, times, status);
+        if (rc) return rc;
+        rc = upload_src(c, c->layer, times, status);
+        if (rc) return rc;
+        HYG_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+        RingArgs a{};
+        a.n_zones = Z;
+        a.W = W;
+        a.n = c->n;
+        a.B = B;
+        a.norm = c->norm;
+        a.biot = c->d_biot;
+        a.attach = c->d_attach;
+        a.coef = c->d_coef;
+        a.n_channels = nch;
+        a.n_sources = nsrc;
+        a.dt = dt;
+        a.zones = c->d_zones;
+        a.links = c->d_zlinks;
+        a.inz = c->d_inz;
+        a.stop = c->d_flag;
+        const int cur0 = c->cur, z0 = c->zcur;
+        int nseg = 0;
+        for (int64_t s0 = 0; s0 < rows; s0 += kRingS, ++nseg) {
+            a.steps = static_cast<int>(std::min<int64_t>(kRingS, rows - s0));
+            a.seg_index = nseg;
+            a.table = c->d_table + s0 * nch;
+            a.src = c->d_src + s0 * (3 * nsrc + 2);
+            const int from = (cur0 + nseg) & 1, zf = (z0 + nseg) & 1;
+            for (int i = 0; i < 4; ++i) {
+                a.in[i] = c->s64[from][i];
+                a.out[i] = c->s64[1 - from][i];
+            }
+            a.zu_in = c->zu[zf];
+            a.zv_in = c->zv[zf];
+            a.zu_out = c->zu[1 - zf];
+            a.zv_out = c->zv[1 - zf];
+            LaunchScope ls(c, "ring_tiled", static_cast<double>(c->cells()) * a.steps);
+            if (npt == 4) launch_ring<4>(a, grid, threads, smem, c->stream);
+            else if (npt == 8) launch_ring<8>(a, grid, threads, smem, c->stream);
+            else launch_ring<16>(a, grid, threads, smem, c->stream);
+        }
+        HYG_CUDA(cudaGetLastError());
+        int flag = 0;
+        HYG_CUDA(cudaMemcpyAsync(&flag, c->d_flag, sizeof flag, cudaMemcpyDeviceToHost, c->stream));
+        HYG_CUDA(cudaStreamSynchronize(c->stream));
+        if (flag == 0) {
+            c->cur = (cur0 + nseg) & 1;
+            c->zcur = (z0 + nseg) & 1;
+            c->t = t;
+            c->layer += rows;
+            done += rows;
+            continue;
+        }
+        // the guard fired in launch K (its input intact): exact per-step path from there
+        const int64_t k0 = static_cast<int64_t>(flag - 1) * kRingS;
+        c->cur = (cur0 + flag - 1) & 1;
+        c->zcur = (z0 + flag - 1) & 1;
+        c->t = times[k0];
+        c->layer += k0;
+        return advance_general(c, nsteps - done - k0, dt, status);
+    }
+    return HYG_OK;
+}
+
 int advance_fused(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
     if (c->precision == HYG_F32) return advance_fused_t<float>(c, c->s32, nsteps, dt, status);
     return advance_fused_t<double>(c, c->s64, nsteps, dt, status);
@@ -1178,6 +1283,43 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
     }
     for (int i = 0; i < 2 * c->n_walls; ++i) rad_tgt[i + 1] += rad_tgt[i];
     c->has_rad = !rg.empty();
+    // K4 (k_ring.cuh): constant walls, face 0 exterior, face 1 on the wall's own
+    // zone, W walls per zone in zone order, zone links = those walls' face 1,
+    // inter-zone peers within +-1 on the ring, n in {64, 128, 256}, no radiation
+    if (d->coeff_kind == HYG_COEFF_CONSTANT && d->precision == HYG_F64 && d->n_zones > 0 && !c->has_rad &&
+        c->n_walls % d->n_zones == 0 && (c->n == 64 || c->n == 128 || c->n == 256)) {
+        const int W = c->n_walls / d->n_zones, Z = d->n_zones;
+        bool ok = W >= 1;
+        for (int w = 0; ok && w < c->n_walls; ++w)
+            ok = d->attach[2 * w].kind == HYG_FACE_EXTERIOR && d->attach[2 * w + 1].kind == HYG_FACE_ZONE &&
+                 d->attach[2 * w + 1].index == w / W;
+        for (int z = 0; ok && z < Z; ++z) {
+            const hyg_zone_desc& zd = d->zones[z];
+            for (int i = 0; ok && i < zd.n_walls; ++i)
+                ok = zd.walls[i].face == 1 && zd.walls[i].wall / W == z;
+            for (int i = 0; ok && i < zd.n_interzone; ++i) {
+                const int p = zd.interzone[i].peer;
+                ok = p == (z + 1) % Z || p == (z - 1 + Z) % Z;
+            }
+        }
+        if (ok) {
+            const int npt = c->n / 16;
+            int B = std::min(Z, 32 - 2 * kRingS);
+            auto fits = [&](int b) {
+                const size_t sm = npt == 4 ? RingShape<4, kRingS>::smem_bytes(b, W)
+                                  : npt == 8 ? RingShape<8, kRingS>::smem_bytes(b, W)
+                                             : RingShape<16, kRingS>::smem_bytes(b, W);
+                const int th = RingShape<8, kRingS>::threads(b, W);
+                return sm <= 227u * 1024u && th <= 896;
+            };
+            while (B > 0 && !fits(B)) --B;
+            if (B >= 1) {
+                c->ring = true;
+                c->ring_W = W;
+                c->ring_B = B;
+            }
+        }
+    }
     c->fused = all_exterior && d->n_zones == 0 && d->coeff_kind == HYG_COEFF_CONSTANT && fused_grid(c->n);
     c->nl_fused = all_exterior && d->n_zones == 0 && d->coeff_kind == HYG_COEFF_ANALYTIC_D && c->n <= 1024 &&
                   c->precision == HYG_F64;
@@ -1426,6 +1568,8 @@ int hyg_set_owned(hyg_ctx* c, int64_t cell0, int64_t cell1, int32_t zone0, int32
     // wall) stays: its fast guard only decides whether to replay on the
     // per-step path, which then applies the owned range exactly.
     if (cell0 > 0 || cell1 < c->cells()) c->fused = c->nl_fused = false;
+    // K4's guard and zone ownership are whole-CTA; shards take the exact per-step path
+    if (cell0 > 0 || cell1 < c->cells() || zone0 > 0 || zone1 < static_cast<int>(c->zones.size())) c->ring = false;
     return HYG_OK;
 }
 
@@ -1705,6 +1849,7 @@ int hyg_advance(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
     int rc = c->fused      ? advance_fused(c, nsteps, dt, status)
              : c->nl_fused ? advance_nonlinear(c, nsteps, dt, status)
              : c->tiled    ? advance_tiled(c, nsteps, dt, status)
+             : c->ring     ? advance_ring(c, nsteps, dt, status)
                            : advance_general(c, nsteps, dt, status);
     if (status && rc == HYG_OK) status->code = HYG_OK;
     return rc;

@@ -1,0 +1,88 @@
+"""K4 (k_ring.cuh): the zone-ring building march temporally blocked S = 8
+steps per launch with halo zones, against the C oracle's whole-building run
+(relative L-infinity <= 1e-10, zones included): zone counts that leave the
+last CTA partial, rings smaller than the halo (local copies of one zone), a
+chain without the wrap-around link, grids of 64/128/256 nodes, step counts
+that are not multiples of S, and a guard failure inside a launch (the host
+replays that launch's steps with the exact per-step path: same first failing
+layer and wall as the oracle)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1703_10119_b200 import Context, api, workloads
+
+from .helpers import rel_linf
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def _gpu(model, init, steps):
+    with Context(model) as ctx:
+        ctx.set_state(**init)
+        ctx.profiling(True)
+        st = ctx.bootstrap("implicit")
+        ctx.advance(steps - 1)
+        ctx.synchronize()
+        stats = {s["name"]: s for s in ctx.kernel_stats()}
+        out = ctx.get_state()
+    return out, st, stats
+
+
+def _oracle(model, init, steps):
+    b = O.Building(model, init)
+    rc, fl, passes = b.run("oracle", steps)
+    return b, rc, fl, passes
+
+
+@pytest.mark.parametrize("n_zones,wpz,n,steps", [(17, 6, 128, 203), (3, 6, 128, 100), (2, 4, 64, 150),
+                                                  (5, 6, 256, 120), (40, 6, 128, 1000), (1, 6, 128, 60)])
+def test_ring_matches_oracle(n_zones, wpz, n, steps):
+    w = workloads.zone_ring(n_zones=n_zones, walls_per_zone=wpz, n_nodes=n, nsteps=steps)
+    rng = np.random.default_rng(n_zones)
+    init = {k: v + (2e-3 * rng.standard_normal(v.size) if k in ("u_prev", "u_curr", "v_prev", "v_curr") else 0)
+            for k, v in w.init.items()}
+    got, st, stats = _gpu(w.model, init, steps)
+    assert stats.get("ring_tiled", {}).get("launches", 0) > 0, stats.keys()
+    b, rc, _, passes = _oracle(w.model, init, steps)
+    assert rc == 0 and st.subiterations == passes
+    err = rel_linf(got, dict(b.state))
+    zerr = max(float(np.max(np.abs(got["zone_u"] - b.zu[:n_zones]))),
+               float(np.max(np.abs(got["zone_v"] - b.zv[:n_zones]))))
+    print(n_zones, wpz, n, steps, "rel L-inf", err, "zone abs", zerr)
+    assert err <= TOL and zerr <= TOL
+
+
+def test_ring_chain_without_wrap():
+    w = workloads.zone_ring(n_zones=12, walls_per_zone=6, n_nodes=128, nsteps=300)
+    zs = w.model.zones
+    zs[0].interzone = [l for l in zs[0].interzone if l[0] == 1]
+    zs[-1].interzone = [l for l in zs[-1].interzone if l[0] == len(zs) - 2]
+    got, st, stats = _gpu(w.model, w.init, 300)
+    assert stats.get("ring_tiled", {}).get("launches", 0) > 0
+    b, rc, _, _ = _oracle(w.model, w.init, 300)
+    assert rc == 0
+    assert rel_linf(got, dict(b.state)) <= TOL
+    assert float(np.max(np.abs(got["zone_u"] - b.zu[:12]))) <= TOL
+
+
+def test_ring_guard_replay():
+    """A norm the march crosses mid-launch: first failing layer and lowest
+    failing wall exactly as the oracle's check_bounded."""
+    w = workloads.zone_ring(n_zones=9, walls_per_zone=6, n_nodes=128, nsteps=400)
+    rng = np.random.default_rng(3)
+    init = {k: v + (0.05 * rng.standard_normal(v.size) if k in ("u_prev", "u_curr", "v_prev", "v_curr") else 0)
+            for k, v in w.init.items()}
+    b, rc, fl, _ = _oracle(w.model, init, 400)
+    assert rc == 0
+    peak = max(np.abs(b.state[k]).max() for k in ("u_curr", "v_curr"))
+    w.model.divergence_norm = float(peak) * 0.999      # trips somewhere inside the march
+    b, rc, fl, _ = _oracle(w.model, init, 400)
+    assert rc == api.A.HYG_EDIVERGED
+    with Context(w.model) as ctx:
+        ctx.set_state(**init)
+        ctx.bootstrap("implicit")
+        with pytest.raises(api.NumericalError) as ei:
+            ctx.advance(399)
+    assert ei.value.layer == fl and ei.value.wall == b.fail_wall, (ei.value.layer, fl, ei.value.wall, b.fail_wall)
