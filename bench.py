@@ -49,7 +49,9 @@ CONFIGS = {
                  run_steps=100_000),
     "cfg2": dict(flop=14, bytes=0, bound="fp32", kernel="df_coupled_fused_f32", scaling="weak", dtype="f32",
                  run_steps=100_000),
-    "cfg3": dict(flop=14.1, bytes=48, bound="hbm", kernel="building_step", scaling="strong", dtype="f64",
+    # cfg3 runs K4 (k_ring.cuh): B = 7 zones per CTA, S = 8 steps per launch,
+    # (64 B x 5376 owned + 32 B x 756 halo nodes) / (5376 x 8) = 8.56 B/update
+    "cfg3": dict(flop=14.1, bytes=8.56, bound="hbm", kernel="ring_tiled", scaling="strong", dtype="f64",
                  run_steps=80_000),
     # cfg4 at N=1 runs the temporally blocked K3 (~4.06 B/update at T=1024, S=16),
     # so min(HBM, FP64) is the FP64 side; sharded (N>1) it streams 48 B/update

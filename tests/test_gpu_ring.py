@@ -68,21 +68,22 @@ def test_ring_chain_without_wrap():
 
 
 def test_ring_guard_replay():
-    """A norm the march crosses mid-launch: first failing layer and lowest
-    failing wall exactly as the oracle's check_bounded."""
+    """A norm the forced march crosses mid-run (inside a K4 launch): first
+    failing layer and lowest failing wall exactly as the oracle's
+    check_bounded."""
     w = workloads.zone_ring(n_zones=9, walls_per_zone=6, n_nodes=128, nsteps=400)
-    rng = np.random.default_rng(3)
-    init = {k: v + (0.05 * rng.standard_normal(v.size) if k in ("u_prev", "u_curr", "v_prev", "v_curr") else 0)
-            for k, v in w.init.items()}
-    b, rc, fl, _ = _oracle(w.model, init, 400)
+    b, rc, _, _ = _oracle(w.model, w.init, 400)
     assert rc == 0
     peak = max(np.abs(b.state[k]).max() for k in ("u_curr", "v_curr"))
-    w.model.divergence_norm = float(peak) * 0.999      # trips somewhere inside the march
-    b, rc, fl, _ = _oracle(w.model, init, 400)
-    assert rc == api.A.HYG_EDIVERGED
+    w.model.divergence_norm = 1.0 + 0.5 * (float(peak) - 1.0)   # the outdoor forcing lifts v steadily
+    b, rc, fl, _ = _oracle(w.model, w.init, 400)
+    assert rc == api.A.HYG_EDIVERGED and 20 < fl < 390, fl
     with Context(w.model) as ctx:
-        ctx.set_state(**init)
+        ctx.set_state(**w.init)
         ctx.bootstrap("implicit")
+        ctx.profiling(True)
         with pytest.raises(api.NumericalError) as ei:
             ctx.advance(399)
+        ctx.synchronize()
+        assert any(s["name"] == "ring_tiled" for s in ctx.kernel_stats())
     assert ei.value.layer == fl and ei.value.wall == b.fail_wall, (ei.value.layer, fl, ei.value.wall, b.fail_wall)
