@@ -942,9 +942,9 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
     const int Z = static_cast<int>(c->zones.size()), W = c->ring_W, B = c->ring_B, npt = c->n / 16;
     const int grid = (Z + B - 1) / B;
     const int threads = RingShape<8, kRingS>::threads(B, W);
-    const size_t smem = npt == 4 ? RingShape<4, kRingS>::smem_bytes(B, W)
-                        : npt == 8 ? RingShape<8, kRingS>::smem_bytes(B, W)
-                                   : RingShape<16, kRingS>::smem_bytes(B, W);
+    const size_t smem = npt == 4 ? RingShape<4, kRingS>::smem_bytes(B, W, nch, nsrc)
+                        : npt == 8 ? RingShape<8, kRingS>::smem_bytes(B, W, nch, nsrc)
+                                   : RingShape<16, kRingS>::smem_bytes(B, W, nch, nsrc);
     const int64_t block = 65536 / kRingS * kRingS;
     for (int64_t done = 0; done < nsteps;) {
         const int64_t rows = std::min(block, nsteps - done);
@@ -1295,6 +1295,7 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
                  d->attach[2 * w + 1].index == w / W;
         for (int z = 0; ok && z < Z; ++z) {
             const hyg_zone_desc& zd = d->zones[z];
+            ok = ok && zd.n_walls <= kRingMaxLinks && zd.n_interzone <= kRingMaxPeers;
             for (int i = 0; ok && i < zd.n_walls; ++i)
                 ok = zd.walls[i].face == 1 && zd.walls[i].wall / W == z;
             for (int i = 0; ok && i < zd.n_interzone; ++i) {
@@ -1305,10 +1306,11 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
         if (ok) {
             const int npt = c->n / 16;
             int B = std::min(Z, 32 - 2 * kRingS);
+            const int nch = std::max(1, d->n_channels), nsrc = d->n_zone_sources;
             auto fits = [&](int b) {
-                const size_t sm = npt == 4 ? RingShape<4, kRingS>::smem_bytes(b, W)
-                                  : npt == 8 ? RingShape<8, kRingS>::smem_bytes(b, W)
-                                             : RingShape<16, kRingS>::smem_bytes(b, W);
+                const size_t sm = npt == 4 ? RingShape<4, kRingS>::smem_bytes(b, W, nch, nsrc)
+                                  : npt == 8 ? RingShape<8, kRingS>::smem_bytes(b, W, nch, nsrc)
+                                             : RingShape<16, kRingS>::smem_bytes(b, W, nch, nsrc);
                 const int th = RingShape<8, kRingS>::threads(b, W);
                 return sm <= 227u * 1024u && th <= 896;
             };

@@ -58,32 +58,49 @@ struct RingArgs {
     int seg_index;
 };
 
+// Per local zone, staged in shared memory before the step loop (the zone
+// warp's inputs, folded exactly as zone_update multiplies them):
+//   [0] 1 + kappa_a_tt1, [1] g_v, [2] q_v1, [3] q_v2, [4] #links, [5] #peers,
+//   [6] source index, links [8 + 4q] = (wall in zone, Bi_TT theta_T,
+//   Bi_TM theta_T, sign Bi_M theta_M), peers [40 + 4q] = (local index,
+//   g_inz, q_inz1, q_inz2)
+constexpr int kRingMaxLinks = 8, kRingMaxPeers = 4, kRingZP = 56;
+constexpr int kRingFace = 9;        // face row: e, b, e_g, c_tv, c_sv, c_tu, c_su, c_q, c_g
+
 template <int NPT, int S>
 struct RingShape {
-    static constexpr int kLanes = 16;              // threads per owned wall
-    static constexpr int kPad = NPT + 1;           // padded segment (bank-conflict free)
+    static constexpr int kLanes = 16;              // threads per owned wall (n = 16 NPT)
     static constexpr int kP = S + 1;               // nodes kept per halo wall
     static constexpr int kHaloZones = 2 * (S - 1);
     static constexpr int kLocalZones = 2 * S;      // + B
-    __host__ __device__ static int wall_stride() { return kLanes * kPad; }       // n = 16 NPT
     __host__ __device__ static int owned_walls(int B, int W) { return B * W; }
     __host__ __device__ static int halo_walls(int W) { return kHaloZones * W; }
-    __host__ __device__ static size_t smem_bytes(int B, int W) {
-        const size_t own = static_cast<size_t>(owned_walls(B, W)) * wall_stride();
+    __host__ __device__ static int row_width(int nch, int nsrc) { return 4 * nch + 3 * nsrc + 2; }
+    __host__ __device__ static size_t smem_bytes(int B, int W, int nch, int nsrc) {
+        const size_t n = 16 * NPT;
+        const size_t own = static_cast<size_t>(owned_walls(B, W)) * n;
         const size_t halo = static_cast<size_t>(halo_walls(W)) * kP;
         const size_t zones = static_cast<size_t>(B + kLocalZones);
-        return sizeof(double) * (4 * own + 4 * halo + 4 * zones);
+        return sizeof(double) * (4 * own + 4 * halo + 4 * zones + zones * kRingZP +
+                                 static_cast<size_t>(owned_walls(B, W)) * 2 * kRingFace +
+                                 static_cast<size_t>(S) * row_width(nch, nsrc));
     }
+    // roles are whole warps (bar.sync from two call sites inside one warp is unsafe)
+    __host__ __device__ static int own_threads(int B, int W) { return (owned_walls(B, W) * kLanes + 31) / 32 * 32; }
+    __host__ __device__ static int halo_threads(int W) { return (halo_walls(W) + 31) / 32 * 32; }
     __host__ __device__ static int threads(int B, int W) {
-        const int own = owned_walls(B, W) * kLanes;
-        const int halo = (halo_walls(W) + 31) / 32 * 32;
-        return own + halo + 32;   // + one zone warp (B + 2S <= 32)
+        return own_threads(B, W) + halo_threads(W) + 32;   // + one zone warp (B + 2S <= 32)
     }
 };
 
-// padded position of node j inside an owned wall
+// position of node j inside an owned wall: segments of NPT nodes, the node
+// index XOR-swizzled per segment so the 16 lanes of a wall (one segment each)
+// hit 16 distinct bank pairs
 template <int NPT>
-__device__ __forceinline__ int ring_pos(int j) { return (j / NPT) * (NPT + 1) + (j % NPT); }
+__device__ __forceinline__ int ring_pos(int j) {
+    const int s = j / NPT, q = j % NPT;
+    return s * NPT + (q ^ ((s / (16 / NPT)) & (NPT - 1)));
+}
 
 template <int NPT, int S>
 __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
@@ -92,30 +109,34 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
     if (*a.stop) return;                          // an earlier launch tripped the guard
     const int n = a.n, W = a.W, B = a.B, Z = a.n_zones;
     const int ow = Sh::owned_walls(B, W), hw = Sh::halo_walls(W);
-    const int ws = Sh::wall_stride();
     const int z0 = blockIdx.x * B;
     const int nown = min(B, Z - z0);              // owned zones of this CTA (the last may own fewer)
     const int L = nown + Sh::kLocalZones;         // local zones: i = 0 .. L-1, global z0 - S + i
+    const int LB = B + Sh::kLocalZones;           // allocated local zones
+    const int rw = Sh::row_width(a.n_channels, a.n_sources);
     constexpr int P = Sh::kP;
-    // layout: owned [field u,v][slot 0,1][ow * ws], halo [field][slot][hw * P], zones [field][slot][L]
+    // layout: owned [field u,v][slot 0,1][ow * n], halo [field][slot][hw * P],
+    // zones [field][slot][LB], zone params [LB][kRingZP], face rows [ow][2][9], rows [S][rw]
     double* OWN = smem;
-    double* HAL = OWN + 4 * static_cast<size_t>(ow) * ws;
+    double* HAL = OWN + 4 * static_cast<size_t>(ow) * n;
     double* ZN = HAL + 4 * static_cast<size_t>(hw) * P;
+    double* ZP = ZN + 4 * LB;
+    double* FC = ZP + static_cast<size_t>(LB) * kRingZP;
+    double* RW = FC + static_cast<size_t>(ow) * 2 * kRingFace;
     auto own_at = [&](int f, int slot, int wl, int j) -> double& {
-        return OWN[(static_cast<size_t>(f * 2 + slot) * ow + wl) * ws + ring_pos<NPT>(j)];
+        return OWN[(static_cast<size_t>(f * 2 + slot) * ow + wl) * n + ring_pos<NPT>(j)];
     };
     auto hal_at = [&](int f, int slot, int hl, int p) -> double& {
         return HAL[(static_cast<size_t>(f * 2 + slot) * hw + hl) * P + p];
     };
-    auto zn_at = [&](int f, int slot, int i) -> double& { return ZN[(f * 2 + slot) * L + i]; };
+    auto zn_at = [&](int f, int slot, int i) -> double& { return ZN[(f * 2 + slot) * LB + i]; };
 
     auto gzone = [&](int i) { return ((z0 - S + i) % Z + Z) % Z; };
     const int tid = threadIdx.x, nthr = blockDim.x;
 
     // ---- load: slot 0 = layer k-1 (prev), slot 1 = layer k (curr) --------------------
-    for (int i = tid; i < ow * n; i += nthr) {
+    for (int i = tid; i < nown * W * n; i += nthr) {
         const int wl = i / n, j = i - wl * n;
-        if (wl >= nown * W) continue;
         const size_t g = (static_cast<size_t>(z0) * W + wl) * n + j;
         own_at(0, 0, wl, j) = a.in[0][g];
         own_at(0, 1, wl, j) = a.in[1][g];
@@ -132,28 +153,67 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
         hal_at(1, 0, hl, p) = a.in[2][g];
         hal_at(1, 1, hl, p) = a.in[3][g];
     }
+    for (int i = tid; i < nown * W * 2; i += nthr) {         // face rows of the owned walls
+        const int wl = i / 2, f = i - wl * 2;
+        const RowCoef c = a.coef[z0 * W + wl].face[f];
+        double* d = FC + static_cast<size_t>(i) * kRingFace;
+        d[0] = c.e; d[1] = c.b; d[2] = c.e_g; d[3] = c.c_tv; d[4] = c.c_sv;
+        d[5] = c.c_tu; d[6] = c.c_su; d[7] = c.c_q; d[8] = c.c_g;
+    }
+    for (int i = tid; i < a.steps * rw; i += nthr) {         // forcing rows of this launch
+        const int k = i / rw, r = i - k * rw;
+        RW[i] = r < 4 * a.n_channels
+                    ? reinterpret_cast<const double*>(a.table + static_cast<size_t>(k) * a.n_channels)[r]
+                    : a.src[static_cast<size_t>(k) * (3 * a.n_sources + 2) + (r - 4 * a.n_channels)];
+    }
     for (int i = tid; i < L; i += nthr) {
-        zn_at(0, 1, i) = a.zu_in[gzone(i)];
-        zn_at(1, 1, i) = a.zv_in[gzone(i)];
+        const int z = gzone(i);
+        zn_at(0, 1, i) = a.zu_in[z];
+        zn_at(1, 1, i) = a.zv_in[z];
+        const ZoneDev d = a.zones[z];
+        double* zp = ZP + static_cast<size_t>(i) * kRingZP;
+        zp[0] = 1.0 + d.kappa_a_tt1;
+        zp[1] = d.g_v;
+        zp[2] = d.q_v1;
+        zp[3] = d.q_v2;
+        zp[4] = d.wall_end - d.wall_begin;
+        zp[5] = d.inz_end - d.inz_begin;
+        zp[6] = d.sources;
+        for (int q = 0; q < d.wall_end - d.wall_begin; ++q) {
+            const ZoneLinkDev l = a.links[d.wall_begin + q];
+            zp[8 + 4 * q] = l.wall - z * W;
+            zp[9 + 4 * q] = l.Bi_TT * l.theta_T;
+            zp[10 + 4 * q] = l.Bi_TM * l.theta_T;
+            zp[11 + 4 * q] = d.sign * l.Bi_M * l.theta_M;
+        }
+        for (int q = 0; q < d.inz_end - d.inz_begin; ++q) {
+            const InzLinkDev l = a.inz[d.inz_begin + q];
+            const int pi = i >= 1 && gzone(i - 1) == l.peer ? i - 1 : i + 1;   // the adjacent copy
+            zp[40 + 4 * q] = pi;
+            zp[41 + 4 * q] = l.g_inz;
+            zp[42 + 4 * q] = l.q_inz1;
+            zp[43 + 4 * q] = l.q_inz2;
+        }
     }
     __syncthreads();
 
     // ---- roles -------------------------------------------------------------------------
-    const int own_thr = ow * Sh::kLanes;
-    const int halo_thr = (hw + 31) / 32 * 32;
+    const int own_thr = Sh::own_threads(B, W);
+    const int halo_thr = Sh::halo_threads(W);
     bool bad = false;
     int cur = 1;                                   // slot holding layer k
-    for (int k = 0; k < a.steps; ++k) {
-        const int prv = cur ^ 1;
-        const Ambient* amb = a.table + static_cast<size_t>(k) * a.n_channels;
-        if (tid < own_thr) {
-            // owned wall wl, nodes [s*NPT, s*NPT + NPT)
-            const int wl = tid / Sh::kLanes, s = tid - wl * Sh::kLanes;
-            if (wl < nown * W) {
-                const int w = z0 * W + wl;
-                const int li = S + wl / W;         // local zone of the wall (face 1)
-                const double cb = a.coef[w].in.b, csu = a.coef[w].in.c_su, csv = a.coef[w].in.c_sv;
-                const int j0 = s * NPT;
+    if (tid < own_thr) {
+        // owned wall wl, nodes [s*NPT, s*NPT + NPT)
+        const int wl = tid / Sh::kLanes, s = tid - wl * Sh::kLanes;
+        const bool live = wl < nown * W;            // (the rounding lanes of the last warp idle)
+        const int w = z0 * W + (live ? wl : 0);
+        const int li = S + wl / W;                 // local zone of the wall (face 1)
+        const double cb = a.coef[w].in.b, csu = a.coef[w].in.c_su, csv = a.coef[w].in.c_sv;
+        const int ch = a.attach[2 * w].index;
+        const int j0 = s * NPT;
+        for (int k = 0; k < a.steps; ++k) {
+            const int prv = cur ^ 1;
+            if (live) {
                 double ul = own_at(0, cur, wl, j0 == 0 ? 1 : j0 - 1);
                 double vl = own_at(1, cur, wl, j0 == 0 ? 1 : j0 - 1);
                 double uc = own_at(0, cur, wl, j0), vc = own_at(1, cur, wl, j0);
@@ -170,24 +230,24 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
                         vn = fma(cb, d, vp);
                         un = fma(csv, d, fma(csu, du, up));
                     } else {
-                        // faces: x=0 exterior channel, x=1 the zone's layer-k air
+                        // faces (coupled_node): x=0 the exterior channel, x=1 the zone's layer-k air
                         const int f = j == 0 ? 0 : 1;
-                        const RowCoef c = a.coef[w].face[f];
+                        const double* c = FC + (static_cast<size_t>(wl) * 2 + f) * kRingFace;
                         double u_inf, v_inf, g_inf = 0.0, q_inf = 0.0;
                         if (f == 0) {
-                            const Ambient am = amb[a.attach[2 * w].index];
-                            u_inf = am.u;
-                            v_inf = am.v;
-                            g_inf = am.g;
-                            q_inf = am.q + 0.0;
+                            const double* am = RW + static_cast<size_t>(k) * rw + 4 * ch;
+                            u_inf = am[0];
+                            v_inf = am[1];
+                            g_inf = am[2];
+                            q_inf = am[3] + 0.0;
                         } else {
                             u_inf = zn_at(0, cur, li);
                             v_inf = zn_at(1, cur, li);
                         }
                         const double t = v_inf - vp, tu = u_inf - up;
-                        vn = fma(c.e, t, fma(c.b, d, fma(c.e_g, g_inf, vp)));
-                        un = fma(c.c_tv, t, fma(c.c_sv, d, fma(c.c_tu, tu, fma(c.c_su, du, fma(c.c_q, q_inf,
-                                                                                          fma(c.c_g, g_inf, up))))));
+                        vn = fma(c[0], t, fma(c[1], d, fma(c[2], g_inf, vp)));
+                        un = fma(c[3], t, fma(c[4], d, fma(c[5], tu, fma(c[6], du, fma(c[7], q_inf,
+                                                                                    fma(c[8], g_inf, up))))));
                     }
                     own_at(0, prv, wl, j) = un;    // layer k+1 overwrites layer k-1
                     own_at(1, prv, wl, j) = vn;
@@ -198,16 +258,23 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
                     vc = vr;
                 }
             }
-        } else if (tid < own_thr + halo_thr) {
-            const int hl = tid - own_thr;
-            if (hl < hw) {
-                // halo wall: global nodes n-P .. n-1; the cut end (p = 0) has no
-                // left neighbour — its error moves inward one node per step and
-                // never reaches the face node within S steps
-                const int hz = hl / W, wi = hl - hz * W;
-                const int li = hz < S - 1 ? 1 + hz : S + nown + (hz - (S - 1));
-                const int w = gzone(li) * W + wi;
-                const double cb = a.coef[w].in.b, csu = a.coef[w].in.c_su, csv = a.coef[w].in.c_sv;
+            __syncthreads();
+            cur ^= 1;
+        }
+    } else if (tid < own_thr + halo_thr) {
+        // halo wall: global nodes n-P .. n-1; the cut end (p = 0) has no left
+        // neighbour — its error moves inward one node per step and never
+        // reaches the face node within S steps
+        const int hl = tid - own_thr;
+        const bool live = hl < hw;
+        const int hz = (live ? hl : 0) / W, wi = (live ? hl : 0) - hz * W;
+        const int li = hz < S - 1 ? 1 + hz : S + nown + (hz - (S - 1));
+        const int w = gzone(li) * W + wi;
+        const double cb = a.coef[w].in.b, csu = a.coef[w].in.c_su, csv = a.coef[w].in.c_sv;
+        const RowCoef c = a.coef[w].face[1];
+        for (int k = 0; k < a.steps; ++k) {
+            const int prv = cur ^ 1;
+            if (live) {
                 double ul = hal_at(0, cur, hl, 0), vl = hal_at(1, cur, hl, 0);
                 double uc = ul, vc = vl;
 #pragma unroll
@@ -222,7 +289,6 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
                         vn = fma(cb, d, vp);
                         un = fma(csv, d, fma(csu, du, up));
                     } else {
-                        const RowCoef c = a.coef[w].face[1];
                         const double t = zn_at(1, cur, li) - vp, tu = zn_at(0, cur, li) - up;
                         vn = fma(c.e, t, fma(c.b, d, fma(c.e_g, 0.0, vp)));
                         un = fma(c.c_tv, t, fma(c.c_sv, d, fma(c.c_tu, tu, fma(c.c_su, du, fma(c.c_q, 0.0,
@@ -236,47 +302,48 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
                     vc = vr;
                 }
             }
-        } else {
-            // zone warp: zone_step_explicit (zone.cpp:69-74) of every local zone
-            // that has a layer-k state and samples (i = 1 .. L-2)
-            const int i = tid - own_thr - halo_thr;
-            if (i >= 1 && i < L - 1) {
-                const int z = gzone(i);
-                const ZoneDev d = a.zones[z];
+            __syncthreads();
+            cur ^= 1;
+        }
+    } else {
+        // zone warp: zone_step_explicit (zone.cpp:69-74) of every local zone
+        // with a layer-k state and samples (i = 1 .. L-2), from staged params
+        const int i = tid - own_thr - halo_thr;
+        const bool live = i >= 1 && i < L - 1;
+        const double* zp = ZP + static_cast<size_t>(live ? i : 0) * kRingZP;
+        const bool owned = i >= S && i < S + nown;
+        const int hz = i < S ? i - 1 : (S - 1) + (i - S - nown);
+        for (int k = 0; k < a.steps; ++k) {
+            if (live) {
                 const double u_a = zn_at(0, cur, i), v_a = zn_at(1, cur, i);
-                const double* srow = a.src + static_cast<size_t>(k) * (3 * a.n_sources + 2);
-                const double* sz = srow + 3 * d.sources;
+                const double* srow = RW + static_cast<size_t>(k) * rw + 4 * a.n_channels;
+                const double* sz = srow + 3 * static_cast<int>(zp[6]);
                 const double u_inf = srow[3 * a.n_sources + 0], v_inf = srow[3 * a.n_sources + 1];
-                double du = sz[1] + sz[2] + d.q_v1 * (u_inf * v_inf - u_a * v_a) + d.q_v2 * (u_inf - u_a);
-                double dv = sz[0] + d.g_v * (v_inf - v_a);
-                for (int q = d.inz_begin; q < d.inz_end; ++q) {
-                    const InzLinkDev l = a.inz[q];
-                    const int pi = gzone(i - 1) == l.peer ? i - 1 : i + 1;   // the adjacent copy
+                double du = sz[1] + sz[2] + zp[2] * (u_inf * v_inf - u_a * v_a) + zp[3] * (u_inf - u_a);
+                double dv = sz[0] + zp[1] * (v_inf - v_a);
+                const int npeer = static_cast<int>(zp[5]), nlink = static_cast<int>(zp[4]);
+                for (int q = 0; q < npeer; ++q) {
+                    const int pi = static_cast<int>(zp[40 + 4 * q]);
                     const double pu = zn_at(0, cur, pi), pv = zn_at(1, cur, pi);
-                    du += l.q_inz1 * (pu * pv - u_a * v_a) + l.q_inz2 * (pu - u_a);
-                    dv += l.g_inz * (pv - v_a);
+                    du += zp[42 + 4 * q] * (pu * pv - u_a * v_a) + zp[43 + 4 * q] * (pu - u_a);
+                    dv += zp[41 + 4 * q] * (pv - v_a);
                 }
-                const bool owned = i >= S && i < S + nown;
-                const int hz = i < S ? i - 1 : (S - 1) + (i - S - nown);
-                for (int q = d.wall_begin; q < d.wall_end; ++q) {
-                    const ZoneLinkDev l = a.links[q];
-                    const int wi = l.wall - z * W;
-                    const double us = owned ? own_at(0, cur, (i - S) * W + wi, n - 1)
-                                            : hal_at(0, cur, hz * W + wi, P - 1);
-                    const double vs = owned ? own_at(1, cur, (i - S) * W + wi, n - 1)
-                                            : hal_at(1, cur, hz * W + wi, P - 1);
-                    du += l.Bi_TT * l.theta_T * (us - u_a) + l.Bi_TM * l.theta_T * (vs - v_a);
-                    dv += d.sign * l.Bi_M * l.theta_M * (v_a - vs);
+                for (int q = 0; q < nlink; ++q) {
+                    const int wi = static_cast<int>(zp[8 + 4 * q]);
+                    const double us = owned ? own_at(0, cur, (i - S) * W + wi, n - 1) : hal_at(0, cur, hz * W + wi, P - 1);
+                    const double vs = owned ? own_at(1, cur, (i - S) * W + wi, n - 1) : hal_at(1, cur, hz * W + wi, P - 1);
+                    du += zp[9 + 4 * q] * (us - u_a) + zp[10 + 4 * q] * (vs - v_a);
+                    dv += zp[11 + 4 * q] * (v_a - vs);
                 }
-                const double nu = u_a + a.dt * (du / (1.0 + d.kappa_a_tt1));
+                const double nu = u_a + a.dt * (du / zp[0]);
                 const double nv = v_a + a.dt * dv;
                 zn_at(0, cur ^ 1, i) = nu;
                 zn_at(1, cur ^ 1, i) = nv;
                 if (owned) bad = bad || !isfinite(nu) || !isfinite(nv) || fabs(nu) > a.norm || fabs(nv) > a.norm;
             }
+            __syncthreads();
+            cur ^= 1;
         }
-        __syncthreads();
-        cur ^= 1;
     }
 
     // ---- guard + store: out = (layer k+S-1, layer k+S) ------------------------------------
