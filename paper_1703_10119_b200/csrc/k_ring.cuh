@@ -211,18 +211,31 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
         const double cb = a.coef[w].in.b, csu = a.coef[w].in.c_su, csv = a.coef[w].in.c_sv;
         const int ch = a.attach[2 * w].index;
         const int j0 = s * NPT;
+        // this wall's four shared rows and the swizzled offsets of the thread's nodes
+        double* U[2] = {OWN + (0 * ow + wl) * n, OWN + (1 * ow + wl) * n};
+        double* V[2] = {OWN + (2 * ow + wl) * n, OWN + (3 * ow + wl) * n};
+        const int g = (s / (16 / NPT)) & (NPT - 1);
+        const int base = s * NPT;
+        const int left = j0 == 0 ? ring_pos<NPT>(1) : ring_pos<NPT>(j0 - 1);
+        const int right = j0 + NPT - 1 == n - 1 ? ring_pos<NPT>(n - 2) : ring_pos<NPT>(j0 + NPT);
+        const double* fc0 = FC + (static_cast<size_t>(wl) * 2 + 0) * kRingFace;
+        const double* fc1 = fc0 + kRingFace;
         for (int k = 0; k < a.steps; ++k) {
             const int prv = cur ^ 1;
             if (live) {
-                double ul = own_at(0, cur, wl, j0 == 0 ? 1 : j0 - 1);
-                double vl = own_at(1, cur, wl, j0 == 0 ? 1 : j0 - 1);
-                double uc = own_at(0, cur, wl, j0), vc = own_at(1, cur, wl, j0);
+                const double* uc_ = U[cur];
+                const double* vc_ = V[cur];
+                double* up_ = U[prv];
+                double* vp_ = V[prv];
+                double ul = uc_[left], vl = vc_[left];
+                double uc = uc_[base + (0 ^ g)], vc = vc_[base + (0 ^ g)];
 #pragma unroll
                 for (int q = 0; q < NPT; ++q) {
                     const int j = j0 + q;
-                    const int jr = j == n - 1 ? n - 2 : j + 1;
-                    const double ur = own_at(0, cur, wl, jr), vr = own_at(1, cur, wl, jr);
-                    const double up = own_at(0, prv, wl, j), vp = own_at(1, prv, wl, j);
+                    const int pq = base + (q ^ g);
+                    const int pr = q == NPT - 1 ? right : base + ((q + 1) ^ g);
+                    const double ur = uc_[pr], vr = vc_[pr];
+                    const double up = up_[pq], vp = vp_[pq];
                     const double d = fma(-2.0, vp, vl + vr);
                     const double du = fma(-2.0, up, ul + ur);
                     double vn, un;
@@ -231,10 +244,9 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
                         un = fma(csv, d, fma(csu, du, up));
                     } else {
                         // faces (coupled_node): x=0 the exterior channel, x=1 the zone's layer-k air
-                        const int f = j == 0 ? 0 : 1;
-                        const double* c = FC + (static_cast<size_t>(wl) * 2 + f) * kRingFace;
+                        const double* c = j == 0 ? fc0 : fc1;
                         double u_inf, v_inf, g_inf = 0.0, q_inf = 0.0;
-                        if (f == 0) {
+                        if (j == 0) {
                             const double* am = RW + static_cast<size_t>(k) * rw + 4 * ch;
                             u_inf = am[0];
                             v_inf = am[1];
@@ -249,8 +261,8 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
                         un = fma(c[3], t, fma(c[4], d, fma(c[5], tu, fma(c[6], du, fma(c[7], q_inf,
                                                                                     fma(c[8], g_inf, up))))));
                     }
-                    own_at(0, prv, wl, j) = un;    // layer k+1 overwrites layer k-1
-                    own_at(1, prv, wl, j) = vn;
+                    up_[pq] = un;                   // layer k+1 overwrites layer k-1
+                    vp_[pq] = vn;
                     bad = bad || !(fabs(un) <= a.norm) || !(fabs(vn) <= a.norm);
                     ul = uc;
                     vl = vc;
