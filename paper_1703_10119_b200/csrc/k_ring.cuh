@@ -93,6 +93,15 @@ struct RingShape {
     }
 };
 
+// Ampere-style asynchronous global -> shared copies: every thread issues all
+// of its copies before one wait, so the load phase keeps the whole tile in
+// flight instead of one register round trip per element.
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // position of node j inside an owned wall: segments of NPT nodes, the node
 // index XOR-swizzled per segment so the 16 lanes of a wall (one segment each)
 // hit 16 distinct bank pairs
@@ -138,20 +147,20 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
     for (int i = tid; i < nown * W * n; i += nthr) {
         const int wl = i / n, j = i - wl * n;
         const size_t g = (static_cast<size_t>(z0) * W + wl) * n + j;
-        own_at(0, 0, wl, j) = a.in[0][g];
-        own_at(0, 1, wl, j) = a.in[1][g];
-        own_at(1, 0, wl, j) = a.in[2][g];
-        own_at(1, 1, wl, j) = a.in[3][g];
+        cp_async8(&own_at(0, 0, wl, j), a.in[0] + g);
+        cp_async8(&own_at(0, 1, wl, j), a.in[1] + g);
+        cp_async8(&own_at(1, 0, wl, j), a.in[2] + g);
+        cp_async8(&own_at(1, 1, wl, j), a.in[3] + g);
     }
     for (int i = tid; i < hw * P; i += nthr) {
         const int hl = i / P, p = i - hl * P;
         const int hz = hl / W, wi = hl - hz * W;             // halo zone 0..2(S-1)-1
         const int li = hz < S - 1 ? 1 + hz : S + nown + (hz - (S - 1));   // its local zone index
         const size_t g = (static_cast<size_t>(gzone(li)) * W + wi) * n + (n - P + p);
-        hal_at(0, 0, hl, p) = a.in[0][g];
-        hal_at(0, 1, hl, p) = a.in[1][g];
-        hal_at(1, 0, hl, p) = a.in[2][g];
-        hal_at(1, 1, hl, p) = a.in[3][g];
+        cp_async8(&hal_at(0, 0, hl, p), a.in[0] + g);
+        cp_async8(&hal_at(0, 1, hl, p), a.in[1] + g);
+        cp_async8(&hal_at(1, 0, hl, p), a.in[2] + g);
+        cp_async8(&hal_at(1, 1, hl, p), a.in[3] + g);
     }
     for (int i = tid; i < nown * W * 2; i += nthr) {         // face rows of the owned walls
         const int wl = i / 2, f = i - wl * 2;
@@ -195,6 +204,7 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
             zp[43 + 4 * q] = l.q_inz2;
         }
     }
+    cp_async_wait_all();
     __syncthreads();
 
     // ---- roles -------------------------------------------------------------------------
