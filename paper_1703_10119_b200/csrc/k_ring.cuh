@@ -126,19 +126,16 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
     constexpr int P = Sh::kP;
     // layout: owned [field u,v][slot 0,1][ow * n], halo [field][slot][hw * P],
     // zones [field][slot][LB], zone params [LB][kRingZP], face rows [ow][2][9], rows [S][rw]
-    double* OWN = smem;
-    double* HAL = OWN + 4 * static_cast<size_t>(ow) * n;
-    double* ZN = HAL + 4 * static_cast<size_t>(hw) * P;
-    double* ZP = ZN + 4 * LB;
-    double* FC = ZP + static_cast<size_t>(LB) * kRingZP;
-    double* RW = FC + static_cast<size_t>(ow) * 2 * kRingFace;
-    auto own_at = [&](int f, int slot, int wl, int j) -> double& {
-        return OWN[(static_cast<size_t>(f * 2 + slot) * ow + wl) * n + ring_pos<NPT>(j)];
-    };
-    auto hal_at = [&](int f, int slot, int hl, int p) -> double& {
-        return HAL[(static_cast<size_t>(f * 2 + slot) * hw + hl) * P + p];
-    };
-    auto zn_at = [&](int f, int slot, int i) -> double& { return ZN[(f * 2 + slot) * LB + i]; };
+    // every access is smem[integer offset] (shared-space loads/stores, never generic)
+    const int oOWN = 0;
+    const int oHAL = oOWN + 4 * ow * n;
+    const int oZN = oHAL + 4 * hw * P;
+    const int oZP = oZN + 4 * LB;
+    const int oFC = oZP + LB * kRingZP;
+    const int oRW = oFC + ow * 2 * kRingFace;
+    auto own_ix = [&](int f, int slot, int wl, int j) { return oOWN + ((f * 2 + slot) * ow + wl) * n + ring_pos<NPT>(j); };
+    auto hal_ix = [&](int f, int slot, int hl, int p) { return oHAL + ((f * 2 + slot) * hw + hl) * P + p; };
+    auto zn_ix = [&](int f, int slot, int i) { return oZN + (f * 2 + slot) * LB + i; };
 
     auto gzone = [&](int i) { return ((z0 - S + i) % Z + Z) % Z; };
     const int tid = threadIdx.x, nthr = blockDim.x;
@@ -147,40 +144,40 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
     for (int i = tid; i < nown * W * n; i += nthr) {
         const int wl = i / n, j = i - wl * n;
         const size_t g = (static_cast<size_t>(z0) * W + wl) * n + j;
-        cp_async8(&own_at(0, 0, wl, j), a.in[0] + g);
-        cp_async8(&own_at(0, 1, wl, j), a.in[1] + g);
-        cp_async8(&own_at(1, 0, wl, j), a.in[2] + g);
-        cp_async8(&own_at(1, 1, wl, j), a.in[3] + g);
+        cp_async8(&smem[own_ix(0, 0, wl, j)], a.in[0] + g);
+        cp_async8(&smem[own_ix(0, 1, wl, j)], a.in[1] + g);
+        cp_async8(&smem[own_ix(1, 0, wl, j)], a.in[2] + g);
+        cp_async8(&smem[own_ix(1, 1, wl, j)], a.in[3] + g);
     }
     for (int i = tid; i < hw * P; i += nthr) {
         const int hl = i / P, p = i - hl * P;
         const int hz = hl / W, wi = hl - hz * W;             // halo zone 0..2(S-1)-1
         const int li = hz < S - 1 ? 1 + hz : S + nown + (hz - (S - 1));   // its local zone index
         const size_t g = (static_cast<size_t>(gzone(li)) * W + wi) * n + (n - P + p);
-        cp_async8(&hal_at(0, 0, hl, p), a.in[0] + g);
-        cp_async8(&hal_at(0, 1, hl, p), a.in[1] + g);
-        cp_async8(&hal_at(1, 0, hl, p), a.in[2] + g);
-        cp_async8(&hal_at(1, 1, hl, p), a.in[3] + g);
+        cp_async8(&smem[hal_ix(0, 0, hl, p)], a.in[0] + g);
+        cp_async8(&smem[hal_ix(0, 1, hl, p)], a.in[1] + g);
+        cp_async8(&smem[hal_ix(1, 0, hl, p)], a.in[2] + g);
+        cp_async8(&smem[hal_ix(1, 1, hl, p)], a.in[3] + g);
     }
     for (int i = tid; i < nown * W * 2; i += nthr) {         // face rows of the owned walls
         const int wl = i / 2, f = i - wl * 2;
         const RowCoef c = a.coef[z0 * W + wl].face[f];
-        double* d = FC + static_cast<size_t>(i) * kRingFace;
-        d[0] = c.e; d[1] = c.b; d[2] = c.e_g; d[3] = c.c_tv; d[4] = c.c_sv;
-        d[5] = c.c_tu; d[6] = c.c_su; d[7] = c.c_q; d[8] = c.c_g;
+        const int d = oFC + i * kRingFace;
+        smem[d + 0] = c.e; smem[d + 1] = c.b; smem[d + 2] = c.e_g; smem[d + 3] = c.c_tv; smem[d + 4] = c.c_sv;
+        smem[d + 5] = c.c_tu; smem[d + 6] = c.c_su; smem[d + 7] = c.c_q; smem[d + 8] = c.c_g;
     }
     for (int i = tid; i < a.steps * rw; i += nthr) {         // forcing rows of this launch
         const int k = i / rw, r = i - k * rw;
-        RW[i] = r < 4 * a.n_channels
+        smem[oRW + i] = r < 4 * a.n_channels
                     ? reinterpret_cast<const double*>(a.table + static_cast<size_t>(k) * a.n_channels)[r]
                     : a.src[static_cast<size_t>(k) * (3 * a.n_sources + 2) + (r - 4 * a.n_channels)];
     }
     for (int i = tid; i < L; i += nthr) {
         const int z = gzone(i);
-        zn_at(0, 1, i) = a.zu_in[z];
-        zn_at(1, 1, i) = a.zv_in[z];
+        smem[zn_ix(0, 1, i)] = a.zu_in[z];
+        smem[zn_ix(1, 1, i)] = a.zv_in[z];
         const ZoneDev d = a.zones[z];
-        double* zp = ZP + static_cast<size_t>(i) * kRingZP;
+        double* zp = &smem[oZP + i * kRingZP];
         zp[0] = 1.0 + d.kappa_a_tt1;
         zp[1] = d.g_v;
         zp[2] = d.q_v1;
@@ -222,30 +219,27 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
         const int ch = a.attach[2 * w].index;
         const int j0 = s * NPT;
         // this wall's four shared rows and the swizzled offsets of the thread's nodes
-        double* U[2] = {OWN + (0 * ow + wl) * n, OWN + (1 * ow + wl) * n};
-        double* V[2] = {OWN + (2 * ow + wl) * n, OWN + (3 * ow + wl) * n};
+        const int U0 = oOWN + (0 * ow + wl) * n, U1 = oOWN + (1 * ow + wl) * n;
+        const int V0 = oOWN + (2 * ow + wl) * n, V1 = oOWN + (3 * ow + wl) * n;
         const int g = (s / (16 / NPT)) & (NPT - 1);
         const int base = s * NPT;
         const int left = j0 == 0 ? ring_pos<NPT>(1) : ring_pos<NPT>(j0 - 1);
         const int right = j0 + NPT - 1 == n - 1 ? ring_pos<NPT>(n - 2) : ring_pos<NPT>(j0 + NPT);
-        const double* fc0 = FC + (static_cast<size_t>(wl) * 2 + 0) * kRingFace;
-        const double* fc1 = fc0 + kRingFace;
+        const int fc0 = oFC + (wl * 2 + 0) * kRingFace, fc1 = fc0 + kRingFace;
         for (int k = 0; k < a.steps; ++k) {
             const int prv = cur ^ 1;
             if (live) {
-                const double* uc_ = U[cur];
-                const double* vc_ = V[cur];
-                double* up_ = U[prv];
-                double* vp_ = V[prv];
-                double ul = uc_[left], vl = vc_[left];
-                double uc = uc_[base + (0 ^ g)], vc = vc_[base + (0 ^ g)];
+                const int uc_ = cur ? U1 : U0, vc_ = cur ? V1 : V0;
+                const int up_ = cur ? U0 : U1, vp_ = cur ? V0 : V1;
+                double ul = smem[uc_ + left], vl = smem[vc_ + left];
+                double uc = smem[uc_ + base + (0 ^ g)], vc = smem[vc_ + base + (0 ^ g)];
 #pragma unroll
                 for (int q = 0; q < NPT; ++q) {
                     const int j = j0 + q;
                     const int pq = base + (q ^ g);
                     const int pr = q == NPT - 1 ? right : base + ((q + 1) ^ g);
-                    const double ur = uc_[pr], vr = vc_[pr];
-                    const double up = up_[pq], vp = vp_[pq];
+                    const double ur = smem[uc_ + pr], vr = smem[vc_ + pr];
+                    const double up = smem[up_ + pq], vp = smem[vp_ + pq];
                     const double d = fma(-2.0, vp, vl + vr);
                     const double du = fma(-2.0, up, ul + ur);
                     double vn, un;
@@ -254,25 +248,25 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
                         un = fma(csv, d, fma(csu, du, up));
                     } else {
                         // faces (coupled_node): x=0 the exterior channel, x=1 the zone's layer-k air
-                        const double* c = j == 0 ? fc0 : fc1;
+                        const int c = j == 0 ? fc0 : fc1;
                         double u_inf, v_inf, g_inf = 0.0, q_inf = 0.0;
                         if (j == 0) {
-                            const double* am = RW + static_cast<size_t>(k) * rw + 4 * ch;
-                            u_inf = am[0];
-                            v_inf = am[1];
-                            g_inf = am[2];
-                            q_inf = am[3] + 0.0;
+                            const int am = oRW + k * rw + 4 * ch;
+                            u_inf = smem[am + 0];
+                            v_inf = smem[am + 1];
+                            g_inf = smem[am + 2];
+                            q_inf = smem[am + 3] + 0.0;
                         } else {
-                            u_inf = zn_at(0, cur, li);
-                            v_inf = zn_at(1, cur, li);
+                            u_inf = smem[zn_ix(0, cur, li)];
+                            v_inf = smem[zn_ix(1, cur, li)];
                         }
                         const double t = v_inf - vp, tu = u_inf - up;
-                        vn = fma(c[0], t, fma(c[1], d, fma(c[2], g_inf, vp)));
-                        un = fma(c[3], t, fma(c[4], d, fma(c[5], tu, fma(c[6], du, fma(c[7], q_inf,
-                                                                                    fma(c[8], g_inf, up))))));
+                        vn = fma(smem[c + 0], t, fma(smem[c + 1], d, fma(smem[c + 2], g_inf, vp)));
+                        un = fma(smem[c + 3], t, fma(smem[c + 4], d, fma(smem[c + 5], tu, fma(smem[c + 6], du,
+                                 fma(smem[c + 7], q_inf, fma(smem[c + 8], g_inf, up))))));
                     }
-                    up_[pq] = un;                   // layer k+1 overwrites layer k-1
-                    vp_[pq] = vn;
+                    smem[up_ + pq] = un;            // layer k+1 overwrites layer k-1
+                    smem[vp_ + pq] = vn;
                     bad = bad || !(fabs(un) <= a.norm) || !(fabs(vn) <= a.norm);
                     ul = uc;
                     vl = vc;
@@ -297,13 +291,15 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
         for (int k = 0; k < a.steps; ++k) {
             const int prv = cur ^ 1;
             if (live) {
-                double ul = hal_at(0, cur, hl, 0), vl = hal_at(1, cur, hl, 0);
+                const int hu = hal_ix(0, cur, hl, 0), hv = hal_ix(1, cur, hl, 0);
+                const int hpu = hal_ix(0, prv, hl, 0), hpv = hal_ix(1, prv, hl, 0);
+                double ul = smem[hu], vl = smem[hv];
                 double uc = ul, vc = vl;
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
                     const int pr = p == P - 1 ? P - 2 : p + 1;
-                    const double ur = hal_at(0, cur, hl, pr), vr = hal_at(1, cur, hl, pr);
-                    const double up = hal_at(0, prv, hl, p), vp = hal_at(1, prv, hl, p);
+                    const double ur = smem[hu + pr], vr = smem[hv + pr];
+                    const double up = smem[hpu + p], vp = smem[hpv + p];
                     const double d = fma(-2.0, vp, vl + vr);
                     const double du = fma(-2.0, up, ul + ur);
                     double vn, un;
@@ -311,13 +307,13 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
                         vn = fma(cb, d, vp);
                         un = fma(csv, d, fma(csu, du, up));
                     } else {
-                        const double t = zn_at(1, cur, li) - vp, tu = zn_at(0, cur, li) - up;
+                        const double t = smem[zn_ix(1, cur, li)] - vp, tu = smem[zn_ix(0, cur, li)] - up;
                         vn = fma(c.e, t, fma(c.b, d, fma(c.e_g, 0.0, vp)));
                         un = fma(c.c_tv, t, fma(c.c_sv, d, fma(c.c_tu, tu, fma(c.c_su, du, fma(c.c_q, 0.0,
                                                                                           fma(c.c_g, 0.0, up))))));
                     }
-                    hal_at(0, prv, hl, p) = un;
-                    hal_at(1, prv, hl, p) = vn;
+                    smem[hpu + p] = un;
+                    smem[hpv + p] = vn;
                     ul = uc;
                     vl = vc;
                     uc = ur;
@@ -332,35 +328,37 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
         // with a layer-k state and samples (i = 1 .. L-2), from staged params
         const int i = tid - own_thr - halo_thr;
         const bool live = i >= 1 && i < L - 1;
-        const double* zp = ZP + static_cast<size_t>(live ? i : 0) * kRingZP;
+        const int zp = oZP + (live ? i : 0) * kRingZP;
         const bool owned = i >= S && i < S + nown;
         const int hz = i < S ? i - 1 : (S - 1) + (i - S - nown);
         for (int k = 0; k < a.steps; ++k) {
             if (live) {
-                const double u_a = zn_at(0, cur, i), v_a = zn_at(1, cur, i);
-                const double* srow = RW + static_cast<size_t>(k) * rw + 4 * a.n_channels;
-                const double* sz = srow + 3 * static_cast<int>(zp[6]);
-                const double u_inf = srow[3 * a.n_sources + 0], v_inf = srow[3 * a.n_sources + 1];
-                double du = sz[1] + sz[2] + zp[2] * (u_inf * v_inf - u_a * v_a) + zp[3] * (u_inf - u_a);
-                double dv = sz[0] + zp[1] * (v_inf - v_a);
-                const int npeer = static_cast<int>(zp[5]), nlink = static_cast<int>(zp[4]);
+                const double u_a = smem[zn_ix(0, cur, i)], v_a = smem[zn_ix(1, cur, i)];
+                const int srow = oRW + k * rw + 4 * a.n_channels;
+                const int sz = srow + 3 * static_cast<int>(smem[zp + 6]);
+                const double u_inf = smem[srow + 3 * a.n_sources + 0], v_inf = smem[srow + 3 * a.n_sources + 1];
+                double du = smem[sz + 1] + smem[sz + 2] + smem[zp + 2] * (u_inf * v_inf - u_a * v_a) +
+                            smem[zp + 3] * (u_inf - u_a);
+                double dv = smem[sz + 0] + smem[zp + 1] * (v_inf - v_a);
+                const int npeer = static_cast<int>(smem[zp + 5]), nlink = static_cast<int>(smem[zp + 4]);
                 for (int q = 0; q < npeer; ++q) {
-                    const int pi = static_cast<int>(zp[40 + 4 * q]);
-                    const double pu = zn_at(0, cur, pi), pv = zn_at(1, cur, pi);
-                    du += zp[42 + 4 * q] * (pu * pv - u_a * v_a) + zp[43 + 4 * q] * (pu - u_a);
-                    dv += zp[41 + 4 * q] * (pv - v_a);
+                    const int pi = static_cast<int>(smem[zp + 40 + 4 * q]);
+                    const double pu = smem[zn_ix(0, cur, pi)], pv = smem[zn_ix(1, cur, pi)];
+                    du += smem[zp + 42 + 4 * q] * (pu * pv - u_a * v_a) + smem[zp + 43 + 4 * q] * (pu - u_a);
+                    dv += smem[zp + 41 + 4 * q] * (pv - v_a);
                 }
                 for (int q = 0; q < nlink; ++q) {
-                    const int wi = static_cast<int>(zp[8 + 4 * q]);
-                    const double us = owned ? own_at(0, cur, (i - S) * W + wi, n - 1) : hal_at(0, cur, hz * W + wi, P - 1);
-                    const double vs = owned ? own_at(1, cur, (i - S) * W + wi, n - 1) : hal_at(1, cur, hz * W + wi, P - 1);
-                    du += zp[9 + 4 * q] * (us - u_a) + zp[10 + 4 * q] * (vs - v_a);
-                    dv += zp[11 + 4 * q] * (v_a - vs);
+                    const int wi = static_cast<int>(smem[zp + 8 + 4 * q]);
+                    const int iu = owned ? own_ix(0, cur, (i - S) * W + wi, n - 1) : hal_ix(0, cur, hz * W + wi, P - 1);
+                    const int iv = owned ? own_ix(1, cur, (i - S) * W + wi, n - 1) : hal_ix(1, cur, hz * W + wi, P - 1);
+                    const double us = smem[iu], vs = smem[iv];
+                    du += smem[zp + 9 + 4 * q] * (us - u_a) + smem[zp + 10 + 4 * q] * (vs - v_a);
+                    dv += smem[zp + 11 + 4 * q] * (v_a - vs);
                 }
-                const double nu = u_a + a.dt * (du / zp[0]);
+                const double nu = u_a + a.dt * (du / smem[zp + 0]);
                 const double nv = v_a + a.dt * dv;
-                zn_at(0, cur ^ 1, i) = nu;
-                zn_at(1, cur ^ 1, i) = nv;
+                smem[zn_ix(0, cur ^ 1, i)] = nu;
+                smem[zn_ix(1, cur ^ 1, i)] = nv;
                 if (owned) bad = bad || !isfinite(nu) || !isfinite(nv) || fabs(nu) > a.norm || fabs(nv) > a.norm;
             }
             __syncthreads();
@@ -377,14 +375,14 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
     for (int i = tid; i < nown * W * n; i += nthr) {
         const int wl = i / n, j = i - wl * n;
         const size_t g = (static_cast<size_t>(z0) * W + wl) * n + j;
-        a.out[0][g] = own_at(0, prv, wl, j);
-        a.out[1][g] = own_at(0, cur, wl, j);
-        a.out[2][g] = own_at(1, prv, wl, j);
-        a.out[3][g] = own_at(1, cur, wl, j);
+        a.out[0][g] = smem[own_ix(0, prv, wl, j)];
+        a.out[1][g] = smem[own_ix(0, cur, wl, j)];
+        a.out[2][g] = smem[own_ix(1, prv, wl, j)];
+        a.out[3][g] = smem[own_ix(1, cur, wl, j)];
     }
     for (int i = tid; i < nown; i += nthr) {
-        a.zu_out[z0 + i] = zn_at(0, cur, S + i);
-        a.zv_out[z0 + i] = zn_at(1, cur, S + i);
+        a.zu_out[z0 + i] = smem[zn_ix(0, cur, S + i)];
+        a.zv_out[z0 + i] = smem[zn_ix(1, cur, S + i)];
     }
 }
 
