@@ -227,7 +227,6 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
         const int right = j0 + NPT - 1 == n - 1 ? ring_pos<NPT>(n - 2) : ring_pos<NPT>(j0 + NPT);
         const int fc0 = oFC + (wl * 2 + 0) * kRingFace, fc1 = fc0 + kRingFace;
         for (int k = 0; k < a.steps; ++k) {
-            const int prv = cur ^ 1;
             if (live) {
                 const int uc_ = cur ? U1 : U0, vc_ = cur ? V1 : V0;
                 const int up_ = cur ? U0 : U1, vp_ = cur ? V0 : V1;
