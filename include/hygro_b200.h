@@ -267,6 +267,21 @@ typedef void (*hyg_frame_fn)(void* user, int64_t layer, double t_star, hyg_ctx* 
 int hyg_run(hyg_ctx* ctx, double horizon, double cadence, int32_t boot_kind,
             hyg_frame_fn frame, void* user, hyg_status* status);
 
+/* run() for each of the reference's schemes (Scheme wall.hpp:62, building.cpp:303-356):
+ * DF (implicit start + DF steps), EulerImplicit (step_implicit every step, the
+ * paper's comparison baseline) and EulerExplicit (step_explicit with
+ * euler_explicit_step walls).  `report` (may be NULL) receives
+ * SimulationResult's counters. */
+enum { HYG_SCHEME_DF = 0, HYG_SCHEME_EULER_IMPLICIT = 1, HYG_SCHEME_EULER_EXPLICIT = 2 };
+typedef struct {
+    int64_t steps;
+    int32_t bootstrap_subiters;
+    int32_t max_subiters_seen;
+    double mean_subiters;
+} hyg_run_report;   /* SimulationResult building.hpp:86-93 */
+int hyg_run_scheme(hyg_ctx* ctx, int32_t scheme, double horizon, double cadence, hyg_frame_fn frame,
+                   void* user, hyg_run_report* report, hyg_status* status);
+
 
 /* ---- host-side setup: dimensionless groups (scaling.cpp, materials.cpp) -
  * Coefficient sets are {c_M, k_M, c_TT, k_TT, c_TM, k_TM} (CoefficientSet,

@@ -160,13 +160,11 @@ inline void on_frame(void* user, int64_t, double t, hyg_ctx* ctx) {
 }
 }  // namespace detail
 
-// Drop-in for hygro::run (building.cpp:303-356), DF scheme, on the device.
+// Drop-in for hygro::run (building.cpp:303-356) on the device, all three schemes.
 inline SimulationResult run(const BuildingModel& m, double cadence, SimulationResult* partial = nullptr,
                             int device = 0) {
     m.validate();
     const auto t_start = std::chrono::steady_clock::now();
-    if (m.scheme != Scheme::DufortFrankel)
-        throw std::invalid_argument("hygro::gpu::run: only the DF scheme runs on the device");
     if (m.walls.empty()) throw std::invalid_argument("hygro::gpu::run: no walls");
     const int nw = static_cast<int>(m.walls.size());
     const int nz = static_cast<int>(m.zones.size());
@@ -315,17 +313,23 @@ inline SimulationResult run(const BuildingModel& m, double cadence, SimulationRe
 
     SimulationResult result;
     detail::Frames fr{&result, nw, n, nz};
-    rc = hyg_run(ctx, m.horizon, cadence, HYG_BOOT_IMPLICIT, &detail::on_frame, &fr, &st);
+    const int32_t scheme = m.scheme == Scheme::EulerImplicit   ? HYG_SCHEME_EULER_IMPLICIT
+                           : m.scheme == Scheme::EulerExplicit ? HYG_SCHEME_EULER_EXPLICIT
+                                                               : HYG_SCHEME_DF;
+    hyg_run_report rep{};
+    rc = hyg_run_scheme(ctx, scheme, m.horizon, cadence, &detail::on_frame, &fr, &rep, &st);
     result.wall_clock_s =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
     if (rc) {
-        result.steps = st.layer > 0 ? st.layer : 0;
+        result.steps = rep.steps;
         const double t_fail = st.layer >= 0 && st.layer < static_cast<int64_t>(L) ? times[st.layer] : st.t_star;
         if (partial) *partial = std::move(result);
         detail::rethrow(rc, st, t_fail);
     }
-    result.steps = nsteps;
-    result.bootstrap_subiters = nsteps > 0 ? st.subiterations : 0;
+    result.steps = rep.steps;
+    result.bootstrap_subiters = rep.bootstrap_subiters;
+    result.max_subiters_seen = rep.max_subiters_seen;
+    result.mean_subiters = rep.mean_subiters;
     return result;
 }
 

@@ -120,5 +120,11 @@ int main(int argc, char** argv) {
     // when the underlying values agree to 1e-14
     if (!(rel <= 1e-10)) ++bad;
     if (cpu.frames.size() != gpu.frames.size() || cpu.bootstrap_subiters != gpu.bootstrap_subiters) ++bad;
+    // SimulationResult counters of the implicit scheme (building.cpp:327-352)
+    std::printf("  steps %ld/%ld, mean subiters %.6f/%.6f, max subiters %d/%d\n", cpu.steps, gpu.steps,
+                cpu.mean_subiters, gpu.mean_subiters, cpu.max_subiters_seen, gpu.max_subiters_seen);
+    if (cpu.steps != gpu.steps || cpu.max_subiters_seen != gpu.max_subiters_seen ||
+        cpu.mean_subiters != gpu.mean_subiters)
+        ++bad;
     return bad ? 1 : 0;
 }

@@ -15,6 +15,7 @@ HYG_MOISTURE_AS_PRINTED, HYG_MOISTURE_FLUX_CONSISTENT = 0, 1
 HYG_COEFF_CONSTANT, HYG_COEFF_ANALYTIC_D, HYG_COEFF_MATERIAL = 0, 1, 2
 HYG_F64, HYG_F32 = 0, 1
 HYG_BOOT_IMPLICIT, HYG_BOOT_EXPLICIT = 0, 1
+HYG_SCHEME_DF, HYG_SCHEME_EULER_IMPLICIT, HYG_SCHEME_EULER_EXPLICIT = 0, 1, 2
 
 dp = C.POINTER(C.c_double)
 
@@ -100,6 +101,11 @@ class Status(C.Structure):
                 ("node", C.c_int32), ("half", C.c_int32), ("message", C.c_char * 256)]
 
 
+class RunReport(C.Structure):
+    _fields_ = [("steps", C.c_int64), ("bootstrap_subiters", C.c_int32), ("max_subiters_seen", C.c_int32),
+                ("mean_subiters", C.c_double)]
+
+
 FRAME_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_double, C.c_void_p)
 REDUCE_FN = C.CFUNCTYPE(C.c_double, C.c_void_p, C.c_double)
 
@@ -124,6 +130,8 @@ PROTOTYPES = {
     "hyg_bootstrap": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Status)]),
     "hyg_advance": (C.c_int, [C.c_void_p, C.c_int64, C.c_double, C.POINTER(Status)]),
     "hyg_run": (C.c_int, [C.c_void_p, C.c_double, C.c_double, C.c_int32, FRAME_FN, C.c_void_p, C.POINTER(Status)]),
+    "hyg_run_scheme": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, C.c_double, FRAME_FN, C.c_void_p,
+                                 C.POINTER(RunReport), C.POINTER(Status)]),
     "hyg_synchronize": (C.c_int, [C.c_void_p]),
     "hyg_host_register": (C.c_int, [C.c_void_p, C.c_size_t]),
     "hyg_host_unregister": (C.c_int, [C.c_void_p]),

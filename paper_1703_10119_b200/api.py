@@ -396,6 +396,19 @@ class Context:
         _check(self.lib.hyg_run(self.h, float(horizon), float(cadence), k, cb, None, C.byref(st)), st, "hyg_run")
         return st
 
+    SCHEMES = {"df": A.HYG_SCHEME_DF, "euler-implicit": A.HYG_SCHEME_EULER_IMPLICIT,
+               "euler-explicit": A.HYG_SCHEME_EULER_EXPLICIT}
+
+    def run_scheme(self, scheme: str, horizon: float, cadence: float = 1e30,
+                   frame: Optional[Callable[[int, float, "Context"], None]] = None) -> A.RunReport:
+        """run() (building.cpp:303-356) with Scheme df | euler-implicit | euler-explicit;
+        returns SimulationResult's counters (steps, bootstrap/mean/max subiterations)."""
+        st, rep = A.Status(), A.RunReport()
+        cb = A.FRAME_FN((lambda u, layer, t, h: frame(layer, t, self)) if frame else (lambda *a: None))
+        _check(self.lib.hyg_run_scheme(self.h, self.SCHEMES[scheme], float(horizon), float(cadence), cb, None,
+                                       C.byref(rep), C.byref(st)), st, "hyg_run_scheme")
+        return rep
+
     # -- measurement -------------------------------------------------------------------
     def synchronize(self):
         _check(self.lib.hyg_synchronize(self.h))

@@ -1891,6 +1891,71 @@ int hyg_run(hyg_ctx* c, double horizon, double cadence, int32_t boot_kind, hyg_f
     return HYG_OK;
 }
 
+int hyg_run_scheme(hyg_ctx* c, int32_t scheme, double horizon, double cadence, hyg_frame_fn frame, void* user,
+                   hyg_run_report* report, hyg_status* status) {
+    clear_status(status);
+    if (!c) return HYG_EINVAL;
+    if (report) *report = hyg_run_report{0, 0, 0, 0.0};
+    if (scheme != HYG_SCHEME_DF && scheme != HYG_SCHEME_EULER_IMPLICIT && scheme != HYG_SCHEME_EULER_EXPLICIT) {
+        set_status(status, HYG_EINVAL, "unknown scheme");
+        return HYG_EINVAL;
+    }
+    if (!(horizon >= 0.0)) {   // validate building.cpp:13
+        set_status(status, HYG_ESCHEMA, "horizon must be non-negative");
+        return HYG_ESCHEMA;
+    }
+    const int64_t nsteps = std::llround(horizon / c->dt);
+    const double strides = cadence / c->dt;
+    const int64_t stride = !(strides < 4.0e18) ? nsteps + 1 : std::max<int64_t>(1, std::llround(strides));
+    if (frame) frame(user, c->layer, c->t, c);
+    int64_t done = 0;
+    int64_t subiter_sum = 0;
+    int max_seen = 0, boot = 0;
+    const int64_t layer0 = c->layer;
+    auto finish = [&](int rc) {
+        // SimulationResult::steps counts the steps completed before a failure
+        // (building.cpp:339-341): the failing step (output layer st.layer) is not
+        if (rc != HYG_OK && status && status->layer > layer0) done = status->layer - 1 - layer0;
+        if (report) {
+            report->steps = done;
+            report->bootstrap_subiters = boot;
+            report->max_subiters_seen = max_seen;
+            const int64_t counted = scheme == HYG_SCHEME_DF ? std::max<int64_t>(done - 1, 0) : done;
+            report->mean_subiters = counted > 0 ? static_cast<double>(subiter_sum) / counted : 0.0;
+        }
+        return rc;
+    };
+    if (scheme == HYG_SCHEME_DF && nsteps > 0) {     // DF: implicit start counted as step 1
+        const int rc = hyg_bootstrap(c, HYG_BOOT_IMPLICIT, status);
+        if (rc) return finish(rc);
+        boot = status ? status->subiterations : 0;
+        ++done;
+        if (frame && (done % stride == 0 || done == nsteps)) frame(user, c->layer, c->t, c);
+    }
+    while (done < nsteps) {
+        if (scheme == HYG_SCHEME_DF) {
+            const int64_t chunk = std::min(stride - done % stride, nsteps - done);
+            const int rc = hyg_advance(c, chunk, c->dt, status);
+            if (rc) return finish(rc);
+            done += chunk;              // DF steps report 0 subiterations
+        } else {
+            // step_implicit / step_explicit(EulerExplicit) per step (building.cpp:327-331),
+            // each guarded like the DF steps
+            hyg_status st{};
+            const int rc = hyg_bootstrap(c, scheme == HYG_SCHEME_EULER_IMPLICIT ? HYG_BOOT_IMPLICIT
+                                                                                : HYG_BOOT_EXPLICIT, &st);
+            if (status) *status = st;
+            if (rc) return finish(rc);
+            subiter_sum += st.subiterations;
+            max_seen = std::max(max_seen, static_cast<int>(st.subiterations));
+            ++done;
+        }
+        if (frame && (done % stride == 0 || done == nsteps)) frame(user, c->layer, c->t, c);
+    }
+    if (status) status->subiterations = boot;
+    return finish(HYG_OK);
+}
+
 int hyg_synchronize(hyg_ctx* c) {
     if (!c) return HYG_EINVAL;
     cudaSetDevice(c->device);
