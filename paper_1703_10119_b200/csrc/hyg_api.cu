@@ -194,6 +194,7 @@ struct hyg_ctx {
     int* d_wall_kind = nullptr;
     mat::Set* d_ref = nullptr;       // reference sets of material walls
     double* d_star = nullptr;        // StarTables scratch [9][cells] (allocated on first use)
+    double* d_impl = nullptr;        // implicit start scratch (allocated on first use)
     unsigned long long* d_dom = nullptr;
     bool has_rad = false;
     bool ring = false;               // K4: zone-ring temporal blocking applies
@@ -1449,6 +1450,7 @@ void hyg_destroy(hyg_ctx* c) {
     cudaFree(c->d_wall_kind);
     cudaFree(c->d_ref);
     cudaFree(c->d_star);
+    cudaFree(c->d_impl);
     for (void* q : {static_cast<void*>(c->d_rad_tgt), static_cast<void*>(c->d_rad_grp),
                     static_cast<void*>(c->d_rad_num), static_cast<void*>(c->d_rad_den),
                     static_cast<void*>(c->d_rad_coef), static_cast<void*>(c->d_qrad),
@@ -1728,9 +1730,15 @@ int hyg_bootstrap(hyg_ctx* c, int32_t kind, hyg_status* status) {
         double* scr = nullptr;
         double* zit = nullptr;         // zone iterates: [4][nz] = (u,v) x (snapshot, new)
         unsigned long long* d_diff = nullptr;
-        HYG_CUDA(cudaMallocAsync(&scr, sizeof(double) * 5 * cells, c->stream));
-        HYG_CUDA(cudaMallocAsync(&zit, sizeof(double) * 4 * nz, c->stream));
-        HYG_CUDA(cudaMallocAsync(&d_diff, sizeof(unsigned long long), c->stream));
+        // scratch kept for the context's lifetime: a stream-ordered free hands the
+        // pages back to the driver and the next start would map them again
+        if (!c->d_impl) {
+            HYG_CUDA(cudaMalloc(&c->d_impl, sizeof(double) * (5 * cells + 4 * static_cast<size_t>(nz)) +
+                                                sizeof(unsigned long long)));
+        }
+        scr = c->d_impl;
+        zit = c->d_impl + 5 * cells;
+        d_diff = reinterpret_cast<unsigned long long*>(zit + 4 * nz);
         // iterates start from layer n (building.cpp:200-206)
         HYG_CUDA(cudaMemcpyAsync(a.out[1], a.in[1], cells * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
         HYG_CUDA(cudaMemcpyAsync(a.out[3], a.in[3], cells * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
@@ -1811,9 +1819,6 @@ int hyg_bootstrap(hyg_ctx* c, int32_t kind, hyg_status* status) {
                                      cudaMemcpyDeviceToDevice, c->stream));
             c->zcur ^= 1;
         }
-        HYG_CUDA(cudaFreeAsync(scr, c->stream));
-        HYG_CUDA(cudaFreeAsync(zit, c->stream));
-        HYG_CUDA(cudaFreeAsync(d_diff, c->stream));
         if (rcl != HYG_OK) {
             HYG_CUDA(cudaStreamSynchronize(c->stream));
             if (status) {
