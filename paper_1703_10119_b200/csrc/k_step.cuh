@@ -55,7 +55,7 @@ struct StepArgs {
     const int* wall_kind;       // [n_walls] kCoeff* of each wall (per-wall CoefficientModel)
     StarTab star;               // nonlinear walls: tables of this layer (node == nullptr: none)
     const double* q_rad;        // [2*n_walls] zone radiation flux per face (nullable)
-    const unsigned long long* dom_key;   // set by this step's k_star_tables on a domain error
+    const unsigned long long* dom_key;   // domain-error key of the material kernels
 };
 
 // A failure raised by an EARLIER step (key layer <= this step's input layer)
@@ -183,53 +183,6 @@ __device__ __forceinline__ void analytic_node(const StepArgs& a, int w, int j, c
          (ctt + b_ * (ktp_b + kt_b) + cplu);
 }
 
-// df_step_nonlinear (wall.cpp:196-264) with all six starred coefficients
-// read from the layer's tables (material walls), literal form.
-__device__ __forceinline__ void table_node(const StepArgs& a, int w, int j, const NodeIn& x, double& un,
-                                           double& vn) {
-    const int n = a.n;
-    const double dx = a.dx, dt = a.dt;
-    const Groups p = a.groups[w];
-    const double ad = p.Fo_M * dt / (dx * dx);
-    const double b_ = p.Fo_TT * dt / (dx * dx);
-    const double g_ = p.Fo_TM * p.gamma * dt / (dx * dx);
-    const double ratio = p.Fo_TT != 0.0 ? p.Fo_TM * p.gamma / p.Fo_TT : 0.0;
-    const StarTab& s = a.star;
-    const int64_t c = static_cast<int64_t>(w) * n + j;
-    if (j > 0 && j < n - 1) {
-        const double kp = s.hf(kHk_M, c), km = s.hf(kHk_M, c - 1), cm = s.nd(kSc_M, c);
-        vn = ((cm - ad * (kp + km)) * x.vp + 2.0 * ad * (kp * x.vr + km * x.vl)) / (cm + ad * (kp + km));
-        const double ktp = s.hf(kHk_TT, c), ktm = s.hf(kHk_TT, c - 1);
-        const double kmp = s.hf(kHk_TM, c), kmm = s.hf(kHk_TM, c - 1);
-        const double ctt = s.nd(kSc_TT, c), ctm = s.nd(kSc_TM, c);
-        un = ((ctt - b_ * (ktp + ktm)) * x.up - p.gamma * ctm * (vn - x.vp) +
-              2.0 * b_ * (ktp * x.ur + ktm * x.ul) + 2.0 * g_ * (kmp * x.vr + kmm * x.vl) -
-              g_ * (kmp + kmm) * (vn + x.vp)) /
-             (ctt + b_ * (ktp + ktm));
-        return;
-    }
-    const int k = j == 0 ? 0 : 1;
-    const double vcn = j == 0 ? x.vr : x.vl, ucn = j == 0 ? x.ur : x.ul;   // vc[jn], uc[jn]
-    const int64_t ch = j == 0 ? c : c - 1;                                  // half_front / half_back
-    const FaceVals b = resolve(a, w, k);
-    const double km_b = s.nd(kSk_M, c), kp_b = s.hf(kHk_M, ch), cm = s.nd(kSc_M, c);
-    const double cpl = 2.0 * ad * dx * b.Bi_M;
-    vn = ((cm - ad * (kp_b + km_b) - cpl) * x.vp + 2.0 * ad * (kp_b + km_b) * vcn +
-          4.0 * ad * dx * (b.Bi_M * b.v_inf + b.g_inf)) /
-         (cm + ad * (kp_b + km_b) + cpl);
-    const double kt_b = s.nd(kSk_TT, c), kTM_b = s.nd(kSk_TM, c);
-    const double ktp_b = s.hf(kHk_TT, ch), kmp_b = s.hf(kHk_TM, ch);
-    const double ctt = s.nd(kSc_TT, c), ctm = s.nd(kSc_TM, c);
-    const double vbar = 0.5 * (vn + x.vp);
-    const double vg = vcn - (2.0 * dx / km_b) * (b.Bi_M * (vbar - b.v_inf) - b.g_inf);
-    const double cplu = 2.0 * b_ * dx * b.Bi_TT;
-    un = ((ctt - b_ * (ktp_b + kt_b) - cplu) * x.up - p.gamma * ctm * (vn - x.vp) +
-          2.0 * b_ * (ktp_b + kt_b) * ucn + 2.0 * b_ * ratio * kTM_b * (vcn - vg) -
-          4.0 * b_ * dx * (b.Bi_TM * (vbar - b.v_inf) - b.q_inf) + 2.0 * cplu * b.u_inf +
-          2.0 * g_ * (kmp_b * vcn + kTM_b * vg) - g_ * (kmp_b + kTM_b) * (vn + x.vp)) /
-         (ctt + b_ * (ktp_b + kt_b) + cplu);
-}
-
 // One DF step of NPT nodes per thread (cells base + k * stride); guard per
 // node (exact check_bounded semantics).  Every state load of all NPT nodes is
 // issued before the stop flag is read and before any arithmetic, so a thread
@@ -257,18 +210,15 @@ __device__ __forceinline__ void wall_nodes_step(const StepArgs& a, int64_t base,
             x[k] = load_node(a, w[k], j[k]);
         }
     }
-    // an earlier step failed, or this step's coefficient tables left the box
-    // (domain_error preempts the step, wall.cpp:206): freeze
-    if (frozen_before(a.fail_key, a.layer) || (KIND == kCoeffMaterial && *a.dom_key != ~0ull)) return;
+    if (frozen_before(a.fail_key, a.layer)) return;    // an earlier step failed: freeze
 #pragma unroll
     for (int k = 0; k < NPT; ++k) {
         if (w[k] < 0) continue;
         const int64_t cell = base + static_cast<int64_t>(k) * stride;
         double un, vn;
+        // (material walls step in k_material_step, k_material.cuh)
         if (KIND == kCoeffConstant) coupled_node(a, w[k], j[k], x[k], un, vn);
-        else if (KIND == kCoeffAnalyticD) analytic_node(a, w[k], j[k], x[k], un, vn);
-        else if (a.wall_kind[w[k]] == kCoeffConstant) coupled_node(a, w[k], j[k], x[k], un, vn);
-        else table_node(a, w[k], j[k], x[k], un, vn);   // df_step_nonlinear of a material wall
+        else analytic_node(a, w[k], j[k], x[k], un, vn);
         // only the new layer is written; the host rotates layer pointers
         // (prev <- curr) instead of copying: 32 B read + 16 B written per update
         a.out[1][cell] = un;
@@ -376,9 +326,7 @@ __global__ void __launch_bounds__(kStepThreads, KIND == kCoeffConstant ? 4 : 3) 
         wall_nodes_step<step_npt(KIND), KIND>(a, base, kStepThreads);
     } else {
         const int zi = (static_cast<int>(blockIdx.x) - wall_blocks) * blockDim.x + threadIdx.x;
-        if (zi < z.n_zones && !frozen_before(z.fail_key, z.layer) &&
-            !(KIND == kCoeffMaterial && *a.dom_key != ~0ull))
-            zone_update(z, zi);
+        if (zi < z.n_zones && !frozen_before(z.fail_key, z.layer)) zone_update(z, zi);
     }
 }
 
