@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <random>
+#include <string>
 #include <vector>
 
 #include "../paper_1703_10119_b200/csrc/k_coupled.cuh"
@@ -18,12 +19,13 @@ __global__ void k_coef(int B, double dx, double dt, const Groups* g, const Biot*
     if (w < B) coupled_coef(g[w], dx, dt, b[2 * w], b[2 * w + 1], c[w]);
 }
 
-struct Bufs { double* in[4]; double* out[4]; };
+template <typename Real> struct BufsT { Real* in[4]; Real* out[4]; };
+using Bufs = BufsT<double>;
 
-template <int LPW, int NPT, int WARPS, int MINB, int UNROLL = 2, bool EDGE = false>
-float run(const char* name, CoupledSegArgs<double> a, Bufs& b, int B, int steps, std::vector<double>* result) {
+template <int LPW, int NPT, int WARPS, int MINB, int UNROLL = 2, bool EDGE = false, typename Real = double>
+float run(const char* name, CoupledSegArgs<Real> a, BufsT<Real>& b, int B, int steps, std::vector<Real>* result) {
     constexpr int CHUNK = 128;
-    auto kern = k_df_coupled<double, LPW, NPT, WARPS, CHUNK, false, false, MINB, UNROLL, EDGE>;
+    auto kern = k_df_coupled<Real, LPW, NPT, WARPS, CHUNK, false, false, MINB, UNROLL, EDGE>;
     const int smem = CHUNK * a.n_channels * sizeof(Ambient);
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cudaFuncAttributes attr;
@@ -53,7 +55,8 @@ float run(const char* name, CoupledSegArgs<double> a, Bufs& b, int B, int steps,
     if (result) {
         result->resize((size_t)B * 256 * 4);
         for (int k = 0; k < 4; ++k)
-            CK(cudaMemcpy(result->data() + (size_t)k * B * 256, b.out[k], (size_t)B * 256 * 8, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(result->data() + (size_t)k * B * 256, b.out[k], (size_t)B * 256 * sizeof(Real),
+                          cudaMemcpyDeviceToHost));
     }
     return ms;
 }
@@ -117,6 +120,37 @@ int main(int argc, char** argv) {
     a.suspect = dflag;
     a.fail_key = dkey;
     std::vector<double> ref, got;
+    if (argc > 2 && std::string(argv[2]) == "f32") {
+        // fp32 deviations from 1 (the cfg2 state), same walls and forcing
+        BufsT<float> bf;
+        std::vector<float> dev(init.size());
+        for (size_t i = 0; i < init.size(); ++i) dev[i] = static_cast<float>(init[i] - 1.0);
+        for (int k = 0; k < 4; ++k) {
+            CK(cudaMalloc(&bf.in[k], (size_t)B * n * 4));
+            CK(cudaMalloc(&bf.out[k], (size_t)B * n * 4));
+            CK(cudaMemcpy(bf.in[k], dev.data(), (size_t)B * n * 4, cudaMemcpyHostToDevice));
+        }
+        CoupledSegArgs<float> af{};
+        af.n_walls = B; af.n_channels = nch; af.divergence_norm = 1e3; af.coef = dc; af.chan = dchan;
+        af.table = dtab; af.stop = dflag; af.suspect = dflag; af.fail_key = dkey;
+        std::vector<float> rf, gf;
+        auto checkf = [&](const char* nm) {
+            double m = 0;
+            for (size_t i = 0; i < rf.size(); ++i) m = std::max(m, (double)std::fabs(rf[i] - gf[i]));
+            std::printf("    %s max |diff| vs prod %.3e\n", nm, m);
+        };
+        run<16, 16, 4, 0, 2, false, float>("f32 16x16 w4 (prod)", af, bf, B, steps, &rf);
+        run<16, 16, 8, 0, 2, false, float>("f32 16x16 w8", af, bf, B, steps, &gf); checkf("w8");
+        run<16, 16, 4, 2, 2, false, float>("f32 16x16 w4 minb2", af, bf, B, steps, &gf); checkf("minb2");
+        run<16, 16, 4, 3, 2, false, float>("f32 16x16 w4 minb3", af, bf, B, steps, &gf); checkf("minb3");
+        run<16, 16, 4, 0, 4, false, float>("f32 16x16 unroll4", af, bf, B, steps, &gf); checkf("u4");
+        run<16, 16, 4, 0, 2, true, float>("f32 16x16 edge", af, bf, B, steps, &gf); checkf("edge");
+        run<32, 8, 4, 0, 2, false, float>("f32 32x8 w4", af, bf, B, steps, &gf); checkf("32x8");
+        run<32, 8, 4, 4, 2, false, float>("f32 32x8 w4 minb4", af, bf, B, steps, &gf); checkf("32x8 minb4");
+        run<32, 8, 8, 0, 4, true, float>("f32 32x8 w8 u4 edge", af, bf, B, steps, &gf); checkf("32x8 w8 u4e");
+        run<8, 32, 4, 0, 2, false, float>("f32 8x32 w4", af, bf, B, steps, &gf); checkf("8x32");
+        return 0;
+    }
     run<16, 16, 4, 0>("16x16 w4 (prod)", a, b, B, steps, &ref);
     auto check = [&](const char* nm) {
         double m = 0;
@@ -128,6 +162,6 @@ int main(int argc, char** argv) {
     run<16, 16, 4, 0, 4, true>("16x16 unroll4 edge", a, b, B, steps, &got); check("unroll4+edge");
     run<16, 16, 4, 0, 8, false>("16x16 unroll8", a, b, B, steps, &got); check("unroll8");
     run<32, 8, 4, 0, 4, true>("32x8 unroll4 edge", a, b, B, steps, &got); check("32x8 u4e");
-    run<32, 8, 4, 4, 4, true>("32x8 u4 edge minb4", a, b, B, steps, nullptr);
+    run<32, 8, 4, 4, 4, true>("32x8 u4 edge minb4", a, b, B, steps, static_cast<std::vector<double>*>(nullptr));
     return 0;
 }
