@@ -121,3 +121,30 @@ def test_analytic_walls_implicit_start():
     err = rel_linf(got, ref)
     print("analytic implicit start rel L-inf", err)
     assert err <= TOL
+
+
+def test_run_scheme_euler_implicit_matches_oracle():
+    """hyg_run_scheme with the Euler-implicit scheme (step_implicit every
+    step, building.cpp:327-331) on a material building with radiation: the
+    state and SimulationResult's subiteration counters as the oracle's march
+    of orc_step_implicit."""
+    import ctypes as C
+    w = workloads.material_building(n_zones=2, n_nodes=41, dt=1e-2)
+    w.model.eta_factor = 1e-3
+    b = O.Building(w.model, w.init)
+    lib = O.oracle_lib()
+    passes = []
+    for _ in range(40):
+        p, r = C.c_int(0), C.c_double(0)
+        assert lib.orc_step_implicit(C.byref(b.desc), C.byref(b.s), w.model.eta_factor * w.model.dt,
+                                     w.model.max_subiters, C.byref(p), C.byref(r)) == 0
+        passes.append(p.value)
+    with Context(w.model) as ctx:
+        ctx.set_state(**w.init)
+        rep = ctx.run_scheme("euler-implicit", horizon=40 * w.model.dt)
+        got = ctx.get_state()
+    assert rep.steps == 40 and rep.max_subiters_seen == max(passes)
+    assert rep.mean_subiters == sum(passes) / 40
+    err = rel_linf(got, dict(b.state))
+    print("euler-implicit rel L-inf", err, "passes", passes[:5])
+    assert err <= TOL
