@@ -198,7 +198,6 @@ struct hyg_ctx {
     unsigned long long* d_dom = nullptr;
     bool has_rad = false;
     bool ring = false;               // K4: zone-ring temporal blocking applies
-    bool ring_reg = false;           // K4 v2 (owned walls in registers) for n <= 128
     int ring_W = 0, ring_B = 0;
     int rad_groups = 0, rad_terms = 0;
     int *d_rad_tgt = nullptr, *d_rad_grp = nullptr;
@@ -929,17 +928,6 @@ int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
 }
 
 // ---- the zone-ring temporally blocked path (K4) ---------------------------------
-template <int NPT, bool FLUX>
-void launch_ring_reg(const RingArgs& a, int grid, int threads, size_t smem, cudaStream_t s) {
-    auto k = k_ring_reg<NPT, kRingS, FLUX>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
-    }
-    k<<<grid, threads, smem, s>>>(a);
-}
-
 template <int NPT>
 void launch_ring(const RingArgs& a, int grid, int threads, size_t smem, cudaStream_t s) {
     auto k = k_ring_tiled<NPT, kRingS>;
@@ -962,11 +950,10 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
     const int nsrc = static_cast<int>(c->zsrc.size() / 3);
     const int Z = static_cast<int>(c->zones.size()), W = c->ring_W, B = c->ring_B, npt = c->n / 16;
     const int grid = (Z + B - 1) / B;
-    const int threads = c->ring_reg ? RingRegShape<4, kRingS>::threads(B, W) : RingShape<8, kRingS>::threads(B, W);
-    const size_t smem = c->ring_reg ? RingRegShape<4, kRingS>::smem_bytes(B, W, nch, nsrc)
-                        : npt == 4  ? RingShape<4, kRingS>::smem_bytes(B, W, nch, nsrc)
-                        : npt == 8  ? RingShape<8, kRingS>::smem_bytes(B, W, nch, nsrc)
-                                    : RingShape<16, kRingS>::smem_bytes(B, W, nch, nsrc);
+    const int threads = RingShape<8, kRingS>::threads(B, W);
+    const size_t smem = npt == 4 ? RingShape<4, kRingS>::smem_bytes(B, W, nch, nsrc)
+                        : npt == 8 ? RingShape<8, kRingS>::smem_bytes(B, W, nch, nsrc)
+                                   : RingShape<16, kRingS>::smem_bytes(B, W, nch, nsrc);
     const int64_t block = 65536 / kRingS * kRingS;
     for (int64_t done = 0; done < nsteps;) {
         const int64_t rows = std::min(block, nsteps - done);
@@ -1014,13 +1001,7 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
             a.zu_out = c->zu[1 - zf];
             a.zv_out = c->zv[1 - zf];
             LaunchScope ls(c, "ring_tiled", static_cast<double>(c->cells()) * a.steps);
-            if (c->ring_reg) {
-                const int rnpt = c->n / 32;
-                if (rnpt == 4) c->flux ? launch_ring_reg<4, true>(a, grid, threads, smem, c->stream)
-                                       : launch_ring_reg<4, false>(a, grid, threads, smem, c->stream);
-                else c->flux ? launch_ring_reg<2, true>(a, grid, threads, smem, c->stream)
-                             : launch_ring_reg<2, false>(a, grid, threads, smem, c->stream);
-            } else if (npt == 4) launch_ring<4>(a, grid, threads, smem, c->stream);
+            if (npt == 4) launch_ring<4>(a, grid, threads, smem, c->stream);
             else if (npt == 8) launch_ring<8>(a, grid, threads, smem, c->stream);
             else launch_ring<16>(a, grid, threads, smem, c->stream);
         }
@@ -1347,19 +1328,6 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
                 c->ring = true;
                 c->ring_W = W;
                 c->ring_B = B;
-            }
-            // v2: one warp per owned wall, n = 32 x {2, 4} nodes in registers
-            if (c->n <= 128) {
-                int B2 = std::min(Z, 32 - 2 * kRingS);
-                while (B2 > 0 && (RingRegShape<4, kRingS>::threads(B2, W) > 768 ||
-                                  RingRegShape<4, kRingS>::smem_bytes(B2, W, nch, nsrc) > 227u * 1024u))
-                    --B2;
-                if (B2 >= 1) {
-                    c->ring = true;
-                    c->ring_reg = true;
-                    c->ring_W = W;
-                    c->ring_B = B2;
-                }
             }
         }
     }

@@ -28,7 +28,6 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-#include "k_coupled.cuh"
 #include "k_step.cuh"
 
 namespace hyg {
@@ -381,293 +380,6 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
         a.out[3][g] = smem[own_ix(1, cur, wl, j)];
     }
     for (int i = tid; i < nown; i += nthr) {
-        a.zu_out[z0 + i] = smem[zn_ix(0, cur, S + i)];
-        a.zv_out[z0 + i] = smem[zn_ix(1, cur, S + i)];
-    }
-}
-
-
-// ---- K4 v2: owned walls register-resident ------------------------------------------
-// One warp per owned wall: 32 lanes x NPT nodes in registers, stepped with
-// K1's coupled_step (k_coupled.cuh: shuffles between lanes, the last lane's
-// nodes reversed so both faces sit in register 0; exact guard).  The face-1
-// ambient of the last lane is the zone's layer-k air; the last lane posts the
-// wall's layer-k zone-face sample to a double-buffered shared slot for the
-// zone warp.  Halo walls and the zone warp are those of k_ring_tiled.  Only
-// the halo (2 (S-1) W walls x (S+1) nodes), the zone tables and the forcing
-// rows use shared memory.
-template <int NPT, int S>
-struct RingRegShape {
-    static constexpr int kP = S + 1;
-    static constexpr int kHaloZones = 2 * (S - 1);
-    __host__ __device__ static int halo_walls(int W) { return kHaloZones * W; }
-    __host__ __device__ static int row_width(int nch, int nsrc) { return 4 * nch + 3 * nsrc + 2; }
-    __host__ __device__ static size_t smem_bytes(int B, int W, int nch, int nsrc) {
-        const size_t halo = static_cast<size_t>(halo_walls(W)) * kP * 4;
-        const size_t LB = static_cast<size_t>(B + 2 * S);
-        return sizeof(double) * (halo + 4 * LB + LB * kRingZP + 4 * static_cast<size_t>(B) * W +
-                                 static_cast<size_t>(S) * row_width(nch, nsrc));
-    }
-    __host__ __device__ static int halo_threads(int W) { return (halo_walls(W) + 31) / 32 * 32; }
-    __host__ __device__ static int threads(int B, int W) { return 32 * B * W + halo_threads(W) + 32; }
-};
-
-template <int NPT, int S, bool FLUX>
-__global__ void __launch_bounds__(768, 1) k_ring_reg(const RingArgs a) {
-    using Sh = RingRegShape<NPT, S>;
-    constexpr int LPW = 32;
-    extern __shared__ double smem[];
-    if (*a.stop) return;                          // an earlier launch tripped the guard
-    const int n = a.n, W = a.W, B = a.B, Z = a.n_zones;
-    const int hw = Sh::halo_walls(W);
-    const int z0 = blockIdx.x * B;
-    const int nown = min(B, Z - z0);
-    const int L = nown + 2 * S, LB = B + 2 * S, BW = B * W;
-    const int rw = Sh::row_width(a.n_channels, a.n_sources);
-    constexpr int P = Sh::kP;
-    const int oHAL = 0;
-    const int oZN = oHAL + 4 * hw * P;
-    const int oZP = oZN + 4 * LB;
-    const int oFACE = oZP + LB * kRingZP;         // [slot 2][field 2][B W]
-    const int oRW = oFACE + 4 * BW;
-    auto hal_ix = [&](int f, int slot, int hl, int p) { return oHAL + ((f * 2 + slot) * hw + hl) * P + p; };
-    auto zn_ix = [&](int f, int slot, int i) { return oZN + (f * 2 + slot) * LB + i; };
-    auto gzone = [&](int i) { return ((z0 - S + i) % Z + Z) % Z; };
-    const int tid = threadIdx.x, nthr = blockDim.x;
-    const int warp = tid / 32, lane = tid % 32;
-    const int own_thr = 32 * BW, halo_thr = Sh::halo_threads(W);
-
-    // ---- stage halo walls, forcing rows, zone states and parameters (as k_ring_tiled)
-    for (int i = tid; i < hw * P; i += nthr) {
-        const int hl = i / P, p = i - hl * P;
-        const int hz = hl / W, wi = hl - hz * W;
-        const int li = hz < S - 1 ? 1 + hz : S + nown + (hz - (S - 1));
-        const size_t g = (static_cast<size_t>(gzone(li)) * W + wi) * n + (n - P + p);
-        cp_async8(&smem[hal_ix(0, 0, hl, p)], a.in[0] + g);
-        cp_async8(&smem[hal_ix(0, 1, hl, p)], a.in[1] + g);
-        cp_async8(&smem[hal_ix(1, 0, hl, p)], a.in[2] + g);
-        cp_async8(&smem[hal_ix(1, 1, hl, p)], a.in[3] + g);
-    }
-    for (int i = tid; i < a.steps * rw; i += nthr) {
-        const int k = i / rw, r = i - k * rw;
-        smem[oRW + i] = r < 4 * a.n_channels
-                            ? reinterpret_cast<const double*>(a.table + static_cast<size_t>(k) * a.n_channels)[r]
-                            : a.src[static_cast<size_t>(k) * (3 * a.n_sources + 2) + (r - 4 * a.n_channels)];
-    }
-    for (int i = tid; i < L; i += nthr) {
-        const int z = gzone(i);
-        smem[zn_ix(0, 1, i)] = a.zu_in[z];
-        smem[zn_ix(1, 1, i)] = a.zv_in[z];
-        const ZoneDev d = a.zones[z];
-        double* zp = &smem[oZP + i * kRingZP];
-        zp[0] = 1.0 + d.kappa_a_tt1;
-        zp[1] = d.g_v;
-        zp[2] = d.q_v1;
-        zp[3] = d.q_v2;
-        zp[4] = d.wall_end - d.wall_begin;
-        zp[5] = d.inz_end - d.inz_begin;
-        zp[6] = d.sources;
-        for (int q = 0; q < d.wall_end - d.wall_begin; ++q) {
-            const ZoneLinkDev l = a.links[d.wall_begin + q];
-            zp[8 + 4 * q] = l.wall - z * W;
-            zp[9 + 4 * q] = l.Bi_TT * l.theta_T;
-            zp[10 + 4 * q] = l.Bi_TM * l.theta_T;
-            zp[11 + 4 * q] = d.sign * l.Bi_M * l.theta_M;
-        }
-        for (int q = 0; q < d.inz_end - d.inz_begin; ++q) {
-            const InzLinkDev l = a.inz[d.inz_begin + q];
-            zp[40 + 4 * q] = i >= 1 && gzone(i - 1) == l.peer ? i - 1 : i + 1;
-            zp[41 + 4 * q] = l.g_inz;
-            zp[42 + 4 * q] = l.q_inz1;
-            zp[43 + 4 * q] = l.q_inz2;
-        }
-    }
-
-    cp_async_wait_all();
-    __syncthreads();
-    bool bad = false;
-
-    if (tid < own_thr) {
-        // ---- owned walls: registers (K1 layout), loaded straight from HBM -----------
-        const int wl = warp;
-        const bool live = wl < nown * W;
-        const int w = z0 * W + (live ? wl : 0);
-        const bool first = lane == 0, rev = lane == LPW - 1, mirror0 = first || rev;
-        double up[NPT], uc[NPT], vp[NPT], vc[NPT];
-        const size_t base = static_cast<size_t>(w) * n + lane * NPT;
-#pragma unroll
-        for (int j = 0; j < NPT; ++j) {
-            const size_t i = base + (rev ? NPT - 1 - j : j);
-            up[j] = live ? a.in[0][i] : 0.0;
-            uc[j] = live ? a.in[1][i] : 0.0;
-            vp[j] = live ? a.in[2][i] : 0.0;
-            vc[j] = live ? a.in[3][i] : 0.0;
-        }
-        const WallCoef& wc = a.coef[w];
-        const InRow<double> ci{wc.in.b, wc.in.c_su, wc.in.c_sv};
-        FaceRow<double> c0{ci.b, 0.0, ci.c_su, 0.0, ci.c_sv, 0.0};
-        double e_g = 0.0, c_q = 0.0, c_g = 0.0;
-        if (mirror0) {
-            const RowCoef& f = wc.face[first ? 0 : 1];
-            c0 = FaceRow<double>{f.b, f.e, f.c_su, f.c_tu, f.c_sv, f.c_tv};
-            e_g = f.e_g;
-            c_q = f.c_q;
-            c_g = f.c_g;
-        }
-        const int ch = a.attach[2 * w].index;
-        const int lz = S + wl / W;                // local zone of the wall
-        unsigned acc = 0;
-        int cur = 1;
-        // P holds layer k-1 on entry and k+1 on exit, C holds layer k
-        auto step = [&](int k, double (&vP)[NPT], double (&vC)[NPT], double (&uP)[NPT], double (&uC)[NPT]) {
-            const int slot = k & 1;
-            if (rev) {                            // post the layer-k zone-face sample
-                smem[oFACE + (slot * 2 + 0) * BW + wl] = uC[0];
-                smem[oFACE + (slot * 2 + 1) * BW + wl] = vC[0];
-            }
-            __syncthreads();
-            StepAmb<double> am{0.0, 0.0, 0.0, 0.0};
-            if (first) {                          // exterior channel, layer-k forcing
-                const int r = oRW + k * rw + 4 * ch;
-                am.u_inf = smem[r + 0];
-                am.v_inf = smem[r + 1];
-                if (FLUX) {
-                    am.ev = e_g * smem[r + 2];
-                    am.eu = fma(c_q, smem[r + 3], c_g * smem[r + 2]);
-                }
-            } else if (rev) {                     // the zone's layer-k air
-                am.u_inf = smem[zn_ix(0, cur, lz)];
-                am.v_inf = smem[zn_ix(1, cur, lz)];
-            }
-            coupled_step<double, LPW, NPT, FLUX, true>(vP, vC, uP, uC, ci, c0, am, mirror0, rev, acc, bad, a.norm);
-            cur ^= 1;
-        };
-        int k = 0;
-        for (; k + 1 < a.steps; k += 2) {
-            step(k, vp, vc, up, uc);              // layer k+1 into (up, vp)
-            step(k + 1, vc, vp, uc, up);          // layer k+2 into (uc, vc)
-        }
-        if (k < a.steps) {                        // odd tail: one step, then rename the layers
-            step(k, vp, vc, up, uc);
-#pragma unroll
-            for (int j = 0; j < NPT; ++j) {
-                double t = vp[j]; vp[j] = vc[j]; vc[j] = t;
-                t = up[j]; up[j] = uc[j]; uc[j] = t;
-            }
-        }
-        if (!live) bad = false;
-        if (__syncthreads_or(bad)) {
-            if (tid == 0) atomicCAS(a.stop, 0, a.seg_index + 1);
-            return;
-        }
-        if (live) {
-#pragma unroll
-            for (int j = 0; j < NPT; ++j) {
-                const size_t i = base + (rev ? NPT - 1 - j : j);
-                a.out[0][i] = up[j];
-                a.out[1][i] = uc[j];
-                a.out[2][i] = vp[j];
-                a.out[3][i] = vc[j];
-            }
-        }
-        return;
-    }
-
-    int cur = 1;                                  // zone / halo slot holding layer k
-    if (tid < own_thr + halo_thr) {
-        // ---- halo walls (as k_ring_tiled) ---------------------------------------------
-        const int hl = tid - own_thr;
-        const bool hlive = hl < hw;
-        const int hz = (hlive ? hl : 0) / W, wi = (hlive ? hl : 0) - hz * W;
-        const int li = hz < S - 1 ? 1 + hz : S + nown + (hz - (S - 1));
-        const int hwall = gzone(li) * W + wi;
-        const double cb = a.coef[hwall].in.b, csu = a.coef[hwall].in.c_su, csv = a.coef[hwall].in.c_sv;
-        for (int k = 0; k < a.steps; ++k) {
-            __syncthreads();
-            if (hlive) {
-                const int prv = cur ^ 1;
-                const int hu = hal_ix(0, cur, hl, 0), hv = hal_ix(1, cur, hl, 0);
-                const int hpu = hal_ix(0, prv, hl, 0), hpv = hal_ix(1, prv, hl, 0);
-                double ul = smem[hu], vl = smem[hv];
-                double ucx = ul, vcx = vl;
-#pragma unroll
-                for (int p = 0; p < P; ++p) {
-                    const int pr = p == P - 1 ? P - 2 : p + 1;
-                    const double ur = smem[hu + pr], vr = smem[hv + pr];
-                    const double upp = smem[hpu + p], vpp = smem[hpv + p];
-                    const double d = fma(-2.0, vpp, vl + vr);
-                    const double du = fma(-2.0, upp, ul + ur);
-                    double vn, un;
-                    if (p < P - 1) {
-                        vn = fma(cb, d, vpp);
-                        un = fma(csv, d, fma(csu, du, upp));
-                    } else {
-                        const RowCoef c = a.coef[hwall].face[1];
-                        const double t = smem[zn_ix(1, cur, li)] - vpp, tu = smem[zn_ix(0, cur, li)] - upp;
-                        vn = fma(c.e, t, fma(c.b, d, fma(c.e_g, 0.0, vpp)));
-                        un = fma(c.c_tv, t, fma(c.c_sv, d, fma(c.c_tu, tu, fma(c.c_su, du, fma(c.c_q, 0.0,
-                                                                                          fma(c.c_g, 0.0, upp))))));
-                    }
-                    smem[hpu + p] = un;
-                    smem[hpv + p] = vn;
-                    ul = ucx;
-                    vl = vcx;
-                    ucx = ur;
-                    vcx = vr;
-                }
-            }
-            cur ^= 1;
-        }
-    } else {
-        // ---- zone warp (zone_step_explicit zone.cpp:69-74): owned samples from the
-        // face slots, halo samples from the halo tiles -------------------------------------
-        const int i = tid - own_thr - halo_thr;
-        const bool zlive = i >= 1 && i < L - 1;
-        const int zp = oZP + (zlive ? i : 0) * kRingZP;
-        const bool owned = i >= S && i < S + nown;
-        const int hz = i < S ? i - 1 : (S - 1) + (i - S - nown);
-        for (int k = 0; k < a.steps; ++k) {
-            __syncthreads();
-            if (zlive) {
-                const int slot = k & 1;
-                const double u_a = smem[zn_ix(0, cur, i)], v_a = smem[zn_ix(1, cur, i)];
-                const int srow = oRW + k * rw + 4 * a.n_channels;
-                const int sz = srow + 3 * static_cast<int>(smem[zp + 6]);
-                const double u_inf = smem[srow + 3 * a.n_sources + 0], v_inf = smem[srow + 3 * a.n_sources + 1];
-                double du = smem[sz + 1] + smem[sz + 2] + smem[zp + 2] * (u_inf * v_inf - u_a * v_a) +
-                            smem[zp + 3] * (u_inf - u_a);
-                double dv = smem[sz + 0] + smem[zp + 1] * (v_inf - v_a);
-                const int npeer = static_cast<int>(smem[zp + 5]), nlink = static_cast<int>(smem[zp + 4]);
-                for (int q = 0; q < npeer; ++q) {
-                    const int pi = static_cast<int>(smem[zp + 40 + 4 * q]);
-                    const double pu = smem[zn_ix(0, cur, pi)], pv = smem[zn_ix(1, cur, pi)];
-                    du += smem[zp + 42 + 4 * q] * (pu * pv - u_a * v_a) + smem[zp + 43 + 4 * q] * (pu - u_a);
-                    dv += smem[zp + 41 + 4 * q] * (pv - v_a);
-                }
-                for (int q = 0; q < nlink; ++q) {
-                    const int wi = static_cast<int>(smem[zp + 8 + 4 * q]);
-                    const int iu = owned ? oFACE + (slot * 2 + 0) * BW + (i - S) * W + wi
-                                         : hal_ix(0, cur, hz * W + wi, P - 1);
-                    const int iv = owned ? oFACE + (slot * 2 + 1) * BW + (i - S) * W + wi
-                                         : hal_ix(1, cur, hz * W + wi, P - 1);
-                    const double us = smem[iu], vs = smem[iv];
-                    du += smem[zp + 9 + 4 * q] * (us - u_a) + smem[zp + 10 + 4 * q] * (vs - v_a);
-                    dv += smem[zp + 11 + 4 * q] * (v_a - vs);
-                }
-                const double nu = u_a + a.dt * (du / smem[zp + 0]);
-                const double nv = v_a + a.dt * dv;
-                smem[zn_ix(0, cur ^ 1, i)] = nu;
-                smem[zn_ix(1, cur ^ 1, i)] = nv;
-                if (owned) bad = bad || !isfinite(nu) || !isfinite(nv) || fabs(nu) > a.norm || fabs(nv) > a.norm;
-            }
-            cur ^= 1;
-        }
-    }
-    if (__syncthreads_or(bad)) {
-        if (tid == 0) atomicCAS(a.stop, 0, a.seg_index + 1);
-        return;
-    }
-    for (int i = tid - own_thr; i < nown; i += nthr - own_thr) {
         a.zu_out[z0 + i] = smem[zn_ix(0, cur, S + i)];
         a.zv_out[z0 + i] = smem[zn_ix(1, cur, S + i)];
     }
