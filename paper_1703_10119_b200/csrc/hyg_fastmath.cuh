@@ -20,11 +20,11 @@
 namespace hyg {
 
 __device__ __forceinline__ double fexp(double x) {
-    if (!(x == x)) return x;                 // NaN
-    if (x < -708.0) return 0.0;
-    if (x > 709.0) return __longlong_as_double(0x7ff0000000000000ll);
-    const double kd = rint(x * 1.4426950408889634074);
-    const double r = fma(-kd, 1.90821492927058770002e-10, fma(-kd, 6.93147180369123816490e-01, x));
+    // branch-free: clamp, evaluate, then select the special results (no
+    // divergent branch on the single-wall step's critical path)
+    const double xc = fmin(fmax(x, -708.0), 709.0);    // NaN -> -708 here, restored below
+    const double kd = rint(xc * 1.4426950408889634074);
+    const double r = fma(-kd, 1.90821492927058770002e-10, fma(-kd, 6.93147180369123816490e-01, xc));
     // Taylor coefficients 1/k!, k = 0..13, in pairs (c_{2i} + c_{2i+1} r)
     const double r2 = r * r;
     const double p01 = fma(r, 1.0, 1.0);
@@ -40,7 +40,10 @@ __device__ __forceinline__ double fexp(double x) {
     const double q811 = fma(r2, p1011, p89);
     const double q = fma(r4, fma(r4, fma(r4, p1213, q811), q47), q03);
     const long long k = static_cast<long long>(kd);
-    return __longlong_as_double(__double_as_longlong(q) + (k << 52));
+    double y = __longlong_as_double(__double_as_longlong(q) + (k << 52));
+    y = x < -708.0 ? 0.0 : y;
+    y = x > 709.0 ? __longlong_as_double(0x7ff0000000000000ll) : y;
+    return x == x ? y : x;                              // NaN propagates
 }
 
 __device__ __forceinline__ double frcp(double d) {

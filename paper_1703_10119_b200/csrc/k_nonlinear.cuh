@@ -22,6 +22,7 @@
 //   coefficient k_M at the boundary node and vg from vbar = (vn + vp)/2.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "hyg_coef.cuh"
@@ -132,11 +133,14 @@ __global__ void __launch_bounds__(IT + 32) k_df_analytic_walls(const NonlinearSe
             s_amb[s][f] = A.table[static_cast<size_t>(c0 + s) * A.n_channels + (f ? chr : chl)];
         }
         __syncthreads();
-        for (int s = 0; s < clen; ++s) {
-            double* up = s_lay[P];
-            const double* uc = s_lay[1 - P];
-            double* vp = s_lay[2 + P];
-            const double* vc = s_lay[3 - P];
+        // one step with compile-time layer roles (PP): the 2-step unroll keeps
+        // every shared address a constant offset (no per-step address math)
+        auto step = [&](int s, auto PPc) {
+            constexpr int PP = decltype(PPc)::value;
+            double* up = s_lay[PP];
+            const double* uc = s_lay[1 - PP];
+            double* vp = s_lay[2 + PP];
+            const double* vc = s_lay[3 - PP];
             if (!face_warp) {
                 for (int j = 1 + tid; j < n - 1; j += IT) {
                     const double vpj = vp[j], upj = up[j], vcj = vc[j];
@@ -161,7 +165,20 @@ __global__ void __launch_bounds__(IT + 32) k_df_analytic_walls(const NonlinearSe
                 up[j] = un;
             }
             __syncthreads();
-            P ^= 1;
+        };
+        int s = 0;
+        if (P == 0) {
+            for (; s + 1 < clen; s += 2) {
+                step(s, std::integral_constant<int, 0>{});
+                step(s + 1, std::integral_constant<int, 1>{});
+            }
+            if (s < clen) { step(s, std::integral_constant<int, 0>{}); P = 1; }
+        } else {
+            for (; s + 1 < clen; s += 2) {
+                step(s, std::integral_constant<int, 1>{});
+                step(s + 1, std::integral_constant<int, 0>{});
+            }
+            if (s < clen) { step(s, std::integral_constant<int, 1>{}); P = 0; }
         }
     }
     // fast guard verdict (bit 30 of the high word: |x| >= 2 or not finite)
