@@ -102,14 +102,13 @@ __device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) 
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// position of node j = s NPT + q inside an owned wall (thread s owns nodes
-// s NPT .. s NPT + NPT-1): pairs (q, q+1) adjacent, pair rows of the 16 lanes
-// contiguous — every 128-bit access of a wall's 16 lanes covers 256
-// consecutive bytes (conflict-free, half the shared-memory instructions)
+// position of node j inside an owned wall: segments of NPT nodes, the node
+// index XOR-swizzled per segment so the 16 lanes of a wall (one segment each)
+// hit 16 distinct bank pairs
 template <int NPT>
 __device__ __forceinline__ int ring_pos(int j) {
     const int s = j / NPT, q = j % NPT;
-    return (q / 2) * 32 + s * 2 + (q & 1);
+    return s * NPT + (q ^ ((s / (16 / NPT)) & (NPT - 1)));
 }
 
 template <int NPT, int S>
@@ -219,71 +218,59 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
         const double cb = a.coef[w].in.b, csu = a.coef[w].in.c_su, csv = a.coef[w].in.c_sv;
         const int ch = a.attach[2 * w].index;
         const int j0 = s * NPT;
-        // this wall's four shared rows; the thread's pair rows start at 2 s
+        // this wall's four shared rows and the swizzled offsets of the thread's nodes
         const int U0 = oOWN + (0 * ow + wl) * n, U1 = oOWN + (1 * ow + wl) * n;
         const int V0 = oOWN + (2 * ow + wl) * n, V1 = oOWN + (3 * ow + wl) * n;
+        const int g = (s / (16 / NPT)) & (NPT - 1);
+        const int base = s * NPT;
         const int left = j0 == 0 ? ring_pos<NPT>(1) : ring_pos<NPT>(j0 - 1);
         const int right = j0 + NPT - 1 == n - 1 ? ring_pos<NPT>(n - 2) : ring_pos<NPT>(j0 + NPT);
         const int fc0 = oFC + (wl * 2 + 0) * kRingFace, fc1 = fc0 + kRingFace;
-        auto pair_at = [&](int off) { return *reinterpret_cast<const double2*>(&smem[off]); };
         for (int k = 0; k < a.steps; ++k) {
             if (live) {
                 const int uc_ = cur ? U1 : U0, vc_ = cur ? V1 : V0;
                 const int up_ = cur ? U0 : U1, vp_ = cur ? V0 : V1;
-                // one node (coupled_node): neighbours l, r of layer k, prev of layer k-1
-                auto node = [&](int j, double ul, double ur, double vl, double vr, double up, double vp,
-                                double& un, double& vn) {
+                double ul = smem[uc_ + left], vl = smem[vc_ + left];
+                double uc = smem[uc_ + base + (0 ^ g)], vc = smem[vc_ + base + (0 ^ g)];
+#pragma unroll
+                for (int q = 0; q < NPT; ++q) {
+                    const int j = j0 + q;
+                    const int pq = base + (q ^ g);
+                    const int pr = q == NPT - 1 ? right : base + ((q + 1) ^ g);
+                    const double ur = smem[uc_ + pr], vr = smem[vc_ + pr];
+                    const double up = smem[up_ + pq], vp = smem[vp_ + pq];
                     const double d = fma(-2.0, vp, vl + vr);
                     const double du = fma(-2.0, up, ul + ur);
+                    double vn, un;
                     if (j > 0 && j < n - 1) {
                         vn = fma(cb, d, vp);
                         un = fma(csv, d, fma(csu, du, up));
-                        return;
-                    }
-                    // faces: x=0 the exterior channel, x=1 the zone's layer-k air
-                    const int c = j == 0 ? fc0 : fc1;
-                    double u_inf, v_inf, g_inf = 0.0, q_inf = 0.0;
-                    if (j == 0) {
-                        const int am = oRW + k * rw + 4 * ch;
-                        u_inf = smem[am + 0];
-                        v_inf = smem[am + 1];
-                        g_inf = smem[am + 2];
-                        q_inf = smem[am + 3] + 0.0;
                     } else {
-                        u_inf = smem[zn_ix(0, cur, li)];
-                        v_inf = smem[zn_ix(1, cur, li)];
+                        // faces (coupled_node): x=0 the exterior channel, x=1 the zone's layer-k air
+                        const int c = j == 0 ? fc0 : fc1;
+                        double u_inf, v_inf, g_inf = 0.0, q_inf = 0.0;
+                        if (j == 0) {
+                            const int am = oRW + k * rw + 4 * ch;
+                            u_inf = smem[am + 0];
+                            v_inf = smem[am + 1];
+                            g_inf = smem[am + 2];
+                            q_inf = smem[am + 3] + 0.0;
+                        } else {
+                            u_inf = smem[zn_ix(0, cur, li)];
+                            v_inf = smem[zn_ix(1, cur, li)];
+                        }
+                        const double t = v_inf - vp, tu = u_inf - up;
+                        vn = fma(smem[c + 0], t, fma(smem[c + 1], d, fma(smem[c + 2], g_inf, vp)));
+                        un = fma(smem[c + 3], t, fma(smem[c + 4], d, fma(smem[c + 5], tu, fma(smem[c + 6], du,
+                                 fma(smem[c + 7], q_inf, fma(smem[c + 8], g_inf, up))))));
                     }
-                    const double t = v_inf - vp, tu = u_inf - up;
-                    vn = fma(smem[c + 0], t, fma(smem[c + 1], d, fma(smem[c + 2], g_inf, vp)));
-                    un = fma(smem[c + 3], t, fma(smem[c + 4], d, fma(smem[c + 5], tu, fma(smem[c + 6], du,
-                             fma(smem[c + 7], q_inf, fma(smem[c + 8], g_inf, up))))));
-                };
-                double ul = smem[uc_ + left], vl = smem[vc_ + left];
-                double2 uq = pair_at(uc_ + 2 * s), vq = pair_at(vc_ + 2 * s);     // layer k, nodes j, j+1
-#pragma unroll
-                for (int qp = 0; qp < NPT / 2; ++qp) {
-                    const int j = j0 + 2 * qp;
-                    const int row = qp * 32 + 2 * s;
-                    double2 un2, vn2, uqn, vqn;
-                    if (qp + 1 < NPT / 2) {
-                        uqn = pair_at(uc_ + row + 32);
-                        vqn = pair_at(vc_ + row + 32);
-                    } else {
-                        uqn.x = smem[uc_ + right];
-                        vqn.x = smem[vc_ + right];
-                        uqn.y = vqn.y = 0.0;
-                    }
-                    const double2 upq = pair_at(up_ + row), vpq = pair_at(vp_ + row);
-                    node(j, ul, uq.y, vl, vq.y, upq.x, vpq.x, un2.x, vn2.x);
-                    node(j + 1, uq.x, uqn.x, vq.x, vqn.x, upq.y, vpq.y, un2.y, vn2.y);
-                    *reinterpret_cast<double2*>(&smem[up_ + row]) = un2;   // layer k+1 overwrites k-1
-                    *reinterpret_cast<double2*>(&smem[vp_ + row]) = vn2;
-                    bad = bad || !(fabs(un2.x) <= a.norm) || !(fabs(vn2.x) <= a.norm) ||
-                          !(fabs(un2.y) <= a.norm) || !(fabs(vn2.y) <= a.norm);
-                    ul = uq.y;
-                    vl = vq.y;
-                    uq = uqn;
-                    vq = vqn;
+                    smem[up_ + pq] = un;            // layer k+1 overwrites layer k-1
+                    smem[vp_ + pq] = vn;
+                    bad = bad || !(fabs(un) <= a.norm) || !(fabs(vn) <= a.norm);
+                    ul = uc;
+                    vl = vc;
+                    uc = ur;
+                    vc = vr;
                 }
             }
             __syncthreads();
