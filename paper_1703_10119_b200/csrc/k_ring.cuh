@@ -232,9 +232,6 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
                 const int up_ = cur ? U0 : U1, vp_ = cur ? V0 : V1;
                 double ul = smem[uc_ + left], vl = smem[vc_ + left];
                 double uc = smem[uc_ + base + (0 ^ g)], vc = smem[vc_ + base + (0 ^ g)];
-                // all NPT new values first, stores after: no store can alias a
-                // later load, so the compiler is free to hoist the loads
-                double un_[NPT], vn_[NPT];
 #pragma unroll
                 for (int q = 0; q < NPT; ++q) {
                     const int j = j0 + q;
@@ -267,18 +264,13 @@ __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
                         un = fma(smem[c + 3], t, fma(smem[c + 4], d, fma(smem[c + 5], tu, fma(smem[c + 6], du,
                                  fma(smem[c + 7], q_inf, fma(smem[c + 8], g_inf, up))))));
                     }
-                    un_[q] = un;
-                    vn_[q] = vn;
+                    smem[up_ + pq] = un;            // layer k+1 overwrites layer k-1
+                    smem[vp_ + pq] = vn;
                     bad = bad || !(fabs(un) <= a.norm) || !(fabs(vn) <= a.norm);
                     ul = uc;
                     vl = vc;
                     uc = ur;
                     vc = vr;
-                }
-#pragma unroll
-                for (int q = 0; q < NPT; ++q) {     // layer k+1 overwrites layer k-1
-                    smem[up_ + base + (q ^ g)] = un_[q];
-                    smem[vp_ + base + (q ^ g)] = vn_[q];
                 }
             }
             __syncthreads();
