@@ -54,6 +54,11 @@ def build_oracle(verbose: bool = False) -> None:
     subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "all"], check=True)
     if Path("/root/reference/proj/src/wall.cpp").exists():
         subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "ref", "adapter"], check=True)
+        # scenario JSON -> reference loader -> both runs -> reference CSV writer
+        # (needs the nlohmann/json copy vendored in this image; optional)
+        r = subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "scenario"])
+        if r.returncode != 0:
+            print("note: oracle/_ref/scenario_check not built (nlohmann/json missing?)", flush=True)
 
 
 def build_all(force: bool = False, verbose: bool = False) -> None:
