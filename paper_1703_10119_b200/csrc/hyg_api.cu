@@ -22,6 +22,7 @@
 #include "k_step.cuh"
 #include "k_nonlinear.cuh"
 #include "k_tiled.cuh"
+#include "k_dv_warp.cuh"
 #include "k_material.cuh"
 #include "k_ring.cuh"
 
@@ -793,7 +794,41 @@ int advance_fused_t(hyg_ctx* c, Real* (&buf)[2][4], int64_t nsteps, double dt, h
     return HYG_OK;
 }
 
-// ---- the fused nonlinear path (K2, analytic d(v), one warp per wall) --------------
+// ---- the fused nonlinear path (K2w, analytic d(v), one warp per wall) -------------
+constexpr int kSplitWallsMax = 148;   // one CTA per SM at most
+
+template <int NPT, int M>
+void launch_dv_walls_m(const NonlinearSegArgs& a, int m, cudaStream_t s) {
+    if constexpr (M <= NPT) {
+        if (m != M) return launch_dv_walls_m<NPT, M + 1>(a, m, s);
+        const int grid = (a.n_walls + kDvWarps - 1) / kDvWarps;
+        k_dv_walls<NPT, M><<<grid, kDvWarps * 32, 0, s>>>(a);
+    }
+}
+
+template <int NW>
+void launch_dv_split(const NonlinearSegArgs& a, int nw, cudaStream_t s) {
+    if constexpr (NW <= 8) {
+        if (nw != NW) return launch_dv_split<NW + 1>(a, nw, s);
+        k_dv_wall_split<NW><<<a.n_walls, NW * 32, 0, s>>>(a);
+    }
+}
+
+// n <= 256.  Fewer walls than SMs: K2s (a wall over ceil(n/32) warps, latency).
+// Otherwise K2w: NPT = the smallest power of two with 32 NPT >= n, M = nodes of
+// the reversed lane.
+void launch_dv_walls(const NonlinearSegArgs& a, int n, cudaStream_t s) {
+    if (a.n_walls <= kSplitWallsMax) return launch_dv_split<1>(a, (n + 31) / 32, s);
+    const int npt = n <= 32 ? 1 : n <= 64 ? 2 : n <= 128 ? 4 : 8;
+    const int m = n - (n - 1) / npt * npt;
+    switch (npt) {
+        case 1: launch_dv_walls_m<1, 1>(a, m, s); break;
+        case 2: launch_dv_walls_m<2, 1>(a, m, s); break;
+        case 4: launch_dv_walls_m<4, 1>(a, m, s); break;
+        default: launch_dv_walls_m<8, 1>(a, m, s); break;
+    }
+}
+
 int advance_nonlinear(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
     const int nch = std::max<int>(1, static_cast<int>(c->channels.size()));
     const int64_t block = 1 << 18;
@@ -834,8 +869,7 @@ int advance_nonlinear(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status)
                 a.out[i] = c->s64[1 - from][i];
             }
             LaunchScope ls(c, "df_analytic_fused", static_cast<double>(c->cells()) * len);
-            if (c->n <= 130) k_df_analytic_walls<130, 128><<<c->n_walls, 160, 0, c->stream>>>(a);
-            else if (c->n <= 258) k_df_analytic_walls<258, 256><<<c->n_walls, 288, 0, c->stream>>>(a);
+            if (c->n <= 32 * 8) launch_dv_walls(a, c->n, c->stream);
             else k_df_analytic_walls<1024, 256><<<c->n_walls, 288, 0, c->stream>>>(a);
         }
         HYG_CUDA(cudaGetLastError());
@@ -861,7 +895,8 @@ int advance_nonlinear(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status)
 }
 
 // ---- the temporally blocked long-wall path (K3, analytic d(v), one wall) ----------
-constexpr int kTileT = 992, kTileS = 16, kTileThreads = 256;   // W = T + 2S = 4 x 256
+constexpr int kTileNPT = 8;             // K3w: W = 256-node windows, S = 8 steps per launch
+constexpr int kTileS = kTileNPT;
 
 int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
     const int nch = std::max<int>(1, static_cast<int>(c->channels.size()));
@@ -890,8 +925,12 @@ int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
         a.br = c->biot[1];
         a.stop = c->d_flag;
         a.suspect = c->d_flag;
-        const int grid = static_cast<int>((c->n + kTileT - 1) / kTileT);
-        const int smem = 5 * (kTileT + 2 * kTileS) * static_cast<int>(sizeof(double));
+        using G = DvTiles<kTileNPT>;
+        const int64_t tr = G::rface(c->n);
+        const int grid = static_cast<int>((tr + kDvWarps - 1) / kDvWarps);
+        // cells owned by the face windows (window 0 and t >= tr) and by the interior ones
+        const double face_cells = static_cast<double>(G::W - kTileNPT) + static_cast<double>(c->n - (tr * G::T + kTileNPT));
+        const double mid_cells = static_cast<double>(c->cells()) - face_cells;
         const int cur0 = c->cur;
         int nseg = 0;
         for (int64_t s0 = 0; s0 < rows; s0 += kTileS, ++nseg) {
@@ -903,8 +942,12 @@ int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
                 a.in[i] = c->s64[from][i];
                 a.out[i] = c->s64[1 - from][i];
             }
-            LaunchScope ls(c, "df_analytic_tiled", static_cast<double>(c->cells()) * a.steps);
-            k_df_analytic_tiled<kTileT, kTileS, kTileThreads><<<grid, kTileThreads, smem, c->stream>>>(a);
+            {
+                LaunchScope ls(c, "df_analytic_tiled", mid_cells * a.steps);
+                k_dv_tiled<kTileNPT, false><<<grid, kDvWarps * 32, 0, c->stream>>>(a);
+            }
+            LaunchScope ls(c, "df_analytic_tiled_faces", face_cells * a.steps);
+            k_dv_tiled<kTileNPT, true><<<1, kDvWarps * 32, 0, c->stream>>>(a);
         }
         HYG_CUDA(cudaGetLastError());
         int flag = 0;
@@ -2066,7 +2109,7 @@ namespace {
 __global__ void k_fastmath(int n, const double* x, double* e, double* r) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
-        e[i] = fexp(x[i]);
+        e[i] = fexp(x[i], kExp2Tab64);
         r[i] = frcp(x[i]);
     }
 }

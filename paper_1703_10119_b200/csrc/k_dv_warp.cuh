@@ -1,0 +1,420 @@
+// k_dv_warp.cuh — register-resident nonlinear DF marches for the analytic
+// d(v) functor (HYG_COEFF_ANALYTIC_D): a warp owns a whole wall (configs[0]
+// and batches of short walls, K2w) or a window of one long wall that it
+// advances NPT steps per launch (configs[4], K3w).
+//
+// Replaces: df_step_nonlinear (/root/reference/proj/src/wall.cpp:196-264) with
+// StarTables (wall.cpp:89-138) for the d(v) functor, called per step from
+// run()/step_explicit (building.cpp:166-177, 325-337); guard as check_bounded
+// (building.cpp:282-300).
+//
+// Layout (as K1, k_coupled.cuh): lane l holds NPT consecutive nodes of the
+// four layers in registers; neighbours across lanes come from shuffles, so a
+// step needs no shared memory and no barrier.  The last live lane holds its
+// M nodes in REVERSED order, so both faces sit in register 0 (lane 0 and the
+// last lane) and only register 0 carries the face row.  In register order a
+// node's successor is register j+1, or for the last register the next lane's
+// first node (shuffle down) — for the reversed lane the previous lane's last
+// node (shuffle up).  The rows are symmetric in their two neighbours, so the
+// reversed lane runs the same code.
+//
+// Per step and lane: the half-node coefficients h_j = d((v_j + v_succ(j))/2)
+// once each (h of the previous lane's last half node by one shuffle), then the
+// rows of wall.cpp:213-217 / 231-240 in increment form around layer n-1 (a
+// uniform state at ambient values is a fixed point bit for bit):
+//   v:  vn = vp + 2a (kp (vR - vp) + km (vL - vp)) / (1 + a (kp + km))
+//   u:  un = up + B (uL + uR - 2 up) + G (vL + vR - (vn + vp)) - Gm (vn - vp)
+//       with B = 2b/(1+2b), G = 2g/(1+2b), Gm = gamma/(1+2b)
+// and the face rows of wall.cpp:218-229, 241-259 (analytic_face) in register
+// 0 of the face lanes, with the ghost-side coefficient d(v_face) (node value).
+// Cost: 38 FP64 instructions per interior node-update (16 of them the half
+// node: fexp is 10), against ~55 in the shared-memory kernels.
+//
+// K3w temporal blocking: a window of W = 32 NPT nodes, S = NPT steps per
+// launch.  An artificial window edge (not a real face) contaminates one node
+// per step, so after S steps exactly lane 0 and lane 31 are stale: a middle
+// window owns lanes 1..30 (T = 30 NPT nodes).  The first window starts at the
+// left face (owns lanes 0..30), the last ends at the right face.  Traffic per
+// launch: 32 W + 32 T bytes for T S updates (8.3 B/update at NPT = 8; NPT = 12
+// or 16 would halve it but exceed 255 registers).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "k_nonlinear.cuh"
+#include "k_tiled.cuh"
+
+namespace hyg {
+
+// d(v) = 1 + p0 v + p1 exp(-p2 (v - p3)^2) at a half node, from the SUM of its
+// two node values (midpoint = sum/2 is exact; e and p0 v round as the
+// reference's midpoint form).  For a node value pass 2 v.
+struct DvParams { double hp0, np2, p3, p1; };
+
+__device__ __forceinline__ DvParams dv_params(const double* p) {
+    return DvParams{0.5 * p[0], -p[2], p[3], p[1]};
+}
+
+__device__ __forceinline__ double d_half(const DvParams& q, double sum, const double* tab) {
+    const double e = fma(0.5, sum, -q.p3);
+    const double E = fexp((q.np2 * e) * e, tab);
+    return fma(q.p1, E, fma(q.hp0, sum, 1.0));
+}
+
+// Interior-row constants of one wall (wall.cpp:199-204).
+struct DvRow { double a, a2, B, G, Gm; };
+
+__device__ __forceinline__ DvRow dv_row(const AnalyticRow& r) {
+    return DvRow{r.a, 2.0 * r.a, 2.0 * r.b * r.inv_u, 2.0 * r.g * r.inv_u, r.gamma * r.inv_u};
+}
+
+__device__ __forceinline__ void dv_interior(const DvRow& r, double vp, double up, double vL, double vR,
+                                            double uL, double uR, double km, double kp, double& vn,
+                                            double& un) {
+    // symmetric in (L, R) and never contracted (__dmul_rn): a node rounds the
+    // same in a reversed lane as in a normal one, so every window computes it
+    // bit for bit alike
+    const double num = __dadd_rn(__dmul_rn(km, vL - vp), __dmul_rn(kp, vR - vp));
+    const double den = fma(r.a, kp + km, 1.0);
+    vn = fma(r.a2 * num, frcp(den), vp);
+    const double du = fma(-2.0, up, uL + uR);
+    const double w = (vL + vR) - (vn + vp);
+    un = fma(-r.Gm, vn - vp, fma(r.G, w, fma(r.B, du, up)));
+}
+
+// Face row (wall.cpp:218-229, 241-259; analytic_face) with the per-lane
+// constants folded once: the u row's denominator is a per-wall constant.
+struct DvFace { double a, a2, cpl1, cpl2, ag4, dx2, BiM, b4, cplu2, gamma, b2r, b4dx, BiTM, g2, inv_fu; };
+
+__device__ __forceinline__ DvFace dv_face_consts(const AnalyticRow& r, const Biot& fb) {
+    DvFace f;
+    const double cpl = 2.0 * r.a * r.dx * fb.Bi_M;
+    const double cplu = 2.0 * r.b * r.dx * fb.Bi_TT;
+    f.a = r.a;
+    f.a2 = 2.0 * r.a;
+    f.cpl1 = 1.0 + cpl;
+    f.cpl2 = 2.0 * cpl;
+    f.ag4 = 4.0 * r.a * r.dx;
+    f.dx2 = 2.0 * r.dx;
+    f.BiM = fb.Bi_M;
+    f.b4 = 4.0 * r.b;
+    f.cplu2 = 2.0 * cplu;
+    f.gamma = r.gamma;
+    f.b2r = 2.0 * r.b * r.ratio;
+    f.b4dx = 4.0 * r.b * r.dx;
+    f.BiTM = fb.Bi_TM;
+    f.g2 = 2.0 * r.g;
+    f.inv_fu = 1.0 / (1.0 + 2.0 * r.b + cplu);
+    return f;
+}
+
+// vcn, ucn: the interior neighbour; km_b = d(v_face) (ghost side), kp_b = the
+// half node next to the face.
+__device__ __forceinline__ void dv_face(const DvFace& f, const Ambient& am, double vp, double up, double vcn,
+                                        double ucn, double km_b, double kp_b, double& vn, double& un) {
+    const double S = kp_b + km_b;
+    const double rk = frcp(km_b);                      // off the v row's chain
+    vn = vp + (f.a2 * S * (vcn - vp) + f.cpl2 * (am.v - vp) + f.ag4 * am.g) * frcp(fma(f.a, S, f.cpl1));
+    const double vbar = 0.5 * (vn + vp);
+    const double vg = vcn - (f.dx2 * rk) * (f.BiM * (vbar - am.v) - am.g);
+    un = up + (f.b4 * (ucn - up) + f.cplu2 * (am.u - up) - f.gamma * (vn - vp) + f.b2r * (vcn - vg) -
+               f.b4dx * (f.BiTM * (vbar - am.v) - am.q) + f.g2 * (vcn + vg) - f.g2 * (vn + vp)) *
+              f.inv_fu;
+}
+
+struct DvLane {
+    bool rev;       // registers hold nodes in reversed order (last live lane / lane 31)
+    bool mirror0;   // register 0's outer neighbour is the mirrored inner one
+    bool face;      // register 0 is a real face (FACES steps only)
+};
+
+// One DF step of this lane's NPT nodes: P holds layer n-1 on entry and n+1 on
+// exit, C holds layer n.  M = live registers of the reversed lane.  FACES: the
+// warp holds a real face (uniform per warp): register 0 also runs the face row.
+template <int NPT, int M, bool FACES>
+__device__ __forceinline__ void dv_step(double (&vP)[NPT], const double (&vC)[NPT], double (&uP)[NPT],
+                                        const double (&uC)[NPT], const DvLane& L, const DvRow& r,
+                                        const DvFace& fc, const DvParams& q, const double* tab,
+                                        const Ambient& am, unsigned& acc) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const double vs = L.rev ? vC[M - 1] : vC[0];       // this lane's lowest node
+    const double us = L.rev ? uC[M - 1] : uC[0];
+    const double vup = __shfl_up_sync(FULL, vC[NPT - 1], 1);
+    const double uup = __shfl_up_sync(FULL, uC[NPT - 1], 1);
+    const double vdn = __shfl_down_sync(FULL, vs, 1);
+    const double udn = __shfl_down_sync(FULL, us, 1);
+    double vN[NPT], uN[NPT];                           // register-order successors
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+        if (M < NPT && j == M - 1) {
+            vN[j] = L.rev ? vup : vC[j + 1];
+            uN[j] = L.rev ? uup : uC[j + 1];
+        } else if (j == NPT - 1) {
+            vN[j] = (M == NPT && L.rev) ? vup : vdn;
+            uN[j] = (M == NPT && L.rev) ? uup : udn;
+        } else {
+            vN[j] = vC[j + 1];
+            uN[j] = uC[j + 1];
+        }
+    }
+    const double hl = d_half(q, vC[NPT - 1] + vN[NPT - 1], tab);
+    double hprev = __shfl_up_sync(FULL, hl, 1);        // half node left of register 0
+    const double dnode = FACES ? d_half(q, vC[0] + vC[0], tab) : 0.0;   // ghost side: node value
+    const double vx0 = L.mirror0 ? vN[0] : vup;
+    const double ux0 = L.mirror0 ? uN[0] : uup;
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+        const double hj = j == NPT - 1 ? hl : d_half(q, vC[j] + vN[j], tab);
+        double vn, un;
+        dv_interior(r, vP[j], uP[j], j == 0 ? vx0 : vC[j - 1], vN[j], j == 0 ? ux0 : uC[j - 1], uN[j], hprev, hj,
+                    vn, un);
+        if (FACES && j == 0) {
+            double vf, uf;
+            dv_face(fc, am, vP[0], uP[0], vN[0], uN[0], dnode, hj, vf, uf);
+            vn = L.face ? vf : vn;
+            un = L.face ? uf : un;
+        }
+        const unsigned g = static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn));
+        if (j < M) acc |= g;
+        else acc |= L.rev ? 0u : g;                    // dead registers of the reversed lane
+        vP[j] = vn;
+        uP[j] = un;
+        hprev = hj;
+    }
+}
+
+constexpr int kDvWarps = 4;     // walls (K2w) or windows (K3w) per CTA
+
+// K2w: one warp per wall, n <= 32 NPT, all steps of a segment in one launch.
+// The host picks NPT = the smallest power of two >= n/32 and M = n - Lr NPT
+// (Lr = (n-1)/NPT, the reversed lane).
+template <int NPT, int M>
+__global__ void __launch_bounds__(kDvWarps * 32) k_dv_walls(const NonlinearSegArgs A) {
+    __shared__ double s_tab[64];
+    __shared__ Ambient s_amb[kDvWarps][kNlChunk][2];   // [warp][step][face]
+    if (*A.stop) return;
+    stage_exp_table(s_tab, threadIdx.x, blockDim.x);
+    __syncthreads();
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int w = blockIdx.x * kDvWarps + warp;
+    if (w >= A.n_walls) return;                        // whole warp
+    const int n = A.n;
+    const int Lr = (n - 1) / NPT;
+    const bool live = lane <= Lr;
+    DvLane L;
+    L.rev = lane == Lr;
+    L.face = lane == 0 || L.rev;
+    L.mirror0 = L.face;
+    const size_t o = static_cast<size_t>(w) * n;
+    double up[NPT], uc[NPT], vp[NPT], vc[NPT];
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+        const bool ok = live && (!L.rev || j < M);
+        const size_t i = o + (L.rev ? n - 1 - j : lane * NPT + j);
+        up[j] = ok ? A.in[0][i] : 1.0;
+        uc[j] = ok ? A.in[1][i] : 1.0;
+        vp[j] = ok ? A.in[2][i] : 1.0;
+        vc[j] = ok ? A.in[3][i] : 1.0;
+    }
+    const AnalyticRow rc = analytic_row(A.groups[w], A.dx, A.dt);
+    const DvRow r = dv_row(rc);
+    const DvParams q = dv_params(A.p);
+    const int f = L.rev ? 1 : 0;
+    const DvFace fc = dv_face_consts(rc, A.biot[2 * w + f]);
+    const int chl = A.chan[2 * w], chr = A.chan[2 * w + 1];
+    unsigned acc = 0;
+    for (int c0 = 0; c0 < A.nsteps; c0 += kNlChunk) {
+        const int clen = min(kNlChunk, A.nsteps - c0);
+        __syncwarp();
+        for (int i = lane; i < 2 * clen; i += 32)
+            s_amb[warp][i >> 1][i & 1] = A.table[static_cast<size_t>(c0 + (i >> 1)) * A.n_channels + ((i & 1) ? chr : chl)];
+        __syncwarp();
+        int s = 0;
+        for (; s + 1 < clen; s += 2) {
+            dv_step<NPT, M, true>(vp, vc, up, uc, L, r, fc, q, s_tab, s_amb[warp][s][f], acc);
+            dv_step<NPT, M, true>(vc, vp, uc, up, L, r, fc, q, s_tab, s_amb[warp][s + 1][f], acc);
+        }
+        if (s < clen) {   // odd tail (last chunk only): rotate by copies
+            dv_step<NPT, M, true>(vp, vc, up, uc, L, r, fc, q, s_tab, s_amb[warp][s][f], acc);
+#pragma unroll
+            for (int j = 0; j < NPT; ++j) {
+                double t = vp[j]; vp[j] = vc[j]; vc[j] = t;
+                t = up[j]; up[j] = uc[j]; uc[j] = t;
+            }
+        }
+    }
+    // fast guard verdict (bit 30 of the high word: |x| >= 2 or not finite)
+    const unsigned any = __reduce_or_sync(0xffffffffu, live ? acc : 0u);
+    if ((any & 0x40000000u) && lane == 0) atomicCAS(A.suspect, 0, A.seg_index + 1);
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+        if (!live || (L.rev && j >= M)) continue;
+        const size_t i = o + (L.rev ? n - 1 - j : lane * NPT + j);
+        A.out[0][i] = up[j];
+        A.out[1][i] = uc[j];
+        A.out[2][i] = vp[j];
+        A.out[3][i] = vc[j];
+    }
+}
+
+// K2s: one wall split over NW warps, one node per lane, for walls too few to
+// fill the GPU (configs[0]: a single 101-node wall).  The march is then bound
+// by the per-step dependency chain of one warp's in-order instruction stream;
+// splitting the wall over NW warps (one per scheduler) cuts that stream NW
+// ways.  Neighbours inside a warp come from shuffles, across warps through
+// shared memory (double-buffered by step parity) behind one barrier per step.
+// Each lane evaluates both of its half nodes (the shared one is computed
+// twice, bit for bit alike: the sum commutes), so no second exchange is
+// needed.  Only the warps holding a face run the face row (warp-uniform).
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) k_dv_wall_split(const NonlinearSegArgs A) {
+    constexpr bool FACE_ALL = NW <= 4;                 // every warp runs the face code: no branch
+    __shared__ double s_tab[64];
+    __shared__ Ambient s_amb[kNlChunk][2];
+    __shared__ double s_x[2][NW][4];                  // [parity][warp] {v, u} of lanes 0 and 31
+    if (*A.stop) return;
+    stage_exp_table(s_tab, threadIdx.x, blockDim.x);
+    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+    const int w = blockIdx.x, n = A.n, j = tid;
+    const bool live = j < n;
+    const bool lf = j == 0, rf = j == n - 1;
+    const bool face_warp = warp == 0 || warp == (n - 1) / 32;
+    const size_t o = static_cast<size_t>(w) * n + j;
+    double up = live ? A.in[0][o] : 1.0, uc = live ? A.in[1][o] : 1.0;
+    double vp = live ? A.in[2][o] : 1.0, vc = live ? A.in[3][o] : 1.0;
+    const AnalyticRow rc = analytic_row(A.groups[w], A.dx, A.dt);
+    const DvRow r = dv_row(rc);
+    const DvParams q = dv_params(A.p);
+    const DvFace fc = dv_face_consts(rc, A.biot[2 * w + (rf ? 1 : 0)]);
+    const int chl = A.chan[2 * w], chr = A.chan[2 * w + 1];
+    constexpr unsigned FULL = 0xffffffffu;
+    unsigned acc = 0;
+    for (int c0 = 0; c0 < A.nsteps; c0 += kNlChunk) {
+        const int clen = min(kNlChunk, A.nsteps - c0);
+        __syncthreads();
+        for (int i = tid; i < 2 * clen; i += NW * 32)
+            s_amb[i >> 1][i & 1] = A.table[static_cast<size_t>(c0 + (i >> 1)) * A.n_channels + ((i & 1) ? chr : chl)];
+        for (int s = 0; s < clen; ++s) {
+            const int b = s & 1;
+            if (lane == 0) { s_x[b][warp][0] = vc; s_x[b][warp][1] = uc; }
+            if (lane == 31) { s_x[b][warp][2] = vc; s_x[b][warp][3] = uc; }
+            __syncthreads();
+            double vL = __shfl_up_sync(FULL, vc, 1), uL = __shfl_up_sync(FULL, uc, 1);
+            double vR = __shfl_down_sync(FULL, vc, 1), uR = __shfl_down_sync(FULL, uc, 1);
+            if (lane == 0 && warp > 0) { vL = s_x[b][warp - 1][2]; uL = s_x[b][warp - 1][3]; }
+            if (lane == 31 && warp < NW - 1) { vR = s_x[b][warp + 1][0]; uR = s_x[b][warp + 1][1]; }
+            const double hL = d_half(q, vL + vc, s_tab);
+            const double hR = d_half(q, vc + vR, s_tab);
+            double vn, un;
+            dv_interior(r, vp, up, vL, vR, uL, uR, hL, hR, vn, un);
+            if (FACE_ALL || face_warp) {
+                // branch-free inside the warp: the face chain runs beside the
+                // interior one, not after it.  Ghost side d(v_face); the row
+                // needs the interior neighbour only.
+                const double dnode = d_half(q, vc + vc, s_tab);
+                double vf, uf;
+                dv_face(fc, s_amb[s][rf ? 1 : 0], vp, up, rf ? vL : vR, rf ? uL : uR, dnode, rf ? hL : hR, vf, uf);
+                vn = (lf || rf) ? vf : vn;
+                un = (lf || rf) ? uf : un;
+            }
+            acc |= live ? (static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn))) : 0u;
+            up = uc;
+            vp = vc;
+            uc = un;
+            vc = vn;
+        }
+    }
+    const unsigned any = __reduce_or_sync(FULL, acc);
+    if ((any & 0x40000000u) && lane == 0) atomicCAS(A.suspect, 0, A.seg_index + 1);
+    if (live) {
+        A.out[0][o] = up;
+        A.out[1][o] = uc;
+        A.out[2][o] = vp;
+        A.out[3][o] = vc;
+    }
+}
+
+// K3w window geometry (n >= 32 NPT): window t starts at min(t T, n - W) and
+// owns [t == 0 ? 0 : t T + NPT, min(t T + 31 NPT, n)).  Window 0 holds the
+// left face, windows t >= rface(n) end at the right face (at most three).
+template <int NPT>
+struct DvTiles {
+    static constexpr int W = 32 * NPT, T = W - 2 * NPT;
+    static __host__ __device__ int64_t count(int64_t n) { return (n - NPT + T - 1) / T; }
+    static __host__ __device__ int64_t rface(int64_t n) { return (n - W + T - 1) / T; }
+};
+
+// K3w: one warp per window, A.steps <= NPT steps per launch.  FACES = false:
+// the interior windows 1 .. rface-1 (no face code, fewer registers); FACES =
+// true: one CTA for window 0 and the right-face windows.
+template <int NPT, bool FACES>
+__global__ void __launch_bounds__(kDvWarps * 32) k_dv_tiled(const TiledArgs A) {
+    using G = DvTiles<NPT>;
+    constexpr int W = G::W, T = G::T;
+    __shared__ double s_tab[64];
+    if (*A.stop) return;
+    stage_exp_table(s_tab, threadIdx.x, blockDim.x);
+    __syncthreads();
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t n = A.n;
+    const int64_t tr = G::rface(n);
+    int64_t t;
+    if (FACES) {
+        t = warp == 0 ? 0 : tr + warp - 1;
+        if (warp > 0 && (t <= 0 || t >= G::count(n))) return;
+    } else {
+        t = static_cast<int64_t>(blockIdx.x) * kDvWarps + warp;
+        if (t == 0 || t >= tr) return;
+    }
+    const int64_t own0 = t == 0 ? 0 : t * T + NPT;
+    const int64_t own1 = min(t * T + 31 * NPT, n);
+    const int64_t g0 = min(t * T, n - W);
+    const bool lf = FACES && g0 == 0, rf = FACES && g0 + W == n;
+    DvLane L;
+    L.rev = lane == 31;
+    L.mirror0 = (lane == 0 && lf) || L.rev;
+    L.face = (lane == 0 && lf) || (L.rev && rf);
+    const bool guard = (lane != 0 || lf) && (lane != 31 || rf);   // stale lanes stay out
+    double up[NPT], uc[NPT], vp[NPT], vc[NPT];
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+        const int64_t i = g0 + (L.rev ? W - 1 - j : lane * NPT + j);
+        up[j] = A.in[0][i];
+        uc[j] = A.in[1][i];
+        vp[j] = A.in[2][i];
+        vc[j] = A.in[3][i];
+    }
+    const AnalyticRow rc = analytic_row(A.groups, A.dx, A.dt);
+    const DvRow r = dv_row(rc);
+    const DvParams q = dv_params(A.p);
+    const DvFace fc = dv_face_consts(rc, L.rev ? A.br : A.bl);
+    const int ch = L.rev ? A.chr : A.chl;
+    unsigned acc = 0;
+    auto amb = [&](int k) { return FACES ? A.table[static_cast<size_t>(k) * A.n_channels + ch] : Ambient{}; };
+    int k = 0;
+    for (; k + 1 < A.steps; k += 2) {
+        dv_step<NPT, NPT, FACES>(vp, vc, up, uc, L, r, fc, q, s_tab, amb(k), acc);
+        dv_step<NPT, NPT, FACES>(vc, vp, uc, up, L, r, fc, q, s_tab, amb(k + 1), acc);
+    }
+    if (k < A.steps) {
+        dv_step<NPT, NPT, FACES>(vp, vc, up, uc, L, r, fc, q, s_tab, amb(k), acc);
+#pragma unroll
+        for (int j = 0; j < NPT; ++j) {
+            double x = vp[j]; vp[j] = vc[j]; vc[j] = x;
+            x = up[j]; up[j] = uc[j]; uc[j] = x;
+        }
+    }
+    const unsigned any = __reduce_or_sync(0xffffffffu, guard ? acc : 0u);
+    if ((any & 0x40000000u) && lane == 0) atomicCAS(A.suspect, 0, A.seg_index + 1);
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+        const int64_t i = g0 + (L.rev ? W - 1 - j : lane * NPT + j);
+        if (i < own0 || i >= own1) continue;
+        A.out[0][i] = up[j];
+        A.out[1][i] = uc[j];
+        A.out[2][i] = vp[j];
+        A.out[3][i] = vc[j];
+    }
+}
+
+}  // namespace hyg

@@ -47,9 +47,14 @@ struct NonlinearSegArgs {
     int* suspect;
 };
 
-__device__ __forceinline__ double d_of(const double* p, double v) {
+__device__ __forceinline__ double d_of(const double* p, double v, const double* tab) {
     const double e = v - p[3];
-    return 1.0 + p[0] * v + p[1] * fexp(-p[2] * e * e);
+    return 1.0 + p[0] * v + p[1] * fexp(-p[2] * e * e, tab);
+}
+
+// Stage the 2^(j/64) table of fexp into shared memory (call before a barrier).
+__device__ __forceinline__ void stage_exp_table(double* s_tab, int tid, int nthreads) {
+    for (int i = tid; i < 64; i += nthreads) s_tab[i] = kExp2Tab64[i];
 }
 
 constexpr int kNlChunk = 64;   // forcing rows staged per chunk
@@ -105,9 +110,11 @@ __global__ void __launch_bounds__(IT + 32) k_df_analytic_walls(const NonlinearSe
     constexpr int THREADS = IT + 32;
     __shared__ double s_lay[4][MAXN];            // up, uc, vp, vc (roles rotate)
     __shared__ Ambient s_amb[kNlChunk][2];       // [step][face]
+    __shared__ double s_tab[64];
     if (*A.stop) return;
     const int w = blockIdx.x, tid = threadIdx.x, n = A.n;
     const size_t o = static_cast<size_t>(w) * n;
+    stage_exp_table(s_tab, tid, THREADS);
     for (int j = tid; j < n; j += THREADS) {
         s_lay[0][j] = A.in[0][o + j];
         s_lay[1][j] = A.in[1][o + j];
@@ -147,7 +154,7 @@ __global__ void __launch_bounds__(IT + 32) k_df_analytic_walls(const NonlinearSe
                     const double vL = vc[j - 1], vR = vc[j + 1];
                     double vn, un;
                     analytic_interior(rc, vpj, upj, vL, vR, uc[j - 1], uc[j + 1],
-                                      d_of(p, 0.5 * (vL + vcj)), d_of(p, 0.5 * (vcj + vR)), vn, un);
+                                      d_of(p, 0.5 * (vL + vcj), s_tab), d_of(p, 0.5 * (vcj + vR), s_tab), vn, un);
                     acc |= static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn));
                     vp[j] = vn;     // layer n-1 slot becomes layer n+1
                     up[j] = un;
@@ -158,8 +165,8 @@ __global__ void __launch_bounds__(IT + 32) k_df_analytic_walls(const NonlinearSe
                 const int jn = left ? 1 : n - 2;
                 const double vcj = vc[j], vcn = vc[jn];
                 double vn, un;
-                analytic_face(rc, fb, s_amb[s][flane], vp[j], up[j], vcn, uc[jn], d_of(p, vcj),
-                              d_of(p, 0.5 * (vcj + vcn)), vn, un);
+                analytic_face(rc, fb, s_amb[s][flane], vp[j], up[j], vcn, uc[jn], d_of(p, vcj, s_tab),
+                              d_of(p, 0.5 * (vcj + vcn), s_tab), vn, un);
                 acc |= static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn));
                 vp[j] = vn;
                 up[j] = un;

@@ -50,6 +50,7 @@ template <int W, int THREADS>
 struct TileCtx {
     double (*lay)[W];          // [4][W] in shared memory
     double* kp;                // [W]
+    const double* tab;         // [64] exp table
     int lmin, lmax, lf, rf;    // real-node range, face slots (-1 if absent)
     int tid;
 };
@@ -70,7 +71,7 @@ __device__ __forceinline__ void tiled_step(const TileCtx<W, THREADS>& c, const T
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
         const int i = c.tid + q * THREADS;
-        const double kv = d_of(p, 0.5 * (vc[i] + vc[min(i + 1, W - 1)]));
+        const double kv = d_of(p, 0.5 * (vc[i] + vc[min(i + 1, W - 1)]), c.tab);
         if (i >= h0 && i < h1) c.kp[i] = kv;
     }
     __syncthreads();
@@ -100,7 +101,7 @@ __device__ __forceinline__ void tiled_step(const TileCtx<W, THREADS>& c, const T
             const int jn = left ? j + 1 : j - 1;
             double vn, un;
             analytic_face(rc, left ? A.bl : A.br, row[left ? A.chl : A.chr], vp[j], up[j], vc[jn], uc[jn],
-                          d_of(p, vc[j]), c.kp[left ? j : j - 1], vn, un);
+                          d_of(p, vc[j], c.tab), c.kp[left ? j : j - 1], vn, un);
             acc |= static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn));
             vp[j] = vn;
             up[j] = un;
@@ -114,10 +115,13 @@ __global__ void __launch_bounds__(THREADS) k_df_analytic_tiled(const TiledArgs A
     constexpr int W = T + 2 * S;
     static_assert(W % THREADS == 0, "window must split evenly over the threads");
     extern __shared__ double sm[];           // lay[4][W], kp[W]
+    __shared__ double s_tab[64];
     if (*A.stop) return;
+    stage_exp_table(s_tab, threadIdx.x, THREADS);
     TileCtx<W, THREADS> c;
     c.lay = reinterpret_cast<double(*)[W]>(sm);
     c.kp = sm + 4 * W;
+    c.tab = s_tab;
     c.tid = threadIdx.x;
     const int64_t n = A.n;
     const int64_t g0 = static_cast<int64_t>(blockIdx.x) * T - S;   // global index of local 0

@@ -257,3 +257,30 @@ def test_advance_with_per_call_dt_fp64():
     got = gpu_run(model, init, 1500, "implicit", dt_schedule=sched)
     ref = oracle_run("oracle", model, init, 1500, "implicit", dt_schedule=sched)
     assert rel_linf(got, ref) <= TOL64
+
+
+@pytest.mark.parametrize("n_walls,n_nodes", [(1, 101), (3, 256), (5, 17), (2, 33), (300, 101), (200, 256),
+                                             (160, 33), (150, 64), (170, 200), (149, 7)])
+def test_dv_wall_batches(n_walls, n_nodes):
+    """Coupled d(v) walls with random groups, Biot numbers and imposed fluxes
+    through K2s (n_walls <= 148: a wall over ceil(n/32) warps) and K2w (one
+    warp per wall, every NPT x reversed-lane width M), explicit start."""
+    model, init = random_walls(n_walls, n_nodes, seed=n_nodes + n_walls, flux=True)
+    # cfg1's Fo_M range times d(v) ~ 50 diverges in the reference arithmetic too
+    # (frozen-coefficient DF with coupled u): scale Fo_M into a bounded regime
+    model.groups = model.groups.copy()
+    model.groups[:, :3] *= np.array([1e-3, 1e-2, 1e-2])
+    model.coeff_kind = "analytic_d"
+    model.coeff_params = workloads.D_PARAMS
+    nsteps = 400
+    with Context(model) as ctx:
+        ctx.profiling(True)
+        ctx.set_state(**init)
+        ctx.bootstrap("explicit")
+        ctx.advance(nsteps - 1)
+        got = ctx.get_state()
+        names = {s["name"] for s in ctx.kernel_stats() if s["launches"] > 0}
+    assert "df_analytic_fused" in names, names
+    assert "df_step_general" not in names, names       # no fallback to the per-step path
+    ref = oracle_run("oracle", model, init, nsteps, "explicit")
+    assert rel_linf(got, ref) <= TOL64
