@@ -53,9 +53,10 @@ CONFIGS = {
     # (64 B x 5376 owned + 32 B x 756 halo nodes) / (5376 x 8) = 8.56 B/update
     "cfg3": dict(flop=14.1, bytes=8.56, bound="hbm", kernel="ring_tiled", scaling="strong", dtype="f64",
                  run_steps=80_000),
-    # cfg4 at N=1 runs the temporally blocked K3 (~4.06 B/update at T=1024, S=16),
-    # so min(HBM, FP64) is the FP64 side; sharded (N>1) it streams 48 B/update
-    "cfg4": dict(flop=33, bytes=4.06, bound="fp64", kernel="df_analytic_tiled", scaling="strong", dtype="f64",
+    # cfg4 runs the temporally blocked K3w (k_dv_warp.cuh: 256-node windows, 8 steps
+    # per launch, (32 x 256 + 32 x 240) / (240 x 8) = 8.27 B/update), so min(HBM,
+    # FP64) is the FP64 side; sharded (N>1) every slab runs K3w too
+    "cfg4": dict(flop=33, bytes=8.27, bound="fp64", kernel="df_analytic_tiled", scaling="strong", dtype="f64",
                  run_steps=10_000),
     # beyond BASELINE's five: load-bearing material walls,
     # k_material_step: 2 strict evaluations x 82 flop (exp/log/pow/div = 1, the

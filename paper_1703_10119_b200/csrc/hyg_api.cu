@@ -21,7 +21,6 @@
 #include "k_coupled.cuh"
 #include "k_step.cuh"
 #include "k_nonlinear.cuh"
-#include "k_tiled.cuh"
 #include "k_dv_warp.cuh"
 #include "k_material.cuh"
 #include "k_ring.cuh"
@@ -927,7 +926,17 @@ int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
         a.suspect = c->d_flag;
         using G = DvTiles<kTileNPT>;
         const int64_t tr = G::rface(c->n);
-        const int grid = static_cast<int>((tr + kDvWarps - 1) / kDvWarps);
+        // persistent interior kernel: as many CTAs as fit at once (each warp
+        // walks the windows with a stride of all warps), 16-byte stores need
+        // 16-byte aligned windows: T and NPT even, the buffers 256-byte aligned
+        static int per_sm = 0, n_sm = 0;
+        if (!per_sm) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dv_tiled_stream<kTileNPT>, kDvWarps * 32, 0);
+            cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, c->device);
+            per_sm = std::max(per_sm, 1);
+        }
+        const int grid = static_cast<int>(std::min<int64_t>((tr - 1 + kDvWarps - 1) / kDvWarps,
+                                                            static_cast<int64_t>(per_sm) * n_sm));
         // cells owned by the face windows (window 0 and t >= tr) and by the interior ones
         const double face_cells = static_cast<double>(G::W - kTileNPT) + static_cast<double>(c->n - (tr * G::T + kTileNPT));
         const double mid_cells = static_cast<double>(c->cells()) - face_cells;
@@ -944,7 +953,7 @@ int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
             }
             {
                 LaunchScope ls(c, "df_analytic_tiled", mid_cells * a.steps);
-                k_dv_tiled<kTileNPT, false><<<grid, kDvWarps * 32, 0, c->stream>>>(a);
+                if (grid > 0) k_dv_tiled_stream<kTileNPT><<<grid, kDvWarps * 32, 0, c->stream>>>(a);
             }
             LaunchScope ls(c, "df_analytic_tiled_faces", face_cells * a.steps);
             k_dv_tiled<kTileNPT, true><<<1, kDvWarps * 32, 0, c->stream>>>(a);

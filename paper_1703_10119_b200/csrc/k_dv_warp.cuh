@@ -42,9 +42,25 @@
 #include <cuda_runtime.h>
 
 #include "k_nonlinear.cuh"
-#include "k_tiled.cuh"
 
 namespace hyg {
+
+// One launch of the long-wall march (K3w): A.steps <= NPT steps over all nodes.
+struct TiledArgs {
+    int64_t n;                 // nodes of the wall
+    int steps;                 // <= NPT
+    int n_channels, chl, chr;
+    int seg_index;
+    double dx, dt;
+    double p[4];
+    Groups groups;
+    Biot bl, br;
+    const Ambient* table;      // [steps][n_channels] rows of this launch
+    const double* in[4];
+    double* out[4];
+    const int* stop;
+    int* suspect;
+};
 
 // d(v) = 1 + p0 v + p1 exp(-p2 (v - p3)^2) at a half node, from the SUM of its
 // two node values (midpoint = sum/2 is exact; e and p0 v round as the
@@ -415,6 +431,100 @@ __global__ void __launch_bounds__(kDvWarps * 32) k_dv_tiled(const TiledArgs A) {
         A.out[2][i] = vp[j];
         A.out[3][i] = vc[j];
     }
+}
+
+__device__ __forceinline__ void dv_cp_async8(double* smem, const double* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void dv_cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void dv_cp_async_wait() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// K3w interior windows, persistent: each warp marches windows t, t + stride, ...
+// (stride = all warps of the grid) and prefetches its next window into its own
+// shared-memory buffer with cp.async while it computes the current one, so
+// the window loads leave the critical path.  Buffer layout per field: lane
+// block l of NPT nodes, node j of the block at l NPT + (j ^ (l mod NPT)) (XOR
+// swizzle: the per-register reads of a warp spread over the banks).
+template <int NPT>
+__global__ void __launch_bounds__(kDvWarps * 32) k_dv_tiled_stream(const TiledArgs A) {
+    using G = DvTiles<NPT>;
+    constexpr int W = G::W, T = G::T;
+    static_assert((NPT & (NPT - 1)) == 0, "NPT must be a power of two");
+    __shared__ double s_tab[64];
+    __shared__ __align__(16) double s_buf[kDvWarps][4][W];
+    if (*A.stop) return;
+    stage_exp_table(s_tab, threadIdx.x, blockDim.x);
+    __syncthreads();
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t tr = G::rface(A.n);
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * kDvWarps;
+    int64_t t = 1 + static_cast<int64_t>(blockIdx.x) * kDvWarps + warp;
+    if (t >= tr) return;
+    double(*buf)[W] = s_buf[warp];
+    auto swz = [](int i) { return (i & ~(NPT - 1)) | ((i ^ (i / NPT)) & (NPT - 1)); };
+    auto prefetch = [&](int64_t tt) {
+        const int64_t g0 = tt * T;
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+            for (int k = 0; k < W / 32; ++k) {
+                const int i = lane + 32 * k;
+                dv_cp_async8(&buf[f][swz(i)], A.in[f] + g0 + i);
+            }
+        dv_cp_async_commit();
+    };
+    prefetch(t);
+    const AnalyticRow rc = analytic_row(A.groups, A.dx, A.dt);
+    const DvRow r = dv_row(rc);
+    const DvParams q = dv_params(A.p);
+    const DvFace fc{};
+    DvLane L;
+    L.rev = lane == 31;
+    L.mirror0 = L.rev;
+    L.face = false;
+    const bool store = lane != 0 && lane != 31;      // the stale lanes stay out of the guard and the output
+    unsigned acc = 0;
+    for (; t < tr; t += stride) {
+        double up[NPT], uc[NPT], vp[NPT], vc[NPT];
+        dv_cp_async_wait();
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < NPT; ++j) {
+            const int i = swz(L.rev ? W - 1 - j : lane * NPT + j);
+            up[j] = buf[0][i];
+            uc[j] = buf[1][i];
+            vp[j] = buf[2][i];
+            vc[j] = buf[3][i];
+        }
+        __syncwarp();
+        if (t + stride < tr) prefetch(t + stride);
+        int k = 0;
+        for (; k + 1 < A.steps; k += 2) {
+            dv_step<NPT, NPT, false>(vp, vc, up, uc, L, r, fc, q, s_tab, Ambient{}, acc);
+            dv_step<NPT, NPT, false>(vc, vp, uc, up, L, r, fc, q, s_tab, Ambient{}, acc);
+        }
+        if (k < A.steps) {
+            dv_step<NPT, NPT, false>(vp, vc, up, uc, L, r, fc, q, s_tab, Ambient{}, acc);
+#pragma unroll
+            for (int j = 0; j < NPT; ++j) {
+                double x = vp[j]; vp[j] = vc[j]; vc[j] = x;
+                x = up[j]; up[j] = uc[j]; uc[j] = x;
+            }
+        }
+        if (store) {   // lanes 1..30: NPT consecutive owned nodes, 16-byte stores
+            const int64_t i0 = t * T + lane * NPT;
+#pragma unroll
+            for (int j = 0; j < NPT; j += 2) {
+                reinterpret_cast<double2*>(A.out[0] + i0)[j / 2] = make_double2(up[j], up[j + 1]);
+                reinterpret_cast<double2*>(A.out[1] + i0)[j / 2] = make_double2(uc[j], uc[j + 1]);
+                reinterpret_cast<double2*>(A.out[2] + i0)[j / 2] = make_double2(vp[j], vp[j + 1]);
+                reinterpret_cast<double2*>(A.out[3] + i0)[j / 2] = make_double2(vc[j], vc[j + 1]);
+            }
+        }
+    }
+    const unsigned any = __reduce_or_sync(0xffffffffu, store ? acc : 0u);
+    if ((any & 0x40000000u) && lane == 0) atomicCAS(A.suspect, 0, A.seg_index + 1);
 }
 
 }  // namespace hyg
