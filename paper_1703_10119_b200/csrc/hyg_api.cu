@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -24,6 +25,7 @@
 #include "k_dv_warp.cuh"
 #include "k_material.cuh"
 #include "k_ring.cuh"
+#include "k_ring_reg.cuh"
 
 using namespace hyg;
 
@@ -199,6 +201,8 @@ struct hyg_ctx {
     bool has_rad = false;
     bool ring = false;               // K4: zone-ring temporal blocking applies
     int ring_W = 0, ring_B = 0;
+    int ring_reg_B = 0;              // K4r (registers + prefetch): zones per CTA, 0 if not applicable
+    double* d_ring_zp = nullptr;     // K4r per-zone parameter blocks [zones][kRingZP]
     int rad_groups = 0, rad_terms = 0;
     int *d_rad_tgt = nullptr, *d_rad_grp = nullptr;
     double *d_rad_num = nullptr, *d_rad_den = nullptr, *d_rad_coef = nullptr, *d_qrad = nullptr;
@@ -979,7 +983,22 @@ int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
     return HYG_OK;
 }
 
-// ---- the zone-ring temporally blocked path (K4) ---------------------------------
+// ---- the zone-ring temporally blocked path (K4, K4r) -----------------------------
+template <int NPT>
+void launch_ring_reg(const RingArgs& a, int threads, size_t smem, cudaStream_t s, int device) {
+    auto k = k_ring_reg<NPT, kRingS>;
+    static int n_sm = 0;
+    if (!n_sm) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device);
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem);
+    const int nblk = (a.n_zones + a.B - 1) / a.B;
+    const int grid = std::max(1, std::min(nblk, std::max(per_sm, 1) * n_sm));
+    k<<<grid, threads, smem, s>>>(a);
+}
+
 template <int NPT>
 void launch_ring(const RingArgs& a, int grid, int threads, size_t smem, cudaStream_t s) {
     auto k = k_ring_tiled<NPT, kRingS>;
@@ -991,7 +1010,7 @@ void launch_ring(const RingArgs& a, int grid, int threads, size_t smem, cudaStre
     k<<<grid, threads, smem, s>>>(a);
 }
 
-int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
+int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool reg = true) {
     if (c->coef_dt != dt) {
         LaunchScope ls(c, "coupled_coef", 0.0);
         k_coupled_coef<<<(c->n_walls + 127) / 128, 128, 0, c->stream>>>(c->n_walls, c->dx, dt, c->d_groups,
@@ -1000,10 +1019,16 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
     }
     const int nch = std::max<int>(1, static_cast<int>(c->channels.size()));
     const int nsrc = static_cast<int>(c->zsrc.size() / 3);
-    const int Z = static_cast<int>(c->zones.size()), W = c->ring_W, B = c->ring_B, npt = c->n / 16;
+    // K4r needs the fast guard (norm >= 2: a clear bit 30 proves |x| < 2); a
+    // flagged K4r launch is replayed by K4 and its exact guard
+    reg = reg && c->ring_reg_B > 0 && c->norm >= 2.0;
+    const int Z = static_cast<int>(c->zones.size()), W = c->ring_W, npt = c->n / 16;
+    const int B = reg ? c->ring_reg_B : c->ring_B;
     const int grid = (Z + B - 1) / B;
-    const int threads = RingShape<8, kRingS>::threads(B, W);
-    const size_t smem = npt == 4 ? RingShape<4, kRingS>::smem_bytes(B, W, nch, nsrc)
+    const int rw = RingShape<8, kRingS>::row_width(nch, nsrc);
+    const int threads = reg ? RingRegShape<8, kRingS>::threads(B, W) : RingShape<8, kRingS>::threads(B, W);
+    const size_t smem = reg ? RingRegShape<8, kRingS>::smem_doubles(B, W, c->n, rw) * sizeof(double)
+                        : npt == 4 ? RingShape<4, kRingS>::smem_bytes(B, W, nch, nsrc)
                         : npt == 8 ? RingShape<8, kRingS>::smem_bytes(B, W, nch, nsrc)
                                    : RingShape<16, kRingS>::smem_bytes(B, W, nch, nsrc);
     const int64_t block = 65536 / kRingS * kRingS;
@@ -1035,6 +1060,7 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
         a.zones = c->d_zones;
         a.links = c->d_zlinks;
         a.inz = c->d_inz;
+        a.zparams = c->d_ring_zp;
         a.stop = c->d_flag;
         const int cur0 = c->cur, z0 = c->zcur;
         int nseg = 0;
@@ -1052,8 +1078,11 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
             a.zv_in = c->zv[zf];
             a.zu_out = c->zu[1 - zf];
             a.zv_out = c->zv[1 - zf];
-            LaunchScope ls(c, "ring_tiled", static_cast<double>(c->cells()) * a.steps);
-            if (npt == 4) launch_ring<4>(a, grid, threads, smem, c->stream);
+            LaunchScope ls(c, reg ? "ring_reg" : "ring_tiled", static_cast<double>(c->cells()) * a.steps);
+            if (reg) {
+                if (npt == 4) launch_ring_reg<4>(a, threads, smem, c->stream, c->device);
+                else launch_ring_reg<8>(a, threads, smem, c->stream, c->device);
+            } else if (npt == 4) launch_ring<4>(a, grid, threads, smem, c->stream);
             else if (npt == 8) launch_ring<8>(a, grid, threads, smem, c->stream);
             else launch_ring<16>(a, grid, threads, smem, c->stream);
         }
@@ -1069,12 +1098,14 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
             done += rows;
             continue;
         }
-        // the guard fired in launch K (its input intact): exact per-step path from there
+        // the guard fired in launch K (its input intact): K4r -> K4 (exact guard)
+        // from there, K4 -> the exact per-step path
         const int64_t k0 = static_cast<int64_t>(flag - 1) * kRingS;
         c->cur = (cur0 + flag - 1) & 1;
         c->zcur = (z0 + flag - 1) & 1;
         c->t = times[k0];
         c->layer += k0;
+        if (reg) return advance_ring(c, nsteps - done - k0, dt, status, false);
         return advance_general(c, nsteps - done - k0, dt, status);
     }
     return HYG_OK;
@@ -1376,6 +1407,17 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
                 return sm <= 227u * 1024u && th <= 896;
             };
             while (B > 0 && !fits(B)) --B;
+            if (B >= 1 && (npt == 4 || npt == 8)) {
+                // K4r: the largest block whose roles fit 512 threads (128 registers each)
+                int Br = std::min(Z, 32 - 2 * kRingS);
+                auto fits_r = [&](int b) {
+                    const int rw = RingShape<8, kRingS>::row_width(nch, nsrc);
+                    return RingRegShape<8, kRingS>::threads(b, W) <= 512 &&
+                           RingRegShape<8, kRingS>::smem_doubles(b, W, c->n, rw) * sizeof(double) <= 227u * 1024u;
+                };
+                while (Br > 0 && !fits_r(Br)) --Br;
+                c->ring_reg_B = Br;
+            }
             if (B >= 1) {
                 c->ring = true;
                 c->ring_W = W;
@@ -1460,6 +1502,37 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
             cudaMemcpy(c->d_zlinks, c->zlinks.data(), sizeof(ZoneLinkDev) * c->zlinks.size(), cudaMemcpyHostToDevice);
         if (!c->inz.empty())
             cudaMemcpy(c->d_inz, c->inz.data(), sizeof(InzLinkDev) * c->inz.size(), cudaMemcpyHostToDevice);
+        if (c->ring_reg_B > 0) {
+            // K4r's per-zone parameter blocks (k_ring_reg.cuh), prefetched with the walls
+            std::vector<double> zp(c->zones.size() * kRingZP, 0.0);
+            for (size_t z = 0; z < c->zones.size(); ++z) {
+                const ZoneDev& d = c->zones[z];
+                double* b = &zp[z * kRingZP];
+                b[0] = 1.0 + d.kappa_a_tt1;
+                b[1] = d.g_v;
+                b[2] = d.q_v1;
+                b[3] = d.q_v2;
+                b[4] = d.wall_end - d.wall_begin;
+                b[5] = d.inz_end - d.inz_begin;
+                b[6] = d.sources;
+                for (int q = 0; q < d.wall_end - d.wall_begin; ++q) {
+                    const ZoneLinkDev& l = c->zlinks[d.wall_begin + q];
+                    b[8 + 4 * q] = l.wall - static_cast<int>(z) * c->ring_W;
+                    b[9 + 4 * q] = l.Bi_TT * l.theta_T;
+                    b[10 + 4 * q] = l.Bi_TM * l.theta_T;
+                    b[11 + 4 * q] = d.sign * l.Bi_M * l.theta_M;
+                }
+                for (int q = 0; q < d.inz_end - d.inz_begin; ++q) {
+                    const InzLinkDev& l = c->inz[d.inz_begin + q];
+                    b[40 + 4 * q] = l.peer;
+                    b[41 + 4 * q] = l.g_inz;
+                    b[42 + 4 * q] = l.q_inz1;
+                    b[43 + 4 * q] = l.q_inz2;
+                }
+            }
+            if (cudaMalloc(&c->d_ring_zp, sizeof(double) * zp.size()) != cudaSuccess) return fail("zone alloc");
+            cudaMemcpy(c->d_ring_zp, zp.data(), sizeof(double) * zp.size(), cudaMemcpyHostToDevice);
+        }
     }
     // WallField::uniform (wall.cpp:24-31) and ZoneState{} (zone.hpp:11-14): all 1
     {
@@ -1501,6 +1574,7 @@ void hyg_destroy(hyg_ctx* c) {
     cudaFree(c->d_zones);
     cudaFree(c->d_zlinks);
     cudaFree(c->d_inz);
+    cudaFree(c->d_ring_zp);
     cudaFree(c->d_table);
     cudaFree(c->d_boot);
     cudaFree(c->d_src);

@@ -48,6 +48,7 @@ struct RingArgs {
     const ZoneDev* zones;
     const ZoneLinkDev* links;
     const InzLinkDev* inz;
+    const double* zparams;         // K4r: per-zone parameter blocks [n_zones][kRingZP]
     const double* in[4];           // up, uc, vp, vc (layer k-1, k)
     double* out[4];
     const double* zu_in;

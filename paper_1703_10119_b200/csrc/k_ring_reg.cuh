@@ -1,0 +1,422 @@
+// k_ring_reg.cuh — K4r: the zone-ring temporal blocking of K4 (k_ring.cuh)
+// with the owned walls in registers and a persistent, prefetching CTA
+// (configs[3]: 8,192 zones x 6 constant walls x 128 nodes).
+//
+// Replaces S consecutive step_explicit calls (building.cpp:152-187) exactly as
+// K4 does — same decomposition, same rows, same zone arithmetic — but:
+//   * owned walls: K1's layout (k_coupled.cuh): 16 lanes x NPT nodes per wall,
+//     two walls per warp, the four layers in registers, neighbours by shuffles,
+//     the last lane reversed so both faces sit in register 0 (face 0: the
+//     exterior channel, face 1: the wall's zone air of the current layer);
+//   * halo walls (the last S+1 nodes of the walls of the S-1 zones on each
+//     side, cut end stale one node per step) and the zone air ODEs: one thread
+//     per halo wall (its S+1 nodes in registers) and one per local zone;
+//   * one barrier per step: surface samples and zone air go through two small
+//     shared arrays double-buffered by step parity;
+//   * persistent: a CTA walks the zone blocks blockIdx.x, +gridDim.x, ... and
+//     while it marches one block in registers, the next block's owned walls
+//     arrive in a shared staging buffer by four 1-D bulk copies (TMA engine,
+//     one contiguous range per field, completion on an mbarrier), its halo
+//     walls, zone parameter blocks and zone air by cp.async (the load leaves
+//     the step loop's critical path); results go out as 16-byte stores.
+// Guard: K1's fast guard (bit 30 of the high word: |x| >= 2 or not finite) over
+// the owned walls and zones; a set bit stops the following launches and the
+// host replays from the flagged launch with K4, whose exact guard reports the
+// reference's first failing layer.  Used for divergence_norm >= 2 only.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "k_ring.cuh"
+
+namespace hyg {
+
+template <int NPT, int S>
+struct RingRegShape {
+    static constexpr int kP = S + 1;                           // nodes kept per halo wall
+    static constexpr int kHaloZones = 2 * (S - 1);
+    __host__ __device__ static int own_warps(int B, int W) { return (B * W + 1) / 2; }
+    __host__ __device__ static int halo_walls(int W) { return kHaloZones * W; }
+    __host__ __device__ static int halo_warps(int W) { return (halo_walls(W) + 31) / 32; }
+    __host__ __device__ static int threads(int B, int W) { return 32 * (own_warps(B, W) + halo_warps(W) + 1); }
+    __host__ __device__ static int local_zones(int B) { return B + 2 * S; }
+    // doubles: staging of the owned walls (one bulk copy per field) and of the
+    // halo walls, of the zone parameters and zone air (double-buffered by block
+    // parity), the per-step surfaces [2][2][B W + halo] and zone air
+    // [2][2][local], forcing rows, and the mbarrier of the owned-wall copies
+    __host__ __device__ static size_t smem_doubles(int B, int W, int n, int rw) {
+        const size_t LB = local_zones(B);
+        return static_cast<size_t>(4) * B * W * n + static_cast<size_t>(4) * halo_walls(W) * kP +
+               2 * LB * kRingZP + 4 * LB + 4 * static_cast<size_t>(B * W + halo_walls(W)) + 4 * LB +
+               static_cast<size_t>(S) * rw + 1;
+    }
+};
+
+// 1-D bulk copies (TMA engine) and their mbarrier
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(void* mb, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(mb)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(void* mb, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(void* mb, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n RING_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra RING_WAIT_%=;\n}\n" ::"r"(smem_u32(mb)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, void* mb) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(mb))
+                 : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(double* smem_dst, const double* gsrc) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
+}
+
+template <int NPT, int S>
+__global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
+    using Sh = RingRegShape<NPT, S>;
+    constexpr int P = Sh::kP, N = 16 * NPT;
+    constexpr unsigned FULL = 0xffffffffu;
+    extern __shared__ double smem[];
+    if (*a.stop) return;
+    const int W = a.W, B = a.B, Z = a.n_zones;
+    const int OW = B * W, HW = Sh::halo_walls(W), LB = Sh::local_zones(B);
+    const int rw = RingShape<NPT, S>::row_width(a.n_channels, a.n_sources);
+    // shared layout (integer offsets; every access a shared-space access)
+    const int oSO = 0;                                  // staging owned [4][OW][N] (linear: bulk copies)
+    const int oSH = oSO + 4 * OW * N;                   // staging halo [4][HW][P]
+    const int oZS = oSH + 4 * HW * P;                   // staged zone parameters [2][LB][kRingZP]
+    const int oZA = oZS + 2 * LB * kRingZP;             // staged zone air [2][2][LB]
+    const int oSF = oZA + 4 * LB;                       // surfaces [parity][field][OW + HW]
+    const int oAR = oSF + 4 * (OW + HW);                // zone air [parity][field][LB]
+    const int oRW = oAR + 4 * LB;                       // forcing rows [S][rw]
+    const int oMB = oRW + S * rw;                       // mbarrier of the owned-wall bulk copies
+    void* mbar = &smem[oMB];
+    auto so_ix = [&](int f, int i) { return oSO + f * OW * N + i; };
+    auto sf_ix = [&](int par, int f, int i) { return oSF + (par * 2 + f) * (OW + HW) + i; };
+    auto ar_ix = [&](int par, int f, int i) { return oAR + (par * 2 + f) * LB + i; };
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int nblk = (Z + B - 1) / B;
+
+    for (int i = tid; i < a.steps * rw; i += nthr) {    // forcing rows of this launch (all blocks)
+        const int k = i / rw, r = i - k * rw;
+        smem[oRW + i] = r < 4 * a.n_channels
+                            ? reinterpret_cast<const double*>(a.table + static_cast<size_t>(k) * a.n_channels)[r]
+                            : a.src[static_cast<size_t>(k) * (3 * a.n_sources + 2) + (r - 4 * a.n_channels)];
+    }
+    auto gz = [&](int z0, int i) { return ((z0 - S + i) % Z + Z) % Z; };
+    auto halo_local = [&](int hz, int nown) { return hz < S - 1 ? 1 + hz : S + nown + (hz - (S - 1)); };
+    // prefetch of block b (zone parameters and air into parity par)
+    auto prefetch = [&](int b, int par) {
+        const int z0 = b * B, nown = min(B, Z - z0), L = nown + 2 * S;
+        if (tid == 0) {   // the owned walls of the block: one contiguous range per field
+            const unsigned bytes = static_cast<unsigned>(nown * W * N * sizeof(double));
+            mbar_expect_tx(mbar, 4 * bytes);
+#pragma unroll
+            for (int f = 0; f < 4; ++f)
+                bulk_g2s(&smem[so_ix(f, 0)], a.in[f] + static_cast<size_t>(z0) * W * N, bytes, mbar);
+        }
+        for (int i = tid; i < HW * P; i += nthr) {
+            const int hl = i / P, p = i - hl * P;
+            const int hz = hl / W, wi = hl - hz * W;
+            const size_t g = (static_cast<size_t>(gz(z0, halo_local(hz, nown))) * W + wi) * N + (N - P + p);
+#pragma unroll
+            for (int f = 0; f < 4; ++f) cp_async8(&smem[oSH + f * HW * P + i], a.in[f] + g);
+        }
+        for (int i = tid; i < L * (kRingZP / 2); i += nthr) {
+            const int li = i / (kRingZP / 2), c = i - li * (kRingZP / 2);
+            cp_async16(&smem[oZS + (par * LB + li) * kRingZP + 2 * c],
+                       a.zparams + static_cast<size_t>(gz(z0, li)) * kRingZP + 2 * c);
+        }
+        for (int i = tid; i < 2 * L; i += nthr) {
+            const int f = i / L, li = i - f * L;
+            cp_async8(&smem[oZA + (par * 2 + f) * LB + li], (f ? a.zv_in : a.zu_in) + gz(z0, li));
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    if (tid == 0) {
+        mbar_init(mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (static_cast<int>(blockIdx.x) < nblk) prefetch(blockIdx.x, 0);
+
+    // ---- roles ------------------------------------------------------------------------
+    const int warp = tid / 32, lane = tid % 32;
+    const int own_w = Sh::own_warps(B, W), halo_w = Sh::halo_warps(W);
+    const bool is_own = warp < own_w, is_halo = !is_own && warp < own_w + halo_w;
+    unsigned acc = 0;
+
+    for (int b = blockIdx.x, it = 0; b < nblk; b += gridDim.x, ++it) {
+        const int z0 = b * B, nown = min(B, Z - z0);
+        const int L = nown + 2 * S;
+        const int par = it & 1;
+        const bool next = b + static_cast<int>(gridDim.x) < nblk;
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        mbar_wait(mbar, it & 1);                         // the owned walls of block b landed
+        __syncthreads();                                 // staging of block b complete
+        int cur = 0;                                     // parity of the layer-k shared slots
+        if (is_own) {
+            // owned wall wl (two per warp), 16 lanes of NPT nodes, last lane reversed
+            const int wl = warp * 2 + lane / 16, sub = lane % 16;
+            const bool live = wl < nown * W;
+            const int wlc = live ? wl : 0;
+            const int w = z0 * W + wlc;
+            const bool first = sub == 0, rev = sub == 15, mirror0 = first || rev;
+            const int li = S + wlc / W;                  // local zone of face 1
+            double up[NPT], uc[NPT], vp[NPT], vc[NPT];
+            const int d0 = wlc * N + sub * NPT;          // this lane's NPT consecutive nodes
+            auto rd = [&](int f, double (&x)[NPT]) {     // 16-byte loads; the reversed lane by selects
+                double t[NPT];
+#pragma unroll
+                for (int q = 0; q < NPT; q += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(&smem[so_ix(f, d0 + q)]);
+                    t[q] = v.x;
+                    t[q + 1] = v.y;
+                }
+#pragma unroll
+                for (int q = 0; q < NPT; ++q) x[q] = rev ? t[NPT - 1 - q] : t[q];
+            };
+            rd(0, up);
+            rd(1, uc);
+            rd(2, vp);
+            rd(3, vc);
+            __syncthreads();                             // (A) staging consumed by every role
+            if (next) prefetch(b + gridDim.x, par ^ 1);
+            const WallCoef& wc = a.coef[w];
+            const double cb = wc.in.b, csu = wc.in.c_su, csv = wc.in.c_sv;
+            // register 0's face-capable row (interior coefficients, zero face terms elsewhere)
+            double fe = 0, fb = cb, feg = 0, fctv = 0, fcsv = csv, fctu = 0, fcsu = csu, fcq = 0, fcg = 0;
+            if (mirror0) {
+                const RowCoef& c = wc.face[first ? 0 : 1];
+                fe = c.e; fb = c.b; feg = c.e_g; fctv = c.c_tv; fcsv = c.c_sv; fctu = c.c_tu; fcsu = c.c_su;
+                fcq = c.c_q; fcg = c.c_g;
+            }
+            const int ch = a.attach[2 * w].index;
+            if (rev && live) {                           // layer-k surface sample (node N-1)
+                smem[sf_ix(0, 0, wl)] = uc[0];
+                smem[sf_ix(0, 1, wl)] = vc[0];
+            }
+            __syncthreads();                             // (B) layer-k surfaces and air published
+            auto step = [&](double (&vP)[NPT], double (&vC)[NPT], double (&uP)[NPT], double (&uC)[NPT], int k) {
+                // face inputs of register 0, branch-free (wall.cpp:162-169, 177-189;
+                // coupled_node): x=0 the exterior channel, x=1 the zone's layer-k air
+                const int am = oRW + k * rw + 4 * ch;
+                const double ru = smem[am + 0], rv = smem[am + 1], rg = smem[am + 2], rq = smem[am + 3] + 0.0;
+                const double au = smem[ar_ix(cur, 0, li)], av = smem[ar_ix(cur, 1, li)];
+                const double u_inf = first ? ru : au, v_inf = first ? rv : av;
+                const double g_inf = first ? rg : 0.0, q_inf = first ? rq : 0.0;
+                const double vs = rev ? vC[NPT - 1] : vC[0], us = rev ? uC[NPT - 1] : uC[0];
+                const double vup = __shfl_up_sync(FULL, vC[NPT - 1], 1, 16);
+                const double uup = __shfl_up_sync(FULL, uC[NPT - 1], 1, 16);
+                const double vdn = __shfl_down_sync(FULL, vs, 1, 16);
+                const double udn = __shfl_down_sync(FULL, us, 1, 16);
+                const double vx0 = mirror0 ? vC[1] : vup, ux0 = mirror0 ? uC[1] : uup;
+                const double vx1 = rev ? vup : vdn, ux1 = rev ? uup : udn;
+#pragma unroll
+                for (int q = 0; q < NPT; ++q) {
+                    const double vl = q == 0 ? vx0 : vC[q - 1], ul = q == 0 ? ux0 : uC[q - 1];
+                    const double vr = q == NPT - 1 ? vx1 : vC[q + 1], ur = q == NPT - 1 ? ux1 : uC[q + 1];
+                    const double d = fma(-2.0, vP[q], vl + vr);
+                    const double du = fma(-2.0, uP[q], ul + ur);
+                    double vn, un;
+                    if (q == 0) {
+                        const double t = v_inf - vP[0], tu = u_inf - uP[0];
+                        vn = fma(fe, t, fma(fb, d, fma(feg, g_inf, vP[0])));
+                        un = fma(fctv, t, fma(fcsv, d, fma(fctu, tu, fma(fcsu, du, fma(fcq, q_inf, fma(fcg, g_inf, uP[0]))))));
+                    } else {
+                        vn = fma(cb, d, vP[q]);
+                        un = fma(csv, d, fma(csu, du, uP[q]));
+                    }
+                    acc |= live ? (static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn))) : 0u;
+                    vP[q] = vn;
+                    uP[q] = un;
+                }
+                if (rev && live) {
+                    smem[sf_ix(cur ^ 1, 0, wl)] = uP[0];
+                    smem[sf_ix(cur ^ 1, 1, wl)] = vP[0];
+                }
+                __syncthreads();
+                cur ^= 1;
+            };
+            int k = 0;
+            for (; k + 1 < a.steps; k += 2) {
+                step(vp, vc, up, uc, k);
+                step(vc, vp, uc, up, k + 1);
+            }
+            if (k < a.steps) {
+                step(vp, vc, up, uc, k);
+#pragma unroll
+                for (int q = 0; q < NPT; ++q) {
+                    double x = vp[q]; vp[q] = vc[q]; vc[q] = x;
+                    x = up[q]; up[q] = uc[q]; uc[q] = x;
+                }
+            }
+            if (live) {                                  // out = (layer k+S-1, layer k+S), 16-byte stores
+                const size_t g0 = static_cast<size_t>(w) * N + sub * NPT;
+#pragma unroll
+                for (int q = 0; q < NPT; q += 2) {
+                    // registers q, q+1 hold nodes g0+q, g0+q+1 (reversed lane: the mirrored pair)
+                    const size_t g = g0 + q;
+                    auto pr = [&](const double (&x)[NPT]) {   // selects: no runtime register index
+                        return rev ? make_double2(x[NPT - 1 - q], x[NPT - 2 - q]) : make_double2(x[q], x[q + 1]);
+                    };
+                    reinterpret_cast<double2*>(a.out[0] + g)[0] = pr(up);
+                    reinterpret_cast<double2*>(a.out[1] + g)[0] = pr(uc);
+                    reinterpret_cast<double2*>(a.out[2] + g)[0] = pr(vp);
+                    reinterpret_cast<double2*>(a.out[3] + g)[0] = pr(vc);
+                }
+            }
+        } else if (is_halo) {
+            // halo wall: global nodes N-P .. N-1; the cut end (p = 0) mirrors
+            // itself — its error moves inward one node per step and never
+            // reaches the face node within S steps
+            const int hl = (warp - own_w) * 32 + lane;
+            const bool live = hl < HW;
+            const int hlc = live ? hl : 0;
+            const int hz = hlc / W, wi = hlc - hz * W;
+            const int li = halo_local(hz, nown);
+            const int w = gz(z0, li) * W + wi;
+            double up[P], uc[P], vp[P], vc[P];
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                const int d = hlc * P + p;
+                up[p] = smem[oSH + 0 * HW * P + d];
+                uc[p] = smem[oSH + 1 * HW * P + d];
+                vp[p] = smem[oSH + 2 * HW * P + d];
+                vc[p] = smem[oSH + 3 * HW * P + d];
+            }
+            __syncthreads();                             // (A)
+            if (next) prefetch(b + gridDim.x, par ^ 1);
+            const double cb = a.coef[w].in.b, csu = a.coef[w].in.c_su, csv = a.coef[w].in.c_sv;
+            const RowCoef c = a.coef[w].face[1];
+            if (live) {
+                smem[sf_ix(0, 0, OW + hl)] = uc[P - 1];
+                smem[sf_ix(0, 1, OW + hl)] = vc[P - 1];
+            }
+            __syncthreads();                             // (B)
+            auto step = [&](double (&vP)[P], double (&vC)[P], double (&uP)[P], double (&uC)[P]) {
+                const double u_a = smem[ar_ix(cur, 0, li)], v_a = smem[ar_ix(cur, 1, li)];
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const double vl = p == 0 ? vC[0] : vC[p - 1], ul = p == 0 ? uC[0] : uC[p - 1];
+                    const double vr = p == P - 1 ? vC[P - 2] : vC[p + 1], ur = p == P - 1 ? uC[P - 2] : uC[p + 1];
+                    const double d = fma(-2.0, vP[p], vl + vr);
+                    const double du = fma(-2.0, uP[p], ul + ur);
+                    double vn, un;
+                    if (p < P - 1) {
+                        vn = fma(cb, d, vP[p]);
+                        un = fma(csv, d, fma(csu, du, uP[p]));
+                    } else {
+                        const double t = v_a - vP[p], tu = u_a - uP[p];
+                        vn = fma(c.e, t, fma(c.b, d, fma(c.e_g, 0.0, vP[p])));
+                        un = fma(c.c_tv, t, fma(c.c_sv, d, fma(c.c_tu, tu, fma(c.c_su, du, fma(c.c_q, 0.0,
+                                                                                            fma(c.c_g, 0.0, uP[p]))))));
+                    }
+                    vP[p] = vn;
+                    uP[p] = un;
+                }
+                if (live) {
+                    smem[sf_ix(cur ^ 1, 0, OW + hl)] = uP[P - 1];
+                    smem[sf_ix(cur ^ 1, 1, OW + hl)] = vP[P - 1];
+                }
+                __syncthreads();
+                cur ^= 1;
+            };
+            int k = 0;
+            for (; k + 1 < a.steps; k += 2) {
+                step(vp, vc, up, uc);
+                step(vc, vp, uc, up);
+            }
+            if (k < a.steps) step(vp, vc, up, uc);
+        } else {
+            // zone thread i: zone_step_explicit (zone.cpp:69-74) of local zone i
+            // (1 .. L-2 live; 0 and L-1 contribute their layer-0 air only), with
+            // the staged parameter block [0] 1 + kappa, [1] g_v, [2] q_v1, [3] q_v2,
+            // [4] #links, [5] #peers, [6] source, links [8 + 4q] = (wall in zone,
+            // Bi_TT theta_T, Bi_TM theta_T, sign Bi_M theta_M), peers [40 + 4q] =
+            // (peer zone, g_inz, q_inz1, q_inz2)
+            const int i = lane;
+            const bool valid = i < L;
+            const bool live = i >= 1 && i < L - 1;
+            const bool owned = i >= S && i < S + nown;
+            const int hz = i < S ? i - 1 : (S - 1) + (i - S - nown);
+            const int zp = oZS + (par * LB + (valid ? i : 0)) * kRingZP;
+            int nlink = 0, npeer = 0, sidx = 0;
+            int ls[kRingMaxLinks], pidx[kRingMaxPeers];
+            if (live) {
+                nlink = static_cast<int>(smem[zp + 4]);
+                npeer = static_cast<int>(smem[zp + 5]);
+                sidx = static_cast<int>(smem[zp + 6]);
+            }
+#pragma unroll
+            for (int q = 0; q < kRingMaxLinks; ++q) {
+                const int wi = q < nlink ? static_cast<int>(smem[zp + 8 + 4 * q]) : 0;
+                ls[q] = owned ? (i - S) * W + wi : OW + hz * W + wi;
+            }
+#pragma unroll
+            for (int q = 0; q < kRingMaxPeers; ++q) {
+                const int pg = q < npeer ? static_cast<int>(smem[zp + 40 + 4 * q]) : -1;
+                pidx[q] = i >= 1 && gz(z0, i - 1) == pg ? i - 1 : i + 1;   // the adjacent copy
+            }
+            if (valid) {
+                smem[ar_ix(0, 0, i)] = smem[oZA + (par * 2 + 0) * LB + i];
+                smem[ar_ix(0, 1, i)] = smem[oZA + (par * 2 + 1) * LB + i];
+            }
+            __syncthreads();                             // (A) staging consumed
+            if (next) prefetch(b + gridDim.x, par ^ 1);
+            __syncthreads();                             // (B) layer-k surfaces and air published
+            for (int k = 0; k < a.steps; ++k) {
+                if (live) {
+                    const double u_a = smem[ar_ix(cur, 0, i)], v_a = smem[ar_ix(cur, 1, i)];
+                    const int srow = oRW + k * rw + 4 * a.n_channels;
+                    const int sz = srow + 3 * sidx;
+                    const double u_inf = smem[srow + 3 * a.n_sources + 0], v_inf = smem[srow + 3 * a.n_sources + 1];
+                    double du = smem[sz + 1] + smem[sz + 2] + smem[zp + 2] * (u_inf * v_inf - u_a * v_a) +
+                                smem[zp + 3] * (u_inf - u_a);
+                    double dv = smem[sz + 0] + smem[zp + 1] * (v_inf - v_a);
+#pragma unroll
+                    for (int q = 0; q < kRingMaxPeers; ++q) {
+                        if (q < npeer) {
+                            const double pu = smem[ar_ix(cur, 0, pidx[q])], pv = smem[ar_ix(cur, 1, pidx[q])];
+                            du += smem[zp + 42 + 4 * q] * (pu * pv - u_a * v_a) + smem[zp + 43 + 4 * q] * (pu - u_a);
+                            dv += smem[zp + 41 + 4 * q] * (pv - v_a);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < kRingMaxLinks; ++q) {
+                        if (q < nlink) {
+                            const double us = smem[sf_ix(cur, 0, ls[q])], vs = smem[sf_ix(cur, 1, ls[q])];
+                            du += smem[zp + 9 + 4 * q] * (us - u_a) + smem[zp + 10 + 4 * q] * (vs - v_a);
+                            dv += smem[zp + 11 + 4 * q] * (v_a - vs);
+                        }
+                    }
+                    const double nu = u_a + a.dt * (du / smem[zp + 0]);
+                    const double nv = v_a + a.dt * dv;
+                    smem[ar_ix(cur ^ 1, 0, i)] = nu;
+                    smem[ar_ix(cur ^ 1, 1, i)] = nv;
+                    if (owned) acc |= static_cast<unsigned>(__double2hiint(nu)) | static_cast<unsigned>(__double2hiint(nv));
+                }
+                __syncthreads();
+                cur ^= 1;
+            }
+            if (owned) {
+                const int z = gz(z0, i);
+                a.zu_out[z] = smem[ar_ix(cur, 0, i)];
+                a.zv_out[z] = smem[ar_ix(cur, 1, i)];
+            }
+        }
+        __syncthreads();                                 // the shared slots are reused by the next block
+    }
+    // fast guard verdict of the whole launch (bit 30: |x| >= 2 or not finite)
+    if (__syncthreads_or((acc & 0x40000000u) != 0u) && tid == 0) atomicCAS(a.stop, 0, a.seg_index + 1);
+}
+
+}  // namespace hyg

@@ -1,4 +1,6 @@
-"""K4 (k_ring.cuh): the zone-ring building march temporally blocked S = 8
+"""K4 (k_ring.cuh) and K4r (k_ring_reg.cuh: owned walls in registers,
+persistent prefetching CTAs, fast guard; used for divergence_norm >= 2 and
+64/128-node walls): the zone-ring building march temporally blocked S = 8
 steps per launch with halo zones, against the C oracle's whole-building run
 (relative L-infinity <= 1e-10, zones included): zone counts that leave the
 last CTA partial, rings smaller than the halo (local copies of one zone), a
@@ -44,7 +46,8 @@ def test_ring_matches_oracle(n_zones, wpz, n, steps):
     init = {k: v + (2e-3 * rng.standard_normal(v.size) if k in ("u_prev", "u_curr", "v_prev", "v_curr") else 0)
             for k, v in w.init.items()}
     got, st, stats = _gpu(w.model, init, steps)
-    assert stats.get("ring_tiled", {}).get("launches", 0) > 0, stats.keys()
+    kern = "ring_reg" if n <= 128 else "ring_tiled"
+    assert stats.get(kern, {}).get("launches", 0) > 0, stats.keys()
     b, rc, _, passes = _oracle(w.model, init, steps)
     assert rc == 0 and st.subiterations == passes
     err = rel_linf(got, dict(b.state))
@@ -60,7 +63,7 @@ def test_ring_chain_without_wrap():
     zs[0].interzone = [l for l in zs[0].interzone if l[0] == 1]
     zs[-1].interzone = [l for l in zs[-1].interzone if l[0] == len(zs) - 2]
     got, st, stats = _gpu(w.model, w.init, 300)
-    assert stats.get("ring_tiled", {}).get("launches", 0) > 0
+    assert stats.get("ring_reg", {}).get("launches", 0) > 0
     b, rc, _, _ = _oracle(w.model, w.init, 300)
     assert rc == 0
     assert rel_linf(got, dict(b.state)) <= TOL
@@ -87,3 +90,19 @@ def test_ring_guard_replay():
         ctx.synchronize()
         assert any(s["name"] == "ring_tiled" for s in ctx.kernel_stats())
     assert ei.value.layer == fl and ei.value.wall == b.fail_wall, (ei.value.layer, fl, ei.value.wall, b.fail_wall)
+
+
+def test_ring_reg_fast_guard_hands_over_to_k4():
+    """Values of 2 and above (inside a norm of 1000) trip K4r's fast guard in
+    its first launch; K4 replays from that launch's input with its exact guard
+    and the march matches the oracle."""
+    w = workloads.zone_ring(n_zones=20, walls_per_zone=6, n_nodes=128, nsteps=120)
+    init = {k: v.copy() for k, v in w.init.items()}
+    for k in ("u_prev", "u_curr"):
+        init[k][5 * 128 + 40: 5 * 128 + 60] += 1.5          # wall 5, interior nodes
+    got, st, stats = _gpu(w.model, init, 120)
+    assert stats.get("ring_reg", {}).get("launches", 0) > 0 and stats.get("ring_tiled", {}).get("launches", 0) > 0
+    b, rc, _, _ = _oracle(w.model, init, 120)
+    assert rc == 0
+    assert rel_linf(got, dict(b.state)) <= TOL
+    assert float(np.max(np.abs(got["zone_u"] - b.zu[:20]))) <= TOL
