@@ -49,9 +49,9 @@ CONFIGS = {
                  run_steps=100_000),
     "cfg2": dict(flop=14, bytes=0, bound="fp32", kernel="df_coupled_fused_f32", scaling="weak", dtype="f32",
                  run_steps=100_000),
-    # cfg3 runs K4 (k_ring.cuh): B = 7 zones per CTA, S = 8 steps per launch,
-    # (64 B x 5376 owned + 32 B x 756 halo nodes) / (5376 x 8) = 8.56 B/update
-    "cfg3": dict(flop=14.1, bytes=8.56, bound="hbm", kernel="ring_tiled", scaling="strong", dtype="f64",
+    # cfg3 runs K4r (k_ring_reg.cuh): B = 4 zones per block, S = 8 steps per launch,
+    # (64 B x 3072 owned + 32 B x 756 halo nodes) / (3072 x 8) = 8.98 B/update
+    "cfg3": dict(flop=14.1, bytes=8.98, bound="hbm", kernel="ring_reg", scaling="strong", dtype="f64",
                  run_steps=80_000),
     # cfg4 runs the temporally blocked K3w (k_dv_warp.cuh: 256-node windows, 8 steps
     # per launch, (32 x 256 + 32 x 240) / (240 x 8) = 8.27 B/update), so min(HBM,
