@@ -833,6 +833,8 @@ void launch_dv_walls(const NonlinearSegArgs& a, int n, cudaStream_t s) {
 }
 
 int advance_nonlinear(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
+    // the fused kernels carry the fast guard only: it proves |x| <= norm for norm >= 2
+    if (!(c->norm >= 2.0)) return advance_general(c, nsteps, dt, status);
     const int nch = std::max<int>(1, static_cast<int>(c->channels.size()));
     const int64_t block = 1 << 18;
     for (int64_t done = 0; done < nsteps;) {
@@ -902,6 +904,7 @@ constexpr int kTileNPT = 8;             // K3w: W = 256-node windows, S = 8 step
 constexpr int kTileS = kTileNPT;
 
 int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
+    if (!(c->norm >= 2.0)) return advance_general(c, nsteps, dt, status);   // fast guard: norm >= 2 only
     const int nch = std::max<int>(1, static_cast<int>(c->channels.size()));
     const int64_t block = 1 << 18;
     for (int64_t done = 0; done < nsteps;) {

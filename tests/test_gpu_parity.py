@@ -118,8 +118,8 @@ def test_tiled_long_wall_edges(n_nodes, steps):
 
 
 def test_nonlinear_fast_guard_fallback():
-    """|v| >= 2 in a nonlinear wall: K2/K3's fast guard fires, the march
-    continues on the per-step kernel with the exact guard, same result."""
+    """|v| >= 2 in a nonlinear wall: the fast guard of K2s/K3w fires, the
+    march continues on the per-step kernel with the exact guard, same result."""
     for n in (101, 4000):
         w = workloads.long_domain(n_nodes=n, nsteps=300)
         # a mild d(v) = 1 + 0.5 v: the stiff configs[0] bump would itself diverge
@@ -130,6 +130,36 @@ def test_nonlinear_fast_guard_fallback():
         got = gpu_run(w.model, w.init, 300, "none")
         ref = oracle_run("oracle", w.model, w.init, 300, "none", nthreads=1)
         assert rel_linf(got, ref) <= TOL64, n
+
+
+@pytest.mark.parametrize("n", [101, 3000])
+def test_nonlinear_norm_below_two(n):
+    """divergence_norm < 2: the fast guard cannot prove |x| <= norm, so d(v)
+    walls take the exact per-step guard; the first failing layer and wall
+    equal the oracle's check_bounded."""
+    w = workloads.long_domain(n_nodes=n, nsteps=400)
+    w.model.coeff_params = (0.5, 0.0, 10.0, 1.5)
+    for k in FIELDS:
+        w.init[k] = w.init[k].copy()
+        w.init[k][n // 2: n // 2 + 5] += 0.2
+    peak = max(float(np.max(np.abs(w.init[k]))) for k in FIELDS)
+    w.model.divergence_norm = peak - 0.05            # crossed in the first steps, inside the wall
+    wb_err = None
+    try:
+        oracle_run("oracle", w.model, w.init, 400, "none", nthreads=1)
+    except AssertionError as e:
+        wb_err = e.args[0]
+    assert wb_err is not None and wb_err[0] == api_codes().HYG_EDIVERGED, wb_err
+    with Context(w.model) as ctx:
+        ctx.set_state(**w.init)
+        with pytest.raises(NumericalError) as ei:
+            ctx.advance(400)
+    assert ei.value.layer == wb_err[1] and ei.value.wall == wb_err[2], (ei.value.layer, ei.value.wall, wb_err)
+
+
+def api_codes():
+    from paper_1703_10119_b200 import api
+    return api.A
 
 
 def test_cfg4_full_size_short_horizon():
