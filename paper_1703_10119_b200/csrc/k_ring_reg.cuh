@@ -43,12 +43,13 @@ struct RingRegShape {
     // doubles: staging of the owned walls (one bulk copy per field) and of the
     // halo walls, of the zone parameters and zone air (double-buffered by block
     // parity), the per-step surfaces [2][2][B W + halo] and zone air
-    // [2][2][local], forcing rows, and the mbarrier of the owned-wall copies
+    // [2][2][local], forcing rows, the mbarrier of the owned-wall copies, and
+    // per owned warp an output scratch [2 fields][2 walls][n] for its bulk stores
     __host__ __device__ static size_t smem_doubles(int B, int W, int n, int rw) {
         const size_t LB = local_zones(B);
         return static_cast<size_t>(4) * B * W * n + static_cast<size_t>(4) * halo_walls(W) * kP +
                2 * LB * kRingZP + 4 * LB + 4 * static_cast<size_t>(B * W + halo_walls(W)) + 4 * LB +
-               static_cast<size_t>(S) * rw + 1;
+               static_cast<size_t>(S) * rw + 1 + static_cast<size_t>(own_warps(B, W)) * 2 * 2 * n;
     }
 };
 
@@ -71,6 +72,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                      smem_u32(dst)),
                  "l"(src), "r"(bytes), "r"(smem_u32(mb))
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
                  : "memory");
 }
 
@@ -98,6 +105,7 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
     const int oAR = oSF + 4 * (OW + HW);                // zone air [parity][field][LB]
     const int oRW = oAR + 4 * LB;                       // forcing rows [S][rw]
     const int oMB = oRW + S * rw;                       // mbarrier of the owned-wall bulk copies
+    const int oOUT = oMB + 2;                           // output scratch [own warps][2][2 N] (16-byte aligned)
     void* mbar = &smem[oMB];
     auto so_ix = [&](int f, int i) { return oSO + f * OW * N + i; };
     auto sf_ix = [&](int par, int f, int i) { return oSF + (par * 2 + f) * (OW + HW) + i; };
@@ -105,11 +113,12 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int nblk = (Z + B - 1) / B;
 
-    for (int i = tid; i < a.steps * rw; i += nthr) {    // forcing rows of this launch (all blocks)
+    for (int i = tid; i < a.steps * rw; i += nthr) {    // forcing rows of this launch (all blocks), asynchronous
         const int k = i / rw, r = i - k * rw;
-        smem[oRW + i] = r < 4 * a.n_channels
-                            ? reinterpret_cast<const double*>(a.table + static_cast<size_t>(k) * a.n_channels)[r]
-                            : a.src[static_cast<size_t>(k) * (3 * a.n_sources + 2) + (r - 4 * a.n_channels)];
+        cp_async8(&smem[oRW + i],
+                  r < 4 * a.n_channels
+                      ? reinterpret_cast<const double*>(a.table + static_cast<size_t>(k) * a.n_channels) + r
+                      : a.src + static_cast<size_t>(k) * (3 * a.n_sources + 2) + (r - 4 * a.n_channels));
     }
     auto gz = [&](int z0, int i) { return ((z0 - S + i) % Z + Z) % Z; };
     auto halo_local = [&](int hz, int nown) { return hz < S - 1 ? 1 + hz : S + nown + (hz - (S - 1)); };
@@ -159,6 +168,34 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
         const int L = nown + 2 * S;
         const int par = it & 1;
         const bool next = b + static_cast<int>(gridDim.x) < nblk;
+        // role coefficients of this block, loaded before the wait so their
+        // latency hides behind it: owned: interior (3) + register 0's face-capable
+        // row (9) + channel; halo: interior (3) + face 1 (9)
+        double cf[12];
+        int ch = 0;
+        if (is_own) {
+            const int wl = warp * 2 + lane / 16, sub = lane % 16;
+            const int w = z0 * W + (wl < nown * W ? wl : 0);
+            const WallCoef& wc = a.coef[w];
+            cf[0] = wc.in.b; cf[1] = wc.in.c_su; cf[2] = wc.in.c_sv;
+            const bool first = sub == 0, rev = sub == 15;
+            const RowCoef& c = wc.face[first ? 0 : 1];
+            const bool m0 = first || rev;
+            cf[3] = m0 ? c.e : 0.0; cf[4] = m0 ? c.b : cf[0]; cf[5] = m0 ? c.e_g : 0.0;
+            cf[6] = m0 ? c.c_tv : 0.0; cf[7] = m0 ? c.c_sv : cf[2]; cf[8] = m0 ? c.c_tu : 0.0;
+            cf[9] = m0 ? c.c_su : cf[1]; cf[10] = m0 ? c.c_q : 0.0; cf[11] = m0 ? c.c_g : 0.0;
+            ch = a.attach[2 * w].index;
+        } else if (is_halo) {
+            const int hl = (warp - own_w) * 32 + lane;
+            const int hlc = hl < HW ? hl : 0;
+            const int hz = hlc / W, wi = hlc - hz * W;
+            const int w = gz(z0, halo_local(hz, nown)) * W + wi;
+            const WallCoef& wc = a.coef[w];
+            cf[0] = wc.in.b; cf[1] = wc.in.c_su; cf[2] = wc.in.c_sv;
+            const RowCoef& c = wc.face[1];
+            cf[3] = c.e; cf[4] = c.b; cf[5] = c.e_g; cf[6] = c.c_tv; cf[7] = c.c_sv; cf[8] = c.c_tu;
+            cf[9] = c.c_su; cf[10] = c.c_q; cf[11] = c.c_g;
+        }
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         mbar_wait(mbar, it & 1);                         // the owned walls of block b landed
         __syncthreads();                                 // staging of block b complete
@@ -168,7 +205,6 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
             const int wl = warp * 2 + lane / 16, sub = lane % 16;
             const bool live = wl < nown * W;
             const int wlc = live ? wl : 0;
-            const int w = z0 * W + wlc;
             const bool first = sub == 0, rev = sub == 15, mirror0 = first || rev;
             const int li = S + wlc / W;                  // local zone of face 1
             double up[NPT], uc[NPT], vp[NPT], vc[NPT];
@@ -190,16 +226,10 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
             rd(3, vc);
             __syncthreads();                             // (A) staging consumed by every role
             if (next) prefetch(b + gridDim.x, par ^ 1);
-            const WallCoef& wc = a.coef[w];
-            const double cb = wc.in.b, csu = wc.in.c_su, csv = wc.in.c_sv;
+            const double cb = cf[0], csu = cf[1], csv = cf[2];
             // register 0's face-capable row (interior coefficients, zero face terms elsewhere)
-            double fe = 0, fb = cb, feg = 0, fctv = 0, fcsv = csv, fctu = 0, fcsu = csu, fcq = 0, fcg = 0;
-            if (mirror0) {
-                const RowCoef& c = wc.face[first ? 0 : 1];
-                fe = c.e; fb = c.b; feg = c.e_g; fctv = c.c_tv; fcsv = c.c_sv; fctu = c.c_tu; fcsu = c.c_su;
-                fcq = c.c_q; fcg = c.c_g;
-            }
-            const int ch = a.attach[2 * w].index;
+            const double fe = cf[3], fb = cf[4], feg = cf[5], fctv = cf[6], fcsv = cf[7], fctu = cf[8], fcsu = cf[9],
+                         fcq = cf[10], fcg = cf[11];
             if (rev && live) {                           // layer-k surface sample (node N-1)
                 smem[sf_ix(0, 0, wl)] = uc[0];
                 smem[sf_ix(0, 1, wl)] = vc[0];
@@ -259,21 +289,41 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
                     x = up[q]; up[q] = uc[q]; uc[q] = x;
                 }
             }
-            if (live) {                                  // out = (layer k+S-1, layer k+S), 16-byte stores
-                const size_t g0 = static_cast<size_t>(w) * N + sub * NPT;
+            // out = (layer k+S-1, layer k+S): the warp's two walls through its
+            // output scratch, two fields at a time, one bulk store (TMA engine)
+            // per field — no store instructions on the warps' path
+            double* out_s = &smem[oOUT + warp * 2 * 2 * N];
+            const int nlive = min(2, max(0, nown * W - warp * 2));
+            auto wr = [&](int f, const double (&x)[NPT]) {
 #pragma unroll
                 for (int q = 0; q < NPT; q += 2) {
-                    // registers q, q+1 hold nodes g0+q, g0+q+1 (reversed lane: the mirrored pair)
-                    const size_t g = g0 + q;
-                    auto pr = [&](const double (&x)[NPT]) {   // selects: no runtime register index
-                        return rev ? make_double2(x[NPT - 1 - q], x[NPT - 2 - q]) : make_double2(x[q], x[q + 1]);
-                    };
-                    reinterpret_cast<double2*>(a.out[0] + g)[0] = pr(up);
-                    reinterpret_cast<double2*>(a.out[1] + g)[0] = pr(uc);
-                    reinterpret_cast<double2*>(a.out[2] + g)[0] = pr(vp);
-                    reinterpret_cast<double2*>(a.out[3] + g)[0] = pr(vc);
+                    const double2 t = rev ? make_double2(x[NPT - 1 - q], x[NPT - 2 - q]) : make_double2(x[q], x[q + 1]);
+                    *reinterpret_cast<double2*>(&out_s[f * 2 * N + (lane / 16) * N + sub * NPT + q]) = t;
                 }
-            }
+            };
+            auto flush = [&](int f0) {
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0 && nlive > 0) {
+                    const unsigned bytes = static_cast<unsigned>(nlive * N * sizeof(double));
+#pragma unroll
+                    for (int f = 0; f < 2; ++f)
+                        bulk_s2g(a.out[f0 + f] + (static_cast<size_t>(z0) * W + warp * 2) * N, &out_s[f * 2 * N], bytes);
+                    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+                }
+            };
+            auto drained = [&]() {   // the scratch may be rewritten once the last copies read it
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                __syncwarp();
+            };
+            drained();
+            wr(0, up);
+            wr(1, uc);
+            flush(0);
+            drained();
+            wr(0, vp);
+            wr(1, vc);
+            flush(2);
         } else if (is_halo) {
             // halo wall: global nodes N-P .. N-1; the cut end (p = 0) mirrors
             // itself — its error moves inward one node per step and never
@@ -295,8 +345,10 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
             }
             __syncthreads();                             // (A)
             if (next) prefetch(b + gridDim.x, par ^ 1);
-            const double cb = a.coef[w].in.b, csu = a.coef[w].in.c_su, csv = a.coef[w].in.c_sv;
-            const RowCoef c = a.coef[w].face[1];
+            const double cb = cf[0], csu = cf[1], csv = cf[2];
+            RowCoef c;
+            c.e = cf[3]; c.b = cf[4]; c.e_g = cf[5]; c.c_tv = cf[6]; c.c_sv = cf[7]; c.c_tu = cf[8];
+            c.c_su = cf[9]; c.c_q = cf[10]; c.c_g = cf[11];
             if (live) {
                 smem[sf_ix(0, 0, OW + hl)] = uc[P - 1];
                 smem[sf_ix(0, 1, OW + hl)] = vc[P - 1];
@@ -415,6 +467,7 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
         }
         __syncthreads();                                 // the shared slots are reused by the next block
     }
+    if (is_own && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // stores drained
     // fast guard verdict of the whole launch (bit 30: |x| >= 2 or not finite)
     if (__syncthreads_or((acc & 0x40000000u) != 0u) && tid == 0) atomicCAS(a.stop, 0, a.seg_index + 1);
 }
