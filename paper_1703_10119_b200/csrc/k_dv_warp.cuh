@@ -446,8 +446,8 @@ __device__ __forceinline__ void dv_cp_async_wait() { asm volatile("cp.async.wait
 // the window loads leave the critical path.  Buffer layout per field: lane
 // block l of NPT nodes, node j of the block at l NPT + (j ^ (l mod NPT)) (XOR
 // swizzle: the per-register reads of a warp spread over the banks).
-template <int NPT>
-__global__ void __launch_bounds__(kDvWarps * 32) k_dv_tiled_stream(const TiledArgs A) {
+template <int NPT, int MINB = 0>
+__global__ void __launch_bounds__(kDvWarps * 32, MINB) k_dv_tiled_stream(const TiledArgs A) {
     using G = DvTiles<NPT>;
     constexpr int W = G::W, T = G::T;
     static_assert((NPT & (NPT - 1)) == 0, "NPT must be a power of two");
