@@ -29,6 +29,12 @@
 
 #include "k_ring.cuh"
 
+// timing experiments only (tools/ring_step_probe.py): skip the arithmetic of
+// roles (1 halo, 2 zone, 4 owned); 0 in the library
+#ifndef RING_SKIP
+#define RING_SKIP 0
+#endif
+
 namespace hyg {
 
 template <int NPT, int S>
@@ -251,7 +257,7 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
                 const double vx0 = mirror0 ? vC[1] : vup, ux0 = mirror0 ? uC[1] : uup;
                 const double vx1 = rev ? vup : vdn, ux1 = rev ? uup : udn;
 #pragma unroll
-                for (int q = 0; q < NPT; ++q) {
+                for (int q = 0; q < NPT * !(RING_SKIP & 4); ++q) {
                     const double vl = q == 0 ? vx0 : vC[q - 1], ul = q == 0 ? ux0 : uC[q - 1];
                     const double vr = q == NPT - 1 ? vx1 : vC[q + 1], ur = q == NPT - 1 ? ux1 : uC[q + 1];
                     const double d = fma(-2.0, vP[q], vl + vr);
@@ -357,7 +363,7 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
             auto step = [&](double (&vP)[P], double (&vC)[P], double (&uP)[P], double (&uC)[P]) {
                 const double u_a = smem[ar_ix(cur, 0, li)], v_a = smem[ar_ix(cur, 1, li)];
 #pragma unroll
-                for (int p = 0; p < P; ++p) {
+                for (int p = 0; p < P * !(RING_SKIP & 1); ++p) {
                     const double vl = p == 0 ? vC[0] : vC[p - 1], ul = p == 0 ? uC[0] : uC[p - 1];
                     const double vr = p == P - 1 ? vC[P - 2] : vC[p + 1], ur = p == P - 1 ? uC[P - 2] : uC[p + 1];
                     const double d = fma(-2.0, vP[p], vl + vr);
@@ -426,7 +432,7 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
             if (next) prefetch(b + gridDim.x, par ^ 1);
             __syncthreads();                             // (B) layer-k surfaces and air published
             for (int k = 0; k < a.steps; ++k) {
-                if (live) {
+                if (live && !(RING_SKIP & 2)) {
                     const double u_a = smem[ar_ix(cur, 0, i)], v_a = smem[ar_ix(cur, 1, i)];
                     const int srow = oRW + k * rw + 4 * a.n_channels;
                     const int sz = srow + 3 * sidx;
@@ -434,21 +440,20 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
                     double du = smem[sz + 1] + smem[sz + 2] + smem[zp + 2] * (u_inf * v_inf - u_a * v_a) +
                                 smem[zp + 3] * (u_inf - u_a);
                     double dv = smem[sz + 0] + smem[zp + 1] * (v_inf - v_a);
+                    // branch-free over the maximum link/peer counts: the unused slots of
+                    // the parameter block are zero (their terms add +0), so every load
+                    // is independent and only the additions stay in order
 #pragma unroll
                     for (int q = 0; q < kRingMaxPeers; ++q) {
-                        if (q < npeer) {
-                            const double pu = smem[ar_ix(cur, 0, pidx[q])], pv = smem[ar_ix(cur, 1, pidx[q])];
-                            du += smem[zp + 42 + 4 * q] * (pu * pv - u_a * v_a) + smem[zp + 43 + 4 * q] * (pu - u_a);
-                            dv += smem[zp + 41 + 4 * q] * (pv - v_a);
-                        }
+                        const double pu = smem[ar_ix(cur, 0, pidx[q])], pv = smem[ar_ix(cur, 1, pidx[q])];
+                        du += smem[zp + 42 + 4 * q] * (pu * pv - u_a * v_a) + smem[zp + 43 + 4 * q] * (pu - u_a);
+                        dv += smem[zp + 41 + 4 * q] * (pv - v_a);
                     }
 #pragma unroll
                     for (int q = 0; q < kRingMaxLinks; ++q) {
-                        if (q < nlink) {
-                            const double us = smem[sf_ix(cur, 0, ls[q])], vs = smem[sf_ix(cur, 1, ls[q])];
-                            du += smem[zp + 9 + 4 * q] * (us - u_a) + smem[zp + 10 + 4 * q] * (vs - v_a);
-                            dv += smem[zp + 11 + 4 * q] * (v_a - vs);
-                        }
+                        const double us = smem[sf_ix(cur, 0, ls[q])], vs = smem[sf_ix(cur, 1, ls[q])];
+                        du += smem[zp + 9 + 4 * q] * (us - u_a) + smem[zp + 10 + 4 * q] * (vs - v_a);
+                        dv += smem[zp + 11 + 4 * q] * (v_a - vs);
                     }
                     const double nu = u_a + a.dt * (du / smem[zp + 0]);
                     const double nv = v_a + a.dt * dv;

@@ -4,7 +4,11 @@ import sys
 from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-from paper_1703_10119_b200 import Context, workloads   # noqa: E402
+from paper_1703_10119_b200 import Context, api, workloads   # noqa: E402
+
+if len(sys.argv) > 1:          # a timing variant of the library (tools/_ringvar)
+    api.load_library(sys.argv[1])
+    print("library", sys.argv[1])
 
 w = workloads.zone_ring(nsteps=100)
 with Context(w.model) as ctx:
