@@ -203,6 +203,7 @@ struct hyg_ctx {
     int ring_W = 0, ring_B = 0;
     int ring_reg_B = 0;              // K4r (registers + prefetch): zones per CTA, 0 if not applicable
     double* d_ring_zp = nullptr;     // K4r per-zone parameter blocks [zones][kRingZP]
+    bool ring_reg_small = false;     // every zone: <= 6 wall links, <= 2 ring peers
     int rad_groups = 0, rad_terms = 0;
     int *d_rad_tgt = nullptr, *d_rad_grp = nullptr;
     double *d_rad_num = nullptr, *d_rad_den = nullptr, *d_rad_coef = nullptr, *d_qrad = nullptr;
@@ -988,11 +989,13 @@ int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
 
 // ---- the zone-ring temporally blocked path (K4, K4r) -----------------------------
 template <int NPT>
-void launch_ring_reg(const RingArgs& a, int threads, size_t smem, cudaStream_t s, int device) {
-    auto k = k_ring_reg<NPT, kRingS>;
+void launch_ring_reg(const RingArgs& a, int threads, size_t smem, cudaStream_t s, int device, bool small) {
+    // small: every zone has <= 6 wall links and <= 2 ring peers (configs[3])
+    auto k = small ? k_ring_reg<NPT, kRingS, 6, 2> : k_ring_reg<NPT, kRingS>;
     static int n_sm = 0;
     if (!n_sm) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_ring_reg<NPT, kRingS, 6, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_ring_reg<NPT, kRingS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device);
     }
     int per_sm = 1;
@@ -1083,8 +1086,8 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool
             a.zv_out = c->zv[1 - zf];
             LaunchScope ls(c, reg ? "ring_reg" : "ring_tiled", static_cast<double>(c->cells()) * a.steps);
             if (reg) {
-                if (npt == 4) launch_ring_reg<4>(a, threads, smem, c->stream, c->device);
-                else launch_ring_reg<8>(a, threads, smem, c->stream, c->device);
+                if (npt == 4) launch_ring_reg<4>(a, threads, smem, c->stream, c->device, c->ring_reg_small);
+                else launch_ring_reg<8>(a, threads, smem, c->stream, c->device, c->ring_reg_small);
             } else if (npt == 4) launch_ring<4>(a, grid, threads, smem, c->stream);
             else if (npt == 8) launch_ring<8>(a, grid, threads, smem, c->stream);
             else launch_ring<16>(a, grid, threads, smem, c->stream);
@@ -1508,6 +1511,9 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
         if (c->ring_reg_B > 0) {
             // K4r's per-zone parameter blocks (k_ring_reg.cuh), prefetched with the walls
             std::vector<double> zp(c->zones.size() * kRingZP, 0.0);
+            c->ring_reg_small = true;
+            for (const ZoneDev& d : c->zones)
+                c->ring_reg_small = c->ring_reg_small && d.wall_end - d.wall_begin <= 6 && d.inz_end - d.inz_begin <= 2;
             for (size_t z = 0; z < c->zones.size(); ++z) {
                 const ZoneDev& d = c->zones[z];
                 double* b = &zp[z * kRingZP];

@@ -92,7 +92,9 @@ __device__ __forceinline__ void cp_async16(double* smem_dst, const double* gsrc)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
 }
 
-template <int NPT, int S>
+// NL, NP: link and peer slots walked per zone (compile-time, branch-free; the
+// host picks the smallest instantiation that covers every zone)
+template <int NPT, int S, int NL = kRingMaxLinks, int NP = kRingMaxPeers>
 __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
     using Sh = RingRegShape<NPT, S>;
     constexpr int P = Sh::kP, N = 16 * NPT;
@@ -408,19 +410,19 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
             const int hz = i < S ? i - 1 : (S - 1) + (i - S - nown);
             const int zp = oZS + (par * LB + (valid ? i : 0)) * kRingZP;
             int nlink = 0, npeer = 0, sidx = 0;
-            int ls[kRingMaxLinks], pidx[kRingMaxPeers];
+            int ls[NL], pidx[NP];
             if (live) {
                 nlink = static_cast<int>(smem[zp + 4]);
                 npeer = static_cast<int>(smem[zp + 5]);
                 sidx = static_cast<int>(smem[zp + 6]);
             }
 #pragma unroll
-            for (int q = 0; q < kRingMaxLinks; ++q) {
+            for (int q = 0; q < NL; ++q) {
                 const int wi = q < nlink ? static_cast<int>(smem[zp + 8 + 4 * q]) : 0;
                 ls[q] = owned ? (i - S) * W + wi : OW + hz * W + wi;
             }
 #pragma unroll
-            for (int q = 0; q < kRingMaxPeers; ++q) {
+            for (int q = 0; q < NP; ++q) {
                 const int pg = q < npeer ? static_cast<int>(smem[zp + 40 + 4 * q]) : -1;
                 pidx[q] = i >= 1 && gz(z0, i - 1) == pg ? i - 1 : i + 1;   // the adjacent copy
             }
@@ -444,13 +446,13 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
                     // the parameter block are zero (their terms add +0), so every load
                     // is independent and only the additions stay in order
 #pragma unroll
-                    for (int q = 0; q < kRingMaxPeers; ++q) {
+                    for (int q = 0; q < NP; ++q) {
                         const double pu = smem[ar_ix(cur, 0, pidx[q])], pv = smem[ar_ix(cur, 1, pidx[q])];
                         du += smem[zp + 42 + 4 * q] * (pu * pv - u_a * v_a) + smem[zp + 43 + 4 * q] * (pu - u_a);
                         dv += smem[zp + 41 + 4 * q] * (pv - v_a);
                     }
 #pragma unroll
-                    for (int q = 0; q < kRingMaxLinks; ++q) {
+                    for (int q = 0; q < NL; ++q) {
                         const double us = smem[sf_ix(cur, 0, ls[q])], vs = smem[sf_ix(cur, 1, ls[q])];
                         du += smem[zp + 9 + 4 * q] * (us - u_a) + smem[zp + 10 + 4 * q] * (vs - v_a);
                         dv += smem[zp + 11 + 4 * q] * (v_a - vs);
