@@ -822,7 +822,7 @@ void launch_dv_split(const NonlinearSegArgs& a, int nw, cudaStream_t s) {
 // Otherwise K2w: NPT = the smallest power of two with 32 NPT >= n, M = nodes of
 // the reversed lane.
 void launch_dv_walls(const NonlinearSegArgs& a, int n, cudaStream_t s) {
-    if (a.n_walls <= kSplitWallsMax) return launch_dv_split<1>(a, (n + 31) / 32, s);
+    if (a.n_walls <= kSplitWallsMax && n >= 3) return launch_dv_split<1>(a, (n + 31) / 32, s);
     const int npt = n <= 32 ? 1 : n <= 64 ? 2 : n <= 128 ? 4 : 8;
     const int m = n - (n - 1) / npt * npt;
     switch (npt) {
