@@ -321,14 +321,14 @@ def run_reference(args):
 class Runner:
     """One rank's engine for the selected config: a Context, or a shard of one."""
 
-    def __init__(self, args, w, rank, world, local, gloo):
+    def __init__(self, args, w, rank, world, local):
         from paper_1703_10119_b200 import Context, shard
         self.w, self.args = w, args
         cfg = CONFIGS[args.config]
         w.model.device = local
         self.shard = None
         if cfg["scaling"] == "strong" and world > 1:
-            comm = shard.Comm(gloo)
+            comm = shard.Comm()          # the NCCL group: halos device to device over NVLink
             if args.config == "cfg4":
                 self.shard = shard.LongDomainShard(w.model, w.init, comm, Context, halo=args.halo or 64)
             else:
@@ -367,11 +367,9 @@ def main():
     cfg = CONFIGS[args.config]
     import torch
     import torch.distributed as dist
-    gloo = None
+    torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        gloo = dist.new_group(backend="gloo")
-    torch.cuda.set_device(local)
     from paper_1703_10119_b200 import api
 
     def barrier():
@@ -388,7 +386,7 @@ def main():
     w = make_workload(args, rank if cfg["scaling"] != "strong" else 0, world)
     peak64 = api.probe_fp64_peak(local)
     peak32 = api.probe_fp32_peak(local) if cfg["bound"] == "fp32" else None
-    R = Runner(args, w, rank, world, local, gloo)
+    R = Runner(args, w, rank, world, local)
     ctx = R.ctx
 
     clocks = Clocks(local)

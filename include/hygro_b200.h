@@ -210,7 +210,10 @@ int hyg_get_state(hyg_ctx* ctx, double* u_prev, double* u_curr, double* v_prev,
 
 /* Sub-range access for halo exchange between shards (fp64 models).  Cells
  * are the flattened wall-major index w*n_nodes + j; any pointer may be NULL
- * to skip that layer.  Zones [zone0, zone0+count). */
+ * to skip that layer.  Zones [zone0, zone0+count).  Pointers may be host
+ * (pageable or pinned) or device memory of any GPU (cudaMemcpyDefault over
+ * UVA): shards exchange halos device to device, e.g. straight into NCCL
+ * buffers, with no host staging.  Each call returns after the copy. */
 int hyg_get_cells(hyg_ctx* ctx, int64_t cell0, int64_t count, double* u_prev, double* u_curr,
                   double* v_prev, double* v_curr);
 int hyg_set_cells(hyg_ctx* ctx, int64_t cell0, int64_t count, const double* u_prev,

@@ -291,6 +291,11 @@ def _ptr(a):
     return None if a is None else a.ctypes.data_as(A.dp)
 
 
+def _addr(a: int):
+    """A raw (host or device) address as the ABI's double*."""
+    return C.cast(C.c_void_p(a), A.dp)
+
+
 def _f64(a, n):
     a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
     if a.size != n:
@@ -343,6 +348,36 @@ class Context:
         arrs = [np.ascontiguousarray(values[k], dtype=np.float64) for k in ("u_prev", "u_curr", "v_prev", "v_curr")]
         count = arrs[0].size
         _check(self.lib.hyg_set_cells(self.h, cell0, count, *map(_ptr, arrs)), None, "hyg_set_cells")
+
+    def get_cells_into(self, cell0: int, count: int, out) -> None:
+        """Copy cells [cell0, cell0+count) of the four layers into `out`, a
+        contiguous float64 torch tensor of shape (4, count) on any device (the
+        halo exchange of shard.py passes NCCL buffers: device to device)."""
+        assert out.is_contiguous() and tuple(out.shape) == (4, count) and out.element_size() == 8
+        base, step = out.data_ptr(), count * 8
+        _check(self.lib.hyg_get_cells(self.h, cell0, count, *[_addr(base + i * step) for i in range(4)]),
+               None, "hyg_get_cells")
+
+    def set_cells_from(self, cell0: int, src) -> None:
+        """Inverse of get_cells_into; the caller orders `src` (e.g. synchronises
+        the stream an NCCL receive completed on) before the call."""
+        assert src.is_contiguous() and src.dim() == 2 and src.shape[0] == 4 and src.element_size() == 8
+        count, base = int(src.shape[1]), src.data_ptr()
+        _check(self.lib.hyg_set_cells(self.h, cell0, count, *[_addr(base + i * count * 8) for i in range(4)]),
+               None, "hyg_set_cells")
+
+    def get_zones_into(self, zone0: int, count: int, out) -> None:
+        """Zones [zone0, zone0+count) into `out`: contiguous float64 (2, count), any device."""
+        assert out.is_contiguous() and tuple(out.shape) == (2, count) and out.element_size() == 8
+        base = out.data_ptr()
+        _check(self.lib.hyg_get_zones(self.h, zone0, count, _addr(base), _addr(base + count * 8)),
+               None, "hyg_get_zones")
+
+    def set_zones_from(self, zone0: int, src) -> None:
+        assert src.is_contiguous() and src.dim() == 2 and src.shape[0] == 2 and src.element_size() == 8
+        count, base = int(src.shape[1]), src.data_ptr()
+        _check(self.lib.hyg_set_zones(self.h, zone0, count, _addr(base), _addr(base + count * 8)),
+               None, "hyg_set_zones")
 
     def get_zones(self, zone0: int, count: int):
         zu, zv = np.empty(count), np.empty(count)

@@ -1661,7 +1661,7 @@ int hyg_get_cells(hyg_ctx* c, int64_t cell0, int64_t count, double* up, double* 
     for (int i = 0; i < 4; ++i)
         if (dst[i])
             HYG_CUDA(cudaMemcpyAsync(dst[i], c->s64[c->cur][i] + cell0, count * sizeof(double),
-                                     cudaMemcpyDeviceToHost, c->stream));
+                                     cudaMemcpyDefault, c->stream));
     HYG_CUDA(cudaStreamSynchronize(c->stream));
     return HYG_OK;
 }
@@ -1676,7 +1676,7 @@ int hyg_set_cells(hyg_ctx* c, int64_t cell0, int64_t count, const double* up, co
     for (int i = 0; i < 4; ++i)
         if (src[i])
             HYG_CUDA(cudaMemcpyAsync(c->s64[c->cur][i] + cell0, src[i], count * sizeof(double),
-                                     cudaMemcpyHostToDevice, c->stream));
+                                     cudaMemcpyDefault, c->stream));
     HYG_CUDA(cudaStreamSynchronize(c->stream));
     return HYG_OK;
 }
@@ -1685,8 +1685,8 @@ int hyg_get_zones(hyg_ctx* c, int32_t z0, int32_t count, double* zu, double* zv)
     hyg_status* status = nullptr;
     if (!c || z0 < 0 || count < 0 || z0 + count > static_cast<int>(c->zones.size())) return HYG_EINVAL;
     cudaSetDevice(c->device);
-    if (zu) HYG_CUDA(cudaMemcpyAsync(zu, c->zu[c->zcur] + z0, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    if (zv) HYG_CUDA(cudaMemcpyAsync(zv, c->zv[c->zcur] + z0, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (zu) HYG_CUDA(cudaMemcpyAsync(zu, c->zu[c->zcur] + z0, count * sizeof(double), cudaMemcpyDefault, c->stream));
+    if (zv) HYG_CUDA(cudaMemcpyAsync(zv, c->zv[c->zcur] + z0, count * sizeof(double), cudaMemcpyDefault, c->stream));
     HYG_CUDA(cudaStreamSynchronize(c->stream));
     return HYG_OK;
 }
@@ -1695,8 +1695,8 @@ int hyg_set_zones(hyg_ctx* c, int32_t z0, int32_t count, const double* zu, const
     hyg_status* status = nullptr;
     if (!c || z0 < 0 || count < 0 || z0 + count > static_cast<int>(c->zones.size())) return HYG_EINVAL;
     cudaSetDevice(c->device);
-    if (zu) HYG_CUDA(cudaMemcpyAsync(c->zu[c->zcur] + z0, zu, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    if (zv) HYG_CUDA(cudaMemcpyAsync(c->zv[c->zcur] + z0, zv, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    if (zu) HYG_CUDA(cudaMemcpyAsync(c->zu[c->zcur] + z0, zu, count * sizeof(double), cudaMemcpyDefault, c->stream));
+    if (zv) HYG_CUDA(cudaMemcpyAsync(c->zv[c->zcur] + z0, zv, count * sizeof(double), cudaMemcpyDefault, c->stream));
     HYG_CUDA(cudaStreamSynchronize(c->stream));
     return HYG_OK;
 }

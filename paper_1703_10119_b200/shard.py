@@ -52,46 +52,84 @@ def slab_bounds(n: int, world: int, rank: int, halo: int) -> Slab:
 
 
 class Comm:
-    """Point-to-point + reductions over a torch.distributed group (gloo for host
-    buffers; the exchange payloads are a few KB per K steps)."""
+    """Point-to-point + reductions over a torch.distributed group.
+
+    On an NCCL group (one process per GPU, bench.py at N > 1) halo payloads
+    stay on the device: the engine copies its boundary cells straight into a
+    CUDA buffer (Context.get_cells_into, device to device), NCCL moves it over
+    NVLink, and the receiver copies it into its halo (set_cells_from) — no
+    host staging.  On a gloo group (CPU tests, or ranks sharing one GPU) the
+    same payloads travel as host tensors."""
 
     def __init__(self, group=None):
+        import torch
         import torch.distributed as dist
         self.dist, self.group = dist, group
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.on_device = dist.get_backend(group) == "nccl"
+        self.device = torch.device("cuda", torch.cuda.current_device()) if self.on_device else torch.device("cpu")
 
-    def _t(self, a):
+    def tensor(self, a):
+        """`a` (ndarray or tensor) as a contiguous float64 tensor on the comm device."""
         import torch
-        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+        if not isinstance(a, torch.Tensor):
+            a = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+        return a.to(self.device, torch.float64).contiguous()
 
     def exchange(self, sends: dict, recvs: dict) -> dict:
-        """sends/recvs: {peer_rank: ndarray | shape}; returns received arrays."""
+        """sends: {peer_rank: ndarray | tensor}; recvs: {peer_rank: shape};
+        returns {peer_rank: tensor on the comm device}, complete and ordered
+        before the host continues."""
         import torch
         reqs, out = [], {}
         for peer, shape in recvs.items():
-            buf = torch.empty(shape, dtype=torch.float64)
+            buf = torch.empty(shape, dtype=torch.float64, device=self.device)
             out[peer] = buf
             reqs.append(self.dist.irecv(buf, src=self._global(peer), group=self.group))
         for peer, arr in sends.items():
-            reqs.append(self.dist.isend(self._t(arr), dst=self._global(peer), group=self.group))
+            reqs.append(self.dist.isend(self.tensor(arr), dst=self._global(peer), group=self.group))
         for r in reqs:
             r.wait()
-        return {k: v.numpy() for k, v in out.items()}
+        if self.on_device:
+            torch.cuda.current_stream(self.device).synchronize()   # engines run on their own stream
+        return out
 
     def _global(self, r):
         return r if self.group is None else self.dist.get_global_rank(self.group, r)
 
-    def allreduce_max(self, x: float) -> float:
+    def _reduce(self, x: float, op) -> float:
         import torch
-        t = torch.tensor([x], dtype=torch.float64)
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        t = torch.tensor([x], dtype=torch.float64, device=self.device)
+        self.dist.all_reduce(t, op=op, group=self.group)
         return float(t.item())
 
+    def allreduce_max(self, x: float) -> float:
+        return self._reduce(x, self.dist.ReduceOp.MAX)
+
     def allreduce_min(self, x: float) -> float:
+        return self._reduce(x, self.dist.ReduceOp.MIN)
+
+
+def _get_block(engine, comm, cell0: int, count: int):
+    """Cells [cell0, cell0+count) of the four layers as a (4, count) payload:
+    a device tensor filled device to device when the engine and the comm are
+    both on the GPU, else a host array."""
+    if comm.on_device and hasattr(engine, "get_cells_into"):
         import torch
-        t = torch.tensor([x], dtype=torch.float64)
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
-        return float(t.item())
+        buf = torch.empty((4, count), dtype=torch.float64, device=comm.device)
+        engine.get_cells_into(cell0, count, buf)
+        return buf
+    c = engine.get_cells(cell0, count)
+    return np.stack([c[f] for f in FIELDS])
+
+
+def _set_block(engine, cell0: int, block):
+    import torch
+    if isinstance(block, torch.Tensor) and block.is_cuda and hasattr(engine, "set_cells_from"):
+        engine.set_cells_from(cell0, block.contiguous())
+        return
+    a = block.cpu().numpy() if isinstance(block, torch.Tensor) else block
+    engine.set_cells(cell0, dict(zip(FIELDS, a)))
 
 
 def _advance_guarded(engine, k, comm):
@@ -143,18 +181,16 @@ class LongDomainShard:
         s, H, r, P = self.slab, self.halo, self.comm.rank, self.comm.world
         sends, recvs = {}, {}
         if r > 0:
-            left = self.engine.get_cells(s.lo - s.a, H)
-            sends[r - 1] = np.stack([left[f] for f in FIELDS])
+            sends[r - 1] = _get_block(self.engine, self.comm, s.lo - s.a, H)
             recvs[r - 1] = (4, H)
         if r < P - 1:
-            right = self.engine.get_cells(s.hi - H - s.a, H)
-            sends[r + 1] = np.stack([right[f] for f in FIELDS])
+            sends[r + 1] = _get_block(self.engine, self.comm, s.hi - H - s.a, H)
             recvs[r + 1] = (4, H)
         got = self.comm.exchange(sends, recvs)
         if r > 0:
-            self.engine.set_cells(0, dict(zip(FIELDS, got[r - 1])))
+            _set_block(self.engine, 0, got[r - 1])
         if r < P - 1:
-            self.engine.set_cells(s.hi - s.a, dict(zip(FIELDS, got[r + 1])))
+            _set_block(self.engine, s.hi - s.a, got[r + 1])
 
     def owned_state(self) -> dict:
         s = self.slab
@@ -225,10 +261,17 @@ class ZoneRingShard:
             done += k
 
     def _zone_block(self, i0, count):
+        """Zones [i0, i0+count) with their walls as one flat payload:
+        4 layers x cells, then zone_u, zone_v."""
         n, W = self.engine_model_n, self.W
-        cells = self.engine.get_cells(i0 * W * n, count * W * n)
+        cells = _get_block(self.engine, self.comm, i0 * W * n, count * W * n)
+        if self.comm.on_device and hasattr(self.engine, "get_zones_into"):
+            import torch
+            z = torch.empty((2, count), dtype=torch.float64, device=self.comm.device)
+            self.engine.get_zones_into(i0, count, z)
+            return torch.cat([cells.reshape(-1), z.reshape(-1)])
         zu, zv = self.engine.get_zones(i0, count)
-        return np.concatenate([np.stack([cells[f] for f in FIELDS]).reshape(-1), zu, zv])
+        return np.concatenate([np.asarray(cells).reshape(-1), zu, zv])
 
     @property
     def engine_model_n(self):
@@ -244,9 +287,11 @@ class ZoneRingShard:
         # my first H owned zones go left (they are its right halo), my last H go right
         first = self._zone_block(H, H)
         last = self._zone_block(own, H)
-        size = first.size
+        size = int(first.shape[0])
         if left == right:   # two ranks: both messages go to the same peer; ship them together
-            got = self.comm.exchange({left: np.concatenate([first, last])}, {left: (2 * size,)})[left]
+            both = (self.comm.tensor(first), self.comm.tensor(last))
+            import torch
+            got = self.comm.exchange({left: torch.cat(both)}, {left: (2 * size,)})[left]
             from_right, from_left = got[:size], got[size:]
         else:
             got = self.comm.exchange({left: first, right: last}, {left: (size,), right: (size,)})
@@ -257,9 +302,13 @@ class ZoneRingShard:
     def _set_zone_block(self, i0, count, flat):
         n, W = self.engine_model_n, self.W
         m = count * W * n
-        cells = flat[:4 * m].reshape(4, m)
-        self.engine.set_cells(i0 * W * n, dict(zip(FIELDS, cells)))
-        self.engine.set_zones(i0, flat[4 * m:4 * m + count], flat[4 * m + count:])
+        _set_block(self.engine, i0 * W * n, flat[:4 * m].reshape(4, m))
+        z = flat[4 * m:4 * m + 2 * count].reshape(2, count)
+        if getattr(z, "is_cuda", False) and hasattr(self.engine, "set_zones_from"):
+            self.engine.set_zones_from(i0, z.contiguous())
+        else:
+            z = z.cpu().numpy() if hasattr(z, "cpu") else z
+            self.engine.set_zones(i0, z[0], z[1])
 
     def owned_state(self) -> dict:
         n, W = self.engine_model_n, self.W

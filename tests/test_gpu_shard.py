@@ -83,3 +83,129 @@ def test_two_ranks_one_device_bitwise(case):
         p.join(timeout=60)
     for rank, ok, err in sorted(results):
         assert ok, f"rank {rank}: {err}"
+
+
+class _LoopbackComm:
+    """Device-payload comm for shards living in threads of one process: what
+    an NCCL group does between GPUs (payloads stay CUDA tensors, filled and
+    drained device to device by Context.get_cells_into / set_cells_from),
+    with a barrier-synchronised mailbox instead of NVLink."""
+
+    def __init__(self, rank, world, hub):
+        import torch
+        self.rank, self.world, self.hub = rank, world, hub
+        self.on_device, self.device = True, torch.device("cuda", 0)
+
+    def tensor(self, a):
+        import torch
+        if not isinstance(a, torch.Tensor):
+            a = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+        return a.to(self.device, torch.float64).contiguous()
+
+    def exchange(self, sends, recvs):
+        box, bar = self.hub
+        for peer, a in sends.items():
+            t = self.tensor(a)
+            assert t.is_cuda
+            box[(self.rank, peer)] = t.clone()
+        bar.wait()
+        out = {peer: box.pop((peer, self.rank)) for peer in recvs}
+        bar.wait()
+        return out
+
+    def _reduce(self, x, f):
+        box, bar = self.hub
+        box[("r", self.rank)] = x
+        bar.wait()
+        v = f(box[("r", r)] for r in range(self.world))
+        bar.wait()
+        return v
+
+    def allreduce_max(self, x):
+        return self._reduce(x, max)
+
+    def allreduce_min(self, x):
+        return self._reduce(x, min)
+
+
+@pytest.mark.parametrize("case", ["long", "ring"])
+def test_device_payload_exchange_bitwise(case):
+    """Halo payloads as CUDA tensors (the NCCL path of shard.Comm): shards
+    in two threads equal the undivided run bit for bit."""
+    import threading
+    import torch
+    from paper_1703_10119_b200 import Context, shard, workloads
+    world = 2
+    hub = ({}, threading.Barrier(world))
+    res, errs = {}, []
+    if case == "long":
+        n, steps = 1 << 15, 120
+        w = workloads.long_domain(n_nodes=n, nsteps=steps)
+        model, init = w.model, w.init
+    else:
+        Z, W, n, steps = 16, 6, 32, 120
+        w = workloads.zone_ring(n_zones=Z, walls_per_zone=W, n_nodes=n, nsteps=steps)
+        rng = np.random.default_rng(5)
+        init = {f: w.init[f] + 1e-3 * rng.standard_normal(w.init[f].size) for f in FIELDS}
+        init.update(zone_u=w.init["zone_u"], zone_v=w.init["zone_v"])
+        model = w.model
+
+    def work(rank):
+        try:
+            torch.cuda.set_device(0)
+            comm = _LoopbackComm(rank, world, hub)
+            if case == "long":
+                sh = shard.LongDomainShard(model, init, comm, Context, halo=24)
+                sh.advance(steps)
+            else:
+                sh = shard.ZoneRingShard(model, init, comm, Context, walls_per_zone=6, halo=4)
+                sh.bootstrap("implicit")
+                sh.advance(steps - 1)
+            res[rank] = (sh, sh.owned_state())
+        except Exception:
+            errs.append(traceback.format_exc())
+            hub[1].abort()
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs[0]
+    with Context(model) as ref:
+        ref.set_state(**init)
+        if case == "long":
+            ref.advance(steps)
+        else:
+            ref.bootstrap("implicit")
+            ref.advance(steps - 1)
+        full = ref.get_state()
+    for rank, (sh, got) in res.items():
+        if case == "long":
+            sl = slice(sh.slab.lo, sh.slab.hi)
+        else:
+            sl = slice(sh.lo * 6 * n, sh.hi * 6 * n)
+            assert np.array_equal(got["zone_u"], full["zone_u"][sh.lo:sh.hi])
+            assert np.array_equal(got["zone_v"], full["zone_v"][sh.lo:sh.hi])
+        for f in FIELDS:
+            assert np.array_equal(got[f], full[f][sl]), (rank, f)
+        sh.engine.close()
+
+
+def test_cells_into_device_roundtrip():
+    """get_cells_into / set_cells_from with CUDA buffers equal the host-array calls."""
+    import torch
+    from paper_1703_10119_b200 import Context, workloads
+    w = workloads.long_domain(n_nodes=4096, nsteps=10)
+    with Context(w.model) as ctx:
+        ctx.set_state(**w.init)
+        ctx.advance(9)
+        host = ctx.get_cells(1000, 300)
+        dev = torch.empty((4, 300), dtype=torch.float64, device="cuda:0")
+        ctx.get_cells_into(1000, 300, dev)
+        for i, f in enumerate(FIELDS):
+            assert np.array_equal(dev[i].cpu().numpy(), host[f])
+        ctx.set_cells_from(2000, dev)
+        back = ctx.get_cells(2000, 300)
+        for f in FIELDS:
+            assert np.array_equal(back[f], host[f])
