@@ -1432,10 +1432,13 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
         }
     }
     c->fused = all_exterior && d->n_zones == 0 && d->coeff_kind == HYG_COEFF_CONSTANT && fused_grid(c->n);
+    // the warp-register d(v) kernels take exp of -p2 (v - p3)^2 <= 0 (fexp_addend); a
+    // growing exponential (p2 < 0) marches on the per-step path with the full exp
+    const bool dv_neg = d->coeff_params[2] >= 0.0;
     c->nl_fused = all_exterior && d->n_zones == 0 && d->coeff_kind == HYG_COEFF_ANALYTIC_D && c->n <= 1024 &&
-                  c->precision == HYG_F64;
+                  c->precision == HYG_F64 && dv_neg;
     c->tiled = all_exterior && d->n_zones == 0 && d->coeff_kind == HYG_COEFF_ANALYTIC_D && c->n > 1024 &&
-               c->n_walls == 1 && c->precision == HYG_F64;
+               c->n_walls == 1 && c->precision == HYG_F64 && dv_neg;
     if (c->precision == HYG_F32 && !c->fused) {
         delete c;
         set_status(status, HYG_ENOTSUP, "fp32 state is implemented for exterior constant walls on fused grids only");

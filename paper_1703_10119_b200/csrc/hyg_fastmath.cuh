@@ -18,7 +18,8 @@
 // ulp in d(v) is ~1e-16 relative in a coefficient, far inside the 1e-10 parity
 // tolerance.
 //
-// frcp: rcp.approx.ftz.f64 (~23 bits) + two Newton steps -> ~1 ulp.
+// frcp: rcp.approx.ftz.f64 (~23 bits), then y (1 + e + e^2) with e = 1 - d y
+// (3 FMAs; the cubic term e^3 ~ 2^-66 is far below an ulp) -> ~1 ulp.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -44,7 +45,8 @@ __device__ __constant__ const double kExp2Tab64[64] = {
     0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0,
 };
 
-__device__ __forceinline__ double fexp(double x, const double* tab) {
+// exp(x) for -708 <= x <= 709 (no special cases; see fexp)
+__device__ __forceinline__ double fexp_core(double x, const double* tab) {
     constexpr double kShift = 6755399441055744.0;                  // 1.5 * 2^52
     constexpr double kInvL = 92.332482616893658;                   // 64 / ln 2
     constexpr double kLHi = 0x1.62e42fee00000p-7;                  // ln2_hi / 64 (32 significant bits)
@@ -62,7 +64,11 @@ __device__ __forceinline__ double fexp(double x, const double* tab) {
     const double t = tab[k & 63];
     const double ts = __hiloint2double(__double2hiint(t) + static_cast<int>(static_cast<unsigned>(k >> 6) << 20),
                                        __double2loint(t));
-    const double y = fma(ts, sm, ts);
+    return fma(ts, sm, ts);
+}
+
+__device__ __forceinline__ double fexp(double x, const double* tab) {
+    const double y = fexp_core(x, tab);
     // |x| >= 708, inf or NaN: integer tests and selects, no branch (a branch
     // per exp would split the caller's independent chains into basic blocks)
     const unsigned long long ax = static_cast<unsigned long long>(__double_as_longlong(x)) & 0x7fffffffffffffffull;
@@ -76,10 +82,18 @@ __device__ __forceinline__ double fexp(double x, const double* tab) {
 __device__ __forceinline__ double frcp(double d) {
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
-    double e = fma(-d, y, 1.0);
-    y = fma(y, e, y);
-    e = fma(-d, y, 1.0);
-    return fma(y, e, y);
+    const double e = fma(-d, y, 1.0);                  // |e| <= ~2^-22
+    return fma(y, fma(e, e, e), y);                    // y (1 + e + e^2): error ~e^3
+}
+
+// exp(x) as a term ADDED TO A VALUE >= 2^-200 in magnitude (the d(v) half
+// node: 1 + p0 v + p1 exp(x), x = -p2 (v - p3)^2 <= 0): x is clamped at -708,
+// where exp is below 2^-1021 and vanishes in the sum exactly as the exact 0
+// would, so the sum rounds bit for bit as with fexp.  NaN/inf states reach
+// the sum through its p0 v term, so no select is needed: one DMNMX instead
+// of fexp's integer tests and three selects.
+__device__ __forceinline__ double fexp_addend(double x, const double* tab) {
+    return fexp_core(fmax(x, -708.0), tab);
 }
 
 }  // namespace hyg

@@ -24,11 +24,13 @@
 // uniform state at ambient values is a fixed point bit for bit):
 //   v:  vn = vp + 2a (kp (vR - vp) + km (vL - vp)) / (1 + a (kp + km))
 //   u:  un = up + B (uL + uR - 2 up) + G (vL + vR - (vn + vp)) - Gm (vn - vp)
-//       with B = 2b/(1+2b), G = 2g/(1+2b), Gm = gamma/(1+2b)
+//       with B = 2b/(1+2b), G = 2g/(1+2b), Gm = gamma/(1+2b), evaluated as
+//       up + B (uL + uR - 2 up) + G ((vL - vp) + (vR - vp)) - (G + Gm) inc
+//       where inc is the v row's increment (vn = vp + inc)
 // and the face rows of wall.cpp:218-229, 241-259 (analytic_face) in register
 // 0 of the face lanes, with the ghost-side coefficient d(v_face) (node value).
-// Cost: 38 FP64 instructions per interior node-update (16 of them the half
-// node: fexp is 10), against ~55 in the shared-memory kernels.
+// Cost: 34 FP64 instructions per interior node-update (16 of them the half
+// node: fexp is 10; frcp 3 FMAs), against ~55 in the shared-memory kernels.
 //
 // K3w temporal blocking: a window of W = 32 NPT nodes, S = NPT steps per
 // launch.  An artificial window edge (not a real face) contaminates one node
@@ -73,15 +75,15 @@ __device__ __forceinline__ DvParams dv_params(const double* p) {
 
 __device__ __forceinline__ double d_half(const DvParams& q, double sum, const double* tab) {
     const double e = fma(0.5, sum, -q.p3);
-    const double E = fexp((q.np2 * e) * e, tab);
+    const double E = fexp_addend((q.np2 * e) * e, tab);   // x <= 0 when p2 >= 0
     return fma(q.p1, E, fma(q.hp0, sum, 1.0));
 }
 
 // Interior-row constants of one wall (wall.cpp:199-204).
-struct DvRow { double a, a2, B, G, Gm; };
+struct DvRow { double a, a2, B, G, Gp; };
 
 __device__ __forceinline__ DvRow dv_row(const AnalyticRow& r) {
-    return DvRow{r.a, 2.0 * r.a, 2.0 * r.b * r.inv_u, 2.0 * r.g * r.inv_u, r.gamma * r.inv_u};
+    return DvRow{r.a, 2.0 * r.a, 2.0 * r.b * r.inv_u, 2.0 * r.g * r.inv_u, (2.0 * r.g + r.gamma) * r.inv_u};
 }
 
 __device__ __forceinline__ void dv_interior(const DvRow& r, double vp, double up, double vL, double vR,
@@ -89,13 +91,17 @@ __device__ __forceinline__ void dv_interior(const DvRow& r, double vp, double up
                                             double& un) {
     // symmetric in (L, R) and never contracted (__dmul_rn): a node rounds the
     // same in a reversed lane as in a normal one, so every window computes it
-    // bit for bit alike
-    const double num = __dadd_rn(__dmul_rn(km, vL - vp), __dmul_rn(kp, vR - vp));
+    // bit for bit alike.  The u row reuses the v row's differences and its
+    // increment inc ~ vn - vp: (vL + vR) - (vn + vp) = dl + dr - inc, so
+    // G w - Gm (vn - vp) = G (dl + dr) - (G + Gm) inc (every term vanishes
+    // exactly at a uniform state)
+    const double dl = vL - vp, dr = vR - vp;
+    const double num = __dadd_rn(__dmul_rn(km, dl), __dmul_rn(kp, dr));
     const double den = fma(r.a, kp + km, 1.0);
-    vn = fma(r.a2 * num, frcp(den), vp);
+    const double inc = __dmul_rn(r.a2 * num, frcp(den));
+    vn = __dadd_rn(vp, inc);
     const double du = fma(-2.0, up, uL + uR);
-    const double w = (vL + vR) - (vn + vp);
-    un = fma(-r.Gm, vn - vp, fma(r.G, w, fma(r.B, du, up)));
+    un = fma(-r.Gp, inc, fma(r.G, dl + dr, fma(r.B, du, up)));
 }
 
 // Face row (wall.cpp:218-229, 241-259; analytic_face) with the per-lane
