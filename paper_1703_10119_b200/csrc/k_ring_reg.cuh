@@ -184,16 +184,14 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
     const bool is_own = warp < own_w, is_halo = !is_own && warp < own_w + halo_w;
     unsigned acc = 0;
 
-    for (int b = blockIdx.x, it = 0; b < nblk; b += gridDim.x, ++it) {
-        const int z0 = b * B, nown = min(B, Z - z0);
-        const int L = nown + 2 * S;
-        const int par = it & 1;
-        const bool next = b + static_cast<int>(gridDim.x) < nblk;
-        // role coefficients of this block, loaded before the wait so their
-        // latency hides behind it: owned: interior (3) + register 0's face-capable
-        // row (9) + channel; halo: interior (3) + face 1 (9)
-        double cf[12];
-        int ch = 0;
+    // role coefficients of block bb: owned: interior (3) + register 0's face-capable
+    // row (9) + channel; halo: interior (3) + face 1 (9).  Loaded one block
+    // ahead (block b+1's right after block b's steps, while the owned warps
+    // write their outputs), so the latency of these scattered loads is hidden
+    double cf[12];
+    int ch = 0;
+    auto load_cf = [&](int bb) {
+        const int z0 = bb * B, nown = min(B, Z - z0);
         if (is_own) {
             const int wl = warp * 2 + lane / 16, sub = lane % 16;
             const int w = z0 * W + (wl < nown * W ? wl : 0);
@@ -217,6 +215,14 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
             cf[3] = c.e; cf[4] = c.b; cf[5] = c.e_g; cf[6] = c.c_tv; cf[7] = c.c_sv; cf[8] = c.c_tu;
             cf[9] = c.c_su; cf[10] = c.c_q; cf[11] = c.c_g;
         }
+    };
+    if (static_cast<int>(blockIdx.x) < nblk) load_cf(blockIdx.x);
+
+    for (int b = blockIdx.x, it = 0; b < nblk; b += gridDim.x, ++it) {
+        const int z0 = b * B, nown = min(B, Z - z0);
+        const int L = nown + 2 * S;
+        const int par = it & 1;
+        const bool next = b + static_cast<int>(gridDim.x) < nblk;
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         mbar_wait(mbar, it & 1);                         // the owned walls of block b landed
         __syncthreads();                                 // staging of block b complete
@@ -328,6 +334,7 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
                     x = up[q]; up[q] = uc[q]; uc[q] = x;
                 }
             }
+            if (next) load_cf(b + gridDim.x);
             // out = (layer k+S-1, layer k+S): the warp's two walls through its
             // output scratch, two fields at a time, one bulk store (TMA engine)
             // per field — no store instructions on the warps' path
@@ -432,6 +439,7 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
                 step(vc, vp, uc, up);
             }
             if (k < a.steps) step(vp, vc, up, uc);
+            if (next) load_cf(b + gridDim.x);
         } else {
             // zone thread i: zone_step_explicit (zone.cpp:69-74) of local zone i
             // (1 .. L-2 live; 0 and L-1 contribute their layer-0 air only), with
