@@ -145,6 +145,7 @@ PROTOTYPES = {
     "hyg_probe_fp64_peak": (C.c_int, [C.c_int32, dp, dp]),
     "hyg_probe_fp32_peak": (C.c_int, [C.c_int32, dp]),
     "hyg_selftest_fastmath": (C.c_int, [C.c_int32, C.c_int32, dp, dp, dp]),
+    "hyg_selftest_fastlog": (C.c_int, [C.c_int32, C.c_int32, dp, dp]),
     "hyg_saturation_pressure": (C.c_int, [C.c_double, dp]),
     "hyg_material_evaluate": (C.c_int, [C.c_double, C.c_double, C.c_int32, C.POINTER(CoeffSet)]),
     "hyg_scale_wall": (C.c_int, [dp, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,

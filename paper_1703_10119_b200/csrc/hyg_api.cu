@@ -2208,7 +2208,25 @@ __global__ void k_fastmath(int n, const double* x, double* e, double* r) {
         r[i] = frcp(x[i]);
     }
 }
+__global__ void k_fastlog(int n, const double* x, double* l) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) l[i] = flog_pos(x[i]);
+}
 }  // namespace
+
+extern "C" int hyg_selftest_fastlog(int32_t device, int32_t n, const double* x, double* log_out) {
+    hyg_status* status = nullptr;
+    if (n <= 0 || !x || !log_out) return HYG_EINVAL;
+    HYG_CUDA(cudaSetDevice(device));
+    double* d = nullptr;
+    HYG_CUDA(cudaMalloc(&d, sizeof(double) * 2 * n));
+    HYG_CUDA(cudaMemcpy(d, x, sizeof(double) * n, cudaMemcpyHostToDevice));
+    k_fastlog<<<(n + 255) / 256, 256>>>(n, d, d + n);
+    HYG_CUDA(cudaGetLastError());
+    HYG_CUDA(cudaMemcpy(log_out, d + n, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    return HYG_OK;
+}
 
 extern "C" int hyg_selftest_fastmath(int32_t device, int32_t n, const double* x, double* exp_out,
                                      double* rcp_out) {

@@ -10,6 +10,9 @@
 // (scenario.cpp:161).
 #pragma once
 #include <math.h>
+#if defined(__CUDACC__)
+#include "hyg_fastmath.cuh"
+#endif
 
 #if defined(__CUDACC__)
 #define HYG_HD __host__ __device__ __forceinline__
@@ -96,49 +99,55 @@ HYG_HD bool evaluate_clamped(double T, double P_v, Set& out) {
 //   x^5, x^6 by multiplication,  log10(2 P_v/P_s) = (ln 2 + ln phi) / ln 10,
 //   10^(1.44 - 0.07 log10 r) = exp(1.44 ln 10 - 0.07 ln r),
 // and moisture_storage's -log(P_v/P_s) is the content's -ln(phi) (the same
-// quotient).  4 logs + 5 exps instead of 11 pows + 3 logs + 2 exps; a few ulp
-// per coefficient against the reference's correctly rounded glibc results
-// (parity is asserted on whole runs, tests/test_gpu_material.py).
+// quotient).  4 logs + 5 exps instead of 11 pows + 3 logs + 2 exps, all but
+// the box test's P_s by the table-driven fexp/flog_pos and reciprocal-based
+// quotients of hyg_fastmath.cuh; a few ulp per coefficient against the
+// reference's correctly rounded glibc results (parity is asserted on whole
+// runs, tests/test_gpu_material.py).
 __device__ __forceinline__ bool evaluate_fast(double T, double P_v, Set& out) {
     const double tol = 1e-9;
     const double P_s = (T >= kBoxTMin - tol && T <= kBoxTMax + tol) ? saturation_pressure(T) : 0.0;
     const double phi = P_s > 0.0 ? P_v / P_s : -1.0;
     if (!(P_s > 0.0) || !(phi >= kBoxPhiMin * (1.0 - tol) && phi <= kBoxPhiMax * (1.0 + tol))) return false;
-    const double lphi = log(phi);                      // < 0
+    // inside the box every argument below is positive, normal and bounded:
+    // table-driven exp/log (hyg_fastmath.cuh) and reciprocal-based quotients
+    const double lphi = flog_pos(phi);                 // < 0
     const double rt = kRv * T;
     const double s = rt * (-lphi);                     // specific capillary potential
+    const double iPv = frcp(P_v);
     // first plateau: x1 = C1 s
     const double x1 = kC1 * s;
-    const double l1 = log(x1);
-    const double x1_165 = exp(1.65 * l1);              // x1^1.65
-    const double x1_065 = x1_165 / x1;                 // x1^0.65
+    const double l1 = flog_pos(x1);
+    const double x1_165 = fexp_g(1.65 * l1);           // x1^1.65
+    const double x1_065 = fdiv(x1_165, x1);            // x1^0.65
     const double B1 = 1.0 + x1_165;
-    const double p1 = exp(-0.39 * log(B1));            // (1 + x1^1.65)^-0.39
-    const double p1m = p1 / B1;                        // (1 + x1^1.65)^-1.39
+    const double p1 = fexp_g(-0.39 * flog_pos(B1));    // (1 + x1^1.65)^-0.39
+    const double p1m = fdiv(p1, B1);                   // (1 + x1^1.65)^-1.39
     // second plateau: x2 = C2 s
     const double x2 = kC2 * s;
     const double x2_2 = x2 * x2;
     const double x2_5 = x2_2 * x2_2 * x2;
     const double x2_6 = x2_5 * x2;
     const double B2 = 1.0 + x2_6;
-    const double p2 = exp(-0.83 * log(B2));            // (1 + x2^6)^-0.83
-    const double p2m = p2 / B2;                        // (1 + x2^6)^-1.83
+    const double p2 = fexp_g(-0.83 * flog_pos(B2));    // (1 + x2^6)^-0.83
+    const double p2m = fdiv(p2, B2);                   // (1 + x2^6)^-1.83
     const double f = 47.1 * p1 + 109.9 * p2;           // moisture_content
     // moisture_storage (materials.cpp:80-89)
-    const double t1 = 30.62 * (kC1 * rt / P_v) * x1_065 * p1m;
-    const double t2 = 549.5 * (kC2 * rt / P_v) * x2_5 * p2m;
+    const double t1 = 30.62 * (kC1 * rt * iPv) * x1_065 * p1m;
+    const double t2 = 549.5 * (kC2 * rt * iPv) * x2_5 * p2m;
     const double c_M = t1 + t2;
-    // moisture_transport (materials.cpp:74-78): r = 2 phi
-    const double r = 2.0 * P_v / P_s;
+    // moisture_transport (materials.cpp:74-78): r = 2 P_v / P_s = 2 phi exactly
+    const double r = 2.0 * phi;
     const double lr = 0.69314718055994530942 + lphi;
-    const double k_M = 1.97e-10 * exp(1.44 * 2.30258509299404568402 - 0.07 * lr) +
-                       1.77e-7 * exp(-8.0 * (r - 2.0) * (r - 2.0));
+    const double k_M = 1.97e-10 * fexp_g(1.44 * 2.30258509299404568402 - 0.07 * lr) +
+                       1.77e-7 * fexp_g(-8.0 * (r - 2.0) * (r - 2.0));
     out.c_M = c_M;
     out.k_M = k_M;
     out.c_TT = kRho0 * kC0 + kCw * f;
     out.k_TT = thermal_conductivity(f);
     out.c_TM = kCw * (T - 273.15) * c_M;
-    out.k_TM = kLv * vapour_permeability(T, f);
+    const double z = 1.0 - f * (1.0 / kSat);           // vapour_permeability (materials.cpp:65-68)
+    out.k_TM = kLv * (1.88e-6 * frcp(T) * z * frcp(0.503 * z * z + 0.497));
     return true;
 }
 #endif
@@ -160,12 +169,21 @@ HYG_HD bool star(double u, double v, double T_i, double P_vi, const Set& ref, bo
     const bool ok = strict ? evaluate(u * T_i, v * P_vi, a) : evaluate_clamped(u * T_i, v * P_vi, a);
 #endif
     if (!ok) return false;
+#if defined(__CUDA_ARCH__)
+    out.c_M = fdiv(a.c_M, ref.c_M);
+    out.k_M = fdiv(a.k_M, ref.k_M);
+    out.c_TT = fdiv(a.c_TT, ref.c_TT);
+    out.k_TT = fdiv(a.k_TT, ref.k_TT);
+    out.c_TM = fdiv(a.c_TM, ref.c_TM);
+    out.k_TM = fdiv(a.k_TM, ref.k_TM);
+#else
     out.c_M = a.c_M / ref.c_M;
     out.k_M = a.k_M / ref.k_M;
     out.c_TT = a.c_TT / ref.c_TT;
     out.k_TT = a.k_TT / ref.k_TT;
     out.c_TM = a.c_TM / ref.c_TM;
     out.k_TM = a.k_TM / ref.k_TM;
+#endif
     return true;
 }
 

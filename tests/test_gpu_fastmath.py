@@ -35,3 +35,20 @@ def test_fexp_frcp_accuracy():
     assert _ulps(rr, 1.0 / nz).max() <= 2.0
     e2, _ = _run(np.array([-800.0, -708.5, np.nan, 710.0, 0.0]))
     assert e2[0] == 0.0 and e2[1] == 0.0 and np.isnan(e2[2]) and np.isinf(e2[3]) and e2[4] == 1.0
+
+
+def test_flog_accuracy():
+    """flog_pos (material correlations): within 2 ulp of the result, or 2 ulp
+    of ln 2 where ln x cancels near 1 (absolute 2.5e-16), on the box's ranges
+    (phi in [0.01, 0.99], capillary potentials, 1 + x^a) and far beyond."""
+    lib = api.load_library()
+    rng = np.random.default_rng(1)
+    x = np.concatenate([rng.uniform(0.01, 0.99, 200_000), 10.0 ** rng.uniform(-300, 300, 100_000),
+                        1.0 + 10.0 ** rng.uniform(-16, 2, 50_000), np.array([1.0, 2.0, 0.5, 1e-300, 1e300])])
+    out = np.empty_like(x)
+    p = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+    assert lib.hyg_selftest_fastlog(0, x.size, p(x), p(out)) == 0
+    ref = np.log(x)
+    err = np.abs(out - ref)
+    assert np.all(err <= np.maximum(2.0 * np.spacing(np.abs(ref)), 2.0 * np.spacing(np.log(2.0))))
+    assert out[-5] == 0.0
