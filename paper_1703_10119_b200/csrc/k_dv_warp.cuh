@@ -29,8 +29,8 @@
 //       where inc is the v row's increment (vn = vp + inc)
 // and the face rows of wall.cpp:218-229, 241-259 (analytic_face) in register
 // 0 of the face lanes, with the ghost-side coefficient d(v_face) (node value).
-// Cost: 34 FP64 instructions per interior node-update (16 of them the half
-// node: fexp is 10; frcp 3 FMAs), against ~55 in the shared-memory kernels.
+// Cost: 33 FP64 instructions per interior node-update (15 of them the half
+// node: fexp is 10 + the clamp; frcp 3 FMAs), against ~55 in the shared-memory kernels.
 //
 // K3w temporal blocking: a window of W = 32 NPT nodes, S = NPT steps per
 // launch.  An artificial window edge (not a real face) contaminates one node
@@ -67,15 +67,18 @@ struct TiledArgs {
 // d(v) = 1 + p0 v + p1 exp(-p2 (v - p3)^2) at a half node, from the SUM of its
 // two node values (midpoint = sum/2 is exact; e and p0 v round as the
 // reference's midpoint form).  For a node value pass 2 v.
-struct DvParams { double hp0, np2, p3, p1; };
+// The exponent -p2 (m - p3)^2 is -(e e) with e = sqrt(p2) (m - p3) from one
+// FMA (p2 >= 0 on this path, hyg_create), one DMUL fewer than (-p2 e) e.
+struct DvParams { double hp0, hsq, nsqp3, p1; };
 
 __device__ __forceinline__ DvParams dv_params(const double* p) {
-    return DvParams{0.5 * p[0], -p[2], p[3], p[1]};
+    const double sq = sqrt(p[2]);
+    return DvParams{0.5 * p[0], 0.5 * sq, -p[3] * sq, p[1]};
 }
 
 __device__ __forceinline__ double d_half(const DvParams& q, double sum, const double* tab) {
-    const double e = fma(0.5, sum, -q.p3);
-    const double E = fexp_addend((q.np2 * e) * e, tab);   // x <= 0 when p2 >= 0
+    const double e = fma(q.hsq, sum, q.nsqp3);
+    const double E = fexp_addend(-(e * e), tab);
     return fma(q.p1, E, fma(q.hp0, sum, 1.0));
 }
 
