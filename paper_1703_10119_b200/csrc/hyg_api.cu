@@ -2296,3 +2296,10 @@ extern "C" int hyg_probe_fp64_peak(int32_t device, double* tflops, double* sm_cl
     if (sm_clock_mhz) *sm_clock_mhz = clk / 1000.0;
     return HYG_OK;
 }
+
+#if RING_PROF
+// timing variants only (tools/_ringvar): the K4r phase stamps of CTA 0
+extern "C" int hyg_ring_prof_read(unsigned long long* out, int n) {
+    return cudaMemcpyFromSymbol(out, g_ring_prof, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 5;
+}
+#endif

@@ -34,9 +34,26 @@
 #include "k_ring.cuh"
 
 // timing experiments only (tools/ring_step_probe.py): skip the arithmetic of
-// roles (1 halo, 2 zone, 4 owned); 0 in the library
+// roles (1 halo, 2 zone, 4 owned), the owned walls' outputs (8), their bulk
+// loads (16), the other prefetches (32); 0 in the library
+#ifndef RING_VSTORE
+#define RING_VSTORE 0
+#endif
 #ifndef RING_SKIP
 #define RING_SKIP 0
+#endif
+// timing experiments only: per-phase clock64 stamps of CTA 0 (owned warp 0,
+// the zone warp) into g_ring_prof[block iteration][event]; 0 in the library
+#ifndef RING_PROF
+#define RING_PROF 0
+#endif
+#if RING_PROF
+__device__ unsigned long long g_ring_prof[32 * 16];
+#define RPROF(e) do { if (blockIdx.x == 0 && tid == 0 && it < 32) g_ring_prof[it * 16 + (e)] = clock64(); } while (0)
+#define ZPROF(e) do { if (blockIdx.x == 0 && tid == 32 * (own_w + halo_w) && it < 32) g_ring_prof[it * 16 + 10 + (e)] = clock64(); } while (0)
+#else
+#define RPROF(e) do { } while (0)
+#define ZPROF(e) do { } while (0)
 #endif
 
 namespace hyg {
@@ -45,6 +62,9 @@ template <int NPT, int S>
 struct RingRegShape {
     static constexpr int kP = S + 1;                           // nodes kept per halo wall
     static constexpr int kHaloZones = 2 * (S - 1);
+    // shared stride of a zone's parameter block: odd, so the zone warp's lanes
+    // (one zone each) read distinct banks (56 put every lane on two banks)
+    static constexpr int kZPS = kRingZP + 1;
     __host__ __device__ static int own_warps(int B, int W) { return (B * W + 1) / 2; }
     __host__ __device__ static int halo_walls(int W) { return kHaloZones * W; }
     __host__ __device__ static int halo_warps(int W) { return (halo_walls(W) + 31) / 32; }
@@ -58,7 +78,7 @@ struct RingRegShape {
     __host__ __device__ static size_t smem_doubles(int B, int W, int n, int rw) {
         const size_t LB = local_zones(B);
         return static_cast<size_t>(4) * B * W * n + static_cast<size_t>(4) * halo_walls(W) * kP +
-               2 * LB * kRingZP + 4 * LB + 4 * static_cast<size_t>(B * W + halo_walls(W)) + 4 * LB +
+               2 * LB * kZPS + 4 * LB + 4 * static_cast<size_t>(B * W + halo_walls(W)) + 4 * LB +
                static_cast<size_t>(S) * rw + 1 + static_cast<size_t>(own_warps(B, W)) * 2 * 2 * n;
     }
 };
@@ -111,8 +131,9 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
     // shared layout (integer offsets; every access a shared-space access)
     const int oSO = 0;                                  // staging owned [4][OW][N] (linear: bulk copies)
     const int oSH = oSO + 4 * OW * N;                   // staging halo [4][HW][P]
-    const int oZS = oSH + 4 * HW * P;                   // staged zone parameters [2][LB][kRingZP]
-    const int oZA = oZS + 2 * LB * kRingZP;             // staged zone air [2][2][LB]
+    constexpr int ZPS = Sh::kZPS;
+    const int oZS = oSH + 4 * HW * P;                   // staged zone parameters [2][LB][ZPS]
+    const int oZA = oZS + 2 * LB * ZPS;                 // staged zone air [2][2][LB]
     const int oSF = oZA + 4 * LB;                       // surfaces [parity][field][OW + HW]
     const int oAR = oSF + 4 * (OW + HW);                // zone air [parity][field][LB]
     const int oRW = oAR + 4 * LB;                       // forcing rows [S][rw]
@@ -120,7 +141,13 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
     const int oOUT = oMB + 2;                           // output scratch [own warps][2][2 N] (16-byte aligned)
     void* mbar = &smem[oMB];
     auto so_ix = [&](int f, int i) { return oSO + f * OW * N + i; };
+    // surfaces: slot of owned wall (zone z, wall q) = q B + z, of halo wall
+    // (halo zone h, wall q) = OW + q HZ + h: the zone warp's lanes (one zone
+    // each) read consecutive slots
+    constexpr int HZ = Sh::kHaloZones;
     auto sf_ix = [&](int par, int f, int i) { return oSF + (par * 2 + f) * (OW + HW) + i; };
+    auto own_slot = [&](int wl) { const int z = wl / W; return (wl - z * W) * B + z; };
+    auto halo_slot = [&](int hl) { const int h = hl / W; return OW + (hl - h * W) * HZ + h; };
     auto ar_ix = [&](int par, int f, int i) { return oAR + (par * 2 + f) * LB + i; };
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int nblk = (Z + B - 1) / B;
@@ -147,11 +174,15 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
     auto prefetch = [&](int b, int par) {
         const int z0 = b * B, nown = min(B, Z - z0), L = nown + 2 * S;
         if (tid == 0) {   // the owned walls of the block: one contiguous range per field
-            const unsigned bytes = static_cast<unsigned>(nown * W * N * sizeof(double));
+            const unsigned bytes = (RING_SKIP & 16) ? 0u : static_cast<unsigned>(nown * W * N * sizeof(double));
             mbar_expect_tx(mbar, 4 * bytes);
 #pragma unroll
-            for (int f = 0; f < 4; ++f)
+            for (int f = 0; f < 4 * !(RING_SKIP & 16); ++f)
                 bulk_g2s(&smem[so_ix(f, 0)], a.in[f] + static_cast<size_t>(z0) * W * N, bytes, mbar);
+        }
+        if (RING_SKIP & 32) {
+            asm volatile("cp.async.commit_group;\n" ::);
+            return;
         }
         for (int i = tid; i < HW * P; i += nthr) {
             const int hl = i / P, p = i - hl * P;
@@ -160,10 +191,9 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
 #pragma unroll
             for (int f = 0; f < 4; ++f) cp_async8(&smem[oSH + f * HW * P + i], a.in[f] + g);
         }
-        for (int i = tid; i < L * (kRingZP / 2); i += nthr) {
-            const int li = i / (kRingZP / 2), c = i - li * (kRingZP / 2);
-            cp_async16(&smem[oZS + (par * LB + li) * kRingZP + 2 * c],
-                       a.zparams + static_cast<size_t>(gz(z0, li)) * kRingZP + 2 * c);
+        for (int i = tid; i < L * kRingZP; i += nthr) {
+            const int li = i / kRingZP, c = i - li * kRingZP;
+            cp_async8(&smem[oZS + (par * LB + li) * ZPS + c], a.zparams + static_cast<size_t>(gz(z0, li)) * kRingZP + c);
         }
         for (int i = tid; i < 2 * L; i += nthr) {
             const int f = i / L, li = i - f * L;
@@ -197,12 +227,12 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
             const int w = z0 * W + (wl < nown * W ? wl : 0);
             const WallCoef& wc = a.coef[w];
             cf[0] = wc.in.b; cf[1] = wc.in.c_su; cf[2] = wc.in.c_sv;
-            const bool first = sub == 0, rev = sub == 15;
-            const RowCoef& c = wc.face[first ? 0 : 1];
-            const bool m0 = first || rev;
-            cf[3] = m0 ? c.e : 0.0; cf[4] = m0 ? c.b : cf[0]; cf[5] = m0 ? c.e_g : 0.0;
-            cf[6] = m0 ? c.c_tv : 0.0; cf[7] = m0 ? c.c_sv : cf[2]; cf[8] = m0 ? c.c_tu : 0.0;
-            cf[9] = m0 ? c.c_su : cf[1]; cf[10] = m0 ? c.c_q : 0.0; cf[11] = m0 ? c.c_g : 0.0;
+            // register 0's row: a face row in the face lanes, else the interior row,
+            // whose face terms are 0 (hyg_coef.cuh) — picked by address, so no
+            // select waits on the loads (they complete behind the outputs)
+            const RowCoef& c = sub == 0 ? wc.face[0] : (sub == 15 ? wc.face[1] : wc.in);
+            cf[3] = c.e; cf[4] = c.b; cf[5] = c.e_g; cf[6] = c.c_tv; cf[7] = c.c_sv; cf[8] = c.c_tu;
+            cf[9] = c.c_su; cf[10] = c.c_q; cf[11] = c.c_g;
             ch = a.attach[2 * w].index;
         } else if (is_halo) {
             const int hl = (warp - own_w) * 32 + lane;
@@ -223,9 +253,11 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
         const int L = nown + 2 * S;
         const int par = it & 1;
         const bool next = b + static_cast<int>(gridDim.x) < nblk;
+        RPROF(0);
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         mbar_wait(mbar, it & 1);                         // the owned walls of block b landed
         __syncthreads();                                 // staging of block b complete
+        RPROF(1);
         int cur = 0;                                     // parity of the layer-k shared slots
         if (is_own) {
             // owned wall wl (two per warp), 16 lanes of NPT nodes, last lane reversed
@@ -269,17 +301,21 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
             rd(1, uc);
             rd(2, vp);
             rd(3, vc);
+            RPROF(2);
             __syncthreads();                             // (A) staging consumed by every role
             if (next) prefetch(b + gridDim.x, par ^ 1);
+            RPROF(3);
             const double cb = cf[0], csu = cf[1], csv = cf[2];
             // register 0's face-capable row (interior coefficients, zero face terms elsewhere)
             const double fe = cf[3], fb = cf[4], feg = cf[5], fctv = cf[6], fcsv = cf[7], fctu = cf[8], fcsu = cf[9],
                          fcq = cf[10], fcg = cf[11];
             if (rev && live) {                           // layer-k surface sample (node N-1)
-                smem[sf_ix(0, 0, wl)] = uc[0];
-                smem[sf_ix(0, 1, wl)] = vc[0];
+                smem[sf_ix(0, 0, own_slot(wl))] = uc[0];
+                smem[sf_ix(0, 1, own_slot(wl))] = vc[0];
             }
             __syncthreads();                             // (B) layer-k surfaces and air published
+            RPROF(4);
+            const int oslot = own_slot(wlc);
             auto step = [&](double (&vP)[NPT], double (&vC)[NPT], double (&uP)[NPT], double (&uC)[NPT], int k) {
                 // face inputs of register 0, branch-free (wall.cpp:162-169, 177-189;
                 // coupled_node): x=0 the exterior channel, x=1 the zone's layer-k air
@@ -315,8 +351,8 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
                     uP[q] = un;
                 }
                 if (rev && live) {
-                    smem[sf_ix(cur ^ 1, 0, wl)] = uP[0];
-                    smem[sf_ix(cur ^ 1, 1, wl)] = vP[0];
+                    smem[sf_ix(cur ^ 1, 0, oslot)] = uP[0];
+                    smem[sf_ix(cur ^ 1, 1, oslot)] = vP[0];
                 }
                 __syncthreads();
                 cur ^= 1;
@@ -334,7 +370,9 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
                     x = up[q]; up[q] = uc[q]; uc[q] = x;
                 }
             }
+            RPROF(5);
             if (next) load_cf(b + gridDim.x);
+            RPROF(6);
             // out = (layer k+S-1, layer k+S): the warp's two walls through its
             // output scratch, two fields at a time, one bulk store (TMA engine)
             // per field — no store instructions on the warps' path
@@ -367,14 +405,29 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
                 if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
                 __syncwarp();
             };
-            drained();
-            wr(0, up);
-            wr(1, uc);
-            flush(0);
-            drained();
-            wr(0, vp);
-            wr(1, vc);
-            flush(2);
+            if (!(RING_SKIP & 8)) {
+                drained();
+                wr(0, up);
+                wr(1, uc);
+                flush(0);
+#if RING_VSTORE
+                if (wl < nown * W) {   // v fields straight from registers (16-byte stores)
+                    double* g2 = a.out[2] + (static_cast<size_t>(z0) * W + wl) * N + sub * NPT;
+                    double* g3 = a.out[3] + (static_cast<size_t>(z0) * W + wl) * N + sub * NPT;
+#pragma unroll
+                    for (int q = 0; q < NPT; q += 2) {
+                        *reinterpret_cast<double2*>(g2 + q) = rev ? make_double2(vp[NPT - 1 - q], vp[NPT - 2 - q]) : make_double2(vp[q], vp[q + 1]);
+                        *reinterpret_cast<double2*>(g3 + q) = rev ? make_double2(vc[NPT - 1 - q], vc[NPT - 2 - q]) : make_double2(vc[q], vc[q + 1]);
+                    }
+                }
+#else
+                if (!(RING_SKIP & 64)) drained();
+                wr(0, vp);
+                wr(1, vc);
+                flush(2);
+#endif
+            }
+            RPROF(7);
         } else if (is_halo) {
             // halo wall: global nodes N-P .. N-1; the cut end (p = 0) mirrors
             // itself — its error moves inward one node per step and never
@@ -401,10 +454,11 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
             c.e = cf[3]; c.b = cf[4]; c.e_g = cf[5]; c.c_tv = cf[6]; c.c_sv = cf[7]; c.c_tu = cf[8];
             c.c_su = cf[9]; c.c_q = cf[10]; c.c_g = cf[11];
             if (live) {
-                smem[sf_ix(0, 0, OW + hl)] = uc[P - 1];
-                smem[sf_ix(0, 1, OW + hl)] = vc[P - 1];
+                smem[sf_ix(0, 0, halo_slot(hl))] = uc[P - 1];
+                smem[sf_ix(0, 1, halo_slot(hl))] = vc[P - 1];
             }
             __syncthreads();                             // (B)
+            const int hslot = halo_slot(hlc);
             auto step = [&](double (&vP)[P], double (&vC)[P], double (&uP)[P], double (&uC)[P]) {
                 const double u_a = smem[ar_ix(cur, 0, li)], v_a = smem[ar_ix(cur, 1, li)];
 #pragma unroll
@@ -427,8 +481,8 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
                     uP[p] = un;
                 }
                 if (live) {
-                    smem[sf_ix(cur ^ 1, 0, OW + hl)] = uP[P - 1];
-                    smem[sf_ix(cur ^ 1, 1, OW + hl)] = vP[P - 1];
+                    smem[sf_ix(cur ^ 1, 0, hslot)] = uP[P - 1];
+                    smem[sf_ix(cur ^ 1, 1, hslot)] = vP[P - 1];
                 }
                 __syncthreads();
                 cur ^= 1;
@@ -452,7 +506,7 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
             const bool live = i >= 1 && i < L - 1;
             const bool owned = i >= S && i < S + nown;
             const int hz = i < S ? i - 1 : (S - 1) + (i - S - nown);
-            const int zp = oZS + (par * LB + (valid ? i : 0)) * kRingZP;
+            const int zp = oZS + (par * LB + (valid ? i : 0)) * ZPS;
             int nlink = 0, npeer = 0, sidx = 0;
             int ls[NL], pidx[NP];
             if (live) {
@@ -463,7 +517,7 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
 #pragma unroll
             for (int q = 0; q < NL; ++q) {
                 const int wi = q < nlink ? static_cast<int>(smem[zp + 8 + 4 * q]) : 0;
-                ls[q] = owned ? (i - S) * W + wi : OW + hz * W + wi;
+                ls[q] = owned ? wi * B + (i - S) : OW + wi * HZ + hz;
             }
 #pragma unroll
             for (int q = 0; q < NP; ++q) {
@@ -474,9 +528,11 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
                 smem[ar_ix(0, 0, i)] = smem[oZA + (par * 2 + 0) * LB + i];
                 smem[ar_ix(0, 1, i)] = smem[oZA + (par * 2 + 1) * LB + i];
             }
+            ZPROF(0);
             __syncthreads();                             // (A) staging consumed
             if (next) prefetch(b + gridDim.x, par ^ 1);
             __syncthreads();                             // (B) layer-k surfaces and air published
+            ZPROF(1);
             for (int k = 0; k < a.steps; ++k) {
                 if (live && !(RING_SKIP & 2)) {
                     const double u_a = smem[ar_ix(cur, 0, i)], v_a = smem[ar_ix(cur, 1, i)];
@@ -510,6 +566,7 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
                 __syncthreads();
                 cur ^= 1;
             }
+            ZPROF(2);
             if (owned) {
                 const int z = gz(z0, i);
                 a.zu_out[z] = smem[ar_ix(cur, 0, i)];
@@ -517,10 +574,12 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
             }
         }
         __syncthreads();                                 // the shared slots are reused by the next block
+        RPROF(8);
     }
     if (is_own && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // stores drained
     // fast guard verdict of the whole launch (bit 30: |x| >= 2 or not finite)
-    if (__syncthreads_or((acc & 0x40000000u) != 0u) && tid == 0) atomicCAS(a.stop, 0, a.seg_index + 1);
+    // (timing variants march stale staging: their verdict is dropped)
+    if (__syncthreads_or((acc & 0x40000000u) != 0u) && tid == 0 && RING_SKIP < 8) atomicCAS(a.stop, 0, a.seg_index + 1);
 }
 
 }  // namespace hyg
