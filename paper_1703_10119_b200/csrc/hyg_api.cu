@@ -939,7 +939,7 @@ int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
         // 16-byte aligned windows: T and NPT even, the buffers 256-byte aligned
         static int per_sm = 0, n_sm = 0;
         if (!per_sm) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dv_tiled_stream<kTileNPT>, kDvWarps * 32, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dv_tiled_stream<kTileNPT, kK3MinB>, kDvWarps * 32, 0);
             cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, c->device);
             per_sm = std::max(per_sm, 1);
         }
@@ -961,7 +961,7 @@ int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
             }
             {
                 LaunchScope ls(c, "df_analytic_tiled", mid_cells * a.steps);
-                if (grid > 0) k_dv_tiled_stream<kTileNPT><<<grid, kDvWarps * 32, 0, c->stream>>>(a);
+                if (grid > 0) k_dv_tiled_stream<kTileNPT, kK3MinB><<<grid, kDvWarps * 32, 0, c->stream>>>(a);
             }
             LaunchScope ls(c, "df_analytic_tiled_faces", face_cells * a.steps);
             k_dv_tiled<kTileNPT, true><<<1, kDvWarps * 32, 0, c->stream>>>(a);

@@ -69,16 +69,25 @@ struct TiledArgs {
 // reference's midpoint form).  For a node value pass 2 v.
 // The exponent -p2 (m - p3)^2 is -(e e) with e = sqrt(p2) (m - p3) from one
 // FMA (p2 >= 0 on this path, hyg_create), one DMUL fewer than (-p2 e) e.
-struct DvParams { double hp0, hsq, nsqp3, p1; };
+struct DvParams { double hp0, hsq, nsqp3, p1, np2, p3; };
 
 __device__ __forceinline__ DvParams dv_params(const double* p) {
     const double sq = sqrt(p[2]);
-    return DvParams{0.5 * p[0], 0.5 * sq, -p[3] * sq, p[1]};
+    return DvParams{0.5 * p[0], 0.5 * sq, -p[3] * sq, p[1], -p[2], p[3]};
 }
 
 __device__ __forceinline__ double d_half(const DvParams& q, double sum, const double* tab) {
     const double e = fma(q.hsq, sum, q.nsqp3);
     const double E = fexp_addend(-(e * e), tab);
+    return fma(q.p1, E, fma(q.hp0, sum, 1.0));
+}
+
+// The same with the exponent as (-p2 e) e, e = m - p3: one DMUL more, but
+// measured 5 % faster in the latency-bound single-wall march (K2s), where
+// the compiler's schedule of the three exps per lane differs.
+__device__ __forceinline__ double d_half_lat(const DvParams& q, double sum, const double* tab) {
+    const double e = fma(0.5, sum, -q.p3);
+    const double E = fexp_addend((q.np2 * e) * e, tab);
     return fma(q.p1, E, fma(q.hp0, sum, 1.0));
 }
 
@@ -209,6 +218,9 @@ __device__ __forceinline__ void dv_step(double (&vP)[NPT], const double (&vC)[NP
 }
 
 constexpr int kDvWarps = 4;     // walls (K2w) or windows (K3w) per CTA
+// K3w: 3 CTAs (12 warps) per SM — caps registers at 168 (uncapped the
+// compiler takes 222 and only 8 warps fit)
+constexpr int kK3MinB = 3;
 
 // K2w: one warp per wall, n <= 32 NPT, all steps of a segment in one launch.
 // The host picks NPT = the smallest power of two >= n/32 and M = n - Lr NPT
@@ -328,15 +340,15 @@ __global__ void __launch_bounds__(NW * 32) k_dv_wall_split(const NonlinearSegArg
             double vR = __shfl_down_sync(FULL, vc, 1), uR = __shfl_down_sync(FULL, uc, 1);
             if (lane == 0 && warp > 0) { vL = s_x[b][warp - 1][2]; uL = s_x[b][warp - 1][3]; }
             if (lane == 31 && warp < NW - 1) { vR = s_x[b][warp + 1][0]; uR = s_x[b][warp + 1][1]; }
-            const double hL = d_half(q, vL + vc, s_tab);
-            const double hR = d_half(q, vc + vR, s_tab);
+            const double hL = d_half_lat(q, vL + vc, s_tab);
+            const double hR = d_half_lat(q, vc + vR, s_tab);
             double vn, un;
             dv_interior(r, vp, up, vL, vR, uL, uR, hL, hR, vn, un);
             if (FACE_ALL || face_warp) {
                 // branch-free inside the warp: the face chain runs beside the
                 // interior one, not after it.  Ghost side d(v_face); the row
                 // needs the interior neighbour only.
-                const double dnode = d_half(q, vc + vc, s_tab);
+                const double dnode = d_half_lat(q, vc + vc, s_tab);
                 double vf, uf;
                 dv_face(fc, s_amb[s][rf ? 1 : 0], vp, up, rf ? vL : vR, rf ? uL : uR, dnode, rf ? hL : hR, vf, uf);
                 vn = (lf || rf) ? vf : vn;
