@@ -33,6 +33,10 @@ namespace {
 
 constexpr int kChunk = 128;     // forcing rows staged per shared-memory chunk
 constexpr int kRingS = 8;       // K4: steps per launch (halo depth S-1 zones)
+#ifndef HYG_RING_REG_S
+#define HYG_RING_REG_S 8
+#endif
+constexpr int kRingRegS = HYG_RING_REG_S;   // K4r: steps per launch (S = 9 measured 3.12e11 vs 3.49e11 at 8: spills)
 constexpr int kWarps = 4;       // warps per CTA of K1
 
 struct SigHost {
@@ -991,11 +995,11 @@ int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
 template <int NPT>
 void launch_ring_reg(const RingArgs& a, int threads, size_t smem, cudaStream_t s, int device, bool small) {
     // small: every zone has <= 6 wall links and <= 2 ring peers (configs[3])
-    auto k = small ? k_ring_reg<NPT, kRingS, 6, 2> : k_ring_reg<NPT, kRingS>;
+    auto k = small ? k_ring_reg<NPT, kRingRegS, 6, 2> : k_ring_reg<NPT, kRingRegS>;
     static int n_sm = 0;
     if (!n_sm) {
-        cudaFuncSetAttribute(k_ring_reg<NPT, kRingS, 6, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(k_ring_reg<NPT, kRingS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_ring_reg<NPT, kRingRegS, 6, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_ring_reg<NPT, kRingRegS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device);
     }
     int per_sm = 1;
@@ -1032,12 +1036,13 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool
     const int B = reg ? c->ring_reg_B : c->ring_B;
     const int grid = (Z + B - 1) / B;
     const int rw = RingShape<8, kRingS>::row_width(nch, nsrc);
-    const int threads = reg ? RingRegShape<8, kRingS>::threads(B, W) : RingShape<8, kRingS>::threads(B, W);
-    const size_t smem = reg ? RingRegShape<8, kRingS>::smem_doubles(B, W, c->n, rw) * sizeof(double)
+    const int S = reg ? kRingRegS : kRingS;             // steps per launch
+    const int threads = reg ? RingRegShape<8, kRingRegS>::threads(B, W) : RingShape<8, kRingS>::threads(B, W);
+    const size_t smem = reg ? RingRegShape<8, kRingRegS>::smem_doubles(B, W, c->n, rw) * sizeof(double)
                         : npt == 4 ? RingShape<4, kRingS>::smem_bytes(B, W, nch, nsrc)
                         : npt == 8 ? RingShape<8, kRingS>::smem_bytes(B, W, nch, nsrc)
                                    : RingShape<16, kRingS>::smem_bytes(B, W, nch, nsrc);
-    const int64_t block = 65536 / kRingS * kRingS;
+    const int64_t block = 65536 / S * S;
     for (int64_t done = 0; done < nsteps;) {
         const int64_t rows = std::min(block, nsteps - done);
         std::vector<double> times(rows);
@@ -1070,8 +1075,8 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool
         a.stop = c->d_flag;
         const int cur0 = c->cur, z0 = c->zcur;
         int nseg = 0;
-        for (int64_t s0 = 0; s0 < rows; s0 += kRingS, ++nseg) {
-            a.steps = static_cast<int>(std::min<int64_t>(kRingS, rows - s0));
+        for (int64_t s0 = 0; s0 < rows; s0 += S, ++nseg) {
+            a.steps = static_cast<int>(std::min<int64_t>(S, rows - s0));
             a.seg_index = nseg;
             a.table = c->d_table + s0 * nch;
             a.src = c->d_src + s0 * (3 * nsrc + 2);
@@ -1106,7 +1111,7 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool
         }
         // the guard fired in launch K (its input intact): K4r -> K4 (exact guard)
         // from there, K4 -> the exact per-step path
-        const int64_t k0 = static_cast<int64_t>(flag - 1) * kRingS;
+        const int64_t k0 = static_cast<int64_t>(flag - 1) * S;
         c->cur = (cur0 + flag - 1) & 1;
         c->zcur = (z0 + flag - 1) & 1;
         c->t = times[k0];
@@ -1415,11 +1420,11 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
             while (B > 0 && !fits(B)) --B;
             if (B >= 1 && (npt == 4 || npt == 8)) {
                 // K4r: the largest block whose roles fit 512 threads (128 registers each)
-                int Br = std::min(Z, 32 - 2 * kRingS);
+                int Br = std::min(Z, 32 - 2 * kRingRegS);
                 auto fits_r = [&](int b) {
                     const int rw = RingShape<8, kRingS>::row_width(nch, nsrc);
-                    return RingRegShape<8, kRingS>::threads(b, W) <= 512 &&
-                           RingRegShape<8, kRingS>::smem_doubles(b, W, c->n, rw) * sizeof(double) <= 227u * 1024u;
+                    return RingRegShape<8, kRingRegS>::threads(b, W) <= kRingRegThreads &&
+                           RingRegShape<8, kRingRegS>::smem_doubles(b, W, c->n, rw) * sizeof(double) <= 227u * 1024u;
                 };
                 while (Br > 0 && !fits_r(Br)) --Br;
                 c->ring_reg_B = Br;

@@ -58,6 +58,13 @@ __device__ unsigned long long g_ring_prof[32 * 16];
 
 namespace hyg {
 
+// K4r CTA size cap: 16 warps (12 owned + 3 halo + 1 zone at B = 4, W = 6, S = 8),
+// 128 registers per thread (ptxas sizes registers for whole 4-warp groups)
+#ifndef HYG_RING_REG_THREADS
+#define HYG_RING_REG_THREADS 512
+#endif
+constexpr int kRingRegThreads = HYG_RING_REG_THREADS;
+
 template <int NPT, int S>
 struct RingRegShape {
     static constexpr int kP = S + 1;                           // nodes kept per halo wall
@@ -79,7 +86,8 @@ struct RingRegShape {
         const size_t LB = local_zones(B);
         return static_cast<size_t>(4) * B * W * n + static_cast<size_t>(4) * halo_walls(W) * kP +
                2 * LB * kZPS + 4 * LB + 4 * static_cast<size_t>(B * W + halo_walls(W)) + 4 * LB +
-               static_cast<size_t>(S) * rw + 1 + static_cast<size_t>(own_warps(B, W)) * 2 * 2 * n;
+               ((static_cast<size_t>(S) * rw + 1) & ~static_cast<size_t>(1)) + 2 +
+               static_cast<size_t>(own_warps(B, W)) * 2 * 2 * n;
     }
 };
 
@@ -119,7 +127,7 @@ __device__ __forceinline__ void cp_async16(double* smem_dst, const double* gsrc)
 // NL, NP: link and peer slots walked per zone (compile-time, branch-free; the
 // host picks the smallest instantiation that covers every zone)
 template <int NPT, int S, int NL = kRingMaxLinks, int NP = kRingMaxPeers>
-__global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
+__global__ void __launch_bounds__(kRingRegThreads, 1) k_ring_reg(const RingArgs a) {
     using Sh = RingRegShape<NPT, S>;
     constexpr int P = Sh::kP, N = 16 * NPT;
     constexpr unsigned FULL = 0xffffffffu;
@@ -137,7 +145,7 @@ __global__ void __launch_bounds__(512, 1) k_ring_reg(const RingArgs a) {
     const int oSF = oZA + 4 * LB;                       // surfaces [parity][field][OW + HW]
     const int oAR = oSF + 4 * (OW + HW);                // zone air [parity][field][LB]
     const int oRW = oAR + 4 * LB;                       // forcing rows [S][rw]
-    const int oMB = oRW + S * rw;                       // mbarrier of the owned-wall bulk copies
+    const int oMB = oRW + ((S * rw + 1) & ~1);          // mbarrier of the owned-wall bulk copies (16-byte aligned)
     const int oOUT = oMB + 2;                           // output scratch [own warps][2][2 N] (16-byte aligned)
     void* mbar = &smem[oMB];
     auto so_ix = [&](int f, int i) { return oSO + f * OW * N + i; };
