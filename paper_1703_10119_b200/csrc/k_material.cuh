@@ -237,11 +237,11 @@ constexpr int kMatThreads = 256, kMatCells = 255;
 
 // df_step_nonlinear rows (wall.cpp:213-259) from the CTA's shared tables:
 // node f at nS[f*256 + t], half (j-1)+1/2 at hS[f*256 + t], j+1/2 at hS[f*256 + t+1]
-__device__ __forceinline__ void material_cell(const StepArgs& a, const NodeIn& x, int w, int j, const double* nS,
-                                              const double* hS, int t, double& un, double& vn) {
+// p: the wall's groups, loaded by the caller before the StarTables evaluation
+__device__ __forceinline__ void material_cell(const StepArgs& a, const NodeIn& x, int w, int j, const Groups& p,
+                                              const double* nS, const double* hS, int t, double& un, double& vn) {
     const int n = a.n;
     const double dx = a.dx, dt = a.dt;
-    const Groups p = a.groups[w];
     const double ad = p.Fo_M * dt / (dx * dx);
     const double b_ = p.Fo_TT * dt / (dx * dx);
     const double g_ = p.Fo_TM * p.gamma * dt / (dx * dx);
@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(kMatThreads) k_material_step(const StepArgs a,
         j = static_cast<int>(c - static_cast<int64_t>(w) * a.n);
     }
     if (out_cell) x = load_node(a, w, j);
+    const Groups gp = a.groups[out_cell ? w : 0];                    // in flight during the evaluations
     const bool frozen = frozen_before(a.fail_key, a.layer);
     const int wk = c < total ? a.wall_kind[w] : kCoeffConstant;
     const bool own = c >= a.own0 && c < a.own1;
@@ -337,7 +338,7 @@ __global__ void __launch_bounds__(kMatThreads) k_material_step(const StepArgs a,
     if (!out_cell || frozen) return;
     double un, vn;
     if (wk == kCoeffConstant) coupled_node(a, w, j, x, un, vn);
-    else material_cell(a, x, w, j, nS, hS, t, un, vn);
+    else material_cell(a, x, w, j, gp, nS, hS, t, un, vn);
     a.out[1][c] = un;
     a.out[3][c] = vn;
     if (own && (!(fabs(un) <= a.norm) || !(fabs(vn) <= a.norm))) {
