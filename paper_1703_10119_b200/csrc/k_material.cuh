@@ -282,7 +282,7 @@ __device__ __forceinline__ void material_cell(const StepArgs& a, const NodeIn& x
          (ctt + b_ * (ktp_b + kt_b) + cplu);
 }
 
-__global__ void __launch_bounds__(kMatThreads) k_material_step(const StepArgs a, const StarArgs s,
+__global__ void __launch_bounds__(kMatThreads, 4) k_material_step(const StepArgs a, const StarArgs s,
                                                               const ZoneArgs z, int wall_blocks) {
     if (static_cast<int>(blockIdx.x) >= wall_blocks) {              // zones (step_explicit :179-183)
         const int zi = (static_cast<int>(blockIdx.x) - wall_blocks) * blockDim.x + threadIdx.x;
