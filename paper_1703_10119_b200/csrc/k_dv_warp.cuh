@@ -354,6 +354,9 @@ __global__ void __launch_bounds__(NW * 32) k_dv_wall_split(const NonlinearSegArg
                 vn = (lf || rf) ? vf : vn;
                 un = (lf || rf) ? uf : un;
             }
+#ifdef DV_SKIP_U   // timing experiment only: the u chain left out of the step
+            un = up;
+#endif
             acc |= live ? (static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn))) : 0u;
             up = uc;
             vp = vc;
