@@ -39,7 +39,8 @@ def _oracle(model, init, steps):
 
 
 @pytest.mark.parametrize("n_zones,wpz,n,steps", [(17, 6, 128, 203), (3, 6, 128, 100), (2, 4, 64, 150),
-                                                  (5, 6, 256, 120), (40, 6, 128, 1000), (1, 6, 128, 60)])
+                                                  (5, 6, 256, 120), (40, 6, 128, 1000), (1, 6, 128, 60),
+                                                  (17, 5, 128, 150)])   # odd W: a one-wall store in the last block
 def test_ring_matches_oracle(n_zones, wpz, n, steps):
     w = workloads.zone_ring(n_zones=n_zones, walls_per_zone=wpz, n_nodes=n, nsteps=steps)
     rng = np.random.default_rng(n_zones)
