@@ -184,6 +184,7 @@ struct hyg_ctx {
     bool fused = false;        // K1: constant exterior walls on a fused grid
     bool nl_fused = false;     // K2: analytic d(v) exterior walls, n <= 1024
     bool tiled = false;        // K3: one long analytic d(v) exterior wall, n > 1024
+    bool fo_m_pos = true;      // every wall has Fo_M > 0 (K2/K3 scale by 2 Fo_M dt/dx^2)
     bool flux = true;
     int seg_len = 4096;
     // measurement
@@ -1281,6 +1282,7 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
     for (int w = 0; w < c->n_walls; ++w) {
         const hyg_wall_groups& g = d->groups[w];
         c->groups[w] = Groups{g.Fo_M, g.Fo_TT, g.Fo_TM, g.gamma};
+        c->fo_m_pos = c->fo_m_pos && g.Fo_M > 0.0;
         for (int k = 0; k < 2; ++k) {
             const hyg_face_biot& b = d->biot[2 * w + k];
             c->biot[2 * w + k] = Biot{b.Bi_M, b.Bi_TT, b.Bi_TM};
@@ -2005,8 +2007,10 @@ int hyg_advance(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
     cudaSetDevice(c->device);
     if (!(dt > 0.0)) dt = c->dt;
     int rc = c->fused      ? advance_fused(c, nsteps, dt, status)
-             : c->nl_fused ? advance_nonlinear(c, nsteps, dt, status)
-             : c->tiled    ? advance_tiled(c, nsteps, dt, status)
+             // the warp-register d(v) kernels scale the half-node coefficients by
+             // 2 Fo_M dt/dx^2 (k_dv_warp.cuh): they need it positive
+             : c->nl_fused && dt > 0.0 && c->fo_m_pos ? advance_nonlinear(c, nsteps, dt, status)
+             : c->tiled && dt > 0.0 && c->fo_m_pos    ? advance_tiled(c, nsteps, dt, status)
              : c->ring     ? advance_ring(c, nsteps, dt, status)
                            : advance_general(c, nsteps, dt, status);
     if (status && rc == HYG_OK) status->code = HYG_OK;

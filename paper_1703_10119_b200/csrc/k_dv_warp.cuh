@@ -69,17 +69,19 @@ struct TiledArgs {
 // reference's midpoint form).  For a node value pass 2 v.
 // The exponent -p2 (m - p3)^2 is -(e e) with e = sqrt(p2) (m - p3) from one
 // FMA (p2 >= 0 on this path, hyg_create), one DMUL fewer than (-p2 e) e.
-struct DvParams { double hp0, hsq, nsqp3, p1, np2, p3; };
+// Every coefficient is returned SCALED by a2 = 2 Fo_M dt/dx^2 (the rows use
+// 2a k only): hp0 = a2 p0/2, p1 = a2 p1, one = a2 — the same two FMAs.
+struct DvParams { double hp0, hsq, nsqp3, p1, np2, p3, one; };
 
-__device__ __forceinline__ DvParams dv_params(const double* p) {
+__device__ __forceinline__ DvParams dv_params(const double* p, double a2) {
     const double sq = sqrt(p[2]);
-    return DvParams{0.5 * p[0], 0.5 * sq, -p[3] * sq, p[1], -p[2], p[3]};
+    return DvParams{a2 * (0.5 * p[0]), 0.5 * sq, -p[3] * sq, a2 * p[1], -p[2], p[3], a2};
 }
 
 __device__ __forceinline__ double d_half(const DvParams& q, double sum, const double* tab) {
     const double e = fma(q.hsq, sum, q.nsqp3);
     const double E = fexp_addend(-(e * e), tab);
-    return fma(q.p1, E, fma(q.hp0, sum, 1.0));
+    return fma(q.p1, E, fma(q.hp0, sum, q.one));
 }
 
 // The same with the exponent as (-p2 e) e, e = m - p3: one DMUL more, but
@@ -88,7 +90,7 @@ __device__ __forceinline__ double d_half(const DvParams& q, double sum, const do
 __device__ __forceinline__ double d_half_lat(const DvParams& q, double sum, const double* tab) {
     const double e = fma(0.5, sum, -q.p3);
     const double E = fexp_addend((q.np2 * e) * e, tab);
-    return fma(q.p1, E, fma(q.hp0, sum, 1.0));
+    return fma(q.p1, E, fma(q.hp0, sum, q.one));
 }
 
 // Interior-row constants of one wall (wall.cpp:199-204).
@@ -107,10 +109,12 @@ __device__ __forceinline__ void dv_interior(const DvRow& r, double vp, double up
     // increment inc ~ vn - vp: (vL + vR) - (vn + vp) = dl + dr - inc, so
     // G w - Gm (vn - vp) = G (dl + dr) - (G + Gm) inc (every term vanishes
     // exactly at a uniform state)
+    // km, kp arrive scaled by 2a (dv_params): num = 2a (km dl + kp dr) and
+    // 1 + a (kp + km) = 1 + (kp' + km')/2
     const double dl = vL - vp, dr = vR - vp;
     const double num = __dadd_rn(__dmul_rn(km, dl), __dmul_rn(kp, dr));
-    const double den = fma(r.a, kp + km, 1.0);
-    const double inc = __dmul_rn(r.a2 * num, frcp(den));
+    const double den = fma(0.5, kp + km, 1.0);
+    const double inc = __dmul_rn(num, frcp(den));
     vn = __dadd_rn(vp, inc);
     const double du = fma(-2.0, up, uL + uR);
     un = fma(-r.Gp, inc, fma(r.G, dl + dr, fma(r.B, du, up)));
@@ -118,7 +122,7 @@ __device__ __forceinline__ void dv_interior(const DvRow& r, double vp, double up
 
 // Face row (wall.cpp:218-229, 241-259; analytic_face) with the per-lane
 // constants folded once: the u row's denominator is a per-wall constant.
-struct DvFace { double a, a2, cpl1, cpl2, ag4, dx2, BiM, b4, cplu2, gamma, b2r, b4dx, BiTM, g2, inv_fu; };
+struct DvFace { double a, a2, cpl1, cpl2, ag4, dx2, BiM, b4, cplu2, gamma, b2r, b4dx, BiTM, g2, inv_fu, dx2a; };
 
 __device__ __forceinline__ DvFace dv_face_consts(const AnalyticRow& r, const Biot& fb) {
     DvFace f;
@@ -139,6 +143,7 @@ __device__ __forceinline__ DvFace dv_face_consts(const AnalyticRow& r, const Bio
     f.BiTM = fb.Bi_TM;
     f.g2 = 2.0 * r.g;
     f.inv_fu = 1.0 / (1.0 + 2.0 * r.b + cplu);
+    f.dx2a = 2.0 * r.dx * (2.0 * r.a);   // 2 dx / k = 2 dx 2a / k' for a scaled k'
     return f;
 }
 
@@ -146,11 +151,12 @@ __device__ __forceinline__ DvFace dv_face_consts(const AnalyticRow& r, const Bio
 // half node next to the face.
 __device__ __forceinline__ void dv_face(const DvFace& f, const Ambient& am, double vp, double up, double vcn,
                                         double ucn, double km_b, double kp_b, double& vn, double& un) {
+    // km_b, kp_b scaled by 2a (dv_params): 2a S = S', a S = S'/2
     const double S = kp_b + km_b;
     const double rk = frcp(km_b);                      // off the v row's chain
-    vn = vp + (f.a2 * S * (vcn - vp) + f.cpl2 * (am.v - vp) + f.ag4 * am.g) * frcp(fma(f.a, S, f.cpl1));
+    vn = vp + (S * (vcn - vp) + f.cpl2 * (am.v - vp) + f.ag4 * am.g) * frcp(fma(0.5, S, f.cpl1));
     const double vbar = 0.5 * (vn + vp);
-    const double vg = vcn - (f.dx2 * rk) * (f.BiM * (vbar - am.v) - am.g);
+    const double vg = vcn - (f.dx2a * rk) * (f.BiM * (vbar - am.v) - am.g);
     un = up + (f.b4 * (ucn - up) + f.cplu2 * (am.u - up) - f.gamma * (vn - vp) + f.b2r * (vcn - vg) -
                f.b4dx * (f.BiTM * (vbar - am.v) - am.q) + f.g2 * (vcn + vg) - f.g2 * (vn + vp)) *
               f.inv_fu;
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(kDvWarps * 32) k_dv_walls(const NonlinearSegAr
     }
     const AnalyticRow rc = analytic_row(A.groups[w], A.dx, A.dt);
     const DvRow r = dv_row(rc);
-    const DvParams q = dv_params(A.p);
+    const DvParams q = dv_params(A.p, 2.0 * rc.a);
     const int f = L.rev ? 1 : 0;
     const DvFace fc = dv_face_consts(rc, A.biot[2 * w + f]);
     const int chl = A.chan[2 * w], chr = A.chan[2 * w + 1];
@@ -321,7 +327,7 @@ __global__ void __launch_bounds__(NW * 32) k_dv_wall_split(const NonlinearSegArg
     double vp = live ? A.in[2][o] : 1.0, vc = live ? A.in[3][o] : 1.0;
     const AnalyticRow rc = analytic_row(A.groups[w], A.dx, A.dt);
     const DvRow r = dv_row(rc);
-    const DvParams q = dv_params(A.p);
+    const DvParams q = dv_params(A.p, 2.0 * rc.a);
     const DvFace fc = dv_face_consts(rc, A.biot[2 * w + (rf ? 1 : 0)]);
     const int chl = A.chan[2 * w], chr = A.chan[2 * w + 1];
     constexpr unsigned FULL = 0xffffffffu;
@@ -426,7 +432,7 @@ __global__ void __launch_bounds__(kDvWarps * 32) k_dv_tiled(const TiledArgs A) {
     }
     const AnalyticRow rc = analytic_row(A.groups, A.dx, A.dt);
     const DvRow r = dv_row(rc);
-    const DvParams q = dv_params(A.p);
+    const DvParams q = dv_params(A.p, 2.0 * rc.a);
     const DvFace fc = dv_face_consts(rc, L.rev ? A.br : A.bl);
     const int ch = L.rev ? A.chr : A.chl;
     unsigned acc = 0;
@@ -501,7 +507,7 @@ __global__ void __launch_bounds__(kDvWarps * 32, MINB) k_dv_tiled_stream(const T
     prefetch(t);
     const AnalyticRow rc = analytic_row(A.groups, A.dx, A.dt);
     const DvRow r = dv_row(rc);
-    const DvParams q = dv_params(A.p);
+    const DvParams q = dv_params(A.p, 2.0 * rc.a);
     const DvFace fc{};
     DvLane L;
     L.rev = lane == 31;
