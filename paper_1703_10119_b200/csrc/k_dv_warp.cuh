@@ -225,7 +225,7 @@ __device__ __forceinline__ void dv_step(double (&vP)[NPT], const double (&vC)[NP
 
 constexpr int kDvWarps = 4;     // walls (K2w) or windows (K3w) per CTA
 // K3w: 3 CTAs (12 warps) per SM — caps registers at 168 (uncapped the
-// compiler takes 222 and only 8 warps fit)
+// compiler takes 222 and only 8 warps fit; 4 CTAs at 128 registers spill: 3.07e11 vs 3.17e11)
 constexpr int kK3MinB = 3;
 
 // K2w: one warp per wall, n <= 32 NPT, all steps of a segment in one launch.
