@@ -823,10 +823,31 @@ void launch_dv_split(const NonlinearSegArgs& a, int nw, cudaStream_t s) {
     }
 }
 
-// n <= 256.  Fewer walls than SMs: K2s (a wall over ceil(n/32) warps, latency).
+template <int NW, int H>
+void launch_dv_halo(const NonlinearSegArgs& a, int nw, cudaStream_t s) {
+    if constexpr (NW <= 8) {
+        if (nw != NW) return launch_dv_halo<NW + 1, H>(a, nw, s);
+        k_dv_wall_halo<NW, H><<<a.n_walls, NW * 32, 0, s>>>(a);
+    }
+}
+
+// n <= 256.  Fewer walls than SMs: K2h/K2s (a wall over ceil(n/32) warps, latency).
 // Otherwise K2w: NPT = the smallest power of two with 32 NPT >= n, M = nodes of
 // the reversed lane.
 void launch_dv_walls(const NonlinearSegArgs& a, int n, cudaStream_t s) {
+    if (a.n_walls <= kSplitWallsMax && n > 32) {
+        // K2h when the same ceil(n/32) warps leave H >= 2 halo lanes a side
+        // (configs[0]: n = 101, 4 warps, H = 3: a barrier every 3 steps)
+        const int nw = (n + 31) / 32, halo = std::min(6, (32 - (n + nw - 1) / nw) / 2);
+        switch (halo) {
+            case 2: return launch_dv_halo<1, 2>(a, nw, s);
+            case 3: return launch_dv_halo<1, 3>(a, nw, s);
+            case 4: return launch_dv_halo<1, 4>(a, nw, s);
+            case 5: return launch_dv_halo<1, 5>(a, nw, s);
+            case 6: return launch_dv_halo<1, 6>(a, nw, s);
+            default: break;
+        }
+    }
     if (a.n_walls <= kSplitWallsMax && n >= 3) return launch_dv_split<1>(a, (n + 31) / 32, s);
     const int npt = n <= 32 ? 1 : n <= 64 ? 2 : n <= 128 ? 4 : 8;
     const int m = n - (n - 1) / npt * npt;

@@ -380,6 +380,83 @@ __global__ void __launch_bounds__(NW * 32) k_dv_wall_split(const NonlinearSegArg
     }
 }
 
+// K2h: K2s with redundant halos instead of a barrier per step.  Warp k holds
+// the 32 consecutive nodes g = k (32 - 2H) - H + lane and owns lanes
+// H .. 31-H; an artificial warp edge corrupts one lane per step, so the owned
+// lanes stay exact for H steps between exchanges (the faces read only their
+// interior neighbour, so lanes outside [0, n) never reach a live node).  Every
+// H steps the owned lanes publish both layers to shared memory and every lane
+// reloads its node behind one barrier.  Per node the arithmetic is K2s's,
+// statement for statement, so the two are bitwise equal.
+template <int NW, int H>
+__global__ void __launch_bounds__(NW * 32) k_dv_wall_halo(const NonlinearSegArgs A) {
+    constexpr int T = 32 - 2 * H;                      // owned nodes per warp
+    __shared__ double s_tab[64];
+    __shared__ Ambient s_amb[kNlChunk][2];
+    __shared__ double s_st[4][NW * T];                 // {u_prev, u_curr, v_prev, v_curr} by node
+    if (*A.stop) return;
+    stage_exp_table(s_tab, threadIdx.x, blockDim.x);
+    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+    const int w = blockIdx.x, n = A.n, j = warp * T - H + lane;
+    const bool live = j >= 0 && j < n;
+    const bool own = live && lane >= H && lane < 32 - H;
+    const bool lf = j == 0, rf = j == n - 1;
+    const size_t base = static_cast<size_t>(w) * n;
+    double up = live ? A.in[0][base + j] : 1.0, uc = live ? A.in[1][base + j] : 1.0;
+    double vp = live ? A.in[2][base + j] : 1.0, vc = live ? A.in[3][base + j] : 1.0;
+    const AnalyticRow rc = analytic_row(A.groups[w], A.dx, A.dt);
+    const DvRow r = dv_row(rc);
+    const DvParams q = dv_params(A.p, 2.0 * rc.a);
+    const DvFace fc = dv_face_consts(rc, A.biot[2 * w + (rf ? 1 : 0)]);
+    const int chl = A.chan[2 * w], chr = A.chan[2 * w + 1];
+    constexpr unsigned FULL = 0xffffffffu;
+    unsigned acc = 0;
+    int since = 0;
+    for (int c0 = 0; c0 < A.nsteps; c0 += kNlChunk) {
+        const int clen = min(kNlChunk, A.nsteps - c0);
+        __syncthreads();
+        for (int i = tid; i < 2 * clen; i += NW * 32)
+            s_amb[i >> 1][i & 1] = A.table[static_cast<size_t>(c0 + (i >> 1)) * A.n_channels + ((i & 1) ? chr : chl)];
+        __syncthreads();
+        for (int s = 0; s < clen; ++s) {
+            if (since == H) {                          // halo refresh (block-uniform)
+                if (own) { s_st[0][j] = up; s_st[1][j] = uc; s_st[2][j] = vp; s_st[3][j] = vc; }
+                __syncthreads();
+                if (live) { up = s_st[0][j]; uc = s_st[1][j]; vp = s_st[2][j]; vc = s_st[3][j]; }
+                __syncthreads();                       // the next refresh overwrites s_st
+                since = 0;
+            }
+            const double vL = __shfl_up_sync(FULL, vc, 1), uL = __shfl_up_sync(FULL, uc, 1);
+            const double vR = __shfl_down_sync(FULL, vc, 1), uR = __shfl_down_sync(FULL, uc, 1);
+            const double hL = d_half_lat(q, vL + vc, s_tab);
+            const double hR = d_half_lat(q, vc + vR, s_tab);
+            double vn, un;
+            dv_interior(r, vp, up, vL, vR, uL, uR, hL, hR, vn, un);
+            {
+                const double dnode = d_half_lat(q, vc + vc, s_tab);
+                double vf, uf;
+                dv_face(fc, s_amb[s][rf ? 1 : 0], vp, up, rf ? vL : vR, rf ? uL : uR, dnode, rf ? hL : hR, vf, uf);
+                vn = (lf || rf) ? vf : vn;
+                un = (lf || rf) ? uf : un;
+            }
+            acc |= own ? (static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn))) : 0u;
+            up = uc;
+            vp = vc;
+            uc = un;
+            vc = vn;
+            ++since;
+        }
+    }
+    const unsigned any = __reduce_or_sync(FULL, acc);
+    if ((any & 0x40000000u) && lane == 0) atomicCAS(A.suspect, 0, A.seg_index + 1);
+    if (own) {
+        A.out[0][base + j] = up;
+        A.out[1][base + j] = uc;
+        A.out[2][base + j] = vp;
+        A.out[3][base + j] = vc;
+    }
+}
+
 // K3w window geometry (n >= 32 NPT): window t starts at min(t T, n - W) and
 // owns [t == 0 ? 0 : t T + NPT, min(t T + 31 NPT, n)).  Window 0 holds the
 // left face, windows t >= rface(n) end at the right face (at most three).

@@ -291,11 +291,14 @@ def test_advance_with_per_call_dt_fp64():
 
 @pytest.mark.parametrize("n_walls,n_nodes", [(1, 101), (3, 256), (5, 17), (2, 33), (300, 101), (200, 256),
                                              (160, 33), (150, 64), (170, 200), (149, 7), (1, 65), (2, 97),
-                                             (1, 3), (1, 32), (4, 129)])
+                                             (1, 3), (1, 32), (4, 129), (1, 40), (1, 70), (2, 104), (1, 150)])
 def test_dv_wall_batches(n_walls, n_nodes):
     """Coupled d(v) walls with random groups, Biot numbers and imposed fluxes
     through K2s (n_walls <= 148: a wall over ceil(n/32) warps; n = 33, 65,
-    97, 129 put the right face in lane 0 of the last warp) and K2w
+    97, 129 put the right face in lane 0 of the last warp; K2h, the halo
+    variant, where ceil(n/32) warps leave H >= 2 spare lanes a side: n = 33
+    (H = 6), 40 (6, exact fit), 65 (5), 70 (4), 97, 101, 104 (3, exact fit),
+    129 (3); n = 150, 256 stay on K2s) and K2w
     (one warp per wall, every NPT x reversed-lane width M), explicit start."""
     model, init = random_walls(n_walls, n_nodes, seed=n_nodes + n_walls, flux=True)
     # cfg1's Fo_M range times d(v) ~ 50 diverges in the reference arithmetic too

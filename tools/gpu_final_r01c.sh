@@ -24,7 +24,7 @@ full() {  # cfg steps kernel skip keep
 lst cfg1 4097; lst cfg2 4097; lst cfg0 4097; lst cfg3 41; lst cfg4 33; lst cfg5 11
 echo lists >> $O/status.txt
 full cfg4 33 k_dv_tiled_stream 2 keep
-full cfg0 4097 k_dv_wall_split 0
+full cfg0 4097 k_dv_wall_halo 0
 full cfg3 41 k_ring_reg 1
 full cfg5 11 k_material_step 3
 echo done >> $O/status.txt
