@@ -386,8 +386,10 @@ __global__ void __launch_bounds__(NW * 32) k_dv_wall_split(const NonlinearSegArg
 // lanes stay exact for H steps between exchanges (the faces read only their
 // interior neighbour, so lanes outside [0, n) never reach a live node).  Every
 // H steps the owned lanes publish both layers to shared memory and every lane
-// reloads its node behind one barrier.  Per node the arithmetic is K2s's,
-// statement for statement, so the two are bitwise equal.
+// reloads its node behind one barrier.  Each lane evaluates its right half
+// node only and takes the left one from the previous lane by a shuffle (K2s
+// evaluates both: its lane 0 has no in-warp predecessor).  Per node the
+// arithmetic is K2s's, so the two are bitwise equal.
 template <int NW, int H>
 __global__ void __launch_bounds__(NW * 32) k_dv_wall_halo(const NonlinearSegArgs A) {
     constexpr int T = 32 - 2 * H;                      // owned nodes per warp
@@ -428,12 +430,22 @@ __global__ void __launch_bounds__(NW * 32) k_dv_wall_halo(const NonlinearSegArgs
             }
             const double vL = __shfl_up_sync(FULL, vc, 1), uL = __shfl_up_sync(FULL, uc, 1);
             const double vR = __shfl_down_sync(FULL, vc, 1), uR = __shfl_down_sync(FULL, uc, 1);
-            const double hL = d_half_lat(q, vL + vc, s_tab);
+            // the left half node is the previous lane's right one (the sum
+            // commutes: bit for bit the local evaluation); lane 0 is a halo lane
+#ifdef DV_HALO_SQRT   // timing experiment only (tools/dv_time_probe.py)
+            const double hR = d_half(q, vc + vR, s_tab);
+#else
             const double hR = d_half_lat(q, vc + vR, s_tab);
+#endif
+            const double hL = __shfl_up_sync(FULL, hR, 1);
             double vn, un;
             dv_interior(r, vp, up, vL, vR, uL, uR, hL, hR, vn, un);
             {
+#ifdef DV_HALO_SQRT
+                const double dnode = d_half(q, vc + vc, s_tab);
+#else
                 const double dnode = d_half_lat(q, vc + vc, s_tab);
+#endif
                 double vf, uf;
                 dv_face(fc, s_amb[s][rf ? 1 : 0], vp, up, rf ? vL : vR, rf ? uL : uR, dnode, rf ? hL : hR, vf, uf);
                 vn = (lf || rf) ? vf : vn;
