@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define HYG_ABI_VERSION 2
+#define HYG_ABI_VERSION 3
 
 /* ---- return codes (errors.hpp:8-45) ------------------------------------ */
 enum {
@@ -324,6 +324,15 @@ int hyg_kernel_stats(hyg_ctx* ctx, int32_t i, const char** name, int64_t* launch
 int hyg_reset_kernel_stats(hyg_ctx* ctx);
 /* Number of kernels this context has launched since creation. */
 int64_t hyg_launch_count(hyg_ctx* ctx);
+
+/* Launch-shape knobs (an extension; the reference has no launch shapes).
+ * HYG_TUNE_RING_GRID: cap on the persistent zone-ring kernel's grid (K4r,
+ * k_ring_reg.cuh; 0 = one CTA per SM).  A cap below the number of zone blocks
+ * makes every CTA walk several blocks, so small rings under test run the
+ * next-block prefetch path the full-size ring runs.  HYG_EINVAL for an
+ * unknown knob or a negative value. */
+enum { HYG_TUNE_RING_GRID = 1 };
+int hyg_set_tuning(hyg_ctx* ctx, int32_t knob, int64_t value);
 
 /* Device FP64 FMA throughput probe (DFMA loop), TFLOP/s counting FMA = 2. */
 int hyg_probe_fp64_peak(int32_t device, double* tflops, double* sm_clock_mhz);

@@ -85,6 +85,8 @@ _ORACLE_PROTOS = {
     "orc_step_implicit": (C.c_int, [C.POINTER(A.ModelDesc), C.POINTER(BuildingState), C.c_double, C.c_int,
                                     _ip, A.dp]),
     "orc_run": (C.c_int, [C.POINTER(A.ModelDesc), C.POINTER(BuildingState), C.c_int64, _i64p, _ip, _ip]),
+    "orc_run_mt": (C.c_int, [C.POINTER(A.ModelDesc), C.POINTER(BuildingState), C.c_int64, C.c_int, _i64p, _ip,
+                             _ip]),
     "orc_set_owned": (None, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "orc_last_domain": (None, [_ip, _ip]),
     "orc_last_domain_wall": (C.c_int, []),
@@ -270,11 +272,16 @@ class Building:
                                _p(self.state["v_curr"]), _p(self.zu), _p(self.zv), state.get("t", 0.0),
                                state.get("layer", 0))
 
-    def run(self, impl: str, nsteps: int, with_bootstrap: bool = True):
+    def run(self, impl: str, nsteps: int, with_bootstrap: bool = True, nthreads: int = 1):
+        """run() from the current state; nthreads > 1 (oracle, with the start):
+        the explicit steps split over threads, bitwise the serial march."""
         fl, fw, bp = C.c_int64(-1), C.c_int(-1), C.c_int(0)
         if impl == "oracle":
             lib = oracle_lib()
-            if with_bootstrap:
+            if with_bootstrap and nthreads > 1:
+                rc = lib.orc_run_mt(C.byref(self.desc), C.byref(self.s), nsteps, nthreads, C.byref(fl), C.byref(fw),
+                                    C.byref(bp))
+            elif with_bootstrap:
                 rc = lib.orc_run(C.byref(self.desc), C.byref(self.s), nsteps, C.byref(fl), C.byref(fw), C.byref(bp))
             else:
                 rc = 0

@@ -7,6 +7,7 @@
  * FMA contraction: -ffp-contract=off) it reproduces the reference bit for
  * bit; tests/test_oracle_vs_ref.py checks exactly that against oracle/_ref.
  */
+#define _POSIX_C_SOURCE 200809L   /* pthread_barrier_t under -std=c11 */
 #include "hygro_oracle.h"
 
 #include <math.h>
@@ -1037,4 +1038,137 @@ int orc_run(const hyg_model_desc* m, orc_building_state* s, int64_t nsteps, int6
         ++done;
     }
     return 0;
+}
+
+/* ---- orc_run_mt: orc_run with the explicit steps split over threads ------
+ * The same run() march (building.cpp:303-356): the implicit start serially,
+ * then every step_explicit (building.cpp:152-187) with the walls and zones
+ * split into contiguous ranges per thread.  Within a step every wall reads
+ * only layer n of its own nodes and the layer-n zone snapshot, every zone
+ * only layer-n samples and peers, so each value is computed by the same
+ * statements as orc_step_explicit and the result is bitwise the serial one.
+ * Three barriers per step: samples/snapshot gathered; walls and zones
+ * stepped; the guard verdict (lowest failing wall, as check_bounded walks
+ * walls in order, then zones).  Constant-coefficient walls without radiation
+ * only (the zone-ring workloads); anything else runs orc_run. */
+typedef struct {
+    const hyg_model_desc* m;
+    orc_building_state* s;
+    int nthr, id;
+    int64_t nsteps;
+    double *zu0, *zv0, *us, *vs;
+    const int* link0;
+    pthread_barrier_t* bar;
+    int* fail_wall;       /* [nthr] lowest failing wall this step (INT_MAX: none) */
+    int* fail_zone;       /* [nthr] any failing zone this step */
+    volatile int* stop;
+    int64_t* done;
+} mt_job;
+
+static void* mt_run(void* arg) {
+    mt_job* J = (mt_job*)arg;
+    const hyg_model_desc* m = J->m;
+    orc_building_state* s = J->s;
+    const int nw = m->n_walls, nz = m->n_zones, n = m->n_nodes;
+    const int w0 = (int)((int64_t)nw * J->id / J->nthr), w1 = (int)((int64_t)nw * (J->id + 1) / J->nthr);
+    const int z0 = (int)((int64_t)nz * J->id / J->nthr), z1 = (int)((int64_t)nz * (J->id + 1) / J->nthr);
+    for (int64_t k = 0; k < J->nsteps; ++k) {
+        const double t = s->t, dt = m->dt;
+        for (int z = z0; z < z1; ++z) {           /* snapshot + samples of layer n (building.cpp:157-164) */
+            J->zu0[z] = s->zu[z];
+            J->zv0[z] = s->zv[z];
+            for (int i = 0; i < m->zones[z].n_walls; ++i) {
+                const hyg_zone_wall_link* l = &m->zones[z].walls[i];
+                const size_t idx = (size_t)l->wall * (size_t)n + (size_t)face_node(m, l->face);
+                J->us[J->link0[z] + i] = s->uc[idx];
+                J->vs[J->link0[z] + i] = s->vc[idx];
+            }
+        }
+        pthread_barrier_wait(J->bar);
+        int fw = 0x7fffffff, fz = 0;
+        for (int w = w0; w < w1; ++w) {
+            orc_face L, R;
+            resolve_face(m, w, 0, J->zu0, J->zv0, t, 0.0, &L);
+            resolve_face(m, w, 1, J->zu0, J->zv0, t, 0.0, &R);
+            orc_field f = bfield(m, s, w);
+            orc_df_step_coupled(&f, m->dx, &m->groups[w], &L, &R, dt);
+            if (fw == 0x7fffffff && !(orc_max_abs_field(&f) <= m->divergence_norm)) fw = w;
+        }
+        const double u_out = orc_signal(&m->outdoor_u, t), v_out = orc_signal(&m->outdoor_v, t);
+        for (int z = z0; z < z1; ++z) {
+            double du, dv;
+            orc_zone_rhs(m, z, J->zu0[z], J->zv0[z], J->us + J->link0[z], J->vs + J->link0[z], J->zu0, J->zv0,
+                         u_out, v_out, t, &du, &dv);
+            s->zu[z] = J->zu0[z] + dt * du;
+            s->zv[z] = J->zv0[z] + dt * dv;
+            if (!isfinite(s->zu[z]) || !isfinite(s->zv[z]) || fabs(s->zu[z]) > m->divergence_norm ||
+                fabs(s->zv[z]) > m->divergence_norm)
+                fz = 1;
+        }
+        J->fail_wall[J->id] = fw;
+        J->fail_zone[J->id] = fz;
+        pthread_barrier_wait(J->bar);
+        if (J->id == 0) {
+            s->t += dt;
+            s->layer += 1;
+            int any = 0;
+            for (int i = 0; i < J->nthr; ++i) any |= J->fail_wall[i] != 0x7fffffff || J->fail_zone[i];
+            *J->stop = any;
+            *J->done = k + 1;
+        }
+        pthread_barrier_wait(J->bar);
+        if (*J->stop) break;
+    }
+    return NULL;
+}
+
+int orc_run_mt(const hyg_model_desc* m, orc_building_state* s, int64_t nsteps, int nthreads,
+               int64_t* fail_layer, int* fail_wall, int* boot_passes) {
+    int simple = m->coeff_kind == HYG_COEFF_CONSTANT || m->coeff_kind == HYG_COEFF_MATERIAL;
+    for (int w = 0; simple && w < m->n_walls; ++w) {
+        orc_model wm;
+        wall_model(m, w, &wm);
+        simple = wm.kind == ORC_COEFF_CONSTANT;
+    }
+    for (int z = 0; simple && z < m->n_zones; ++z) simple = m->zones[z].n_radiation == 0;
+    if (nthreads <= 1 || !simple || nsteps < 2) return orc_run(m, s, nsteps, fail_layer, fail_wall, boot_passes);
+    int rc = orc_run(m, s, 1, fail_layer, fail_wall, boot_passes);   /* the implicit start (step 1) */
+    if (rc) return rc;
+    const int nz = m->n_zones;
+    int* link0 = (int*)malloc(sizeof(int) * (size_t)(nz + 1));
+    int tot = 0;
+    for (int z = 0; z < nz; ++z) {
+        link0[z] = tot;
+        tot += m->zones[z].n_walls;
+    }
+    double* buf = (double*)malloc(sizeof(double) * (size_t)(2 * nz + 2 * tot + 2));
+    pthread_barrier_t bar;
+    pthread_barrier_init(&bar, NULL, (unsigned)nthreads);
+    int* fw = (int*)malloc(sizeof(int) * (size_t)nthreads * 2);
+    volatile int stop = 0;
+    int64_t done = 0;
+    mt_job* jobs = (mt_job*)calloc((size_t)nthreads, sizeof(mt_job));
+    pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+    for (int i = 0; i < nthreads; ++i) {
+        mt_job J = {m, s, nthreads, i, nsteps - 1, buf, buf + nz, buf + 2 * nz, buf + 2 * nz + tot, link0, &bar,
+                    fw, fw + nthreads, &stop, &done};
+        jobs[i] = J;
+        if (i) pthread_create(&th[i], NULL, mt_run, &jobs[i]);
+    }
+    mt_run(&jobs[0]);
+    for (int i = 1; i < nthreads; ++i) pthread_join(th[i], NULL);
+    if (stop) {
+        int w = 0x7fffffff;
+        for (int i = 0; i < nthreads; ++i) w = fw[i] < w ? fw[i] : w;
+        if (fail_layer) *fail_layer = s->layer;
+        if (fail_wall) *fail_wall = w == 0x7fffffff ? -1 : w;
+        rc = HYG_EDIVERGED;
+    }
+    pthread_barrier_destroy(&bar);
+    free(jobs);
+    free(th);
+    free(fw);
+    free(buf);
+    free(link0);
+    return rc;
 }

@@ -16,6 +16,7 @@ HYG_COEFF_CONSTANT, HYG_COEFF_ANALYTIC_D, HYG_COEFF_MATERIAL = 0, 1, 2
 HYG_F64, HYG_F32 = 0, 1
 HYG_BOOT_IMPLICIT, HYG_BOOT_EXPLICIT = 0, 1
 HYG_SCHEME_DF, HYG_SCHEME_EULER_IMPLICIT, HYG_SCHEME_EULER_EXPLICIT = 0, 1, 2
+HYG_TUNE_RING_GRID = 1
 
 dp = C.POINTER(C.c_double)
 
@@ -142,6 +143,7 @@ PROTOTYPES = {
     "hyg_kernel_stats": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_char_p), C.POINTER(C.c_int64), dp, dp]),
     "hyg_reset_kernel_stats": (C.c_int, [C.c_void_p]),
     "hyg_launch_count": (C.c_int64, [C.c_void_p]),
+    "hyg_set_tuning": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64]),
     "hyg_probe_fp64_peak": (C.c_int, [C.c_int32, dp, dp]),
     "hyg_probe_fp32_peak": (C.c_int, [C.c_int32, dp]),
     "hyg_selftest_fastmath": (C.c_int, [C.c_int32, C.c_int32, dp, dp, dp]),

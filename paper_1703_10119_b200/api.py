@@ -467,6 +467,12 @@ class Context:
             out.append(dict(name=name.value.decode(), launches=n.value, ms=ms.value, node_updates=upd.value))
         return out
 
+    TUNING = {"ring_grid": A.HYG_TUNE_RING_GRID}
+
+    def set_tuning(self, knob: str, value: int) -> None:
+        """Launch-shape knob (hyg_set_tuning), e.g. ring_grid = cap on K4r's persistent grid."""
+        _check(self.lib.hyg_set_tuning(self.h, self.TUNING[knob], int(value)), None, "hyg_set_tuning")
+
     def reset_kernel_stats(self):
         _check(self.lib.hyg_reset_kernel_stats(self.h))
 

@@ -15,6 +15,8 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -207,6 +209,7 @@ struct hyg_ctx {
     bool ring = false;               // K4: zone-ring temporal blocking applies
     int ring_W = 0, ring_B = 0;
     int ring_reg_B = 0;              // K4r (registers + prefetch): zones per CTA, 0 if not applicable
+    int ring_grid_cap = 0;           // HYG_TUNE_RING_GRID: K4r persistent grid cap (0: one CTA per SM)
     double* d_ring_zp = nullptr;     // K4r per-zone parameter blocks [zones][kRingZP]
     bool ring_reg_small = false;     // every zone: <= 6 wall links, <= 2 ring peers
     int rad_groups = 0, rad_terms = 0;
@@ -274,18 +277,40 @@ void drain_pending(hyg_ctx* c) {
     c->pending.clear();
 }
 
+// ---- per-device launch attributes ----------------------------------------------
+// cudaFuncSetAttribute and the SM count are per device: every kernel keeps a
+// bit per device (set under a lock) instead of a process-wide "done" flag, so
+// contexts on several GPUs of one process each configure their own device
+constexpr int kMaxDevices = 64;
+std::mutex g_attr_mu;
+
+template <typename K>
+void ensure_smem_attr(K kernel, int device, int bytes) {
+    static std::unordered_map<const void*, unsigned long long> done;   // kernel -> device mask
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    const unsigned long long bit = 1ull << (device & (kMaxDevices - 1));
+    unsigned long long& m = done[reinterpret_cast<const void*>(kernel)];
+    if (m & bit) return;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    m |= bit;
+}
+
+int sm_count(int device) {
+    static int n[kMaxDevices] = {};
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    int& x = n[device & (kMaxDevices - 1)];
+    if (!x) cudaDeviceGetAttribute(&x, cudaDevAttrMultiProcessorCount, device);
+    return std::max(x, 1);
+}
+
 // ---- K1 dispatch -------------------------------------------------------------
 template <typename Real>
-using SegFn = void (*)(const CoupledSegArgs<Real>&, int grid, int smem, cudaStream_t);
+using SegFn = void (*)(const CoupledSegArgs<Real>&, int grid, int smem, cudaStream_t, int device);
 
 template <typename Real, int LPW, int NPT, bool FLUX, bool EXACT>
-void launch_seg(const CoupledSegArgs<Real>& a, int grid, int smem, cudaStream_t s) {
+void launch_seg(const CoupledSegArgs<Real>& a, int grid, int smem, cudaStream_t s, int device) {
     auto k = k_df_coupled<Real, LPW, NPT, kWarps, kChunk, FLUX, EXACT>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-        attr = true;
-    }
+    ensure_smem_attr(k, device, 64 * 1024);
     k<<<grid, kWarps * 32, smem, s>>>(a);
 }
 
@@ -737,7 +762,7 @@ int advance_fused_t(hyg_ctx* c, Real* (&buf)[2][4], int64_t nsteps, double dt, h
             }
             LaunchScope ls(c, sizeof(Real) == 8 ? "df_coupled_fused_f64" : "df_coupled_fused_f32",
                            static_cast<double>(c->cells()) * len);
-            fast(a, grid, smem, c->stream);
+            fast(a, grid, smem, c->stream, c->device);
         }
         HYG_CUDA(cudaGetLastError());
         int flag = 0;
@@ -776,7 +801,7 @@ int advance_fused_t(hyg_ctx* c, Real* (&buf)[2][4], int64_t nsteps, double dt, h
             {
                 LaunchScope ls(c, sizeof(Real) == 8 ? "df_coupled_exact_f64" : "df_coupled_exact_f32",
                                static_cast<double>(c->cells()) * len);
-                exact(a, grid, smem, c->stream);
+                exact(a, grid, smem, c->stream, c->device);
             }
             HYG_CUDA(cudaGetLastError());
             unsigned long long key;
@@ -963,12 +988,10 @@ int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
         // persistent interior kernel: as many CTAs as fit at once (each warp
         // walks the windows with a stride of all warps), 16-byte stores need
         // 16-byte aligned windows: T and NPT even, the buffers 256-byte aligned
-        static int per_sm = 0, n_sm = 0;
-        if (!per_sm) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dv_tiled_stream<kTileNPT, kK3MinB>, kDvWarps * 32, 0);
-            cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, c->device);
-            per_sm = std::max(per_sm, 1);
-        }
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dv_tiled_stream<kTileNPT, kK3MinB>, kDvWarps * 32, 0);
+        per_sm = std::max(per_sm, 1);
+        const int n_sm = sm_count(c->device);
         const int grid = static_cast<int>(std::min<int64_t>((tr - 1 + kDvWarps - 1) / kDvWarps,
                                                             static_cast<int64_t>(per_sm) * n_sm));
         // cells owned by the face windows (window 0 and t >= tr) and by the interior ones
@@ -1014,31 +1037,26 @@ int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
 }
 
 // ---- the zone-ring temporally blocked path (K4, K4r) -----------------------------
+// grid_cap > 0 (HYG_TUNE_RING_GRID) bounds the persistent grid, so each CTA
+// walks several zone blocks (the next-block prefetch path) even in small rings
 template <int NPT>
-void launch_ring_reg(const RingArgs& a, int threads, size_t smem, cudaStream_t s, int device, bool small) {
+void launch_ring_reg(const RingArgs& a, int threads, size_t smem, cudaStream_t s, int device, bool small,
+                     int grid_cap) {
     // small: every zone has <= 6 wall links and <= 2 ring peers (configs[3])
     auto k = small ? k_ring_reg<NPT, kRingRegS, 6, 2> : k_ring_reg<NPT, kRingRegS>;
-    static int n_sm = 0;
-    if (!n_sm) {
-        cudaFuncSetAttribute(k_ring_reg<NPT, kRingRegS, 6, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(k_ring_reg<NPT, kRingRegS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device);
-    }
+    ensure_smem_attr(k, device, 227 * 1024);
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem);
     const int nblk = (a.n_zones + a.B - 1) / a.B;
-    const int grid = std::max(1, std::min(nblk, std::max(per_sm, 1) * n_sm));
+    int grid = std::max(1, std::min(nblk, std::max(per_sm, 1) * sm_count(device)));
+    if (grid_cap > 0) grid = std::min(grid, grid_cap);
     k<<<grid, threads, smem, s>>>(a);
 }
 
 template <int NPT>
-void launch_ring(const RingArgs& a, int grid, int threads, size_t smem, cudaStream_t s) {
+void launch_ring(const RingArgs& a, int grid, int threads, size_t smem, cudaStream_t s, int device) {
     auto k = k_ring_tiled<NPT, kRingS>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
-    }
+    ensure_smem_attr(k, device, 227 * 1024);
     k<<<grid, threads, smem, s>>>(a);
 }
 
@@ -1113,11 +1131,11 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool
             a.zv_out = c->zv[1 - zf];
             LaunchScope ls(c, reg ? "ring_reg" : "ring_tiled", static_cast<double>(c->cells()) * a.steps);
             if (reg) {
-                if (npt == 4) launch_ring_reg<4>(a, threads, smem, c->stream, c->device, c->ring_reg_small);
-                else launch_ring_reg<8>(a, threads, smem, c->stream, c->device, c->ring_reg_small);
-            } else if (npt == 4) launch_ring<4>(a, grid, threads, smem, c->stream);
-            else if (npt == 8) launch_ring<8>(a, grid, threads, smem, c->stream);
-            else launch_ring<16>(a, grid, threads, smem, c->stream);
+                if (npt == 4) launch_ring_reg<4>(a, threads, smem, c->stream, c->device, c->ring_reg_small, c->ring_grid_cap);
+                else launch_ring_reg<8>(a, threads, smem, c->stream, c->device, c->ring_reg_small, c->ring_grid_cap);
+            } else if (npt == 4) launch_ring<4>(a, grid, threads, smem, c->stream, c->device);
+            else if (npt == 8) launch_ring<8>(a, grid, threads, smem, c->stream, c->device);
+            else launch_ring<16>(a, grid, threads, smem, c->stream, c->device);
         }
         HYG_CUDA(cudaGetLastError());
         int flag = 0;
@@ -2184,6 +2202,14 @@ int hyg_kernel_stats(hyg_ctx* c, int32_t i, const char** name, int64_t* launches
     if (updates) *updates = s.updates;
     return HYG_OK;
 }
+int hyg_set_tuning(hyg_ctx* c, int32_t knob, int64_t value) {
+    if (!c || value < 0) return HYG_EINVAL;
+    switch (knob) {
+        case HYG_TUNE_RING_GRID: c->ring_grid_cap = static_cast<int>(std::min<int64_t>(value, INT32_MAX)); return HYG_OK;
+        default: return HYG_EINVAL;
+    }
+}
+
 int hyg_reset_kernel_stats(hyg_ctx* c) {
     if (!c) return HYG_EINVAL;
     hyg_synchronize(c);

@@ -32,6 +32,16 @@
 #endif
 
 namespace hyg {
+#ifdef __CUDACC__
+// The stop flag of a launch sequence (an earlier launch — or another CTA of
+// this launch — tripped the guard).  Read once per CTA by thread 0 and decided
+// for the whole block through a barrier, so every warp of the CTA agrees
+// (a per-thread read could let some warps leave while others wait on a
+// barrier: undefined behaviour).
+__device__ __forceinline__ bool launch_stopped(const int* stop) {
+    return __syncthreads_or(threadIdx.x == 0 ? *const_cast<const volatile int*>(stop) : 0) != 0;
+}
+#endif
 
 struct Groups { double Fo_M, Fo_TT, Fo_TM, gamma; };
 struct Biot { double Bi_M, Bi_TT, Bi_TM; };

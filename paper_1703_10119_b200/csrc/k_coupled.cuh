@@ -133,7 +133,7 @@ k_df_coupled(const CoupledSegArgs<Real> a) {
     constexpr int N = LPW * NPT;
     extern __shared__ Ambient s_tab[];   // [CHUNK][n_channels]
 
-    if (*a.stop) return;
+    if (launch_stopped(a.stop)) return;
     const int tid = threadIdx.x;
     const int sub = tid % LPW;
     const int wall = blockIdx.x * WALLS_PER_CTA + tid / LPW;

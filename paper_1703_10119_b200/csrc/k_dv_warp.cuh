@@ -235,7 +235,7 @@ template <int NPT, int M>
 __global__ void __launch_bounds__(kDvWarps * 32) k_dv_walls(const NonlinearSegArgs A) {
     __shared__ double s_tab[64];
     __shared__ Ambient s_amb[kDvWarps][kNlChunk][2];   // [warp][step][face]
-    if (*A.stop) return;
+    if (launch_stopped(A.stop)) return;
     stage_exp_table(s_tab, threadIdx.x, blockDim.x);
     __syncthreads();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(NW * 32) k_dv_wall_split(const NonlinearSegArg
     __shared__ double s_tab[64];
     __shared__ Ambient s_amb[kNlChunk][2];
     __shared__ double s_x[2][NW][4];                  // [parity][warp] {v, u} of lanes 0 and 31
-    if (*A.stop) return;
+    if (launch_stopped(A.stop)) return;
     stage_exp_table(s_tab, threadIdx.x, blockDim.x);
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
     const int w = blockIdx.x, n = A.n, j = tid;
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(NW * 32) k_dv_wall_halo(const NonlinearSegArgs
     __shared__ double s_tab[64];
     __shared__ Ambient s_amb[kNlChunk][2];
     __shared__ double s_st[4][NW * T];                 // {u_prev, u_curr, v_prev, v_curr} by node
-    if (*A.stop) return;
+    if (launch_stopped(A.stop)) return;
     stage_exp_table(s_tab, threadIdx.x, blockDim.x);
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
     const int w = blockIdx.x, n = A.n, j = warp * T - H + lane;
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(kDvWarps * 32) k_dv_tiled(const TiledArgs A) {
     using G = DvTiles<NPT>;
     constexpr int W = G::W, T = G::T;
     __shared__ double s_tab[64];
-    if (*A.stop) return;
+    if (launch_stopped(A.stop)) return;
     stage_exp_table(s_tab, threadIdx.x, blockDim.x);
     __syncthreads();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(kDvWarps * 32, MINB) k_dv_tiled_stream(const T
     static_assert((NPT & (NPT - 1)) == 0, "NPT must be a power of two");
     __shared__ double s_tab[64];
     __shared__ __align__(16) double s_buf[kDvWarps][4][W];
-    if (*A.stop) return;
+    if (launch_stopped(A.stop)) return;
     stage_exp_table(s_tab, threadIdx.x, blockDim.x);
     __syncthreads();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;

@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(IT + 32) k_df_analytic_walls(const NonlinearSe
     __shared__ double s_lay[4][MAXN];            // up, uc, vp, vc (roles rotate)
     __shared__ Ambient s_amb[kNlChunk][2];       // [step][face]
     __shared__ double s_tab[64];
-    if (*A.stop) return;
+    if (launch_stopped(A.stop)) return;
     const int w = blockIdx.x, tid = threadIdx.x, n = A.n;
     const size_t o = static_cast<size_t>(w) * n;
     stage_exp_table(s_tab, tid, THREADS);

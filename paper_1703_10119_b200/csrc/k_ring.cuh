@@ -116,7 +116,7 @@ template <int NPT, int S>
 __global__ void __launch_bounds__(896, 1) k_ring_tiled(const RingArgs a) {
     using Sh = RingShape<NPT, S>;
     extern __shared__ double smem[];
-    if (*a.stop) return;                          // an earlier launch tripped the guard
+    if (launch_stopped(a.stop)) return;                          // an earlier launch tripped the guard
     const int n = a.n, W = a.W, B = a.B, Z = a.n_zones;
     const int ow = Sh::owned_walls(B, W), hw = Sh::halo_walls(W);
     const int z0 = blockIdx.x * B;

@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kRingRegThreads, 1) k_ring_reg(const RingArgs 
     constexpr int P = Sh::kP, N = 16 * NPT;
     constexpr unsigned FULL = 0xffffffffu;
     extern __shared__ double smem[];
-    if (*a.stop) return;
+    if (launch_stopped(a.stop)) return;
     const int W = a.W, B = a.B, Z = a.n_zones;
     const int OW = B * W, HW = Sh::halo_walls(W), LB = Sh::local_zones(B);
     const int rw = RingShape<NPT, S>::row_width(a.n_channels, a.n_sources);

@@ -30,7 +30,7 @@ def test_library_exports_every_header_symbol():
     assert missing == []
     # and the binding's prototype table covers the header exactly
     assert sorted(A.PROTOTYPES) == declared
-    assert lib.hyg_abi_version() == 2
+    assert lib.hyg_abi_version() == 3
     assert lib.hyg_strerror(A.HYG_EDIVERGED).decode().startswith("numerical error")
 
 

@@ -20,9 +20,11 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-10
 
 
-def _gpu(model, init, steps):
+def _gpu(model, init, steps, grid_cap=0):
     with Context(model) as ctx:
         ctx.set_state(**init)
+        if grid_cap:
+            ctx.set_tuning("ring_grid", grid_cap)
         ctx.profiling(True)
         st = ctx.bootstrap("implicit")
         ctx.advance(steps - 1)
@@ -32,10 +34,78 @@ def _gpu(model, init, steps):
     return out, st, stats
 
 
-def _oracle(model, init, steps):
+def _oracle(model, init, steps, nthreads=1):
     b = O.Building(model, init)
-    rc, fl, passes = b.run("oracle", steps)
+    rc, fl, passes = b.run("oracle", steps, nthreads=nthreads)
     return b, rc, fl, passes
+
+
+def _noisy(w, seed, amp=2e-3):
+    rng = np.random.default_rng(seed)
+    return {k: v + (amp * rng.standard_normal(v.size) if k in ("u_prev", "u_curr", "v_prev", "v_curr") else 0)
+            for k, v in w.init.items()}
+
+
+def _compare(got, b, n_zones):
+    err = rel_linf(got, dict(b.state))
+    zref = max(float(np.max(np.abs(b.zu[:n_zones]))), float(np.max(np.abs(b.zv[:n_zones]))))
+    zerr = max(float(np.max(np.abs(got["zone_u"] - b.zu[:n_zones]))),
+               float(np.max(np.abs(got["zone_v"] - b.zv[:n_zones])))) / zref
+    return err, zerr
+
+
+# K4r's persistent CTAs (one per SM) walk blocks b, b + grid, ... of B = 4
+# zones; the next block's bulk/cp.async prefetch into the other staging
+# parity, the mbarrier phase flip, load_cf(b + grid) and the staging reuse
+# run only when a CTA owns more than one block.  The grid cap forces that in
+# small rings: 42 zones = 11 blocks (the last one partial, 2 zones) over 3
+# CTAs walk 4/4/3 blocks; 64 zones over 2 CTAs walk 8 blocks each.
+@pytest.mark.parametrize("n_zones,cap,steps", [(42, 3, 203), (64, 2, 160), (42, 1, 77), (13, 2, 96)])
+def test_ring_reg_multi_block_per_cta(n_zones, cap, steps):
+    w = workloads.zone_ring(n_zones=n_zones, walls_per_zone=6, n_nodes=128, nsteps=steps)
+    init = _noisy(w, n_zones + cap)
+    got, st, stats = _gpu(w.model, init, steps, grid_cap=cap)
+    assert stats.get("ring_reg", {}).get("launches", 0) > 0, stats.keys()
+    assert "ring_tiled" not in stats                 # no guard hand-over: K4r marched every launch
+    b, rc, _, passes = _oracle(w.model, init, steps, nthreads=O.threads())
+    assert rc == 0 and st.subiterations == passes
+    err, zerr = _compare(got, b, n_zones)
+    print(n_zones, cap, steps, "rel L-inf", err, "zones", zerr)
+    assert err <= TOL and zerr <= TOL
+
+
+def test_ring_cfg3_full_ring_1000_steps():
+    """configs[3] at its BASELINE shape: 8,192 zones x 6 walls x 128 nodes
+    through K4r (about 14 blocks per persistent CTA) for 1,000 steps, against
+    the oracle's building run (threaded, bitwise the serial one):
+    relative L-infinity <= 1e-10 over walls and zones."""
+    steps = 1000
+    w = workloads.zone_ring(n_zones=8192, walls_per_zone=6, n_nodes=128, nsteps=steps)
+    init = _noisy(w, 8192)
+    got, st, stats = _gpu(w.model, init, steps)
+    assert stats.get("ring_reg", {}).get("launches", 0) > 0, stats.keys()
+    assert "ring_tiled" not in stats
+    b, rc, _, passes = _oracle(w.model, init, steps, nthreads=O.threads())
+    assert rc == 0 and st.subiterations == passes
+    err, zerr = _compare(got, b, 8192)
+    print("cfg3 8192 zones x 1000 steps: rel L-inf", err, "zones", zerr)
+    assert err <= TOL and zerr <= TOL
+
+
+@pytest.mark.parametrize("cap", [0, 5])
+def test_ring_64_zones_full_horizon(cap):
+    """A 64-zone ring at configs[3]'s full 8e4 steps (80 h) through K4r, with
+    the default grid (16 CTAs, one block each) and capped at 5 CTAs."""
+    steps = 80_000
+    w = workloads.zone_ring(n_zones=64, walls_per_zone=6, n_nodes=128, nsteps=steps)
+    init = _noisy(w, 64)
+    got, st, stats = _gpu(w.model, init, steps, grid_cap=cap)
+    assert stats.get("ring_reg", {}).get("launches", 0) > 0
+    b, rc, _, passes = _oracle(w.model, init, steps, nthreads=O.threads())
+    assert rc == 0 and st.subiterations == passes
+    err, zerr = _compare(got, b, 64)
+    print("64 zones x 8e4 steps cap", cap, "rel L-inf", err, "zones", zerr)
+    assert err <= TOL and zerr <= TOL
 
 
 @pytest.mark.parametrize("n_zones,wpz,n,steps", [(17, 6, 128, 203), (3, 6, 128, 100), (2, 4, 64, 150),
