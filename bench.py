@@ -200,21 +200,36 @@ def make_workload(args, rank, world):
     return workloads.long_domain(n_nodes=args.long_nodes, nsteps=args.run_steps)
 
 
-def workload_config(args, w, world):
+def workload_config(args, world):
+    """The `config` block of both arms, from the arguments alone (the reference
+    arm never builds the GPU arm's Workload)."""
     c = CONFIGS[args.config]
-    d = {"workload": f"{w.name}: {w.notes}, {args.run_steps} steps per run "
-                     f"(start: {w.boot}{'' if w.boot == 'none' else ', counted as step 1'})",
-         "config_index": int(args.config[-1]), "nodes": w.model.n_nodes, "walls": w.model.n_walls,
-         "zones": len(w.model.zones), "steps_per_run": args.run_steps, "dt": w.model.dt,
-         "state_bytes": w.cells * 32,
-         "l2": ("inputs larger than L2" if w.cells * 32 > 126e6 else
+    cfg = args.config
+    boot = {"cfg0": "explicit", "cfg4": "none"}.get(cfg, "implicit")
+    name, notes, nodes, walls, zones = {
+        "cfg0": ("cfg0_single_wall_d", "N=101, tau=24.0", 101, 1, 0),
+        "cfg1": ("cfg1_batched_fp64", f"{args.walls} walls x {args.nodes} nodes, seed 1", args.nodes, args.walls, 0),
+        "cfg2": ("cfg2_batched_fp32_vardt", f"{args.walls} walls x {args.nodes} nodes, seed 1", args.nodes,
+                 args.walls, 0),
+        "cfg3": ("cfg3_zone_ring", f"{args.zones} zones x 6 walls x 128", 128, 6 * args.zones, args.zones),
+        "cfg4": ("cfg4_long_domain", f"N={args.long_nodes}, seed 4", args.long_nodes, 1, 0),
+        "cfg5": ("material_walls", f"{args.material_walls} material walls x 101", 101, args.material_walls, 0),
+    }[cfg]
+    cells = nodes * walls
+    d = {"workload": f"{name}: {notes}, {args.run_steps} steps per run "
+                     f"(start: {boot}{'' if boot == 'none' else ', counted as step 1'})",
+         "config_index": int(cfg[-1]), "nodes": nodes, "walls": walls, "zones": zones,
+         "steps_per_run": args.run_steps, "dt": 1e-3, "state_bytes": cells * 32,
+         "l2": ("inputs larger than L2" if cells * 32 > 126e6 else
                 "working set L2/on-chip resident (single wall); no L2 flush between runs"),
          "parallelism": {"weak": f"walls sharded per rank (weak), {world} rank(s), no collective on the data path",
                          "replicas": f"{world} independent replica(s)",
                          "strong": f"{'deep-halo shards (shard.py)' if world > 1 else 'one GPU'}, {world} rank(s)"}
          [c["scaling"]]}
-    if w.dt_schedule:
-        d["dt_schedule"] = w.dt_schedule
+    if cfg == "cfg2":
+        n, dt = args.run_steps, 1e-3
+        sched = [(10_000, dt), (10_000, 2 * dt), (10_000, 4 * dt), (10_000, 8 * dt), (n - 40_000, 16 * dt)]
+        d["dt_schedule"] = [(k, x) for k, x in sched if k > 0]
     return d
 
 
@@ -230,66 +245,39 @@ def run_steps_of(w):
 
 
 # ---------------------------------------------------------------------------------
-def cpu_reference_rate(args, w, threads):
-    """Time the reference CPU path on a bounded sample of w; returns (rate, sample, kind, implicit)."""
-    import oracle as O
-    from paper_1703_10119_b200 import workloads
-    ref = O.ref_lib() is not None
-    impl, kind = ("ref", "reference") if ref else ("oracle", "port")
-    dt = w.model.dt
-    c = args.config
-    if c in ("cfg3",):
-        nsteps = 40
-        b = O.Building(w.model, w.init)
-        t0 = time.perf_counter()
-        b.run(impl, nsteps, with_bootstrap=False)
-        sec = time.perf_counter() - t0
-        return (w.cells * nsteps / sec, f"all {len(w.model.zones)} zones x {nsteps} step_explicit steps "
-                f"(single thread: one building, building.cpp:152-187), {sec:.1f} s", kind, None)
-    if c == "cfg4":
-        n = min(w.model.n_nodes, 1 << 22)
-        from paper_1703_10119_b200.api import Model
-        m = w.model
-        sub = Model(n, m.dx, m.groups, m.biot, m.attach, channels=m.channels, dt=dt, coeff_kind=m.coeff_kind,
-                    coeff_params=m.coeff_params)
-        init = {k: w.init[k][:n] for k in ("u_prev", "u_curr", "v_prev", "v_curr")}
-        nsteps = 10
-    elif c == "cfg0":
-        sub, init, nsteps = w.model, w.init, 20_000
-    elif c == "cfg5":
-        # the reference's df_step_nonlinear with CoefficientModel::material
-        nw = min(w.model.n_walls, 16 * threads)
-        from paper_1703_10119_b200.api import Model
-        m = w.model
-        n = m.n_nodes
-        sub = Model(n, m.dx, m.groups[:nw], m.biot[:nw], m.attach[:nw], channels=m.channels, dt=dt,
-                    coeff_kind="material", T_i=m.T_i, P_vi=m.P_vi, wall_reference=m.wall_reference[:nw])
-        init = {k: w.init[k][:nw * n] for k in ("u_prev", "u_curr", "v_prev", "v_curr")}
-        nsteps = 100
-    else:
-        sub, init = w.model, w.init
-        nsteps = max(1, int(4e8 // w.cells))
-    times = workloads.accumulate_times(np.full(nsteps + 1, dt))
-    tab = O.forcing_table(sub, times, 0, w.tables)
-    wb = O.WallBatch(sub, init, tab)
-    t0 = time.perf_counter()
-    rc = O.march(impl, wb, nsteps, dt, threads)
-    sec = time.perf_counter() - t0
-    cells = sub.n_walls * sub.n_nodes
-    what = {"cfg0": "the reference's d(v) transcription oracle (df_oracle.hpp)" if ref else "oracle restatement",
-            "cfg4": "the reference's d(v) transcription oracle on the first 2^22 nodes" if ref else "oracle",
-            "cfg5": "the reference's df_step_nonlinear with the load-bearing material (wall.cpp:196-264), "
-                    "threads split walls" if ref else "oracle restatement",
-            }.get(c, "df_step_coupled (wall.cpp:144-194), threads split walls")
-    imp = None
-    if c in ("cfg1", "cfg2"):
-        wi = O.WallBatch(sub, init, tab)
-        ns = max(1, nsteps // 4)
-        t1 = time.perf_counter()
-        O.march_implicit(impl, wi, ns, dt, nthreads=threads)
-        imp = (cells * ns / (time.perf_counter() - t1), f"all walls x {ns} Euler-implicit steps")
-    return cells * nsteps / sec, f"{sub.n_walls} wall(s) x {sub.n_nodes} nodes x {nsteps} steps, {what}, " \
-                                  f"{sec:.1f} s", kind, imp
+REF_BENCH = ROOT / "oracle" / "_ref" / "ref_bench"
+
+
+def ref_bench(args, steps: int, warmup: int, threads: int) -> dict:
+    """The reference's own CPU path on the host cores: oracle/_ref/ref_bench,
+    a program linked from the unmodified reference sources that builds the
+    config's workload through the reference's API and times its stepping
+    functions (DF, and the Euler-implicit path beside it).  Runs as a child
+    process: nothing of this package is imported, linked or loaded there."""
+    if not REF_BENCH.exists():
+        raise FileNotFoundError(f"{REF_BENCH} is missing (built from /root/reference by `make -C oracle refbench`)")
+    cmd = [str(REF_BENCH), "--config", args.config, "--steps", str(steps), "--warmup", str(warmup),
+           "--threads", str(threads), "--walls", str(args.walls), "--nodes", str(args.nodes),
+           "--zones", str(args.zones), "--long-nodes", str(args.long_nodes),
+           "--material-walls", str(args.material_walls)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=3600)
+    if r.returncode != 0:
+        raise RuntimeError(f"ref_bench rc={r.returncode}: {r.stderr[-400:]}")
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def cpu_baseline_of(rb: dict, warmup: int) -> dict:
+    df = rb["df"]
+    out = {"value": statistics.median(df["rates"][warmup:]), "unit": UNIT, "cores": df["cores"],
+           "kind": df["kind"], "sample": f"{df['sample']}; {df['path']}",
+           "host_threads": rb["threads"], "effective_cores": rb["effective_cores"]}
+    imp = rb.get("implicit")
+    if imp:
+        out.update(implicit_value=statistics.median(imp["rates"][warmup:]), implicit_kind=imp["kind"],
+                   implicit_cores=imp["cores"], implicit_sample=f"{imp['sample']}; {imp['path']}")
+    if "serial_step_explicit" in rb:
+        out["serial_step_explicit_value"] = rb["serial_step_explicit"]
+    return out
 
 
 def run_reference(args):
@@ -297,22 +285,21 @@ def run_reference(args):
     if rank != 0:
         return 0
     threads = len(os.sched_getaffinity(0))
-    w = make_workload(args, 0, 1)
-    rates, secs = [], []
-    kind, sample = "port", ""
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        r, sample, kind, _ = cpu_reference_rate(args, w, threads)
-        if i >= args.warmup:
-            rates.append(r)
-            secs.append(time.perf_counter() - t0)
-    value = statistics.median(rates)
+    try:
+        rb = ref_bench(args, args.steps, args.warmup, threads)
+    except Exception as e:     # the compiled reference did not travel with the snapshot
+        print(json.dumps({"impl": "reference", "unavailable": str(e).splitlines()[0]}), flush=True)
+        return 0
+    cpu = cpu_baseline_of(rb, args.warmup)
+    value = cpu["value"]
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(secs), "higher_is_better": True,
-            "scaling": CONFIGS[args.config]["scaling"], "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded)", "config": workload_config(args, w, 1), "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(rb["df"]["secs"][args.warmup:]),
+            "higher_is_better": True, "scaling": "strong" if CONFIGS[args.config]["scaling"] == "strong" else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+            "config": workload_config(args, 1), "impl": "reference", "cpu_baseline": cpu,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "each step = one bounded sample of the workload through the reference's own stepping "
+                    "functions (oracle/_ref/ref_bench, linked from the unmodified reference sources)"}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -471,11 +458,10 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = len(os.sched_getaffinity(0))
-        r, sample, kind, imp = cpu_reference_rate(args, w, threads)
-        cpu = {"value": r, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample}
-        if imp:
-            cpu["implicit_value"], cpu["implicit_sample"] = imp
+        try:
+            cpu = cpu_baseline_of(ref_bench(args, 2, 1, len(os.sched_getaffinity(0))), 1)
+        except Exception as e:
+            cpu = {"unavailable": str(e).splitlines()[0]}
 
     traffic = None
     tf = ROOT / "profiles" / f"{top['name']}_traffic.json"
@@ -489,7 +475,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "strong" if cfg["scaling"] == "strong" else "weak", "vs_baseline": None,
-                "dtype": cfg["dtype"], "data": "synthetic (seeded)", "config": workload_config(args, w, world),
+                "dtype": cfg["dtype"], "data": "synthetic (seeded)", "config": workload_config(args, world),
                 "roofline": {"bound": cfg["bound"], "achieved": achieved, "peak": peak, "unit": unit,
                              "frac": achieved / peak if peak else None, "traffic": traffic,
                              "kernel": top["name"], "kernel_share_of_step": share,

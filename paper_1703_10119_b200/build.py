@@ -53,7 +53,7 @@ def build_oracle(verbose: bool = False) -> None:
     """Checker libraries (test infrastructure, never linked by the product)."""
     subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "all"], check=True)
     if Path("/root/reference/proj/src/wall.cpp").exists():
-        subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "ref", "adapter"], check=True)
+        subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "ref", "refbench", "adapter"], check=True)
         # scenario JSON -> reference loader -> both runs -> reference CSV writer
         # (needs the nlohmann/json copy vendored in this image; optional)
         r = subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "scenario"])
