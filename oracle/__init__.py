@@ -85,6 +85,7 @@ _ORACLE_PROTOS = {
     "orc_step_implicit": (C.c_int, [C.POINTER(A.ModelDesc), C.POINTER(BuildingState), C.c_double, C.c_int,
                                     _ip, A.dp]),
     "orc_run": (C.c_int, [C.POINTER(A.ModelDesc), C.POINTER(BuildingState), C.c_int64, _i64p, _ip, _ip]),
+    "orc_march_long_mt": (C.c_int, [_BP, _MP, C.c_int, C.c_double, C.c_int, _i64p]),
     "orc_run_mt": (C.c_int, [C.POINTER(A.ModelDesc), C.POINTER(BuildingState), C.c_int64, C.c_int, _i64p, _ip,
                              _ip]),
     "orc_set_owned": (None, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
@@ -234,6 +235,15 @@ def march(impl: str, wb: WallBatch, nsteps: int, dt: float, nthreads: int = 1):
         else:   # d(v) is expressible only through the reference's test oracle (df_oracle.hpp)
             rc = lib.ref_oracle_march_analytic(C.byref(wb.b), C.byref(m), nsteps, dt, nthreads, C.byref(fl), C.byref(fw))
     return rc, fl.value, fw.value
+
+
+def march_long_mt(wb: WallBatch, nsteps: int, dt: float, nthreads: int):
+    """nsteps DF steps of a one-wall batch with its nodes split over threads
+    (oracle only; bitwise the serial march)."""
+    fl = C.c_int64(-1)
+    m = coeff_model(wb.model)
+    rc = oracle_lib().orc_march_long_mt(C.byref(wb.b), C.byref(m), nsteps, dt, nthreads, C.byref(fl))
+    return rc, fl.value, 0
 
 
 def bootstrap(impl: str, wb: WallBatch, kind: str, dt: float, eta: float = 1e-5, max_subiters: int = 100,

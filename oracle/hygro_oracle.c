@@ -216,15 +216,94 @@ static void free_tables(star_tables* s) { free(s->node); }
 static const orc_coeffs* at_node(const star_tables* s, int j) { return s->unit ? &kUnit : &s->node[j]; }
 static const orc_coeffs* at_half(const star_tables* s, int j) { return s->unit ? &kUnit : &s->half[j]; }
 
+/* df_step_nonlinear (wall.cpp:196-264) in pieces over node ranges, so the
+ * threaded long-wall march (orc_march_long_mt) runs the very statements the
+ * serial step runs: interior v rows of [j0, j1), a face's v row, interior u
+ * rows of [j0, j1) (u reads only its own node's new v), a face's u row. */
+typedef struct {
+    int n;
+    double dx, a, b_, g_, ratio;
+    const hyg_wall_groups* p;
+} nl_consts;
+
+static nl_consts nl_setup(int n, double dx, const hyg_wall_groups* p, double dt) {
+    nl_consts c;
+    c.n = n;
+    c.dx = dx;
+    c.p = p;
+    c.a = p->Fo_M * dt / (dx * dx);
+    c.b_ = p->Fo_TT * dt / (dx * dx);
+    c.g_ = p->Fo_TM * p->gamma * dt / (dx * dx);
+    c.ratio = p->Fo_TT != 0.0 ? p->Fo_TM * p->gamma / p->Fo_TT : 0.0;
+    return c;
+}
+
+static void nl_v_rows(const nl_consts* c, const star_tables* s, const orc_field* f, double* vn, int j0, int j1) {
+    const double a = c->a;
+    const double *vp = f->vp, *vc = f->vc;
+    if (j0 < 1) j0 = 1;
+    if (j1 > c->n - 1) j1 = c->n - 1;
+    for (int j = j0; j < j1; ++j) {
+        const double kp = at_half(s, j)->k_M, km = at_half(s, j - 1)->k_M, cm = at_node(s, j)->c_M;
+        vn[j] = ((cm - a * (kp + km)) * vp[j] + 2.0 * a * (kp * vc[j + 1] + km * vc[j - 1])) /
+                (cm + a * (kp + km));
+    }
+}
+
+static void nl_v_face(const nl_consts* c, const star_tables* s, const orc_field* f, double* vn, int k,
+                      const orc_face* b) {
+    const int n = c->n, jb = k == 0 ? 0 : n - 1, jn = k == 0 ? 1 : n - 2;
+    const double a = c->a, dx = c->dx;
+    const double km_b = at_node(s, jb)->k_M;
+    const double kp_b = at_half(s, jb == 0 ? 0 : n - 2)->k_M;
+    const double cm = at_node(s, jb)->c_M;
+    const double cpl = 2.0 * a * dx * b->Bi_M;
+    vn[jb] = ((cm - a * (kp_b + km_b) - cpl) * f->vp[jb] + 2.0 * a * (kp_b + km_b) * f->vc[jn] +
+              4.0 * a * dx * (b->Bi_M * b->v_inf + b->g_inf)) /
+             (cm + a * (kp_b + km_b) + cpl);
+}
+
+static void nl_u_rows(const nl_consts* c, const star_tables* s, const orc_field* f, const double* vn, double* un,
+                      int j0, int j1) {
+    const double b_ = c->b_, g_ = c->g_, gamma = c->p->gamma;
+    const double *vp = f->vp, *vc = f->vc, *up = f->up, *uc = f->uc;
+    if (j0 < 1) j0 = 1;
+    if (j1 > c->n - 1) j1 = c->n - 1;
+    for (int j = j0; j < j1; ++j) {
+        const double ktp = at_half(s, j)->k_TT, ktm = at_half(s, j - 1)->k_TT;
+        const double kmp = at_half(s, j)->k_TM, kmm = at_half(s, j - 1)->k_TM;
+        const double ctt = at_node(s, j)->c_TT, ctm = at_node(s, j)->c_TM;
+        un[j] = ((ctt - b_ * (ktp + ktm)) * up[j] - gamma * ctm * (vn[j] - vp[j]) +
+                 2.0 * b_ * (ktp * uc[j + 1] + ktm * uc[j - 1]) +
+                 2.0 * g_ * (kmp * vc[j + 1] + kmm * vc[j - 1]) - g_ * (kmp + kmm) * (vn[j] + vp[j])) /
+                (ctt + b_ * (ktp + ktm));
+    }
+}
+
+static void nl_u_face(const nl_consts* c, const star_tables* s, const orc_field* f, const double* vn, double* un,
+                      int k, const orc_face* b) {
+    const int n = c->n, jb = k == 0 ? 0 : n - 1, jn = k == 0 ? 1 : n - 2;
+    const double b_ = c->b_, g_ = c->g_, dx = c->dx, ratio = c->ratio;
+    const double *vp = f->vp, *vc = f->vc, *up = f->up, *uc = f->uc;
+    const orc_coeffs* nb = at_node(s, jb);
+    const double kt_b = nb->k_TT, kTM_b = nb->k_TM, km_b = nb->k_M;
+    const orc_coeffs* hb = at_half(s, jb == 0 ? 0 : n - 2);
+    const double ktp_b = hb->k_TT, kmp_b = hb->k_TM;
+    const double vbar = 0.5 * (vn[jb] + vp[jb]);
+    const double vg = vc[jn] - (2.0 * dx / km_b) * (b->Bi_M * (vbar - b->v_inf) - b->g_inf);
+    const double cplu = 2.0 * b_ * dx * b->Bi_TT;
+    un[jb] = ((nb->c_TT - b_ * (ktp_b + kt_b) - cplu) * up[jb] - c->p->gamma * nb->c_TM * (vn[jb] - vp[jb]) +
+              2.0 * b_ * (ktp_b + kt_b) * uc[jn] + 2.0 * b_ * ratio * kTM_b * (vc[jn] - vg) -
+              4.0 * b_ * dx * (b->Bi_TM * (vbar - b->v_inf) - b->q_inf) + 2.0 * cplu * b->u_inf +
+              2.0 * g_ * (kmp_b * vc[jn] + kTM_b * vg) - g_ * (kmp_b + kTM_b) * (vn[jb] + vp[jb])) /
+             (nb->c_TT + b_ * (ktp_b + kt_b) + cplu);
+}
+
 int orc_df_step_nonlinear(orc_field* f, double dx, const hyg_wall_groups* p, const orc_model* m,
                           const orc_face* left, const orc_face* right,
                           double dt) { /* wall.cpp:196-264 */
     const int n = f->n;
-    const double a = p->Fo_M * dt / (dx * dx);
-    const double b_ = p->Fo_TT * dt / (dx * dx);
-    const double g_ = p->Fo_TM * p->gamma * dt / (dx * dx);
-    const double ratio = p->Fo_TT != 0.0 ? p->Fo_TM * p->gamma / p->Fo_TT : 0.0;
-
+    const nl_consts c = nl_setup(n, dx, p, dt);
     star_tables s;
     const int rc = build_tables(&s, m, n, f->uc, f->vc, 1);
     if (rc) {
@@ -233,53 +312,13 @@ int orc_df_step_nonlinear(orc_field* f, double dx, const hyg_wall_groups* p, con
     }
     double* vn = (double*)malloc(sizeof(double) * (size_t)n * 2);
     double* un = vn + n;
-    const double *vp = f->vp, *vc = f->vc, *up = f->up, *uc = f->uc;
-
-    for (int j = 1; j + 1 < n; ++j) {
-        const double kp = at_half(&s, j)->k_M, km = at_half(&s, j - 1)->k_M, cm = at_node(&s, j)->c_M;
-        vn[j] = ((cm - a * (kp + km)) * vp[j] + 2.0 * a * (kp * vc[j + 1] + km * vc[j - 1])) /
-                (cm + a * (kp + km));
-    }
-    const int jb[2] = {0, n - 1}, jn[2] = {1, n - 2};
-    const orc_face* bcs[2] = {left, right};
-    for (int k = 0; k < 2; ++k) {
-        const orc_face* b = bcs[k];
-        const double km_b = at_node(&s, jb[k])->k_M;
-        const double kp_b = at_half(&s, jb[k] == 0 ? 0 : n - 2)->k_M;
-        const double cm = at_node(&s, jb[k])->c_M;
-        const double cpl = 2.0 * a * dx * b->Bi_M;
-        vn[jb[k]] = ((cm - a * (kp_b + km_b) - cpl) * vp[jb[k]] + 2.0 * a * (kp_b + km_b) * vc[jn[k]] +
-                     4.0 * a * dx * (b->Bi_M * b->v_inf + b->g_inf)) /
-                    (cm + a * (kp_b + km_b) + cpl);
-    }
-    for (int j = 1; j + 1 < n; ++j) {
-        const double ktp = at_half(&s, j)->k_TT, ktm = at_half(&s, j - 1)->k_TT;
-        const double kmp = at_half(&s, j)->k_TM, kmm = at_half(&s, j - 1)->k_TM;
-        const double ctt = at_node(&s, j)->c_TT, ctm = at_node(&s, j)->c_TM;
-        un[j] = ((ctt - b_ * (ktp + ktm)) * up[j] - p->gamma * ctm * (vn[j] - vp[j]) +
-                 2.0 * b_ * (ktp * uc[j + 1] + ktm * uc[j - 1]) +
-                 2.0 * g_ * (kmp * vc[j + 1] + kmm * vc[j - 1]) - g_ * (kmp + kmm) * (vn[j] + vp[j])) /
-                (ctt + b_ * (ktp + ktm));
-    }
-    for (int k = 0; k < 2; ++k) {
-        const orc_face* b = bcs[k];
-        const orc_coeffs* nb = at_node(&s, jb[k]);
-        const double kt_b = nb->k_TT, kTM_b = nb->k_TM, km_b = nb->k_M;
-        const orc_coeffs* hb = at_half(&s, jb[k] == 0 ? 0 : n - 2);
-        const double ktp_b = hb->k_TT, kmp_b = hb->k_TM;
-        const double vbar = 0.5 * (vn[jb[k]] + vp[jb[k]]);
-        const double vg = vc[jn[k]] - (2.0 * dx / km_b) * (b->Bi_M * (vbar - b->v_inf) - b->g_inf);
-        const double cplu = 2.0 * b_ * dx * b->Bi_TT;
-        un[jb[k]] = ((nb->c_TT - b_ * (ktp_b + kt_b) - cplu) * up[jb[k]] -
-                     p->gamma * nb->c_TM * (vn[jb[k]] - vp[jb[k]]) +
-                     2.0 * b_ * (ktp_b + kt_b) * uc[jn[k]] +
-                     2.0 * b_ * ratio * kTM_b * (vc[jn[k]] - vg) -
-                     4.0 * b_ * dx * (b->Bi_TM * (vbar - b->v_inf) - b->q_inf) +
-                     2.0 * cplu * b->u_inf + 2.0 * g_ * (kmp_b * vc[jn[k]] + kTM_b * vg) -
-                     g_ * (kmp_b + kTM_b) * (vn[jb[k]] + vp[jb[k]])) /
-                    (nb->c_TT + b_ * (ktp_b + kt_b) + cplu);
-    }
-    rotate(n, f->vp, f->vc, vn);
+    nl_v_rows(&c, &s, f, vn, 1, n - 1);                 /* wall.cpp:213-217 */
+    nl_v_face(&c, &s, f, vn, 0, left);                  /* wall.cpp:218-229 */
+    nl_v_face(&c, &s, f, vn, 1, right);
+    nl_u_rows(&c, &s, f, vn, un, 1, n - 1);             /* wall.cpp:231-240 */
+    nl_u_face(&c, &s, f, vn, un, 0, left);              /* wall.cpp:241-259 */
+    nl_u_face(&c, &s, f, vn, un, 1, right);
+    rotate(n, f->vp, f->vc, vn);                        /* wall.cpp:261-263 */
     rotate(n, f->up, f->uc, un);
     f->t_star += dt;
     free(vn);
@@ -1170,5 +1209,121 @@ int orc_run_mt(const hyg_model_desc* m, orc_building_state* s, int64_t nsteps, i
     free(fw);
     free(buf);
     free(link0);
+    return rc;
+}
+
+/* ---- orc_march_long_mt: one long wall, its nodes split over threads ------
+ * nsteps of df_step_nonlinear (wall.cpp:196-264) on wall 0 of the batch with
+ * the guard of run(), each thread owning a contiguous node range: the
+ * StarTables of its nodes and half nodes, then its v rows (+ a face row),
+ * then its u rows (+ the face row), then the layer rotation of its range —
+ * barriers between the phases.  A node's new values are a pure function of
+ * layers n and n-1 computed by the same statements as the serial step (the
+ * nl_* pieces above), so the march is bitwise the serial one.  Strict
+ * coefficient failures abort the march with HYG_EDOMAIN (no location). */
+typedef struct {
+    const orc_batch* b;
+    const orc_model* m;
+    int nsteps, nthr, id;
+    double dt;
+    star_tables* s;
+    double *vn, *un;
+    pthread_barrier_t* bar;
+    double* mx;          /* [nthr] max |x| of the new layers */
+    int* dom;            /* [nthr] strict failure */
+    volatile int* stop;
+    int64_t* fail_layer;
+} long_job;
+
+static void* long_run(void* arg) {
+    long_job* J = (long_job*)arg;
+    const orc_batch* b = J->b;
+    const int n = b->n;
+    const int j0 = (int)((int64_t)n * J->id / J->nthr), j1 = (int)((int64_t)n * (J->id + 1) / J->nthr);
+    orc_field f = field_of(b, 0);
+    const nl_consts c = nl_setup(n, b->dx, &b->groups[0], J->dt);
+    star_tables* s = J->s;
+    for (int k = 0; k < J->nsteps; ++k) {
+        const int64_t lay = b->layer0 + k;
+        int bad = 0;
+        if (!s->unit) {                           /* StarTables of layer n (wall.cpp:89-138) */
+            for (int j = j0; j < j1 && !bad; ++j) bad = orc_star(J->m, f.uc[j], f.vc[j], 1, &s->node[j]);
+            for (int j = j0; j < j1 && j + 1 < n && !bad; ++j)
+                bad = orc_star(J->m, 0.5 * (f.uc[j] + f.uc[j + 1]), 0.5 * (f.vc[j] + f.vc[j + 1]), 1, &s->half[j]);
+        }
+        J->dom[J->id] = bad;
+        pthread_barrier_wait(J->bar);
+        int any = 0;
+        for (int i = 0; i < J->nthr; ++i) any |= J->dom[i];
+        if (any) {
+            if (J->id == 0) *J->stop = HYG_EDOMAIN;
+            break;
+        }
+        orc_face L, R;
+        face_of(b, 0, 0, lay, &L);
+        face_of(b, 0, 1, lay, &R);
+        nl_v_rows(&c, s, &f, J->vn, j0, j1);
+        if (j0 == 0) nl_v_face(&c, s, &f, J->vn, 0, &L);
+        if (j1 == n) nl_v_face(&c, s, &f, J->vn, 1, &R);
+        nl_u_rows(&c, s, &f, J->vn, J->un, j0, j1);
+        if (j0 == 0) nl_u_face(&c, s, &f, J->vn, J->un, 0, &L);
+        if (j1 == n) nl_u_face(&c, s, &f, J->vn, J->un, 1, &R);
+        pthread_barrier_wait(J->bar);             /* every row read layers n, n-1 */
+        double mx = 0.0;
+        int inf = 0;
+        for (int j = j0; j < j1; ++j) {           /* rotate (wall.cpp:261-263), max_abs_field (:579-587) */
+            f.vp[j] = f.vc[j];
+            f.vc[j] = J->vn[j];
+            f.up[j] = f.uc[j];
+            f.uc[j] = J->un[j];
+            mx = fmax(mx, fmax(fabs(f.uc[j]), fabs(f.vc[j])));
+            if (!isfinite(f.uc[j]) || !isfinite(f.vc[j])) inf = 1;
+        }
+        J->mx[J->id] = inf ? INFINITY : mx;
+        pthread_barrier_wait(J->bar);
+        if (J->id == 0) {
+            for (int i = 0; i < J->nthr; ++i)
+                if (!(J->mx[i] <= b->divergence_norm)) *J->stop = HYG_EDIVERGED;
+            if (*J->stop) *J->fail_layer = lay + 1;
+        }
+        pthread_barrier_wait(J->bar);
+        if (*J->stop) break;
+    }
+    return NULL;
+}
+
+int orc_march_long_mt(const orc_batch* b, const orc_model* m, int nsteps, double dt, int nthreads,
+                      int64_t* fail_layer) {
+    const int n = b->n;
+    if (b->n_walls != 1 || n < 3) return HYG_EINVAL;
+    if (nthreads > n / 64) nthreads = n / 64 > 0 ? n / 64 : 1;
+    if (nthreads < 1) nthreads = 1;
+    star_tables s;
+    s.unit = (m == NULL || m->kind == ORC_COEFF_CONSTANT);
+    s.node = s.unit ? NULL : (orc_coeffs*)malloc(sizeof(orc_coeffs) * (size_t)(2 * n - 1));
+    s.half = s.unit ? NULL : s.node + n;
+    double* buf = (double*)malloc(sizeof(double) * (size_t)(2 * n + 2 * nthreads));
+    int* dom = (int*)calloc((size_t)nthreads, sizeof(int));
+    pthread_barrier_t bar;
+    pthread_barrier_init(&bar, NULL, (unsigned)nthreads);
+    volatile int stop = 0;
+    int64_t fl = -1;
+    long_job* jobs = (long_job*)calloc((size_t)nthreads, sizeof(long_job));
+    pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+    for (int i = 0; i < nthreads; ++i) {
+        long_job J = {b, m, nsteps, nthreads, i, dt, &s, buf, buf + n, &bar, buf + 2 * n, dom, &stop, &fl};
+        jobs[i] = J;
+        if (i) pthread_create(&th[i], NULL, long_run, &jobs[i]);
+    }
+    long_run(&jobs[0]);
+    for (int i = 1; i < nthreads; ++i) pthread_join(th[i], NULL);
+    pthread_barrier_destroy(&bar);
+    if (fail_layer) *fail_layer = fl;
+    const int rc = stop;
+    free(jobs);
+    free(th);
+    free(dom);
+    free(buf);
+    free(s.node);
     return rc;
 }

@@ -68,7 +68,10 @@ def oracle_run(impl, model, init, nsteps, boot, tables=None, dt=None, nthreads=N
         while L + n < nsteps and dts[L + n] == d:
             n += 1
         wb.set_layer0(L, tab[L:])
-        rc, fl, fw = O.march(impl, wb, n, float(d), nthreads)
+        if impl == "oracle" and model.n_walls == 1 and model.n_nodes >= 4096 and nthreads > 1:
+            rc, fl, fw = O.march_long_mt(wb, n, float(d), nthreads)    # one long wall: nodes over threads
+        else:
+            rc, fl, fw = O.march(impl, wb, n, float(d), nthreads)
         assert rc == 0, (rc, fl, fw)
         L += n
     return {k: wb.state[k] for k in FIELDS}

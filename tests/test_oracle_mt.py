@@ -40,3 +40,29 @@ def test_run_mt_guard_matches_serial():
     assert ra[0] != 0 and ra[:2] == rc[:2] and a.fail_wall == c.fail_wall
     for k in a.state:
         assert np.array_equal(a.state[k], c.state[k]), k
+
+
+@pytest.mark.parametrize("n,steps,threads", [(5000, 60, 4), (4099, 17, 7), (70001, 9, 16)])
+def test_long_wall_mt_bitwise_serial(n, steps, threads):
+    """orc_march_long_mt (one long d(v) wall, nodes split over threads) equals
+    the serial orc_df_step_nonlinear march bit for bit."""
+    w = workloads.long_domain(n_nodes=n, nsteps=steps)
+    times = workloads.accumulate_times(np.full(steps, w.model.dt))
+    tab = O.forcing_table(w.model, times, 0, {})
+    a, b = O.WallBatch(w.model, w.init, tab), O.WallBatch(w.model, w.init, tab)
+    ra = O.march("oracle", a, steps, w.model.dt, 1)
+    rb = O.march_long_mt(b, steps, w.model.dt, threads)
+    assert ra[0] == 0 and rb[0] == 0
+    for k in a.state:
+        assert np.array_equal(a.state[k], b.state[k]), k
+
+
+def test_long_wall_mt_guard():
+    w = workloads.long_domain(n_nodes=6000, nsteps=40)
+    w.model.divergence_norm = 1.0 + 1e-3         # the initial modes already exceed it
+    times = workloads.accumulate_times(np.full(40, w.model.dt))
+    tab = O.forcing_table(w.model, times, 0, {})
+    a, b = O.WallBatch(w.model, w.init, tab), O.WallBatch(w.model, w.init, tab)
+    ra = O.march("oracle", a, 40, w.model.dt, 1)
+    rb = O.march_long_mt(b, 40, w.model.dt, 5)
+    assert ra[0] == rb[0] != 0 and ra[1] == rb[1] == 1
