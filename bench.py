@@ -257,7 +257,8 @@ def ref_bench(args, steps: int, warmup: int, threads: int) -> dict:
     if not REF_BENCH.exists():
         raise FileNotFoundError(f"{REF_BENCH} is missing (built from /root/reference by `make -C oracle refbench`)")
     cmd = [str(REF_BENCH), "--config", args.config, "--steps", str(steps), "--warmup", str(warmup),
-           "--threads", str(threads), "--walls", str(args.walls), "--nodes", str(args.nodes),
+           "--threads", str(threads), "--walls", str(args.walls),
+           "--nodes", str(128 if args.config == "cfg3" else args.nodes),
            "--zones", str(args.zones), "--long-nodes", str(args.long_nodes),
            "--material-walls", str(args.material_walls)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=3600)

@@ -329,9 +329,17 @@ int64_t hyg_launch_count(hyg_ctx* ctx);
  * HYG_TUNE_RING_GRID: cap on the persistent zone-ring kernel's grid (K4r,
  * k_ring_reg.cuh; 0 = one CTA per SM).  A cap below the number of zone blocks
  * makes every CTA walk several blocks, so small rings under test run the
- * next-block prefetch path the full-size ring runs.  HYG_EINVAL for an
+ * next-block prefetch path the full-size ring runs.  HYG_TUNE_RING_KERNEL
+ * picks the zone-ring kernel: 0 = automatic (K5 k_ring_pipe.cuh where it
+ * applies, else K4r), 1 = K4r (k_ring_reg.cuh), 2 = K4 (k_ring.cuh), for
+ * A/B measurement and cross-checks.  HYG_TUNE_MATERIAL_FAST = 1 evaluates the
+ * load-bearing material with the fast table-driven exp/log and reciprocal
+ * quotients (~2x throughput, a few ulp per coefficient: the reference's
+ * wall_nonlinear fixture then drifts 1.7e-9 relative over 8e4 steps); 0 (the
+ * default) is the parity evaluation (hyg_crmath.cuh, IEEE divisions, no FMA
+ * contraction).  HYG_EINVAL for an
  * unknown knob or a negative value. */
-enum { HYG_TUNE_RING_GRID = 1 };
+enum { HYG_TUNE_RING_GRID = 1, HYG_TUNE_RING_KERNEL = 2, HYG_TUNE_MATERIAL_FAST = 3 };
 int hyg_set_tuning(hyg_ctx* ctx, int32_t knob, int64_t value);
 
 /* Device FP64 FMA throughput probe (DFMA loop), TFLOP/s counting FMA = 2. */
@@ -342,6 +350,10 @@ int hyg_selftest_fastmath(int32_t device, int32_t n, const double* x, double* ex
 /* Self-test of the device log of the material correlations (flog_pos,
  * hyg_fastmath.cuh; positive normal x): log_out[i] = ln x[i] on the device. */
 int hyg_selftest_fastlog(int32_t device, int32_t n, const double* x, double* log_out);
+/* Self-test of the accurate device exp/log/log10/pow of the material parity
+ * path (hyg_crmath.cuh): out[0..n) = exp(x), [n..2n) = log(x), [2n..3n) =
+ * log10(x), [3n..4n) = pow(x, y), computed on the device. */
+int hyg_selftest_crmath(int32_t device, int32_t n, const double* x, const double* y, double* out);
 /* Device FP32 FMA throughput probe (FFMA loop), TFLOP/s counting FMA = 2. */
 int hyg_probe_fp32_peak(int32_t device, double* tflops);
 

@@ -1,0 +1,165 @@
+// acceptance_check.cpp — TEST INFRASTRUCTURE: the reference's own scenario
+// fixtures and acceptance criteria 5 and 6 (proj/tests/acceptance.cpp:165-230)
+// evaluated on the drop-in hygro::gpu::run (include/hygro_b200.hpp).
+//
+//   acceptance_check fixtures <scenario.json>...
+//       the fixture at its own horizon and cadence through the reference's
+//       run() (building.cpp:303-356) and through hygro::gpu::run: every frame's
+//       wall u, v and zone u_a, v_a compared as doubles (relative L-inf over all
+//       frames), frame times, step counts, start passes; wall clocks of both.
+//   acceptance_check c5 <dir>
+//       criterion 5: EulerImplicit with eta = 1e-10 dt* on one_zone_linear (80 h),
+//       two_zone_nonlinear (12 h), wall_nonlinear (12 h); mean sub-iterations of
+//       both runs and the windows [2,5], [4,12], [5,15].
+//   acceptance_check c6 <dir>
+//       criterion 6: DF / EulerImplicit wall-clock ratio of two_zone_nonlinear at
+//       tau* = 20 and 40 on the device (limit 40 %, drift <= 10 points).
+// One JSON object per line on stdout; exit 1 when a check fails.
+// Built by oracle/Makefile (target `scenario`); run by tests/test_gpu_acceptance.py.
+#define HYGRO_B200_WITH_REFERENCE
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hygro/errors.hpp"
+#include "hygro/scenario.hpp"
+#include "hygro_b200.hpp"
+
+using namespace hygro;
+
+namespace {
+
+struct Cmp {
+    double num = 0.0, den = 0.0;
+    void add(double got, double ref) {
+        num = std::max(num, std::fabs(got - ref));
+        den = std::max(den, std::fabs(ref));
+        if (!std::isfinite(got)) num = INFINITY;
+    }
+    double rel() const { return den > 0 ? num / den : num; }
+};
+
+int fixtures(int argc, char** argv) {
+    int bad = 0;
+    for (int i = 2; i < argc; ++i) {
+        const Scenario sc = load_scenario(argv[i]);
+        SimulationResult cpu, gpu;
+        std::string err;
+        try {
+            cpu = run(sc.model, sc.cadence);
+            gpu = hygro::gpu::run(sc.model, sc.cadence);
+        } catch (const std::exception& e) {
+            err = e.what();
+        }
+        Cmp walls, zones;
+        double tmax = 0.0;
+        const bool same_frames = err.empty() && cpu.frames.size() == gpu.frames.size();
+        if (same_frames) {
+            for (size_t f = 0; f < cpu.frames.size(); ++f) {
+                const Frame &a = cpu.frames[f], &b = gpu.frames[f];
+                tmax = std::max(tmax, std::fabs(a.t - b.t));
+                for (size_t w = 0; w < a.wall_u.size(); ++w)
+                    for (size_t j = 0; j < a.wall_u[w].size(); ++j) {
+                        walls.add(b.wall_u[w][j], a.wall_u[w][j]);
+                        walls.add(b.wall_v[w][j], a.wall_v[w][j]);
+                    }
+                for (size_t z = 0; z < a.zones.size(); ++z) {
+                    zones.add(b.zones[z].u_a, a.zones[z].u_a);
+                    zones.add(b.zones[z].v_a, a.zones[z].v_a);
+                }
+            }
+        }
+        const bool ok = same_frames && walls.rel() <= 1e-10 && zones.rel() <= 1e-10 && tmax == 0.0 &&
+                        cpu.steps == gpu.steps && cpu.bootstrap_subiters == gpu.bootstrap_subiters;
+        bad += !ok;
+        std::printf("{\"check\": \"fixture\", \"name\": \"%s\", \"ok\": %s, \"horizon\": %g, \"cadence\": %g, "
+                    "\"frames\": [%zu, %zu], \"steps\": [%ld, %ld], \"boot_passes\": [%d, %d], "
+                    "\"rel_linf_walls\": %.3e, \"rel_linf_zones\": %.3e, \"frame_t_diff\": %g, "
+                    "\"wall_clock_s\": {\"cpu\": %.3f, \"gpu\": %.3f}, \"error\": \"%s\"}\n",
+                    sc.name.c_str(), ok ? "true" : "false", sc.model.horizon, sc.cadence, cpu.frames.size(),
+                    gpu.frames.size(), cpu.steps, gpu.steps, cpu.bootstrap_subiters, gpu.bootstrap_subiters,
+                    walls.rel(), zones.rel(), tmax, cpu.wall_clock_s, gpu.wall_clock_s, err.c_str());
+        std::fflush(stdout);
+    }
+    return bad ? 1 : 0;
+}
+
+int criterion5(const std::string& dir) {
+    struct Case { const char* file; double horizon, lo, hi; };
+    const Case cases[3] = {{"one_zone_linear.json", 0.0, 2.0, 5.0},
+                           {"two_zone_nonlinear.json", 12.0, 4.0, 12.0},
+                           {"wall_nonlinear.json", 12.0, 5.0, 15.0}};
+    int bad = 0;
+    for (const Case& c : cases) {
+        Scenario sc = load_scenario(dir + "/" + c.file);
+        BuildingModel m = sc.model;
+        m.scheme = Scheme::EulerImplicit;
+        m.eta_factor = 1e-10;
+        if (c.horizon > 0) m.horizon = c.horizon;
+        const SimulationResult cpu = run(m, 1.0);
+        const SimulationResult gpu = hygro::gpu::run(m, 1.0);
+        const bool in_window = gpu.mean_subiters >= c.lo && gpu.mean_subiters <= c.hi;
+        // at eta = 1e-10 dt* a pass count can flip where a residual lands within
+        // an ulp of the tolerance: the means must agree to 0.1 %
+        const bool same = gpu.mean_subiters == cpu.mean_subiters && gpu.max_subiters_seen == cpu.max_subiters_seen;
+        const bool close = std::fabs(gpu.mean_subiters - cpu.mean_subiters) <= 1e-3 * cpu.mean_subiters;
+        bad += !(in_window && close);
+        std::printf("{\"check\": \"criterion5\", \"name\": \"%s\", \"ok\": %s, \"identical\": %s, \"horizon\": %g, "
+                    "\"mean_subiters\": {\"cpu\": %.6f, \"gpu\": %.6f}, \"max_subiters\": {\"cpu\": %d, \"gpu\": %d}, "
+                    "\"window\": [%g, %g], \"wall_clock_s\": {\"cpu\": %.3f, \"gpu\": %.3f}}\n",
+                    sc.name.c_str(), (in_window && close) ? "true" : "false", same ? "true" : "false", m.horizon,
+                    cpu.mean_subiters,
+                    gpu.mean_subiters, cpu.max_subiters_seen, gpu.max_subiters_seen, c.lo, c.hi, cpu.wall_clock_s,
+                    gpu.wall_clock_s);
+        std::fflush(stdout);
+    }
+    return bad ? 1 : 0;
+}
+
+int criterion6(const std::string& dir, bool with_cpu) {
+    const Scenario sc = load_scenario(dir + "/two_zone_nonlinear.json");
+    auto clock_of = [&](Scheme s, double horizon, bool gpu) {
+        BuildingModel m = sc.model;
+        m.scheme = s;
+        m.horizon = horizon;
+        return gpu ? hygro::gpu::run(m, 1.0).wall_clock_s : run(m, 1.0).wall_clock_s;
+    };
+    hygro::gpu::run(sc.model, 1.0);   // device warm-up (context, module load)
+    int bad = 0;
+    for (int gpu = 1; gpu >= (with_cpu ? 0 : 1); --gpu) {
+        const double df_20 = clock_of(Scheme::DufortFrankel, 20.0, gpu);
+        const double im_20 = clock_of(Scheme::EulerImplicit, 20.0, gpu);
+        const double df_40 = clock_of(Scheme::DufortFrankel, 40.0, gpu);
+        const double im_40 = clock_of(Scheme::EulerImplicit, 40.0, gpu);
+        const double r20 = df_20 / im_20, r40 = df_40 / im_40;
+        const bool ok = r20 <= 0.40 && r40 <= 0.40 && std::fabs(r20 - r40) <= 0.10;
+        if (gpu) bad += !ok;
+        std::printf("{\"check\": \"criterion6\", \"path\": \"%s\", \"ok\": %s, \"ratio_20\": %.4f, \"ratio_40\": %.4f, "
+                    "\"df_s\": [%.3f, %.3f], \"implicit_s\": [%.3f, %.3f]}\n",
+                    gpu ? "hygro::gpu::run" : "hygro::run (CPU reference)", ok ? "true" : "false", r20, r40, df_20,
+                    df_40, im_20, im_40);
+        std::fflush(stdout);
+    }
+    return bad ? 1 : 0;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    if (argc < 3) {
+        std::fprintf(stderr, "usage: acceptance_check fixtures <json>... | c5 <dir> | c6 <dir> [cpu]\n");
+        return 2;
+    }
+    const std::string mode = argv[1];
+    try {
+        if (mode == "fixtures") return fixtures(argc, argv);
+        if (mode == "c5") return criterion5(argv[2]);
+        if (mode == "c6") return criterion6(argv[2], argc > 3 && std::string(argv[3]) == "cpu");
+    } catch (const std::exception& e) {
+        std::printf("{\"check\": \"%s\", \"ok\": false, \"error\": \"%s\"}\n", mode.c_str(), e.what());
+        return 1;
+    }
+    return 2;
+}

@@ -16,7 +16,7 @@ HYG_COEFF_CONSTANT, HYG_COEFF_ANALYTIC_D, HYG_COEFF_MATERIAL = 0, 1, 2
 HYG_F64, HYG_F32 = 0, 1
 HYG_BOOT_IMPLICIT, HYG_BOOT_EXPLICIT = 0, 1
 HYG_SCHEME_DF, HYG_SCHEME_EULER_IMPLICIT, HYG_SCHEME_EULER_EXPLICIT = 0, 1, 2
-HYG_TUNE_RING_GRID = 1
+HYG_TUNE_RING_GRID, HYG_TUNE_RING_KERNEL, HYG_TUNE_MATERIAL_FAST = 1, 2, 3
 
 dp = C.POINTER(C.c_double)
 
@@ -148,6 +148,7 @@ PROTOTYPES = {
     "hyg_probe_fp32_peak": (C.c_int, [C.c_int32, dp]),
     "hyg_selftest_fastmath": (C.c_int, [C.c_int32, C.c_int32, dp, dp, dp]),
     "hyg_selftest_fastlog": (C.c_int, [C.c_int32, C.c_int32, dp, dp]),
+    "hyg_selftest_crmath": (C.c_int, [C.c_int32, C.c_int32, dp, dp, dp]),
     "hyg_saturation_pressure": (C.c_int, [C.c_double, dp]),
     "hyg_material_evaluate": (C.c_int, [C.c_double, C.c_double, C.c_int32, C.POINTER(CoeffSet)]),
     "hyg_scale_wall": (C.c_int, [dp, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,

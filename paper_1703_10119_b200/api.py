@@ -467,10 +467,13 @@ class Context:
             out.append(dict(name=name.value.decode(), launches=n.value, ms=ms.value, node_updates=upd.value))
         return out
 
-    TUNING = {"ring_grid": A.HYG_TUNE_RING_GRID}
+    TUNING = {"ring_grid": A.HYG_TUNE_RING_GRID, "ring_kernel": A.HYG_TUNE_RING_KERNEL,
+              "material_fast": A.HYG_TUNE_MATERIAL_FAST}
 
     def set_tuning(self, knob: str, value: int) -> None:
-        """Launch-shape knob (hyg_set_tuning), e.g. ring_grid = cap on K4r's persistent grid."""
+        """Launch-shape knob (hyg_set_tuning): ring_grid = cap on the persistent
+        zone-ring grid; ring_kernel = 0 auto (K5), 1 K4r, 2 K4; material_fast = 1 for
+        the fast (few-ulp) material evaluation instead of the parity one."""
         _check(self.lib.hyg_set_tuning(self.h, self.TUNING[knob], int(value)), None, "hyg_set_tuning")
 
     def reset_kernel_stats(self):

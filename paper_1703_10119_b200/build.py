@@ -17,11 +17,15 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libhygro_b200.so"
 SOURCES = [CSRC / "hyg_api.cu", CSRC / "hyg_scaling.cpp"]
-DEPS = SOURCES + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "hygro_b200.h"]
+DEPS = SOURCES + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [ROOT / "include" / "hygro_b200.h"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
     "-cudart", "static", "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills",
+    # no FMA contraction of plain a*b+c: the hot kernels write their FMAs
+    # explicitly; everything else (material correlations, literal rows, zone
+    # balances) then rounds like the reference's x86-64 build
+    "-fmad=false",
 ]
 
 

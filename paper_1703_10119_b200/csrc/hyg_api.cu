@@ -28,6 +28,7 @@
 #include "k_material.cuh"
 #include "k_ring.cuh"
 #include "k_ring_reg.cuh"
+#include "k_ring_pipe.cuh"
 
 using namespace hyg;
 
@@ -39,6 +40,10 @@ constexpr int kRingS = 8;       // K4: steps per launch (halo depth S-1 zones)
 #define HYG_RING_REG_S 8
 #endif
 constexpr int kRingRegS = HYG_RING_REG_S;   // K4r: steps per launch (S = 9 measured 3.12e11 vs 3.49e11 at 8: spills)
+#ifndef HYG_RING_PIPE_S
+#define HYG_RING_PIPE_S 12
+#endif
+constexpr int kRingPipeS = HYG_RING_PIPE_S; // K5: steps per launch
 constexpr int kWarps = 4;       // warps per CTA of K1
 
 struct SigHost {
@@ -209,7 +214,10 @@ struct hyg_ctx {
     bool ring = false;               // K4: zone-ring temporal blocking applies
     int ring_W = 0, ring_B = 0;
     int ring_reg_B = 0;              // K4r (registers + prefetch): zones per CTA, 0 if not applicable
-    int ring_grid_cap = 0;           // HYG_TUNE_RING_GRID: K4r persistent grid cap (0: one CTA per SM)
+    int ring_grid_cap = 0;           // HYG_TUNE_RING_GRID: K4r/K5 persistent grid cap (0: one CTA per SM)
+    int ring_pipe_B = 0;             // K5 (k_ring_pipe.cuh): zones per block, 0 if not applicable
+    int ring_kernel = 0;             // HYG_TUNE_RING_KERNEL: 0 auto (K5, else K4r), 1 K4r, 2 K4
+    bool mat_fast = false;           // HYG_TUNE_MATERIAL_FAST: evaluate_fast + reciprocal rows
     double* d_ring_zp = nullptr;     // K4r per-zone parameter blocks [zones][kRingZP]
     bool ring_reg_small = false;     // every zone: <= 6 wall links, <= 2 ring peers
     int rad_groups = 0, rad_terms = 0;
@@ -464,6 +472,7 @@ StarArgs star_args(hyg_ctx* c, const double* u, const double* v, bool strict, in
     s.dom_key = c->d_dom;
     s.own0 = c->own_c0;
     s.own1 = c->own_c1;
+    s.exact = c->mat_fast ? 0 : 1;
     return s;
 }
 
@@ -634,7 +643,8 @@ int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
                 const int mgrid = static_cast<int>((c->cells() + kMatCells - 1) / kMatCells);
                 const int zblocks = (z.n_zones + kMatThreads - 1) / kMatThreads;
                 LaunchScope ls(c, "material_step", static_cast<double>(c->cells()));
-                k_material_step<<<mgrid + zblocks, kMatThreads, 0, c->stream>>>(a, sa, z, mgrid);
+                if (c->mat_fast) k_material_step<false><<<mgrid + zblocks, kMatThreads, 0, c->stream>>>(a, sa, z, mgrid);
+                else k_material_step<true><<<mgrid + zblocks, kMatThreads, 0, c->stream>>>(a, sa, z, mgrid);
                 if (!c->zones.empty()) c->zcur ^= 1;
             } else if (c->zones.empty()) {
                 LaunchScope ls(c, "df_step_general", static_cast<double>(c->cells()));
@@ -1053,6 +1063,16 @@ void launch_ring_reg(const RingArgs& a, int threads, size_t smem, cudaStream_t s
     k<<<grid, threads, smem, s>>>(a);
 }
 
+void launch_ring_pipe(const RingArgs& a, size_t smem, cudaStream_t s, int device, int grid_cap) {
+    using Sh = RingPipeShape<kRingPipeS>;
+    auto k = k_ring_pipe<kRingPipeS, Sh::kThreads>;
+    ensure_smem_attr(k, device, 227 * 1024);
+    const int nblk = (a.n_zones + a.B - 1) / a.B;
+    int grid = std::max(1, std::min(nblk, sm_count(device)));
+    if (grid_cap > 0) grid = std::min(grid, grid_cap);
+    k<<<grid, Sh::threads(a.B, a.W), smem, s>>>(a);
+}
+
 template <int NPT>
 void launch_ring(const RingArgs& a, int grid, int threads, size_t smem, cudaStream_t s, int device) {
     auto k = k_ring_tiled<NPT, kRingS>;
@@ -1061,6 +1081,9 @@ void launch_ring(const RingArgs& a, int grid, int threads, size_t smem, cudaStre
 }
 
 int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool reg = true) {
+    // K5 (pipelined, S = 12) where it applies, unless a tuning knob picks K4r/K4
+    const bool pipe = reg && c->ring_pipe_B > 0 && c->norm >= 2.0 && c->ring_kernel == 0;
+    if (c->ring_kernel == 2) reg = false;
     if (c->coef_dt != dt) {
         LaunchScope ls(c, "coupled_coef", 0.0);
         k_coupled_coef<<<(c->n_walls + 127) / 128, 128, 0, c->stream>>>(c->n_walls, c->dx, dt, c->d_groups,
@@ -1073,12 +1096,13 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool
     // flagged K4r launch is replayed by K4 and its exact guard
     reg = reg && c->ring_reg_B > 0 && c->norm >= 2.0;
     const int Z = static_cast<int>(c->zones.size()), W = c->ring_W, npt = c->n / 16;
-    const int B = reg ? c->ring_reg_B : c->ring_B;
+    const int B = pipe ? c->ring_pipe_B : reg ? c->ring_reg_B : c->ring_B;
     const int grid = (Z + B - 1) / B;
     const int rw = RingShape<8, kRingS>::row_width(nch, nsrc);
-    const int S = reg ? kRingRegS : kRingS;             // steps per launch
+    const int S = pipe ? kRingPipeS : reg ? kRingRegS : kRingS;   // steps per launch
     const int threads = reg ? RingRegShape<8, kRingRegS>::threads(B, W) : RingShape<8, kRingS>::threads(B, W);
-    const size_t smem = reg ? RingRegShape<8, kRingRegS>::smem_doubles(B, W, c->n, rw) * sizeof(double)
+    const size_t smem = pipe ? RingPipeShape<kRingPipeS>::smem_doubles(B, W, rw) * sizeof(double)
+                        : reg ? RingRegShape<8, kRingRegS>::smem_doubles(B, W, c->n, rw) * sizeof(double)
                         : npt == 4 ? RingShape<4, kRingS>::smem_bytes(B, W, nch, nsrc)
                         : npt == 8 ? RingShape<8, kRingS>::smem_bytes(B, W, nch, nsrc)
                                    : RingShape<16, kRingS>::smem_bytes(B, W, nch, nsrc);
@@ -1129,8 +1153,10 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool
             a.zv_in = c->zv[zf];
             a.zu_out = c->zu[1 - zf];
             a.zv_out = c->zv[1 - zf];
-            LaunchScope ls(c, reg ? "ring_reg" : "ring_tiled", static_cast<double>(c->cells()) * a.steps);
-            if (reg) {
+            LaunchScope ls(c, pipe ? "ring_pipe" : reg ? "ring_reg" : "ring_tiled", static_cast<double>(c->cells()) * a.steps);
+            if (pipe) {
+                launch_ring_pipe(a, smem, c->stream, c->device, c->ring_grid_cap);
+            } else if (reg) {
                 if (npt == 4) launch_ring_reg<4>(a, threads, smem, c->stream, c->device, c->ring_reg_small, c->ring_grid_cap);
                 else launch_ring_reg<8>(a, threads, smem, c->stream, c->device, c->ring_reg_small, c->ring_grid_cap);
             } else if (npt == 4) launch_ring<4>(a, grid, threads, smem, c->stream, c->device);
@@ -1469,6 +1495,16 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
                 };
                 while (Br > 0 && !fits_r(Br)) --Br;
                 c->ring_reg_B = Br;
+                // K5: 128-node walls; the CTA's roles must fit its compiled size
+                using SP = RingPipeShape<kRingPipeS>;
+                int Bp = npt == 8 ? std::min(Z, SP::kB) : 0;
+                auto fits_p = [&](int b) {
+                    const int rw = RingShape<8, kRingS>::row_width(nch, nsrc);
+                    return SP::threads(b, W) <= SP::kThreads && SP::local_zones(b) <= 64 &&
+                           SP::smem_doubles(b, W, rw) * sizeof(double) <= 227u * 1024u;
+                };
+                while (Bp > 0 && !fits_p(Bp)) --Bp;
+                c->ring_pipe_B = Bp;
             }
             if (B >= 1) {
                 c->ring = true;
@@ -1563,6 +1599,7 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
             c->ring_reg_small = true;
             for (const ZoneDev& d : c->zones)
                 c->ring_reg_small = c->ring_reg_small && d.wall_end - d.wall_begin <= 6 && d.inz_end - d.inz_begin <= 2;
+            if (!c->ring_reg_small) c->ring_pipe_B = 0;   // K5 walks exactly 6 link and 2 peer slots
             for (size_t z = 0; z < c->zones.size(); ++z) {
                 const ZoneDev& d = c->zones[z];
                 double* b = &zp[z * kRingZP];
@@ -2206,6 +2243,14 @@ int hyg_set_tuning(hyg_ctx* c, int32_t knob, int64_t value) {
     if (!c || value < 0) return HYG_EINVAL;
     switch (knob) {
         case HYG_TUNE_RING_GRID: c->ring_grid_cap = static_cast<int>(std::min<int64_t>(value, INT32_MAX)); return HYG_OK;
+        case HYG_TUNE_RING_KERNEL:
+            if (value > 2) return HYG_EINVAL;
+            c->ring_kernel = static_cast<int>(value);
+            return HYG_OK;
+        case HYG_TUNE_MATERIAL_FAST:
+            if (value > 1) return HYG_EINVAL;
+            c->mat_fast = value != 0;
+            return HYG_OK;
         default: return HYG_EINVAL;
     }
 }
@@ -2264,11 +2309,35 @@ __global__ void k_fastmath(int n, const double* x, double* e, double* r) {
         r[i] = frcp(x[i]);
     }
 }
+__global__ void k_crmath(int n, const double* x, const double* y, double* o) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        o[i] = cr::exp(x[i]);
+        o[n + i] = cr::log(x[i]);
+        o[2 * n + i] = cr::log10(x[i]);
+        o[3 * n + i] = cr::pow(x[i], y[i]);
+    }
+}
 __global__ void k_fastlog(int n, const double* x, double* l) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) l[i] = flog_pos(x[i]);
 }
 }  // namespace
+
+extern "C" int hyg_selftest_crmath(int32_t device, int32_t n, const double* x, const double* y, double* out) {
+    hyg_status* status = nullptr;
+    if (n <= 0 || !x || !y || !out) return HYG_EINVAL;
+    HYG_CUDA(cudaSetDevice(device));
+    double* d = nullptr;
+    HYG_CUDA(cudaMalloc(&d, sizeof(double) * 6 * n));
+    HYG_CUDA(cudaMemcpy(d, x, sizeof(double) * n, cudaMemcpyHostToDevice));
+    HYG_CUDA(cudaMemcpy(d + n, y, sizeof(double) * n, cudaMemcpyHostToDevice));
+    k_crmath<<<(n + 255) / 256, 256>>>(n, d, d + n, d + 2 * n);
+    HYG_CUDA(cudaGetLastError());
+    HYG_CUDA(cudaMemcpy(out, d + 2 * n, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    return HYG_OK;
+}
 
 extern "C" int hyg_selftest_fastlog(int32_t device, int32_t n, const double* x, double* log_out) {
     hyg_status* status = nullptr;

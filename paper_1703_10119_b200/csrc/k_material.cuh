@@ -37,6 +37,7 @@ struct StarArgs {
     unsigned long long* fail_key;
     unsigned long long* dom_key;   // (wall << 32) | order, order = j (node) or n + j (half)
     int64_t own0, own1;
+    int exact;                  // 1: the parity evaluation (CrMath, IEEE divisions); 0: evaluate_fast
 };
 
 __device__ __forceinline__ bool star_at(const StarArgs& a, int wk, int w, double u, double v, mat::Set& s) {
@@ -44,7 +45,7 @@ __device__ __forceinline__ bool star_at(const StarArgs& a, int wk, int w, double
         s = mat::Set{1.0, analytic_kM(a.p, v), 1.0, 1.0, 1.0, 1.0};
         return true;
     }
-    return mat::star(u, v, a.T_i, a.P_vi, a.ref[w], a.strict != 0, s);
+    return mat::star(u, v, a.T_i, a.P_vi, a.ref[w], a.strict != 0, s, a.exact != 0);
 }
 
 __device__ __forceinline__ void star_fail(const StarArgs& a, int w, unsigned order) {
@@ -237,21 +238,23 @@ constexpr int kMatThreads = 256, kMatCells = 255;
 
 // df_step_nonlinear rows (wall.cpp:213-259) from the CTA's shared tables:
 // node f at nS[f*256 + t], half (j-1)+1/2 at hS[f*256 + t], j+1/2 at hS[f*256 + t+1]
-// p: the wall's groups, loaded by the caller before the StarTables evaluation
+// p: the wall's groups, loaded by the caller before the StarTables evaluation.
+// EXACT (the default, parity path): the reference's statements with IEEE
+// divisions (and, the library being built with -fmad=false, no contraction).
+// !EXACT (HYG_TUNE_MATERIAL_FAST): reciprocals (frcp, 3 FMAs) instead of the
+// divisions, <= 1 ulp per quotient (cfg5 1.78e10 -> 1.90e10); a zero
+// denominator gives NaN where the division gave inf, both trip the guard.
+template <bool EXACT>
 __device__ __forceinline__ void material_cell(const StepArgs& a, const NodeIn& x, int w, int j, const Groups& p,
                                               const double* nS, const double* hS, int t, double& un, double& vn) {
     const int n = a.n;
     const double dx = a.dx, dt = a.dt;
-    // reciprocals (frcp, 3 FMAs) instead of IEEE divisions: <= 1 ulp per
-    // quotient (the parity bound is 1e-10); a zero denominator gives NaN
-    // where the division gave inf, and both trip the divergence guard
-    // (measured: cfg5 1.78e10 -> 1.90e10)
-    const double idx2 = frcp(dx * dx);
-    const double ad = p.Fo_M * dt * idx2;
-    const double b_ = p.Fo_TT * dt * idx2;
-    const double g_ = p.Fo_TM * p.gamma * dt * idx2;
-    const double ratio = p.Fo_TT != 0.0 ? p.Fo_TM * p.gamma * frcp(p.Fo_TT) : 0.0;
-#define MAT_DIV(x, y) ((x) * frcp(y))
+    const double idx2 = EXACT ? 0.0 : frcp(dx * dx);
+    const double ad = EXACT ? p.Fo_M * dt / (dx * dx) : p.Fo_M * dt * idx2;
+    const double b_ = EXACT ? p.Fo_TT * dt / (dx * dx) : p.Fo_TT * dt * idx2;
+    const double g_ = EXACT ? p.Fo_TM * p.gamma * dt / (dx * dx) : p.Fo_TM * p.gamma * dt * idx2;
+    const double ratio = p.Fo_TT != 0.0 ? (EXACT ? p.Fo_TM * p.gamma / p.Fo_TT : p.Fo_TM * p.gamma * frcp(p.Fo_TT)) : 0.0;
+#define MAT_DIV(x, y) (EXACT ? (x) / (y) : (x) * frcp(y))
     auto nd = [&](int f) { return nS[f * kMatThreads + t]; };
     auto hl = [&](int f) { return hS[f * kMatThreads + t]; };       // (j-1)+1/2
     auto hr = [&](int f) { return hS[f * kMatThreads + t + 1]; };   // j+1/2
@@ -289,6 +292,7 @@ __device__ __forceinline__ void material_cell(const StepArgs& a, const NodeIn& x
 }
 #undef MAT_DIV
 
+template <bool EXACT>
 __global__ void __launch_bounds__(kMatThreads, 4) k_material_step(const StepArgs a, const StarArgs s,
                                                               const ZoneArgs z, int wall_blocks) {
     if (static_cast<int>(blockIdx.x) >= wall_blocks) {              // zones (step_explicit :179-183)
@@ -345,7 +349,7 @@ __global__ void __launch_bounds__(kMatThreads, 4) k_material_step(const StepArgs
     if (!out_cell || frozen) return;
     double un, vn;
     if (wk == kCoeffConstant) coupled_node(a, w, j, x, un, vn);
-    else material_cell(a, x, w, j, gp, nS, hS, t, un, vn);
+    else material_cell<EXACT>(a, x, w, j, gp, nS, hS, t, un, vn);
     a.out[1][c] = un;
     a.out[3][c] = vn;
     if (own && (!(fabs(un) <= a.norm) || !(fabs(vn) <= a.norm))) {

@@ -52,3 +52,36 @@ def test_flog_accuracy():
     err = np.abs(out - ref)
     assert np.all(err <= np.maximum(2.0 * np.spacing(np.abs(ref)), 2.0 * np.spacing(np.log(2.0))))
     assert out[-5] == 0.0
+
+
+def _cr(vals, fn):
+    """Correctly rounded reference values (mpmath, 60 digits)."""
+    import mpmath as mp
+    mp.mp.dps = 60
+    return np.array([float(fn(mp.mpf(float(v)))) for v in vals])
+
+
+def test_crmath_correctly_rounded():
+    """The accurate exp/log/log10/pow of the material parity path
+    (hyg_crmath.cuh) return the correctly rounded double on samples spanning
+    the material correlations' arguments (and beyond)."""
+    import mpmath as mp
+    rng = np.random.default_rng(7)
+    x = np.concatenate([rng.uniform(1e-6, 3.0, 3000), np.exp(rng.uniform(-30, 30, 3000)),
+                        1.0 + rng.uniform(-1e-3, 1e-3, 1000), [1.0, 2.0, 0.5, 10.0, 1e-300 * 1e10]])
+    y = np.concatenate([rng.choice([1.65, -0.39, 6.0, -0.83, 0.65, 5.0, -1.39, -1.83], x.size - 10),
+                        rng.uniform(-3, 3, 10)])
+    ex = rng.uniform(-700, 700, x.size)
+    lib = api.load_library()
+    p = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+    out = np.empty(4 * x.size)
+    assert lib.hyg_selftest_crmath(0, x.size, p(ex), p(y), p(out)) == 0
+    e = out[:x.size]
+    assert np.array_equal(e, _cr(ex, mp.exp)), np.flatnonzero(e != _cr(ex, mp.exp))[:5]
+    assert lib.hyg_selftest_crmath(0, x.size, p(np.ascontiguousarray(x)), p(y), p(out)) == 0
+    lg, l10, pw = out[x.size:2 * x.size], out[2 * x.size:3 * x.size], out[3 * x.size:]
+    assert np.array_equal(lg, _cr(x, mp.log))
+    assert np.array_equal(l10, _cr(x, mp.log10))
+    ref = np.array([float(mp.power(mp.mpf(float(a)), mp.mpf(float(b)))) for a, b in zip(x, y)])
+    finite = np.isfinite(ref) & (ref > 1e-300)
+    assert np.array_equal(pw[finite], ref[finite])
