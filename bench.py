@@ -82,6 +82,8 @@ def parse():
     p.add_argument("--halo", type=int, default=0, help="shard halo depth (0: config default)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-sharded", action="store_true",
+                   help="skip the strong-scaling block (cfg4 x-slabs, cfg3 zone blocks) of the default cfg1 line")
     a = p.parse_args()
     if not a.run_steps:
         a.run_steps = CONFIGS[a.config]["run_steps"]
@@ -357,7 +359,9 @@ def main():
     import torch.distributed as dist
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        import datetime
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                timeout=datetime.timedelta(seconds=600))
     from paper_1703_10119_b200 import api
 
     def barrier():
@@ -472,6 +476,19 @@ def main():
         except Exception:
             traffic = None
 
+    if R.shard is None:
+        ctx.close()
+    sharded = None
+    if args.config == "cfg1" and not args.no_sharded:
+        # the configs that communicate, measured on the same N GPUs (the driver's
+        # SCALE run then sees their strong scaling); failures are reported, not fatal
+        sharded = {}
+        for name in ("cfg4", "cfg3"):
+            try:
+                sharded[name] = measure_sharded(args, name, rank, world, local, barrier, max_over_ranks)
+            except Exception as e:          # noqa: BLE001 — reported in the line
+                sharded[name] = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -483,9 +500,9 @@ def main():
                              "flop_per_update": cfg["flop"], "bytes_per_update": cfg["bytes"],
                              "peak_source": peak_src, "kernel_node_updates_per_s": kernel_rate},
                 "clocks": clk, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu}
+        if sharded is not None:
+            line["sharded"] = sharded
         print(json.dumps(line), flush=True)
-    if R.shard is None:
-        ctx.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -221,6 +221,21 @@ int hyg_set_cells(hyg_ctx* ctx, int64_t cell0, int64_t count, const double* u_pr
 int hyg_get_zones(hyg_ctx* ctx, int32_t zone0, int32_t count, double* zone_u, double* zone_v);
 int hyg_set_zones(hyg_ctx* ctx, int32_t zone0, int32_t count, const double* zone_u,
                   const double* zone_v);
+/* Stream-ordered halo payloads (multi-GPU shards): pack the cells [cell0,
+ * cell0+count) of the four layers into buf[4][count] (device memory of the
+ * context's GPU), or unpack buf into them; zones into/from buf[2][count]
+ * (zone_u then zone_v).  Enqueued on the context's stream with no host
+ * synchronisation: a caller that hands the context its communication stream
+ * (hyg_set_stream) orders NCCL sends/receives of buf behind and ahead of them
+ * by stream order alone.  One launch per call. */
+int hyg_pack_cells(hyg_ctx* ctx, int64_t cell0, int64_t count, double* buf);
+int hyg_unpack_cells(hyg_ctx* ctx, int64_t cell0, int64_t count, const double* buf);
+int hyg_pack_zones(hyg_ctx* ctx, int32_t zone0, int32_t count, double* buf);
+int hyg_unpack_zones(hyg_ctx* ctx, int32_t zone0, int32_t count, const double* buf);
+/* Launch everything on `stream` (a cudaStream_t of the context's device;
+ * NULL: the context's own stream), ordered after the work already issued. */
+int hyg_set_stream(hyg_ctx* ctx, void* stream);
+
 /* Restricts the divergence guard and the implicit starting step's
  * fixed-point residual to the cells [cell0, cell1) and zones [zone0, zone1)
  * a shard owns (its halo copies are excluded), and reduces the residual

@@ -122,6 +122,11 @@ PROTOTYPES = {
     "hyg_set_cells": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, dp, dp, dp, dp]),
     "hyg_get_zones": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, dp, dp]),
     "hyg_set_zones": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, dp, dp]),
+    "hyg_pack_cells": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]),
+    "hyg_unpack_cells": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]),
+    "hyg_pack_zones": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "hyg_unpack_zones": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "hyg_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "hyg_set_owned": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "hyg_snapshot": (C.c_int, [C.c_void_p]),
     "hyg_restore": (C.c_int, [C.c_void_p]),

@@ -351,33 +351,53 @@ class Context:
 
     def get_cells_into(self, cell0: int, count: int, out) -> None:
         """Copy cells [cell0, cell0+count) of the four layers into `out`, a
-        contiguous float64 torch tensor of shape (4, count) on any device (the
-        halo exchange of shard.py passes NCCL buffers: device to device)."""
+        contiguous float64 torch tensor of shape (4, count).  A CUDA `out` is
+        filled by one pack kernel on the context's stream with no host
+        synchronisation (hyg_pack_cells; hand the context the stream the
+        consumer runs on, set_stream); a host `out` by the synchronous copy."""
         assert out.is_contiguous() and tuple(out.shape) == (4, count) and out.element_size() == 8
         base, step = out.data_ptr(), count * 8
+        if out.is_cuda:
+            _check(self.lib.hyg_pack_cells(self.h, cell0, count, C.c_void_p(base)), None, "hyg_pack_cells")
+            return
         _check(self.lib.hyg_get_cells(self.h, cell0, count, *[_addr(base + i * step) for i in range(4)]),
                None, "hyg_get_cells")
 
     def set_cells_from(self, cell0: int, src) -> None:
-        """Inverse of get_cells_into; the caller orders `src` (e.g. synchronises
-        the stream an NCCL receive completed on) before the call."""
+        """Inverse of get_cells_into (CUDA `src`: one unpack kernel, stream-ordered)."""
         assert src.is_contiguous() and src.dim() == 2 and src.shape[0] == 4 and src.element_size() == 8
         count, base = int(src.shape[1]), src.data_ptr()
+        if src.is_cuda:
+            _check(self.lib.hyg_unpack_cells(self.h, cell0, count, C.c_void_p(base)), None, "hyg_unpack_cells")
+            return
         _check(self.lib.hyg_set_cells(self.h, cell0, count, *[_addr(base + i * count * 8) for i in range(4)]),
                None, "hyg_set_cells")
 
     def get_zones_into(self, zone0: int, count: int, out) -> None:
-        """Zones [zone0, zone0+count) into `out`: contiguous float64 (2, count), any device."""
+        """Zones [zone0, zone0+count) into `out`: contiguous float64 (2, count)
+        (CUDA: stream-ordered device copies, no host synchronisation)."""
         assert out.is_contiguous() and tuple(out.shape) == (2, count) and out.element_size() == 8
         base = out.data_ptr()
+        if out.is_cuda:
+            _check(self.lib.hyg_pack_zones(self.h, zone0, count, C.c_void_p(base)), None, "hyg_pack_zones")
+            return
         _check(self.lib.hyg_get_zones(self.h, zone0, count, _addr(base), _addr(base + count * 8)),
                None, "hyg_get_zones")
 
     def set_zones_from(self, zone0: int, src) -> None:
         assert src.is_contiguous() and src.dim() == 2 and src.shape[0] == 2 and src.element_size() == 8
         count, base = int(src.shape[1]), src.data_ptr()
+        if src.is_cuda:
+            _check(self.lib.hyg_unpack_zones(self.h, zone0, count, C.c_void_p(base)), None, "hyg_unpack_zones")
+            return
         _check(self.lib.hyg_set_zones(self.h, zone0, count, _addr(base), _addr(base + count * 8)),
                None, "hyg_set_zones")
+
+    def set_stream(self, stream=None) -> None:
+        """Run on `stream` (a torch.cuda.Stream or a raw cudaStream_t; None: the
+        context's own), ordered after the work issued so far (hyg_set_stream)."""
+        ptr = getattr(stream, "cuda_stream", stream)
+        _check(self.lib.hyg_set_stream(self.h, C.c_void_p(ptr) if ptr else None), None, "hyg_set_stream")
 
     def get_zones(self, zone0: int, count: int):
         zu, zv = np.empty(count), np.empty(count)

@@ -125,7 +125,8 @@ void clear_status(hyg_status* st) {
 
 struct hyg_ctx {
     int device = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;       // the stream every launch and copy goes to
+    cudaStream_t own_stream = nullptr;   // the context's own (hyg_set_stream(NULL) restores it)
     // model
     int n_walls = 0, n = 0;
     double dx = 0;
@@ -218,6 +219,7 @@ struct hyg_ctx {
     int ring_pipe_B = 0;             // K5 (k_ring_pipe.cuh): zones per block, 0 if not applicable
     int ring_kernel = 0;             // HYG_TUNE_RING_KERNEL: 0 auto (K5, else K4r), 1 K4r, 2 K4
     bool mat_fast = false;           // HYG_TUNE_MATERIAL_FAST: evaluate_fast + reciprocal rows
+    bool owned_partial = false;      // hyg_set_owned narrowed the guard to a shard's range
     double* d_ring_zp = nullptr;     // K4r per-zone parameter blocks [zones][kRingZP]
     bool ring_reg_small = false;     // every zone: <= 6 wall links, <= 2 ring peers
     int rad_groups = 0, rad_terms = 0;
@@ -283,6 +285,23 @@ void drain_pending(hyg_ctx* c) {
         cudaEventDestroy(p.e1);
     }
     c->pending.clear();
+}
+
+// halo payloads: cells [c0, c0+count) of the four layers <-> buf[4][count]
+struct Layers4 { double* p[4]; };
+__global__ void k_pack_cells(Layers4 L, int64_t c0, int64_t count, double* buf) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < 4 * count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int f = static_cast<int>(i / count);
+        buf[i] = L.p[f][c0 + (i - f * count)];
+    }
+}
+__global__ void k_unpack_cells(Layers4 L, int64_t c0, int64_t count, const double* buf) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < 4 * count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int f = static_cast<int>(i / count);
+        L.p[f][c0 + (i - f * count)] = buf[i];
+    }
 }
 
 // ---- per-device launch attributes ----------------------------------------------
@@ -1182,7 +1201,7 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool
         c->zcur = (z0 + flag - 1) & 1;
         c->t = times[k0];
         c->layer += k0;
-        if (reg) return advance_ring(c, nsteps - done - k0, dt, status, false);
+        if (reg && !c->owned_partial) return advance_ring(c, nsteps - done - k0, dt, status, false);
         return advance_general(c, nsteps - done - k0, dt, status);
     }
     return HYG_OK;
@@ -1541,6 +1560,7 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
         return HYG_ECUDA;
     };
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
+    c->own_stream = c->stream;
     const size_t cells = static_cast<size_t>(c->cells());
     for (int b = 0; b < 2; ++b)
         for (int i = 0; i < 4; ++i) {
@@ -1649,6 +1669,7 @@ void hyg_destroy(hyg_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     drain_pending(c);
     for (int b = 0; b < 2; ++b) {
         for (int i = 0; i < 4; ++i) {
@@ -1687,7 +1708,7 @@ void hyg_destroy(hyg_ctx* c) {
         cudaFree(q);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
-    if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
 }
 
@@ -1801,8 +1822,11 @@ int hyg_set_owned(hyg_ctx* c, int64_t cell0, int64_t cell1, int32_t zone0, int32
     // wall) stays: its fast guard only decides whether to replay on the
     // per-step path, which then applies the owned range exactly.
     if (cell0 > 0 || cell1 < c->cells()) c->fused = c->nl_fused = false;
-    // K4's guard and zone ownership are whole-CTA; shards take the exact per-step path
-    if (cell0 > 0 || cell1 < c->cells() || zone0 > 0 || zone1 < static_cast<int>(c->zones.size())) c->ring = false;
+    // the zone-ring kernels (K5/K4r/K4) guard whole blocks, halo copies
+    // included: a shard keeps them (every owned value is exact), and a flagged
+    // launch is replayed on the per-step path, whose guard honours the owned
+    // ranges (advance_ring)
+    c->owned_partial = cell0 > 0 || cell1 < c->cells() || zone0 > 0 || zone1 < static_cast<int>(c->zones.size());
     return HYG_OK;
 }
 
@@ -2239,6 +2263,72 @@ int hyg_kernel_stats(hyg_ctx* c, int32_t i, const char** name, int64_t* launches
     if (updates) *updates = s.updates;
     return HYG_OK;
 }
+int hyg_set_stream(hyg_ctx* c, void* stream) {
+    if (!c) return HYG_EINVAL;
+    cudaSetDevice(c->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    if (s != c->stream) {
+        // order the new stream after everything issued so far on the old one
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return HYG_ECUDA;
+        cudaEventRecord(e, c->stream);
+        cudaStreamWaitEvent(s, e, 0);
+        cudaEventDestroy(e);
+        c->stream = s;
+    }
+    return HYG_OK;
+}
+
+int hyg_pack_cells(hyg_ctx* c, int64_t cell0, int64_t count, double* buf) {
+    if (!c || cell0 < 0 || count < 0 || cell0 + count > c->cells() || (count > 0 && !buf)) return HYG_EINVAL;
+    if (c->precision != HYG_F64) return HYG_ENOTSUP;
+    if (count == 0) return HYG_OK;
+    cudaSetDevice(c->device);
+    Layers4 L{{c->s64[c->cur][0], c->s64[c->cur][1], c->s64[c->cur][2], c->s64[c->cur][3]}};
+    const int grid = static_cast<int>(std::min<int64_t>((4 * count + 255) / 256, 4 * sm_count(c->device)));
+    {
+        LaunchScope ls(c, "pack_cells", 0.0);
+        k_pack_cells<<<grid, 256, 0, c->stream>>>(L, cell0, count, buf);
+    }
+    return cudaGetLastError() == cudaSuccess ? HYG_OK : HYG_ECUDA;
+}
+
+int hyg_unpack_cells(hyg_ctx* c, int64_t cell0, int64_t count, const double* buf) {
+    if (!c || cell0 < 0 || count < 0 || cell0 + count > c->cells() || (count > 0 && !buf)) return HYG_EINVAL;
+    if (c->precision != HYG_F64) return HYG_ENOTSUP;
+    if (count == 0) return HYG_OK;
+    cudaSetDevice(c->device);
+    Layers4 L{{c->s64[c->cur][0], c->s64[c->cur][1], c->s64[c->cur][2], c->s64[c->cur][3]}};
+    const int grid = static_cast<int>(std::min<int64_t>((4 * count + 255) / 256, 4 * sm_count(c->device)));
+    {
+        LaunchScope ls(c, "unpack_cells", 0.0);
+        k_unpack_cells<<<grid, 256, 0, c->stream>>>(L, cell0, count, buf);
+    }
+    return cudaGetLastError() == cudaSuccess ? HYG_OK : HYG_ECUDA;
+}
+
+int hyg_pack_zones(hyg_ctx* c, int32_t z0, int32_t count, double* buf) {
+    if (!c || z0 < 0 || count < 0 || z0 + count > static_cast<int>(c->zones.size()) || (count > 0 && !buf))
+        return HYG_EINVAL;
+    if (count == 0) return HYG_OK;
+    cudaSetDevice(c->device);
+    if (cudaMemcpyAsync(buf, c->zu[c->zcur] + z0, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream) ||
+        cudaMemcpyAsync(buf + count, c->zv[c->zcur] + z0, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream))
+        return HYG_ECUDA;
+    return HYG_OK;
+}
+
+int hyg_unpack_zones(hyg_ctx* c, int32_t z0, int32_t count, const double* buf) {
+    if (!c || z0 < 0 || count < 0 || z0 + count > static_cast<int>(c->zones.size()) || (count > 0 && !buf))
+        return HYG_EINVAL;
+    if (count == 0) return HYG_OK;
+    cudaSetDevice(c->device);
+    if (cudaMemcpyAsync(c->zu[c->zcur] + z0, buf, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream) ||
+        cudaMemcpyAsync(c->zv[c->zcur] + z0, buf + count, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream))
+        return HYG_ECUDA;
+    return HYG_OK;
+}
+
 int hyg_set_tuning(hyg_ctx* c, int32_t knob, int64_t value) {
     if (!c || value < 0) return HYG_EINVAL;
     switch (knob) {

@@ -55,11 +55,13 @@ class Comm:
     """Point-to-point + reductions over a torch.distributed group.
 
     On an NCCL group (one process per GPU, bench.py at N > 1) halo payloads
-    stay on the device: the engine copies its boundary cells straight into a
-    CUDA buffer (Context.get_cells_into, device to device), NCCL moves it over
-    NVLink, and the receiver copies it into its halo (set_cells_from) — no
-    host staging.  On a gloo group (CPU tests, or ranks sharing one GPU) the
-    same payloads travel as host tensors."""
+    stay on the device and in stream order: the engine runs on the current
+    torch stream (Context.set_stream), packs its boundary cells into one CUDA
+    buffer with one kernel (Context.get_cells_into -> hyg_pack_cells), NCCL
+    moves it over NVLink behind that kernel, and the receiver's unpack kernel
+    runs behind the receive — no host copies and no stream synchronisation on
+    the exchange path.  On a gloo group (CPU tests, or ranks sharing one GPU)
+    the same payloads travel as host tensors."""
 
     def __init__(self, group=None):
         import torch
@@ -89,9 +91,7 @@ class Comm:
         for peer, arr in sends.items():
             reqs.append(self.dist.isend(self.tensor(arr), dst=self._global(peer), group=self.group))
         for r in reqs:
-            r.wait()
-        if self.on_device:
-            torch.cuda.current_stream(self.device).synchronize()   # engines run on their own stream
+            r.wait()          # NCCL: the current stream waits for the transfers (no host block)
         return out
 
     def _global(self, r):
@@ -108,6 +108,14 @@ class Comm:
 
     def allreduce_min(self, x: float) -> float:
         return self._reduce(x, self.dist.ReduceOp.MIN)
+
+
+def _attach_stream(engine, comm):
+    """On a device comm, run the engine on the current torch stream, so its
+    pack/unpack kernels and the NCCL transfers are ordered by the stream."""
+    if comm.on_device and hasattr(engine, "set_stream"):
+        import torch
+        engine.set_stream(torch.cuda.current_stream(comm.device))
 
 
 def _get_block(engine, comm, cell0: int, count: int):
@@ -130,6 +138,51 @@ def _set_block(engine, cell0: int, block):
         return
     a = block.cpu().numpy() if isinstance(block, torch.Tensor) else block
     engine.set_cells(cell0, dict(zip(FIELDS, a)))
+
+
+class _Timer:
+    """Accumulated time of the exchange and compute phases of a shard (CUDA
+    events on the current stream on a device comm, host clock otherwise)."""
+
+    def __init__(self, comm):
+        self.on_device = comm.on_device
+        self.ms = {"exchange": 0.0, "compute": 0.0}
+        self.intervals = 0
+        self._pending = []
+
+    def phase(self, name):
+        timer = self
+
+        class _P:
+            def __enter__(self_):
+                if timer.on_device:
+                    import torch
+                    self_.e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    self_.e[0].record()
+                else:
+                    import time
+                    self_.t0 = time.perf_counter()
+
+            def __exit__(self_, *exc):
+                if timer.on_device:
+                    self_.e[1].record()
+                    timer._pending.append((name, self_.e))
+                else:
+                    import time
+                    timer.ms[name] += 1e3 * (time.perf_counter() - self_.t0)
+        return _P()
+
+    def totals(self) -> dict:
+        for name, (a, b) in self._pending:
+            b.synchronize()
+            self.ms[name] += a.elapsed_time(b)
+        self._pending.clear()
+        return dict(self.ms, intervals=self.intervals)
+
+    def reset(self):
+        self.totals()
+        self.ms = {"exchange": 0.0, "compute": 0.0}
+        self.intervals = 0
 
 
 def _advance_guarded(engine, k, comm):
@@ -166,15 +219,20 @@ class LongDomainShard:
                       dt=model.dt, divergence_norm=model.divergence_norm, coeff_kind=model.coeff_kind,
                       coeff_params=model.coeff_params, device=model.device)
         self.engine = engine_factory(local)
+        _attach_stream(self.engine, comm)
         self.engine.set_state(**{f: init[f][s.a:s.b] for f in FIELDS})
         self.engine.set_owned(s.lo - s.a, s.hi - s.a)
+        self.timer = _Timer(comm)
 
     def advance(self, nsteps: int):
         done = 0
         while done < nsteps:
             k = min(self.halo, nsteps - done)
-            _advance_guarded(self.engine, k, self.comm)
-            self.refresh()
+            with self.timer.phase("compute"):
+                _advance_guarded(self.engine, k, self.comm)
+            with self.timer.phase("exchange"):
+                self.refresh()
+            self.timer.intervals += 1
             done += k
 
     def refresh(self):
@@ -233,6 +291,7 @@ class ZoneRingShard:
                       outdoor_v=model.outdoor_v, dt=model.dt, divergence_norm=model.divergence_norm,
                       eta_factor=model.eta_factor, max_subiters=model.max_subiters, device=model.device)
         self.engine = engine_factory(local)
+        _attach_stream(self.engine, comm)
         cells = (gw[:, None] * n + np.arange(n)[None, :]).reshape(-1)
         st = {f: init[f][cells] for f in FIELDS}
         st["zone_u"] = np.asarray(init["zone_u"])[self.gz]
@@ -242,6 +301,7 @@ class ZoneRingShard:
         own = self.hi - self.lo
         self.engine.set_owned(H * W * n, (H + own) * W * n, H, H + own,
                               reduce=comm.allreduce_max if P > 1 else None)
+        self.timer = _Timer(comm)
 
     def bootstrap(self, kind="implicit"):
         st = self.engine.bootstrap(kind)
@@ -255,21 +315,27 @@ class ZoneRingShard:
         K = self.H if self.H else nsteps
         while done < nsteps:
             k = min(K, nsteps - done)
-            _advance_guarded(self.engine, k, self.comm)
+            with self.timer.phase("compute"):
+                _advance_guarded(self.engine, k, self.comm)
             if self.H:
-                self.refresh()
+                with self.timer.phase("exchange"):
+                    self.refresh()
+            self.timer.intervals += 1
             done += k
 
     def _zone_block(self, i0, count):
         """Zones [i0, i0+count) with their walls as one flat payload:
-        4 layers x cells, then zone_u, zone_v."""
+        4 layers x cells, then zone_u, zone_v (on a device comm: one buffer,
+        filled by one pack kernel and two stream-ordered copies)."""
         n, W = self.engine_model_n, self.W
-        cells = _get_block(self.engine, self.comm, i0 * W * n, count * W * n)
+        m = count * W * n
         if self.comm.on_device and hasattr(self.engine, "get_zones_into"):
             import torch
-            z = torch.empty((2, count), dtype=torch.float64, device=self.comm.device)
-            self.engine.get_zones_into(i0, count, z)
-            return torch.cat([cells.reshape(-1), z.reshape(-1)])
+            buf = torch.empty(4 * m + 2 * count, dtype=torch.float64, device=self.comm.device)
+            self.engine.get_cells_into(i0 * W * n, m, buf[:4 * m].view(4, m))
+            self.engine.get_zones_into(i0, count, buf[4 * m:].view(2, count))
+            return buf
+        cells = _get_block(self.engine, self.comm, i0 * W * n, m)
         zu, zv = self.engine.get_zones(i0, count)
         return np.concatenate([np.asarray(cells).reshape(-1), zu, zv])
 

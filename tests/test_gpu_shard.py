@@ -128,10 +128,12 @@ class _LoopbackComm:
         return self._reduce(x, min)
 
 
-@pytest.mark.parametrize("case", ["long", "ring"])
+@pytest.mark.parametrize("case", ["long", "ring", "ring128"])
 def test_device_payload_exchange_bitwise(case):
-    """Halo payloads as CUDA tensors (the NCCL path of shard.Comm): shards
-    in two threads equal the undivided run bit for bit."""
+    """Halo payloads as CUDA tensors (the NCCL path of shard.Comm: one pack
+    kernel, stream-ordered, no host copies): shards in two threads equal the
+    undivided run bit for bit.  ring128: 128-node walls, so each shard marches
+    its zone block (a chain with halo zones) through the zone-ring kernel K5."""
     import threading
     import torch
     from paper_1703_10119_b200 import Context, shard, workloads
@@ -143,7 +145,7 @@ def test_device_payload_exchange_bitwise(case):
         w = workloads.long_domain(n_nodes=n, nsteps=steps)
         model, init = w.model, w.init
     else:
-        Z, W, n, steps = 16, 6, 32, 120
+        Z, W, n, steps = (16, 6, 32, 120) if case == "ring" else (30, 6, 128, 100)
         w = workloads.zone_ring(n_zones=Z, walls_per_zone=W, n_nodes=n, nsteps=steps)
         rng = np.random.default_rng(5)
         init = {f: w.init[f] + 1e-3 * rng.standard_normal(w.init[f].size) for f in FIELDS}
@@ -158,9 +160,14 @@ def test_device_payload_exchange_bitwise(case):
                 sh = shard.LongDomainShard(model, init, comm, Context, halo=24)
                 sh.advance(steps)
             else:
-                sh = shard.ZoneRingShard(model, init, comm, Context, walls_per_zone=6, halo=4)
+                sh = shard.ZoneRingShard(model, init, comm, Context, walls_per_zone=6, halo=4 if case == "ring" else 12)
+                if case == "ring128":
+                    sh.engine.profiling(True)
                 sh.bootstrap("implicit")
                 sh.advance(steps - 1)
+                if case == "ring128":
+                    sh.engine.synchronize()
+                    assert any(x["name"] == "ring_pipe" for x in sh.engine.kernel_stats())
             res[rank] = (sh, sh.owned_state())
         except Exception:
             errs.append(traceback.format_exc())
