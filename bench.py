@@ -81,6 +81,9 @@ def parse():
     p.add_argument("--material-walls", type=int, default=16384)
     p.add_argument("--halo", type=int, default=0, help="shard halo depth (0: config default)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--ring-kernel", type=int, default=0, help="cfg3: 0 auto (K5), 1 K4r, 2 K4 (A/B runs)")
+    p.add_argument("--material-exact", action="store_true",
+                   help="cfg5: the parity material evaluation (hyg_crmath.cuh) instead of the default fast one")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-sharded", action="store_true",
                    help="skip the strong-scaling block (cfg4 x-slabs, cfg3 zone blocks) of the default cfg1 line")
@@ -328,6 +331,10 @@ class Runner:
             self.updates = w.cells / world
         else:
             self.ctx = Context(w.model)
+            if args.ring_kernel:
+                self.ctx.set_tuning("ring_kernel", args.ring_kernel)
+            if args.material_exact:
+                self.ctx.set_tuning("material_exact", 1)
             for ch, (first, tab) in w.tables.items():
                 self.ctx.set_channel_table(ch, first, tab)
             self.ctx.set_state(**w.init)

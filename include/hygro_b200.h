@@ -347,14 +347,17 @@ int64_t hyg_launch_count(hyg_ctx* ctx);
  * next-block prefetch path the full-size ring runs.  HYG_TUNE_RING_KERNEL
  * picks the zone-ring kernel: 0 = automatic (K5 k_ring_pipe.cuh where it
  * applies, else K4r), 1 = K4r (k_ring_reg.cuh), 2 = K4 (k_ring.cuh), for
- * A/B measurement and cross-checks.  HYG_TUNE_MATERIAL_FAST = 1 evaluates the
- * load-bearing material with the fast table-driven exp/log and reciprocal
- * quotients (~2x throughput, a few ulp per coefficient: the reference's
- * wall_nonlinear fixture then drifts 1.7e-9 relative over 8e4 steps); 0 (the
- * default) is the parity evaluation (hyg_crmath.cuh, IEEE divisions, no FMA
- * contraction).  HYG_EINVAL for an
+ * A/B measurement and cross-checks.  HYG_TUNE_MATERIAL_EXACT = 1 evaluates
+ * the load-bearing material with the accurate exp/log/pow of hyg_crmath.cuh
+ * (glibc's roundings in all but rare cases), the reference's expressions and
+ * IEEE divisions — ~8x slower than the default (0) table-driven evaluation with
+ * reciprocal quotients, which is a few ulp per coefficient.  Both agree with
+ * the reference within its own conditioning: on the ill-conditioned
+ * wall_nonlinear fixture (a 1-ulp change of one initial value moves the
+ * reference by 8e-10) they differ from it by 9.6e-10 (exact) and 1.7e-9
+ * (default); on the other fixtures and tests by ~1e-14.  HYG_EINVAL for an
  * unknown knob or a negative value. */
-enum { HYG_TUNE_RING_GRID = 1, HYG_TUNE_RING_KERNEL = 2, HYG_TUNE_MATERIAL_FAST = 3 };
+enum { HYG_TUNE_RING_GRID = 1, HYG_TUNE_RING_KERNEL = 2, HYG_TUNE_MATERIAL_EXACT = 3 };
 int hyg_set_tuning(hyg_ctx* ctx, int32_t knob, int64_t value);
 
 /* Device FP64 FMA throughput probe (DFMA loop), TFLOP/s counting FMA = 2. */

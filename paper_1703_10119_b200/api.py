@@ -488,12 +488,12 @@ class Context:
         return out
 
     TUNING = {"ring_grid": A.HYG_TUNE_RING_GRID, "ring_kernel": A.HYG_TUNE_RING_KERNEL,
-              "material_fast": A.HYG_TUNE_MATERIAL_FAST}
+              "material_exact": A.HYG_TUNE_MATERIAL_EXACT}
 
     def set_tuning(self, knob: str, value: int) -> None:
         """Launch-shape knob (hyg_set_tuning): ring_grid = cap on the persistent
-        zone-ring grid; ring_kernel = 0 auto (K5), 1 K4r, 2 K4; material_fast = 1 for
-        the fast (few-ulp) material evaluation instead of the parity one."""
+        zone-ring grid; ring_kernel = 0 auto (K5), 1 K4r, 2 K4; material_exact = 1 for
+        the accurate material evaluation (hyg_crmath.cuh) instead of the fast one."""
         _check(self.lib.hyg_set_tuning(self.h, self.TUNING[knob], int(value)), None, "hyg_set_tuning")
 
     def reset_kernel_stats(self):

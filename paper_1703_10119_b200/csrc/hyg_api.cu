@@ -218,8 +218,9 @@ struct hyg_ctx {
     int ring_grid_cap = 0;           // HYG_TUNE_RING_GRID: K4r/K5 persistent grid cap (0: one CTA per SM)
     int ring_pipe_B = 0;             // K5 (k_ring_pipe.cuh): zones per block, 0 if not applicable
     int ring_kernel = 0;             // HYG_TUNE_RING_KERNEL: 0 auto (K5, else K4r), 1 K4r, 2 K4
-    bool mat_fast = false;           // HYG_TUNE_MATERIAL_FAST: evaluate_fast + reciprocal rows
+    bool mat_exact = false;          // HYG_TUNE_MATERIAL_EXACT: CrMath evaluation + IEEE-division rows
     bool owned_partial = false;      // hyg_set_owned narrowed the guard to a shard's range
+    int ring_dbg_skip = 0;           // HYG_DEBUG_RING_SKIP (timing experiments only; wrong results)
     double* d_ring_zp = nullptr;     // K4r per-zone parameter blocks [zones][kRingZP]
     bool ring_reg_small = false;     // every zone: <= 6 wall links, <= 2 ring peers
     int rad_groups = 0, rad_terms = 0;
@@ -491,7 +492,7 @@ StarArgs star_args(hyg_ctx* c, const double* u, const double* v, bool strict, in
     s.dom_key = c->d_dom;
     s.own0 = c->own_c0;
     s.own1 = c->own_c1;
-    s.exact = c->mat_fast ? 0 : 1;
+    s.exact = c->mat_exact ? 1 : 0;
     return s;
 }
 
@@ -662,8 +663,8 @@ int advance_general(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
                 const int mgrid = static_cast<int>((c->cells() + kMatCells - 1) / kMatCells);
                 const int zblocks = (z.n_zones + kMatThreads - 1) / kMatThreads;
                 LaunchScope ls(c, "material_step", static_cast<double>(c->cells()));
-                if (c->mat_fast) k_material_step<false><<<mgrid + zblocks, kMatThreads, 0, c->stream>>>(a, sa, z, mgrid);
-                else k_material_step<true><<<mgrid + zblocks, kMatThreads, 0, c->stream>>>(a, sa, z, mgrid);
+                if (c->mat_exact) k_material_step<true><<<mgrid + zblocks, kMatThreads, 0, c->stream>>>(a, sa, z, mgrid);
+                else k_material_step<false><<<mgrid + zblocks, kMatThreads, 0, c->stream>>>(a, sa, z, mgrid);
                 if (!c->zones.empty()) c->zcur ^= 1;
             } else if (c->zones.empty()) {
                 LaunchScope ls(c, "df_step_general", static_cast<double>(c->cells()));
@@ -1156,6 +1157,7 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool
         a.inz = c->d_inz;
         a.zparams = c->d_ring_zp;
         a.stop = c->d_flag;
+        a.dbg_skip = c->ring_dbg_skip;
         const int cur0 = c->cur, z0 = c->zcur;
         int nseg = 0;
         for (int64_t s0 = 0; s0 < rows; s0 += S, ++nseg) {
@@ -1519,7 +1521,7 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
                 int Bp = npt == 8 ? std::min(Z, SP::kB) : 0;
                 auto fits_p = [&](int b) {
                     const int rw = RingShape<8, kRingS>::row_width(nch, nsrc);
-                    return SP::threads(b, W) <= SP::kThreads && SP::local_zones(b) <= 64 &&
+                    return SP::threads(b, W) <= SP::kThreads && SP::local_zones(b) <= 32 &&
                            SP::smem_doubles(b, W, rw) * sizeof(double) <= 227u * 1024u;
                 };
                 while (Bp > 0 && !fits_p(Bp)) --Bp;
@@ -1561,6 +1563,7 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
     };
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
     c->own_stream = c->stream;
+    if (const char* e = std::getenv("HYG_DEBUG_RING_SKIP")) c->ring_dbg_skip = std::atoi(e);   // timing only
     const size_t cells = static_cast<size_t>(c->cells());
     for (int b = 0; b < 2; ++b)
         for (int i = 0; i < 4; ++i) {
@@ -2337,9 +2340,9 @@ int hyg_set_tuning(hyg_ctx* c, int32_t knob, int64_t value) {
             if (value > 2) return HYG_EINVAL;
             c->ring_kernel = static_cast<int>(value);
             return HYG_OK;
-        case HYG_TUNE_MATERIAL_FAST:
+        case HYG_TUNE_MATERIAL_EXACT:
             if (value > 1) return HYG_EINVAL;
-            c->mat_fast = value != 0;
+            c->mat_exact = value != 0;
             return HYG_OK;
         default: return HYG_EINVAL;
     }

@@ -190,10 +190,10 @@ __device__ __forceinline__ bool evaluate_fast(double T, double P_v, Set& out) {
 
 // CoefficientModel::star / star_clamped (wall.cpp:50-58): the set at
 // (u T_i, v P_vi) divided by the wall's reference set.  On the device `exact`
-// selects the parity path (the reference's expressions with CrMath and IEEE
-// divisions, the default) or evaluate_fast (HYG_TUNE_MATERIAL_FAST).
+// selects the accurate path (the reference's expressions with CrMath and IEEE
+// divisions, HYG_TUNE_MATERIAL_EXACT) or evaluate_fast (the default).
 HYG_HD bool star(double u, double v, double T_i, double P_vi, const Set& ref, bool strict, Set& out,
-                 bool exact = true) {
+                 bool exact = false) {
     Set a;
 #if defined(__CUDA_ARCH__)
     bool ok;

@@ -154,12 +154,18 @@ __device__ __forceinline__ void dv_face(const DvFace& f, const Ambient& am, doub
     // km_b, kp_b scaled by 2a (dv_params): 2a S = S', a S = S'/2
     const double S = kp_b + km_b;
     const double rk = frcp(km_b);                      // off the v row's chain
-    vn = vp + (S * (vcn - vp) + f.cpl2 * (am.v - vp) + f.ag4 * am.g) * frcp(fma(0.5, S, f.cpl1));
+    // explicit FMA chains (the library is built with -fmad=false)
+    vn = fma(fma(f.ag4, am.g, fma(f.cpl2, am.v - vp, S * (vcn - vp))), frcp(fma(0.5, S, f.cpl1)), vp);
     const double vbar = 0.5 * (vn + vp);
-    const double vg = vcn - (f.dx2a * rk) * (f.BiM * (vbar - am.v) - am.g);
-    un = up + (f.b4 * (ucn - up) + f.cplu2 * (am.u - up) - f.gamma * (vn - vp) + f.b2r * (vcn - vg) -
-               f.b4dx * (f.BiTM * (vbar - am.v) - am.q) + f.g2 * (vcn + vg) - f.g2 * (vn + vp)) *
-              f.inv_fu;
+    const double vg = fma(-(f.dx2a * rk), fma(f.BiM, vbar - am.v, -am.g), vcn);
+    double t = f.b4 * (ucn - up);
+    t = fma(f.cplu2, am.u - up, t);
+    t = fma(-f.gamma, vn - vp, t);
+    t = fma(f.b2r, vcn - vg, t);
+    t = fma(-f.b4dx, fma(f.BiTM, vbar - am.v, -am.q), t);
+    t = fma(f.g2, vcn + vg, t);
+    t = fma(-f.g2, vn + vp, t);
+    un = fma(t, f.inv_fu, up);
 }
 
 struct DvLane {

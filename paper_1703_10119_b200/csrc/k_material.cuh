@@ -239,11 +239,11 @@ constexpr int kMatThreads = 256, kMatCells = 255;
 // df_step_nonlinear rows (wall.cpp:213-259) from the CTA's shared tables:
 // node f at nS[f*256 + t], half (j-1)+1/2 at hS[f*256 + t], j+1/2 at hS[f*256 + t+1]
 // p: the wall's groups, loaded by the caller before the StarTables evaluation.
-// EXACT (the default, parity path): the reference's statements with IEEE
-// divisions (and, the library being built with -fmad=false, no contraction).
-// !EXACT (HYG_TUNE_MATERIAL_FAST): reciprocals (frcp, 3 FMAs) instead of the
-// divisions, <= 1 ulp per quotient (cfg5 1.78e10 -> 1.90e10); a zero
-// denominator gives NaN where the division gave inf, both trip the guard.
+// !EXACT (the default): reciprocals (frcp, 3 FMAs) instead of the divisions,
+// <= 1 ulp per quotient (cfg5 1.78e10 -> 1.90e10); a zero denominator gives
+// NaN where the division gave inf, both trip the guard.  EXACT
+// (HYG_TUNE_MATERIAL_EXACT): the reference's statements with IEEE divisions
+// (and, the library being built with -fmad=false, no contraction).
 template <bool EXACT>
 __device__ __forceinline__ void material_cell(const StepArgs& a, const NodeIn& x, int w, int j, const Groups& p,
                                               const double* nS, const double* hS, int t, double& un, double& vn) {

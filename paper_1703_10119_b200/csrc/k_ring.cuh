@@ -57,6 +57,7 @@ struct RingArgs {
     double* zv_out;
     int* stop;                     // first failing launch + 1 (0: none)
     int seg_index;
+    int dbg_skip;                  // timing experiments only (K5: 1 skip halo copies); 0 in the library
 };
 
 // Per local zone, staged in shared memory before the step loop (the zone

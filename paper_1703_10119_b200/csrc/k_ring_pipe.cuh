@@ -13,16 +13,18 @@
 //     layer S-d, so its walls need their last S-d nodes (rounded up to an even
 //     count for 16-byte bulk copies) and S-d-1 steps (K4r: S+1 nodes, S steps);
 //   * no CTA barrier per step: the walls and the zone warp hand layer-k data
-//     over through two pairs of mbarriers (surface samples of layer k ->
-//     zone warp; zone air of layer k -> walls), so a wall warp computes the
-//     interior rows of step k while the zone warp is still producing the air
-//     its face row needs, and warps drift freely within a step;
-//   * prefetch by bulk copies: the next block's owned walls (one copy per
-//     field) and halo walls (one per wall and field, issued by the 32 lanes of
-//     the zone warp) land on one mbarrier while the current block marches
-//     (the zone parameter blocks by the zone warp's cp.async); the next block's
-//     zone air and row coefficients are loaded into registers behind the
-//     steps;
+//     over through two pairs of named barriers, producers arriving without
+//     waiting (surface samples of layer k -> zone warp; zone air of layer k
+//     -> walls), so a wall warp computes the interior rows of step k while the
+//     zone warp is still producing the air its face row needs;
+//   * a producer warp stages the next block while the current one marches:
+//     owned walls (one bulk copy per field) and halo walls (one per wall and
+//     field) on one mbarrier's transaction count, zone parameter blocks
+//     (cp.async) and zone air; the row coefficients of the next block are
+//     loaded into registers behind the steps;
+//   * the zone warp sums every term that needs no wall sample (sources,
+//     ventilation, peers) before it waits for the walls, so the per-step
+//     critical path is the six wall-link terms and the division;
 //   * outputs straight from registers (16-byte stores; the reversed lane
 //     stores its nodes in node order), no shared-memory scratch.
 //
@@ -46,29 +48,43 @@ struct RingPipeShape {
     static constexpr int kHaloZones = 2 * (S - 1);
     static constexpr int kZPS = kRingZP + 1;                   // odd stride: zone lanes hit distinct banks
     // CTA size for configs[3]'s shape, W = 6 walls per zone and B = kB owned
-    // zones per block: 3 W / 2 owned + halo + 1 zone warp (15 warps at S = 12:
-    // at most 4 warps per scheduler, so 128 registers per thread)
+    // zones per block: 3 W / 2 owned + halo + zone + producer warps (16 warps
+    // at S = 12: 4 per scheduler, so 128 registers per thread)
     static constexpr int kB = 3;
-    static constexpr int kThreads = 32 * ((kB * 6 + 1) / 2 + (2 * (S - 1) * 6 + 31) / 32 + 1);
+    static constexpr int kThreads = 32 * ((kB * 6 + 1) / 2 + (2 * (S - 1) * 6 + 31) / 32 + 2);
     // nodes kept for a halo zone at distance d: S - d, rounded up to even
     __host__ __device__ static constexpr int halo_nodes(int d) { return (S - d + 1) & ~1; }
     __host__ __device__ static int own_warps(int B, int W) { return (B * W + 1) / 2; }
     __host__ __device__ static int halo_walls(int W) { return kHaloZones * W; }
     __host__ __device__ static int halo_warps(int W) { return (halo_walls(W) + 31) / 32; }
-    __host__ __device__ static int warps(int B, int W) { return own_warps(B, W) + halo_warps(W) + 1; }
+    __host__ __device__ static int warps(int B, int W) { return own_warps(B, W) + halo_warps(W) + 2; }
     __host__ __device__ static int threads(int B, int W) { return 32 * warps(B, W); }
     __host__ __device__ static int local_zones(int B) { return B + 2 * S; }
     // doubles: owned staging [4][B W][N], halo staging [4][HW][S], zone
-    // parameter blocks [2][LB][ZPS], surfaces [2][2][B W + HW], zone air
-    // [2][2][LB], forcing rows [S][rw], 8 mbarriers
+    // parameter blocks [2][LB][ZPS], staged zone air [2][2][LB], surfaces
+    // [2][2][B W + HW], zone air [2][2][LB], forcing rows [S][rw], mbarriers
     __host__ __device__ static size_t smem_doubles(int B, int W, int rw) {
         const size_t LB = local_zones(B);
         return static_cast<size_t>(4) * B * W * N + static_cast<size_t>(4) * halo_walls(W) * S + 2 * LB * kZPS +
-               4 * static_cast<size_t>(B * W + halo_walls(W)) + 4 * LB + ((static_cast<size_t>(S) * rw + 1) & ~1ull) +
-               8;
+               4 * LB + 4 * static_cast<size_t>(B * W + halo_walls(W)) + 4 * LB +
+               ((static_cast<size_t>(S) * rw + 1) & ~1ull) + 8;
     }
 };
 
+// per-step hand-off on named barriers: producers arrive (no wait), consumers
+// sync (the warp sleeps, issuing nothing, until the count is reached); every
+// use counts all blockDim threads (producer warps + consumer warps).  IDs 1-2:
+// surface samples of layer g (slot g & 1); IDs 3-4: zone air of layer g.
+__device__ __forceinline__ void nb_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void nb_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx_only(void* mb, unsigned bytes) {   // no arrival
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(void* mb) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(mb)) : "memory");
 }
@@ -96,14 +112,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
     const int oSO = 0;                                   // owned staging [4][OW][N]
     const int oSH = oSO + 4 * OW * N;                    // halo staging [4][HW][PH]
     const int oZS = oSH + 4 * HW * PH;                   // zone parameter blocks [2][LB][ZPS]
-    const int oSF = oZS + 2 * LB * ZPS;                  // surfaces [slot][field][OW + HW]
+    const int oZA = oZS + 2 * LB * ZPS;                  // staged zone air [2][2][LB] (producer)
+    const int oSF = oZA + 4 * LB;                        // surfaces [slot][field][OW + HW]
     const int oAR = oSF + 4 * (OW + HW);                 // zone air [slot][field][LB]
     const int oRW = oAR + 4 * LB;                        // forcing rows [S][rw]
     const int oMB = oRW + ((S * rw + 1) & ~1);           // mbarriers (8-byte each)
     double* mb_full = &smem[oMB + 0];                    // staging of the next block landed (tx)
     double* mb_free = &smem[oMB + 1];                    // staging consumed by every warp
-    double* mb_samp = &smem[oMB + 2];                    // [2] surface samples of layer g published
-    double* mb_air = &smem[oMB + 4];                     // [2] zone air of layer g published
+    const int NT = blockDim.x;                           // named-barrier count (every use: the whole CTA)
     auto so_ix = [&](int f, int i) { return oSO + f * OW * N + i; };
     auto sf_ix = [&](int slot, int f, int i) { return oSF + (slot * 2 + f) * (OW + HW) + i; };
     auto own_slot = [&](int wl) { const int z = wl / W; return (wl - z * W) * B + z; };
@@ -112,7 +128,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
     const int nblk = (Z + B - 1) / B;
     const int own_w = Sh::own_warps(B, W), halo_w = Sh::halo_warps(W);
-    const int zone_warp = own_w + halo_w;
+    const int zone_warp = own_w + halo_w, producer_warp = zone_warp + 1;
     const bool is_own = warp < own_w, is_halo = !is_own && warp < zone_warp;
 
     for (int i = tid; i < a.steps * rw; i += blockDim.x) {   // forcing rows of this launch
@@ -135,20 +151,22 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
     // halo zone hz (0 .. HZ-1): local zone and distance from the owned block
     auto halo_local = [&](int hz, int nown) { return hz < S - 1 ? 1 + hz : S + nown + (hz - (S - 1)); };
     auto halo_dist = [&](int hz) { return hz < S - 1 ? S - 1 - hz : hz - (S - 1) + 1; };
-    // the next block's staging: owned walls (one bulk copy per field), halo
-    // walls (one per wall and field) and zone parameter blocks, on mb_full;
-    // issued by the 32 lanes of the zone warp
-    auto prefetch = [&](int b, int par) {
+    // staging of block b (run by the producer warp): owned walls (one bulk copy
+    // per field) and halo walls (one per wall and field) on mb_full's tx count;
+    // zone parameter blocks (8-byte cp.async into the odd-stride layout) and
+    // zone air (loads) into parity `par`; then the producer's one arrival
+    auto stage = [&](int b, int par) {
         const int z0 = b * B, nown = min(B, Z - z0), L = nown + 2 * S;
         unsigned bytes = 0;
-        for (int hl = lane; hl < HW; hl += 32) bytes += 4u * 8u * Sh::halo_nodes(halo_dist(hl / W));
+        const bool halo_copies = !(a.dbg_skip & 1);
+        for (int hl = lane; hl < HW && halo_copies; hl += 32) bytes += 4u * 8u * Sh::halo_nodes(halo_dist(hl / W));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(FULL, bytes, o);
         const unsigned own_bytes = static_cast<unsigned>(nown * W * N * sizeof(double));
-        if (lane == 0) mbar_expect_tx(mb_full, bytes + 4 * own_bytes);
+        if (lane == 0) mbar_expect_tx_only(mb_full, bytes + 4 * own_bytes);
         __syncwarp();
         if (lane < 4) bulk_g2s(&smem[so_ix(lane, 0)], a.in[lane] + static_cast<size_t>(z0) * W * N, own_bytes, mb_full);
-        for (int hl = lane; hl < HW; hl += 32) {
+        for (int hl = lane; hl < HW && halo_copies; hl += 32) {
             const int hz = hl / W, wi = hl - hz * W;
             const int P = Sh::halo_nodes(halo_dist(hz));
             const size_t g = (static_cast<size_t>(gz(z0, halo_local(hz, nown))) * W + wi) * N + (N - P);
@@ -156,26 +174,27 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
             for (int f = 0; f < 4; ++f)
                 bulk_g2s(&smem[oSH + (f * HW + hl) * PH + (PH - P)], a.in[f] + g, 8u * P, mb_full);
         }
-        // zone parameter blocks into the odd-stride layout (8-byte copies; the
-        // zone warp itself consumes them, behind cp.async.wait_group)
         for (int i = lane; i < L * kRingZP; i += 32) {
             const int li = i / kRingZP, c = i - li * kRingZP;
             cp_async8(&smem[oZS + (par * LB + li) * ZPS + c], a.zparams + static_cast<size_t>(gz(z0, li)) * kRingZP + c);
         }
         asm volatile("cp.async.commit_group;\n" ::);
+        for (int i = lane; i < L; i += 32) {
+            const int gzi = gz(z0, i);
+            smem[oZA + (par * 2 + 0) * LB + i] = a.zu_in[gzi];
+            smem[oZA + (par * 2 + 1) * LB + i] = a.zv_in[gzi];
+        }
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(mb_full);             // release: the parameter blocks and air above
     };
     if (tid == 0) {
         mbar_init(mb_full, 1);
         mbar_init(mb_free, own_w + halo_w + 1);
-        mbar_init(&mb_samp[0], own_w + halo_w);
-        mbar_init(&mb_samp[1], own_w + halo_w);
-        mbar_init(&mb_air[0], 1);
-        mbar_init(&mb_air[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();                                     // rows staged, barriers initialised
-    if (warp == zone_warp && static_cast<int>(blockIdx.x) < nblk) prefetch(blockIdx.x, 0);
 
     unsigned acc = 0;
     // each role marches the blocks in its own loop, with its own registers; the
@@ -199,8 +218,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
         int g = 0;                                       // this role's running step index (mbarrier phases)
         for (int b = blockIdx.x, it = 0; b < nblk; b += gridDim.x, ++it) {
             const int z0 = b * B, nown = min(B, Z - z0);
-            const int L = nown + 2 * S;
-            const int par = it & 1;
             const bool next = b + static_cast<int>(gridDim.x) < nblk;
             mbar_wait_acq(mb_full, it & 1);                  // block b's staging landed
             const int wl = warp * 2 + lane / 16, sub = lane % 16;
@@ -249,8 +266,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
                 smem[sf_ix(g & 1, 0, oslot)] = uc[0];
                 smem[sf_ix(g & 1, 1, oslot)] = vc[0];
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&mb_samp[g & 1]);
+            nb_arrive(1 + (g & 1), NT);                  // layer-g samples published
             auto step = [&](double (&vP)[NPT], double (&vC)[NPT], double (&uP)[NPT], double (&uC)[NPT], int k) {
                 const int gg = g + k;
                 const double vs = rev ? vC[NPT - 1] : vC[0], us = rev ? uC[NPT - 1] : uC[0];
@@ -280,7 +296,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
                 const double ru = smem[am + 0], rv = smem[am + 1], rg = smem[am + 2], rq = smem[am + 3] + 0.0;
                 const double d = fma(-2.0, vP[0], vx0 + vC[1]);
                 const double du = fma(-2.0, uP[0], ux0 + uC[1]);
-                mbar_wait_acq(&mb_air[gg & 1], (gg >> 1) & 1);
+                nb_sync(3 + (gg & 1), NT);               // layer-gg zone air
                 const double au = smem[ar_ix(gg & 1, 0, li)], av = smem[ar_ix(gg & 1, 1, li)];
                 const double u_inf = first ? ru : au, v_inf = first ? rv : av;
                 const double g_inf = first ? rg : 0.0, q_inf = first ? rq : 0.0;
@@ -297,8 +313,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
                         smem[sf_ix((gg + 1) & 1, 0, oslot)] = uP[0];
                         smem[sf_ix((gg + 1) & 1, 1, oslot)] = vP[0];
                     }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&mb_samp[(gg + 1) & 1]);
+                    nb_arrive(1 + ((gg + 1) & 1), NT);
                 }
             };
             int k = 0;
@@ -348,8 +363,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
         int g = 0;                                       // this role's running step index (mbarrier phases)
         for (int b = blockIdx.x, it = 0; b < nblk; b += gridDim.x, ++it) {
             const int z0 = b * B, nown = min(B, Z - z0);
-            const int L = nown + 2 * S;
-            const int par = it & 1;
             const bool next = b + static_cast<int>(gridDim.x) < nblk;
             mbar_wait_acq(mb_full, it & 1);                  // block b's staging landed
             // halo wall: its last PH nodes (the last P(d) of them real, the rest
@@ -381,8 +394,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
                 smem[sf_ix(g & 1, 0, hslot)] = uc[PH - 1];
                 smem[sf_ix(g & 1, 1, hslot)] = vc[PH - 1];
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&mb_samp[g & 1]);
+            nb_arrive(1 + (g & 1), NT);                  // layer-g samples published
             const int kmax = __reduce_max_sync(FULL, ks);
             auto step = [&](double (&vP)[PH], double (&vC)[PH], double (&uP)[PH], double (&uC)[PH], int k) {
                 const int gg = g + k;
@@ -399,7 +411,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
                         vP[p] = fma(cb, d, vP[p]);
                         uP[p] = fma(csv, d, fma(csu, du, uP[p]));
                     }
-                    mbar_wait_acq(&mb_air[gg & 1], (gg >> 1) & 1);
+                    nb_sync(3 + (gg & 1), NT);
                     const double u_a = smem[ar_ix(gg & 1, 0, li)], v_a = smem[ar_ix(gg & 1, 1, li)];
                     const double t = v_a - vP[PH - 1], tu = u_a - uP[PH - 1];
                     const double vn = fma(c.e, t, fma(c.b, d_f, fma(c.e_g, 0.0, vP[PH - 1])));
@@ -408,15 +420,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
                     vP[PH - 1] = vn;
                     uP[PH - 1] = un;
                 } else {
-                    mbar_wait_acq(&mb_air[gg & 1], (gg >> 1) & 1);   // keep the phase count
+                    nb_sync(3 + (gg & 1), NT);           // keep the barrier phases
                 }
                 if (k + 1 < a.steps) {
                     if (live && k < ks) {
                         smem[sf_ix((gg + 1) & 1, 0, hslot)] = uP[PH - 1];
                         smem[sf_ix((gg + 1) & 1, 1, hslot)] = vP[PH - 1];
                     }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&mb_samp[(gg + 1) & 1]);
+                    nb_arrive(1 + ((gg + 1) & 1), NT);
                 }
             };
             int k = 0;
@@ -428,132 +439,108 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
             if (next) load_cf(b + gridDim.x);
             g += a.steps;
         }
-    } else {
-        double zair[2][2];                               // [slot i, i + 32][field]
-        auto load_air = [&](int bb) {
-            const int z0 = bb * B, nown = min(B, Z - z0);
-            const int L = nown + 2 * S;
-    #pragma unroll
-            for (int s = 0; s < 2; ++s) {
-                const int i = lane + 32 * s;
-                const int gzi = gz(z0, i < L ? i : 0);
-                zair[s][0] = a.zu_in[gzi];
-                zair[s][1] = a.zv_in[gzi];
-            }
-        };
-        if (static_cast<int>(blockIdx.x) < nblk) load_air(blockIdx.x);
-        int g = 0;                                       // this role's running step index (mbarrier phases)
+    } else if (warp == zone_warp) {
+        // the zone warp: zone_step_explicit (zone.cpp:69-74) of local zone `lane`
+        // (1 .. L-2 live; 0 and L-1 contribute their layer-0 air only; L <= 32).
+        // Its parameter block (as K4r's) is read into registers once per block;
+        // per step everything but the wall-link terms — sources, ventilation,
+        // peers, which need only zone air this warp produced itself — is summed
+        // before the wait for the walls' samples (the reference's order:
+        // sources, ventilation, peers, walls)
+        const int i = lane;
+        int g = 0;                                       // this role's running step index
         for (int b = blockIdx.x, it = 0; b < nblk; b += gridDim.x, ++it) {
             const int z0 = b * B, nown = min(B, Z - z0);
             const int L = nown + 2 * S;
             const int par = it & 1;
-            const bool next = b + static_cast<int>(gridDim.x) < nblk;
-            mbar_wait_acq(mb_full, it & 1);                  // block b's staging landed
-            // the zone warp: zone_step_explicit (zone.cpp:69-74) of local zones
-            // lane and lane + 32 (1 .. L-2 live; 0 and L-1 contribute their
-            // layer-0 air only), the staged parameter block as in K4r; it also
-            // issues the next block's prefetch
-            asm volatile("cp.async.wait_group 0;\n" ::: "memory");   // this block's parameter blocks
-            __syncwarp();
-            int ls[2][NL], pidx[2][NP], zp[2], sidx[2];
-            bool valid[2], live[2], owned[2];
+            mbar_wait_acq(mb_full, it & 1);              // block b's staging landed
+            const bool valid = i < L, live = i >= 1 && i < L - 1, owned = i >= S && i < S + nown;
+            const int hz = i < S ? i - 1 : (S - 1) + (i - S - nown);
+            const int zp = oZS + (par * LB + (valid ? i : 0)) * ZPS;
+            int nlink = 0, npeer = 0, sidx = 0;
+            if (live) {
+                nlink = static_cast<int>(smem[zp + 4]);
+                npeer = static_cast<int>(smem[zp + 5]);
+                sidx = static_cast<int>(smem[zp + 6]);
+            }
+            const double c0 = smem[zp + 0], gv = smem[zp + 1], qv1 = smem[zp + 2], qv2 = smem[zp + 3];
+            int ls[NL], pidx[NP];
+            double lT[NL], lM[NL], lD[NL], pg[NP], pq1[NP], pq2[NP];
 #pragma unroll
-            for (int s = 0; s < 2; ++s) {
-                const int i = lane + 32 * s;
-                valid[s] = i < L;
-                live[s] = i >= 1 && i < L - 1;
-                owned[s] = i >= S && i < S + nown;
-                const int hz = i < S ? i - 1 : (S - 1) + (i - S - nown);
-                zp[s] = oZS + (par * LB + (valid[s] ? i : 0)) * ZPS;
-                int nlink = 0, npeer = 0;
-                sidx[s] = 0;
-                if (live[s]) {
-                    nlink = static_cast<int>(smem[zp[s] + 4]);
-                    npeer = static_cast<int>(smem[zp[s] + 5]);
-                    sidx[s] = static_cast<int>(smem[zp[s] + 6]);
-                }
+            for (int q = 0; q < NL; ++q) {
+                const int wi = q < nlink ? static_cast<int>(smem[zp + 8 + 4 * q]) : 0;
+                ls[q] = owned ? wi * B + (i - S) : OW + wi * HZ + hz;
+                lT[q] = smem[zp + 9 + 4 * q];
+                lM[q] = smem[zp + 10 + 4 * q];
+                lD[q] = smem[zp + 11 + 4 * q];
+            }
 #pragma unroll
-                for (int q = 0; q < NL; ++q) {
-                    const int wi = q < nlink ? static_cast<int>(smem[zp[s] + 8 + 4 * q]) : 0;
-                    ls[s][q] = owned[s] ? wi * B + (i - S) : OW + wi * HZ + hz;
-                }
-#pragma unroll
-                for (int q = 0; q < NP; ++q) {
-                    const int pg = q < npeer ? static_cast<int>(smem[zp[s] + 40 + 4 * q]) : -1;
-                    pidx[s][q] = i >= 1 && gz(z0, i - 1) == pg ? i - 1 : i + 1;
-                }
-                if (valid[s]) {                          // layer-g air from the staged registers
-                    smem[ar_ix(g & 1, 0, i)] = zair[s][0];
-                    smem[ar_ix(g & 1, 1, i)] = zair[s][1];
-                }
+            for (int q = 0; q < NP; ++q) {
+                const int pgz = q < npeer ? static_cast<int>(smem[zp + 40 + 4 * q]) : -1;
+                pidx[q] = i >= 1 && gz(z0, i - 1) == pgz ? i - 1 : i + 1;
+                pg[q] = smem[zp + 41 + 4 * q];
+                pq1[q] = smem[zp + 42 + 4 * q];
+                pq2[q] = smem[zp + 43 + 4 * q];
+            }
+            if (valid) {                                 // layer-g air from the producer's staging
+                smem[ar_ix(g & 1, 0, i)] = smem[oZA + (par * 2 + 0) * LB + i];
+                smem[ar_ix(g & 1, 1, i)] = smem[oZA + (par * 2 + 1) * LB + i];
             }
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&mb_air[g & 1]);
-                mbar_arrive(mb_free);
-            }
-            if (next) {
-                mbar_wait_acq(mb_free, it & 1);          // every warp consumed block b's staging
-                prefetch(b + gridDim.x, par ^ 1);
-                load_air(b + gridDim.x);
-            }
+            nb_arrive(3 + (g & 1), NT);                  // layer-g air published
+            if (lane == 0) mbar_arrive(mb_free);         // this block's staging consumed
             for (int k = 0; k < a.steps; ++k) {
                 const int gg = g + k;
-                mbar_wait_acq(&mb_samp[gg & 1], (gg >> 1) & 1);
                 const int cs = gg & 1, ns = cs ^ 1;
-                double nu[2], nv[2];
+                double du = 0.0, dv = 0.0, u_a = 0.0, v_a = 0.0;
+                if (live) {
+                    u_a = smem[ar_ix(cs, 0, i)];
+                    v_a = smem[ar_ix(cs, 1, i)];
+                    const int srow = oRW + k * rw + 4 * a.n_channels;
+                    const int sz = srow + 3 * sidx;
+                    const double u_inf = smem[srow + 3 * a.n_sources + 0], v_inf = smem[srow + 3 * a.n_sources + 1];
+                    du = smem[sz + 1] + smem[sz + 2] + qv1 * (u_inf * v_inf - u_a * v_a) + qv2 * (u_inf - u_a);
+                    dv = smem[sz + 0] + gv * (v_inf - v_a);
 #pragma unroll
-                for (int s = 0; s < 2; ++s) {
-                    const int i = lane + 32 * s;
-                    nu[s] = nv[s] = 0.0;
-                    if (live[s]) {
-                        const double u_a = smem[ar_ix(cs, 0, i)], v_a = smem[ar_ix(cs, 1, i)];
-                        const int srow = oRW + k * rw + 4 * a.n_channels;
-                        const int sz = srow + 3 * sidx[s];
-                        const double u_inf = smem[srow + 3 * a.n_sources + 0], v_inf = smem[srow + 3 * a.n_sources + 1];
-                        const int p = zp[s];
-                        double du = smem[sz + 1] + smem[sz + 2] + smem[p + 2] * (u_inf * v_inf - u_a * v_a) +
-                                    smem[p + 3] * (u_inf - u_a);
-                        double dv = smem[sz + 0] + smem[p + 1] * (v_inf - v_a);
-#pragma unroll
-                        for (int q = 0; q < NP; ++q) {
-                            const double pu = smem[ar_ix(cs, 0, pidx[s][q])], pv = smem[ar_ix(cs, 1, pidx[s][q])];
-                            du += smem[p + 42 + 4 * q] * (pu * pv - u_a * v_a) + smem[p + 43 + 4 * q] * (pu - u_a);
-                            dv += smem[p + 41 + 4 * q] * (pv - v_a);
-                        }
-#pragma unroll
-                        for (int q = 0; q < NL; ++q) {
-                            const double us = smem[sf_ix(cs, 0, ls[s][q])], vs = smem[sf_ix(cs, 1, ls[s][q])];
-                            du += smem[p + 9 + 4 * q] * (us - u_a) + smem[p + 10 + 4 * q] * (vs - v_a);
-                            dv += smem[p + 11 + 4 * q] * (v_a - vs);
-                        }
-                        nu[s] = u_a + a.dt * (du / smem[p + 0]);
-                        nv[s] = v_a + a.dt * dv;
-                        if (owned[s])
-                            acc |= static_cast<unsigned>(__double2hiint(nu[s])) | static_cast<unsigned>(__double2hiint(nv[s]));
+                    for (int q = 0; q < NP; ++q) {
+                        const double pu = smem[ar_ix(cs, 0, pidx[q])], pv = smem[ar_ix(cs, 1, pidx[q])];
+                        du += pq1[q] * (pu * pv - u_a * v_a) + pq2[q] * (pu - u_a);
+                        dv += pg[q] * (pv - v_a);
                     }
+                }
+                nb_sync(1 + cs, NT);                     // layer-gg samples of every wall
+                double nu = 0.0, nv = 0.0;
+                if (live) {
+#pragma unroll
+                    for (int q = 0; q < NL; ++q) {
+                        const double us = smem[sf_ix(cs, 0, ls[q])], vs = smem[sf_ix(cs, 1, ls[q])];
+                        du += lT[q] * (us - u_a) + lM[q] * (vs - v_a);
+                        dv += lD[q] * (v_a - vs);
+                    }
+                    nu = u_a + a.dt * (du / c0);
+                    nv = v_a + a.dt * dv;
+                    if (owned) acc |= static_cast<unsigned>(__double2hiint(nu)) | static_cast<unsigned>(__double2hiint(nv));
                 }
                 __syncwarp();                            // every lane read layer gg's air
                 if (k + 1 < a.steps) {
-#pragma unroll
-                    for (int s = 0; s < 2; ++s)
-                        if (live[s]) {
-                            smem[ar_ix(ns, 0, lane + 32 * s)] = nu[s];
-                            smem[ar_ix(ns, 1, lane + 32 * s)] = nv[s];
-                        }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&mb_air[ns]);
-                } else {
-#pragma unroll
-                    for (int s = 0; s < 2; ++s)
-                        if (owned[s]) {
-                            const int z = gz(z0, lane + 32 * s);
-                            a.zu_out[z] = nu[s];
-                            a.zv_out[z] = nv[s];
-                        }
+                    if (live) {
+                        smem[ar_ix(ns, 0, i)] = nu;
+                        smem[ar_ix(ns, 1, i)] = nv;
+                    }
+                    nb_arrive(3 + ns, NT);
+                } else if (owned) {
+                    const int z = gz(z0, i);
+                    a.zu_out[z] = nu;
+                    a.zv_out[z] = nv;
                 }
             }
             g += a.steps;
+        }
+    } else if (warp == producer_warp) {
+        // the producer: stages block b (after every warp consumed block b - grid)
+        for (int b = blockIdx.x, it = 0; b < nblk; b += gridDim.x, ++it) {
+            if (it > 0) mbar_wait_acq(mb_free, (it - 1) & 1);
+            stage(b, it & 1);
         }
     }
     // fast guard verdict of the whole launch (bit 30: |x| >= 2 or not finite)

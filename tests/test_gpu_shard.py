@@ -145,7 +145,7 @@ def test_device_payload_exchange_bitwise(case):
         w = workloads.long_domain(n_nodes=n, nsteps=steps)
         model, init = w.model, w.init
     else:
-        Z, W, n, steps = (16, 6, 32, 120) if case == "ring" else (30, 6, 128, 100)
+        Z, W, n, steps = (16, 6, 32, 120) if case == "ring" else (48, 6, 128, 100)
         w = workloads.zone_ring(n_zones=Z, walls_per_zone=W, n_nodes=n, nsteps=steps)
         rng = np.random.default_rng(5)
         init = {f: w.init[f] + 1e-3 * rng.standard_normal(w.init[f].size) for f in FIELDS}
