@@ -49,10 +49,12 @@ CONFIGS = {
                  run_steps=100_000),
     "cfg2": dict(flop=14, bytes=0, bound="fp32", kernel="df_coupled_fused_f32", scaling="weak", dtype="f32",
                  run_steps=100_000),
-    # cfg3 runs K4r (k_ring_reg.cuh): B = 4 zones per block, S = 8 steps per launch,
-    # (64 B x 3072 owned + 32 B x 756 halo nodes) / (3072 x 8) = 8.98 B/update
-    "cfg3": dict(flop=14.1, bytes=8.98, bound="hbm", kernel="ring_reg", scaling="strong", dtype="f64",
-                 run_steps=80_000),
+    # cfg3 runs K5 (k_ring_pipe.cuh): B = 3 zones per block, S = 12 steps per launch,
+    # halo trimmed to the cone: (64 B x 2304 owned + 32 B x 864 halo nodes) / (2304 x 12)
+    # = 6.33 B/update (K4r, --ring-kernel 1: B = 4, S = 8, (64 x 3072 + 32 x 756) / (3072 x 8)
+    # = 8.98 B/update)
+    "cfg3": dict(flop=14.1, bytes=6.33, bound="hbm", kernel="ring_pipe", scaling="strong", dtype="f64",
+                 run_steps=80_000, bytes_by_kernel={"ring_pipe": 6.33, "ring_reg": 8.98}),
     # cfg4 runs the temporally blocked K3w (k_dv_warp.cuh: 256-node windows, 8 steps
     # per launch, (32 x 256 + 32 x 240) / (240 x 8) = 8.27 B/update), so min(HBM,
     # FP64) is the FP64 side; sharded (N>1) every slab runs K3w too
@@ -422,8 +424,13 @@ def main():
     top = max(stats, key=lambda s: s["ms"])
     kernel_rate = top["node_updates"] / (top["ms"] * 1e-3) if top["node_updates"] else 0.0
     share = top["ms"] / sum(s["ms"] for s in stats)
+    bytes_per_update = cfg.get("bytes_by_kernel", {}).get(top["name"], cfg["bytes"])
+    extra = {}
     if cfg["bound"] == "hbm":
-        achieved = kernel_rate * cfg["bytes"] / 1e9
+        achieved = kernel_rate * bytes_per_update / 1e9
+        # the same kernel against SURVEY §8(d)'s FP64 roofline (its own convention)
+        extra = {"fp64_achieved_tflops": kernel_rate * cfg["flop"] / 1e12, "fp64_peak_tflops": peak64,
+                 "fp64_frac": kernel_rate * cfg["flop"] / 1e12 / peak64}
         peak, unit, peak_src = 6458.4, "GB/s", "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
         try:
             peak = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
@@ -504,8 +511,8 @@ def main():
                 "roofline": {"bound": cfg["bound"], "achieved": achieved, "peak": peak, "unit": unit,
                              "frac": achieved / peak if peak else None, "traffic": traffic,
                              "kernel": top["name"], "kernel_share_of_step": share,
-                             "flop_per_update": cfg["flop"], "bytes_per_update": cfg["bytes"],
-                             "peak_source": peak_src, "kernel_node_updates_per_s": kernel_rate},
+                             "flop_per_update": cfg["flop"], "bytes_per_update": bytes_per_update,
+                             "peak_source": peak_src, "kernel_node_updates_per_s": kernel_rate, **extra},
                 "clocks": clk, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu}
         if sharded is not None:
             line["sharded"] = sharded

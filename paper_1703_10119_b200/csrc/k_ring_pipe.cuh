@@ -73,7 +73,7 @@ struct RingPipeShape {
 
 // per-step hand-off on named barriers: producers arrive (no wait), consumers
 // sync (the warp sleeps, issuing nothing, until the count is reached); every
-// use counts all blockDim threads (producer warps + consumer warps).  IDs 1-2:
+// use counts the wall warps and the zone warp (the producer warp stays out).  IDs 1-2:
 // surface samples of layer g (slot g & 1); IDs 3-4: zone air of layer g.
 __device__ __forceinline__ void nb_arrive(int id, int n) {
     asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
@@ -119,7 +119,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
     const int oMB = oRW + ((S * rw + 1) & ~1);           // mbarriers (8-byte each)
     double* mb_full = &smem[oMB + 0];                    // staging of the next block landed (tx)
     double* mb_free = &smem[oMB + 1];                    // staging consumed by every warp
-    const int NT = blockDim.x;                           // named-barrier count (every use: the whole CTA)
     auto so_ix = [&](int f, int i) { return oSO + f * OW * N + i; };
     auto sf_ix = [&](int slot, int f, int i) { return oSF + (slot * 2 + f) * (OW + HW) + i; };
     auto own_slot = [&](int wl) { const int z = wl / W; return (wl - z * W) * B + z; };
@@ -129,6 +128,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
     const int nblk = (Z + B - 1) / B;
     const int own_w = Sh::own_warps(B, W), halo_w = Sh::halo_warps(W);
     const int zone_warp = own_w + halo_w, producer_warp = zone_warp + 1;
+    const int NT = 32 * (zone_warp + 1);                 // named-barrier count: walls + zone warp (no producer)
     const bool is_own = warp < own_w, is_halo = !is_own && warp < zone_warp;
 
     for (int i = tid; i < a.steps * rw; i += blockDim.x) {   // forcing rows of this launch
