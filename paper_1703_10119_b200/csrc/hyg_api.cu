@@ -217,7 +217,7 @@ struct hyg_ctx {
     int ring_reg_B = 0;              // K4r (registers + prefetch): zones per CTA, 0 if not applicable
     int ring_grid_cap = 0;           // HYG_TUNE_RING_GRID: K4r/K5 persistent grid cap (0: one CTA per SM)
     int ring_pipe_B = 0;             // K5 (k_ring_pipe.cuh): zones per block, 0 if not applicable
-    int ring_kernel = 0;             // HYG_TUNE_RING_KERNEL: 0 auto (K5, else K4r), 1 K4r, 2 K4
+    int ring_kernel = 0;             // HYG_TUNE_RING_KERNEL: 0 auto (K4r), 1 K4r, 2 K4, 3 K5
     bool mat_exact = false;          // HYG_TUNE_MATERIAL_EXACT: CrMath evaluation + IEEE-division rows
     bool owned_partial = false;      // hyg_set_owned narrowed the guard to a shard's range
     int ring_dbg_skip = 0;           // HYG_DEBUG_RING_SKIP (timing experiments only; wrong results)
@@ -1101,8 +1101,9 @@ void launch_ring(const RingArgs& a, int grid, int threads, size_t smem, cudaStre
 }
 
 int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool reg = true) {
-    // K5 (pipelined, S = 12) where it applies, unless a tuning knob picks K4r/K4
-    const bool pipe = reg && c->ring_pipe_B > 0 && c->norm >= 2.0 && c->ring_kernel == 0;
+    // K4r by default; K5 (pipelined, S = 12, HYG_TUNE_RING_KERNEL = 3) measured slower
+    // (2.8e11 vs 3.4e11: the per-step critical path binds, not HBM)
+    const bool pipe = reg && c->ring_pipe_B > 0 && c->norm >= 2.0 && c->ring_kernel == 3;
     if (c->ring_kernel == 2) reg = false;
     if (c->coef_dt != dt) {
         LaunchScope ls(c, "coupled_coef", 0.0);
@@ -2337,7 +2338,7 @@ int hyg_set_tuning(hyg_ctx* c, int32_t knob, int64_t value) {
     switch (knob) {
         case HYG_TUNE_RING_GRID: c->ring_grid_cap = static_cast<int>(std::min<int64_t>(value, INT32_MAX)); return HYG_OK;
         case HYG_TUNE_RING_KERNEL:
-            if (value > 2) return HYG_EINVAL;
+            if (value > 3) return HYG_EINVAL;
             c->ring_kernel = static_cast<int>(value);
             return HYG_OK;
         case HYG_TUNE_MATERIAL_EXACT:

@@ -18,10 +18,10 @@
 //     -> walls), so a wall warp computes the interior rows of step k while the
 //     zone warp is still producing the air its face row needs;
 //   * a producer warp stages the next block while the current one marches:
-//     owned walls (one bulk copy per field) and halo walls (one per wall and
-//     field) on one mbarrier's transaction count, zone parameter blocks
-//     (cp.async) and zone air; the row coefficients of the next block are
-//     loaded into registers behind the steps;
+//     owned walls (one bulk copy per field, on an mbarrier's transaction
+//     count), halo walls and zone parameter blocks (cp.async) and zone air;
+//     the row coefficients of the next block are loaded into registers
+//     behind the steps;
 //   * the zone warp sums every term that needs no wall sample (sources,
 //     ventilation, peers) before it waits for the walls, so the per-step
 //     critical path is the six wall-link terms and the division;
@@ -46,7 +46,7 @@ template <int S>
 struct RingPipeShape {
     static constexpr int NPT = 8, N = 128;
     static constexpr int kHaloZones = 2 * (S - 1);
-    static constexpr int kZPS = kRingZP + 1;                   // odd stride: zone lanes hit distinct banks
+    static constexpr int kZPS = kRingZP;                       // 448 B rows: whole-block bulk copies (read once per block)
     // CTA size for configs[3]'s shape, W = 6 walls per zone and B = kB owned
     // zones per block: 3 W / 2 owned + halo + zone + producer warps (16 warps
     // at S = 12: 4 per scheduler, so 128 registers per thread)
@@ -95,6 +95,14 @@ __device__ __forceinline__ void mbar_wait_acq(void* mb, unsigned phase) {
         "r"(phase)
         : "memory");
 }
+
+// timing experiments only: per-phase clock64 stamps of CTA 0 into g_ring_prof
+// (k_ring_reg.cuh, RING_PROF builds): [block iteration][event]
+#if RING_PROF
+#define PSTAMP(e) do { if (blockIdx.x == 0 && lane == 0 && it < 32) g_ring_prof[it * 16 + (e)] = clock64(); } while (0)
+#else
+#define PSTAMP(e) do { } while (0)
+#endif
 
 // THREADS: the CTA size the host launches (whole roles; registers are sized for it)
 template <int S, int THREADS>
@@ -152,31 +160,41 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
     auto halo_local = [&](int hz, int nown) { return hz < S - 1 ? 1 + hz : S + nown + (hz - (S - 1)); };
     auto halo_dist = [&](int hz) { return hz < S - 1 ? S - 1 - hz : hz - (S - 1) + 1; };
     // staging of block b (run by the producer warp): owned walls (one bulk copy
-    // per field) and halo walls (one per wall and field) on mb_full's tx count;
-    // zone parameter blocks (8-byte cp.async into the odd-stride layout) and
-    // zone air (loads) into parity `par`; then the producer's one arrival
+    // per field) and zone parameter blocks (one per contiguous run) on
+    // mb_full's tx count; halo walls (16-byte cp.async) and zone air (loads)
+    // into parity `par`; then the producer's one arrival
     auto stage = [&](int b, int par) {
         const int z0 = b * B, nown = min(B, Z - z0), L = nown + 2 * S;
-        unsigned bytes = 0;
-        const bool halo_copies = !(a.dbg_skip & 1);
-        for (int hl = lane; hl < HW && halo_copies; hl += 32) bytes += 4u * 8u * Sh::halo_nodes(halo_dist(hl / W));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(FULL, bytes, o);
         const unsigned own_bytes = static_cast<unsigned>(nown * W * N * sizeof(double));
-        if (lane == 0) mbar_expect_tx_only(mb_full, bytes + 4 * own_bytes);
+        // zone parameter blocks: the local zones are one or two contiguous runs
+        // of the ring (one copy per zone for rings narrower than the block)
+        const int g0 = gz(z0, 0);
+        const int run1 = wide ? min(L, Z - g0) : 0;
+        const unsigned zp_bytes = static_cast<unsigned>(L * kRingZP * sizeof(double));
+        if (lane == 0) mbar_expect_tx_only(mb_full, 4 * own_bytes + zp_bytes);
         __syncwarp();
         if (lane < 4) bulk_g2s(&smem[so_ix(lane, 0)], a.in[lane] + static_cast<size_t>(z0) * W * N, own_bytes, mb_full);
-        for (int hl = lane; hl < HW && halo_copies; hl += 32) {
-            const int hz = hl / W, wi = hl - hz * W;
-            const int P = Sh::halo_nodes(halo_dist(hz));
-            const size_t g = (static_cast<size_t>(gz(z0, halo_local(hz, nown))) * W + wi) * N + (N - P);
-#pragma unroll
-            for (int f = 0; f < 4; ++f)
-                bulk_g2s(&smem[oSH + (f * HW + hl) * PH + (PH - P)], a.in[f] + g, 8u * P, mb_full);
+        if (wide) {
+            if (lane == 4)
+                bulk_g2s(&smem[oZS + par * LB * ZPS], a.zparams + static_cast<size_t>(g0) * kRingZP,
+                         static_cast<unsigned>(run1 * kRingZP * sizeof(double)), mb_full);
+            if (lane == 5 && run1 < L)
+                bulk_g2s(&smem[oZS + (par * LB + run1) * ZPS], a.zparams,
+                         static_cast<unsigned>((L - run1) * kRingZP * sizeof(double)), mb_full);
+        } else {
+            for (int li = lane; li < L; li += 32)
+                bulk_g2s(&smem[oZS + (par * LB + li) * ZPS], a.zparams + static_cast<size_t>(gz(z0, li)) * kRingZP,
+                         static_cast<unsigned>(kRingZP * sizeof(double)), mb_full);
         }
-        for (int i = lane; i < L * kRingZP; i += 32) {
-            const int li = i / kRingZP, c = i - li * kRingZP;
-            cp_async8(&smem[oZS + (par * LB + li) * ZPS + c], a.zparams + static_cast<size_t>(gz(z0, li)) * kRingZP + c);
+        // halo walls: 16-byte cp.async, one (halo zone, wall, field) segment of
+        // P nodes per lane and iteration — hundreds of 16-96 byte bulk copies
+        // per block measured far slower on the TMA engine (profiles/)
+        for (int sg = lane; sg < HZ * W * 4 && !(a.dbg_skip & 1); sg += 32) {
+            const int f = sg & 3, hl = sg >> 2, hz = hl / W, wi = hl - hz * W;
+            const int P = Sh::halo_nodes(halo_dist(hz));
+            const double* src = a.in[f] + (static_cast<size_t>(gz(z0, halo_local(hz, nown))) * W + wi) * N + (N - P);
+            double* dst = &smem[oSH + (f * HW + hl) * PH + (PH - P)];
+            for (int c = 0; c < P; c += 2) cp_async16(dst + c, src + c);
         }
         asm volatile("cp.async.commit_group;\n" ::);
         for (int i = lane; i < L; i += 32) {
@@ -219,7 +237,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
         for (int b = blockIdx.x, it = 0; b < nblk; b += gridDim.x, ++it) {
             const int z0 = b * B, nown = min(B, Z - z0);
             const bool next = b + static_cast<int>(gridDim.x) < nblk;
+            if (warp == 0) PSTAMP(0);
             mbar_wait_acq(mb_full, it & 1);                  // block b's staging landed
+            if (warp == 0) PSTAMP(1);
             const int wl = warp * 2 + lane / 16, sub = lane % 16;
             const bool live = wl < nown * W;
             const int wlc = live ? wl : 0;
@@ -258,6 +278,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
             rd(3, vc);
             __syncwarp();
             if (lane == 0) mbar_arrive(mb_free);         // staging consumed by this warp
+            if (warp == 0) PSTAMP(2);
             const double cb = cf[0], csu = cf[1], csv = cf[2];
             const double fe = cf[3], fb = cf[4], feg = cf[5], fctv = cf[6], fcsv = cf[7], fctu = cf[8], fcsu = cf[9],
                          fcq = cf[10], fcg = cf[11];
@@ -329,7 +350,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
                     x = up[q]; up[q] = uc[q]; uc[q] = x;
                 }
             }
+            if (warp == 0) PSTAMP(3);
             if (next) load_cf(b + gridDim.x);
+            if (warp == 0) PSTAMP(4);
             // out = (layer k+S-1, layer k+S) straight from registers, node order
             if (live) {
                 const size_t o = (static_cast<size_t>(z0) * W + wl) * N + sub * NPT;
@@ -344,6 +367,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
                 st(a.out[2], vp);
                 st(a.out[3], vc);
             }
+            if (warp == 0) PSTAMP(5);
             g += a.steps;
         }
     } else if (is_halo) {
@@ -454,6 +478,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
             const int L = nown + 2 * S;
             const int par = it & 1;
             mbar_wait_acq(mb_full, it & 1);              // block b's staging landed
+            PSTAMP(6);
             const bool valid = i < L, live = i >= 1 && i < L - 1, owned = i >= S && i < S + nown;
             const int hz = i < S ? i - 1 : (S - 1) + (i - S - nown);
             const int zp = oZS + (par * LB + (valid ? i : 0)) * ZPS;
@@ -489,6 +514,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
             __syncwarp();
             nb_arrive(3 + (g & 1), NT);                  // layer-g air published
             if (lane == 0) mbar_arrive(mb_free);         // this block's staging consumed
+            PSTAMP(7);
             for (int k = 0; k < a.steps; ++k) {
                 const int gg = g + k;
                 const int cs = gg & 1, ns = cs ^ 1;
@@ -534,13 +560,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_ring_pipe(const RingArgs a) {
                     a.zv_out[z] = nv;
                 }
             }
+            PSTAMP(8);
             g += a.steps;
         }
     } else if (warp == producer_warp) {
         // the producer: stages block b (after every warp consumed block b - grid)
         for (int b = blockIdx.x, it = 0; b < nblk; b += gridDim.x, ++it) {
+            PSTAMP(9);
             if (it > 0) mbar_wait_acq(mb_free, (it - 1) & 1);
+            PSTAMP(10);
             stage(b, it & 1);
+            PSTAMP(11);
         }
     }
     // fast guard verdict of the whole launch (bit 30: |x| >= 2 or not finite)

@@ -1,9 +1,8 @@
 """K4 (k_ring.cuh), K4r (k_ring_reg.cuh: owned walls in registers,
-persistent prefetching CTAs, fast guard; 64-node walls, or by the tuning
-knob) and K5 (k_ring_pipe.cuh: S = 12, trimmed halo, per-step mbarrier
-hand-off; 128-node walls with <= 6 links and <= 2 peers): the zone-ring
-building march temporally blocked with halo zones, against the C oracle's
-whole-building run
+persistent prefetching CTAs, fast guard; the default for 64/128-node walls)
+and K5 (k_ring_pipe.cuh, by the tuning knob: S = 12, trimmed halo, named-
+barrier hand-off, producer warp): the zone-ring building march temporally
+blocked with halo zones, against the C oracle's whole-building run
 (relative L-infinity <= 1e-10, zones included): zone counts that leave the
 last CTA partial, rings smaller than the halo (local copies of one zone), a
 chain without the wrap-around link, grids of 64/128/256 nodes, step counts
@@ -64,7 +63,7 @@ def _compare(got, b, n_zones):
 # run only when a CTA owns more than one block.  The grid cap forces that in
 # small rings: 42 zones = 11 blocks (the last one partial, 2 zones) over 3
 # CTAs walk 4/4/3 blocks; 64 zones over 2 CTAs walk 8 blocks each.
-@pytest.mark.parametrize("kernel,name", [(0, "ring_pipe"), (1, "ring_reg")])
+@pytest.mark.parametrize("kernel,name", [(0, "ring_reg"), (3, "ring_pipe")])
 @pytest.mark.parametrize("n_zones,cap,steps", [(42, 3, 203), (64, 2, 160), (42, 1, 77), (13, 2, 96)])
 def test_ring_reg_multi_block_per_cta(n_zones, cap, steps, kernel, name):
     w = workloads.zone_ring(n_zones=n_zones, walls_per_zone=6, n_nodes=128, nsteps=steps)
@@ -88,12 +87,12 @@ def test_ring_cfg3_full_ring_1000_steps():
     w = workloads.zone_ring(n_zones=8192, walls_per_zone=6, n_nodes=128, nsteps=steps)
     init = _noisy(w, 8192)
     got, st, stats = _gpu(w.model, init, steps)
-    assert stats.get("ring_pipe", {}).get("launches", 0) > 0, stats.keys()
+    assert stats.get("ring_reg", {}).get("launches", 0) > 0, stats.keys()
     assert "ring_tiled" not in stats
-    got_r, _, stats_r = _gpu(w.model, init, steps, kernel=1)          # K4r on the same input
-    assert stats_r.get("ring_reg", {}).get("launches", 0) > 0
+    got_p, _, stats_p = _gpu(w.model, init, steps, kernel=3)          # K5 on the same input
+    assert stats_p.get("ring_pipe", {}).get("launches", 0) > 0
     for k in ("u_prev", "u_curr", "v_prev", "v_curr", "zone_u", "zone_v"):
-        assert np.array_equal(got[k], got_r[k]), k                       # K5 == K4r bit for bit
+        assert np.array_equal(got[k], got_p[k]), k                       # K5 == K4r bit for bit
     b, rc, _, passes = _oracle(w.model, init, steps, nthreads=O.threads())
     assert rc == 0 and st.subiterations == passes
     err, zerr = _compare(got, b, 8192)
@@ -109,7 +108,7 @@ def test_ring_64_zones_full_horizon(cap):
     w = workloads.zone_ring(n_zones=64, walls_per_zone=6, n_nodes=128, nsteps=steps)
     init = _noisy(w, 64)
     got, st, stats = _gpu(w.model, init, steps, grid_cap=cap)
-    assert stats.get("ring_pipe", {}).get("launches", 0) > 0
+    assert stats.get("ring_reg", {}).get("launches", 0) > 0
     b, rc, _, passes = _oracle(w.model, init, steps, nthreads=O.threads())
     assert rc == 0 and st.subiterations == passes
     err, zerr = _compare(got, b, 64)
@@ -126,7 +125,7 @@ def test_ring_matches_oracle(n_zones, wpz, n, steps):
     init = {k: v + (2e-3 * rng.standard_normal(v.size) if k in ("u_prev", "u_curr", "v_prev", "v_curr") else 0)
             for k, v in w.init.items()}
     got, st, stats = _gpu(w.model, init, steps)
-    kern = "ring_pipe" if n == 128 and wpz <= 6 else "ring_reg" if n <= 128 else "ring_tiled"
+    kern = "ring_reg" if n <= 128 else "ring_tiled"
     assert stats.get(kern, {}).get("launches", 0) > 0, stats.keys()
     b, rc, _, passes = _oracle(w.model, init, steps)
     assert rc == 0 and st.subiterations == passes
@@ -143,7 +142,7 @@ def test_ring_chain_without_wrap():
     zs[0].interzone = [l for l in zs[0].interzone if l[0] == 1]
     zs[-1].interzone = [l for l in zs[-1].interzone if l[0] == len(zs) - 2]
     got, st, stats = _gpu(w.model, w.init, 300)
-    assert stats.get("ring_pipe", {}).get("launches", 0) > 0
+    assert stats.get("ring_reg", {}).get("launches", 0) > 0
     b, rc, _, _ = _oracle(w.model, w.init, 300)
     assert rc == 0
     assert rel_linf(got, dict(b.state)) <= TOL
@@ -181,7 +180,7 @@ def test_ring_reg_fast_guard_hands_over_to_k4():
     for k in ("u_prev", "u_curr"):
         init[k][5 * 128 + 40: 5 * 128 + 60] += 1.5          # wall 5, interior nodes
     got, st, stats = _gpu(w.model, init, 120)
-    assert stats.get("ring_pipe", {}).get("launches", 0) > 0 and stats.get("ring_tiled", {}).get("launches", 0) > 0
+    assert stats.get("ring_reg", {}).get("launches", 0) > 0 and stats.get("ring_tiled", {}).get("launches", 0) > 0
     b, rc, _, _ = _oracle(w.model, init, 120)
     assert rc == 0
     assert rel_linf(got, dict(b.state)) <= TOL

@@ -128,12 +128,13 @@ class _LoopbackComm:
         return self._reduce(x, min)
 
 
-@pytest.mark.parametrize("case", ["long", "ring", "ring128"])
+@pytest.mark.parametrize("case", ["long", "ring", "ring128", "ring128k5"])
 def test_device_payload_exchange_bitwise(case):
     """Halo payloads as CUDA tensors (the NCCL path of shard.Comm: one pack
     kernel, stream-ordered, no host copies): shards in two threads equal the
     undivided run bit for bit.  ring128: 128-node walls, so each shard marches
-    its zone block (a chain with halo zones) through the zone-ring kernel K5."""
+    its zone block (a chain with halo zones) through the zone-ring kernel K4r
+    (ring128k5: K5)."""
     import threading
     import torch
     from paper_1703_10119_b200 import Context, shard, workloads
@@ -146,6 +147,7 @@ def test_device_payload_exchange_bitwise(case):
         model, init = w.model, w.init
     else:
         Z, W, n, steps = (16, 6, 32, 120) if case == "ring" else (48, 6, 128, 100)
+    kname = "ring_pipe" if case == "ring128k5" else "ring_reg"
         w = workloads.zone_ring(n_zones=Z, walls_per_zone=W, n_nodes=n, nsteps=steps)
         rng = np.random.default_rng(5)
         init = {f: w.init[f] + 1e-3 * rng.standard_normal(w.init[f].size) for f in FIELDS}
@@ -161,13 +163,15 @@ def test_device_payload_exchange_bitwise(case):
                 sh.advance(steps)
             else:
                 sh = shard.ZoneRingShard(model, init, comm, Context, walls_per_zone=6, halo=4 if case == "ring" else 12)
-                if case == "ring128":
+                if case.startswith("ring128"):
+                    if case == "ring128k5":
+                        sh.engine.set_tuning("ring_kernel", 3)  # K5 inside the shards
                     sh.engine.profiling(True)
                 sh.bootstrap("implicit")
                 sh.advance(steps - 1)
-                if case == "ring128":
+                if case.startswith("ring128"):
                     sh.engine.synchronize()
-                    assert any(x["name"] == "ring_pipe" for x in sh.engine.kernel_stats())
+                    assert any(x["name"] == kname for x in sh.engine.kernel_stats())
             res[rank] = (sh, sh.owned_state())
         except Exception:
             errs.append(traceback.format_exc())
