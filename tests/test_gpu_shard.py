@@ -147,12 +147,13 @@ def test_device_payload_exchange_bitwise(case):
         model, init = w.model, w.init
     else:
         Z, W, n, steps = (16, 6, 32, 120) if case == "ring" else (48, 6, 128, 100)
-    kname = "ring_pipe" if case == "ring128k5" else "ring_reg"
         w = workloads.zone_ring(n_zones=Z, walls_per_zone=W, n_nodes=n, nsteps=steps)
         rng = np.random.default_rng(5)
         init = {f: w.init[f] + 1e-3 * rng.standard_normal(w.init[f].size) for f in FIELDS}
         init.update(zone_u=w.init["zone_u"], zone_v=w.init["zone_v"])
         model = w.model
+
+    kname = "ring_pipe" if case == "ring128k5" else "ring_reg"
 
     def work(rank):
         try:
