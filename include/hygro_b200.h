@@ -301,6 +301,15 @@ int hyg_run_scheme(hyg_ctx* ctx, int32_t scheme, double horizon, double cadence,
                    void* user, hyg_run_report* report, hyg_status* status);
 
 
+/* df_step_linear (wall.hpp:73-74, wall.cpp:60-71; the single-field DF form of
+ * the paper's Eq. 8, boundary nodes copied) applied `steps` times, with the
+ * layer rotation of wall.cpp:80-83, to n_fields independent fields of n nodes
+ * on the device: prev/curr ([n_fields][n], host or device pointers) hold
+ * layers n-1 and n on entry and the last two layers on return.  The
+ * reference's property tests use this form (test_wall.cpp:43-61, 171-194). */
+int hyg_df_march_linear(int32_t device, int32_t n_fields, int32_t n, double lambda, int64_t steps,
+                        double* prev, double* curr);
+
 /* ---- host-side setup: dimensionless groups (scaling.cpp, materials.cpp) -
  * Coefficient sets are {c_M, k_M, c_TT, k_TT, c_TM, k_TM} (CoefficientSet,
  * materials.hpp:21-28).  Scaling context from (T_i [K], phi_i, t_0 [s]),

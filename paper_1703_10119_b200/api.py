@@ -521,6 +521,18 @@ class Context:
             pass
 
 
+def df_march_linear(prev, curr, lam: float, steps: int, device: int = 0):
+    """df_step_linear (wall.cpp:60-71) `steps` times with layer rotation on the
+    device, for a [fields, n] batch of single fields; returns (prev, curr)."""
+    p = np.array(prev, dtype=np.float64, order="C", ndmin=2)
+    c = np.array(curr, dtype=np.float64, order="C", ndmin=2)
+    if p.shape != c.shape:
+        raise InvalidArgument("prev and curr must have the same shape")
+    _check(load_library().hyg_df_march_linear(device, p.shape[0], p.shape[1], float(lam), int(steps), _ptr(p),
+                                              _ptr(c)), None, "hyg_df_march_linear")
+    return p, c
+
+
 # ---- host-side setup (scaling.cpp) -------------------------------------------------
 def saturation_pressure(T: float) -> float:
     out = C.c_double()

@@ -2403,6 +2403,16 @@ __global__ void k_fastmath(int n, const double* x, double* e, double* r) {
         r[i] = frcp(x[i]);
     }
 }
+// df_step_linear (wall.cpp:60-71) of n_fields independent single fields:
+// next[j] = a0 prev[j] + a1 (curr[j+1] + curr[j-1]) inside, ends copied
+__global__ void k_df_linear(int n_fields, int n, double a0, double a1, const double* prev, const double* curr,
+                            double* next) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= static_cast<int64_t>(n_fields) * n) return;
+    const int j = static_cast<int>(i % n);
+    next[i] = (j == 0 || j == n - 1) ? curr[i] : a0 * prev[i] + a1 * (curr[i + 1] + curr[i - 1]);
+}
+
 __global__ void k_crmath(int n, const double* x, const double* y, double* o) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
@@ -2417,6 +2427,35 @@ __global__ void k_fastlog(int n, const double* x, double* l) {
     if (i < n) l[i] = flog_pos(x[i]);
 }
 }  // namespace
+
+extern "C" int hyg_df_march_linear(int32_t device, int32_t n_fields, int32_t n, double lambda, int64_t steps,
+                                   double* prev, double* curr) {
+    hyg_status* status = nullptr;
+    if (n_fields < 0 || n < 2 || steps < 0 || !prev || !curr) return HYG_EINVAL;
+    if (n_fields == 0 || steps == 0) return HYG_OK;
+    HYG_CUDA(cudaSetDevice(device));
+    const size_t cells = static_cast<size_t>(n_fields) * n, bytes = cells * sizeof(double);
+    double* d = nullptr;
+    HYG_CUDA(cudaMalloc(&d, 3 * bytes));
+    double* L[3] = {d, d + cells, d + 2 * cells};
+    HYG_CUDA(cudaMemcpy(L[0], prev, bytes, cudaMemcpyDefault));
+    HYG_CUDA(cudaMemcpy(L[1], curr, bytes, cudaMemcpyDefault));
+    const double a0 = (1.0 - lambda) / (1.0 + lambda);   // wall.cpp:66-67
+    const double a1 = lambda / (1.0 + lambda);
+    const int grid = static_cast<int>((cells + 255) / 256);
+    for (int64_t k = 0; k < steps; ++k) {                // rotate (wall.cpp:80-83) by renaming
+        k_df_linear<<<grid, 256>>>(n_fields, n, a0, a1, L[0], L[1], L[2]);
+        double* t = L[0];
+        L[0] = L[1];
+        L[1] = L[2];
+        L[2] = t;
+    }
+    HYG_CUDA(cudaGetLastError());
+    HYG_CUDA(cudaMemcpy(prev, L[0], bytes, cudaMemcpyDefault));
+    HYG_CUDA(cudaMemcpy(curr, L[1], bytes, cudaMemcpyDefault));
+    cudaFree(d);
+    return HYG_OK;
+}
 
 extern "C" int hyg_selftest_crmath(int32_t device, int32_t n, const double* x, const double* y, double* out) {
     hyg_status* status = nullptr;
