@@ -68,6 +68,7 @@ constexpr int kRingRegThreads = HYG_RING_REG_THREADS;
 template <int NPT, int S>
 struct RingRegShape {
     static constexpr int kP = S + 1;                           // nodes kept per halo wall
+    static constexpr int kPS = (kP + 1) & ~1;                   // their staging slot (even: 16-byte copies)
     static constexpr int kHaloZones = 2 * (S - 1);
     // shared stride of a zone's parameter block: odd, so the zone warp's lanes
     // (one zone each) read distinct banks (56 put every lane on two banks)
@@ -84,7 +85,7 @@ struct RingRegShape {
     // per owned warp an output scratch [2 fields][2 walls][n] for its bulk stores
     __host__ __device__ static size_t smem_doubles(int B, int W, int n, int rw) {
         const size_t LB = local_zones(B);
-        return static_cast<size_t>(4) * B * W * n + static_cast<size_t>(4) * halo_walls(W) * kP +
+        return static_cast<size_t>(4) * B * W * n + static_cast<size_t>(4) * halo_walls(W) * kPS +
                2 * LB * kZPS + 4 * LB + 4 * static_cast<size_t>(B * W + halo_walls(W)) + 4 * LB +
                ((static_cast<size_t>(S) * rw + 1) & ~static_cast<size_t>(1)) + 2 +
                static_cast<size_t>(own_warps(B, W)) * 2 * 2 * n;
@@ -129,7 +130,7 @@ __device__ __forceinline__ void cp_async16(double* smem_dst, const double* gsrc)
 template <int NPT, int S, int NL = kRingMaxLinks, int NP = kRingMaxPeers>
 __global__ void __launch_bounds__(kRingRegThreads, 1) k_ring_reg(const RingArgs a) {
     using Sh = RingRegShape<NPT, S>;
-    constexpr int P = Sh::kP, N = 16 * NPT;
+    constexpr int P = Sh::kP, PS = Sh::kPS, N = 16 * NPT;
     constexpr unsigned FULL = 0xffffffffu;
     extern __shared__ double smem[];
     if (launch_stopped(a.stop)) return;
@@ -138,9 +139,9 @@ __global__ void __launch_bounds__(kRingRegThreads, 1) k_ring_reg(const RingArgs 
     const int rw = RingShape<NPT, S>::row_width(a.n_channels, a.n_sources);
     // shared layout (integer offsets; every access a shared-space access)
     const int oSO = 0;                                  // staging owned [4][OW][N] (linear: bulk copies)
-    const int oSH = oSO + 4 * OW * N;                   // staging halo [4][HW][P]
+    const int oSH = oSO + 4 * OW * N;                   // staging halo [4][HW][PS] (last PS nodes)
     constexpr int ZPS = Sh::kZPS;
-    const int oZS = oSH + 4 * HW * P;                   // staged zone parameters [2][LB][ZPS]
+    const int oZS = oSH + 4 * HW * PS;                  // staged zone parameters [2][LB][ZPS]
     const int oZA = oZS + 2 * LB * ZPS;                 // staged zone air [2][2][LB]
     const int oSF = oZA + 4 * LB;                       // surfaces [parity][field][OW + HW]
     const int oAR = oSF + 4 * (OW + HW);                // zone air [parity][field][LB]
@@ -192,12 +193,12 @@ __global__ void __launch_bounds__(kRingRegThreads, 1) k_ring_reg(const RingArgs 
             asm volatile("cp.async.commit_group;\n" ::);
             return;
         }
-        for (int i = tid; i < HW * P; i += nthr) {
-            const int hl = i / P, p = i - hl * P;
+        for (int i = tid; i < HW * (PS / 2); i += nthr) {   // the last PS nodes, 16-byte pieces
+            const int hl = i / (PS / 2), c = i - hl * (PS / 2);
             const int hz = hl / W, wi = hl - hz * W;
-            const size_t g = (static_cast<size_t>(gz(z0, halo_local(hz, nown))) * W + wi) * N + (N - P + p);
+            const size_t g = (static_cast<size_t>(gz(z0, halo_local(hz, nown))) * W + wi) * N + (N - PS) + 2 * c;
 #pragma unroll
-            for (int f = 0; f < 4; ++f) cp_async8(&smem[oSH + f * HW * P + i], a.in[f] + g);
+            for (int f = 0; f < 4; ++f) cp_async16(&smem[oSH + (f * HW + hl) * PS + 2 * c], a.in[f] + g);
         }
         for (int i = tid; i < L * kRingZP; i += nthr) {
             const int li = i / kRingZP, c = i - li * kRingZP;
@@ -449,11 +450,11 @@ __global__ void __launch_bounds__(kRingRegThreads, 1) k_ring_reg(const RingArgs 
             double up[P], uc[P], vp[P], vc[P];
 #pragma unroll
             for (int p = 0; p < P; ++p) {
-                const int d = hlc * P + p;
-                up[p] = smem[oSH + 0 * HW * P + d];
-                uc[p] = smem[oSH + 1 * HW * P + d];
-                vp[p] = smem[oSH + 2 * HW * P + d];
-                vc[p] = smem[oSH + 3 * HW * P + d];
+                const int d = hlc * PS + (PS - P) + p;
+                up[p] = smem[oSH + 0 * HW * PS + d];
+                uc[p] = smem[oSH + 1 * HW * PS + d];
+                vp[p] = smem[oSH + 2 * HW * PS + d];
+                vc[p] = smem[oSH + 3 * HW * PS + d];
             }
             __syncthreads();                             // (A)
             if (next) prefetch(b + gridDim.x, par ^ 1);
@@ -536,6 +537,22 @@ __global__ void __launch_bounds__(kRingRegThreads, 1) k_ring_reg(const RingArgs 
                 smem[ar_ix(0, 0, i)] = smem[oZA + (par * 2 + 0) * LB + i];
                 smem[ar_ix(0, 1, i)] = smem[oZA + (par * 2 + 1) * LB + i];
             }
+            // the parameter block in registers for the whole block (the step loop
+            // then loads only states: layer-k air of the zone and peers, samples)
+            const double c0 = smem[zp + 0], gv = smem[zp + 1], qv1 = smem[zp + 2], qv2 = smem[zp + 3];
+            double lT[NL], lM[NL], lD[NL], pg[NP], pq1[NP], pq2[NP];
+#pragma unroll
+            for (int q = 0; q < NL; ++q) {
+                lT[q] = smem[zp + 9 + 4 * q];
+                lM[q] = smem[zp + 10 + 4 * q];
+                lD[q] = smem[zp + 11 + 4 * q];
+            }
+#pragma unroll
+            for (int q = 0; q < NP; ++q) {
+                pg[q] = smem[zp + 41 + 4 * q];
+                pq1[q] = smem[zp + 42 + 4 * q];
+                pq2[q] = smem[zp + 43 + 4 * q];
+            }
             ZPROF(0);
             __syncthreads();                             // (A) staging consumed
             if (next) prefetch(b + gridDim.x, par ^ 1);
@@ -547,25 +564,24 @@ __global__ void __launch_bounds__(kRingRegThreads, 1) k_ring_reg(const RingArgs 
                     const int srow = oRW + k * rw + 4 * a.n_channels;
                     const int sz = srow + 3 * sidx;
                     const double u_inf = smem[srow + 3 * a.n_sources + 0], v_inf = smem[srow + 3 * a.n_sources + 1];
-                    double du = smem[sz + 1] + smem[sz + 2] + smem[zp + 2] * (u_inf * v_inf - u_a * v_a) +
-                                smem[zp + 3] * (u_inf - u_a);
-                    double dv = smem[sz + 0] + smem[zp + 1] * (v_inf - v_a);
+                    double du = smem[sz + 1] + smem[sz + 2] + qv1 * (u_inf * v_inf - u_a * v_a) + qv2 * (u_inf - u_a);
+                    double dv = smem[sz + 0] + gv * (v_inf - v_a);
                     // branch-free over the maximum link/peer counts: the unused slots of
                     // the parameter block are zero (their terms add +0), so every load
                     // is independent and only the additions stay in order
 #pragma unroll
                     for (int q = 0; q < NP; ++q) {
                         const double pu = smem[ar_ix(cur, 0, pidx[q])], pv = smem[ar_ix(cur, 1, pidx[q])];
-                        du += smem[zp + 42 + 4 * q] * (pu * pv - u_a * v_a) + smem[zp + 43 + 4 * q] * (pu - u_a);
-                        dv += smem[zp + 41 + 4 * q] * (pv - v_a);
+                        du += pq1[q] * (pu * pv - u_a * v_a) + pq2[q] * (pu - u_a);
+                        dv += pg[q] * (pv - v_a);
                     }
 #pragma unroll
                     for (int q = 0; q < NL; ++q) {
                         const double us = smem[sf_ix(cur, 0, ls[q])], vs = smem[sf_ix(cur, 1, ls[q])];
-                        du += smem[zp + 9 + 4 * q] * (us - u_a) + smem[zp + 10 + 4 * q] * (vs - v_a);
-                        dv += smem[zp + 11 + 4 * q] * (v_a - vs);
+                        du += lT[q] * (us - u_a) + lM[q] * (vs - v_a);
+                        dv += lD[q] * (v_a - vs);
                     }
-                    const double nu = u_a + a.dt * (du / smem[zp + 0]);
+                    const double nu = u_a + a.dt * (du / c0);
                     const double nv = v_a + a.dt * dv;
                     smem[ar_ix(cur ^ 1, 0, i)] = nu;
                     smem[ar_ix(cur ^ 1, 1, i)] = nv;
