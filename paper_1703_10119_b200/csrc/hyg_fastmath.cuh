@@ -102,6 +102,9 @@ __device__ __forceinline__ double frcp(double d) {
 // a dependent FMA less than fexp): |kd L_double - kd ln2/64| <= |kd| 8.7e-19,
 // i.e. <= 5e-16 relative in the result for |x| <= 40 (d(v) of configs[0]/[4]:
 // |x| <= 6.4) and <= 6e-14 at x = -708, where the term is ~1e-308.
+// STRIDE: the table's element stride (16: the bank-replicated copy of
+// k_dv_warp.cuh, each lane reading its own copy)
+template <int STRIDE = 1>
 __device__ __forceinline__ double fexp_addend(double x, const double* tab) {
     constexpr double kShift = 6755399441055744.0;                  // 1.5 * 2^52
     constexpr double kInvL = 92.332482616893658;                   // 64 / ln 2
@@ -116,7 +119,7 @@ __device__ __forceinline__ double fexp_addend(double x, const double* tab) {
     const double c23 = fma(r, 1.0 / 6.0, 0.5);
     const double q = fma(r2, c45, c23);
     const double sm = fma(r2, q, r);
-    const double t = tab[k & 63];
+    const double t = tab[(k & 63) * STRIDE];
     const double ts = __hiloint2double(__double2hiint(t) + static_cast<int>(static_cast<unsigned>(k >> 6) << 20),
                                        __double2loint(t));
     return fma(ts, sm, ts);

@@ -80,7 +80,7 @@ __device__ __forceinline__ DvParams dv_params(const double* p, double a2) {
 
 __device__ __forceinline__ double d_half(const DvParams& q, double sum, const double* tab) {
     const double e = fma(q.hsq, sum, q.nsqp3);
-    const double E = fexp_addend(-(e * e), tab);
+    const double E = fexp_addend<kExpRep>(-(e * e), tab);
     return fma(q.p1, E, fma(q.hp0, sum, q.one));
 }
 
@@ -89,7 +89,7 @@ __device__ __forceinline__ double d_half(const DvParams& q, double sum, const do
 // the compiler's schedule of the three exps per lane differs.
 __device__ __forceinline__ double d_half_lat(const DvParams& q, double sum, const double* tab) {
     const double e = fma(0.5, sum, -q.p3);
-    const double E = fexp_addend((q.np2 * e) * e, tab);
+    const double E = fexp_addend<kExpRep>((q.np2 * e) * e, tab);
     return fma(q.p1, E, fma(q.hp0, sum, q.one));
 }
 
@@ -239,10 +239,11 @@ constexpr int kK3MinB = 3;
 // (Lr = (n-1)/NPT, the reversed lane).
 template <int NPT, int M>
 __global__ void __launch_bounds__(kDvWarps * 32) k_dv_walls(const NonlinearSegArgs A) {
-    __shared__ double s_tab[64];
+    __shared__ double s_tab_rep[64 * kExpRep];
+    const double* s_tab = s_tab_rep + (threadIdx.x & (kExpRep - 1));   // this lane's copy
     __shared__ Ambient s_amb[kDvWarps][kNlChunk][2];   // [warp][step][face]
     if (launch_stopped(A.stop)) return;
-    stage_exp_table(s_tab, threadIdx.x, blockDim.x);
+    stage_exp_table_rep(s_tab_rep, threadIdx.x, blockDim.x);
     __syncthreads();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int w = blockIdx.x * kDvWarps + warp;
@@ -318,11 +319,12 @@ __global__ void __launch_bounds__(kDvWarps * 32) k_dv_walls(const NonlinearSegAr
 template <int NW>
 __global__ void __launch_bounds__(NW * 32) k_dv_wall_split(const NonlinearSegArgs A) {
     constexpr bool FACE_ALL = NW <= 4;                 // every warp runs the face code: no branch
-    __shared__ double s_tab[64];
+    __shared__ double s_tab_rep[64 * kExpRep];
+    const double* s_tab = s_tab_rep + (threadIdx.x & (kExpRep - 1));   // this lane's copy
     __shared__ Ambient s_amb[kNlChunk][2];
     __shared__ double s_x[2][NW][4];                  // [parity][warp] {v, u} of lanes 0 and 31
     if (launch_stopped(A.stop)) return;
-    stage_exp_table(s_tab, threadIdx.x, blockDim.x);
+    stage_exp_table_rep(s_tab_rep, threadIdx.x, blockDim.x);
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
     const int w = blockIdx.x, n = A.n, j = tid;
     const bool live = j < n;
@@ -399,11 +401,12 @@ __global__ void __launch_bounds__(NW * 32) k_dv_wall_split(const NonlinearSegArg
 template <int NW, int H>
 __global__ void __launch_bounds__(NW * 32) k_dv_wall_halo(const NonlinearSegArgs A) {
     constexpr int T = 32 - 2 * H;                      // owned nodes per warp
-    __shared__ double s_tab[64];
+    __shared__ double s_tab_rep[64 * kExpRep];
+    const double* s_tab = s_tab_rep + (threadIdx.x & (kExpRep - 1));   // this lane's copy
     __shared__ Ambient s_amb[kNlChunk][2];
     __shared__ double s_st[4][NW * T];                 // {u_prev, u_curr, v_prev, v_curr} by node
     if (launch_stopped(A.stop)) return;
-    stage_exp_table(s_tab, threadIdx.x, blockDim.x);
+    stage_exp_table_rep(s_tab_rep, threadIdx.x, blockDim.x);
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
     const int w = blockIdx.x, n = A.n, j = warp * T - H + lane;
     const bool live = j >= 0 && j < n;
@@ -492,9 +495,10 @@ template <int NPT, bool FACES>
 __global__ void __launch_bounds__(kDvWarps * 32) k_dv_tiled(const TiledArgs A) {
     using G = DvTiles<NPT>;
     constexpr int W = G::W, T = G::T;
-    __shared__ double s_tab[64];
+    __shared__ double s_tab_rep[64 * kExpRep];
+    const double* s_tab = s_tab_rep + (threadIdx.x & (kExpRep - 1));   // this lane's copy
     if (launch_stopped(A.stop)) return;
-    stage_exp_table(s_tab, threadIdx.x, blockDim.x);
+    stage_exp_table_rep(s_tab_rep, threadIdx.x, blockDim.x);
     __syncthreads();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int64_t n = A.n;
@@ -576,10 +580,11 @@ __global__ void __launch_bounds__(kDvWarps * 32, MINB) k_dv_tiled_stream(const T
     using G = DvTiles<NPT>;
     constexpr int W = G::W, T = G::T;
     static_assert((NPT & (NPT - 1)) == 0, "NPT must be a power of two");
-    __shared__ double s_tab[64];
+    __shared__ double s_tab_rep[64 * kExpRep];
+    const double* s_tab = s_tab_rep + (threadIdx.x & (kExpRep - 1));   // this lane's copy
     __shared__ __align__(16) double s_buf[kDvWarps][4][W];
     if (launch_stopped(A.stop)) return;
-    stage_exp_table(s_tab, threadIdx.x, blockDim.x);
+    stage_exp_table_rep(s_tab_rep, threadIdx.x, blockDim.x);
     __syncthreads();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int64_t tr = G::rface(A.n);

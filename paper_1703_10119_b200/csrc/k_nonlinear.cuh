@@ -57,6 +57,15 @@ __device__ __forceinline__ void stage_exp_table(double* s_tab, int tid, int nthr
     for (int i = tid; i < 64; i += nthreads) s_tab[i] = kExp2Tab64[i];
 }
 
+// The exp table replicated 16 times, entry j of copy c at j * 16 + c: lane l
+// reads copy l & 15, so the 64-bit reads of a half warp hit 16 distinct bank
+// pairs whatever the indices (the single 64-entry table put ~4-5 lanes on one
+// bank pair: ncu counted ~3.8e7 shared-memory bank conflicts per K3w launch)
+constexpr int kExpRep = 16;
+__device__ __forceinline__ void stage_exp_table_rep(double* s_tab, int tid, int nthreads) {
+    for (int i = tid; i < 64 * kExpRep; i += nthreads) s_tab[i] = kExp2Tab64[i / kExpRep];
+}
+
 constexpr int kNlChunk = 64;   // forcing rows staged per chunk
 
 // Per-wall scalars of the d(v) rows (wall.cpp:199-204).

@@ -28,6 +28,8 @@ full() {  # cfg steps kernel skip
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$3 -s $4 -c 1 -o $O/full_$1 python tools/profile_target.py $1 $2 > $O/ncu_f_$1.log 2>&1
   ncu -i $O/full_$1.ncu-rep --page raw --csv > $O/raw_$1.csv 2>/dev/null
   python tools/ncu_lines.py $O/full_$1.ncu-rep 30 > $O/lines_$1.txt 2>&1
+  python tools/ncu_summary.py $O $1 > $O/summary_$1.txt 2>&1
+  rm -f $O/full_$1.ncu-rep            # gpurun copies back <= 64 MiB
 }
 for c in "cfg1 4097" "cfg2 4097" "cfg0 4097" "cfg3 41" "cfg4 33" "cfg5 11"; do
   set -- $c
