@@ -54,7 +54,7 @@ CONFIGS = {
     # (--ring-kernel 3, k_ring_pipe.cuh: B = 3, S = 12, halo trimmed to the cone):
     # (64 B x 2304 + 32 B x 864) / (2304 x 12) = 6.33 B/update
     "cfg3": dict(flop=14.1, bytes=8.98, bound="hbm", kernel="ring_reg", scaling="strong", dtype="f64",
-                 run_steps=80_000, bytes_by_kernel={"ring_pipe": 6.33, "ring_reg": 8.98}),
+                 run_steps=80_000, bytes_by_kernel={"ring_pipe": 6.33, "ring_reg": 8.98, "ring_walls": 8.40}),
     # cfg4 runs the temporally blocked K3w (k_dv_warp.cuh: 256-node windows, 8 steps
     # per launch, (32 x 256 + 32 x 240) / (240 x 8) = 8.27 B/update), so min(HBM,
     # FP64) is the FP64 side; sharded (N>1) every slab runs K3w too
@@ -83,7 +83,7 @@ def parse():
     p.add_argument("--material-walls", type=int, default=16384)
     p.add_argument("--halo", type=int, default=0, help="shard halo depth (0: config default)")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--ring-kernel", type=int, default=0, help="cfg3: 0 auto (K4r), 1 K4r, 2 K4, 3 K5 (A/B runs)")
+    p.add_argument("--ring-kernel", type=int, default=0, help="cfg3: 0 auto (K6), 1 K4r, 2 K4, 3 K5, 4 K6 (A/B runs)")
     p.add_argument("--material-exact", action="store_true",
                    help="cfg5: the parity material evaluation (hyg_crmath.cuh) instead of the default fast one")
     p.add_argument("--no-e2e", action="store_true")

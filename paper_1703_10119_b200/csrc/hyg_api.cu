@@ -29,6 +29,7 @@
 #include "k_ring.cuh"
 #include "k_ring_reg.cuh"
 #include "k_ring_pipe.cuh"
+#include "k_ring_split.cuh"
 
 using namespace hyg;
 
@@ -44,6 +45,14 @@ constexpr int kRingRegS = HYG_RING_REG_S;   // K4r: steps per launch (S = 9 meas
 #define HYG_RING_PIPE_S 12
 #endif
 constexpr int kRingPipeS = HYG_RING_PIPE_S; // K5: steps per launch
+#ifndef HYG_RING_SPLIT_S
+#define HYG_RING_SPLIT_S 8
+#endif
+#ifndef HYG_RING_AUTO
+#define HYG_RING_AUTO 4
+#endif
+constexpr int kRingAuto = HYG_RING_AUTO;         // the zone-ring kernel HYG_TUNE_RING_KERNEL = 0 selects (4: K6, 1: K4r)
+constexpr int kRingSplitS = HYG_RING_SPLIT_S;   // K6 (k_ring_split.cuh): steps per launch pair
 constexpr int kWarps = 4;       // warps per CTA of K1
 
 struct SigHost {
@@ -217,7 +226,9 @@ struct hyg_ctx {
     int ring_reg_B = 0;              // K4r (registers + prefetch): zones per CTA, 0 if not applicable
     int ring_grid_cap = 0;           // HYG_TUNE_RING_GRID: K4r/K5 persistent grid cap (0: one CTA per SM)
     int ring_pipe_B = 0;             // K5 (k_ring_pipe.cuh): zones per block, 0 if not applicable
-    int ring_kernel = 0;             // HYG_TUNE_RING_KERNEL: 0 auto (K4r), 1 K4r, 2 K4, 3 K5
+    int ring_kernel = 0;             // HYG_TUNE_RING_KERNEL: 0 auto (K6), 1 K4r, 2 K4, 3 K5, 4 K6
+    int ring_cone_LB = 0;            // K6 phase 1: local zones per CTA (owned + 2 S halo), 0 if not applicable
+    double* d_ring_series = nullptr; // K6: layer-k air of every zone for the S steps of a launch [zones][S][2]
     bool mat_exact = false;          // HYG_TUNE_MATERIAL_EXACT: CrMath evaluation + IEEE-division rows
     bool owned_partial = false;      // hyg_set_owned narrowed the guard to a shard's range
     int ring_dbg_skip = 0;           // HYG_DEBUG_RING_SKIP (timing experiments only; wrong results)
@@ -1093,6 +1104,25 @@ void launch_ring_pipe(const RingArgs& a, size_t smem, cudaStream_t s, int device
     k<<<grid, Sh::threads(a.B, a.W), smem, s>>>(a);
 }
 
+// K6 (k_ring_split.cuh): phase 1 (zone air + wall cones, records the air series),
+// then phase 2 (every wall in registers, no barrier per step)
+void launch_ring_cone(const RingArgs& a, double* series, int LB, bool small, cudaStream_t s, int device) {
+    using Sh = RingConeShape<kRingSplitS>;
+    auto k = small ? k_ring_cone<kRingSplitS, 6, 2> : k_ring_cone<kRingSplitS>;
+    const int rw = RingShape<8, kRingSplitS>::row_width(a.n_channels, a.n_sources);
+    const size_t smem = Sh::smem_doubles(LB, a.W, rw) * sizeof(double);
+    ensure_smem_attr(k, device, 227 * 1024);
+    const int OB = LB - 2 * kRingSplitS;
+    k<<<(a.n_zones + OB - 1) / OB, Sh::threads(LB, a.W), smem, s>>>(a, series, LB);
+}
+
+template <int NPT>
+void launch_ring_walls(const RingArgs& a, const double* series, cudaStream_t s) {
+    const size_t smem = (static_cast<size_t>(kRingSplitS) * 4 * a.n_channels + kRingWallWarps * 2 * 2 * kRingSplitS) * sizeof(double);
+    const int walls = a.n_zones * a.W, per_cta = 2 * kRingWallWarps;
+    k_ring_walls<NPT, kRingSplitS><<<(walls + per_cta - 1) / per_cta, 32 * kRingWallWarps, smem, s>>>(a, series);
+}
+
 template <int NPT>
 void launch_ring(const RingArgs& a, int grid, int threads, size_t smem, cudaStream_t s, int device) {
     auto k = k_ring_tiled<NPT, kRingS>;
@@ -1103,8 +1133,11 @@ void launch_ring(const RingArgs& a, int grid, int threads, size_t smem, cudaStre
 int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool reg = true) {
     // K4r by default; K5 (pipelined, S = 12, HYG_TUNE_RING_KERNEL = 3) measured slower
     // (2.8e11 vs 3.4e11: the per-step critical path binds, not HBM)
-    const bool pipe = reg && c->ring_pipe_B > 0 && c->norm >= 2.0 && c->ring_kernel == 3;
-    if (c->ring_kernel == 2) reg = false;
+    const int rk = c->ring_kernel == 0 ? kRingAuto : c->ring_kernel;
+    const bool pipe = reg && c->ring_pipe_B > 0 && c->norm >= 2.0 && rk == 3;
+    // K6: the split march (no per-step barrier on the walls' path), the default
+    const bool split = reg && c->ring_cone_LB > 0 && c->norm >= 2.0 && rk == 4;
+    if (rk == 2) reg = false;
     if (c->coef_dt != dt) {
         LaunchScope ls(c, "coupled_coef", 0.0);
         k_coupled_coef<<<(c->n_walls + 127) / 128, 128, 0, c->stream>>>(c->n_walls, c->dx, dt, c->d_groups,
@@ -1120,7 +1153,7 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool
     const int B = pipe ? c->ring_pipe_B : reg ? c->ring_reg_B : c->ring_B;
     const int grid = (Z + B - 1) / B;
     const int rw = RingShape<8, kRingS>::row_width(nch, nsrc);
-    const int S = pipe ? kRingPipeS : reg ? kRingRegS : kRingS;   // steps per launch
+    const int S = split ? kRingSplitS : pipe ? kRingPipeS : reg ? kRingRegS : kRingS;   // steps per launch
     const int threads = reg ? RingRegShape<8, kRingRegS>::threads(B, W) : RingShape<8, kRingS>::threads(B, W);
     const size_t smem = pipe ? RingPipeShape<kRingPipeS>::smem_doubles(B, W, rw) * sizeof(double)
                         : reg ? RingRegShape<8, kRingRegS>::smem_doubles(B, W, c->n, rw) * sizeof(double)
@@ -1175,6 +1208,16 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool
             a.zv_in = c->zv[zf];
             a.zu_out = c->zu[1 - zf];
             a.zv_out = c->zv[1 - zf];
+            if (split) {
+                {
+                    LaunchScope ls(c, "ring_cone", 0.0);
+                    launch_ring_cone(a, c->d_ring_series, c->ring_cone_LB, c->ring_reg_small, c->stream, c->device);
+                }
+                LaunchScope ls(c, "ring_walls", static_cast<double>(c->cells()) * a.steps);
+                if (npt == 4) launch_ring_walls<4>(a, c->d_ring_series, c->stream);
+                else launch_ring_walls<8>(a, c->d_ring_series, c->stream);
+                continue;
+            }
             LaunchScope ls(c, pipe ? "ring_pipe" : reg ? "ring_reg" : "ring_tiled", static_cast<double>(c->cells()) * a.steps);
             if (pipe) {
                 launch_ring_pipe(a, smem, c->stream, c->device, c->ring_grid_cap);
@@ -1527,6 +1570,23 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
                 };
                 while (Bp > 0 && !fits_p(Bp)) --Bp;
                 c->ring_pipe_B = Bp;
+                // K6 phase 1: LB local zones per CTA (LB - 2 S owned); about one CTA per
+                // SM for long rings, never fewer than min(Z, 8) owned zones
+                using SC = RingConeShape<kRingSplitS>;
+                if (c->n >= 2 * (kRingSplitS + 2)) {
+                    const int rw = RingShape<8, kRingSplitS>::row_width(nch, nsrc);
+                    int lb = 2 * kRingSplitS + 1;
+                    while (SC::threads(lb + 1, W) <= kRingConeThreads &&
+                           SC::smem_doubles(lb + 1, W, rw) * sizeof(double) <= 200u * 1024u)
+                        ++lb;
+                    if (SC::threads(lb, W) <= kRingConeThreads) {
+                        const int nsm = sm_count(c->device);
+                        int ob = (Z + nsm - 1) / nsm;
+                        ob = std::max(ob, std::min(Z, 8));
+                        ob = std::min(ob, lb - 2 * kRingSplitS);
+                        c->ring_cone_LB = ob + 2 * kRingSplitS;
+                    }
+                }
             }
             if (B >= 1) {
                 c->ring = true;
@@ -1650,6 +1710,9 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
                 }
             }
             if (cudaMalloc(&c->d_ring_zp, sizeof(double) * zp.size()) != cudaSuccess) return fail("zone alloc");
+            if (c->ring_cone_LB > 0 &&
+                cudaMalloc(&c->d_ring_series, sizeof(double) * c->zones.size() * kRingSplitS * 2) != cudaSuccess)
+                return fail("zone alloc");
             cudaMemcpy(c->d_ring_zp, zp.data(), sizeof(double) * zp.size(), cudaMemcpyHostToDevice);
         }
     }
@@ -1695,6 +1758,7 @@ void hyg_destroy(hyg_ctx* c) {
     cudaFree(c->d_zlinks);
     cudaFree(c->d_inz);
     cudaFree(c->d_ring_zp);
+    cudaFree(c->d_ring_series);
     cudaFree(c->d_table);
     cudaFree(c->d_boot);
     cudaFree(c->d_src);
@@ -2338,7 +2402,7 @@ int hyg_set_tuning(hyg_ctx* c, int32_t knob, int64_t value) {
     switch (knob) {
         case HYG_TUNE_RING_GRID: c->ring_grid_cap = static_cast<int>(std::min<int64_t>(value, INT32_MAX)); return HYG_OK;
         case HYG_TUNE_RING_KERNEL:
-            if (value > 3) return HYG_EINVAL;
+            if (value > 4) return HYG_EINVAL;
             c->ring_kernel = static_cast<int>(value);
             return HYG_OK;
         case HYG_TUNE_MATERIAL_EXACT:

@@ -32,7 +32,7 @@ def _same(a, b, keys=KEYS):
     return all(np.array_equal(a[k], b[k]) for k in keys)
 
 
-@pytest.mark.parametrize("kernel", [1, 3])
+@pytest.mark.parametrize("kernel", [0, 1, 3])
 def test_ring_kernels_repeatable_across_grids(kernel):
     w = workloads.zone_ring(n_zones=50, walls_per_zone=6, n_nodes=128, nsteps=150)
     rng = np.random.default_rng(11)

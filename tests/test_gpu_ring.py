@@ -1,5 +1,7 @@
-"""K4 (k_ring.cuh), K4r (k_ring_reg.cuh: owned walls in registers,
-persistent prefetching CTAs, fast guard; the default for 64/128-node walls)
+"""K6 (k_ring_split.cuh: the march split along its dependency cone — zone air
+and wall cones first, then every wall in registers with no barrier per step;
+the default for 64/128-node walls), K4 (k_ring.cuh), K4r (k_ring_reg.cuh:
+owned walls in registers, persistent prefetching CTAs, fast guard; knob 1)
 and K5 (k_ring_pipe.cuh, by the tuning knob: S = 12, trimmed halo, named-
 barrier hand-off, producer warp): the zone-ring building march temporally
 blocked with halo zones, against the C oracle's whole-building run
@@ -63,14 +65,16 @@ def _compare(got, b, n_zones):
 # run only when a CTA owns more than one block.  The grid cap forces that in
 # small rings: 42 zones = 11 blocks (the last one partial, 2 zones) over 3
 # CTAs walk 4/4/3 blocks; 64 zones over 2 CTAs walk 8 blocks each.
-@pytest.mark.parametrize("kernel,name", [(0, "ring_reg"), (3, "ring_pipe")])
+@pytest.mark.parametrize("kernel,name", [(0, "ring_walls"), (1, "ring_reg"), (3, "ring_pipe")])
 @pytest.mark.parametrize("n_zones,cap,steps", [(42, 3, 203), (64, 2, 160), (42, 1, 77), (13, 2, 96)])
 def test_ring_reg_multi_block_per_cta(n_zones, cap, steps, kernel, name):
     w = workloads.zone_ring(n_zones=n_zones, walls_per_zone=6, n_nodes=128, nsteps=steps)
     init = _noisy(w, n_zones + cap)
     got, st, stats = _gpu(w.model, init, steps, grid_cap=cap, kernel=kernel)
     assert stats.get(name, {}).get("launches", 0) > 0, stats.keys()
-    assert "ring_tiled" not in stats                 # no guard hand-over: K4r marched every launch
+    assert "ring_tiled" not in stats                 # no guard hand-over: the kernel marched every launch
+    if kernel == 0:
+        assert stats.get("ring_cone", {}).get("launches", 0) == stats["ring_walls"]["launches"]
     b, rc, _, passes = _oracle(w.model, init, steps, nthreads=O.threads())
     assert rc == 0 and st.subiterations == passes
     err, zerr = _compare(got, b, n_zones)
@@ -80,18 +84,22 @@ def test_ring_reg_multi_block_per_cta(n_zones, cap, steps, kernel, name):
 
 def test_ring_cfg3_full_ring_1000_steps():
     """configs[3] at its BASELINE shape: 8,192 zones x 6 walls x 128 nodes
-    through K4r (about 14 blocks per persistent CTA) for 1,000 steps, against
-    the oracle's building run (threaded, bitwise the serial one):
-    relative L-infinity <= 1e-10 over walls and zones."""
+    through K6 (the default), K4r (about 14 blocks per persistent CTA) and K5
+    for 1,000 steps — bitwise equal to one another — against the oracle's
+    building run (threaded, bitwise the serial one): relative L-infinity <=
+    1e-10 over walls and zones."""
     steps = 1000
     w = workloads.zone_ring(n_zones=8192, walls_per_zone=6, n_nodes=128, nsteps=steps)
     init = _noisy(w, 8192)
     got, st, stats = _gpu(w.model, init, steps)
-    assert stats.get("ring_reg", {}).get("launches", 0) > 0, stats.keys()
-    assert "ring_tiled" not in stats
+    assert stats.get("ring_walls", {}).get("launches", 0) > 0, stats.keys()
+    assert "ring_tiled" not in stats and "ring_reg" not in stats
+    got_r, _, stats_r = _gpu(w.model, init, steps, kernel=1)          # K4r on the same input
+    assert stats_r.get("ring_reg", {}).get("launches", 0) > 0 and "ring_tiled" not in stats_r
     got_p, _, stats_p = _gpu(w.model, init, steps, kernel=3)          # K5 on the same input
     assert stats_p.get("ring_pipe", {}).get("launches", 0) > 0
     for k in ("u_prev", "u_curr", "v_prev", "v_curr", "zone_u", "zone_v"):
+        assert np.array_equal(got[k], got_r[k]), k                       # K6 == K4r bit for bit
         assert np.array_equal(got[k], got_p[k]), k                       # K5 == K4r bit for bit
     b, rc, _, passes = _oracle(w.model, init, steps, nthreads=O.threads())
     assert rc == 0 and st.subiterations == passes
@@ -100,15 +108,16 @@ def test_ring_cfg3_full_ring_1000_steps():
     assert err <= TOL and zerr <= TOL
 
 
-@pytest.mark.parametrize("cap", [0, 5])
-def test_ring_64_zones_full_horizon(cap):
-    """A 64-zone ring at configs[3]'s full 8e4 steps (80 h) through K4r, with
-    the default grid (16 CTAs, one block each) and capped at 5 CTAs."""
+@pytest.mark.parametrize("cap,kernel,name", [(0, 0, "ring_walls"), (0, 1, "ring_reg"), (5, 1, "ring_reg")])
+def test_ring_64_zones_full_horizon(cap, kernel, name):
+    """A 64-zone ring at configs[3]'s full 8e4 steps (80 h) through K6 and
+    through K4r with the default grid (16 CTAs, one block each) and capped at
+    5 CTAs."""
     steps = 80_000
     w = workloads.zone_ring(n_zones=64, walls_per_zone=6, n_nodes=128, nsteps=steps)
     init = _noisy(w, 64)
-    got, st, stats = _gpu(w.model, init, steps, grid_cap=cap)
-    assert stats.get("ring_reg", {}).get("launches", 0) > 0
+    got, st, stats = _gpu(w.model, init, steps, grid_cap=cap, kernel=kernel)
+    assert stats.get(name, {}).get("launches", 0) > 0
     b, rc, _, passes = _oracle(w.model, init, steps, nthreads=O.threads())
     assert rc == 0 and st.subiterations == passes
     err, zerr = _compare(got, b, 64)
@@ -125,7 +134,7 @@ def test_ring_matches_oracle(n_zones, wpz, n, steps):
     init = {k: v + (2e-3 * rng.standard_normal(v.size) if k in ("u_prev", "u_curr", "v_prev", "v_curr") else 0)
             for k, v in w.init.items()}
     got, st, stats = _gpu(w.model, init, steps)
-    kern = "ring_reg" if n <= 128 else "ring_tiled"
+    kern = "ring_walls" if n <= 128 else "ring_tiled"
     assert stats.get(kern, {}).get("launches", 0) > 0, stats.keys()
     b, rc, _, passes = _oracle(w.model, init, steps)
     assert rc == 0 and st.subiterations == passes
@@ -142,7 +151,7 @@ def test_ring_chain_without_wrap():
     zs[0].interzone = [l for l in zs[0].interzone if l[0] == 1]
     zs[-1].interzone = [l for l in zs[-1].interzone if l[0] == len(zs) - 2]
     got, st, stats = _gpu(w.model, w.init, 300)
-    assert stats.get("ring_reg", {}).get("launches", 0) > 0
+    assert stats.get("ring_walls", {}).get("launches", 0) > 0
     b, rc, _, _ = _oracle(w.model, w.init, 300)
     assert rc == 0
     assert rel_linf(got, dict(b.state)) <= TOL
@@ -171,16 +180,17 @@ def test_ring_guard_replay():
     assert ei.value.layer == fl and ei.value.wall == b.fail_wall, (ei.value.layer, fl, ei.value.wall, b.fail_wall)
 
 
-def test_ring_reg_fast_guard_hands_over_to_k4():
-    """Values of 2 and above (inside a norm of 1000) trip K4r's fast guard in
-    its first launch; K4 replays from that launch's input with its exact guard
-    and the march matches the oracle."""
+@pytest.mark.parametrize("kernel,name", [(0, "ring_walls"), (1, "ring_reg")])
+def test_ring_reg_fast_guard_hands_over_to_k4(kernel, name):
+    """Values of 2 and above (inside a norm of 1000) trip the fast guard of K6
+    / K4r in the first launch; K4 replays from that launch's input with its
+    exact guard and the march matches the oracle."""
     w = workloads.zone_ring(n_zones=20, walls_per_zone=6, n_nodes=128, nsteps=120)
     init = {k: v.copy() for k, v in w.init.items()}
     for k in ("u_prev", "u_curr"):
         init[k][5 * 128 + 40: 5 * 128 + 60] += 1.5          # wall 5, interior nodes
-    got, st, stats = _gpu(w.model, init, 120)
-    assert stats.get("ring_reg", {}).get("launches", 0) > 0 and stats.get("ring_tiled", {}).get("launches", 0) > 0
+    got, st, stats = _gpu(w.model, init, 120, kernel=kernel)
+    assert stats.get(name, {}).get("launches", 0) > 0 and stats.get("ring_tiled", {}).get("launches", 0) > 0
     b, rc, _, _ = _oracle(w.model, init, 120)
     assert rc == 0
     assert rel_linf(got, dict(b.state)) <= TOL

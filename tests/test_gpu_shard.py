@@ -128,7 +128,7 @@ class _LoopbackComm:
         return self._reduce(x, min)
 
 
-@pytest.mark.parametrize("case", ["long", "ring", "ring128", "ring128k5"])
+@pytest.mark.parametrize("case", ["long", "ring", "ring128", "ring128k4r", "ring128k5"])
 def test_device_payload_exchange_bitwise(case):
     """Halo payloads as CUDA tensors (the NCCL path of shard.Comm: one pack
     kernel, stream-ordered, no host copies): shards in two threads equal the
@@ -153,7 +153,7 @@ def test_device_payload_exchange_bitwise(case):
         init.update(zone_u=w.init["zone_u"], zone_v=w.init["zone_v"])
         model = w.model
 
-    kname = "ring_pipe" if case == "ring128k5" else "ring_reg"
+    kname = {"ring128k5": "ring_pipe", "ring128k4r": "ring_reg"}.get(case, "ring_walls")   # ring128: K6, the default
 
     def work(rank):
         try:
@@ -167,6 +167,8 @@ def test_device_payload_exchange_bitwise(case):
                 if case.startswith("ring128"):
                     if case == "ring128k5":
                         sh.engine.set_tuning("ring_kernel", 3)  # K5 inside the shards
+                    if case == "ring128k4r":
+                        sh.engine.set_tuning("ring_kernel", 1)  # K4r inside the shards
                     sh.engine.profiling(True)
                 sh.bootstrap("implicit")
                 sh.advance(steps - 1)

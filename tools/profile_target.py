@@ -1,7 +1,7 @@
 """Minimal profiling target (no nvidia-smi child, no CPU legs): one run of a
 config's hot path, for ncu launch lists and --set full captures.
 
-  python tools/profile_target.py cfg1 [steps]
+  python tools/profile_target.py cfg1 [steps [ring_kernel [prof]]]
 """
 import sys
 import time
@@ -29,6 +29,11 @@ def main():
     else:
         w = workloads.long_domain(nsteps=steps)
     with Context(w.model) as ctx:
+        if len(sys.argv) > 3:                       # cfg3: zone-ring kernel (HYG_TUNE_RING_KERNEL)
+            ctx.set_tuning("ring_kernel", int(sys.argv[3]))
+        prof = len(sys.argv) > 4                    # per-kernel CUDA-event times
+        if prof:
+            ctx.profiling(True)
         for ch, (first, tab) in w.tables.items():
             ctx.set_channel_table(ch, first, tab)
         ctx.set_state(**w.init)
@@ -38,6 +43,10 @@ def main():
         ctx.advance(w.nsteps - (0 if w.boot == "none" else 1))
         ctx.synchronize()
         print(f"{cfg}: {w.nsteps} steps in {time.perf_counter() - t0:.3f} s, {ctx.launches} launches")
+        if prof:
+            for s in ctx.kernel_stats():
+                print(f"  {s['name']:28s} {s['launches']:6d} launches  {s['ms']:10.3f} ms  "
+                      f"{1e3 * s['ms'] / max(1, s['launches']):9.2f} us/launch")
 
 
 if __name__ == "__main__":
