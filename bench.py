@@ -49,11 +49,15 @@ CONFIGS = {
                  run_steps=100_000),
     "cfg2": dict(flop=14, bytes=0, bound="fp32", kernel="df_coupled_fused_f32", scaling="weak", dtype="f32",
                  run_steps=100_000),
-    # cfg3 runs K4r (k_ring_reg.cuh): B = 4 zones per block, S = 8 steps per launch,
+    # cfg3 runs K6 (k_ring_split.cuh: the zone air + wall cones of S = 8 steps first,
+    # then every wall in registers): per zone and launch 64 B x 768 nodes (walls) +
+    # 4 layers x 80 B x 6 walls x 72/56 (cone tails, halo copies included) + 128 B
+    # (air series), over 768 x 8 updates = 8.40 B/update; K4r (--ring-kernel 1,
+    # k_ring_reg.cuh: B = 4 zones per block, S = 8 steps per launch):
     # (64 B x 3072 owned + 32 B x 756 halo nodes) / (3072 x 8) = 8.98 B/update; K5
     # (--ring-kernel 3, k_ring_pipe.cuh: B = 3, S = 12, halo trimmed to the cone):
     # (64 B x 2304 + 32 B x 864) / (2304 x 12) = 6.33 B/update
-    "cfg3": dict(flop=14.1, bytes=8.98, bound="hbm", kernel="ring_reg", scaling="strong", dtype="f64",
+    "cfg3": dict(flop=14.1, bytes=8.98, bound="hbm", kernel="ring_walls", scaling="strong", dtype="f64",
                  run_steps=80_000, bytes_by_kernel={"ring_pipe": 6.33, "ring_reg": 8.98, "ring_walls": 8.40}),
     # cfg4 runs the temporally blocked K3w (k_dv_warp.cuh: 256-node windows, 8 steps
     # per launch, (32 x 256 + 32 x 240) / (240 x 8) = 8.27 B/update), so min(HBM,

@@ -1117,10 +1117,16 @@ void launch_ring_cone(const RingArgs& a, double* series, int LB, bool small, cud
 }
 
 template <int NPT>
-void launch_ring_walls(const RingArgs& a, const double* series, cudaStream_t s) {
-    const size_t smem = (static_cast<size_t>(kRingSplitS) * 4 * a.n_channels + kRingWallWarps * 2 * 2 * kRingSplitS) * sizeof(double);
-    const int walls = a.n_zones * a.W, per_cta = 2 * kRingWallWarps;
-    k_ring_walls<NPT, kRingSplitS><<<(walls + per_cta - 1) / per_cta, 32 * kRingWallWarps, smem, s>>>(a, series);
+void launch_ring_walls(const RingArgs& a, const double* series, cudaStream_t s, int device, int grid_cap) {
+    auto k = k_ring_walls<NPT, kRingSplitS>;
+    const size_t smem = RingWallShape<NPT>::smem_doubles(kRingSplitS, a.n_channels, kRingWallWarps) * sizeof(double);
+    ensure_smem_attr(k, device, 100 * 1024);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * kRingWallWarps, smem);
+    const int pairs = (a.n_zones * a.W + 1) / 2, nblk = (pairs + kRingWallWarps - 1) / kRingWallWarps;
+    int grid = std::max(1, std::min(nblk, std::max(per_sm, 1) * sm_count(device)));
+    if (grid_cap > 0) grid = std::min(grid, grid_cap);   // HYG_TUNE_RING_GRID: several pairs per warp in small rings
+    k<<<grid, 32 * kRingWallWarps, smem, s>>>(a, series);
 }
 
 template <int NPT>
@@ -1214,8 +1220,8 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool
                     launch_ring_cone(a, c->d_ring_series, c->ring_cone_LB, c->ring_reg_small, c->stream, c->device);
                 }
                 LaunchScope ls(c, "ring_walls", static_cast<double>(c->cells()) * a.steps);
-                if (npt == 4) launch_ring_walls<4>(a, c->d_ring_series, c->stream);
-                else launch_ring_walls<8>(a, c->d_ring_series, c->stream);
+                if (npt == 4) launch_ring_walls<4>(a, c->d_ring_series, c->stream, c->device, c->ring_grid_cap);
+                else launch_ring_walls<8>(a, c->d_ring_series, c->stream, c->device, c->ring_grid_cap);
                 continue;
             }
             LaunchScope ls(c, pipe ? "ring_pipe" : reg ? "ring_reg" : "ring_tiled", static_cast<double>(c->cells()) * a.steps);
@@ -1577,7 +1583,7 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
                     const int rw = RingShape<8, kRingSplitS>::row_width(nch, nsrc);
                     int lb = 2 * kRingSplitS + 1;
                     while (SC::threads(lb + 1, W) <= kRingConeThreads &&
-                           SC::smem_doubles(lb + 1, W, rw) * sizeof(double) <= 200u * 1024u)
+                           SC::smem_doubles(lb + 1, W, rw) * sizeof(double) <= 227u * 1024u)
                         ++lb;
                     if (SC::threads(lb, W) <= kRingConeThreads) {
                         const int nsm = sm_count(c->device);

@@ -58,6 +58,9 @@ struct WallCoef {
     RowCoef face[2];     // [0]: node 0 (x*=0), [1]: node n-1 (x*=1)
 };
 
+// k_ring_split.cuh stages rows as arrays of doubles in this order
+static_assert(sizeof(RowCoef) == 9 * sizeof(double) && sizeof(WallCoef) == 27 * sizeof(double), "row layout");
+
 HYG_HD void coupled_face(const Groups& p, double dx, double lam, double mu, double beta,
                          double ratio, const Biot& f, RowCoef& c) {
     const double g = p.gamma;

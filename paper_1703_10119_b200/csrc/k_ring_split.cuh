@@ -35,6 +35,20 @@
 
 #include "k_ring_reg.cuh"
 
+// timing experiments only (tools/ring_walls_probe.cu): skip the steps (1), the
+// outputs (2), the layer loads (4); minimum CTAs per SM; 0 / 4 in the library
+#ifndef RW_SKIP
+#define RW_SKIP 0
+#endif
+#ifndef RW_MINB
+#define RW_MINB 3
+#endif
+// k_ring_cone: skip the steps (1), the staged loads (2), the zone parameter loads (4),
+// the zone arithmetic (8), the cone arithmetic (16), the division (32)
+#ifndef RC_SKIP
+#define RC_SKIP 0
+#endif
+
 namespace hyg {
 
 #ifndef HYG_RING_CONE_THREADS
@@ -50,9 +64,14 @@ struct RingConeShape {
     __host__ __device__ static int cone_warps(int LB, int W) { return ((LB - 2) * W + 31) / 32; }
     __host__ __device__ static int zone_warps(int LB) { return (LB + 31) / 32; }
     __host__ __device__ static int threads(int LB, int W) { return 32 * (cone_warps(LB, W) + zone_warps(LB)); }
-    // doubles: surfaces [parity][field][W][LB], zone air [parity][field][LB], forcing rows [S][rw]
+    // per cone warp: the 32 cones' staged tails [32][4 fields x kPS, + 2: an odd count of
+    // 16-byte chunks, so the lanes' reads are conflict-free] and rows [32][12 + 1]
+    static constexpr int kTail = 4 * kPS + 2, kRow = 13;
+    // doubles: surfaces [parity][field][W][LB], zone air [parity][field][LB], forcing rows
+    // [S][rw] (even), then per cone warp tails and rows
     __host__ __device__ static size_t smem_doubles(int LB, int W, int rw) {
-        return static_cast<size_t>(4) * W * LB + 4 * LB + static_cast<size_t>(S) * rw;
+        return static_cast<size_t>(4) * W * LB + 4 * LB + ((static_cast<size_t>(S) * rw + 1) & ~static_cast<size_t>(1)) +
+               static_cast<size_t>(cone_warps(LB, W)) * 32 * (kTail + kRow);
     }
 };
 
@@ -62,13 +81,14 @@ __global__ void __launch_bounds__(kRingConeThreads, 1) k_ring_cone(const RingArg
                                                                   const int LB) {
     using Sh = RingConeShape<S>;
     constexpr int P = Sh::kP, PS = Sh::kPS;
-    extern __shared__ double smem[];
+    extern __shared__ __align__(16) double smem[];
     if (launch_stopped(a.stop)) return;
     const int W = a.W, Z = a.n_zones, N = a.n;
     const int OB = LB - 2 * S;                          // owned zones per CTA
     const int z0 = blockIdx.x * OB, nown = min(OB, Z - z0), L = nown + 2 * S;
     const int rw = RingShape<8, S>::row_width(a.n_channels, a.n_sources);
     const int oSF = 0, oAR = oSF + 4 * W * LB, oRW = oAR + 4 * LB;
+    const int oCW = oRW + ((S * rw + 1) & ~1);          // per cone warp: staged tails and rows
     auto sf_ix = [&](int par, int f, int slot) { return oSF + (par * 2 + f) * W * LB + slot; };
     auto ar_ix = [&](int par, int f, int i) { return oAR + (par * 2 + f) * LB + i; };
     const int tid = threadIdx.x, nthr = blockDim.x;
@@ -93,17 +113,38 @@ __global__ void __launch_bounds__(kRingConeThreads, 1) k_ring_cone(const RingArg
         const bool live = li0 <= L - 2;
         const int li = live ? li0 : 1;
         const int w = gz(li) * W + wi;
-        const WallCoef& wc = a.coef[w];
-        const double cb = wc.in.b, csu = wc.in.c_su, csv = wc.in.c_sv;
-        const RowCoef c = wc.face[1];
+        // the warp stages its 32 cones together: tails (the last PS nodes of the four
+        // layers, runs of 16-byte copies) and rows (interior b, c_su, c_sv + face[1]) by
+        // cp.async, consecutive lanes on consecutive addresses of one wall
+        constexpr int TS = Sh::kTail, RS = Sh::kRow, CPW = 4 * (PS / 2);   // chunks per wall
+        double* tails = smem + oCW + warp * 32 * (TS + RS);
+        double* rows = tails + 32 * TS;
+#pragma unroll
+        for (int r = 0; r < CPW * !(RC_SKIP & 2); ++r) {
+            const int m = r * 32 + lane, wj = m / CPW, fc = m - wj * CPW, f = fc / (PS / 2), cc = fc - f * (PS / 2);
+            const int ws = __shfl_sync(0xffffffffu, w, wj);
+            cp_async16(&tails[wj * TS + f * PS + 2 * cc], a.in[f] + static_cast<size_t>(ws) * N + (N - PS) + 2 * cc);
+        }
+#pragma unroll
+        for (int r = 0; r < 12 * !(RC_SKIP & 2); ++r) {
+            const int m = r * 32 + lane, wj = m / 12, k = m - wj * 12;
+            const int ws = __shfl_sync(0xffffffffu, w, wj);
+            const int src = k == 0 ? 0 : k == 1 ? 3 : k == 2 ? 5 : 15 + k;   // in.b, in.c_su, in.c_sv, face[1][0..8]
+            cp_async8(&rows[wj * RS + k], reinterpret_cast<const double*>(a.coef + ws) + src);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncwarp();
+        const double* rw_ = rows + lane * RS;
+        const double cb = rw_[0], csu = rw_[1], csv = rw_[2];
+        // face[1]: b, e, e_g, c_su, c_tu, c_sv, c_tv, c_q, c_g at rw_[3 ..]; read per step
         double up[P], uc[P], vp[P], vc[P];
         {
-            const size_t g0 = static_cast<size_t>(w) * N + (N - PS);
             auto rd = [&](int f, double (&x)[P]) {
                 double t[PS];
 #pragma unroll
                 for (int q = 0; q < PS / 2; ++q) {
-                    const double2 v = *reinterpret_cast<const double2*>(a.in[f] + g0 + 2 * q);
+                    const double2 v = *reinterpret_cast<const double2*>(&tails[lane * TS + f * PS + 2 * q]);
                     t[2 * q] = v.x;
                     t[2 * q + 1] = v.y;
                 }
@@ -124,7 +165,7 @@ __global__ void __launch_bounds__(kRingConeThreads, 1) k_ring_cone(const RingArg
         auto step = [&](double (&vP)[P], double (&vC)[P], double (&uP)[P], double (&uC)[P]) {
             const double u_a = smem[ar_ix(cur, 0, li)], v_a = smem[ar_ix(cur, 1, li)];
 #pragma unroll
-            for (int p = 0; p < P; ++p) {
+            for (int p = (RC_SKIP & 16) ? P - 1 : 0; p < P; ++p) {
                 const double vl = p == 0 ? vC[0] : vC[p - 1], ul = p == 0 ? uC[0] : uC[p - 1];
                 const double vr = p == P - 1 ? vC[P - 2] : vC[p + 1], ur = p == P - 1 ? uC[P - 2] : uC[p + 1];
                 const double d = fma(-2.0, vP[p], vl + vr);
@@ -135,9 +176,10 @@ __global__ void __launch_bounds__(kRingConeThreads, 1) k_ring_cone(const RingArg
                     un = fma(csv, d, fma(csu, du, uP[p]));
                 } else {
                     const double t = v_a - vP[p], tu = u_a - uP[p];
-                    vn = fma(c.e, t, fma(c.b, d, fma(c.e_g, 0.0, vP[p])));
-                    un = fma(c.c_tv, t, fma(c.c_sv, d, fma(c.c_tu, tu, fma(c.c_su, du, fma(c.c_q, 0.0,
-                                                                                        fma(c.c_g, 0.0, uP[p]))))));
+                    const double fb = rw_[3], fe = rw_[4], feg = rw_[5], fcsu = rw_[6], fctu = rw_[7], fcsv = rw_[8],
+                                 fctv = rw_[9], fcq = rw_[10], fcg = rw_[11];
+                    vn = fma(fe, t, fma(fb, d, fma(feg, 0.0, vP[p])));
+                    un = fma(fctv, t, fma(fcsv, d, fma(fctu, tu, fma(fcsu, du, fma(fcq, 0.0, fma(fcg, 0.0, uP[p]))))));
                 }
                 vP[p] = vn;
                 uP[p] = un;
@@ -149,12 +191,13 @@ __global__ void __launch_bounds__(kRingConeThreads, 1) k_ring_cone(const RingArg
             __syncthreads();
             cur ^= 1;
         };
-        int k = 0;
+        int k = (RC_SKIP & 1) ? a.steps : 0;
         for (; k + 1 < a.steps; k += 2) {
             step(vp, vc, up, uc);
             step(vc, vp, uc, up);
         }
         if (k < a.steps) step(vp, vc, up, uc);
+        if (RC_SKIP & 1) acc |= __double2hiint(up[0] + uc[1] + vp[2] + vc[3] + cb + csu + csv) & 1;
     } else {
         // zone thread i: zone_step_explicit (zone.cpp:69-74) of local zone i (1 .. L-2
         // live; 0 and L-1 contribute their layer-0 air only); parameter block as K4r's
@@ -163,7 +206,7 @@ __global__ void __launch_bounds__(kRingConeThreads, 1) k_ring_cone(const RingArg
         const bool live = i >= 1 && i < L - 1;
         const bool owned = i >= S && i < S + nown;
         const int zg = gz(valid ? i : 0);
-        const double* zp = a.zparams + static_cast<size_t>(zg) * kRingZP;
+        const double* zp = a.zparams + static_cast<size_t>((RC_SKIP & 4) ? 0 : zg) * kRingZP;
         int nlink = 0, npeer = 0, sidx = 0;
         if (live) {
             nlink = static_cast<int>(zp[4]);
@@ -197,8 +240,8 @@ __global__ void __launch_bounds__(kRingConeThreads, 1) k_ring_cone(const RingArg
         }
         double* ser = series + static_cast<size_t>(zg) * S * 2;
         __syncthreads();
-        for (int k = 0; k < a.steps; ++k) {
-            if (live) {
+        for (int k = (RC_SKIP & 1) ? a.steps : 0; k < a.steps; ++k) {
+            if (live && !(RC_SKIP & 8)) {
                 const double u_a = smem[ar_ix(cur, 0, i)], v_a = smem[ar_ix(cur, 1, i)];
                 if (owned) *reinterpret_cast<double2*>(ser + 2 * k) = make_double2(u_a, v_a);   // layer-k air for phase 2
                 const int srow = oRW + k * rw + 4 * a.n_channels;
@@ -220,7 +263,7 @@ __global__ void __launch_bounds__(kRingConeThreads, 1) k_ring_cone(const RingArg
                     du += lT[q] * (us - u_a) + lM[q] * (vs - v_a);
                     dv += lD[q] * (v_a - vs);
                 }
-                const double nu = u_a + a.dt * (du / c0);
+                const double nu = u_a + a.dt * ((RC_SKIP & 32) ? du * c0 : du / c0);
                 const double nv = v_a + a.dt * dv;
                 smem[ar_ix(cur ^ 1, 0, i)] = nu;
                 smem[ar_ix(cur ^ 1, 1, i)] = nv;
@@ -238,114 +281,228 @@ __global__ void __launch_bounds__(kRingConeThreads, 1) k_ring_cone(const RingArg
 }
 
 // ---- phase 2 ---------------------------------------------------------------------------
+// Persistent warps: warp g of the grid marches the wall pairs g, g + G, ...
+// While a pair is marched in registers, the next pair's four layers (8 KB at
+// n = 128) arrive in the warp's own shared buffer by four 1-D bulk copies on
+// the TMA engine (completion on the warp's mbarrier), its zones' air series and
+// row coefficients by 8-byte cp.async; results leave through a per-warp scratch
+// and TMA bulk stores, two fields at a time.  No per-thread global loads or
+// stores of state: a lane's NPT consecutive nodes are a 64-byte segment, and
+// strided 16-byte LDG/STG cost 16 L1 data-pipe passes per instruction (the
+// first version of this kernel ran into that pipe at 72 %, DRAM at 50 %);
+// shared reads and writes start each lane at a rotated 16-byte pair
+// (conflict-free quarter warps, K4r's select network restores the order).
+// Measured and not kept: walking the pairs backwards in odd launches so a launch
+// starts on the data the previous one wrote last (82.7 vs 83.8 us: nothing of the
+// previous output is served from L2), 4 CTAs per SM (128 registers, spills: 92 us
+// vs 83 at 3), coalesced cp.async into an XOR-swizzled buffer + direct 16-byte
+// stores (95 us).  tools/ring_walls_probe.cu: loads alone 39 us, stores alone 46,
+// loads + stores without the steps 79 (5.1 TB/s for this eight-stream pattern).
+template <int NPT>
+struct RingWallShape {
+    static constexpr int kN = 16 * NPT;
+    static constexpr int kCoef = static_cast<int>(sizeof(WallCoef) / sizeof(double));   // 27
+    // doubles per warp: the pair's four layers, the output scratch (two fields), the
+    // (double-buffered) air series and row coefficients of its two walls, the mbarrier
+    __host__ __device__ static int warp_doubles(int S) {
+        return 4 * 2 * kN + 2 * 2 * kN + 2 * 2 * 2 * S + 2 * 2 * kCoef + 2;
+    }
+    __host__ __device__ static size_t smem_doubles(int S, int nch, int warps) {
+        return ((static_cast<size_t>(S) * 4 * nch + 1) & ~static_cast<size_t>(1)) +
+               static_cast<size_t>(warps) * warp_doubles(S);
+    }
+};
+
 template <int NPT, int S>
-__global__ void __launch_bounds__(32 * kRingWallWarps, 4) k_ring_walls(const RingArgs a,
+__global__ void __launch_bounds__(32 * kRingWallWarps, RW_MINB) k_ring_walls(const RingArgs a,
                                                                       const double* __restrict__ series) {
-    constexpr int N = 16 * NPT;
+    using Sh = RingWallShape<NPT>;
+    constexpr int N = Sh::kN, NC = Sh::kCoef;
     constexpr unsigned FULL = 0xffffffffu;
-    extern __shared__ double smem[];                    // forcing rows [S][4 nch], air [warps][2 walls][S][2]
+    extern __shared__ __align__(16) double smem[];      // forcing rows [S][4 nch], then the warps' blocks
     if (launch_stopped(a.stop)) return;
     const int W = a.W, n_walls = a.n_zones * W;
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
     const int rwc = 4 * a.n_channels;
     for (int i = tid; i < a.steps * rwc; i += blockDim.x)
         smem[i] = reinterpret_cast<const double*>(a.table)[i];
-    const int wl = (blockIdx.x * kRingWallWarps + warp) * 2 + lane / 16, sub = lane % 16;
-    const bool live = wl < n_walls;
-    const int w = live ? wl : 0;
-    double* s_air = smem + S * rwc + (warp * 2 + lane / 16) * 2 * S;
-    for (int i = sub; i < 2 * a.steps; i += 16) s_air[i] = series[static_cast<size_t>(w / W) * S * 2 + i];
+    double* buf = smem + ((S * rwc + 1) & ~1) + warp * Sh::warp_doubles(S);   // [4][2 N] staged layers
+    double* out_s = buf + 4 * 2 * N;                    // [2][2 N] output scratch
+    double* air = out_s + 2 * 2 * N;                    // [parity][wall of the pair][S][2]
+    double* cfs = air + 2 * 2 * 2 * S;                  // [parity][wall of the pair][WallCoef]
+    void* mbar = cfs + 2 * 2 * NC;
+    if (lane == 0) {
+        mbar_init(mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();                                    // rows staged, mbarriers initialised
+    const int n_pairs = (n_walls + 1) / 2;
+    const int stride = gridDim.x * kRingWallWarps;
+    const int half = lane / 16, sub = lane % 16;
     const bool first = sub == 0, rev = sub == 15, mirror0 = first || rev;
-    const WallCoef& wc = a.coef[w];
-    const double cb = wc.in.b, csu = wc.in.c_su, csv = wc.in.c_sv;
-    // register 0's row: a face row in the face lanes, else the interior row,
-    // whose face terms are 0 (hyg_coef.cuh)
-    const RowCoef& c = first ? wc.face[0] : (rev ? wc.face[1] : wc.in);
-    const double fe = c.e, fb = c.b, feg = c.e_g, fctv = c.c_tv, fcsv = c.c_sv, fctu = c.c_tu, fcsu = c.c_su,
-                 fcq = c.c_q, fcg = c.c_g;
-    const int ch = a.attach[2 * w].index;
-    double up[NPT], uc[NPT], vp[NPT], vc[NPT];
-    const size_t g0 = static_cast<size_t>(w) * N + sub * NPT;
-    auto rd = [&](int f, double (&x)[NPT]) {
-        double t[NPT];
+    const int rot = (sub / (16 / NPT)) & (NPT / 2 - 1);
+    auto shift_pairs = [&](double (&t)[NPT], int r) {   // t pair p <- t pair (p - r) mod NPT/2
 #pragma unroll
-        for (int q = 0; q < NPT / 2; ++q) {
-            const double2 v = __ldcs(reinterpret_cast<const double2*>(a.in[f] + g0 + 2 * q));
-            t[2 * q] = v.x;
-            t[2 * q + 1] = v.y;
+        for (int bit = 1; bit < NPT / 2; bit <<= 1) {
+            const bool on = r & bit;
+            double o[NPT];
+#pragma unroll
+            for (int q = 0; q < NPT; ++q) o[q] = t[q];
+#pragma unroll
+            for (int q = 0; q < NPT; ++q) t[q] = on ? o[(q + NPT - 2 * bit) % NPT] : o[q];
         }
-#pragma unroll
-        for (int q = 0; q < NPT; ++q) x[q] = rev ? t[NPT - 1 - q] : t[q];
     };
-    rd(0, up);
-    rd(1, uc);
-    rd(2, vp);
-    rd(3, vc);
-    __syncthreads();                                    // rows and air staged
+    auto prefetch = [&](int pair, int par) {
+        const int nw = 2 * pair + 1 < n_walls ? 2 : 1;  // the last pair of an odd wall count has one wall
+        if (lane == 0) {
+            const unsigned bytes = static_cast<unsigned>(nw * N * sizeof(double));
+            mbar_expect_tx(mbar, (RW_SKIP & 4) ? 0u : 4 * bytes);
+#pragma unroll
+            for (int f = 0; f < 4 * !(RW_SKIP & 4); ++f)
+                bulk_g2s(&buf[f * 2 * N], a.in[f] + static_cast<size_t>(pair) * 2 * N, bytes, mbar);
+        }
+        for (int i = lane; i < 2 * 2 * a.steps; i += 32) {
+            const int wj = i / (2 * a.steps), r = i - wj * 2 * a.steps;
+            const int w = min(2 * pair + wj, n_walls - 1);
+            cp_async8(&air[(par * 2 + wj) * 2 * S + r], series + static_cast<size_t>(w / W) * S * 2 + r);
+        }
+        for (int i = lane; i < nw * NC; i += 32)
+            cp_async8(&cfs[par * 2 * NC + i], reinterpret_cast<const double*>(a.coef + 2 * pair) + i);
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    int pair = blockIdx.x * kRingWallWarps + warp;
+    if (pair < n_pairs) prefetch(pair, 0);
     unsigned acc = 0;
-    auto step = [&](double (&vP)[NPT], double (&vC)[NPT], double (&uP)[NPT], double (&uC)[NPT], int k) {
-        // face inputs of register 0, branch-free (wall.cpp:162-169, 177-189):
-        // x = 0 the exterior channel, x = 1 the zone's layer-k air (phase 1)
-        const int am = k * rwc + 4 * ch;
-        const double ru = smem[am + 0], rv = smem[am + 1], rg = smem[am + 2], rq = smem[am + 3] + 0.0;
-        const double au = s_air[2 * k], av = s_air[2 * k + 1];
-        const double u_inf = first ? ru : au, v_inf = first ? rv : av;
-        const double g_inf = first ? rg : 0.0, q_inf = first ? rq : 0.0;
-        const double vs = rev ? vC[NPT - 1] : vC[0], us = rev ? uC[NPT - 1] : uC[0];
-        const double vup = __shfl_up_sync(FULL, vC[NPT - 1], 1, 16);
-        const double uup = __shfl_up_sync(FULL, uC[NPT - 1], 1, 16);
-        const double vdn = __shfl_down_sync(FULL, vs, 1, 16);
-        const double udn = __shfl_down_sync(FULL, us, 1, 16);
-        const double vx0 = mirror0 ? vC[1] : vup, ux0 = mirror0 ? uC[1] : uup;
-        const double vx1 = rev ? vup : vdn, ux1 = rev ? uup : udn;
+    for (int it = 0; pair < n_pairs; pair += stride, ++it) {
+        const int par = it & 1;
+        const int wl = 2 * pair + half;
+        const bool live = wl < n_walls;
+        const int nlive = min(2, n_walls - 2 * pair);
+        const int ch = a.attach[2 * (live ? wl : n_walls - 1)].index;
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        mbar_wait(mbar, par);                           // the pair's layers landed
+        __syncwarp();                                   // ... and every lane's air / row copies
+        // rows (WallCoef = in, face[0], face[1]; RowCoef = b, e, e_g, c_su, c_tu, c_sv, c_tv, c_q, c_g).
+        // Register 0's row: a face row in the face lanes, else the interior row,
+        // whose face terms are 0 (hyg_coef.cuh)
+        const double* wc = cfs + (par * 2 + (live ? half : 0)) * NC;
+        const double cb = wc[0], csu = wc[3], csv = wc[5];
+        const double* c = wc + (first ? 9 : (rev ? 18 : 0));
+        const double fb = c[0], fe = c[1], feg = c[2], fcsu = c[3], fctu = c[4], fcsv = c[5], fctv = c[6],
+                     fcq = c[7], fcg = c[8];
+        double up[NPT], uc[NPT], vp[NPT], vc[NPT];
+        auto rd = [&](int f, double (&x)[NPT]) {        // the reversed lane by selects
+            double t[NPT];
 #pragma unroll
-        for (int q = 0; q < NPT; ++q) {
-            const double vl = q == 0 ? vx0 : vC[q - 1], ul = q == 0 ? ux0 : uC[q - 1];
-            const double vr = q == NPT - 1 ? vx1 : vC[q + 1], ur = q == NPT - 1 ? ux1 : uC[q + 1];
-            const double d = fma(-2.0, vP[q], vl + vr);
-            const double du = fma(-2.0, uP[q], ul + ur);
-            double vn, un;
-            if (q == 0) {
-                const double t = v_inf - vP[0], tu = u_inf - uP[0];
-                vn = fma(fe, t, fma(fb, d, fma(feg, g_inf, vP[0])));
-                un = fma(fctv, t, fma(fcsv, d, fma(fctu, tu, fma(fcsu, du, fma(fcq, q_inf, fma(fcg, g_inf, uP[0]))))));
-            } else {
-                vn = fma(cb, d, vP[q]);
-                un = fma(csv, d, fma(csu, du, uP[q]));
+            for (int qq = 0; qq < NPT / 2; ++qq) {      // t pair qq = node pair (qq + rot) mod NPT/2
+                const int pr = (qq + rot) & (NPT / 2 - 1);
+                const double2 v = *reinterpret_cast<const double2*>(&buf[f * 2 * N + lane * NPT + 2 * pr]);
+                t[2 * qq] = v.x;
+                t[2 * qq + 1] = v.y;
             }
-            acc |= static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn));
-            vP[q] = vn;
-            uP[q] = un;
-        }
-    };
-    int k = 0;
-    for (; k + 1 < a.steps; k += 2) {
-        step(vp, vc, up, uc, k);
-        step(vc, vp, uc, up, k + 1);
-    }
-    if (k < a.steps) {
-        step(vp, vc, up, uc, k);
+            shift_pairs(t, rot);
 #pragma unroll
-        for (int q = 0; q < NPT; ++q) {
-            double x = vp[q]; vp[q] = vc[q]; vc[q] = x;
-            x = up[q]; up[q] = uc[q]; uc[q] = x;
-        }
-    }
-    if (live) {
-        auto wr = [&](int f, const double (&x)[NPT]) {
+            for (int q = 0; q < NPT; ++q) x[q] = rev ? t[NPT - 1 - q] : t[q];
+        };
+        rd(0, up);
+        rd(1, uc);
+        rd(2, vp);
+        rd(3, vc);
+        __syncwarp();                                   // the buffer is free for the next pair
+        if (pair + stride < n_pairs) prefetch(pair + stride, par ^ 1);
+        const double* s_air = air + (par * 2 + half) * 2 * S;
+        unsigned acc_t = 0;
+        auto step = [&](double (&vP)[NPT], double (&vC)[NPT], double (&uP)[NPT], double (&uC)[NPT], int k) {
+            // face inputs of register 0, branch-free (wall.cpp:162-169, 177-189):
+            // x = 0 the exterior channel, x = 1 the zone's layer-k air (phase 1)
+            const int am = k * rwc + 4 * ch;
+            const double ru = smem[am + 0], rv = smem[am + 1], rg = smem[am + 2], rq = smem[am + 3] + 0.0;
+            const double au = s_air[2 * k], av = s_air[2 * k + 1];
+            const double u_inf = first ? ru : au, v_inf = first ? rv : av;
+            const double g_inf = first ? rg : 0.0, q_inf = first ? rq : 0.0;
+            const double vs = rev ? vC[NPT - 1] : vC[0], us = rev ? uC[NPT - 1] : uC[0];
+            const double vup = __shfl_up_sync(FULL, vC[NPT - 1], 1, 16);
+            const double uup = __shfl_up_sync(FULL, uC[NPT - 1], 1, 16);
+            const double vdn = __shfl_down_sync(FULL, vs, 1, 16);
+            const double udn = __shfl_down_sync(FULL, us, 1, 16);
+            const double vx0 = mirror0 ? vC[1] : vup, ux0 = mirror0 ? uC[1] : uup;
+            const double vx1 = rev ? vup : vdn, ux1 = rev ? uup : udn;
 #pragma unroll
-            for (int q = 0; q < NPT / 2; ++q) {
-                const double2 v = rev ? make_double2(x[NPT - 1 - 2 * q], x[NPT - 2 - 2 * q]) : make_double2(x[2 * q], x[2 * q + 1]);
-                __stcs(reinterpret_cast<double2*>(a.out[f] + g0 + 2 * q), v);
+            for (int q = 0; q < NPT; ++q) {
+                const double vl = q == 0 ? vx0 : vC[q - 1], ul = q == 0 ? ux0 : uC[q - 1];
+                const double vr = q == NPT - 1 ? vx1 : vC[q + 1], ur = q == NPT - 1 ? ux1 : uC[q + 1];
+                const double d = fma(-2.0, vP[q], vl + vr);
+                const double du = fma(-2.0, uP[q], ul + ur);
+                double vn, un;
+                if (q == 0) {
+                    const double t = v_inf - vP[0], tu = u_inf - uP[0];
+                    vn = fma(fe, t, fma(fb, d, fma(feg, g_inf, vP[0])));
+                    un = fma(fctv, t, fma(fcsv, d, fma(fctu, tu, fma(fcsu, du, fma(fcq, q_inf, fma(fcg, g_inf, uP[0]))))));
+                } else {
+                    vn = fma(cb, d, vP[q]);
+                    un = fma(csv, d, fma(csu, du, uP[q]));
+                }
+                acc_t |= static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn));
+                vP[q] = vn;
+                uP[q] = un;
             }
         };
+        int k = (RW_SKIP & 1) ? a.steps : 0;
+        for (; k + 1 < a.steps; k += 2) {
+            step(vp, vc, up, uc, k);
+            step(vc, vp, uc, up, k + 1);
+        }
+        if (k < a.steps) {
+            step(vp, vc, up, uc, k);
+#pragma unroll
+            for (int q = 0; q < NPT; ++q) {
+                double x = vp[q]; vp[q] = vc[q]; vc[q] = x;
+                x = up[q]; up[q] = uc[q]; uc[q] = x;
+            }
+        }
+        if (live) acc |= acc_t;
+        if (RW_SKIP & 2) {
+            acc |= __double2hiint(up[0] + uc[1] + vp[2] + vc[3]) & 1;   // keep the values alive
+            continue;
+        }
+        // out = (layer k+S-1, layer k+S): the pair through the warp's scratch, two
+        // fields at a time, one bulk store (TMA engine) per field
+        auto wr = [&](int f, const double (&x)[NPT]) {  // node order, then pair (qq + rot) first
+            double t[NPT];
+#pragma unroll
+            for (int q = 0; q < NPT; ++q) t[q] = rev ? x[NPT - 1 - q] : x[q];
+            shift_pairs(t, (NPT / 2 - rot) & (NPT / 2 - 1));
+#pragma unroll
+            for (int qq = 0; qq < NPT / 2; ++qq) {
+                const int pr = (qq + rot) & (NPT / 2 - 1);
+                *reinterpret_cast<double2*>(&out_s[f * 2 * N + lane * NPT + 2 * pr]) = make_double2(t[2 * qq], t[2 * qq + 1]);
+            }
+        };
+        auto flush = [&](int f0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                const unsigned bytes = static_cast<unsigned>(nlive * N * sizeof(double));
+#pragma unroll
+                for (int f = 0; f < 2; ++f)
+                    bulk_s2g(a.out[f0 + f] + static_cast<size_t>(pair) * 2 * N, &out_s[f * 2 * N], bytes);
+                asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+            }
+        };
+        auto drained = [&]() {   // the scratch may be rewritten once the last copies read it
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+            __syncwarp();
+        };
+        drained();
         wr(0, up);
         wr(1, uc);
-        wr(2, vp);
-        wr(3, vc);
-    } else {
-        acc = 0;
+        flush(0);
+        drained();
+        wr(0, vp);
+        wr(1, vc);
+        flush(2);
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // stores drained
     if (__syncthreads_or((acc & 0x40000000u) != 0u) && tid == 0) atomicCAS(a.stop, 0, a.seg_index + 1);
 }
 
