@@ -228,6 +228,9 @@ struct hyg_ctx {
     int ring_pipe_B = 0;             // K5 (k_ring_pipe.cuh): zones per block, 0 if not applicable
     int ring_kernel = 0;             // HYG_TUNE_RING_KERNEL: 0 auto (K6), 1 K4r, 2 K4, 3 K5, 4 K6
     int ring_cone_LB = 0;            // K6 phase 1: local zones per CTA (owned + 2 S halo), 0 if not applicable
+    double* d_ring_rowsT = nullptr;  // K6 phase 1: cone rows transposed [12][walls] for rows_dt (k_ring_cone_rows)
+    double* d_ring_zpT = nullptr;    // K6 phase 1: the zone parameter blocks transposed [kRingZP][zones]
+    double rows_dt = -1.0;
     double* d_ring_series = nullptr; // K6: layer-k air of every zone for the S steps of a launch [zones][S][2]
     bool mat_exact = false;          // HYG_TUNE_MATERIAL_EXACT: CrMath evaluation + IEEE-division rows
     bool owned_partial = false;      // hyg_set_owned narrowed the guard to a shard's range
@@ -1106,14 +1109,15 @@ void launch_ring_pipe(const RingArgs& a, size_t smem, cudaStream_t s, int device
 
 // K6 (k_ring_split.cuh): phase 1 (zone air + wall cones, records the air series),
 // then phase 2 (every wall in registers, no barrier per step)
-void launch_ring_cone(const RingArgs& a, double* series, int LB, bool small, cudaStream_t s, int device) {
+void launch_ring_cone(const RingArgs& a, double* series, int LB, bool small, cudaStream_t s, int device,
+                      const double* rowsT, const double* zpT) {
     using Sh = RingConeShape<kRingSplitS>;
     auto k = small ? k_ring_cone<kRingSplitS, 6, 2> : k_ring_cone<kRingSplitS>;
     const int rw = RingShape<8, kRingSplitS>::row_width(a.n_channels, a.n_sources);
     const size_t smem = Sh::smem_doubles(LB, a.W, rw) * sizeof(double);
     ensure_smem_attr(k, device, 227 * 1024);
     const int OB = LB - 2 * kRingSplitS;
-    k<<<(a.n_zones + OB - 1) / OB, Sh::threads(LB, a.W), smem, s>>>(a, series, LB);
+    k<<<(a.n_zones + OB - 1) / OB, Sh::threads(LB, a.W), smem, s>>>(a, series, LB, rowsT, zpT);
 }
 
 template <int NPT>
@@ -1149,6 +1153,11 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool
         k_coupled_coef<<<(c->n_walls + 127) / 128, 128, 0, c->stream>>>(c->n_walls, c->dx, dt, c->d_groups,
                                                                          c->d_biot, c->d_coef);
         c->coef_dt = dt;
+    }
+    if (split && c->rows_dt != dt) {
+        LaunchScope ls(c, "ring_cone_rows", 0.0);
+        k_ring_cone_rows<<<(c->n_walls + 127) / 128, 128, 0, c->stream>>>(c->n_walls, c->d_coef, c->d_ring_rowsT);
+        c->rows_dt = dt;
     }
     const int nch = std::max<int>(1, static_cast<int>(c->channels.size()));
     const int nsrc = static_cast<int>(c->zsrc.size() / 3);
@@ -1217,7 +1226,8 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool
             if (split) {
                 {
                     LaunchScope ls(c, "ring_cone", 0.0);
-                    launch_ring_cone(a, c->d_ring_series, c->ring_cone_LB, c->ring_reg_small, c->stream, c->device);
+                    launch_ring_cone(a, c->d_ring_series, c->ring_cone_LB, c->ring_reg_small, c->stream, c->device,
+                                     c->d_ring_rowsT, c->d_ring_zpT);
                 }
                 LaunchScope ls(c, "ring_walls", static_cast<double>(c->cells()) * a.steps);
                 if (npt == 4) launch_ring_walls<4>(a, c->d_ring_series, c->stream, c->device, c->ring_grid_cap);
@@ -1716,9 +1726,17 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
                 }
             }
             if (cudaMalloc(&c->d_ring_zp, sizeof(double) * zp.size()) != cudaSuccess) return fail("zone alloc");
-            if (c->ring_cone_LB > 0 &&
-                cudaMalloc(&c->d_ring_series, sizeof(double) * c->zones.size() * kRingSplitS * 2) != cudaSuccess)
-                return fail("zone alloc");
+            if (c->ring_cone_LB > 0) {
+                const size_t Zn = c->zones.size();
+                std::vector<double> zpT(zp.size());
+                for (size_t z = 0; z < Zn; ++z)
+                    for (int k = 0; k < kRingZP; ++k) zpT[k * Zn + z] = zp[z * kRingZP + k];
+                if (cudaMalloc(&c->d_ring_series, sizeof(double) * Zn * kRingSplitS * 2) != cudaSuccess ||
+                    cudaMalloc(&c->d_ring_rowsT, sizeof(double) * 12 * c->n_walls) != cudaSuccess ||
+                    cudaMalloc(&c->d_ring_zpT, sizeof(double) * zpT.size()) != cudaSuccess)
+                    return fail("zone alloc");
+                cudaMemcpy(c->d_ring_zpT, zpT.data(), sizeof(double) * zpT.size(), cudaMemcpyHostToDevice);
+            }
             cudaMemcpy(c->d_ring_zp, zp.data(), sizeof(double) * zp.size(), cudaMemcpyHostToDevice);
         }
     }
@@ -1765,6 +1783,8 @@ void hyg_destroy(hyg_ctx* c) {
     cudaFree(c->d_inz);
     cudaFree(c->d_ring_zp);
     cudaFree(c->d_ring_series);
+    cudaFree(c->d_ring_rowsT);
+    cudaFree(c->d_ring_zpT);
     cudaFree(c->d_table);
     cudaFree(c->d_boot);
     cudaFree(c->d_src);

@@ -75,10 +75,20 @@ struct RingConeShape {
     }
 };
 
+// rows of the cone threads, transposed: rowsT[k][wall], k = in.b, in.c_su, in.c_sv, face[1][0..8]
+__global__ void k_ring_cone_rows(int n_walls, const WallCoef* __restrict__ coef, double* __restrict__ rowsT) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= n_walls) return;
+    const double* c = reinterpret_cast<const double*>(coef + w);
+#pragma unroll
+    for (int k = 0; k < 12; ++k) rowsT[static_cast<size_t>(k) * n_walls + w] = c[k == 0 ? 0 : k == 1 ? 3 : k == 2 ? 5 : 15 + k];
+}
+
 // ---- phase 1 ---------------------------------------------------------------------------
 template <int S, int NL = kRingMaxLinks, int NP = kRingMaxPeers>
 __global__ void __launch_bounds__(kRingConeThreads, 1) k_ring_cone(const RingArgs a, double* __restrict__ series,
-                                                                  const int LB) {
+                                                                  const int LB, const double* __restrict__ rowsT,
+                                                                  const double* __restrict__ zpT) {
     using Sh = RingConeShape<S>;
     constexpr int P = Sh::kP, PS = Sh::kPS;
     extern __shared__ __align__(16) double smem[];
@@ -125,12 +135,12 @@ __global__ void __launch_bounds__(kRingConeThreads, 1) k_ring_cone(const RingArg
             const int ws = __shfl_sync(0xffffffffu, w, wj);
             cp_async16(&tails[wj * TS + f * PS + 2 * cc], a.in[f] + static_cast<size_t>(ws) * N + (N - PS) + 2 * cc);
         }
+        // rows: interior b, c_su, c_sv + face[1], transposed per wall (k_ring_cone_rows):
+        // consecutive lanes read consecutive walls
+        {
+            const int n_walls = Z * W;
 #pragma unroll
-        for (int r = 0; r < 12 * !(RC_SKIP & 2); ++r) {
-            const int m = r * 32 + lane, wj = m / 12, k = m - wj * 12;
-            const int ws = __shfl_sync(0xffffffffu, w, wj);
-            const int src = k == 0 ? 0 : k == 1 ? 3 : k == 2 ? 5 : 15 + k;   // in.b, in.c_su, in.c_sv, face[1][0..8]
-            cp_async8(&rows[wj * RS + k], reinterpret_cast<const double*>(a.coef + ws) + src);
+            for (int k = 0; k < 12 * !(RC_SKIP & 2); ++k) rows[lane * RS + k] = rowsT[static_cast<size_t>(k) * n_walls + w];
         }
         asm volatile("cp.async.commit_group;\n" ::);
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -206,33 +216,34 @@ __global__ void __launch_bounds__(kRingConeThreads, 1) k_ring_cone(const RingArg
         const bool live = i >= 1 && i < L - 1;
         const bool owned = i >= S && i < S + nown;
         const int zg = gz(valid ? i : 0);
-        const double* zp = a.zparams + static_cast<size_t>((RC_SKIP & 4) ? 0 : zg) * kRingZP;
+        // parameter k of zone z at zpT[k Z + z]: consecutive lanes read consecutive zones
+        auto zpv = [&](int k) { return zpT[static_cast<size_t>(k) * Z + ((RC_SKIP & 4) ? 0 : zg)]; };
         int nlink = 0, npeer = 0, sidx = 0;
         if (live) {
-            nlink = static_cast<int>(zp[4]);
-            npeer = static_cast<int>(zp[5]);
-            sidx = static_cast<int>(zp[6]);
+            nlink = static_cast<int>(zpv(4));
+            npeer = static_cast<int>(zpv(5));
+            sidx = static_cast<int>(zpv(6));
         }
         int ls[NL], pidx[NP];
-        const double c0 = zp[0], gv = zp[1], qv1 = zp[2], qv2 = zp[3];
+        const double c0 = zpv(0), gv = zpv(1), qv1 = zpv(2), qv2 = zpv(3);
         double lT[NL], lM[NL], lD[NL], pg[NP], pq1[NP], pq2[NP];
         const int iv = valid ? i : 0;
 #pragma unroll
         for (int q = 0; q < NL; ++q) {
-            const int wi = q < nlink ? static_cast<int>(zp[8 + 4 * q]) : 0;
+            const int wi = q < nlink ? static_cast<int>(zpv(8 + 4 * q)) : 0;
             ls[q] = wi * LB + iv;
-            lT[q] = zp[9 + 4 * q];
-            lM[q] = zp[10 + 4 * q];
-            lD[q] = zp[11 + 4 * q];
+            lT[q] = zpv(9 + 4 * q);
+            lM[q] = zpv(10 + 4 * q);
+            lD[q] = zpv(11 + 4 * q);
         }
         const int zprev = gz(iv >= 1 ? iv - 1 : 0);
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
-            const int pz = q < npeer ? static_cast<int>(zp[40 + 4 * q]) : -1;
+            const int pz = q < npeer ? static_cast<int>(zpv(40 + 4 * q)) : -1;
             pidx[q] = live ? (zprev == pz ? iv - 1 : iv + 1) : 0;   // the adjacent copy
-            pg[q] = zp[41 + 4 * q];
-            pq1[q] = zp[42 + 4 * q];
-            pq2[q] = zp[43 + 4 * q];
+            pg[q] = zpv(41 + 4 * q);
+            pq1[q] = zpv(42 + 4 * q);
+            pq2[q] = zpv(43 + 4 * q);
         }
         if (valid) {
             smem[ar_ix(0, 0, i)] = a.zu_in[zg];

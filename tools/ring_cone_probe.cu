@@ -51,6 +51,14 @@ int main(int argc, char** argv) {
     for (auto& w : wc) coupled_coef(g, 1.0 / (N - 1), 1e-3, bb, bb, w);
     cudaMalloc(&coef, sizeof(WallCoef) * walls);
     cudaMemcpy(coef, wc.data(), sizeof(WallCoef) * walls, cudaMemcpyHostToDevice);
+    double *rowsT, *zpT;
+    cudaMalloc(&rowsT, sizeof(double) * 12 * walls);
+    k_ring_cone_rows<<<(walls + 127) / 128, 128>>>(walls, coef, rowsT);
+    std::vector<double> zt(zpar.size());
+    for (int z = 0; z < Z; ++z)
+        for (int k = 0; k < kRingZP; ++k) zt[static_cast<size_t>(k) * Z + z] = zpar[static_cast<size_t>(z) * kRingZP + k];
+    cudaMalloc(&zpT, zt.size() * 8);
+    cudaMemcpy(zpT, zt.data(), zt.size() * 8, cudaMemcpyHostToDevice);
     cudaMalloc(&stop, 4);
     cudaMemset(stop, 0, 4);
     RingArgs a{};
@@ -73,7 +81,7 @@ int main(int argc, char** argv) {
     for (int r = 0; r < reps + 5; ++r) {
         a.zu_in = zu[r & 1]; a.zv_in = zv[r & 1]; a.zu_out = zu[1 - (r & 1)]; a.zv_out = zv[1 - (r & 1)];
         cudaEventRecord(e0);
-        k<<<grid, threads, smem>>>(a, series, lb);
+        k<<<grid, threads, smem>>>(a, series, lb, rowsT, zpT);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;

@@ -20,11 +20,21 @@ int main(int argc, char** argv) {
     Attach* attach;
     int* stop;
     std::vector<double> ones(cells, 1.0);
+    // argv[2]: byte skew between the eight arrays (carved from one allocation), 0: separate cudaMallocs
+    const size_t skew = argc > 2 ? strtoull(argv[2], nullptr, 10) : 0;
+    char* pool = nullptr;
+    if (skew) cudaMalloc(&pool, 8 * (cells * 8 + skew) + (1 << 21));
     for (int f = 0; f < 4; ++f) {
-        cudaMalloc(&in[f], cells * 8);
-        cudaMalloc(&out[f], cells * 8);
+        if (skew) {
+            in[f] = reinterpret_cast<double*>(pool + (2 * f) * (cells * 8 + skew));
+            out[f] = reinterpret_cast<double*>(pool + (2 * f + 1) * (cells * 8 + skew));
+        } else {
+            cudaMalloc(&in[f], cells * 8);
+            cudaMalloc(&out[f], cells * 8);
+        }
         cudaMemcpy(in[f], ones.data(), cells * 8, cudaMemcpyHostToDevice);
     }
+    printf("in0 %p in1 %p out0 %p\n", (void*)in[0], (void*)in[1], (void*)out[0]);
     std::vector<double> ser(static_cast<size_t>(Z) * S * 2, 1.0), tab(S * 4, 1.0);
     cudaMalloc(&series, ser.size() * 8);
     cudaMemcpy(series, ser.data(), ser.size() * 8, cudaMemcpyHostToDevice);
