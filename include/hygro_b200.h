@@ -353,11 +353,13 @@ int64_t hyg_launch_count(hyg_ctx* ctx);
  * HYG_TUNE_RING_GRID: cap on the persistent zone-ring kernel's grid (K4r,
  * k_ring_reg.cuh; 0 = one CTA per SM).  A cap below the number of zone blocks
  * makes every CTA walk several blocks, so small rings under test run the
- * next-block prefetch path the full-size ring runs.  HYG_TUNE_RING_KERNEL
- * picks the zone-ring kernel: 0 = automatic (K4r k_ring_reg.cuh where it
- * applies), 1 = K4r, 2 = K4 (k_ring.cuh), 3 = K5 (k_ring_pipe.cuh: S = 12,
- * trimmed halo, named-barrier hand-off; bitwise K4r, measured slower), for
- * A/B measurement and cross-checks.  HYG_TUNE_MATERIAL_EXACT = 1 evaluates
+ * next-block prefetch path the full-size ring runs (for K6 it caps the walls
+ * kernel's grid, so every warp walks several wall pairs).  HYG_TUNE_RING_KERNEL
+ * picks the zone-ring kernel: 0 = automatic (K6 k_ring_split.cuh where it
+ * applies: zone air + wall cones first, then every wall in registers), 1 = K4r
+ * (k_ring_reg.cuh), 2 = K4 (k_ring.cuh), 3 = K5 (k_ring_pipe.cuh: S = 12,
+ * trimmed halo, named-barrier hand-off), 4 = K6; all bitwise equal, for A/B
+ * measurement and cross-checks.  HYG_TUNE_MATERIAL_EXACT = 1 evaluates
  * the load-bearing material with the accurate exp/log/pow of hyg_crmath.cuh
  * (glibc's roundings in all but rare cases), the reference's expressions and
  * IEEE divisions — ~8x slower than the default (0) table-driven evaluation with

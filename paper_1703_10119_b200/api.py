@@ -492,7 +492,7 @@ class Context:
 
     def set_tuning(self, knob: str, value: int) -> None:
         """Launch-shape knob (hyg_set_tuning): ring_grid = cap on the persistent
-        zone-ring grid; ring_kernel = 0 auto (K4r), 1 K4r, 2 K4, 3 K5; material_exact = 1 for
+        zone-ring grid; ring_kernel = 0 auto (K6), 1 K4r, 2 K4, 3 K5, 4 K6; material_exact = 1 for
         the accurate material evaluation (hyg_crmath.cuh) instead of the fast one."""
         _check(self.lib.hyg_set_tuning(self.h, self.TUNING[knob], int(value)), None, "hyg_set_tuning")
 
