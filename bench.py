@@ -90,6 +90,8 @@ def parse():
     p.add_argument("--ring-kernel", type=int, default=0, help="cfg3: 0 auto (K6), 1 K4r, 2 K4, 3 K5, 4 K6 (A/B runs)")
     p.add_argument("--material-exact", action="store_true",
                    help="cfg5: the parity material evaluation (hyg_crmath.cuh) instead of the default fast one")
+    p.add_argument("--tiled-load", type=int, default=0,
+                   help="cfg4: 0 TMA tiles (k_dv_tiled_tma), 1 per-lane cp.async (k_dv_tiled_stream) (A/B runs)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-sharded", action="store_true",
                    help="skip the strong-scaling block (cfg4 x-slabs, cfg3 zone blocks) of the default cfg1 line")
@@ -341,6 +343,8 @@ class Runner:
                 self.ctx.set_tuning("ring_kernel", args.ring_kernel)
             if args.material_exact:
                 self.ctx.set_tuning("material_exact", 1)
+            if args.tiled_load:
+                self.ctx.set_tuning("tiled_load", args.tiled_load)
             for ch, (first, tab) in w.tables.items():
                 self.ctx.set_channel_table(ch, first, tab)
             self.ctx.set_state(**w.init)

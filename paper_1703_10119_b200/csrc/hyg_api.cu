@@ -201,6 +201,9 @@ struct hyg_ctx {
     bool fused = false;        // K1: constant exterior walls on a fused grid
     bool nl_fused = false;     // K2: analytic d(v) exterior walls, n <= 1024
     bool tiled = false;        // K3: one long analytic d(v) exterior wall, n > 1024
+    TiledMaps tmaps[2];        // K3w: tensor maps of the state arrays s64[b][0..3] (rows of 8 nodes, 64-byte swizzle)
+    bool tmaps_ok = false;     // cuTensorMapEncodeTiled succeeded for all eight
+    int tiled_load = 0;        // HYG_TUNE_TILED_LOAD: 0 TMA tiles (k_dv_tiled_tma), 1 cp.async (k_dv_tiled_stream)
     bool fo_m_pos = true;      // every wall has Fo_M > 0 (K2/K3 scale by 2 Fo_M dt/dx^2)
     bool flux = true;
     int seg_len = 4096;
@@ -343,6 +346,36 @@ int sm_count(int device) {
     int& x = n[device & (kMaxDevices - 1)];
     if (!x) cudaDeviceGetAttribute(&x, cudaDevAttrMultiProcessorCount, device);
     return std::max(x, 1);
+}
+
+// ---- tensor maps (driver entry point through the runtime: libcuda is not linked) ----
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// a state array of n fp64 nodes as rows of 8 nodes (64 B), boxes of 32 rows (one K3w
+// window), 64-byte swizzle (k_dv_tiled_tma)
+bool make_row_map(CUtensorMap* m, double* base, int64_t n) {
+    EncodeTiledFn fn = encode_tiled_fn();
+    if (!fn || n < 8 * 32) return false;
+    const cuuint64_t dims[2] = {8, static_cast<cuuint64_t>(n / 8)};
+    const cuuint64_t strides[1] = {64};
+    const cuuint32_t box[2] = {8, 32};
+    const cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // ---- K1 dispatch -------------------------------------------------------------
@@ -1032,8 +1065,10 @@ int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
         // persistent interior kernel: as many CTAs as fit at once (each warp
         // walks the windows with a stride of all warps), 16-byte stores need
         // 16-byte aligned windows: T and NPT even, the buffers 256-byte aligned
+        const bool tma = c->tmaps_ok && c->tiled_load == 0;
         int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dv_tiled_stream<kTileNPT, kK3MinB>, kDvWarps * 32, 0);
+        if (tma) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dv_tiled_tma<kTileNPT, kK3MinB>, kDvWarps * 32, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dv_tiled_stream<kTileNPT, kK3MinB>, kDvWarps * 32, 0);
         per_sm = std::max(per_sm, 1);
         const int n_sm = sm_count(c->device);
         const int grid = static_cast<int>(std::min<int64_t>((tr - 1 + kDvWarps - 1) / kDvWarps,
@@ -1054,7 +1089,8 @@ int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
             }
             {
                 LaunchScope ls(c, "df_analytic_tiled", mid_cells * a.steps);
-                if (grid > 0) k_dv_tiled_stream<kTileNPT, kK3MinB><<<grid, kDvWarps * 32, 0, c->stream>>>(a);
+                if (grid > 0 && tma) k_dv_tiled_tma<kTileNPT, kK3MinB><<<grid, kDvWarps * 32, 0, c->stream>>>(a, c->tmaps[from]);
+                else if (grid > 0) k_dv_tiled_stream<kTileNPT, kK3MinB><<<grid, kDvWarps * 32, 0, c->stream>>>(a);
             }
             LaunchScope ls(c, "df_analytic_tiled_faces", face_cells * a.steps);
             k_dv_tiled<kTileNPT, true><<<1, kDvWarps * 32, 0, c->stream>>>(a);
@@ -1648,6 +1684,12 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
             if (c->precision == HYG_F32 && cudaMalloc(&c->s32[b][i], cells * sizeof(float)) != cudaSuccess)
                 return fail("state alloc");
         }
+    if (c->tiled && kTileNPT == 8) {
+        c->tmaps_ok = true;
+        for (int b = 0; b < 2; ++b)
+            for (int i = 0; i < 4; ++i)
+                c->tmaps_ok = c->tmaps_ok && make_row_map(&c->tmaps[b].m[i], c->s64[b][i], static_cast<int64_t>(cells));
+    }
     if (cudaMalloc(&c->d_groups, sizeof(Groups) * c->n_walls) != cudaSuccess ||
         cudaMalloc(&c->d_biot, sizeof(Biot) * 2 * c->n_walls) != cudaSuccess ||
         cudaMalloc(&c->d_attach, sizeof(Attach) * 2 * c->n_walls) != cudaSuccess ||
@@ -2430,6 +2472,10 @@ int hyg_set_tuning(hyg_ctx* c, int32_t knob, int64_t value) {
         case HYG_TUNE_RING_KERNEL:
             if (value > 4) return HYG_EINVAL;
             c->ring_kernel = static_cast<int>(value);
+            return HYG_OK;
+        case HYG_TUNE_TILED_LOAD:
+            if (value > 1) return HYG_EINVAL;
+            c->tiled_load = static_cast<int>(value);
             return HYG_OK;
         case HYG_TUNE_MATERIAL_EXACT:
             if (value > 1) return HYG_EINVAL;

@@ -41,6 +41,7 @@
 // or 16 would halve it but exceed 255 registers).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "k_nonlinear.cuh"
@@ -628,6 +629,133 @@ __global__ void __launch_bounds__(kDvWarps * 32, MINB) k_dv_tiled_stream(const T
             vc[j] = buf[3][i];
         }
         __syncwarp();
+        if (t + stride < tr) prefetch(t + stride);
+        int k = 0;
+        for (; k + 1 < A.steps; k += 2) {
+            dv_step<NPT, NPT, false>(vp, vc, up, uc, L, r, fc, q, s_tab, Ambient{}, acc);
+            dv_step<NPT, NPT, false>(vc, vp, uc, up, L, r, fc, q, s_tab, Ambient{}, acc);
+        }
+        if (k < A.steps) {
+            dv_step<NPT, NPT, false>(vp, vc, up, uc, L, r, fc, q, s_tab, Ambient{}, acc);
+#pragma unroll
+            for (int j = 0; j < NPT; ++j) {
+                double x = vp[j]; vp[j] = vc[j]; vc[j] = x;
+                x = up[j]; up[j] = uc[j]; uc[j] = x;
+            }
+        }
+        if (store) {   // lanes 1..30: NPT consecutive owned nodes, 16-byte stores
+            const int64_t i0 = t * T + lane * NPT;
+#pragma unroll
+            for (int j = 0; j < NPT; j += 2) {
+                reinterpret_cast<double2*>(A.out[0] + i0)[j / 2] = make_double2(up[j], up[j + 1]);
+                reinterpret_cast<double2*>(A.out[1] + i0)[j / 2] = make_double2(uc[j], uc[j + 1]);
+                reinterpret_cast<double2*>(A.out[2] + i0)[j / 2] = make_double2(vp[j], vp[j + 1]);
+                reinterpret_cast<double2*>(A.out[3] + i0)[j / 2] = make_double2(vc[j], vc[j + 1]);
+            }
+        }
+    }
+    const unsigned any = __reduce_or_sync(0xffffffffu, store ? acc : 0u);
+    if ((any & 0x40000000u) && lane == 0) atomicCAS(A.suspect, 0, A.seg_index + 1);
+}
+
+
+// ---- K3w with TMA-staged windows ------------------------------------------------------
+// The four layers of a window arrive as 2-D tiles on the TMA engine (UTMALDG):
+// each state array is described to the hardware as rows of NPT = 8 nodes (64 B),
+// a window is a box of 32 rows (W = 256 nodes, 2 KB), and the 64-byte swizzle
+// mode stores 16-byte chunk c of row r at chunk c ^ ((r / 2) mod 4).  Lane l owns
+// row l, so its four 16-byte reads hit eight distinct bank groups per quarter
+// warp in register order — no per-lane copies (64 LDGSTS per window in
+// k_dv_tiled_stream), no swizzled address arithmetic, no select network.  One
+// elected lane issues the four copies of the warp's NEXT window on the warp's
+// mbarrier while the current window is marched in registers.
+struct TiledMaps { CUtensorMap m[4]; };   // the launch's input layers (up, uc, vp, vc)
+
+__device__ __forceinline__ unsigned dv_smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void dv_mbar_init(void* mb, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(dv_smem_u32(mb)), "r"(count));
+}
+__device__ __forceinline__ void dv_mbar_expect_tx(void* mb, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(dv_smem_u32(mb)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void dv_mbar_wait(void* mb, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n DV_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra DV_WAIT_%=;\n}\n" ::"r"(dv_smem_u32(mb)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void dv_tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, void* mb) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            dv_smem_u32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(dv_smem_u32(mb))
+        : "memory");
+}
+
+template <int NPT, int MINB = 0>
+__global__ void __launch_bounds__(kDvWarps * 32, MINB) k_dv_tiled_tma(const TiledArgs A,
+                                                                      const __grid_constant__ TiledMaps M) {
+    using G = DvTiles<NPT>;
+    constexpr int W = G::W, T = G::T;
+    static_assert(NPT == 8, "a row of the tensor maps is NPT = 8 nodes (64-byte swizzle)");
+    __shared__ double s_tab_rep[64 * kExpRep];
+    const double* s_tab = s_tab_rep + (threadIdx.x & (kExpRep - 1));   // this lane's copy
+    __shared__ __align__(1024) double s_buf[kDvWarps][4][W];           // 2 KB tiles, swizzle period 512 B
+    __shared__ __align__(8) unsigned long long s_mbar[kDvWarps];
+    if (launch_stopped(A.stop)) return;
+    stage_exp_table_rep(s_tab_rep, threadIdx.x, blockDim.x);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (lane == 0) {
+        dv_mbar_init(&s_mbar[warp], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t tr = G::rface(A.n);
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * kDvWarps;
+    int64_t t = 1 + static_cast<int64_t>(blockIdx.x) * kDvWarps + warp;
+    if (t >= tr) return;
+    double(*buf)[W] = s_buf[warp];
+    void* mbar = &s_mbar[warp];
+    auto prefetch = [&](int64_t tt) {
+        if (lane == 0) {
+            dv_mbar_expect_tx(mbar, 4u * W * sizeof(double));
+            const int row = static_cast<int>(tt * (T / NPT));          // window start tt T = row tt T / 8
+#pragma unroll
+            for (int f = 0; f < 4; ++f) dv_tma_load_2d(buf[f], &M.m[f], 0, row, mbar);
+        }
+    };
+    prefetch(t);
+    const AnalyticRow rc = analytic_row(A.groups, A.dx, A.dt);
+    const DvRow r = dv_row(rc);
+    const DvParams q = dv_params(A.p, 2.0 * rc.a);
+    const DvFace fc{};
+    DvLane L;
+    L.rev = lane == 31;
+    L.mirror0 = L.rev;
+    L.face = false;
+    const bool store = lane != 0 && lane != 31;      // the stale lanes stay out of the guard and the output
+    const int sw = (lane >> 1) & 3;                  // this row's chunk swizzle
+    unsigned acc = 0;
+    for (int it = 0; t < tr; t += stride, ++it) {
+        double up[NPT], uc[NPT], vp[NPT], vc[NPT];
+        dv_mbar_wait(mbar, it & 1);
+        auto rd = [&](int f, double (&x)[NPT]) {
+            double tv[NPT];
+#pragma unroll
+            for (int c = 0; c < NPT / 2; ++c) {
+                const double2 v = *reinterpret_cast<const double2*>(&buf[f][lane * NPT + 2 * (c ^ sw)]);
+                tv[2 * c] = v.x;
+                tv[2 * c + 1] = v.y;
+            }
+#pragma unroll
+            for (int j = 0; j < NPT; ++j) x[j] = L.rev ? tv[NPT - 1 - j] : tv[j];
+        };
+        rd(0, up);
+        rd(1, uc);
+        rd(2, vp);
+        rd(3, vc);
+        __syncwarp();                                // the tiles are free for the next window
         if (t + stride < tr) prefetch(t + stride);
         int k = 0;
         for (; k + 1 < A.steps; k += 2) {

@@ -1,9 +1,9 @@
 """Race evidence without compute-sanitizer (closed on this GPU pool: the
 sanitizer run prints that runs under it have left GPUs needing a reset,
 profiles/r02_sanitizer_attempt.txt): a shared-memory or barrier race in the
-kernels that stage data asynchronously (K4r / K5: bulk copies + mbarriers +
-cp.async + named barriers; K2h: shared refresh every H steps; K3w: cp.async
-prefetch into per-warp buffers; the material step's shared tables) shows up as
+kernels that stage data asynchronously (K6 / K4r / K5: bulk copies + mbarriers +
+cp.async + named barriers; K2h: shared refresh every H steps; K3w: TMA tiles or
+cp.async prefetch into per-warp buffers; the material step's shared tables) shows up as
 run-to-run or launch-shape-dependent results.  Each case runs repeatedly and
 under different persistent-grid caps; every output must be bitwise identical."""
 import numpy as np
@@ -49,6 +49,17 @@ def test_dv_kernels_repeatable():
     w4 = workloads.long_domain(n_nodes=1 << 18, nsteps=120)        # K3w, persistent (several windows per warp)
     a, b = _run(w4, 120), _run(w4, 120)
     assert _same(a, b)
+
+
+def test_long_wall_tma_tiles_equal_cp_async():
+    """K3w's two window-staging paths — 2-D TMA tiles through tensor maps with the
+    64-byte swizzle (k_dv_tiled_tma, the default) and per-lane cp.async copies
+    (k_dv_tiled_stream) — are bitwise equal, at a size where every persistent warp
+    walks several windows and at a node count that is not a multiple of 8."""
+    for n in (1 << 18, (1 << 17) + 1234):
+        w4 = workloads.long_domain(n_nodes=n, nsteps=120)
+        a, b, c = _run(w4, 120, (("tiled_load", 0),)), _run(w4, 120, (("tiled_load", 1),)), _run(w4, 120)
+        assert _same(a, b) and _same(a, c)
 
 
 def test_material_step_repeatable():
