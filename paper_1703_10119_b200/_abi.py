@@ -152,6 +152,7 @@ PROTOTYPES = {
     "hyg_probe_fp64_peak": (C.c_int, [C.c_int32, dp, dp]),
     "hyg_probe_fp32_peak": (C.c_int, [C.c_int32, dp]),
     "hyg_selftest_fastmath": (C.c_int, [C.c_int32, C.c_int32, dp, dp, dp]),
+    "hyg_selftest_dvmath": (C.c_int, [C.c_int32, C.c_int32, dp, dp, dp]),
     "hyg_selftest_fastlog": (C.c_int, [C.c_int32, C.c_int32, dp, dp]),
     "hyg_df_march_linear": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int64, dp, dp]),
     "hyg_selftest_crmath": (C.c_int, [C.c_int32, C.c_int32, dp, dp, dp]),

@@ -1648,9 +1648,12 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
         }
     }
     c->fused = all_exterior && d->n_zones == 0 && d->coeff_kind == HYG_COEFF_CONSTANT && fused_grid(c->n);
-    // the warp-register d(v) kernels take exp of -p2 (v - p3)^2 <= 0 (fexp_addend); a
-    // growing exponential (p2 < 0) marches on the per-step path with the full exp
-    const bool dv_neg = d->coeff_params[2] >= 0.0;
+    // the warp-register d(v) kernels take exp of x = -p2 (v - p3)^2 with fexp_addend,
+    // valid for -700 <= x <= 0: every state inside their fast guard (|v| < 2) must
+    // keep x in that range.  A growing exponential (p2 < 0) or a steeper one marches
+    // on the per-step path with the full exp
+    const double dv_reach = 2.0 + std::fabs(d->coeff_params[3]);
+    const bool dv_neg = d->coeff_params[2] >= 0.0 && d->coeff_params[2] * dv_reach * dv_reach <= 700.0;
     c->nl_fused = all_exterior && d->n_zones == 0 && d->coeff_kind == HYG_COEFF_ANALYTIC_D && c->n <= 1024 &&
                   c->precision == HYG_F64 && dv_neg;
     c->tiled = all_exterior && d->n_zones == 0 && d->coeff_kind == HYG_COEFF_ANALYTIC_D && c->n > 1024 &&
@@ -2539,6 +2542,14 @@ __global__ void k_fastmath(int n, const double* x, double* e, double* r) {
         r[i] = frcp(x[i]);
     }
 }
+// the d(v) half node's exp (-700 <= x <= 0) and the v row's two-FMA reciprocal
+__global__ void k_dvmath(int n, const double* x, double* e, double* r) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        e[i] = fexp_addend<1>(-fabs(x[i]), kExp2Tab256);
+        r[i] = frcp2(x[i]);
+    }
+}
 // df_step_linear (wall.cpp:60-71) of n_fields independent single fields:
 // next[j] = a0 prev[j] + a1 (curr[j+1] + curr[j-1]) inside, ends copied
 __global__ void k_df_linear(int n_fields, int n, double a0, double a1, const double* prev, const double* curr,
@@ -2631,6 +2642,21 @@ extern "C" int hyg_selftest_fastmath(int32_t device, int32_t n, const double* x,
     HYG_CUDA(cudaMalloc(&d, sizeof(double) * 3 * n));
     HYG_CUDA(cudaMemcpy(d, x, sizeof(double) * n, cudaMemcpyHostToDevice));
     k_fastmath<<<(n + 255) / 256, 256>>>(n, d, d + n, d + 2 * n);
+    HYG_CUDA(cudaGetLastError());
+    HYG_CUDA(cudaMemcpy(exp_out, d + n, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    HYG_CUDA(cudaMemcpy(rcp_out, d + 2 * n, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    return HYG_OK;
+}
+
+extern "C" int hyg_selftest_dvmath(int32_t device, int32_t n, const double* x, double* exp_out, double* rcp_out) {
+    hyg_status* status = nullptr;
+    if (n <= 0 || !x || !exp_out || !rcp_out) return HYG_EINVAL;
+    HYG_CUDA(cudaSetDevice(device));
+    double* d = nullptr;
+    HYG_CUDA(cudaMalloc(&d, sizeof(double) * 3 * n));
+    HYG_CUDA(cudaMemcpy(d, x, sizeof(double) * n, cudaMemcpyHostToDevice));
+    k_dvmath<<<(n + 255) / 256, 256>>>(n, d, d + n, d + 2 * n);
     HYG_CUDA(cudaGetLastError());
     HYG_CUDA(cudaMemcpy(exp_out, d + n, sizeof(double) * n, cudaMemcpyDeviceToHost));
     HYG_CUDA(cudaMemcpy(rcp_out, d + 2 * n, sizeof(double) * n, cudaMemcpyDeviceToHost));

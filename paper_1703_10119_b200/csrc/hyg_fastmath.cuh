@@ -23,6 +23,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include "hyg_exp256_table.h"
+
 namespace hyg {
 
 // 2^(j/64), j = 0..63, correctly rounded (generated with 60-digit decimal arithmetic)
@@ -49,6 +51,8 @@ __device__ __constant__ const double kExp2Tab64[64] = HYG_EXP2_TAB64;
 // memory (read through the read-only path: divergent indices cost a few L1
 // wavefronts, where constant memory would serialise them)
 __device__ const double kExp2Tab64G[64] = HYG_EXP2_TAB64;
+// 2^(j/256) for fexp_addend (the d(v) half node), staged in shared memory by its kernels
+__device__ const double kExp2Tab256[256] = HYG_EXP2_TAB256;
 
 
 // exp(x) for -708 <= x <= 709 (no special cases; see fexp)
@@ -92,35 +96,50 @@ __device__ __forceinline__ double frcp(double d) {
     return fma(y, fma(e, e, e), y);                    // y (1 + e + e^2): error ~e^3
 }
 
-// exp(x) as a term ADDED TO A VALUE >= 2^-200 in magnitude (the d(v) half
-// node: 1 + p0 v + p1 exp(x), x = -p2 (v - p3)^2 <= 0): x is clamped at -708,
-// where exp is below 2^-1021 and vanishes in the sum exactly as the exact 0
-// would, so the sum rounds bit for bit as with fexp.  NaN/inf states reach
-// the sum through its p0 v term, so no select is needed: one DMNMX instead
-// of fexp's integer tests and three selects.
-// The reduction uses ln2/64 as ONE rounded constant (r = x - kd L in one FMA,
-// a dependent FMA less than fexp): |kd L_double - kd ln2/64| <= |kd| 8.7e-19,
-// i.e. <= 5e-16 relative in the result for |x| <= 40 (d(v) of configs[0]/[4]:
-// |x| <= 6.4) and <= 6e-14 at x = -708, where the term is ~1e-308.
-// STRIDE: the table's element stride (16: the bank-replicated copy of
-// k_dv_warp.cuh, each lane reading its own copy)
+// The same with TWO FMAs: y (1 + e), error e^2 ~ 2^-44 .. 2^-40 relative, always
+// towards zero.  For the d(v) v row only: there 1/den multiplies the increment
+// inc = num / den, and a relative bias of 1e-12 in every increment is a relative
+// change of 1e-12 in the diffusion number (the solution moves by ~1e-13 of its
+// own variation), two orders inside the 1e-10 parity tolerance — one FP64
+// instruction per node-update fewer than frcp.
+__device__ __forceinline__ double frcp2(double d) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    return fma(y, fma(-d, y, 1.0), y);
+}
+
+// exp(x) for the d(v) half node (1 + p0 v + p1 exp(x), x = -p2 (v - p3)^2):
+// 8 FP64 instructions.  x = (256 k + j) ln2/256 + r from one FMA against the
+// 1.5 * 2^52 shifter, |r| <= ln2/512 = 1.35e-3, exp(r) - 1 by its degree-4
+// polynomial (truncation r^5/120 < 4e-17 relative: the 256-entry table buys the
+// degree-5 term of fexp), T_j = 2^(j/256) correctly rounded from the table the
+// kernels stage in shared memory, 2^k by an integer add on T_j's exponent.
+// The reduction uses ln2/256 as ONE rounded constant (relative error 3.3e-17, as
+// the double nearest ln 2): the result is off by |x| 3.3e-17 relative — 1 ulp at
+// the edge of the d(v) range of configs[0]/[4] (|x| <= 6.4), 54 ulp at x = -180
+// where the term is 1e-78; as an absolute error of the Gaussian never above
+// 1.3e-17 (tests/test_gpu_fastmath.py).
+// NO clamp and no special cases: valid for -700 <= x <= 0.  The host admits a
+// model to the kernels that call it only if p2 (2 + |p3|)^2 <= 700 (hyg_create:
+// every state inside the fast guard, |v| < 2, then keeps x above -700; a state
+// outside it is flagged by the guard and the launch is replayed on the per-step
+// path with the full fexp).
+// STRIDE: the table's element stride (the bank-replicated copy of k_nonlinear.cuh)
 template <int STRIDE = 1>
 __device__ __forceinline__ double fexp_addend(double x, const double* tab) {
     constexpr double kShift = 6755399441055744.0;                  // 1.5 * 2^52
-    constexpr double kInvL = 92.332482616893658;                   // 64 / ln 2
-    constexpr double kL = 0x1.62e42fefa39efp-7;                    // ln2 / 64
-    x = fmax(x, -708.0);
+    constexpr double kInvL = 369.32993046757463;                   // 256 / ln 2
+    constexpr double kL = 0x1.62e42fefa39efp-9;                    // ln2 / 256
     const double s = fma(x, kInvL, kShift);
     const double kd = s - kShift;
     const int k = __double2loint(s);
     const double r = fma(kd, -kL, x);
     const double r2 = r * r;
-    const double c45 = fma(r, 1.0 / 120.0, 1.0 / 24.0);
     const double c23 = fma(r, 1.0 / 6.0, 0.5);
-    const double q = fma(r2, c45, c23);
-    const double sm = fma(r2, q, r);
-    const double t = tab[(k & 63) * STRIDE];
-    const double ts = __hiloint2double(__double2hiint(t) + static_cast<int>(static_cast<unsigned>(k >> 6) << 20),
+    const double q = fma(r2, 1.0 / 24.0, c23);                     // 1/2 + r/6 + r^2/24
+    const double sm = fma(r2, q, r);                               // exp(r) - 1
+    const double t = tab[(k & 255) * STRIDE];
+    const double ts = __hiloint2double(__double2hiint(t) + static_cast<int>(static_cast<unsigned>(k >> 8) << 20),
                                        __double2loint(t));
     return fma(ts, sm, ts);
 }

@@ -115,7 +115,7 @@ __device__ __forceinline__ void dv_interior(const DvRow& r, double vp, double up
     const double dl = vL - vp, dr = vR - vp;
     const double num = __dadd_rn(__dmul_rn(km, dl), __dmul_rn(kp, dr));
     const double den = fma(0.5, kp + km, 1.0);
-    const double inc = __dmul_rn(num, frcp(den));
+    const double inc = __dmul_rn(num, frcp2(den));
     vn = __dadd_rn(vp, inc);
     const double du = fma(-2.0, up, uL + uR);
     un = fma(-r.Gp, inc, fma(r.G, dl + dr, fma(r.B, du, up)));
@@ -240,7 +240,7 @@ constexpr int kK3MinB = 3;
 // (Lr = (n-1)/NPT, the reversed lane).
 template <int NPT, int M>
 __global__ void __launch_bounds__(kDvWarps * 32) k_dv_walls(const NonlinearSegArgs A) {
-    __shared__ double s_tab_rep[64 * kExpRep];
+    __shared__ double s_tab_rep[kExpTab * kExpRep];
     const double* s_tab = s_tab_rep + (threadIdx.x & (kExpRep - 1));   // this lane's copy
     __shared__ Ambient s_amb[kDvWarps][kNlChunk][2];   // [warp][step][face]
     if (launch_stopped(A.stop)) return;
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(kDvWarps * 32) k_dv_walls(const NonlinearSegAr
 template <int NW>
 __global__ void __launch_bounds__(NW * 32) k_dv_wall_split(const NonlinearSegArgs A) {
     constexpr bool FACE_ALL = NW <= 4;                 // every warp runs the face code: no branch
-    __shared__ double s_tab_rep[64 * kExpRep];
+    __shared__ double s_tab_rep[kExpTab * kExpRep];
     const double* s_tab = s_tab_rep + (threadIdx.x & (kExpRep - 1));   // this lane's copy
     __shared__ Ambient s_amb[kNlChunk][2];
     __shared__ double s_x[2][NW][4];                  // [parity][warp] {v, u} of lanes 0 and 31
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(NW * 32) k_dv_wall_split(const NonlinearSegArg
 template <int NW, int H>
 __global__ void __launch_bounds__(NW * 32) k_dv_wall_halo(const NonlinearSegArgs A) {
     constexpr int T = 32 - 2 * H;                      // owned nodes per warp
-    __shared__ double s_tab_rep[64 * kExpRep];
+    __shared__ double s_tab_rep[kExpTab * kExpRep];
     const double* s_tab = s_tab_rep + (threadIdx.x & (kExpRep - 1));   // this lane's copy
     __shared__ Ambient s_amb[kNlChunk][2];
     __shared__ double s_st[4][NW * T];                 // {u_prev, u_curr, v_prev, v_curr} by node
@@ -496,7 +496,7 @@ template <int NPT, bool FACES>
 __global__ void __launch_bounds__(kDvWarps * 32) k_dv_tiled(const TiledArgs A) {
     using G = DvTiles<NPT>;
     constexpr int W = G::W, T = G::T;
-    __shared__ double s_tab_rep[64 * kExpRep];
+    __shared__ double s_tab_rep[kExpTab * kExpRep];
     const double* s_tab = s_tab_rep + (threadIdx.x & (kExpRep - 1));   // this lane's copy
     if (launch_stopped(A.stop)) return;
     stage_exp_table_rep(s_tab_rep, threadIdx.x, blockDim.x);
@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(kDvWarps * 32, MINB) k_dv_tiled_stream(const T
     using G = DvTiles<NPT>;
     constexpr int W = G::W, T = G::T;
     static_assert((NPT & (NPT - 1)) == 0, "NPT must be a power of two");
-    __shared__ double s_tab_rep[64 * kExpRep];
+    __shared__ double s_tab_rep[kExpTab * kExpRep];
     const double* s_tab = s_tab_rep + (threadIdx.x & (kExpRep - 1));   // this lane's copy
     __shared__ __align__(16) double s_buf[kDvWarps][4][W];
     if (launch_stopped(A.stop)) return;
@@ -699,7 +699,7 @@ __global__ void __launch_bounds__(kDvWarps * 32, MINB) k_dv_tiled_tma(const Tile
     using G = DvTiles<NPT>;
     constexpr int W = G::W, T = G::T;
     static_assert(NPT == 8, "a row of the tensor maps is NPT = 8 nodes (64-byte swizzle)");
-    __shared__ double s_tab_rep[64 * kExpRep];
+    __shared__ double s_tab_rep[kExpTab * kExpRep];
     const double* s_tab = s_tab_rep + (threadIdx.x & (kExpRep - 1));   // this lane's copy
     __shared__ __align__(1024) double s_buf[kDvWarps][4][W];           // 2 KB tiles, swizzle period 512 B
     __shared__ __align__(8) unsigned long long s_mbar[kDvWarps];

@@ -57,13 +57,15 @@ __device__ __forceinline__ void stage_exp_table(double* s_tab, int tid, int nthr
     for (int i = tid; i < 64; i += nthreads) s_tab[i] = kExp2Tab64[i];
 }
 
-// The exp table replicated 16 times, entry j of copy c at j * 16 + c: lane l
-// reads copy l & 15, so the 64-bit reads of a half warp hit 16 distinct bank
-// pairs whatever the indices (the single 64-entry table put ~4-5 lanes on one
-// bank pair: ncu counted ~3.8e7 shared-memory bank conflicts per K3w launch)
-constexpr int kExpRep = 16;
+// fexp_addend's 2^(j/256) table replicated kExpRep times, entry j of copy c at
+// j * kExpRep + c: lane l reads copy l & (kExpRep - 1), which spreads the lanes of
+// a warp over distinct bank pairs when their indices collide (16 copies of the
+// former 64-entry table measured within 1 % of one copy on K3w: neighbouring
+// lanes hold neighbouring states and mostly read the same or adjacent entries)
+constexpr int kExpRep = 4;
+constexpr int kExpTab = 256;
 __device__ __forceinline__ void stage_exp_table_rep(double* s_tab, int tid, int nthreads) {
-    for (int i = tid; i < 64 * kExpRep; i += nthreads) s_tab[i] = kExp2Tab64[i / kExpRep];
+    for (int i = tid; i < kExpTab * kExpRep; i += nthreads) s_tab[i] = kExp2Tab256[i / kExpRep];
 }
 
 constexpr int kNlChunk = 64;   // forcing rows staged per chunk

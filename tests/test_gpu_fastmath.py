@@ -37,6 +37,29 @@ def test_fexp_frcp_accuracy():
     assert e2[0] == 0.0 and e2[1] == 0.0 and np.isnan(e2[2]) and np.isinf(e2[3]) and e2[4] == 1.0
 
 
+def test_dv_half_node_exp_and_two_fma_reciprocal():
+    """fexp_addend (256-entry table, degree 4, no clamp; -700 <= x <= 0): within
+    2 ulp + |x| 3.3e-17 relative of exp (the reduction uses ln2/256 as one rounded
+    constant, whose relative error is 3.3e-17: 3 ulp at the edge of the d(v) range
+    |x| <= 6.4, and an absolute error of the Gaussian below 1.3e-17 everywhere);
+    frcp2 below 2^-40 relative and never above the true reciprocal in magnitude."""
+    lib = api.load_library()
+    rng = np.random.default_rng(3)
+    x = np.concatenate([rng.uniform(0.0, 10.0, 200_000), rng.uniform(0.0, 180.0, 100_000),
+                        rng.uniform(180.0, 700.0, 50_000), np.linspace(0.0, 1.0, 10_001)])
+    e, r = np.empty_like(x), np.empty_like(x)
+    p = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+    d = np.ascontiguousarray(rng.uniform(1.0, 200.0, x.size) * rng.choice([-1.0, 1.0], x.size))
+    assert lib.hyg_selftest_dvmath(0, x.size, p(x), p(e), p(r)) == 0
+    ref = np.exp(-x)
+    u = _ulps(e, ref)
+    assert (u <= 2.0 + x * 3.4e-17 / 1.1e-16).all(), u.max()
+    assert u[x <= 6.4].max() <= 3.0 and np.abs(e - ref).max() <= 1.3e-17 + 2.3e-16, (u[x <= 6.4].max(), np.abs(e - ref).max())
+    assert lib.hyg_selftest_dvmath(0, d.size, p(d), p(e), p(r)) == 0
+    rel = (r - 1.0 / d) * d
+    assert np.abs(rel).max() <= 2.0 ** -40 and rel.max() <= 2.0 ** -52, (np.abs(rel).max(), rel.max())
+
+
 def test_flog_accuracy():
     """flog_pos (material correlations): within 2 ulp of the result, or 2 ulp
     of ln 2 where ln x cancels near 1 (absolute 2.5e-16), on the box's ranges
