@@ -1,5 +1,5 @@
 #!/bin/bash
-# round 2 full pass: GPU tests + smoke, bench lines for every config (with the CPU
+# round 2 full pass (cfg3 on K6, cfg4 on TMA tiles): GPU tests + smoke, bench lines for every config (with the CPU
 # baselines), the reference arm (cfg1, cfg3), ncu launch lists and one --set full
 # capture per config's dominant kernel (each ncu command only after its plain run
 # exited 0).  Output under gpurun_out/$1.
@@ -17,6 +17,8 @@ for c in cfg0 cfg2 cfg3 cfg4 cfg5; do
   timeout 900 python bench.py --config $c --steps 3 --warmup 3 > $O/bench_$c.json 2> $O/bench_$c.err
 done
 timeout 600 python bench.py --config cfg3 --steps 3 --warmup 2 --ring-kernel 3 --no-cpu-baseline --no-e2e > $O/bench_cfg3_k5.json 2> $O/bench_cfg3_k5.err
+timeout 600 python bench.py --config cfg3 --steps 3 --warmup 2 --ring-kernel 1 --no-cpu-baseline --no-e2e > $O/bench_cfg3_k4r.json 2> $O/bench_cfg3_k4r.err
+timeout 600 python bench.py --config cfg4 --steps 3 --warmup 2 --tiled-load 1 --no-cpu-baseline --no-e2e > $O/bench_cfg4_cpasync.json 2> $O/bench_cfg4_cpasync.err
 timeout 600 python bench.py --config cfg5 --steps 3 --warmup 2 --material-exact --no-cpu-baseline --no-e2e > $O/bench_cfg5_exact.json 2> $O/bench_cfg5_exact.err
 timeout 900 python bench.py --impl reference --config cfg3 --steps 3 --warmup 1 > $O/bench_ref_cfg3.json 2> $O/bench_ref_cfg3.err
 echo benches >> $O/status.txt
@@ -37,8 +39,8 @@ for c in "cfg1 4097" "cfg2 4097" "cfg0 4097" "cfg3 41" "cfg4 33" "cfg5 11"; do
 done
 echo lists >> $O/status.txt
 full cfg1 4097 k_df_coupled 0
-full cfg3 41 k_ring_reg 1
-full cfg4 33 k_dv_tiled_stream 2
+full cfg3 41 k_ring_walls 1
+full cfg4 33 k_dv_tiled_tma 2
 full cfg0 4097 k_dv_wall_halo 0
 full cfg5 11 k_material_step 3
 echo done >> $O/status.txt
