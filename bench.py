@@ -49,16 +49,20 @@ CONFIGS = {
                  run_steps=100_000),
     "cfg2": dict(flop=14, bytes=0, bound="fp32", kernel="df_coupled_fused_f32", scaling="weak", dtype="f32",
                  run_steps=100_000),
-    # cfg3 runs K6 (k_ring_split.cuh: the zone air + wall cones of S = 8 steps first,
-    # then every wall in registers): per zone and launch 64 B x 768 nodes (walls) +
-    # 4 layers x 80 B x 6 walls x 72/56 (cone tails, halo copies included) + 128 B
-    # (air series), over 768 x 8 updates = 8.40 B/update; K4r (--ring-kernel 1,
+    # cfg3 runs K6 (k_ring_split.cuh: zone air + wall cones in launches of 8 steps, then
+    # every wall in registers for 16 steps): per zone and walls launch 64 B x 768 nodes
+    # (walls) + 2 x 4 layers x 80 B x 6 walls x 72/56 (cone tails, halo copies included)
+    # + 4 x (144 + 80) B x 6 walls (stub: tails read, compact tails written) + 256 B (air
+    # series), over 768 x 16 updates = 4.86 B/update — so its bound is SURVEY §8(d)'s:
+    # FP64 (14.1 flop/update), with the HBM fraction of its own traffic beside (the walls
+    # kernel alone: 64 B per node + 256 B per zone over 16 steps = 4.02 B/update);
+    # --ring-depth 1 (8 steps per walls launch): 8.40 B/update; K4r (--ring-kernel 1,
     # k_ring_reg.cuh: B = 4 zones per block, S = 8 steps per launch):
     # (64 B x 3072 owned + 32 B x 756 halo nodes) / (3072 x 8) = 8.98 B/update; K5
     # (--ring-kernel 3, k_ring_pipe.cuh: B = 3, S = 12, halo trimmed to the cone):
     # (64 B x 2304 + 32 B x 864) / (2304 x 12) = 6.33 B/update
-    "cfg3": dict(flop=14.1, bytes=8.98, bound="hbm", kernel="ring_walls", scaling="strong", dtype="f64",
-                 run_steps=80_000, bytes_by_kernel={"ring_pipe": 6.33, "ring_reg": 8.98, "ring_walls": 8.40}),
+    "cfg3": dict(flop=14.1, bytes=4.86, bound="fp64", kernel="ring_walls", scaling="strong", dtype="f64",
+                 run_steps=80_000, bytes_by_kernel={"ring_pipe": 6.33, "ring_reg": 8.98, "ring_walls": 4.02}),
     # cfg4 runs the temporally blocked K3w (k_dv_warp.cuh: 256-node windows, 8 steps
     # per launch, (32 x 256 + 32 x 240) / (240 x 8) = 8.27 B/update), so min(HBM,
     # FP64) is the FP64 side; sharded (N>1) every slab runs K3w too
@@ -90,6 +94,8 @@ def parse():
     p.add_argument("--ring-kernel", type=int, default=0, help="cfg3: 0 auto (K6), 1 K4r, 2 K4, 3 K5, 4 K6 (A/B runs)")
     p.add_argument("--material-exact", action="store_true",
                    help="cfg5: the parity material evaluation (hyg_crmath.cuh) instead of the default fast one")
+    p.add_argument("--ring-depth", type=int, default=0,
+                   help="cfg3, K6: cone launches (8 steps each) per walls launch, 1..3 (0: library default) (A/B runs)")
     p.add_argument("--tiled-load", type=int, default=0,
                    help="cfg4: 0 TMA tiles (k_dv_tiled_tma), 1 per-lane cp.async (k_dv_tiled_stream) (A/B runs)")
     p.add_argument("--no-e2e", action="store_true")
@@ -345,6 +351,8 @@ class Runner:
                 self.ctx.set_tuning("material_exact", 1)
             if args.tiled_load:
                 self.ctx.set_tuning("tiled_load", args.tiled_load)
+            if args.ring_depth:
+                self.ctx.set_tuning("ring_depth", args.ring_depth)
             for ch, (first, tab) in w.tables.items():
                 self.ctx.set_channel_table(ch, first, tab)
             self.ctx.set_state(**w.init)
@@ -451,6 +459,14 @@ def main():
         achieved, peak, unit = kernel_rate * cfg["flop"] / 1e12, peak64, "TFLOP/s"
         peak_src = ("DFMA probe measured in this run (MEASURED_PEAKS.json has no FP64 figure); "
                     "nominal 148 SM x 64 x 2 x 1.965 GHz = 37.2")
+        if bytes_per_update:
+            # the same kernel against the HBM roofline of its own algorithmic traffic
+            try:
+                hbm = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+            except Exception:
+                hbm = 6650.0
+            extra = {"hbm_achieved_gbs": kernel_rate * bytes_per_update / 1e9, "hbm_peak_gbs": hbm,
+                     "hbm_frac": kernel_rate * bytes_per_update / 1e9 / hbm}
         if args.config == "cfg0":
             peak = peak64 / 148.0
             peak_src = "one SM's share of the DFMA probe (a single wall is one dependency chain per step)"

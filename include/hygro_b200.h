@@ -367,12 +367,16 @@ int64_t hyg_launch_count(hyg_ctx* ctx);
  * the reference within its own conditioning: on the ill-conditioned
  * wall_nonlinear fixture (a 1-ulp change of one initial value moves the
  * reference by 8e-10) they differ from it by 9.6e-10 (exact) and 1.7e-9
- * (default); on the other fixtures and tests by ~1e-14.  HYG_TUNE_TILED_LOAD picks how the long-wall
+ * (default); on the other fixtures and tests by ~1e-14.  HYG_TUNE_RING_DEPTH = m (1..3) makes K6's
+ * walls kernel march m x 8 steps per launch, fed by m cone launches (the later
+ * ones on tails a stub kernel marches ahead); bitwise equal for every m.
+ * HYG_TUNE_TILED_LOAD picks how the long-wall
  * kernel K3w stages its windows: 0 = 2-D tiles on the TMA engine through tensor
  * maps of the state arrays (k_dv_tiled_tma), 1 = per-lane cp.async copies
  * (k_dv_tiled_stream); bitwise equal.  HYG_EINVAL for an unknown knob or a
  * negative value. */
-enum { HYG_TUNE_RING_GRID = 1, HYG_TUNE_RING_KERNEL = 2, HYG_TUNE_MATERIAL_EXACT = 3, HYG_TUNE_TILED_LOAD = 4 };
+enum { HYG_TUNE_RING_GRID = 1, HYG_TUNE_RING_KERNEL = 2, HYG_TUNE_MATERIAL_EXACT = 3, HYG_TUNE_TILED_LOAD = 4,
+       HYG_TUNE_RING_DEPTH = 5 };
 int hyg_set_tuning(hyg_ctx* ctx, int32_t knob, int64_t value);
 
 /* Device FP64 FMA throughput probe (DFMA loop), TFLOP/s counting FMA = 2. */

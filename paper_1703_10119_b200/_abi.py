@@ -16,7 +16,7 @@ HYG_COEFF_CONSTANT, HYG_COEFF_ANALYTIC_D, HYG_COEFF_MATERIAL = 0, 1, 2
 HYG_F64, HYG_F32 = 0, 1
 HYG_BOOT_IMPLICIT, HYG_BOOT_EXPLICIT = 0, 1
 HYG_SCHEME_DF, HYG_SCHEME_EULER_IMPLICIT, HYG_SCHEME_EULER_EXPLICIT = 0, 1, 2
-HYG_TUNE_RING_GRID, HYG_TUNE_RING_KERNEL, HYG_TUNE_MATERIAL_EXACT, HYG_TUNE_TILED_LOAD = 1, 2, 3, 4
+HYG_TUNE_RING_GRID, HYG_TUNE_RING_KERNEL, HYG_TUNE_MATERIAL_EXACT, HYG_TUNE_TILED_LOAD, HYG_TUNE_RING_DEPTH = 1, 2, 3, 4, 5
 
 dp = C.POINTER(C.c_double)
 

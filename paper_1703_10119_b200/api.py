@@ -488,7 +488,8 @@ class Context:
         return out
 
     TUNING = {"ring_grid": A.HYG_TUNE_RING_GRID, "ring_kernel": A.HYG_TUNE_RING_KERNEL,
-              "material_exact": A.HYG_TUNE_MATERIAL_EXACT, "tiled_load": A.HYG_TUNE_TILED_LOAD}
+              "material_exact": A.HYG_TUNE_MATERIAL_EXACT, "tiled_load": A.HYG_TUNE_TILED_LOAD,
+              "ring_depth": A.HYG_TUNE_RING_DEPTH}
 
     def set_tuning(self, knob: str, value: int) -> None:
         """Launch-shape knob (hyg_set_tuning): ring_grid = cap on the persistent

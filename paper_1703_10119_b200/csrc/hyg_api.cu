@@ -52,7 +52,12 @@ constexpr int kRingPipeS = HYG_RING_PIPE_S; // K5: steps per launch
 #define HYG_RING_AUTO 4
 #endif
 constexpr int kRingAuto = HYG_RING_AUTO;         // the zone-ring kernel HYG_TUNE_RING_KERNEL = 0 selects (4: K6, 1: K4r)
-constexpr int kRingSplitS = HYG_RING_SPLIT_S;   // K6 (k_ring_split.cuh): steps per launch pair
+constexpr int kRingSplitS = HYG_RING_SPLIT_S;   // K6 (k_ring_split.cuh): steps per cone launch
+#ifndef HYG_RING_SPLIT_M
+#define HYG_RING_SPLIT_M 2
+#endif
+constexpr int kRingSplitM = HYG_RING_SPLIT_M;   // K6: cone launches per walls launch (walls march M x S steps), default
+constexpr int kRingSplitMaxM = 3;
 constexpr int kWarps = 4;       // warps per CTA of K1
 
 struct SigHost {
@@ -234,6 +239,9 @@ struct hyg_ctx {
     double* d_ring_rowsT = nullptr;  // K6 phase 1: cone rows transposed [12][walls] for rows_dt (k_ring_cone_rows)
     double* d_ring_zpT = nullptr;    // K6 phase 1: the zone parameter blocks transposed [kRingZP][zones]
     double rows_dt = -1.0;
+    int ring_split_m = kRingSplitM;  // HYG_TUNE_RING_DEPTH: cone launches (of kRingSplitS steps) per walls launch, 1..3
+    double* d_ring_tail[2][4] = {};  // K6: compact tails between the cone launches of one walls launch (k_ring_stub)
+    double* d_ring_zt[2][2] = {};    // K6: zone air between those cone launches [buffer][u, v]
     double* d_ring_series = nullptr; // K6: layer-k air of every zone for the S steps of a launch [zones][S][2]
     bool mat_exact = false;          // HYG_TUNE_MATERIAL_EXACT: CrMath evaluation + IEEE-division rows
     bool owned_partial = false;      // hyg_set_owned narrowed the guard to a shard's range
@@ -1146,20 +1154,28 @@ void launch_ring_pipe(const RingArgs& a, size_t smem, cudaStream_t s, int device
 // K6 (k_ring_split.cuh): phase 1 (zone air + wall cones, records the air series),
 // then phase 2 (every wall in registers, no barrier per step)
 void launch_ring_cone(const RingArgs& a, double* series, int LB, bool small, cudaStream_t s, int device,
-                      const double* rowsT, const double* zpT) {
+                      const double* rowsT, const double* zpT, const ConeIO& io) {
     using Sh = RingConeShape<kRingSplitS>;
     auto k = small ? k_ring_cone<kRingSplitS, 6, 2> : k_ring_cone<kRingSplitS>;
     const int rw = RingShape<8, kRingSplitS>::row_width(a.n_channels, a.n_sources);
     const size_t smem = Sh::smem_doubles(LB, a.W, rw) * sizeof(double);
     ensure_smem_attr(k, device, 227 * 1024);
     const int OB = LB - 2 * kRingSplitS;
-    k<<<(a.n_zones + OB - 1) / OB, Sh::threads(LB, a.W), smem, s>>>(a, series, LB, rowsT, zpT);
+    k<<<(a.n_zones + OB - 1) / OB, Sh::threads(LB, a.W), smem, s>>>(a, series, LB, rowsT, zpT, io);
 }
 
-template <int NPT>
-void launch_ring_walls(const RingArgs& a, const double* series, cudaStream_t s, int device, int grid_cap) {
-    auto k = k_ring_walls<NPT, kRingSplitS>;
-    const size_t smem = RingWallShape<NPT>::smem_doubles(kRingSplitS, a.n_channels, kRingWallWarps) * sizeof(double);
+// tails of depth DIN (state arrays or a previous stub's output) -> tails of depth DIN - S, S steps later
+template <int DIN>
+void launch_ring_stub(const RingArgs& a, const double* series, const double* rowsT, const ConeIO& in,
+                      double* const (&out)[4], cudaStream_t s, int /*device*/) {
+    const int walls = a.n_zones * a.W;
+    k_ring_stub<DIN, kRingSplitS><<<(walls + 127) / 128, 128, 0, s>>>(a, series, rowsT, in, out[0], out[1], out[2], out[3]);
+}
+
+template <int NPT, int SW>
+void launch_ring_walls_sw(const RingArgs& a, const double* series, cudaStream_t s, int device, int grid_cap) {
+    auto k = k_ring_walls<NPT, SW>;
+    const size_t smem = RingWallShape<NPT>::smem_doubles(SW, a.n_channels, kRingWallWarps) * sizeof(double);
     ensure_smem_attr(k, device, 100 * 1024);
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * kRingWallWarps, smem);
@@ -1167,6 +1183,14 @@ void launch_ring_walls(const RingArgs& a, const double* series, cudaStream_t s, 
     int grid = std::max(1, std::min(nblk, std::max(per_sm, 1) * sm_count(device)));
     if (grid_cap > 0) grid = std::min(grid, grid_cap);   // HYG_TUNE_RING_GRID: several pairs per warp in small rings
     k<<<grid, 32 * kRingWallWarps, smem, s>>>(a, series);
+}
+
+// m: cone launches per walls launch (the series row of a zone has m S slots)
+template <int NPT>
+void launch_ring_walls(const RingArgs& a, const double* series, cudaStream_t s, int device, int grid_cap, int m) {
+    if (m == 1) launch_ring_walls_sw<NPT, kRingSplitS>(a, series, s, device, grid_cap);
+    else if (m == 2) launch_ring_walls_sw<NPT, 2 * kRingSplitS>(a, series, s, device, grid_cap);
+    else launch_ring_walls_sw<NPT, 3 * kRingSplitS>(a, series, s, device, grid_cap);
 }
 
 template <int NPT>
@@ -1204,7 +1228,8 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool
     const int B = pipe ? c->ring_pipe_B : reg ? c->ring_reg_B : c->ring_B;
     const int grid = (Z + B - 1) / B;
     const int rw = RingShape<8, kRingS>::row_width(nch, nsrc);
-    const int S = split ? kRingSplitS : pipe ? kRingPipeS : reg ? kRingRegS : kRingS;   // steps per launch
+    const int split_m = std::min(std::max(c->ring_split_m, 1), kRingSplitMaxM);
+    const int S = split ? split_m * kRingSplitS : pipe ? kRingPipeS : reg ? kRingRegS : kRingS;   // steps per launch
     const int threads = reg ? RingRegShape<8, kRingRegS>::threads(B, W) : RingShape<8, kRingS>::threads(B, W);
     const size_t smem = pipe ? RingPipeShape<kRingPipeS>::smem_doubles(B, W, rw) * sizeof(double)
                         : reg ? RingRegShape<8, kRingRegS>::smem_doubles(B, W, c->n, rw) * sizeof(double)
@@ -1260,14 +1285,46 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool
             a.zu_out = c->zu[1 - zf];
             a.zv_out = c->zv[1 - zf];
             if (split) {
-                {
+                // a.steps <= m S steps: one cone launch per S steps (the later ones on the
+                // tails k_ring_stub marches from the launch's input), then the walls
+                constexpr int CS = kRingSplitS, PS = RingConeShape<kRingSplitS>::kPS;
+                const int steps = a.steps, nsub = (steps + CS - 1) / CS;
+                ConeIO io{};
+                io.ser_stride = S;
+                for (int j = 0; j < nsub; ++j) {
+                    if (j == 0) {
+                        for (int i = 0; i < 4; ++i) io.tin[i] = a.in[i];
+                        io.tstride = c->n;
+                    } else {
+                        // tails at the start of cone launch j: depth 9 + 8 (nsub - 1 - j), from depth + 8
+                        ConeIO sin = io;                 // the previous launch's tails source and series slots
+                        const int din = PS - 1 + CS * (nsub - j);   // depth at the start of launch j - 1
+                        const int ds = (din + 1) & ~1;
+                        sin.toff = j == 1 ? c->n - ds : 0;       // the state arrays' last ds nodes, else a whole tail row
+                        LaunchScope ls(c, "ring_stub", 0.0);
+                        if (din == PS - 1 + CS) launch_ring_stub<PS - 1 + CS>(a, c->d_ring_series, c->d_ring_rowsT, sin, c->d_ring_tail[j & 1], c->stream, c->device);
+                        else launch_ring_stub<PS - 1 + 2 * CS>(a, c->d_ring_series, c->d_ring_rowsT, sin, c->d_ring_tail[j & 1], c->stream, c->device);
+                        for (int i = 0; i < 4; ++i) io.tin[i] = c->d_ring_tail[j & 1][i];
+                        io.tstride = (din - CS + 1) & ~1;
+                    }
+                    // this launch reads the last PS nodes of its tails
+                    io.toff = io.tstride - PS;
+                    io.ser_off = j * CS;
+                    RingArgs ac = a;
+                    ac.steps = std::min(CS, steps - j * CS);
+                    ac.table = a.table + static_cast<size_t>(j) * CS * nch;
+                    ac.src = a.src + static_cast<size_t>(j) * CS * (3 * nsrc + 2);
+                    ac.zu_in = j == 0 ? a.zu_in : c->d_ring_zt[(j - 1) & 1][0];
+                    ac.zv_in = j == 0 ? a.zv_in : c->d_ring_zt[(j - 1) & 1][1];
+                    ac.zu_out = j == nsub - 1 ? a.zu_out : c->d_ring_zt[j & 1][0];
+                    ac.zv_out = j == nsub - 1 ? a.zv_out : c->d_ring_zt[j & 1][1];
                     LaunchScope ls(c, "ring_cone", 0.0);
-                    launch_ring_cone(a, c->d_ring_series, c->ring_cone_LB, c->ring_reg_small, c->stream, c->device,
-                                     c->d_ring_rowsT, c->d_ring_zpT);
+                    launch_ring_cone(ac, c->d_ring_series, c->ring_cone_LB, c->ring_reg_small, c->stream, c->device,
+                                     c->d_ring_rowsT, c->d_ring_zpT, io);
                 }
                 LaunchScope ls(c, "ring_walls", static_cast<double>(c->cells()) * a.steps);
-                if (npt == 4) launch_ring_walls<4>(a, c->d_ring_series, c->stream, c->device, c->ring_grid_cap);
-                else launch_ring_walls<8>(a, c->d_ring_series, c->stream, c->device, c->ring_grid_cap);
+                if (npt == 4) launch_ring_walls<4>(a, c->d_ring_series, c->stream, c->device, c->ring_grid_cap, split_m);
+                else launch_ring_walls<8>(a, c->d_ring_series, c->stream, c->device, c->ring_grid_cap, split_m);
                 continue;
             }
             LaunchScope ls(c, pipe ? "ring_pipe" : reg ? "ring_reg" : "ring_tiled", static_cast<double>(c->cells()) * a.steps);
@@ -1776,7 +1833,15 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
                 std::vector<double> zpT(zp.size());
                 for (size_t z = 0; z < Zn; ++z)
                     for (int k = 0; k < kRingZP; ++k) zpT[k * Zn + z] = zp[z * kRingZP + k];
-                if (cudaMalloc(&c->d_ring_series, sizeof(double) * Zn * kRingSplitS * 2) != cudaSuccess ||
+                constexpr int kTailMax = (RingConeShape<kRingSplitS>::kP + kRingSplitS * (kRingSplitMaxM - 2) + 1) & ~1;
+                for (int b = 0; b < 2; ++b) {
+                    for (int i = 0; i < 4; ++i)
+                        if (cudaMalloc(&c->d_ring_tail[b][i], sizeof(double) * c->n_walls * kTailMax) != cudaSuccess)
+                            return fail("zone alloc");
+                    for (int i = 0; i < 2; ++i)
+                        if (cudaMalloc(&c->d_ring_zt[b][i], sizeof(double) * Zn) != cudaSuccess) return fail("zone alloc");
+                }
+                if (cudaMalloc(&c->d_ring_series, sizeof(double) * Zn * kRingSplitS * kRingSplitMaxM * 2) != cudaSuccess ||
                     cudaMalloc(&c->d_ring_rowsT, sizeof(double) * 12 * c->n_walls) != cudaSuccess ||
                     cudaMalloc(&c->d_ring_zpT, sizeof(double) * zpT.size()) != cudaSuccess)
                     return fail("zone alloc");
@@ -1828,6 +1893,10 @@ void hyg_destroy(hyg_ctx* c) {
     cudaFree(c->d_inz);
     cudaFree(c->d_ring_zp);
     cudaFree(c->d_ring_series);
+    for (int b = 0; b < 2; ++b) {
+        for (int i = 0; i < 4; ++i) cudaFree(c->d_ring_tail[b][i]);
+        for (int i = 0; i < 2; ++i) cudaFree(c->d_ring_zt[b][i]);
+    }
     cudaFree(c->d_ring_rowsT);
     cudaFree(c->d_ring_zpT);
     cudaFree(c->d_table);
@@ -2475,6 +2544,10 @@ int hyg_set_tuning(hyg_ctx* c, int32_t knob, int64_t value) {
         case HYG_TUNE_RING_KERNEL:
             if (value > 4) return HYG_EINVAL;
             c->ring_kernel = static_cast<int>(value);
+            return HYG_OK;
+        case HYG_TUNE_RING_DEPTH:
+            if (value < 1 || value > kRingSplitMaxM) return HYG_EINVAL;
+            c->ring_split_m = static_cast<int>(value);
             return HYG_OK;
         case HYG_TUNE_TILED_LOAD:
             if (value > 1) return HYG_EINVAL;

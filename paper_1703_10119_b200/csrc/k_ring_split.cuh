@@ -31,6 +31,7 @@
 // replays from the flagged launch's untouched input with K4 (exact guard).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "k_ring_reg.cuh"
@@ -84,16 +85,28 @@ __global__ void k_ring_cone_rows(int n_walls, const WallCoef* __restrict__ coef,
     for (int k = 0; k < 12; ++k) rowsT[static_cast<size_t>(k) * n_walls + w] = c[k == 0 ? 0 : k == 1 ? 3 : k == 2 ? 5 : 15 + k];
 }
 
+// Where a cone launch finds its tails and puts its air series.  The walls kernel
+// may march SW = m S steps per launch (m = 1, 2, 3): then m cone launches of S
+// steps fill the slots [ser_off, ser_off + S) of a zone's SW-slot series row,
+// the first from the state arrays (tails = the last nodes of every wall: stride
+// n, offset n - PS), the later ones from the compact tail arrays k_ring_stub
+// leaves behind (stride PS, offset 0).
+struct ConeIO {
+    const double* tin[4];          // up, uc, vp, vc
+    int tstride, toff;             // tail of wall w: tin[f] + w tstride + toff, PS nodes
+    int ser_stride, ser_off;       // series slots per zone, first slot of this launch
+};
+
 // ---- phase 1 ---------------------------------------------------------------------------
 template <int S, int NL = kRingMaxLinks, int NP = kRingMaxPeers>
 __global__ void __launch_bounds__(kRingConeThreads, 1) k_ring_cone(const RingArgs a, double* __restrict__ series,
                                                                   const int LB, const double* __restrict__ rowsT,
-                                                                  const double* __restrict__ zpT) {
+                                                                  const double* __restrict__ zpT, const ConeIO io) {
     using Sh = RingConeShape<S>;
     constexpr int P = Sh::kP, PS = Sh::kPS;
     extern __shared__ __align__(16) double smem[];
     if (launch_stopped(a.stop)) return;
-    const int W = a.W, Z = a.n_zones, N = a.n;
+    const int W = a.W, Z = a.n_zones;
     const int OB = LB - 2 * S;                          // owned zones per CTA
     const int z0 = blockIdx.x * OB, nown = min(OB, Z - z0), L = nown + 2 * S;
     const int rw = RingShape<8, S>::row_width(a.n_channels, a.n_sources);
@@ -133,7 +146,7 @@ __global__ void __launch_bounds__(kRingConeThreads, 1) k_ring_cone(const RingArg
         for (int r = 0; r < CPW * !(RC_SKIP & 2); ++r) {
             const int m = r * 32 + lane, wj = m / CPW, fc = m - wj * CPW, f = fc / (PS / 2), cc = fc - f * (PS / 2);
             const int ws = __shfl_sync(0xffffffffu, w, wj);
-            cp_async16(&tails[wj * TS + f * PS + 2 * cc], a.in[f] + static_cast<size_t>(ws) * N + (N - PS) + 2 * cc);
+            cp_async16(&tails[wj * TS + f * PS + 2 * cc], io.tin[f] + static_cast<size_t>(ws) * io.tstride + io.toff + 2 * cc);
         }
         // rows: interior b, c_su, c_sv + face[1], transposed per wall (k_ring_cone_rows):
         // consecutive lanes read consecutive walls
@@ -249,7 +262,7 @@ __global__ void __launch_bounds__(kRingConeThreads, 1) k_ring_cone(const RingArg
             smem[ar_ix(0, 0, i)] = a.zu_in[zg];
             smem[ar_ix(0, 1, i)] = a.zv_in[zg];
         }
-        double* ser = series + static_cast<size_t>(zg) * S * 2;
+        double* ser = series + (static_cast<size_t>(zg) * io.ser_stride + io.ser_off) * 2;
         __syncthreads();
         for (int k = (RC_SKIP & 1) ? a.steps : 0; k < a.steps; ++k) {
             if (live && !(RC_SKIP & 8)) {
@@ -289,6 +302,100 @@ __global__ void __launch_bounds__(kRingConeThreads, 1) k_ring_cone(const RingArg
         }
     }
     if (__syncthreads_or((acc & 0x40000000u) != 0u) && tid == 0) atomicCAS(a.stop, 0, a.seg_index + 1);
+}
+
+// ---- tails for the later cone launches of a long walls launch ------------------------------
+// k_ring_stub<DIN>: one thread per wall marches the wall's last DIN nodes (its
+// tail at the start of the previous cone launch, from the state arrays or from the
+// previous stub's output) S steps with the air series that cone launch recorded
+// — the cone arithmetic without the zone coupling — and leaves the last DIN - S
+// nodes, exact at the new time, as the next cone launch's (or stub's) tails.
+// Step k only computes the nodes still needed (p > k: the cut end goes stale one
+// node per step).  Bound by its scattered reads: 144-byte runs out of every 1 KB
+// wall cost 56 MB of DRAM traffic per launch (ncu), ~19 us; staging them by
+// coalesced cp.async through shared memory measured slower (27.6 vs 21.4 us).
+template <int DIN, int S>
+__global__ void __launch_bounds__(128) k_ring_stub(const RingArgs a, const double* __restrict__ series,
+                                                   const double* __restrict__ rowsT, const ConeIO in,
+                                                   double* __restrict__ tout0, double* __restrict__ tout1,
+                                                   double* __restrict__ tout2, double* __restrict__ tout3) {
+    constexpr int DS = (DIN + 1) & ~1;                  // loaded (even: 16-byte loads)
+    constexpr int DOUT = DIN - S, OS = (DOUT + 1) & ~1; // kept, stored
+    static_assert(S % 2 == 0 && S <= 8, "the layers end where they began; unrolled for S <= 8");
+    if (launch_stopped(a.stop)) return;
+    const int n_walls = a.n_zones * a.W;
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= n_walls) return;
+    double up[DIN], uc[DIN], vp[DIN], vc[DIN];
+    auto rd = [&](int f, double (&x)[DIN]) {
+        double t[DS];
+        const double* g = in.tin[f] + static_cast<size_t>(w) * in.tstride + in.toff;
+#pragma unroll
+        for (int q = 0; q < DS / 2; ++q) {
+            const double2 v = *reinterpret_cast<const double2*>(g + 2 * q);
+            t[2 * q] = v.x;
+            t[2 * q + 1] = v.y;
+        }
+#pragma unroll
+        for (int p = 0; p < DIN; ++p) x[p] = t[DS - DIN + p];
+    };
+    rd(0, up);
+    rd(1, uc);
+    rd(2, vp);
+    rd(3, vc);
+    double cf[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) cf[k] = rowsT[static_cast<size_t>(k) * n_walls + w];
+    const double cb = cf[0], csu = cf[1], csv = cf[2];
+    const double fb = cf[3], fe = cf[4], feg = cf[5], fcsu = cf[6], fctu = cf[7], fcsv = cf[8], fctv = cf[9],
+                 fcq = cf[10], fcg = cf[11];
+    const double* ser = series + (static_cast<size_t>(w / a.W) * in.ser_stride + in.ser_off) * 2;
+    // step K (0-based) produces layer K + 1, exact at nodes p >= K + 1
+    auto step = [&](auto KC, double (&vP)[DIN], double (&vC)[DIN], double (&uP)[DIN], double (&uC)[DIN]) {
+        constexpr int K = decltype(KC)::value;
+        const double2 air = *reinterpret_cast<const double2*>(ser + 2 * K);
+        const double u_a = air.x, v_a = air.y;
+#pragma unroll
+        for (int p = K + 1; p < DIN; ++p) {
+            const double vl = vC[p - 1], ul = uC[p - 1];
+            const double vr = p == DIN - 1 ? vC[DIN - 2] : vC[p + 1], ur = p == DIN - 1 ? uC[DIN - 2] : uC[p + 1];
+            const double d = fma(-2.0, vP[p], vl + vr);
+            const double du = fma(-2.0, uP[p], ul + ur);
+            double vn, un;
+            if (p < DIN - 1) {
+                vn = fma(cb, d, vP[p]);
+                un = fma(csv, d, fma(csu, du, uP[p]));
+            } else {
+                const double t = v_a - vP[p], tu = u_a - uP[p];
+                vn = fma(fe, t, fma(fb, d, fma(feg, 0.0, vP[p])));
+                un = fma(fctv, t, fma(fcsv, d, fma(fctu, tu, fma(fcsu, du, fma(fcq, 0.0, fma(fcg, 0.0, uP[p]))))));
+            }
+            vP[p] = vn;
+            uP[p] = un;
+        }
+    };
+    auto two = [&](auto KC) {
+        constexpr int K = decltype(KC)::value;
+        step(std::integral_constant<int, K>{}, vp, vc, up, uc);
+        step(std::integral_constant<int, K + 1>{}, vc, vp, uc, up);
+    };
+    two(std::integral_constant<int, 0>{});
+    if constexpr (S > 2) two(std::integral_constant<int, 2>{});
+    if constexpr (S > 4) two(std::integral_constant<int, 4>{});
+    if constexpr (S > 6) two(std::integral_constant<int, 6>{});
+    // the last OS nodes (the first may be a stale pad node, never read)
+    auto wr = [&](double* t, const double (&x)[DIN]) {
+        double* g = t + static_cast<size_t>(w) * OS;
+#pragma unroll
+        for (int q = 0; q < OS / 2; ++q) {
+            const int p0 = DIN - OS + 2 * q;
+            *reinterpret_cast<double2*>(g + 2 * q) = make_double2(x[p0], x[p0 + 1]);
+        }
+    };
+    wr(tout0, up);
+    wr(tout1, uc);
+    wr(tout2, vp);
+    wr(tout3, vc);
 }
 
 // ---- phase 2 ---------------------------------------------------------------------------

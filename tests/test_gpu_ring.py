@@ -23,13 +23,15 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-10
 
 
-def _gpu(model, init, steps, grid_cap=0, kernel=0):
+def _gpu(model, init, steps, grid_cap=0, kernel=0, depth=0):
     with Context(model) as ctx:
         ctx.set_state(**init)
         if grid_cap:
             ctx.set_tuning("ring_grid", grid_cap)
         if kernel:
             ctx.set_tuning("ring_kernel", kernel)
+        if depth:
+            ctx.set_tuning("ring_depth", depth)   # K6: cone launches (8 steps each) per walls launch
         ctx.profiling(True)
         st = ctx.bootstrap("implicit")
         ctx.advance(steps - 1)
@@ -65,16 +67,22 @@ def _compare(got, b, n_zones):
 # run only when a CTA owns more than one block.  The grid cap forces that in
 # small rings: 42 zones = 11 blocks (the last one partial, 2 zones) over 3
 # CTAs walk 4/4/3 blocks; 64 zones over 2 CTAs walk 8 blocks each.
-@pytest.mark.parametrize("kernel,name", [(0, "ring_walls"), (1, "ring_reg"), (3, "ring_pipe")])
+@pytest.mark.parametrize("kernel,name,depth", [(0, "ring_walls", 0), (0, "ring_walls", 1), (0, "ring_walls", 3),
+                                               (1, "ring_reg", 0), (3, "ring_pipe", 0)])
 @pytest.mark.parametrize("n_zones,cap,steps", [(42, 3, 203), (64, 2, 160), (42, 1, 77), (13, 2, 96)])
-def test_ring_reg_multi_block_per_cta(n_zones, cap, steps, kernel, name):
+def test_ring_reg_multi_block_per_cta(n_zones, cap, steps, kernel, name, depth):
     w = workloads.zone_ring(n_zones=n_zones, walls_per_zone=6, n_nodes=128, nsteps=steps)
     init = _noisy(w, n_zones + cap)
-    got, st, stats = _gpu(w.model, init, steps, grid_cap=cap, kernel=kernel)
+    got, st, stats = _gpu(w.model, init, steps, grid_cap=cap, kernel=kernel, depth=depth)
     assert stats.get(name, {}).get("launches", 0) > 0, stats.keys()
     assert "ring_tiled" not in stats                 # no guard hand-over: the kernel marched every launch
     if kernel == 0:
-        assert stats.get("ring_cone", {}).get("launches", 0) == stats["ring_walls"]["launches"]
+        # K6: one cone launch per 8 steps, one stub between the cone launches of a walls launch
+        m = depth or 2
+        walls, cones = stats["ring_walls"]["launches"], stats["ring_cone"]["launches"]
+        assert walls == -(-(steps - 1) // (8 * m)) and cones == sum(
+            -(-min(8 * m, steps - 1 - s0) // 8) for s0 in range(0, steps - 1, 8 * m))
+        assert stats.get("ring_stub", {}).get("launches", 0) == cones - walls
     b, rc, _, passes = _oracle(w.model, init, steps, nthreads=O.threads())
     assert rc == 0 and st.subiterations == passes
     err, zerr = _compare(got, b, n_zones)
@@ -96,6 +104,11 @@ def test_ring_cfg3_full_ring_1000_steps():
     assert "ring_tiled" not in stats and "ring_reg" not in stats
     got_r, _, stats_r = _gpu(w.model, init, steps, kernel=1)          # K4r on the same input
     assert stats_r.get("ring_reg", {}).get("launches", 0) > 0 and "ring_tiled" not in stats_r
+    for depth in (1, 3):                                               # K6 with 8 and 24 steps per walls launch
+        got_d, _, stats_d = _gpu(w.model, init, steps, depth=depth)
+        assert stats_d.get("ring_walls", {}).get("launches", 0) > 0 and "ring_tiled" not in stats_d
+        for k in ("u_prev", "u_curr", "v_prev", "v_curr", "zone_u", "zone_v"):
+            assert np.array_equal(got[k], got_d[k]), (depth, k)
     got_p, _, stats_p = _gpu(w.model, init, steps, kernel=3)          # K5 on the same input
     assert stats_p.get("ring_pipe", {}).get("launches", 0) > 0
     for k in ("u_prev", "u_curr", "v_prev", "v_curr", "zone_u", "zone_v"):

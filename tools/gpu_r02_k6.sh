@@ -19,6 +19,17 @@ except Exception as e:
     print("kernel $k failed", e); print(open("$O/bench_cfg3_k$k.err").read()[-2000:])
 PY
 done
+for d in ${DEPTHS:-1 2 3}; do
+  timeout 600 python bench.py --config cfg3 --steps 3 --warmup 3 --ring-depth $d --no-cpu-baseline --no-e2e > $O/bench_cfg3_d$d.json 2> $O/bench_cfg3_d$d.err
+  python - <<PY
+import json
+try:
+    d = json.loads(open("$O/bench_cfg3_d$d.json").read().strip().splitlines()[-1])
+    print("depth $d value %.4g  %s rate %.4g share %.3f" % (d["value"], d["roofline"]["kernel"], d["roofline"]["kernel_node_updates_per_s"], d["roofline"]["kernel_share_of_step"]))
+except Exception as e:
+    print("depth $d failed", e); print(open("$O/bench_cfg3_d$d.err").read()[-2000:])
+PY
+done
 for k in ${KERNELS:-0 1}; do
   timeout 300 python tools/profile_target.py cfg3 801 $k prof > $O/stats_k$k.txt 2>&1; cat $O/stats_k$k.txt
 done
