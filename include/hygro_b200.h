@@ -386,7 +386,7 @@ int hyg_probe_fp64_peak(int32_t device, double* tflops, double* sm_clock_mhz);
 int hyg_selftest_fastmath(int32_t device, int32_t n, const double* x, double* exp_out, double* rcp_out);
 /* The d(v) half node's exp and the v row's two-FMA reciprocal (fexp_addend, frcp2):
  * exp_out[i] = exp(-|x[i]|) for |x[i]| <= 700, rcp_out[i] ~ 1/x[i] (relative error
- * below 2^-40, towards zero). */
+ * below 1.1e-12, towards zero). */
 int hyg_selftest_dvmath(int32_t device, int32_t n, const double* x, double* exp_out, double* rcp_out);
 /* Self-test of the device log of the material correlations (flog_pos,
  * hyg_fastmath.cuh; positive normal x): log_out[i] = ln x[i] on the device. */

@@ -1682,13 +1682,17 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
                 // K6 phase 1: LB local zones per CTA (LB - 2 S owned); about one CTA per
                 // SM for long rings, never fewer than min(Z, 8) owned zones
                 using SC = RingConeShape<kRingSplitS>;
-                if (c->n >= 2 * (kRingSplitS + 2)) {
+                // the walls need their deepest stub's tail (26 nodes) inside the wall, the
+                // forcing rows of a launch must fit both kernels' shared memory
+                const size_t walls_smem = RingWallShape<8>::smem_doubles(kRingSplitS * kRingSplitMaxM, nch, kRingWallWarps) * sizeof(double);
+                if (c->n >= RingConeShape<kRingSplitS>::kPS + kRingSplitS * (kRingSplitMaxM - 1) && walls_smem <= 100u * 1024u) {
                     const int rw = RingShape<8, kRingSplitS>::row_width(nch, nsrc);
                     int lb = 2 * kRingSplitS + 1;
                     while (SC::threads(lb + 1, W) <= kRingConeThreads &&
                            SC::smem_doubles(lb + 1, W, rw) * sizeof(double) <= 227u * 1024u)
                         ++lb;
-                    if (SC::threads(lb, W) <= kRingConeThreads) {
+                    if (SC::threads(lb, W) <= kRingConeThreads &&
+                        SC::smem_doubles(lb, W, rw) * sizeof(double) <= 227u * 1024u) {
                         const int nsm = sm_count(c->device);
                         int ob = (Z + nsm - 1) / nsm;
                         ob = std::max(ob, std::min(Z, 8));

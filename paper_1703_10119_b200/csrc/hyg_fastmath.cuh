@@ -96,7 +96,7 @@ __device__ __forceinline__ double frcp(double d) {
     return fma(y, fma(e, e, e), y);                    // y (1 + e + e^2): error ~e^3
 }
 
-// The same with TWO FMAs: y (1 + e), error e^2 ~ 2^-44 .. 2^-40 relative, always
+// The same with TWO FMAs: y (1 + e), error e^2 <= 1e-12 relative (rcp.approx is good to 2^-20), always
 // towards zero.  For the d(v) v row only: there 1/den multiplies the increment
 // inc = num / den, and a relative bias of 1e-12 in every increment is a relative
 // change of 1e-12 in the diffusion number (the solution moves by ~1e-13 of its
