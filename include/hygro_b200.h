@@ -228,6 +228,12 @@ int hyg_set_zones(hyg_ctx* ctx, int32_t zone0, int32_t count, const double* zone
  * synchronisation: a caller that hands the context its communication stream
  * (hyg_set_stream) orders NCCL sends/receives of buf behind and ahead of them
  * by stream order alone.  One launch per call. */
+/* The pack / unpack calls below run on `stream` (a cudaStream_t) instead of the
+ * context's stream; NULL: on the context's stream again.  No implicit ordering:
+ * the caller orders the two streams with events (shard.py: the exchange stream
+ * waits for the interval's compute, hyg_advance_overlapped takes the event
+ * recorded behind the unpack). */
+int hyg_set_exchange_stream(hyg_ctx* ctx, void* stream);
 int hyg_pack_cells(hyg_ctx* ctx, int64_t cell0, int64_t count, double* buf);
 int hyg_unpack_cells(hyg_ctx* ctx, int64_t cell0, int64_t count, const double* buf);
 int hyg_pack_zones(hyg_ctx* ctx, int32_t zone0, int32_t count, double* buf);
@@ -277,6 +283,17 @@ int hyg_bootstrap(hyg_ctx* ctx, int32_t kind, hyg_status* status);
  * layer that passed the guard for every wall and status names the first
  * failing layer and the lowest failing wall index. */
 int hyg_advance(hyg_ctx* ctx, int64_t nsteps, double dt, hyg_status* status);
+/* hyg_advance for a shard whose halo cells are being refreshed on ANOTHER stream
+ * (shard.py: pack -> NCCL -> unpack behind the previous interval): `event` is a
+ * cudaEvent_t recorded on that stream after the refresh of the first edge_lo and
+ * the last edge_hi cells of the context.  On the long-wall path (K3w) the windows
+ * of the first launch that read none of those cells are launched at once — they
+ * march while the exchange is in flight — and the remaining windows, the face
+ * windows and every later launch follow behind the event in stream order; on
+ * every other path the context's stream waits for the event first.  Same results
+ * as hyg_advance after the refresh.  event == NULL: hyg_advance. */
+int hyg_advance_overlapped(hyg_ctx* ctx, int64_t nsteps, double dt, int64_t edge_lo, int64_t edge_hi, void* event,
+                           hyg_status* status);
 
 /* run() building.cpp:303-356: nsteps = lround(horizon/dt); DF bootstrap
  * (`boot_kind`) counted as step 1; frames every lround(cadence/dt) steps and

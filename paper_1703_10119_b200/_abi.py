@@ -135,6 +135,9 @@ PROTOTYPES = {
     "hyg_set_outdoor_table": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, dp]),
     "hyg_bootstrap": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Status)]),
     "hyg_advance": (C.c_int, [C.c_void_p, C.c_int64, C.c_double, C.POINTER(Status)]),
+    "hyg_advance_overlapped": (C.c_int, [C.c_void_p, C.c_int64, C.c_double, C.c_int64, C.c_int64, C.c_void_p,
+                                         C.POINTER(Status)]),
+    "hyg_set_exchange_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "hyg_run": (C.c_int, [C.c_void_p, C.c_double, C.c_double, C.c_int32, FRAME_FN, C.c_void_p, C.POINTER(Status)]),
     "hyg_run_scheme": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, C.c_double, FRAME_FN, C.c_void_p,
                                  C.POINTER(RunReport), C.POINTER(Status)]),

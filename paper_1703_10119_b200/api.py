@@ -438,10 +438,29 @@ class Context:
         _check(self.lib.hyg_bootstrap(self.h, k, C.byref(st)), st, "hyg_bootstrap")
         return st
 
-    def advance(self, nsteps: int, dt: Optional[float] = None) -> A.Status:
+    def advance(self, nsteps: int, dt: Optional[float] = None, edge: Optional[tuple] = None,
+                wait_event=None) -> A.Status:
+        """hyg_advance; with `wait_event` (a torch.cuda.Event or a raw cudaEvent_t recorded
+        behind a halo refresh of the first edge[0] / last edge[1] cells on another stream)
+        hyg_advance_overlapped: the windows clear of those cells march at once."""
         st = A.Status()
-        _check(self.lib.hyg_advance(self.h, int(nsteps), float(dt or 0.0), C.byref(st)), st, "hyg_advance")
+        if wait_event is None:
+            _check(self.lib.hyg_advance(self.h, int(nsteps), float(dt or 0.0), C.byref(st)), st, "hyg_advance")
+            return st
+        ev = getattr(wait_event, "cuda_event", wait_event)
+        ev = getattr(ev, "value", ev)
+        lo, hi = edge or (0, 0)
+        _check(self.lib.hyg_advance_overlapped(self.h, int(nsteps), float(dt or 0.0), int(lo), int(hi),
+                                               C.c_void_p(ev), C.byref(st)), st, "hyg_advance_overlapped")
         return st
+
+    def set_exchange_stream(self, stream=None) -> None:
+        """Pack / unpack kernels (get_cells_into, set_cells_from, get_zones_into,
+        set_zones_from) run on `stream` (torch.cuda.Stream or raw cudaStream_t; None: the
+        context's stream again), with no implicit ordering (hyg_set_exchange_stream)."""
+        ptr = getattr(stream, "cuda_stream", stream)
+        _check(self.lib.hyg_set_exchange_stream(self.h, C.c_void_p(ptr) if ptr else None), None,
+               "hyg_set_exchange_stream")
 
     def run(self, horizon: float, cadence: float = 1e30, boot: str = "implicit",
             frame: Optional[Callable[[int, float, "Context"], None]] = None) -> A.Status:

@@ -208,6 +208,11 @@ struct hyg_ctx {
     bool tiled = false;        // K3: one long analytic d(v) exterior wall, n > 1024
     TiledMaps tmaps[2];        // K3w: tensor maps of the state arrays s64[b][0..3] (rows of 8 nodes, 64-byte swizzle)
     bool tmaps_ok = false;     // cuTensorMapEncodeTiled succeeded for all eight
+    // hyg_advance_overlapped (one-shot, consumed by the next K3w launch): the windows reading
+    // none of the first ov_lo / last ov_hi cells go first, the rest waits for ov_event
+    int64_t ov_lo = 0, ov_hi = 0;
+    cudaEvent_t ov_event = nullptr;
+    cudaStream_t xstream = nullptr;   // hyg_set_exchange_stream: pack / unpack run here (nullptr: on `stream`)
     int tiled_load = 0;        // HYG_TUNE_TILED_LOAD: 0 TMA tiles (k_dv_tiled_tma), 1 cp.async (k_dv_tiled_stream)
     bool fo_m_pos = true;      // every wall has Fo_M > 0 (K2/K3 scale by 2 Fo_M dt/dx^2)
     bool flux = true;
@@ -1095,10 +1100,32 @@ int advance_tiled(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
                 a.in[i] = c->s64[from][i];
                 a.out[i] = c->s64[1 - from][i];
             }
+            auto interior = [&](int64_t t0, int64_t t1) {
+                if (t1 <= t0) return;
+                TiledArgs ai = a;
+                ai.t_begin = t0;
+                ai.t_end = t1;
+                const int g = static_cast<int>(std::min<int64_t>((t1 - t0 + kDvWarps - 1) / kDvWarps, std::max(grid, 1)));
+                if (tma) k_dv_tiled_tma<kTileNPT, kK3MinB><<<g, kDvWarps * 32, 0, c->stream>>>(ai, c->tmaps[from]);
+                else k_dv_tiled_stream<kTileNPT, kK3MinB><<<g, kDvWarps * 32, 0, c->stream>>>(ai);
+            };
             {
                 LaunchScope ls(c, "df_analytic_tiled", mid_cells * a.steps);
-                if (grid > 0 && tma) k_dv_tiled_tma<kTileNPT, kK3MinB><<<grid, kDvWarps * 32, 0, c->stream>>>(a, c->tmaps[from]);
-                else if (grid > 0) k_dv_tiled_stream<kTileNPT, kK3MinB><<<grid, kDvWarps * 32, 0, c->stream>>>(a);
+                if (c->ov_event) {
+                    // overlapped halo refresh (hyg_advance_overlapped): window t reads cells
+                    // [t T, t T + W); those clear of the refreshed cells march while the
+                    // exchange is still in flight, the rest behind its event
+                    const int64_t t_lo = std::min<int64_t>(tr, std::max<int64_t>(1, (c->ov_lo + G::T - 1) / G::T));
+                    const int64_t t_hi = std::max<int64_t>(
+                        t_lo, std::min<int64_t>(tr, c->ov_hi > 0 ? (c->n - c->ov_hi - G::W) / G::T + 1 : tr));
+                    interior(t_lo, t_hi);
+                    HYG_CUDA(cudaStreamWaitEvent(c->stream, c->ov_event, 0));
+                    interior(1, t_lo);
+                    interior(t_hi, tr);
+                    c->ov_event = nullptr;
+                } else {
+                    interior(1, tr);
+                }
             }
             LaunchScope ls(c, "df_analytic_tiled_faces", face_cells * a.steps);
             k_dv_tiled<kTileNPT, true><<<1, kDvWarps * 32, 0, c->stream>>>(a);
@@ -2312,6 +2339,24 @@ int hyg_bootstrap(hyg_ctx* c, int32_t kind, hyg_status* status) {
     return HYG_OK;
 }
 
+int hyg_advance_overlapped(hyg_ctx* c, int64_t nsteps, double dt, int64_t edge_lo, int64_t edge_hi, void* event,
+                           hyg_status* status) {
+    if (!c || nsteps < 0 || edge_lo < 0 || edge_hi < 0) return HYG_EINVAL;
+    if (!event) return hyg_advance(c, nsteps, dt, status);
+    cudaSetDevice(c->device);
+    const double dte = dt > 0.0 ? dt : c->dt;
+    if (nsteps > 0 && c->tiled && dte > 0.0 && c->fo_m_pos && c->norm >= 2.0) {
+        c->ov_lo = edge_lo;                   // consumed by advance_tiled's first launch
+        c->ov_hi = edge_hi;
+        c->ov_event = static_cast<cudaEvent_t>(event);
+    } else if (cudaStreamWaitEvent(c->stream, static_cast<cudaEvent_t>(event), 0) != cudaSuccess) {
+        return HYG_ECUDA;                     // every other path: behind the refresh, no overlap
+    }
+    const int rc = hyg_advance(c, nsteps, dt, status);
+    c->ov_event = nullptr;
+    return rc;
+}
+
 int hyg_advance(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status) {
     clear_status(status);
     if (!c || nsteps < 0) return HYG_EINVAL;
@@ -2491,6 +2536,12 @@ int hyg_set_stream(hyg_ctx* c, void* stream) {
     return HYG_OK;
 }
 
+int hyg_set_exchange_stream(hyg_ctx* c, void* stream) {
+    if (!c) return HYG_EINVAL;
+    c->xstream = static_cast<cudaStream_t>(stream);
+    return HYG_OK;
+}
+
 int hyg_pack_cells(hyg_ctx* c, int64_t cell0, int64_t count, double* buf) {
     if (!c || cell0 < 0 || count < 0 || cell0 + count > c->cells() || (count > 0 && !buf)) return HYG_EINVAL;
     if (c->precision != HYG_F64) return HYG_ENOTSUP;
@@ -2500,7 +2551,7 @@ int hyg_pack_cells(hyg_ctx* c, int64_t cell0, int64_t count, double* buf) {
     const int grid = static_cast<int>(std::min<int64_t>((4 * count + 255) / 256, 4 * sm_count(c->device)));
     {
         LaunchScope ls(c, "pack_cells", 0.0);
-        k_pack_cells<<<grid, 256, 0, c->stream>>>(L, cell0, count, buf);
+        k_pack_cells<<<grid, 256, 0, c->xstream ? c->xstream : c->stream>>>(L, cell0, count, buf);
     }
     return cudaGetLastError() == cudaSuccess ? HYG_OK : HYG_ECUDA;
 }
@@ -2514,7 +2565,7 @@ int hyg_unpack_cells(hyg_ctx* c, int64_t cell0, int64_t count, const double* buf
     const int grid = static_cast<int>(std::min<int64_t>((4 * count + 255) / 256, 4 * sm_count(c->device)));
     {
         LaunchScope ls(c, "unpack_cells", 0.0);
-        k_unpack_cells<<<grid, 256, 0, c->stream>>>(L, cell0, count, buf);
+        k_unpack_cells<<<grid, 256, 0, c->xstream ? c->xstream : c->stream>>>(L, cell0, count, buf);
     }
     return cudaGetLastError() == cudaSuccess ? HYG_OK : HYG_ECUDA;
 }
@@ -2524,8 +2575,9 @@ int hyg_pack_zones(hyg_ctx* c, int32_t z0, int32_t count, double* buf) {
         return HYG_EINVAL;
     if (count == 0) return HYG_OK;
     cudaSetDevice(c->device);
-    if (cudaMemcpyAsync(buf, c->zu[c->zcur] + z0, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream) ||
-        cudaMemcpyAsync(buf + count, c->zv[c->zcur] + z0, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream))
+    cudaStream_t xs = c->xstream ? c->xstream : c->stream;
+    if (cudaMemcpyAsync(buf, c->zu[c->zcur] + z0, count * sizeof(double), cudaMemcpyDeviceToDevice, xs) ||
+        cudaMemcpyAsync(buf + count, c->zv[c->zcur] + z0, count * sizeof(double), cudaMemcpyDeviceToDevice, xs))
         return HYG_ECUDA;
     return HYG_OK;
 }
@@ -2535,8 +2587,9 @@ int hyg_unpack_zones(hyg_ctx* c, int32_t z0, int32_t count, const double* buf) {
         return HYG_EINVAL;
     if (count == 0) return HYG_OK;
     cudaSetDevice(c->device);
-    if (cudaMemcpyAsync(c->zu[c->zcur] + z0, buf, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream) ||
-        cudaMemcpyAsync(c->zv[c->zcur] + z0, buf + count, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream))
+    cudaStream_t xs = c->xstream ? c->xstream : c->stream;
+    if (cudaMemcpyAsync(c->zu[c->zcur] + z0, buf, count * sizeof(double), cudaMemcpyDeviceToDevice, xs) ||
+        cudaMemcpyAsync(c->zv[c->zcur] + z0, buf + count, count * sizeof(double), cudaMemcpyDeviceToDevice, xs))
         return HYG_ECUDA;
     return HYG_OK;
 }

@@ -63,6 +63,7 @@ struct TiledArgs {
     double* out[4];
     const int* stop;
     int* suspect;
+    int64_t t_begin, t_end;    // interior windows of this launch: [t_begin, t_end) within [1, rface(n))
 };
 
 // d(v) = 1 + p0 v + p1 exp(-p2 (v - p3)^2) at a half node, from the SUM of its
@@ -588,9 +589,9 @@ __global__ void __launch_bounds__(kDvWarps * 32, MINB) k_dv_tiled_stream(const T
     stage_exp_table_rep(s_tab_rep, threadIdx.x, blockDim.x);
     __syncthreads();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int64_t tr = G::rface(A.n);
+    const int64_t tr = A.t_end;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * kDvWarps;
-    int64_t t = 1 + static_cast<int64_t>(blockIdx.x) * kDvWarps + warp;
+    int64_t t = A.t_begin + static_cast<int64_t>(blockIdx.x) * kDvWarps + warp;
     if (t >= tr) return;
     double(*buf)[W] = s_buf[warp];
     auto swz = [](int i) { return (i & ~(NPT - 1)) | ((i ^ (i / NPT)) & (NPT - 1)); };
@@ -711,9 +712,9 @@ __global__ void __launch_bounds__(kDvWarps * 32, MINB) k_dv_tiled_tma(const Tile
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    const int64_t tr = G::rface(A.n);
+    const int64_t tr = A.t_end;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * kDvWarps;
-    int64_t t = 1 + static_cast<int64_t>(blockIdx.x) * kDvWarps + warp;
+    int64_t t = A.t_begin + static_cast<int64_t>(blockIdx.x) * kDvWarps + warp;
     if (t >= tr) return;
     double(*buf)[W] = s_buf[warp];
     void* mbar = &s_mbar[warp];

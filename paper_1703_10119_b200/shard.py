@@ -185,13 +185,18 @@ class _Timer:
         self.intervals = 0
 
 
-def _advance_guarded(engine, k, comm):
+def _advance_guarded(engine, k, comm, edge=None, wait_event=None):
     """k steps on every rank; a divergence anywhere stops all ranks with the
-    earliest failing layer (check_bounded semantics across shards)."""
+    earliest failing layer (check_bounded semantics across shards).  With
+    `wait_event` the halo refresh of the first edge[0] / last edge[1] cells is
+    still in flight on another stream (hyg_advance_overlapped)."""
     fail = float("inf")
     err = None
     try:
-        engine.advance(k)
+        if wait_event is None:
+            engine.advance(k)
+        else:
+            engine.advance(k, edge=edge, wait_event=wait_event)
     except NumericalError as e:
         fail, err = float(e.layer), e
     first = comm.allreduce_min(fail)
@@ -204,9 +209,17 @@ def _advance_guarded(engine, k, comm):
 # ---------------------------------------------------------------------------------
 class LongDomainShard:
     """configs[4]: one long wall cut into x-slabs.  `engine_factory(model)`
-    returns a Context-like engine for the local slab."""
+    returns a Context-like engine for the local slab.
 
-    def __init__(self, model: Model, init: dict, comm, engine_factory: Callable, halo: int = 32):
+    overlap (default: on a device comm with a CUDA engine): the halo refresh of
+    an interval — pack, NCCL send/recv, unpack — runs on a second stream behind
+    the interval's compute, and the next interval starts at once: the windows of
+    its first launch that read no halo cell march while the exchange is in
+    flight, the edge windows and the later launches follow behind the refresh's
+    event (Context.advance(edge=, wait_event=) -> hyg_advance_overlapped)."""
+
+    def __init__(self, model: Model, init: dict, comm, engine_factory: Callable, halo: int = 32,
+                 overlap: Optional[bool] = None):
         self.comm, self.halo = comm, halo
         n = model.n_nodes
         s = self.slab = slab_bounds(n, comm.world, comm.rank, halo)
@@ -223,17 +236,55 @@ class LongDomainShard:
         self.engine.set_state(**{f: init[f][s.a:s.b] for f in FIELDS})
         self.engine.set_owned(s.lo - s.a, s.hi - s.a)
         self.timer = _Timer(comm)
+        can = bool(getattr(comm, "on_device", False)) and hasattr(self.engine, "set_exchange_stream")
+        self.overlap = can if overlap is None else (bool(overlap) and can)
+        self._xstream, self._pending = None, None
+        # local cells a refresh rewrites: the left halo [0, lo - a), the right one [hi - a, b - a)
+        self._edge = (s.lo - s.a, s.b - s.hi)
 
     def advance(self, nsteps: int):
         done = 0
         while done < nsteps:
             k = min(self.halo, nsteps - done)
             with self.timer.phase("compute"):
-                _advance_guarded(self.engine, k, self.comm)
-            with self.timer.phase("exchange"):
-                self.refresh()
+                _advance_guarded(self.engine, k, self.comm, edge=self._edge, wait_event=self._pending)
+            self._pending = None
+            if self.overlap:
+                self._refresh_async()
+            else:
+                with self.timer.phase("exchange"):
+                    self.refresh()
             self.timer.intervals += 1
             done += k
+        self.join()
+
+    def _refresh_async(self):
+        """The refresh on the exchange stream, behind the compute issued so far; the
+        compute stream does not wait for it (the next advance takes its event)."""
+        import torch
+        dev = self.comm.device
+        cs = torch.cuda.current_stream(dev)
+        if self._xstream is None:
+            self._xstream = torch.cuda.Stream(dev)
+        xs = self._xstream
+        xs.wait_stream(cs)
+        self.engine.set_exchange_stream(xs)
+        try:
+            with torch.cuda.stream(xs):
+                with self.timer.phase("exchange"):
+                    self.refresh()
+                ev = torch.cuda.Event()
+                ev.record(xs)
+        finally:
+            self.engine.set_exchange_stream(None)
+        self._pending = ev
+
+    def join(self):
+        """The compute stream waits for a refresh still in flight."""
+        if self._pending is not None:
+            import torch
+            torch.cuda.current_stream(self.comm.device).wait_event(self._pending)
+            self._pending = None
 
     def refresh(self):
         s, H, r, P = self.slab, self.halo, self.comm.rank, self.comm.world
@@ -252,6 +303,7 @@ class LongDomainShard:
 
     def owned_state(self) -> dict:
         s = self.slab
+        self.join()
         return self.engine.get_cells(s.lo - s.a, s.hi - s.lo)
 
 

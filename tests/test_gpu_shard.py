@@ -103,13 +103,24 @@ class _LoopbackComm:
         return a.to(self.device, torch.float64).contiguous()
 
     def exchange(self, sends, recvs):
+        # payloads cross threads AND streams (the shards' exchange streams when the
+        # refresh overlaps compute): an event per payload orders the receiver's stream
+        # behind the sender's copy, as NCCL orders its transfer behind the pack kernel
+        import torch
         box, bar = self.hub
         for peer, a in sends.items():
             t = self.tensor(a)
             assert t.is_cuda
-            box[(self.rank, peer)] = t.clone()
+            c = t.clone()
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(self.device))
+            box[(self.rank, peer)] = (c, ev)
         bar.wait()
-        out = {peer: box.pop((peer, self.rank)) for peer in recvs}
+        out = {}
+        for peer in recvs:
+            c, ev = box.pop((peer, self.rank))
+            torch.cuda.current_stream(self.device).wait_event(ev)
+            out[peer] = c
         bar.wait()
         return out
 
@@ -128,11 +139,13 @@ class _LoopbackComm:
         return self._reduce(x, min)
 
 
-@pytest.mark.parametrize("case", ["long", "ring", "ring128", "ring128k4r", "ring128k5"])
+@pytest.mark.parametrize("case", ["long", "long_serial", "ring", "ring128", "ring128k4r", "ring128k5"])
 def test_device_payload_exchange_bitwise(case):
     """Halo payloads as CUDA tensors (the NCCL path of shard.Comm: one pack
     kernel, stream-ordered, no host copies): shards in two threads equal the
-    undivided run bit for bit.  ring128: 128-node walls, so each shard marches
+    undivided run bit for bit.  long: the halo refresh runs on a second stream
+    and overlaps the interior windows of the next interval's first launch
+    (hyg_advance_overlapped); long_serial: the same on one stream.  ring128: 128-node walls, so each shard marches
     its zone block (a chain with halo zones) through the zone-ring kernel K4r
     (ring128k5: K5)."""
     import threading
@@ -141,7 +154,7 @@ def test_device_payload_exchange_bitwise(case):
     world = 2
     hub = ({}, threading.Barrier(world))
     res, errs = {}, []
-    if case == "long":
+    if case.startswith("long"):
         n, steps = 1 << 15, 120
         w = workloads.long_domain(n_nodes=n, nsteps=steps)
         model, init = w.model, w.init
@@ -159,8 +172,9 @@ def test_device_payload_exchange_bitwise(case):
         try:
             torch.cuda.set_device(0)
             comm = _LoopbackComm(rank, world, hub)
-            if case == "long":
-                sh = shard.LongDomainShard(model, init, comm, Context, halo=24)
+            if case.startswith("long"):
+                sh = shard.LongDomainShard(model, init, comm, Context, halo=24, overlap=case == "long")
+                assert sh.overlap == (case == "long")
                 sh.advance(steps)
             else:
                 sh = shard.ZoneRingShard(model, init, comm, Context, walls_per_zone=6, halo=4 if case == "ring" else 12)
@@ -188,14 +202,14 @@ def test_device_payload_exchange_bitwise(case):
     assert not errs, errs[0]
     with Context(model) as ref:
         ref.set_state(**init)
-        if case == "long":
+        if case.startswith("long"):
             ref.advance(steps)
         else:
             ref.bootstrap("implicit")
             ref.advance(steps - 1)
         full = ref.get_state()
     for rank, (sh, got) in res.items():
-        if case == "long":
+        if case.startswith("long"):
             sl = slice(sh.slab.lo, sh.slab.hi)
         else:
             sl = slice(sh.lo * 6 * n, sh.hi * 6 * n)
