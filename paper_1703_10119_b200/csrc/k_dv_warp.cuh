@@ -104,17 +104,23 @@ __device__ __forceinline__ DvRow dv_row(const AnalyticRow& r) {
 
 __device__ __forceinline__ void dv_interior(const DvRow& r, double vp, double up, double vL, double vR,
                                             double uL, double uR, double km, double kp, double& vn,
-                                            double& un) {
-    // symmetric in (L, R) and never contracted (__dmul_rn): a node rounds the
-    // same in a reversed lane as in a normal one, so every window computes it
-    // bit for bit alike.  The u row reuses the v row's differences and its
-    // increment inc ~ vn - vp: (vL + vR) - (vn + vp) = dl + dr - inc, so
-    // G w - Gm (vn - vp) = G (dl + dr) - (G + Gm) inc (every term vanishes
-    // exactly at a uniform state)
+                                            double& un, bool rev = false) {
+    // Every node rounds the same whatever lane holds it, so every window of K3w
+    // (and the sharded run) computes it bit for bit alike.  The sums dl + dr and
+    // kp + km commute; the numerator k_left d_left + k_right d_right is ONE
+    // product and one FMA in the geometric order — the right-hand product rounded
+    // first, the left-hand one inside the FMA — so a lane whose registers hold
+    // its nodes reversed (rev: its "L" arguments are the geometric right) swaps
+    // the operands by selects; where rev is a compile-time false (K3w's interior
+    // windows, the one-node-per-lane kernels) they fold away.  The u row reuses
+    // the v row's differences and its increment inc ~ vn - vp: (vL + vR) - (vn + vp)
+    // = dl + dr - inc, so G w - Gm (vn - vp) = G (dl + dr) - (G + Gm) inc (every
+    // term vanishes exactly at a uniform state)
     // km, kp arrive scaled by 2a (dv_params): num = 2a (km dl + kp dr) and
     // 1 + a (kp + km) = 1 + (kp' + km')/2
     const double dl = vL - vp, dr = vR - vp;
-    const double num = __dadd_rn(__dmul_rn(km, dl), __dmul_rn(kp, dr));
+    const double ka = rev ? kp : km, da = rev ? dr : dl, kb = rev ? km : kp, db = rev ? dl : dr;
+    const double num = fma(ka, da, __dmul_rn(kb, db));
     const double den = fma(0.5, kp + km, 1.0);
     const double inc = __dmul_rn(num, frcp2(den));
     vn = __dadd_rn(vp, inc);
@@ -215,7 +221,7 @@ __device__ __forceinline__ void dv_step(double (&vP)[NPT], const double (&vC)[NP
         const double hj = j == NPT - 1 ? hl : d_half(q, vC[j] + vN[j], tab);
         double vn, un;
         dv_interior(r, vP[j], uP[j], j == 0 ? vx0 : vC[j - 1], vN[j], j == 0 ? ux0 : uC[j - 1], uN[j], hprev, hj,
-                    vn, un);
+                    vn, un, L.rev);
         if (FACES && j == 0) {
             double vf, uf;
             dv_face(fc, am, vP[0], uP[0], vN[0], uN[0], dnode, hj, vf, uf);
@@ -612,9 +618,9 @@ __global__ void __launch_bounds__(kDvWarps * 32, MINB) k_dv_tiled_stream(const T
     const DvParams q = dv_params(A.p, 2.0 * rc.a);
     const DvFace fc{};
     DvLane L;
-    L.rev = lane == 31;
-    L.mirror0 = L.rev;
-    L.face = false;
+    L.rev = false;        // no reversed lane here (lanes 0 and 31 are the stale ones): the selects of
+    L.mirror0 = false;    // dv_step / dv_interior fold away; the artificial window edges are the
+    L.face = false;       // shuffles' own-value results in lanes 0 and 31
     const bool store = lane != 0 && lane != 31;      // the stale lanes stay out of the guard and the output
     unsigned acc = 0;
     for (; t < tr; t += stride) {
@@ -732,9 +738,9 @@ __global__ void __launch_bounds__(kDvWarps * 32, MINB) k_dv_tiled_tma(const Tile
     const DvParams q = dv_params(A.p, 2.0 * rc.a);
     const DvFace fc{};
     DvLane L;
-    L.rev = lane == 31;
-    L.mirror0 = L.rev;
-    L.face = false;
+    L.rev = false;        // no reversed lane here (lanes 0 and 31 are the stale ones): the selects of
+    L.mirror0 = false;    // dv_step / dv_interior fold away; the artificial window edges are the
+    L.face = false;       // shuffles' own-value results in lanes 0 and 31
     const bool store = lane != 0 && lane != 31;      // the stale lanes stay out of the guard and the output
     const int sw = (lane >> 1) & 3;                  // this row's chunk swizzle
     unsigned acc = 0;
