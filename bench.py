@@ -374,6 +374,53 @@ class Runner:
             self.ctx.advance(n, d)
 
 
+def measure_sharded(args, name, rank, world, local, barrier, max_over_ranks):
+    """`name` (cfg4: x-slabs with 64-node halos; cfg3: zone blocks with 24-zone halos)
+    divided over the job's GPUs — the configs that communicate — as full-length runs:
+    device time (CUDA events on the engine's stream, max over ranks) and, per halo
+    interval, the exchange and compute time of the shards.  At N = 1 the undivided
+    run, so the lines of a 1/2/4/8 SCALE run give the strong-scaling efficiency."""
+    import copy
+    import torch
+    a = copy.copy(args)
+    a.config, a.run_steps = name, CONFIGS[name]["run_steps"]
+    a.halo = args.halo or {"cfg4": 64, "cfg3": 24}[name]
+    a.ring_kernel = a.ring_depth = a.tiled_load = 0
+    a.material_exact = False
+    w = make_workload(a, 0, world)
+    R = Runner(a, w, rank, world, local)
+    ctx = R.ctx
+    try:
+        R.run()                                   # warm-up
+        ctx.synchronize()
+        if R.shard is not None:
+            R.shard.timer.reset()
+        runs = 2
+        barrier()
+        torch.cuda.synchronize()
+        ctx.record(0)
+        for _ in range(runs):
+            R.run()
+        ctx.record(1)
+        ctx.synchronize()
+        barrier()
+        ms = max_over_ranks(ctx.elapsed_ms(0, 1))
+        out = {"value": float(w.cells) * w.nsteps * runs / (ms * 1e-3), "unit": UNIT, "ms_per_run": ms / runs,
+               "n_gpus": world, "scaling": "strong", "steps_per_run": w.nsteps,
+               "workload": workload_config(a, world)["workload"]}
+        if R.shard is not None:
+            t = R.shard.timer.totals()
+            n = max(1, t["intervals"])
+            out["halo"] = a.halo
+            out["per_interval_us"] = {"exchange": 1e3 * max_over_ranks(t["exchange"]) / n,
+                                      "compute": 1e3 * max_over_ranks(t["compute"]) / n,
+                                      "intervals": t["intervals"],
+                                      "overlapped": bool(getattr(R.shard, "overlap", False))}
+        return out
+    finally:
+        ctx.close()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
