@@ -11,17 +11,20 @@
 //   phase 1, k_ring_cone: for every zone the air ODE together with the last
 //     S + 1 nodes of each of its walls (the "cone": the cut end goes stale one
 //     node per step and never reaches the face node within S steps) is marched
-//     S steps — one thread per wall cone, one per zone, a CTA of LB
+//     S = 8 steps — one thread per wall cone, one per zone, a CTA of LB
 //     consecutive zones whose outer S on each side are halo copies (the zone
 //     cone grows one zone per step along the ring).  It records the layer-k
-//     air of every owned zone, k = 0 .. S-1, in `series` ([zone][S][2]) and
-//     writes the zone air of layer S.  ~4 % of the walls' node-updates.
-//   phase 2, k_ring_walls: every wall is marched S steps in registers in K1's
-//     layout (k_coupled.cuh: 16 lanes x NPT nodes, two walls per warp,
-//     neighbours by shuffles, both faces in register 0), its face-1 ambient
-//     read from `series`.  No shared surfaces, no barrier in the step loop,
-//     no halo walls: 64 B per node per S steps of HBM traffic (8 B per update
-//     at S = 8) and K1's 7 FP64 instructions per update.
+//     air of every owned zone in `series` and writes the zone air of layer S.
+//   phase 2, k_ring_walls: every wall is marched SW = m S steps (m = 1, 2, 3)
+//     in registers in K1's layout (k_coupled.cuh: 16 lanes x NPT nodes, two
+//     walls per warp, neighbours by shuffles, both faces in register 0), its
+//     face-1 ambient read from `series`.  No shared surfaces, no barrier in the
+//     step loop, no halo walls: 64 B per node per SW steps of HBM traffic (4 B
+//     per update at m = 2) and K1's 7 FP64 instructions per update.
+//   between the m cone launches that feed one walls launch, k_ring_stub marches
+//     the walls' last 17 (25) nodes S steps with the air series just recorded:
+//     the tails the next cone launch starts from, which the walls kernel has not
+//     produced yet.  ~7 % of the walls' node-updates for cones and stubs.
 //
 // The face-1 node is computed twice (cone thread and owning lane) with the
 // same instruction sequence on the same inputs, so both phases hold the same
@@ -37,7 +40,7 @@
 #include "k_ring_reg.cuh"
 
 // timing experiments only (tools/ring_walls_probe.cu): skip the steps (1), the
-// outputs (2), the layer loads (4); minimum CTAs per SM; 0 / 4 in the library
+// outputs (2), the layer loads (4); minimum CTAs per SM; 0 / 3 in the library
 #ifndef RW_SKIP
 #define RW_SKIP 0
 #endif
