@@ -138,16 +138,21 @@ class Clocks:
                     N.nvmlClocksThrottleReasonSwThermalSlowdown, N.nvmlClocksThrottleReasonSwPowerCap]
             smax = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
 
+            def once():
+                try:
+                    sm = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                    pw = N.nvmlDeviceGetPowerUsage(h) / 1000.0
+                    r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                    self.rows.append((time.time(), [sm, smax, pw] + [bool(r & b) for b in bits]))
+                except Exception:
+                    pass
+
             def poll():
                 while not self.stop_flag.is_set():
-                    try:
-                        sm = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
-                        pw = N.nvmlDeviceGetPowerUsage(h) / 1000.0
-                        r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                        self.rows.append((time.time(), [sm, smax, pw] + [bool(r & b) for b in bits]))
-                    except Exception:
-                        pass
+                    once()
                     self.stop_flag.wait(0.2)
+
+            self.once = once
 
             self.nvml = N
             self.source = "nvml"
@@ -178,7 +183,17 @@ class Clocks:
                     pass
 
     def mark(self, which: str):
-        setattr(self, which, time.time())
+        # one sample right inside each end of the window, so a timed region shorter than
+        # the polling period (configs[0]: tens of milliseconds) still carries its clocks
+        once = getattr(self, "once", None)
+        if which == "t_start":
+            setattr(self, which, time.time())
+            if once:
+                once()
+        else:
+            if once:
+                once()
+            setattr(self, which, time.time())
 
     def stop(self) -> dict:
         self.stop_flag.set()
