@@ -2674,9 +2674,12 @@ __global__ void k_fastmath(int n, const double* x, double* e, double* r) {
 }
 // the d(v) half node's exp (-700 <= x <= 0) and the v row's two-FMA reciprocal
 __global__ void k_dvmath(int n, const double* x, double* e, double* r) {
+    __shared__ double s_tab[256];
+    for (int j = threadIdx.x; j < 256; j += blockDim.x) s_tab[j] = exp_tab_biased(j);
+    __syncthreads();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
-        e[i] = fexp_addend<1>(-fabs(x[i]), kExp2Tab256);
+        e[i] = fexp_addend<1>(-fabs(x[i]), s_tab);
         r[i] = frcp2(x[i]);
     }
 }

@@ -124,7 +124,8 @@ __device__ __forceinline__ double frcp2(double d) {
 // every state inside the fast guard, |v| < 2, then keeps x above -700; a state
 // outside it is flagged by the guard and the launch is replayed on the per-step
 // path with the full fexp).
-// STRIDE: the table's element stride (the bank-replicated copy of k_nonlinear.cuh)
+// STRIDE: the table's element stride (the bank-replicated copy of k_nonlinear.cuh);
+// tab: entries exp_tab_biased(j) (stage_exp_table_rep)
 template <int STRIDE = 1>
 __device__ __forceinline__ double fexp_addend(double x, const double* tab) {
     constexpr double kShift = 6755399441055744.0;                  // 1.5 * 2^52
@@ -138,10 +139,19 @@ __device__ __forceinline__ double fexp_addend(double x, const double* tab) {
     const double c23 = fma(r, 1.0 / 6.0, 0.5);
     const double q = fma(r2, 1.0 / 24.0, c23);                     // 1/2 + r/6 + r^2/24
     const double sm = fma(r2, q, r);                               // exp(r) - 1
+    // tab holds T_j with its high word lowered by j << 12 (exp_tab_biased): k << 12 =
+    // ((k >> 8) << 20) + (j << 12), so ONE multiply-add puts 2^(k >> 8) into the exponent
+    // field (shift, mask and add before: two integer instructions and their register
+    // reads less per exp, off the FP64 pipe's register bandwidth)
     const double t = tab[(k & 255) * STRIDE];
-    const double ts = __hiloint2double(__double2hiint(t) + static_cast<int>(static_cast<unsigned>(k >> 8) << 20),
-                                       __double2loint(t));
+    const double ts = __hiloint2double(__double2hiint(t) + (k << 12), __double2loint(t));
     return fma(ts, sm, ts);
+}
+
+// entry j of fexp_addend's table: 2^(j/256) with the high word lowered by j << 12
+__device__ __forceinline__ double exp_tab_biased(int j) {
+    const double t = kExp2Tab256[j];
+    return __hiloint2double(__double2hiint(t) - (j << 12), __double2loint(t));
 }
 
 // flog_pos: ln x for positive normal finite x (the material correlations call

@@ -65,7 +65,7 @@ __device__ __forceinline__ void stage_exp_table(double* s_tab, int tid, int nthr
 constexpr int kExpRep = 4;
 constexpr int kExpTab = 256;
 __device__ __forceinline__ void stage_exp_table_rep(double* s_tab, int tid, int nthreads) {
-    for (int i = tid; i < kExpTab * kExpRep; i += nthreads) s_tab[i] = kExp2Tab256[i / kExpRep];
+    for (int i = tid; i < kExpTab * kExpRep; i += nthreads) s_tab[i] = exp_tab_biased(i / kExpRep);
 }
 
 constexpr int kNlChunk = 64;   // forcing rows staged per chunk
