@@ -57,12 +57,14 @@ __device__ __forceinline__ void stage_exp_table(double* s_tab, int tid, int nthr
     for (int i = tid; i < 64; i += nthreads) s_tab[i] = kExp2Tab64[i];
 }
 
-// fexp_addend's 2^(j/256) table replicated kExpRep times, entry j of copy c at
-// j * kExpRep + c: lane l reads copy l & (kExpRep - 1), which spreads the lanes of
-// a warp over distinct bank pairs when their indices collide (16 copies of the
-// former 64-entry table measured within 1 % of one copy on K3w: neighbouring
-// lanes hold neighbouring states and mostly read the same or adjacent entries)
-constexpr int kExpRep = 4;
+// fexp_addend's table (exp_tab_biased) in shared memory, kExpRep copies (entry j of copy c
+// at j * kExpRep + c, lane l reading copy l & (kExpRep - 1)).  One copy: neighbouring
+// lanes hold neighbouring states and mostly read the same or adjacent entries, so bank
+// replication buys nothing (16 copies of the round-1 table were within 1 % of one on K3w),
+// while a single copy lets the compiler address the table as an immediate offset from the
+// masked index — an LEA and a mask fewer per exp (4 copies: cfg4 3.53e11, one: 3.55e11;
+// cfg0 4.16e8 -> 4.21e8)
+constexpr int kExpRep = 1;
 constexpr int kExpTab = 256;
 __device__ __forceinline__ void stage_exp_table_rep(double* s_tab, int tid, int nthreads) {
     for (int i = tid; i < kExpTab * kExpRep; i += nthreads) s_tab[i] = exp_tab_biased(i / kExpRep);
