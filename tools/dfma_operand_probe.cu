@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(128, 2) k_d(double* out, const double* coef, i
         vp[k] = vc[k] = 1.0 + 1e-3 * ((threadIdx.x + 3 * k) % 5);
     }
     unsigned acc = 0;
+    bool bad = false;
     auto step = [&](double (&vP)[N], double (&vC)[N], double (&uP)[N], double (&uC)[N], int k) {
         double vx0 = vC[N - 1], ux0 = uC[N - 1], vx1 = vC[0], ux1 = uC[0];
         if (BITS & 1) {
@@ -123,6 +124,10 @@ __global__ void __launch_bounds__(128, 2) k_d(double* out, const double* coef, i
             // one packed word: PRMT gathers the top bytes of un, vn of two nodes, one OR per two nodes
             if (BITS & 32) acc |= static_cast<unsigned>(__double2hiint(vn));
             if ((BITS & 64) && (j & 1)) acc |= static_cast<unsigned>(__double2hiint(un)) | static_cast<unsigned>(__double2hiint(vn));
+            // 256: the guard as unsigned compares into a predicate (one register read per value, no
+            // accumulator read): hi >= 0x40000000 as unsigned <=> |x| >= 2, not finite, or negative
+            if (BITS & 256) bad |= (static_cast<unsigned>(__double2hiint(un)) >= 0x40000000u) |
+                                   (static_cast<unsigned>(__double2hiint(vn)) >= 0x40000000u);
             // 16: the guard one step late — on the step's INPUT layer, whose values are a step old
             if (BITS & 16) acc |= static_cast<unsigned>(__double2hiint(uC[j])) | static_cast<unsigned>(__double2hiint(vC[j]));
             vP[j] = vn;
@@ -133,7 +138,7 @@ __global__ void __launch_bounds__(128, 2) k_d(double* out, const double* coef, i
         step(vp, vc, up, uc, i);
         step(vc, vp, uc, up, i + 1);
     }
-    double s = acc & 1;
+    double s = (acc & 1) + (bad ? 1.0 : 0.0);
 #pragma unroll
     for (int k = 0; k < N; ++k) s += up[k] + uc[k] + vp[k] + vc[k];
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
@@ -195,5 +200,7 @@ int main() {
     run("D32: + guard, v only", k_d<32>, 128, 8, 4096, 16 * 7, 16 * 12, o, cd, nsm);
     run("D64: + guard, every other node", k_d<64>, 128, 8, 4096, 16 * 7, 16 * 12, o, cd, nsm);
     run("D27: all with the lagged guard", k_d<27>, 128, 8, 4096, 16 * 7 + 6, 16 * 12, o, cd, nsm);
+    run("D256: + predicate guard", k_d<256>, 128, 8, 4096, 16 * 7, 16 * 12, o, cd, nsm);
+    run("D267: all with the predicate guard", k_d<267>, 128, 8, 4096, 16 * 7 + 6, 16 * 12, o, cd, nsm);
     return 0;
 }
