@@ -388,9 +388,10 @@ int64_t hyg_launch_count(hyg_ctx* ctx);
  * walls kernel march m x 8 steps per launch, fed by m cone launches (the later
  * ones on tails a stub kernel marches ahead); bitwise equal for every m.
  * HYG_TUNE_TILED_LOAD picks how the long-wall
- * kernel K3w stages its windows: 0 = 2-D tiles on the TMA engine through tensor
- * maps of the state arrays (k_dv_tiled_tma), 1 = per-lane cp.async copies
- * (k_dv_tiled_stream); bitwise equal.  HYG_EINVAL for an unknown knob or a
+ * kernel K3w stages its windows and K6's walls kernel its wall pairs: 0 = 2-D
+ * tiles on the TMA engine through tensor maps of the state arrays
+ * (k_dv_tiled_tma; k_ring_walls<.., true>), 1 = per-lane cp.async copies
+ * (k_dv_tiled_stream) / 1-D bulk copies with rotated shared accesses; bitwise equal.  HYG_EINVAL for an unknown knob or a
  * negative value. */
 enum { HYG_TUNE_RING_GRID = 1, HYG_TUNE_RING_KERNEL = 2, HYG_TUNE_MATERIAL_EXACT = 3, HYG_TUNE_TILED_LOAD = 4,
        HYG_TUNE_RING_DEPTH = 5 };

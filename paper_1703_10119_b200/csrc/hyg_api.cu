@@ -1199,25 +1199,38 @@ void launch_ring_stub(const RingArgs& a, const double* series, const double* row
     k_ring_stub<DIN, kRingSplitS><<<(walls + 127) / 128, 128, 0, s>>>(a, series, rowsT, in, out[0], out[1], out[2], out[3]);
 }
 
-template <int NPT, int SW>
-void launch_ring_walls_sw(const RingArgs& a, const double* series, cudaStream_t s, int device, int grid_cap) {
-    auto k = k_ring_walls<NPT, SW>;
-    const size_t smem = RingWallShape<NPT>::smem_doubles(SW, a.n_channels, kRingWallWarps) * sizeof(double);
+template <int NPT, int SW, bool TMAP>
+void launch_ring_walls_sw(const RingArgs& a, const double* series, cudaStream_t s, int device, int grid_cap,
+                          const TiledMaps& mi, const TiledMaps& mo) {
+    auto k = k_ring_walls<NPT, SW, TMAP>;
+    const size_t smem = RingWallShape<NPT>::smem_doubles(SW, a.n_channels, kRingWallWarps) * sizeof(double) +
+                        (TMAP ? 1024 : 0);
     ensure_smem_attr(k, device, 100 * 1024);
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * kRingWallWarps, smem);
     const int pairs = (a.n_zones * a.W + 1) / 2, nblk = (pairs + kRingWallWarps - 1) / kRingWallWarps;
     int grid = std::max(1, std::min(nblk, std::max(per_sm, 1) * sm_count(device)));
     if (grid_cap > 0) grid = std::min(grid, grid_cap);   // HYG_TUNE_RING_GRID: several pairs per warp in small rings
-    k<<<grid, 32 * kRingWallWarps, smem, s>>>(a, series);
+    k<<<grid, 32 * kRingWallWarps, smem, s>>>(a, series, mi, mo);
 }
 
-// m: cone launches per walls launch (the series row of a zone has m S slots)
+// m: cone launches per walls launch (the series row of a zone has m S slots); maps: the
+// state arrays' tensor maps (n = 128 and an even wall count), else the 1-D bulk copies
 template <int NPT>
-void launch_ring_walls(const RingArgs& a, const double* series, cudaStream_t s, int device, int grid_cap, int m) {
-    if (m == 1) launch_ring_walls_sw<NPT, kRingSplitS>(a, series, s, device, grid_cap);
-    else if (m == 2) launch_ring_walls_sw<NPT, 2 * kRingSplitS>(a, series, s, device, grid_cap);
-    else launch_ring_walls_sw<NPT, 3 * kRingSplitS>(a, series, s, device, grid_cap);
+void launch_ring_walls(const RingArgs& a, const double* series, cudaStream_t s, int device, int grid_cap, int m,
+                       const TiledMaps* mi, const TiledMaps* mo) {
+    static const TiledMaps none{};
+    if constexpr (NPT == 8) {
+        if (mi && mo) {
+            if (m == 1) launch_ring_walls_sw<8, kRingSplitS, true>(a, series, s, device, grid_cap, *mi, *mo);
+            else if (m == 2) launch_ring_walls_sw<8, 2 * kRingSplitS, true>(a, series, s, device, grid_cap, *mi, *mo);
+            else launch_ring_walls_sw<8, 3 * kRingSplitS, true>(a, series, s, device, grid_cap, *mi, *mo);
+            return;
+        }
+    }
+    if (m == 1) launch_ring_walls_sw<NPT, kRingSplitS, false>(a, series, s, device, grid_cap, none, none);
+    else if (m == 2) launch_ring_walls_sw<NPT, 2 * kRingSplitS, false>(a, series, s, device, grid_cap, none, none);
+    else launch_ring_walls_sw<NPT, 3 * kRingSplitS, false>(a, series, s, device, grid_cap, none, none);
 }
 
 template <int NPT>
@@ -1350,8 +1363,10 @@ int advance_ring(hyg_ctx* c, int64_t nsteps, double dt, hyg_status* status, bool
                                      c->d_ring_rowsT, c->d_ring_zpT, io);
                 }
                 LaunchScope ls(c, "ring_walls", static_cast<double>(c->cells()) * a.steps);
-                if (npt == 4) launch_ring_walls<4>(a, c->d_ring_series, c->stream, c->device, c->ring_grid_cap, split_m);
-                else launch_ring_walls<8>(a, c->d_ring_series, c->stream, c->device, c->ring_grid_cap, split_m);
+                const bool tmap = c->tmaps_ok && c->tiled_load == 0 && c->n_walls % 2 == 0;
+                if (npt == 4) launch_ring_walls<4>(a, c->d_ring_series, c->stream, c->device, c->ring_grid_cap, split_m, nullptr, nullptr);
+                else launch_ring_walls<8>(a, c->d_ring_series, c->stream, c->device, c->ring_grid_cap, split_m,
+                                          tmap ? &c->tmaps[from] : nullptr, tmap ? &c->tmaps[1 - from] : nullptr);
                 continue;
             }
             LaunchScope ls(c, pipe ? "ring_pipe" : reg ? "ring_reg" : "ring_tiled", static_cast<double>(c->cells()) * a.steps);
@@ -1775,7 +1790,9 @@ int hyg_create(const hyg_model_desc* d, hyg_ctx** out, hyg_status* status) {
             if (c->precision == HYG_F32 && cudaMalloc(&c->s32[b][i], cells * sizeof(float)) != cudaSuccess)
                 return fail("state alloc");
         }
-    if (c->tiled && kTileNPT == 8) {
+    // tensor maps of the state arrays (rows of 8 nodes, boxes of 32 rows): K3w's windows and,
+    // for 128-node zone rings, K6's wall pairs
+    if ((c->tiled && kTileNPT == 8) || (c->ring_cone_LB > 0 && c->n == 128)) {
         c->tmaps_ok = true;
         for (int b = 0; b < 2; ++b)
             for (int i = 0; i < 4; ++i)

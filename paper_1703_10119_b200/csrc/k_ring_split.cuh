@@ -37,6 +37,7 @@
 #include <type_traits>
 #include <cuda_runtime.h>
 
+#include "k_dv_warp.cuh"
 #include "k_ring_reg.cuh"
 
 // timing experiments only (tools/ring_walls_probe.cu): skip the steps (1), the
@@ -432,24 +433,48 @@ struct RingWallShape {
         return ((static_cast<size_t>(S) * 4 * nch + 1) & ~static_cast<size_t>(1)) +
                static_cast<size_t>(warps) * warp_doubles(S);
     }
+    // shared layout: the warps' staged layers and output scratch first (kBig doubles each: a
+    // multiple of 512 B, the period of the tensor maps' 64-byte swizzle), then the forcing
+    // rows, then the warps' small blocks; TMAP launches add 1 KB to align the base
+    static constexpr int kBig = 4 * 2 * kN + 2 * 2 * kN;
+    __host__ __device__ static int small_doubles(int S) { return 2 * 2 * 2 * S + 2 * 2 * kCoef + 2; }
 };
 
-template <int NPT, int S>
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, const void* src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                     reinterpret_cast<unsigned long long>(map)),
+                 "r"(c0), "r"(c1), "r"(smem_u32(src))
+                 : "memory");
+}
+
+// TMAP (n = 128, an even number of walls): the pair's layers travel as 2-D TMA tiles through
+// tensor maps of the state arrays (rows of 8 nodes, boxes of 32 rows = one wall pair, 64-byte
+// swizzle: chunk c of row r at chunk c ^ ((r / 2) mod 4)) in both directions — UTMALDG in,
+// UTMASTG out.  Lane l owns row l, so its 16-byte shared reads and writes are conflict-free
+// in register order and the rotation's select network (~380 selects per pair, each reading
+// two registers beside the FP64 stream) disappears.
+template <int NPT, int S, bool TMAP = false>
 __global__ void __launch_bounds__(32 * kRingWallWarps, RW_MINB) k_ring_walls(const RingArgs a,
-                                                                      const double* __restrict__ series) {
+                                                                      const double* __restrict__ series,
+                                                                      const __grid_constant__ TiledMaps MI,
+                                                                      const __grid_constant__ TiledMaps MO) {
     using Sh = RingWallShape<NPT>;
     constexpr int N = Sh::kN, NC = Sh::kCoef;
     constexpr unsigned FULL = 0xffffffffu;
-    extern __shared__ __align__(16) double smem[];      // forcing rows [S][4 nch], then the warps' blocks
+    static_assert(!TMAP || NPT == 8, "a row of the tensor maps is 8 nodes");
+    extern __shared__ __align__(16) double smem_raw[];
     if (launch_stopped(a.stop)) return;
+    // TMAP: the swizzle pattern is a function of the shared address, so the base is 1 KB aligned
+    double* smem = TMAP ? smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) / sizeof(double) : smem_raw;
     const int W = a.W, n_walls = a.n_zones * W;
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
     const int rwc = 4 * a.n_channels;
+    double* rows = smem + kRingWallWarps * Sh::kBig;    // forcing rows [S][4 nch]
     for (int i = tid; i < a.steps * rwc; i += blockDim.x)
-        smem[i] = reinterpret_cast<const double*>(a.table)[i];
-    double* buf = smem + ((S * rwc + 1) & ~1) + warp * Sh::warp_doubles(S);   // [4][2 N] staged layers
+        rows[i] = reinterpret_cast<const double*>(a.table)[i];
+    double* buf = smem + warp * Sh::kBig;               // [4][2 N] staged layers
     double* out_s = buf + 4 * 2 * N;                    // [2][2 N] output scratch
-    double* air = out_s + 2 * 2 * N;                    // [parity][wall of the pair][S][2]
+    double* air = rows + ((S * rwc + 1) & ~1) + warp * Sh::small_doubles(S);   // [parity][wall of the pair][S][2]
     double* cfs = air + 2 * 2 * 2 * S;                  // [parity][wall of the pair][WallCoef]
     void* mbar = cfs + 2 * 2 * NC;
     if (lane == 0) {
@@ -479,8 +504,10 @@ __global__ void __launch_bounds__(32 * kRingWallWarps, RW_MINB) k_ring_walls(con
             const unsigned bytes = static_cast<unsigned>(nw * N * sizeof(double));
             mbar_expect_tx(mbar, (RW_SKIP & 4) ? 0u : 4 * bytes);
 #pragma unroll
-            for (int f = 0; f < 4 * !(RW_SKIP & 4); ++f)
-                bulk_g2s(&buf[f * 2 * N], a.in[f] + static_cast<size_t>(pair) * 2 * N, bytes, mbar);
+            for (int f = 0; f < 4 * !(RW_SKIP & 4); ++f) {
+                if (TMAP) dv_tma_load_2d(&buf[f * 2 * N], &MI.m[f], 0, pair * (2 * N / 8), mbar);
+                else bulk_g2s(&buf[f * 2 * N], a.in[f] + static_cast<size_t>(pair) * 2 * N, bytes, mbar);
+            }
         }
         for (int i = lane; i < 2 * 2 * a.steps; i += 32) {
             const int wj = i / (2 * a.steps), r = i - wj * 2 * a.steps;
@@ -512,16 +539,17 @@ __global__ void __launch_bounds__(32 * kRingWallWarps, RW_MINB) k_ring_walls(con
         const double fb = c[0], fe = c[1], feg = c[2], fcsu = c[3], fctu = c[4], fcsv = c[5], fctv = c[6],
                      fcq = c[7], fcg = c[8];
         double up[NPT], uc[NPT], vp[NPT], vc[NPT];
+        const int sw = (lane >> 1) & 3;                 // TMAP: this row's chunk swizzle
         auto rd = [&](int f, double (&x)[NPT]) {        // the reversed lane by selects
             double t[NPT];
 #pragma unroll
-            for (int qq = 0; qq < NPT / 2; ++qq) {      // t pair qq = node pair (qq + rot) mod NPT/2
-                const int pr = (qq + rot) & (NPT / 2 - 1);
+            for (int qq = 0; qq < NPT / 2; ++qq) {      // t pair qq = node pair (qq + rot) mod NPT/2; TMAP: pair qq
+                const int pr = TMAP ? (qq ^ sw) : ((qq + rot) & (NPT / 2 - 1));
                 const double2 v = *reinterpret_cast<const double2*>(&buf[f * 2 * N + lane * NPT + 2 * pr]);
                 t[2 * qq] = v.x;
                 t[2 * qq + 1] = v.y;
             }
-            shift_pairs(t, rot);
+            if (!TMAP) shift_pairs(t, rot);
 #pragma unroll
             for (int q = 0; q < NPT; ++q) x[q] = rev ? t[NPT - 1 - q] : t[q];
         };
@@ -537,7 +565,7 @@ __global__ void __launch_bounds__(32 * kRingWallWarps, RW_MINB) k_ring_walls(con
             // face inputs of register 0, branch-free (wall.cpp:162-169, 177-189):
             // x = 0 the exterior channel, x = 1 the zone's layer-k air (phase 1)
             const int am = k * rwc + 4 * ch;
-            const double ru = smem[am + 0], rv = smem[am + 1], rg = smem[am + 2], rq = smem[am + 3] + 0.0;
+            const double ru = rows[am + 0], rv = rows[am + 1], rg = rows[am + 2], rq = rows[am + 3] + 0.0;
             const double au = s_air[2 * k], av = s_air[2 * k + 1];
             const double u_inf = first ? ru : au, v_inf = first ? rv : av;
             const double g_inf = first ? rg : 0.0, q_inf = first ? rq : 0.0;
@@ -592,10 +620,10 @@ __global__ void __launch_bounds__(32 * kRingWallWarps, RW_MINB) k_ring_walls(con
             double t[NPT];
 #pragma unroll
             for (int q = 0; q < NPT; ++q) t[q] = rev ? x[NPT - 1 - q] : x[q];
-            shift_pairs(t, (NPT / 2 - rot) & (NPT / 2 - 1));
+            if (!TMAP) shift_pairs(t, (NPT / 2 - rot) & (NPT / 2 - 1));
 #pragma unroll
             for (int qq = 0; qq < NPT / 2; ++qq) {
-                const int pr = (qq + rot) & (NPT / 2 - 1);
+                const int pr = TMAP ? (qq ^ sw) : ((qq + rot) & (NPT / 2 - 1));
                 *reinterpret_cast<double2*>(&out_s[f * 2 * N + lane * NPT + 2 * pr]) = make_double2(t[2 * qq], t[2 * qq + 1]);
             }
         };
@@ -605,8 +633,10 @@ __global__ void __launch_bounds__(32 * kRingWallWarps, RW_MINB) k_ring_walls(con
             if (lane == 0) {
                 const unsigned bytes = static_cast<unsigned>(nlive * N * sizeof(double));
 #pragma unroll
-                for (int f = 0; f < 2; ++f)
-                    bulk_s2g(a.out[f0 + f] + static_cast<size_t>(pair) * 2 * N, &out_s[f * 2 * N], bytes);
+                for (int f = 0; f < 2; ++f) {
+                    if (TMAP) tma_store_2d(&MO.m[f0 + f], 0, pair * (2 * N / 8), &out_s[f * 2 * N]);
+                    else bulk_s2g(a.out[f0 + f] + static_cast<size_t>(pair) * 2 * N, &out_s[f * 2 * N], bytes);
+                }
                 asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
             }
         };

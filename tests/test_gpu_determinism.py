@@ -42,6 +42,19 @@ def test_ring_kernels_repeatable_across_grids(kernel):
         assert _same(runs[0], r, KEYS + ("zone_u", "zone_v"))
 
 
+def test_ring_walls_tma_tiles_equal_bulk_copies():
+    """K6's walls kernel with its two staging paths — 2-D TMA tiles through the state arrays'
+    tensor maps (64-byte swizzle, the default for 128-node walls) and 1-D bulk copies with
+    rotated shared accesses (tiled_load = 1) — bitwise equal, for every launch depth."""
+    w = workloads.zone_ring(n_zones=50, walls_per_zone=6, n_nodes=128, nsteps=150)
+    rng = np.random.default_rng(12)
+    w.init.update({k: w.init[k] + 2e-3 * rng.standard_normal(w.init[k].size) for k in KEYS})
+    for depth in (1, 2, 3):
+        a = _run(w, 150, (("ring_depth", depth), ("tiled_load", 0), ("ring_grid", 3)))
+        b = _run(w, 150, (("ring_depth", depth), ("tiled_load", 1), ("ring_grid", 3)))
+        assert _same(a, b, KEYS + ("zone_u", "zone_v")), depth
+
+
 def test_dv_kernels_repeatable():
     w0 = workloads.single_wall_d(nsteps=400)                       # K2h
     a, b = _run(w0, 400), _run(w0, 400)

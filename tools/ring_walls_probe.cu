@@ -71,7 +71,7 @@ int main(int argc, char** argv) {
     for (int r = 0; r < reps + 5; ++r) {
         for (int f = 0; f < 4; ++f) { a.in[f] = (r & 1) ? out[f] : in[f]; a.out[f] = (r & 1) ? in[f] : out[f]; }
         cudaEventRecord(e0);
-        k<<<grid, 32 * kRingWallWarps, smem>>>(a, series);
+        k<<<grid, 32 * kRingWallWarps, smem>>>(a, series, TiledMaps{}, TiledMaps{});
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
